@@ -1,0 +1,340 @@
+/*
+ * oracle.c -- fp64 CPU oracle for the conv2d-family hot path of
+ * arXiv 1802.04647 ("Deep Learning with Apache SystemML", SysML'18).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or helper with the CUDA library
+ * (paper_1802_04647_b200/csrc); neither includes nor links the other.
+ *
+ * Every operator is the plain definition written out as direct nested loops
+ * in double precision (SURVEY.md §8(c) "Definitions").
+ * Citations: "P:n" = /root/reference/PAPER.md line n, "S:n" = SPEC.md line n.
+ *
+ * Tensor layout ("a 4-dimensional tensor of shape [N, C, H, W] is
+ * represented as a matrix with N rows and C*H*W columns"): element (n,c,h,w)
+ * lives at X[n*(C*H*W) + (c*H + h)*W + w]  (S:100 nchw_to_flat).
+ *
+ * Readings of the paper where it is silent (listed in DESIGN.md "Readings"):
+ *   R1 cross-correlation (no filter flip), S:159 f . im2col(x)
+ *   R2 output extent P = floor((H + 2ph - R)/sh) + 1
+ *   R3 conv padding contributes 0; pool padding is excluded (-inf)
+ *   R4 fully padded pool window -> out 0, argmax -1
+ *   R5 pool ties -> first position in row-major window order (strict >)
+ *   R6 argmax = column index (c*H+h)*W+w into the pool-input row
+ *   R7 relu(x) = x > 0 ? x : +0.0
+ *   R9 maxpool_bwd with relu mask routes dout iff pooled out > 0
+ *   R11 loss = -(1/N_global) sum log(max(p[y], 1e-15)); dscores = (p - onehot)/N_global
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define EXPORT __attribute__((visibility("default")))
+
+static inline int64_t out_extent(int64_t in, int64_t pad, int64_t k, int64_t stride) {
+  /* R2: floor((in + 2 pad - k) / stride) + 1 ; <1 means invalid */
+  int64_t num = in + 2 * pad - k;
+  if (num < 0) return 0;
+  return num / stride + 1;
+}
+
+EXPORT int64_t oracle_out_extent(int64_t in, int64_t pad, int64_t k, int64_t stride) {
+  return out_extent(in, pad, k, stride);
+}
+
+/* ------------------------------------------------------------------------ */
+/* conv2d forward  (P:138-140 builtin conv2d; SURVEY §8(c) def 2)
+ *   Y[n,(k*P+p)*Q+q] = [b[k]] + sum_{c,r,s} F[k,(c*R+r)*S+s] * x(n,c,p*sh-ph+r,q*sw-pw+s)
+ * Summation order: for each output plane (n,k): start from b[k] (or 0), then
+ * c ascending, r ascending, s ascending, each term added to every (p,q). */
+EXPORT void oracle_conv2d_fwd(int64_t N, int64_t C, int64_t H, int64_t W, int64_t K,
+                              int64_t R, int64_t S, int64_t sh, int64_t sw, int64_t ph,
+                              int64_t pw, const double *x, const double *f,
+                              const double *bias, double *y) {
+  const int64_t P = out_extent(H, ph, R, sh), Q = out_extent(W, pw, S, sw);
+  const int64_t CHW = C * H * W, CRS = C * R * S, KPQ = K * P * Q;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t n = 0; n < N; ++n) {
+    for (int64_t k = 0; k < K; ++k) {
+      double *plane = y + n * KPQ + k * P * Q;
+      const double b0 = bias ? bias[k] : 0.0;
+      for (int64_t i = 0; i < P * Q; ++i) plane[i] = b0;
+      for (int64_t c = 0; c < C; ++c)
+        for (int64_t r = 0; r < R; ++r)
+          for (int64_t s = 0; s < S; ++s) {
+            const double wgt = f[k * CRS + (c * R + r) * S + s];
+            for (int64_t p = 0; p < P; ++p) {
+              const int64_t h = p * sh - ph + r;
+              if (h < 0 || h >= H) continue;
+              const double *xrow = x + n * CHW + (c * H + h) * W;
+              double *yrow = plane + p * Q;
+              for (int64_t q = 0; q < Q; ++q) {
+                const int64_t w = q * sw - pw + s;
+                if (w < 0 || w >= W) continue;
+                yrow[q] += wgt * xrow[w];
+              }
+            }
+          }
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* bias_add ("broadcasting operations over scalars and vectors";
+ * reading R10: bias is fp32[K], added to all P*Q outputs of filter k)
+ *   Y[n, k*PQ + j] += b[k] */
+EXPORT void oracle_bias_add(int64_t N, int64_t K, int64_t PQ, double *y, const double *b) {
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t k = 0; k < K; ++k)
+      for (int64_t j = 0; j < PQ; ++j) y[(n * K + k) * PQ + j] += b[k];
+}
+
+/* ------------------------------------------------------------------------ */
+/* conv2d_backward_filter ("their respective backward functions";
+ * S:165-173; SURVEY §8(c) def 4)
+ *   dF[k,(c*R+r)*S+s] = sum_n sum_p sum_q dY[n,(k*P+p)*Q+q] * x(n,c,p*sh-ph+r,q*sw-pw+s)
+ *   db[k] = sum_{n,p,q} dY[n,(k*P+p)*Q+q]
+ * Summation order: n, p, q ascending. */
+EXPORT void oracle_conv2d_bwd_filter(int64_t N, int64_t C, int64_t H, int64_t W, int64_t K,
+                                     int64_t R, int64_t S, int64_t sh, int64_t sw, int64_t ph,
+                                     int64_t pw, const double *x, const double *dy, double *df,
+                                     double *db) {
+  const int64_t P = out_extent(H, ph, R, sh), Q = out_extent(W, pw, S, sw);
+  const int64_t CHW = C * H * W, CRS = C * R * S, KPQ = K * P * Q;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t k = 0; k < K; ++k) {
+    for (int64_t c = 0; c < C; ++c) {
+      for (int64_t r = 0; r < R; ++r)
+        for (int64_t s = 0; s < S; ++s) {
+          double acc = 0.0;
+          for (int64_t n = 0; n < N; ++n)
+            for (int64_t p = 0; p < P; ++p) {
+              const int64_t h = p * sh - ph + r;
+              if (h < 0 || h >= H) continue;
+              for (int64_t q = 0; q < Q; ++q) {
+                const int64_t w = q * sw - pw + s;
+                if (w < 0 || w >= W) continue;
+                acc += dy[n * KPQ + (k * P + p) * Q + q] * x[n * CHW + (c * H + h) * W + w];
+              }
+            }
+          df[k * CRS + (c * R + r) * S + s] = acc;
+        }
+    }
+  }
+  if (db) {
+    for (int64_t k = 0; k < K; ++k) {
+      double acc = 0.0;
+      for (int64_t n = 0; n < N; ++n)
+        for (int64_t j = 0; j < P * Q; ++j) acc += dy[n * KPQ + k * P * Q + j];
+      db[k] = acc;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* conv2d_backward_data (SURVEY §8(c) def 5): the exact adjoint
+ * (transpose) of conv2d_fwd in X, written as the forward loop nest with the
+ * multiply-add redirected into dX:
+ *   dX[n,(c*H+h)*W+w] = sum_{k,r,s,p,q : p*sh-ph+r=h, q*sw-pw+s=w} F[k,c,r,s] dY[n,k,p,q]
+ * Summation order per dX element: k, r, s, p, q ascending (loop nest order). */
+EXPORT void oracle_conv2d_bwd_data(int64_t N, int64_t C, int64_t H, int64_t W, int64_t K,
+                                   int64_t R, int64_t S, int64_t sh, int64_t sw, int64_t ph,
+                                   int64_t pw, const double *f, const double *dy, double *dx) {
+  const int64_t P = out_extent(H, ph, R, sh), Q = out_extent(W, pw, S, sw);
+  const int64_t CHW = C * H * W, CRS = C * R * S, KPQ = K * P * Q;
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n) {
+    double *dxn = dx + n * CHW;
+    for (int64_t i = 0; i < CHW; ++i) dxn[i] = 0.0;
+    for (int64_t c = 0; c < C; ++c)
+      for (int64_t k = 0; k < K; ++k)
+        for (int64_t r = 0; r < R; ++r)
+          for (int64_t s = 0; s < S; ++s) {
+            const double wgt = f[k * CRS + (c * R + r) * S + s];
+            for (int64_t p = 0; p < P; ++p) {
+              const int64_t h = p * sh - ph + r;
+              if (h < 0 || h >= H) continue;
+              for (int64_t q = 0; q < Q; ++q) {
+                const int64_t w = q * sw - pw + s;
+                if (w < 0 || w >= W) continue;
+                dxn[(c * H + h) * W + w] += wgt * dy[n * KPQ + (k * P + p) * Q + q];
+              }
+            }
+          }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* relu_maxpool (P:138-140 pooling builtin; SURVEY §8(c) def 6)
+ * For each (n,c,p',q'): scan r outer, s inner over the window; skip padded
+ * positions (R3); v = relu ? (x>0 ? x : +0.0) : x (R7); first valid position or
+ * v > best (strict, R5) updates best and arg = (c*H+h)*W+w (R6).
+ * Fully padded window: out 0, argmax -1 (R4). */
+EXPORT void oracle_relu_maxpool(int64_t N, int64_t C, int64_t H, int64_t W, int64_t R,
+                                int64_t S, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                                int64_t relu, const double *x, double *out, int32_t *argmax) {
+  const int64_t P = out_extent(H, ph, R, sh), Q = out_extent(W, pw, S, sw);
+  const int64_t CHW = C * H * W, CPQ = C * P * Q;
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t c = 0; c < C; ++c)
+      for (int64_t p = 0; p < P; ++p)
+        for (int64_t q = 0; q < Q; ++q) {
+          int found = 0;
+          double best = 0.0;
+          int64_t arg = -1;
+          for (int64_t r = 0; r < R; ++r)
+            for (int64_t s = 0; s < S; ++s) {
+              const int64_t h = p * sh - ph + r, w = q * sw - pw + s;
+              if (h < 0 || h >= H || w < 0 || w >= W) continue;
+              double v = x[n * CHW + (c * H + h) * W + w];
+              if (relu) v = v > 0.0 ? v : 0.0;
+              if (!found || v > best) {
+                found = 1;
+                best = v;
+                arg = (c * H + h) * W + w;
+              }
+            }
+          const int64_t o = n * CPQ + (c * P + p) * Q + q;
+          out[o] = found ? best : 0.0;
+          if (argmax) argmax[o] = (int32_t)arg;
+        }
+}
+
+/* ------------------------------------------------------------------------ */
+/* maxpool_backward (SURVEY §8(c) def 7)
+ *   dX = 0; for each window in ascending (c,p',q') order: if argmax >= 0 and
+ *   (no mask or out > 0, R9): dX[n, argmax] += dout[n, (c*P'+p')*Q'+q'] */
+EXPORT void oracle_maxpool_bwd(int64_t N, int64_t C, int64_t H, int64_t W, int64_t P,
+                               int64_t Q, const int32_t *argmax, const double *dout,
+                               const double *out_mask, double *dx) {
+  const int64_t CHW = C * H * W, CPQ = C * P * Q;
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n) {
+    double *dxn = dx + n * CHW;
+    for (int64_t i = 0; i < CHW; ++i) dxn[i] = 0.0;
+    for (int64_t j = 0; j < CPQ; ++j) {
+      const int32_t a = argmax[n * CPQ + j];
+      if (a < 0) continue;
+      if (out_mask && !(out_mask[n * CPQ + j] > 0.0)) continue;
+      dxn[a] += dout[n * CPQ + j];
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* CSR densify ("various sparse formats (COO, CSR and Modified CSR)";
+ * S:28-34).  The CSR input case of every operator is defined as the operator
+ * on this densification (duplicates summed). */
+EXPORT void oracle_csr_densify(int64_t rows, int64_t cols, const int32_t *row_ptr,
+                               const int32_t *col_idx, const double *val, double *dense) {
+  memset(dense, 0, sizeof(double) * (size_t)(rows * cols));
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t j = row_ptr[r]; j < row_ptr[r + 1]; ++j) dense[r * cols + col_idx[j]] += val[j];
+}
+
+/* ------------------------------------------------------------------------ */
+/* LeNet-min minibatch SGD step (Listing 1 loop body: forward, backward,
+ * sgd::update with lr = 0.01; "LeNet"; SURVEY §8(c) def 8):
+ *   z1 = conv(X; F1,b1, 5x5 p2 s1);  a1,i1 = relu_maxpool(z1, 2x2/2)
+ *   z2 = conv(a1; F2,b2, 5x5 p2 s1); a2,i2 = relu_maxpool(z2, 2x2/2)
+ *   s  = a2 W3^T + b3;  p = softmax(s) (max shift)
+ *   L  = -(1/Ng) sum_n log(max(p[n,y_n], 1e-15))       (R11)
+ *   ds = (p - onehot(y)) / Ng
+ *   dW3 = ds^T a2; db3 = colsum(ds); da2 = ds W3
+ *   dz2 = maxpool_bwd(i2, da2, a2>0); dF2,db2 = bwd_filter(a1,dz2); da1 = bwd_data(F2,dz2)
+ *   dz1 = maxpool_bwd(i1, da1, a1>0); dF1,db1 = bwd_filter(X,dz1)
+ * Parameter order (flat): F1[32x25], b1[32], F2[64x800], b2[64], W3[10x3136], b3[10]. */
+#define L_F1 0
+#define L_B1 (L_F1 + 32 * 25)
+#define L_F2 (L_B1 + 32)
+#define L_B2 (L_F2 + 64 * 800)
+#define L_W3 (L_B2 + 64)
+#define L_B3 (L_W3 + 10 * 3136)
+#define L_NP (L_B3 + 10)
+
+EXPORT int64_t oracle_lenet_num_params(void) { return L_NP; }
+
+EXPORT void oracle_lenet_forward(int64_t n, const double *x, const double *prm, double *a1,
+                                 int32_t *i1, double *a2, int32_t *i2, double *scores) {
+  double *z1 = (double *)malloc(sizeof(double) * (size_t)(n * 32 * 784));
+  double *z2 = (double *)malloc(sizeof(double) * (size_t)(n * 64 * 196));
+  oracle_conv2d_fwd(n, 1, 28, 28, 32, 5, 5, 1, 1, 2, 2, x, prm + L_F1, prm + L_B1, z1);
+  oracle_relu_maxpool(n, 32, 28, 28, 2, 2, 2, 2, 0, 0, 1, z1, a1, i1);
+  oracle_conv2d_fwd(n, 32, 14, 14, 64, 5, 5, 1, 1, 2, 2, a1, prm + L_F2, prm + L_B2, z2);
+  oracle_relu_maxpool(n, 64, 14, 14, 2, 2, 2, 2, 0, 0, 1, z2, a2, i2);
+  const double *W3 = prm + L_W3, *b3 = prm + L_B3;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < 10; ++j) {
+      double acc = b3[j];
+      for (int64_t d = 0; d < 3136; ++d) acc += a2[i * 3136 + d] * W3[j * 3136 + d];
+      scores[i * 10 + j] = acc;
+    }
+  free(z1);
+  free(z2);
+}
+
+EXPORT void oracle_lenet_fwd_bwd(int64_t n, int64_t n_global, const double *x,
+                                 const int32_t *labels, const double *prm, double *grads,
+                                 double *loss_sum) {
+  double *a1 = (double *)malloc(sizeof(double) * (size_t)(n * 6272));
+  double *a2 = (double *)malloc(sizeof(double) * (size_t)(n * 3136));
+  int32_t *i1 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n * 6272));
+  int32_t *i2 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n * 3136));
+  double *sc = (double *)malloc(sizeof(double) * (size_t)(n * 10));
+  double *ds = (double *)malloc(sizeof(double) * (size_t)(n * 10));
+  double *da2 = (double *)malloc(sizeof(double) * (size_t)(n * 3136));
+  double *dz2 = (double *)malloc(sizeof(double) * (size_t)(n * 12544));
+  double *da1 = (double *)malloc(sizeof(double) * (size_t)(n * 6272));
+  double *dz1 = (double *)malloc(sizeof(double) * (size_t)(n * 25088));
+  oracle_lenet_forward(n, x, prm, a1, i1, a2, i2, sc);
+
+  double loss = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double m = sc[i * 10];
+    for (int j = 1; j < 10; ++j) m = sc[i * 10 + j] > m ? sc[i * 10 + j] : m;
+    double den = 0.0;
+    for (int j = 0; j < 10; ++j) den += exp(sc[i * 10 + j] - m);
+    for (int j = 0; j < 10; ++j) {
+      const double pj = exp(sc[i * 10 + j] - m) / den;
+      ds[i * 10 + j] = (pj - (j == labels[i] ? 1.0 : 0.0)) / (double)n_global;
+      if (j == labels[i]) loss += -log(pj > 1e-15 ? pj : 1e-15);
+    }
+  }
+  if (loss_sum) *loss_sum = loss / (double)n_global;
+
+  const double *W3 = prm + L_W3;
+  double *dW3 = grads + L_W3, *db3 = grads + L_B3;
+  for (int j = 0; j < 10; ++j) {
+    double accb = 0.0;
+    for (int64_t i = 0; i < n; ++i) accb += ds[i * 10 + j];
+    db3[j] = accb;
+    for (int64_t d = 0; d < 3136; ++d) {
+      double acc = 0.0;
+      for (int64_t i = 0; i < n; ++i) acc += ds[i * 10 + j] * a2[i * 3136 + d];
+      dW3[j * 3136 + d] = acc;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t d = 0; d < 3136; ++d) {
+      double acc = 0.0;
+      for (int j = 0; j < 10; ++j) acc += ds[i * 10 + j] * W3[j * 3136 + d];
+      da2[i * 3136 + d] = acc;
+    }
+  oracle_maxpool_bwd(n, 64, 14, 14, 7, 7, i2, da2, a2, dz2);
+  oracle_conv2d_bwd_filter(n, 32, 14, 14, 64, 5, 5, 1, 1, 2, 2, a1, dz2, grads + L_F2,
+                           grads + L_B2);
+  oracle_conv2d_bwd_data(n, 32, 14, 14, 64, 5, 5, 1, 1, 2, 2, prm + L_F2, dz2, da1);
+  oracle_maxpool_bwd(n, 32, 28, 28, 14, 14, i1, da1, a1, dz1);
+  oracle_conv2d_bwd_filter(n, 1, 28, 28, 32, 5, 5, 1, 1, 2, 2, x, dz1, grads + L_F1,
+                           grads + L_B1);
+  free(a1); free(a2); free(i1); free(i2); free(sc); free(ds);
+  free(da2); free(dz2); free(da1); free(dz1);
+}
+
+/* SGD ("lr = 0.01", P:80-81 sgd::update): theta <- theta - lr * g */
+EXPORT void oracle_sgd_update(int64_t n, double *params, const double *grads, double lr) {
+  for (int64_t i = 0; i < n; ++i) params[i] = params[i] - lr * grads[i];
+}
