@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark of the conv2d-family hot path (BASELINE.json metric:
+"LeNet train-step images/s at 1/2/4/8 B200; conv2d GFLOP/s vs TF32 peak").
+
+Workload (BJ configs[4]): data-parallel LeNet minibatch SGD, global batch 8192
+sharded over the ranks (strong scaling), synthetic MNIST-shaped dense input
+(family M of synth/), random-init LeNet weights, lr 0.01.  One step = one pass
+of the whole hot path: conv1/conv2 fused conv+bias+relu+maxpool forward, affine +
+softmax + cross-entropy, maxpool_bwd, conv bwd_filter / bwd_data, the NCCL
+allreduce of dW/db (N > 1) and the SGD update -- all in libsysml kernels.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  (N > 1: torchrun --nproc-per-node N ... bench.py --gpus N)
+
+Prints ONE JSON line (rank 0).  Timing: CUDA events on the launching stream,
+barrier + synchronize on both sides, max over ranks.  L2: each step reads one of
+8 rotating input batches (8 x 25.7 MB at N=1) and writes ~0.6 GB of activations,
+so the step working set is far larger than the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GLOBAL_BATCH = 8192
+METRIC = "LeNet train-step images/s at 1/2/4/8 B200; conv2d GFLOP/s vs TF32 peak"
+UNIT = "images/s"
+ROTATE = 8
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    sm_max=d.get("sm_max_mhz", 1965.0), src="measured (MEASURED_PEAKS.json)")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, sm_max=1965.0, src="fallback (B200_PROFILING.md)")
+
+
+# Per-image algorithmic work of each step stage:
+# (flops, bytes, bound-if-tensor-math).  Bytes = fp32/int32 tensors each kernel must
+# read or write once; params are negligible.
+STAGE_WORK = {
+    "F1_conv1_pool": (2 * 32 * 25 * 784, 784 * 4 + 6272 * 4 * 2, "hbm"),
+    "F2_conv2_pool": (2 * 64 * 800 * 196, 6272 * 4 + 3136 * 4 * 2, "tensor"),
+    "F3_affine_softmax_ce": (2 * 10 * 3136, 3136 * 4 + 10 * 4, "hbm"),
+    "B3_affine_bwd": (4 * 10 * 3136, 3136 * 4 * 2 + 10 * 4, "hbm"),
+    "B2p_maxpool_bwd2": (0, 3136 * 4 * 3 + 12544 * 4, "hbm"),
+    "B2f_conv2_bwd_filter": (2 * 64 * 800 * 196, 6272 * 4 + 12544 * 4, "tensor"),
+    "B2d_conv2_bwd_data": (2 * 64 * 800 * 196, 12544 * 4 + 6272 * 4, "tensor"),
+    "B1p_maxpool_bwd1": (0, 6272 * 4 * 3 + 25088 * 4, "hbm"),
+    "B1f_conv1_bwd_filter": (2 * 32 * 25 * 784, 784 * 4 + 25088 * 4, "hbm"),
+}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=1)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_oracle_rate(target_s: float = 15.0, max_images: int = 4096):
+    """Time the fp64 oracle LeNet step (fwd+bwd+SGD) on a bounded sample of the workload."""
+    import oracle
+    import synth
+    prm = synth.lenet_params(seed=(6,)).astype(np.float64)
+    def run(n):
+        x = synth.mnist_like(n, seed=(77, n))
+        y = synth.labels(n, seed=(78, n))
+        t0 = time.perf_counter()
+        g, _ = oracle.lenet_fwd_bwd(x, y, prm, n_global=GLOBAL_BATCH)
+        oracle.sgd_update(prm, g, 0.01)
+        return time.perf_counter() - t0
+    t16 = run(16)
+    n = int(min(max_images, max(16, 16 * target_s / max(t16, 1e-6))))
+    t = run(n)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return n / t, n, t, cores
+
+
+def reference_arm(args, world, rank):
+    """--impl reference: the fp64 oracle (this tier's reference arm) on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    prm = synth.lenet_params(seed=(6,)).astype(np.float64)
+    # size each step's bounded sample so warmup+steps finish in ~2-3 minutes
+    x16 = synth.mnist_like(16, seed=(79,))
+    y16 = synth.labels(16, seed=(80,))
+    t0 = time.perf_counter(); oracle.lenet_fwd_bwd(x16, y16, prm, n_global=GLOBAL_BATCH); t16 = time.perf_counter() - t0
+    total_steps = args.steps + args.warmup
+    per_step = int(max(8, min(GLOBAL_BATCH, 16 * (150.0 / total_steps) / max(t16, 1e-6))))
+    times = []
+    for i in range(total_steps):
+        x = synth.mnist_like(per_step, seed=(81, i))
+        y = synth.labels(per_step, seed=(82, i))
+        t0 = time.perf_counter()
+        g, _ = oracle.lenet_fwd_bwd(x, y, prm, n_global=GLOBAL_BATCH)
+        prm = oracle.sgd_update(prm, g, 0.01)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = per_step * len(times) / tot
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": "DP LeNet minibatch SGD (BJ configs[4])",
+                                        "global_batch": GLOBAL_BATCH, "sample_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{per_step} images of the global-batch-{GLOBAL_BATCH} step per timed step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def time_op(fn, reps, flush=None):
+    import torch
+    st = torch.cuda.current_stream()
+    ts = []
+    for i in range(reps + 3):
+        if flush is not None:
+            flush.zero_()
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(st); fn(); b.record(st)
+        b.synchronize()
+        if i >= 3:
+            ts.append(a.elapsed_time(b))
+    return statistics.median(ts), min(ts)
+
+
+def layer_section(S, peaks, quick=False):
+    """conv2d GFLOP/s vs TF32 peak on the BJ ResNet-style layers (cfg 4) and the CSR
+    conv1 bandwidth case (cfg 3), each op timed alone with an L2 flush between reps."""
+    import torch
+    import synth
+    tf32_peak = peaks["bf16"] * 0.5  # nominal tf32/bf16 = 1.125/2.25
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    out = {}
+    reps = 5 if quick else 20
+    for name, (N, C, H, W, K, R, S_, pd) in {
+        "resnet3x3_C256_K256_14x14_N128": (128, 256, 14, 14, 256, 3, 3, 1),
+        "resnet1x1_C1024_K256_14x14_N128": (128, 1024, 14, 14, 256, 1, 1, 0),
+        "lenet_conv2_C32_K64_14x14_N8192": (8192, 32, 14, 14, 64, 5, 5, 2),
+    }.items():
+        P = Q = H
+        x, f, b, dy = synth.conv_problem_U(N, C, H, W, K, R, S_, P, Q, seed=(1000,))
+        x, f, b, dy = (torch.from_numpy(t).cuda() for t in (x, f, b, dy))
+        d = S.conv_desc(N, C, H, W, K, R, S_, 1, pd, "tf32")
+        y = torch.empty(N, K * P * Q, device="cuda")
+        dx = torch.empty(N, C * H * W, device="cuda")
+        df = torch.empty(K, C * R * S_, device="cuda"); db = torch.empty(K, device="cuda")
+        ws = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+        flops = 2.0 * N * K * C * R * S_ * P * Q
+        res = {}
+        for op, fn, nbytes in (
+            ("fwd", lambda: S.sysml_conv2d(x, f, d, bias=b, out=y, workspace=ws), 4 * (x.numel() + f.numel() + K + y.numel())),
+            ("bwd_filter", lambda: S.sysml_conv2d_bwd_filter(x, dy, d, df=df, db=db, workspace=ws), 4 * (x.numel() + dy.numel() + df.numel() + K)),
+            ("bwd_data", lambda: S.sysml_conv2d_bwd_data(f, dy, d, dx=dx, workspace=ws), 4 * (f.numel() + dy.numel() + dx.numel())),
+        ):
+            med, mn = time_op(fn, reps, flush)
+            tfs = flops / (med * 1e-3) / 1e12
+            res[op] = {"ms": round(med, 4), "tflops": round(tfs, 2), "frac_tf32_peak": round(tfs / tf32_peak, 4),
+                       "gbs": round(nbytes / (med * 1e-3) / 1e9, 1)}
+        out[name] = res
+        del x, f, b, dy, y, dx
+    # CSR conv1 (BJ cfg 3 shape, N = 16384 as the bandwidth headline)
+    N = 2048 if quick else 16384
+    xd = synth.mnist_like(N, seed=(1001,))
+    rp, ci, v = synth.to_csr(xd)
+    m = S.CSR(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(), torch.from_numpy(v).cuda(), N, 784)
+    f = torch.from_numpy(synth.normal((32, 25), 0.28, seed=(1002,))).cuda()
+    b = torch.zeros(32, device="cuda")
+    d = S.conv_desc(N, 1, 28, 28, 32, 5, 5, 1, 2, "tf32")
+    y = torch.empty(N, 32 * 784, device="cuda")
+    dy = torch.from_numpy(synth.normal((N, 32 * 784), seed=(1003,))).cuda()
+    df = torch.empty(32, 25, device="cuda"); db = torch.empty(32, device="cuda")
+    ws = torch.empty(1 << 26, dtype=torch.uint8, device="cuda")
+    nnz = ci.size
+    fwd_bytes = 4 * (N + 1) + 8 * nnz + 4 * (800 + 32) + 4 * N * 32 * 784
+    bwf_bytes = 4 * (N + 1) + 8 * nnz + 4 * N * 32 * 784 + 4 * 832
+    res = {"nnz": int(nnz), "density": round(nnz / (N * 784), 4)}
+    for op, fn, nbytes in (("fwd", lambda: S.sysml_conv2d(m, f, d, bias=b, out=y, workspace=ws), fwd_bytes),
+                           ("bwd_filter", lambda: S.sysml_conv2d_bwd_filter(m, dy, d, df=df, db=db, workspace=ws), bwf_bytes)):
+        med, mn = time_op(fn, reps, flush)
+        gbs = nbytes / (med * 1e-3) / 1e9
+        res[op] = {"ms": round(med, 4), "gbs": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 4)}
+    out[f"csr_lenet_conv1_N{N}"] = res
+    return out
+
+
+def ours_arm(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_1802_04647_b200 as S
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    S.lib(build_if_missing=True)
+    peaks = load_peaks()
+    b = GLOBAL_BATCH // world
+    math = args.math
+    # data: ROTATE distinct input batches per rank, resident in HBM
+    xs_host = [synth.mnist_like(b, seed=(rank, i)) for i in range(ROTATE)]
+    ys_host = [synth.labels(b, seed=(100 + rank, i)) for i in range(ROTATE)]
+    xs = [torch.from_numpy(x).cuda() for x in xs_host]
+    ys = [torch.from_numpy(y).cuda() for y in ys_host]
+    params = torch.from_numpy(synth.lenet_params(seed=(6,))).cuda()
+    grads = torch.empty_like(params)
+    loss = torch.empty(1, device="cuda")
+    net = S.LeNet(b, math=math)
+    comm = None
+    if world > 1:
+        t = torch.ones(1, device="cuda")
+        dist.all_reduce(t)  # creates the NCCL communicator
+        comm = S.nccl_comm_ptr()
+    st = torch.cuda.current_stream()
+
+    def step(i):
+        net.step(params, grads, xs[i % ROTATE], ys[i % ROTATE], GLOBAL_BATCH, lr=0.01,
+                 nccl_comm=comm, loss_sum=loss)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    net.set_timing(True)
+    net.get_timing(reset=True)
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    l0 = S.sysml_launch_counter()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(args.steps):
+        step(i)
+    e1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = S.sysml_launch_counter() - l0
+    clocks = clk.stop()
+    net.set_timing(False)
+    stages = net.get_timing()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = GLOBAL_BATCH * args.steps / (ms * 1e-3)
+
+    # ---- end to end through the host-input C-ABI entry point (pinned host batches)
+    xs_pin = [torch.from_numpy(x).pin_memory() for x in xs_host]
+    ys_pin = [torch.from_numpy(y).pin_memory() for y in ys_host]
+    for i in range(2):
+        net.step_host(params, grads, xs_pin[i % ROTATE], ys_pin[i % ROTATE], GLOBAL_BATCH, nccl_comm=comm)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2 = torch.cuda.Event(enable_timing=True); e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(st)
+    for i in range(args.steps):
+        net.step_host(params, grads, xs_pin[i % ROTATE], ys_pin[i % ROTATE], GLOBAL_BATCH, nccl_comm=comm)
+    e3.record(st)
+    torch.cuda.synchronize()
+    ms_e2e = e2.elapsed_time(e3)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e_value = GLOBAL_BATCH * args.steps / (ms_e2e * 1e-3)
+
+    # ---- roofline of the dominant stage
+    tf32_sus = peaks["bf16_sus"] * 0.5
+    fp32_alu = 148 * 128 * 2 * peaks["sm_max"] * 1e6 / 1e12
+    stage_rows = {}
+    for name, (tot_ms, calls) in stages.items():
+        if calls == 0:
+            continue
+        fl, by, bound = STAGE_WORK[name]
+        avg = tot_ms / calls
+        stage_rows[name] = {"avg_ms": round(avg, 4), "share": round(tot_ms / max(ms, 1e-9), 4),
+                            "tflops": round(fl * b / (avg * 1e-3) / 1e12, 2),
+                            "gbs": round(by * b / (avg * 1e-3) / 1e9, 1)}
+    dom = max(stage_rows, key=lambda k: stage_rows[k]["avg_ms"])
+    fl, by, bound = STAGE_WORK[dom]
+    avg_s = stage_rows[dom]["avg_ms"] * 1e-3
+    if bound == "tensor" and math == "tf32":
+        achieved = fl * b / avg_s / 1e12
+        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(tf32_sus, 1), "unit": "TFLOP/s",
+                "frac": round(achieved / tf32_sus, 4),
+                "peak_note": "TF32 = measured bf16 sustained x 0.5 (nominal 1.125/2.25 PF)"}
+    elif bound == "tensor":
+        achieved = fl * b / avg_s / 1e12
+        roof = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(fp32_alu, 1), "unit": "TFLOP/s",
+                "frac": round(achieved / fp32_alu, 4), "peak_note": "148 SM x 128 FFMA x 2 x sm_max_mhz"}
+    else:
+        achieved = by * b / avg_s / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm"], 4)}
+    roof.update({"kernel": dom, "traffic": None, "peak_src": peaks["src"]})
+
+    result = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "tf32" if math == "tf32" else "f32", "data": "synthetic",
+        "config": {"workload": "DP LeNet minibatch SGD (BJ configs[4]): conv5x5(32)+relu+pool2 -> conv5x5(64)+relu+pool2 "
+                               "-> affine(3136->10) -> softmax-CE, SGD lr 0.01",
+                   "global_batch": GLOBAL_BATCH, "local_batch": b, "input": "dense MNIST-shaped (density ~0.19)",
+                   "parallelism": f"dp{world}", "l2": f"{ROTATE} rotating input batches + ~0.6 GB/step activations >> 126 MB L2"},
+        "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": b * 784 * 4 + b * 4,
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": roof,
+        "stages": stage_rows,
+    }
+    if rank == 0 and world == 1 and not args.no_layers:
+        result["layers"] = layer_section(S, peaks, quick=args.quick)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, n, t, cores = cpu_oracle_rate()
+        result["cpu_baseline"] = {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+                                  "sample": f"fp64 oracle LeNet fwd+bwd+SGD on {n} images ({t:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--math", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--no-layers", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+        return
+    ours_arm(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,419 @@
+"""Python binding of libsysml.so -- the B200-native conv2d-family hot path of
+arXiv 1802.04647 ("Deep Learning with Apache SystemML", §3 GPU backend).
+
+Argument marshalling only: every step of the path runs in the CUDA kernels of
+``csrc/`` behind the C ABI declared in ``include/sysml.h``; the names below are
+that ABI's names.  PyTorch supplies device memory, streams and process groups.
+There is no CPU fallback: importing works anywhere (so the symbol table can be
+checked on a CPU box), but every compute call requires CUDA tensors and raises
+if the library or a GPU is missing.
+
+Tensor encoding (§3 "Tensor Representation"): [N, C, H, W] is the
+row-major matrix N x (C*H*W); tensors passed here are 2-D float32 CUDA tensors
+of that shape (any contiguous shape with the right numel is accepted).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+from . import _build
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsysml.so")
+
+MATH_FP32 = 0
+MATH_TF32 = 1
+_MATH = {"fp32": MATH_FP32, "tf32": MATH_TF32, MATH_FP32: MATH_FP32, MATH_TF32: MATH_TF32}
+
+STATUS = {0: "SYSML_OK", 1: "SYSML_ERR_ARG", 2: "SYSML_ERR_SHAPE", 3: "SYSML_ERR_UNSUPPORTED",
+          4: "SYSML_ERR_CUDA", 5: "SYSML_ERR_NCCL", 6: "SYSML_ERR_WORKSPACE"}
+
+# every symbol include/sysml.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "sysml_version", "sysml_last_error", "sysml_device_sm_count", "sysml_launch_counter",
+    "sysml_conv2d_workspace_size", "sysml_conv2d",
+    "sysml_conv2d_bwd_filter_workspace_size", "sysml_conv2d_bwd_filter",
+    "sysml_conv2d_bwd_data_workspace_size", "sysml_conv2d_bwd_data",
+    "sysml_bias_add", "sysml_relu_maxpool", "sysml_maxpool_bwd",
+    "sysml_conv2d_bias_relu_maxpool_workspace_size", "sysml_conv2d_bias_relu_maxpool",
+    "sysml_csr_check",
+    "sysml_lenet_num_params", "sysml_lenet_create", "sysml_lenet_destroy", "sysml_lenet_fwd_bwd",
+    "sysml_sgd_update", "sysml_lenet_step", "sysml_lenet_step_host",
+    "sysml_lenet_set_timing", "sysml_lenet_get_timing",
+)
+
+
+class SysmlError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ConvDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("N", "C", "H", "W", "K", "R", "S", "stride_h", "stride_w", "pad_h", "pad_w", "math")]
+
+    @property
+    def P(self):
+        return (self.H + 2 * self.pad_h - self.R) // self.stride_h + 1
+
+    @property
+    def Q(self):
+        return (self.W + 2 * self.pad_w - self.S) // self.stride_w + 1
+
+
+class PoolDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("N", "C", "H", "W", "R", "S", "stride_h", "stride_w", "pad_h", "pad_w", "relu")]
+
+    @property
+    def P(self):
+        return (self.H + 2 * self.pad_h - self.R) // self.stride_h + 1
+
+    @property
+    def Q(self):
+        return (self.W + 2 * self.pad_w - self.S) // self.stride_w + 1
+
+
+class _Csr(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("val", ctypes.c_void_p)]
+
+
+class _Input(ctypes.Structure):
+    _fields_ = [("is_csr", ctypes.c_int32), ("dense", ctypes.c_void_p), ("csr", _Csr)]
+
+
+@dataclass
+class CSR:
+    """Device CSR matrix (§3 "Sparse Operations"): int32 row_ptr[rows+1],
+    int32 col_idx[nnz], float32 val[nnz] (torch CUDA tensors)."""
+    row_ptr: "object"
+    col_idx: "object"
+    val: "object"
+    rows: int
+    cols: int
+
+    @property
+    def nnz(self):
+        return int(self.col_idx.numel())
+
+
+def conv_desc(N, C, H, W, K, R, S, stride=(1, 1), pad=(0, 0), math="tf32") -> ConvDesc:
+    stride = (stride, stride) if isinstance(stride, int) else tuple(stride)
+    pad = (pad, pad) if isinstance(pad, int) else tuple(pad)
+    return ConvDesc(N, C, H, W, K, R, S, stride[0], stride[1], pad[0], pad[1], _MATH[math])
+
+
+def pool_desc(N, C, H, W, R, S, stride=None, pad=(0, 0), relu=True) -> PoolDesc:
+    stride = (R, S) if stride is None else ((stride, stride) if isinstance(stride, int) else tuple(stride))
+    pad = (pad, pad) if isinstance(pad, int) else tuple(pad)
+    return PoolDesc(N, C, H, W, R, S, stride[0], stride[1], pad[0], pad[1], int(bool(relu)))
+
+
+_lib = None
+
+
+def lib(build_if_missing: bool = False):
+    """Load libsysml.so (raises if absent: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing and not os.path.exists(LIB_PATH):
+        _build.build()
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libsysml.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    c_i32, c_i64, vp, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+    CD, PD, IN, CS = ctypes.POINTER(ConvDesc), ctypes.POINTER(PoolDesc), ctypes.POINTER(_Input), ctypes.POINTER(_Csr)
+    psz = ctypes.POINTER(ctypes.c_size_t)
+    sig = {
+        "sysml_version": (ctypes.c_char_p, []),
+        "sysml_last_error": (ctypes.c_char_p, []),
+        "sysml_device_sm_count": (c_i32, []),
+        "sysml_launch_counter": (c_i64, []),
+        "sysml_conv2d_workspace_size": (c_i32, [CD, c_i32, psz]),
+        "sysml_conv2d": (c_i32, [CD, IN, vp, vp, vp, vp, sz, vp]),
+        "sysml_conv2d_bwd_filter_workspace_size": (c_i32, [CD, c_i32, psz]),
+        "sysml_conv2d_bwd_filter": (c_i32, [CD, IN, vp, vp, vp, vp, sz, vp]),
+        "sysml_conv2d_bwd_data_workspace_size": (c_i32, [CD, psz]),
+        "sysml_conv2d_bwd_data": (c_i32, [CD, vp, vp, vp, vp, sz, vp]),
+        "sysml_bias_add": (c_i32, [c_i32, c_i32, c_i32, vp, vp, vp]),
+        "sysml_relu_maxpool": (c_i32, [PD, vp, vp, vp, vp]),
+        "sysml_maxpool_bwd": (c_i32, [PD, vp, vp, vp, vp, vp]),
+        "sysml_conv2d_bias_relu_maxpool_workspace_size": (c_i32, [CD, PD, c_i32, psz]),
+        "sysml_conv2d_bias_relu_maxpool": (c_i32, [CD, PD, IN, vp, vp, vp, vp, vp, sz, vp]),
+        "sysml_csr_check": (c_i32, [CS, ctypes.POINTER(c_i64), vp]),
+        "sysml_lenet_num_params": (c_i64, []),
+        "sysml_lenet_create": (c_i32, [c_i32, c_i32, c_i32, c_i64, ctypes.POINTER(vp)]),
+        "sysml_lenet_destroy": (c_i32, [vp]),
+        "sysml_lenet_fwd_bwd": (c_i32, [vp, vp, IN, vp, c_i32, c_i64, vp, vp, vp]),
+        "sysml_sgd_update": (c_i32, [vp, vp, c_i64, ctypes.c_float, vp]),
+        "sysml_lenet_step": (c_i32, [vp, vp, vp, IN, vp, c_i32, c_i64, ctypes.c_float, vp, vp, vp]),
+        "sysml_lenet_step_host": (c_i32, [vp, vp, vp, vp, vp, c_i32, c_i64, ctypes.c_float, vp, vp, vp]),
+        "sysml_lenet_set_timing": (c_i32, [vp, c_i32]),
+        "sysml_lenet_get_timing": (c_i32, [vp, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(ctypes.c_double),
+                                           ctypes.POINTER(c_i64), ctypes.POINTER(ctypes.c_char_p)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype, fn.argtypes = res, args
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise SysmlError(status, lib().sysml_last_error().decode())
+
+
+# ---------------------------------------------------------------------------- helpers
+def _torch():
+    import torch
+    return torch
+
+
+def _stream(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t, dtype=None, name="tensor"):
+    if t is None:
+        return None
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA torch.Tensor (no CPU path exists)")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _input(x) -> _Input:
+    torch = _torch()
+    if isinstance(x, CSR):
+        return _Input(1, None, _Csr(x.rows, x.cols, x.nnz,
+                                    _ptr(x.row_ptr, torch.int32, "row_ptr").value,
+                                    _ptr(x.col_idx, torch.int32, "col_idx").value if x.nnz else None,
+                                    _ptr(x.val, torch.float32, "val").value if x.nnz else None))
+    return _Input(0, _ptr(x, torch.float32, "x").value, _Csr())
+
+
+def _workspace(nbytes: int, workspace=None, device=None):
+    torch = _torch()
+    if nbytes == 0:
+        return None, 0
+    if workspace is not None and workspace.numel() * workspace.element_size() >= nbytes:
+        return ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size()
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
+    _workspace.keep = buf  # keep alive until the next call (stream-ordered reuse)
+    return ctypes.c_void_p(buf.data_ptr()), nbytes
+
+
+def _ws_size(fn, *args) -> int:
+    n = ctypes.c_size_t(0)
+    _check(fn(*args, ctypes.byref(n)))
+    return n.value
+
+
+# ---------------------------------------------------------------------------- operators
+def sysml_conv2d(x, f, d: ConvDesc, bias=None, out=None, workspace=None, stream=None):
+    """conv2d / conv2d_bias_add (§3 Builtin NN Functions): N x (K*P*Q)."""
+    torch = _torch()
+    L = lib()
+    inp = _input(x)
+    if out is None:
+        out = torch.empty((d.N, d.K * d.P * d.Q), dtype=torch.float32, device="cuda")
+    nb = _ws_size(L.sysml_conv2d_workspace_size, ctypes.byref(d), inp.is_csr)
+    ws, wsb = _workspace(nb, workspace)
+    _check(L.sysml_conv2d(ctypes.byref(d), ctypes.byref(inp), _ptr(f, torch.float32, "f"),
+                          _ptr(bias, torch.float32, "bias"), _ptr(out, torch.float32, "out"),
+                          ws, wsb, _stream(stream)))
+    return out
+
+
+def sysml_conv2d_bwd_filter(x, dy, d: ConvDesc, df=None, db=None, want_db=True, workspace=None, stream=None):
+    torch = _torch()
+    L = lib()
+    inp = _input(x)
+    if df is None:
+        df = torch.empty((d.K, d.C * d.R * d.S), dtype=torch.float32, device="cuda")
+    if db is None and want_db:
+        db = torch.empty((d.K,), dtype=torch.float32, device="cuda")
+    nb = _ws_size(L.sysml_conv2d_bwd_filter_workspace_size, ctypes.byref(d), inp.is_csr)
+    ws, wsb = _workspace(nb, workspace)
+    _check(L.sysml_conv2d_bwd_filter(ctypes.byref(d), ctypes.byref(inp), _ptr(dy, torch.float32, "dy"),
+                                     _ptr(df, torch.float32, "df"), _ptr(db, torch.float32, "db"),
+                                     ws, wsb, _stream(stream)))
+    return df, db
+
+
+def sysml_conv2d_bwd_data(f, dy, d: ConvDesc, dx=None, workspace=None, stream=None):
+    torch = _torch()
+    L = lib()
+    if dx is None:
+        dx = torch.empty((d.N, d.C * d.H * d.W), dtype=torch.float32, device="cuda")
+    nb = _ws_size(L.sysml_conv2d_bwd_data_workspace_size, ctypes.byref(d))
+    ws, wsb = _workspace(nb, workspace)
+    _check(L.sysml_conv2d_bwd_data(ctypes.byref(d), _ptr(f, torch.float32, "f"), _ptr(dy, torch.float32, "dy"),
+                                   _ptr(dx, torch.float32, "dx"), ws, wsb, _stream(stream)))
+    return dx
+
+
+def sysml_bias_add(y, bias, N, K, PQ, stream=None):
+    torch = _torch()
+    _check(lib().sysml_bias_add(N, K, PQ, _ptr(y, torch.float32, "y"), _ptr(bias, torch.float32, "bias"),
+                                _stream(stream)))
+    return y
+
+
+def sysml_relu_maxpool(x, d: PoolDesc, out=None, argmax=None, want_argmax=True, stream=None):
+    torch = _torch()
+    if out is None:
+        out = torch.empty((d.N, d.C * d.P * d.Q), dtype=torch.float32, device="cuda")
+    if argmax is None and want_argmax:
+        argmax = torch.empty((d.N, d.C * d.P * d.Q), dtype=torch.int32, device="cuda")
+    _check(lib().sysml_relu_maxpool(ctypes.byref(d), _ptr(x, torch.float32, "x"), _ptr(out, torch.float32, "out"),
+                                    _ptr(argmax, torch.int32, "argmax"), _stream(stream)))
+    return out, argmax
+
+
+def sysml_maxpool_bwd(argmax, dout, d: PoolDesc, out_mask=None, dx=None, stream=None):
+    torch = _torch()
+    if dx is None:
+        dx = torch.empty((d.N, d.C * d.H * d.W), dtype=torch.float32, device="cuda")
+    _check(lib().sysml_maxpool_bwd(ctypes.byref(d), _ptr(argmax, torch.int32, "argmax"),
+                                   _ptr(dout, torch.float32, "dout"), _ptr(out_mask, torch.float32, "out_mask"),
+                                   _ptr(dx, torch.float32, "dx"), _stream(stream)))
+    return dx
+
+
+def sysml_conv2d_bias_relu_maxpool(x, f, bias, cd: ConvDesc, pd: PoolDesc, out=None, argmax=None,
+                                   workspace=None, stream=None):
+    torch = _torch()
+    L = lib()
+    inp = _input(x)
+    if out is None:
+        out = torch.empty((pd.N, pd.C * pd.P * pd.Q), dtype=torch.float32, device="cuda")
+    if argmax is None:
+        argmax = torch.empty((pd.N, pd.C * pd.P * pd.Q), dtype=torch.int32, device="cuda")
+    nb = _ws_size(L.sysml_conv2d_bias_relu_maxpool_workspace_size, ctypes.byref(cd), ctypes.byref(pd), inp.is_csr)
+    ws, wsb = _workspace(nb, workspace)
+    _check(L.sysml_conv2d_bias_relu_maxpool(ctypes.byref(cd), ctypes.byref(pd), ctypes.byref(inp),
+                                            _ptr(f, torch.float32, "f"), _ptr(bias, torch.float32, "bias"),
+                                            _ptr(out, torch.float32, "out"), _ptr(argmax, torch.int32, "argmax"),
+                                            ws, wsb, _stream(stream)))
+    return out, argmax
+
+
+def sysml_csr_check(m: CSR, stream=None) -> int:
+    torch = _torch()
+    v = ctypes.c_int64(0)
+    c = _Csr(m.rows, m.cols, m.nnz, _ptr(m.row_ptr, torch.int32).value,
+             _ptr(m.col_idx, torch.int32).value if m.nnz else None,
+             _ptr(m.val, torch.float32).value if m.nnz else None)
+    _check(lib().sysml_csr_check(ctypes.byref(c), ctypes.byref(v), _stream(stream)))
+    return v.value
+
+
+def sysml_sgd_update(params, grads, lr=0.01, stream=None):
+    torch = _torch()
+    _check(lib().sysml_sgd_update(_ptr(params, torch.float32, "params"), _ptr(grads, torch.float32, "grads"),
+                                  params.numel(), ctypes.c_float(lr), _stream(stream)))
+    return params
+
+
+def sysml_launch_counter() -> int:
+    return int(lib().sysml_launch_counter())
+
+
+def sysml_version() -> str:
+    return lib().sysml_version().decode()
+
+
+def nccl_comm_ptr(group=None) -> Optional[int]:
+    """ncclComm_t of torch's ProcessGroupNCCL (created lazily; run one collective first)."""
+    torch = _torch()
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return None
+    pg = group or dist.distributed_c10d._get_default_group()
+    be = pg._get_backend(torch.device("cuda"))
+    return int(be._comm_ptr())
+
+
+class LeNet:
+    """Minibatch SGD-step driver (Listing 1; P:142 LeNet; P:187-192 data-parallel plan)."""
+
+    NUM_PARAMS = 83466
+
+    def __init__(self, max_local_batch: int, math="tf32", csr=False, max_nnz=0):
+        L = lib()
+        h = ctypes.c_void_p()
+        _check(L.sysml_lenet_create(int(max_local_batch), _MATH[math], int(bool(csr)), int(max_nnz), ctypes.byref(h)))
+        self.h = h
+        self.max_local_batch = max_local_batch
+        self.csr = bool(csr)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sysml_lenet_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def fwd_bwd(self, params, x, labels, n_global, grads, loss_sum=None, stream=None):
+        torch = _torch()
+        inp = _input(x)
+        n = x.rows if isinstance(x, CSR) else x.shape[0]
+        _check(lib().sysml_lenet_fwd_bwd(self.h, _ptr(params, torch.float32, "params"), ctypes.byref(inp),
+                                         _ptr(labels, torch.int32, "labels"), int(n), int(n_global),
+                                         _ptr(grads, torch.float32, "grads"), _ptr(loss_sum, torch.float32, "loss_sum"),
+                                         _stream(stream)))
+
+    def step(self, params, grads, x, labels, n_global, lr=0.01, nccl_comm=None, loss_sum=None, stream=None):
+        torch = _torch()
+        inp = _input(x)
+        n = x.rows if isinstance(x, CSR) else x.shape[0]
+        _check(lib().sysml_lenet_step(self.h, _ptr(params, torch.float32, "params"), _ptr(grads, torch.float32, "grads"),
+                                      ctypes.byref(inp), _ptr(labels, torch.int32, "labels"), int(n), int(n_global),
+                                      ctypes.c_float(lr), ctypes.c_void_p(nccl_comm) if nccl_comm else None,
+                                      _ptr(loss_sum, torch.float32, "loss_sum"), _stream(stream)))
+
+    def step_host(self, params, grads, x_host, labels_host, n_global, lr=0.01, nccl_comm=None, stream=None) -> float:
+        """End-to-end step from HOST (ideally pinned) float32 / int32 CPU tensors."""
+        torch = _torch()
+        loss = ctypes.c_float(0.0)
+        if x_host.is_cuda or labels_host.is_cuda or x_host.dtype != torch.float32 or labels_host.dtype != torch.int32:
+            raise TypeError("step_host takes float32 / int32 CPU tensors")
+        _check(lib().sysml_lenet_step_host(self.h, _ptr(params, torch.float32), _ptr(grads, torch.float32),
+                                           ctypes.c_void_p(x_host.data_ptr()), ctypes.c_void_p(labels_host.data_ptr()),
+                                           int(x_host.shape[0]), int(n_global), ctypes.c_float(lr),
+                                           ctypes.c_void_p(nccl_comm) if nccl_comm else None,
+                                           ctypes.byref(loss), _stream(stream)))
+        return loss.value
+
+    def set_timing(self, enable: bool):
+        _check(lib().sysml_lenet_set_timing(self.h, int(bool(enable))))
+
+    def get_timing(self, reset=False):
+        n = 16
+        ms = (ctypes.c_double * n)()
+        calls = (ctypes.c_int64 * n)()
+        names = (ctypes.c_char_p * n)()
+        ns = ctypes.c_int32(0)
+        _check(lib().sysml_lenet_get_timing(self.h, n, ctypes.byref(ns), ms, calls, names))
+        out = {names[i].decode(): (ms[i], calls[i]) for i in range(ns.value)}
+        if reset:
+            _check(lib().sysml_lenet_get_timing(self.h, -1, None, None, None, None))
+        return out

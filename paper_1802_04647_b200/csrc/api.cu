@@ -1,0 +1,283 @@
+// api.cu -- the extern "C" entry points of include/sysml.h: validation and dispatch
+// to the sm_100a kernels.  No CPU fallback exists (BJ north_star): every path
+// below launches CUDA kernels on the caller's stream.
+//
+// Dispatch:
+//   dense conv fwd / bwd_data / bwd_filter:
+//     math == TF32 and the tcgen05 kernel covers the shape -> conv_tc.cu (K3/K5/K6)
+//     otherwise                                             -> conv_simt.cu (fp32 FMA)
+//   CSR input: fwd -> csr.cu K7 (fused epilogue optional); bwd_filter -> csr.cu K8;
+//     shapes beyond K7/K8's shared-memory budget are densified into the workspace
+//     first (still on the GPU) and take the dense path.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sysml {
+
+thread_local int64_t g_launches = 0;
+
+static bool fused_pool_ok(const ConvGeom &cg, const ConvGeom &pg, const sysml_pool_desc *pd) {
+  return pg.N == cg.N && pg.C == cg.K && pg.H == cg.P && pg.W == cg.Q && pd->relu &&
+         pd->R == pd->stride_h && pd->S == pd->stride_w && pd->pad_h == 0 && pd->pad_w == 0;
+}
+
+sysml_status conv_fwd_ws(const sysml_conv_desc &cd, const sysml_pool_desc *pd, int is_csr,
+                         size_t *bytes) {
+  ConvGeom g;
+  SYSML_TRY(validate_conv(&cd, &g));
+  const ConvArgs a = conv_args(g);
+  size_t b = 0;
+  const bool use_tc = cd.math == SYSML_MATH_TF32;
+  PoolArgs pa{};
+  const PoolArgs *pap = nullptr;
+  if (pd) {
+    ConvGeom pg;
+    SYSML_TRY(validate_pool(pd, &pg));
+    pa = pool_args(pg, 1);
+    pap = &pa;
+  }
+  if (is_csr) {
+    if (!csr_fwd_supported(a)) {
+      b += align_up((size_t)g.N * g.CHW() * sizeof(float), 256);  // densified input
+      if (use_tc && tc_fwd_supported(a, pap)) b += tc_fwd_ws(a);
+      else if (pd) b += align_up((size_t)g.N * g.KPQ() * sizeof(float), 256);
+    }
+  } else if (use_tc && tc_fwd_supported(a, pap)) {
+    b += tc_fwd_ws(a);
+  } else if (pd) {
+    b += align_up((size_t)g.N * g.KPQ() * sizeof(float), 256);  // unfused z
+  }
+  *bytes = b;
+  return SYSML_OK;
+}
+
+sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, const float *f,
+                               const float *bias, float *y, const sysml_pool_desc *pd,
+                               float *pout, int32_t *parg, void *ws, size_t ws_bytes,
+                               cudaStream_t st) {
+  ConvGeom g;
+  SYSML_TRY(validate_conv(&cd, &g));
+  SYSML_TRY(validate_input(&x, g));
+  SYSML_CHECK_ARG(f != nullptr, "filter pointer is NULL");
+  const ConvArgs a = conv_args(g);
+  PoolArgs pa{};
+  const PoolArgs *pap = nullptr;
+  if (pd) {
+    ConvGeom pg;
+    SYSML_TRY(validate_pool(pd, &pg));
+    SYSML_CHECK_SHAPE(pg.N == g.N && pg.C == g.K && pg.H == g.P && pg.W == g.Q,
+                      "pool input %lldx(%lld*%lld*%lld) must equal the conv output %lldx(%lld*%lld*%lld)",
+                      (long long)pg.N, (long long)pg.C, (long long)pg.H, (long long)pg.W,
+                      (long long)g.N, (long long)g.K, (long long)g.P, (long long)g.Q);
+    if (!fused_pool_ok(g, pg, pd)) {
+      set_error("fused conv+bias+relu+maxpool supports relu=1, window == stride, pad 0 "
+                "(got window %dx%d stride %dx%d pad %dx%d relu %d)",
+                pd->R, pd->S, pd->stride_h, pd->stride_w, pd->pad_h, pd->pad_w, pd->relu);
+      return SYSML_ERR_UNSUPPORTED;
+    }
+    SYSML_CHECK_ARG(pout != nullptr, "pooled output pointer is NULL");
+    pa = pool_args(pg, 1);
+    pap = &pa;
+  } else {
+    SYSML_CHECK_ARG(y != nullptr, "output pointer is NULL");
+  }
+  size_t need = 0;
+  SYSML_TRY(conv_fwd_ws(cd, pd, x.is_csr, &need));
+  if (need > 0 && (ws == nullptr || ws_bytes < need)) {
+    set_error("workspace too small: need %zu bytes, got %zu", need, ws ? ws_bytes : 0);
+    return SYSML_ERR_WORKSPACE;
+  }
+  WsCarve wc(ws, ws_bytes);
+  const bool use_tc = cd.math == SYSML_MATH_TF32 && tc_fwd_supported(a, pap);
+  const float *xd = x.dense;
+  if (x.is_csr) {
+    if (csr_fwd_supported(a)) return csr_conv_fwd(a, x.csr, f, bias, y, pap, pout, parg, st);
+    float *dense = wc.take<float>((size_t)g.N * g.CHW());
+    SYSML_TRY(csr_densify(x.csr, dense, st));
+    xd = dense;
+  }
+  if (use_tc) {
+    void *tws = wc.take<char>(tc_fwd_ws(a));
+    return tc_conv_fwd(a, xd, f, bias, y, pap, pout, parg, tws, st);
+  }
+  if (pap) {
+    float *z = wc.take<float>((size_t)g.N * g.KPQ());
+    SYSML_TRY(simt_conv_fwd(a, xd, f, bias, z, st));
+    return launch_relu_maxpool(*pap, z, pout, parg, st);
+  }
+  return simt_conv_fwd(a, xd, f, bias, y, st);
+}
+
+sysml_status conv_bwd_filter_ws(const sysml_conv_desc &cd, int is_csr, size_t *bytes) {
+  ConvGeom g;
+  SYSML_TRY(validate_conv(&cd, &g));
+  const ConvArgs a = conv_args(g);
+  size_t b = 0;
+  if (is_csr && csr_bwd_filter_supported(a)) {
+    b = csr_bwd_filter_ws(a);
+  } else {
+    if (is_csr) b += align_up((size_t)g.N * g.CHW() * sizeof(float), 256);
+    if (cd.math == SYSML_MATH_TF32 && tc_bwd_filter_supported(a)) b += tc_bwd_filter_ws(a);
+    else b += simt_bwd_filter_ws(a);
+  }
+  *bytes = b;
+  return SYSML_OK;
+}
+
+sysml_status conv_bwd_filter_dispatch(const sysml_conv_desc &cd, const sysml_input &x,
+                                      const float *dy, float *df, float *db, void *ws,
+                                      size_t ws_bytes, cudaStream_t st) {
+  ConvGeom g;
+  SYSML_TRY(validate_conv(&cd, &g));
+  SYSML_TRY(validate_input(&x, g));
+  SYSML_CHECK_ARG(dy && df, "dy/df pointer is NULL");
+  const ConvArgs a = conv_args(g);
+  size_t need = 0;
+  SYSML_TRY(conv_bwd_filter_ws(cd, x.is_csr, &need));
+  if (need > 0 && (ws == nullptr || ws_bytes < need)) {
+    set_error("workspace too small: need %zu bytes, got %zu", need, ws ? ws_bytes : 0);
+    return SYSML_ERR_WORKSPACE;
+  }
+  WsCarve wc(ws, ws_bytes);
+  const float *xd = x.dense;
+  if (x.is_csr) {
+    if (csr_bwd_filter_supported(a)) return csr_conv_bwd_filter(a, x.csr, dy, df, db, ws, st);
+    float *dense = wc.take<float>((size_t)g.N * g.CHW());
+    SYSML_TRY(csr_densify(x.csr, dense, st));
+    xd = dense;
+  }
+  if (cd.math == SYSML_MATH_TF32 && tc_bwd_filter_supported(a)) {
+    void *tws = wc.take<char>(tc_bwd_filter_ws(a));
+    return tc_conv_bwd_filter(a, xd, dy, df, db, tws, st);
+  }
+  void *sws = wc.take<char>(simt_bwd_filter_ws(a));
+  return simt_conv_bwd_filter(a, xd, dy, df, db, sws, st);
+}
+
+sysml_status conv_bwd_data_ws(const sysml_conv_desc &cd, size_t *bytes) {
+  ConvGeom g;
+  SYSML_TRY(validate_conv(&cd, &g));
+  const ConvArgs a = conv_args(g);
+  *bytes = (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a)) ? tc_bwd_data_ws(a) : 0;
+  return SYSML_OK;
+}
+
+sysml_status conv_bwd_data_dispatch(const sysml_conv_desc &cd, const float *f, const float *dy,
+                                    float *dx, void *ws, size_t ws_bytes, cudaStream_t st) {
+  ConvGeom g;
+  SYSML_TRY(validate_conv(&cd, &g));
+  SYSML_CHECK_ARG(f && dy && dx, "f/dy/dx pointer is NULL");
+  const ConvArgs a = conv_args(g);
+  size_t need = 0;
+  SYSML_TRY(conv_bwd_data_ws(cd, &need));
+  if (need > 0 && (ws == nullptr || ws_bytes < need)) {
+    set_error("workspace too small: need %zu bytes, got %zu", need, ws ? ws_bytes : 0);
+    return SYSML_ERR_WORKSPACE;
+  }
+  if (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a))
+    return tc_conv_bwd_data(a, f, dy, dx, ws, st);
+  return simt_conv_bwd_data(a, f, dy, dx, st);
+}
+
+}  // namespace sysml
+
+using namespace sysml;
+
+extern "C" {
+
+const char *sysml_version(void) { return "sysml-b200 0.1 (sm_100a; tcgen05 TF32 + fp32 SIMT + CSR)"; }
+const char *sysml_last_error(void) { return get_error(); }
+int32_t sysml_device_sm_count(void) { return sm_count(); }
+int64_t sysml_launch_counter(void) { return g_launches; }
+
+sysml_status sysml_conv2d_workspace_size(const sysml_conv_desc *d, int32_t is_csr, size_t *bytes) {
+  SYSML_CHECK_ARG(d && bytes, "NULL argument");
+  return conv_fwd_ws(*d, nullptr, is_csr, bytes);
+}
+
+sysml_status sysml_conv2d(const sysml_conv_desc *d, const sysml_input *x, const float *f,
+                          const float *bias, float *y, void *workspace, size_t workspace_bytes,
+                          sysml_stream_t stream) {
+  SYSML_CHECK_ARG(d && x, "NULL descriptor or input");
+  return conv_fwd_dispatch(*d, *x, f, bias, y, nullptr, nullptr, nullptr, workspace,
+                           workspace_bytes, (cudaStream_t)stream);
+}
+
+sysml_status sysml_conv2d_bwd_filter_workspace_size(const sysml_conv_desc *d, int32_t is_csr,
+                                                    size_t *bytes) {
+  SYSML_CHECK_ARG(d && bytes, "NULL argument");
+  return conv_bwd_filter_ws(*d, is_csr, bytes);
+}
+
+sysml_status sysml_conv2d_bwd_filter(const sysml_conv_desc *d, const sysml_input *x,
+                                     const float *dy, float *df, float *db, void *workspace,
+                                     size_t workspace_bytes, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(d && x, "NULL descriptor or input");
+  return conv_bwd_filter_dispatch(*d, *x, dy, df, db, workspace, workspace_bytes,
+                                  (cudaStream_t)stream);
+}
+
+sysml_status sysml_conv2d_bwd_data_workspace_size(const sysml_conv_desc *d, size_t *bytes) {
+  SYSML_CHECK_ARG(d && bytes, "NULL argument");
+  return conv_bwd_data_ws(*d, bytes);
+}
+
+sysml_status sysml_conv2d_bwd_data(const sysml_conv_desc *d, const float *f, const float *dy,
+                                   float *dx, void *workspace, size_t workspace_bytes,
+                                   sysml_stream_t stream) {
+  SYSML_CHECK_ARG(d, "NULL descriptor");
+  return conv_bwd_data_dispatch(*d, f, dy, dx, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+sysml_status sysml_bias_add(int32_t N, int32_t K, int32_t PQ, float *y, const float *bias,
+                            sysml_stream_t stream) {
+  SYSML_CHECK_ARG(N >= 1 && K >= 1 && PQ >= 1, "bias_add dims must be >= 1 (N=%d K=%d PQ=%d)", N,
+                  K, PQ);
+  SYSML_CHECK_ARG(y && bias, "NULL pointer");
+  return launch_bias_add(N, K, PQ, y, bias, (cudaStream_t)stream);
+}
+
+sysml_status sysml_relu_maxpool(const sysml_pool_desc *d, const float *x, float *out,
+                                int32_t *argmax, sysml_stream_t stream) {
+  ConvGeom g;
+  SYSML_TRY(validate_pool(d, &g));
+  SYSML_CHECK_ARG(x && out, "NULL pointer");
+  return launch_relu_maxpool(pool_args(g, d->relu ? 1 : 0), x, out, argmax, (cudaStream_t)stream);
+}
+
+sysml_status sysml_maxpool_bwd(const sysml_pool_desc *d, const int32_t *argmax,
+                               const float *dout, const float *out_mask, float *dx,
+                               sysml_stream_t stream) {
+  ConvGeom g;
+  SYSML_TRY(validate_pool(d, &g));
+  SYSML_CHECK_ARG(argmax && dout && dx, "NULL pointer");
+  return launch_maxpool_bwd(pool_args(g, d->relu ? 1 : 0), argmax, dout, out_mask, dx,
+                            (cudaStream_t)stream);
+}
+
+sysml_status sysml_conv2d_bias_relu_maxpool_workspace_size(const sysml_conv_desc *cd,
+                                                           const sysml_pool_desc *pd,
+                                                           int32_t is_csr, size_t *bytes) {
+  SYSML_CHECK_ARG(cd && pd && bytes, "NULL argument");
+  return conv_fwd_ws(*cd, pd, is_csr, bytes);
+}
+
+sysml_status sysml_conv2d_bias_relu_maxpool(const sysml_conv_desc *cd, const sysml_pool_desc *pd,
+                                            const sysml_input *x, const float *f,
+                                            const float *bias, float *out, int32_t *argmax,
+                                            void *workspace, size_t workspace_bytes,
+                                            sysml_stream_t stream) {
+  SYSML_CHECK_ARG(cd && pd && x, "NULL descriptor or input");
+  SYSML_CHECK_ARG(bias != nullptr, "bias pointer is NULL");
+  return conv_fwd_dispatch(*cd, *x, f, bias, nullptr, pd, out, argmax, workspace, workspace_bytes,
+                           (cudaStream_t)stream);
+}
+
+sysml_status sysml_csr_check(const sysml_csr *m, int64_t *violations, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(m && violations && m->row_ptr, "NULL argument");
+  return csr_check(*m, violations, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// common.cuh -- shared host/device helpers of libsysml (product path only).
+// No code here is shared with the oracle (oracle/oracle.c).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/sysml.h"
+
+namespace sysml {
+
+// Thread-local last error message (sysml_last_error).
+void set_error(const char *fmt, ...) __attribute__((format(printf, 1, 2)));
+const char *get_error();
+
+#define SYSML_CHECK_ARG(cond, ...)   \
+  do {                               \
+    if (!(cond)) {                   \
+      ::sysml::set_error(__VA_ARGS__); \
+      return SYSML_ERR_ARG;          \
+    }                                \
+  } while (0)
+
+#define SYSML_CHECK_SHAPE(cond, ...) \
+  do {                               \
+    if (!(cond)) {                   \
+      ::sysml::set_error(__VA_ARGS__); \
+      return SYSML_ERR_SHAPE;        \
+    }                                \
+  } while (0)
+
+#define SYSML_CUDA(call)                                                           \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      ::sysml::set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(e_),        \
+                         __FILE__, __LINE__, cudaGetErrorString(e_));              \
+      return SYSML_ERR_CUDA;                                                       \
+    }                                                                              \
+  } while (0)
+
+extern thread_local int64_t g_launches;  // kernels launched by this thread (api.cu)
+
+// After a kernel launch: count it and report launch-configuration errors.
+#define SYSML_LAUNCH_CHECK()               \
+  do {                                     \
+    ++::sysml::g_launches;                 \
+    SYSML_CUDA(cudaPeekAtLastError());     \
+  } while (0)
+
+#define SYSML_TRY(expr)                     \
+  do {                                      \
+    sysml_status s_ = (expr);               \
+    if (s_ != SYSML_OK) return s_;          \
+  } while (0)
+
+inline int64_t out_extent(int64_t in, int64_t pad, int64_t k, int64_t stride) {
+  int64_t num = in + 2 * pad - k;
+  if (num < 0 || stride <= 0) return 0;
+  return num / stride + 1;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline size_t align_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
+
+int sm_count();              // cached per device
+int device_cc_major();       // cached per device
+
+// Derived geometry of a conv descriptor.
+struct ConvGeom {
+  int64_t N, C, H, W, K, R, S, sh, sw, ph, pw, P, Q;
+  int64_t CHW() const { return C * H * W; }
+  int64_t CRS() const { return C * R * S; }
+  int64_t KPQ() const { return K * P * Q; }
+  int64_t PQ() const { return P * Q; }
+  int64_t HW() const { return H * W; }
+};
+
+sysml_status validate_conv(const sysml_conv_desc *d, ConvGeom *g);
+sysml_status validate_input(const sysml_input *x, const ConvGeom &g);
+sysml_status validate_pool(const sysml_pool_desc *d, ConvGeom *g /* R,S,sh,... P,Q; K unused */);
+
+// Simple bump allocator over a caller workspace.
+struct WsCarve {
+  char *base;
+  size_t size, off = 0;
+  WsCarve(void *b, size_t s) : base((char *)b), size(s) {}
+  template <class T>
+  T *take(size_t count) {
+    off = align_up(off, 256);
+    T *p = (T *)(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    return p;
+  }
+  size_t used() const { return align_up(off, 256); }
+};
+
+}  // namespace sysml

@@ -1,0 +1,74 @@
+// kernels.cuh -- launcher declarations shared between the API layer and kernels.
+#pragma once
+#include "common.cuh"
+
+namespace sysml {
+
+struct PoolArgs {
+  int N, C, H, W, R, S, sh, sw, ph, pw, P, Q, relu;
+};
+
+inline PoolArgs pool_args(const ConvGeom &g, int relu) {
+  return PoolArgs{(int)g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.R, (int)g.S, (int)g.sh,
+                  (int)g.sw, (int)g.ph, (int)g.pw, (int)g.P, (int)g.Q, relu};
+}
+
+struct ConvArgs {
+  int N, C, H, W, K, R, S, sh, sw, ph, pw, P, Q;
+};
+
+inline ConvArgs conv_args(const ConvGeom &g) {
+  return ConvArgs{(int)g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.K, (int)g.R, (int)g.S,
+                  (int)g.sh, (int)g.sw, (int)g.ph, (int)g.pw, (int)g.P, (int)g.Q};
+}
+
+// pool.cu
+sysml_status launch_relu_maxpool(const PoolArgs &a, const float *x, float *out, int32_t *argmax,
+                                 cudaStream_t st);
+sysml_status launch_maxpool_bwd(const PoolArgs &a, const int32_t *argmax, const float *dout,
+                                const float *mask, float *dx, cudaStream_t st);
+sysml_status launch_bias_add(int32_t N, int32_t K, int32_t PQ, float *y, const float *bias,
+                             cudaStream_t st);
+sysml_status launch_zero(float *p, int64_t n, cudaStream_t st);
+
+// conv_simt.cu : fp32 CUDA-core implicit GEMM (all shapes; SYSML_MATH_FP32)
+sysml_status simt_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
+                           float *y, cudaStream_t st);
+size_t simt_bwd_filter_ws(const ConvArgs &a);
+sysml_status simt_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,
+                                  float *db, void *ws, cudaStream_t st);
+sysml_status simt_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
+                                cudaStream_t st);
+sysml_status launch_bias_grad(const ConvArgs &a, const float *dy, float *db, float *part,
+                              cudaStream_t st);
+size_t bias_grad_ws(const ConvArgs &a);
+
+// csr.cu : CSR-input kernels (CUDA cores, HBM-bound)
+bool csr_fwd_supported(const ConvArgs &a);
+sysml_status csr_conv_fwd(const ConvArgs &a, const sysml_csr &x, const float *f,
+                          const float *bias, float *y, const PoolArgs *pool, float *pout,
+                          int32_t *parg, cudaStream_t st);
+bool csr_bwd_filter_supported(const ConvArgs &a);
+size_t csr_bwd_filter_ws(const ConvArgs &a);
+sysml_status csr_conv_bwd_filter(const ConvArgs &a, const sysml_csr &x, const float *dy,
+                                 float *df, float *db, void *ws, cudaStream_t st);
+sysml_status csr_densify(const sysml_csr &x, float *dense, cudaStream_t st);
+sysml_status csr_check(const sysml_csr &m, int64_t *violations, cudaStream_t st);
+
+// conv_tc.cu : tcgen05 TF32 implicit GEMM (SYSML_MATH_TF32)
+struct TcPlan;  // opaque
+bool tc_fwd_supported(const ConvArgs &a, const PoolArgs *pool);
+size_t tc_fwd_ws(const ConvArgs &a);
+sysml_status tc_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
+                         float *y, const PoolArgs *pool, float *pout, int32_t *parg, void *ws,
+                         cudaStream_t st);
+bool tc_bwd_data_supported(const ConvArgs &a);
+size_t tc_bwd_data_ws(const ConvArgs &a);
+sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
+                              void *ws, cudaStream_t st);
+bool tc_bwd_filter_supported(const ConvArgs &a);
+size_t tc_bwd_filter_ws(const ConvArgs &a);
+sysml_status tc_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,
+                                float *db, void *ws, cudaStream_t st);
+
+}  // namespace sysml

@@ -1,0 +1,543 @@
+// lenet.cu -- minibatch SGD-step driver (Listing 1; P:142 LeNet; P:187-192
+// data-parallel plan) over the conv2d-family kernels, plus the step glue kernels:
+// affine + softmax + cross-entropy, SGD and the NCCL
+// gradient allreduce of the data-parallel plan.
+//
+// Step (SURVEY §8(c) def 8), local batch b, global batch Ng:
+//   F1  conv1+bias+relu+pool    X[b x 784]      -> a1[b x 6272], i1
+//   F2  conv2+bias+relu+pool    a1              -> a2[b x 3136], i2
+//   F3  affine+softmax+CE       a2, W3, b3      -> ds[b x 10] = (p - onehot)/Ng, loss_n
+//   B3  dW3 = ds^T a2 (split over samples, ordered sum); db3 = colsum ds; da2 = ds W3
+//   B2p dz2 = maxpool_bwd(i2, da2, a2 > 0)
+//   B2f dF2, db2 = bwd_filter(a1, dz2);  B2d da1 = bwd_data(F2, dz2)
+//   B1p dz1 = maxpool_bwd(i1, da1, a1 > 0); B1f dF1, db1 = bwd_filter(X, dz1)
+#include <dlfcn.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sysml {
+sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, const float *f,
+                               const float *bias, float *y, const sysml_pool_desc *pd,
+                               float *pout, int32_t *parg, void *ws, size_t ws_bytes,
+                               cudaStream_t st);
+sysml_status conv_fwd_ws(const sysml_conv_desc &cd, const sysml_pool_desc *pd, int is_csr,
+                         size_t *bytes);
+sysml_status conv_bwd_filter_dispatch(const sysml_conv_desc &cd, const sysml_input &x,
+                                      const float *dy, float *df, float *db, void *ws,
+                                      size_t ws_bytes, cudaStream_t st);
+sysml_status conv_bwd_filter_ws(const sysml_conv_desc &cd, int is_csr, size_t *bytes);
+sysml_status conv_bwd_data_dispatch(const sysml_conv_desc &cd, const float *f, const float *dy,
+                                    float *dx, void *ws, size_t ws_bytes, cudaStream_t st);
+sysml_status conv_bwd_data_ws(const sysml_conv_desc &cd, size_t *bytes);
+}  // namespace sysml
+
+using namespace sysml;
+
+namespace {
+
+constexpr int OFF_F1 = 0, OFF_B1 = OFF_F1 + 32 * 25, OFF_F2 = OFF_B1 + 32,
+              OFF_B2 = OFF_F2 + 64 * 800, OFF_W3 = OFF_B2 + 64, OFF_B3 = OFF_W3 + 10 * 3136,
+              NUM_PARAMS = OFF_B3 + 10;
+constexpr int D3 = 3136, NCLS = 10;
+
+// F3: one warp per sample: logits, max-shifted softmax, ds = (p - onehot)/Ng,
+// per-sample loss -log(max(p_y, 1e-15))/Ng.
+__global__ void affine_softmax_ce_kernel(int n, float inv_ng, const float *__restrict__ a2,
+                                         const float *__restrict__ W3, const float *__restrict__ b3,
+                                         const int32_t *__restrict__ labels,
+                                         float *__restrict__ ds, float *__restrict__ loss_n) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const float4 *row = reinterpret_cast<const float4 *>(a2 + (int64_t)warp * D3);
+  float acc[NCLS];
+#pragma unroll
+  for (int j = 0; j < NCLS; ++j) acc[j] = 0.f;
+  for (int d4 = lane; d4 < D3 / 4; d4 += 32) {
+    const float4 v = __ldg(row + d4);
+#pragma unroll
+    for (int j = 0; j < NCLS; ++j) {
+      const float4 w = __ldg(reinterpret_cast<const float4 *>(W3 + j * D3) + d4);
+      acc[j] = fmaf(v.x, w.x, fmaf(v.y, w.y, fmaf(v.z, w.z, fmaf(v.w, w.w, acc[j]))));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NCLS; ++j)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+  if (lane == 0) {
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < NCLS; ++j) {
+      acc[j] += __ldg(b3 + j);
+      m = fmaxf(m, acc[j]);
+    }
+    float den = 0.f;
+#pragma unroll
+    for (int j = 0; j < NCLS; ++j) den += expf(acc[j] - m);
+    const int y = labels[warp];
+    float lossv = 0.f;
+#pragma unroll
+    for (int j = 0; j < NCLS; ++j) {
+      const float p = expf(acc[j] - m) / den;
+      ds[warp * NCLS + j] = (p - (j == y ? 1.f : 0.f)) * inv_ng;
+      if (j == y) lossv = -logf(fmaxf(p, 1e-15f)) * inv_ng;
+    }
+    loss_n[warp] = lossv;
+  }
+}
+
+// ordered sum of v[0..n) into *out (single block, fixed tree)
+__global__ void ordered_total_kernel(const float *__restrict__ v, int n, float *__restrict__ out) {
+  __shared__ float red[1024];
+  float s = 0.f;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int i0 = threadIdx.x * per, i1 = min(n, i0 + per);
+  for (int i = i0; i < i1; ++i) s += v[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+// B3 stage 1: partial dW3/db3 over a chunk of samples.  Thread owns column d (all
+// 10 classes); part[chunk][j][d] (j < 10) and part[chunk][10][j] for db3.
+constexpr int DW3_THREADS = 256;
+__global__ void dw3_partial_kernel(int n, int n_per_chunk, const float *__restrict__ ds,
+                                   const float *__restrict__ a2, float *__restrict__ part) {
+  const int d = blockIdx.x * DW3_THREADS + threadIdx.x;
+  const int chunk = blockIdx.y;
+  const int n0 = chunk * n_per_chunk, n1 = min(n, n0 + n_per_chunk);
+  __shared__ float dss[64 * NCLS];
+  float acc[NCLS];
+#pragma unroll
+  for (int j = 0; j < NCLS; ++j) acc[j] = 0.f;
+  for (int nb = n0; nb < n1; nb += 64) {
+    const int cnt = min(64, n1 - nb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt * NCLS; i += DW3_THREADS) dss[i] = ds[(int64_t)nb * NCLS + i];
+    __syncthreads();
+    if (d < D3) {
+      for (int i = 0; i < cnt; ++i) {
+        const float v = __ldg(a2 + (int64_t)(nb + i) * D3 + d);
+#pragma unroll
+        for (int j = 0; j < NCLS; ++j) acc[j] = fmaf(dss[i * NCLS + j], v, acc[j]);
+      }
+    }
+  }
+  float *pc = part + (int64_t)chunk * (NCLS * D3 + NCLS);
+  if (d < D3) {
+#pragma unroll
+    for (int j = 0; j < NCLS; ++j) pc[j * D3 + d] = acc[j];
+  }
+  if (blockIdx.x == 0 && threadIdx.x < NCLS) {
+    float s = 0.f;
+    for (int i = n0; i < n1; ++i) s += ds[(int64_t)i * NCLS + threadIdx.x];
+    pc[NCLS * D3 + threadIdx.x] = s;
+  }
+}
+
+__global__ void chunk_sum_kernel(const float *__restrict__ part, int chunks, int64_t len,
+                                 float *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int c = 0; c < chunks; ++c) s += part[(int64_t)c * len + i];
+    out[i] = s;
+  }
+}
+
+// da2[n,d] = sum_j ds[n,j] W3[j,d]
+__global__ void da2_kernel(int n, const float *__restrict__ ds, const float *__restrict__ W3,
+                           float *__restrict__ da2) {
+  const int64_t total = (int64_t)n * D3;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = i / D3;
+    const int d = (int)(i - s * D3);
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < NCLS; ++j) acc = fmaf(__ldg(ds + s * NCLS + j), __ldg(W3 + j * D3 + d), acc);
+    da2[i] = acc;
+  }
+}
+
+__global__ void sgd_kernel(float *__restrict__ p, const float *__restrict__ g, int64_t n,
+                           float lr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = p[i] - lr * g[i];
+}
+
+// ---- NCCL (resolved at run time from the library the caller already loaded) ----
+typedef int (*nccl_allreduce_fn)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+typedef const char *(*nccl_errstr_fn)(int);
+
+struct NcclSyms {
+  nccl_allreduce_fn allreduce = nullptr;
+  nccl_errstr_fn errstr = nullptr;
+};
+
+NcclSyms &nccl_syms() {
+  static NcclSyms s;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    void *h = nullptr;
+    for (const char *nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_NOLOAD);
+      if (h) break;
+    }
+    if (!h) h = RTLD_DEFAULT;
+    s.allreduce = (nccl_allreduce_fn)dlsym(h, "ncclAllReduce");
+    s.errstr = (nccl_errstr_fn)dlsym(h, "ncclGetErrorString");
+  });
+  return s;
+}
+
+const char *STAGE_NAMES[] = {"F1_conv1_pool", "F2_conv2_pool", "F3_affine_softmax_ce",
+                             "B3_affine_bwd", "B2p_maxpool_bwd2", "B2f_conv2_bwd_filter",
+                             "B2d_conv2_bwd_data", "B1p_maxpool_bwd1", "B1f_conv1_bwd_filter"};
+constexpr int NSTAGES = 9;
+
+}  // namespace
+
+struct sysml_lenet {
+  int max_b = 0, math = 0, csr = 0;
+  int64_t max_nnz = 0;
+  float *a1 = nullptr, *a2 = nullptr, *ds = nullptr, *lossn = nullptr, *da2 = nullptr,
+        *dz2 = nullptr, *da1 = nullptr, *dz1 = nullptr, *part3 = nullptr;
+  int32_t *i1 = nullptr, *i2 = nullptr;
+  void *ws = nullptr;
+  size_t ws_bytes = 0;
+  // host-input path buffers
+  float *x_dev = nullptr, *loss_dev = nullptr;
+  int32_t *lab_dev = nullptr;
+  // timing
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool, pending[NSTAGES];
+  double ms[NSTAGES] = {0};
+  int64_t calls[NSTAGES] = {0};
+  int launches = 0;
+  int dw3_chunks = 1;
+};
+
+namespace {
+
+sysml_conv_desc conv1_desc(int n, int math) {
+  return sysml_conv_desc{n, 1, 28, 28, 32, 5, 5, 1, 1, 2, 2, math};
+}
+sysml_conv_desc conv2_desc(int n, int math) {
+  return sysml_conv_desc{n, 32, 14, 14, 64, 5, 5, 1, 1, 2, 2, math};
+}
+sysml_pool_desc pool1_desc(int n) { return sysml_pool_desc{n, 32, 28, 28, 2, 2, 2, 2, 0, 0, 1}; }
+sysml_pool_desc pool2_desc(int n) { return sysml_pool_desc{n, 64, 14, 14, 2, 2, 2, 2, 0, 0, 1}; }
+
+int dw3_chunks_for(int n) {
+  int64_t c = ceil_div(2 * sm_count(), ceil_div(D3, DW3_THREADS));
+  if (c > ceil_div(n, 16)) c = ceil_div(n, 16);
+  return (int)(c < 1 ? 1 : c);
+}
+
+struct StageTimer {
+  sysml_lenet *h;
+  cudaStream_t st;
+  int stage = -1;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  StageTimer(sysml_lenet *h_, cudaStream_t st_) : h(h_), st(st_) {}
+  sysml_status begin(int s) {
+    stage = s;
+    if (!h->timing) return SYSML_OK;
+    if (h->pool.empty()) {
+      cudaEvent_t a, b;
+      SYSML_CUDA(cudaEventCreate(&a));
+      SYSML_CUDA(cudaEventCreate(&b));
+      h->pool.push_back({a, b});
+    }
+    ev = h->pool.back();
+    h->pool.pop_back();
+    SYSML_CUDA(cudaEventRecord(ev.first, st));
+    return SYSML_OK;
+  }
+  sysml_status end() {
+    if (!h->timing) return SYSML_OK;
+    SYSML_CUDA(cudaEventRecord(ev.second, st));
+    h->pending[stage].push_back(ev);
+    return SYSML_OK;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int64_t sysml_lenet_num_params(void) { return NUM_PARAMS; }
+
+sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t input_is_csr,
+                                int64_t max_nnz, sysml_lenet **out) {
+  SYSML_CHECK_ARG(out != nullptr, "out is NULL");
+  SYSML_CHECK_ARG(max_local_batch >= 1, "max_local_batch must be >= 1 (got %d)", max_local_batch);
+  SYSML_CHECK_ARG(math == SYSML_MATH_FP32 || math == SYSML_MATH_TF32, "bad math %d", math);
+  SYSML_CHECK_ARG(!input_is_csr || max_nnz >= 0, "max_nnz must be >= 0");
+  sysml_lenet *h = new sysml_lenet();
+  h->max_b = max_local_batch;
+  h->math = math;
+  h->csr = input_is_csr ? 1 : 0;
+  h->max_nnz = max_nnz;
+  const int64_t b = max_local_batch;
+  h->dw3_chunks = dw3_chunks_for(max_local_batch);
+  auto fail = [&](sysml_status s) {
+    sysml_lenet_destroy(h);
+    return s;
+  };
+#define ALLOC(ptr, count)                                                        \
+  do {                                                                           \
+    cudaError_t e_ = cudaMalloc((void **)&(ptr), sizeof(*(ptr)) * (size_t)(count)); \
+    if (e_ != cudaSuccess) {                                                     \
+      set_error("cudaMalloc(%s) failed: %s", #ptr, cudaGetErrorString(e_));      \
+      return fail(SYSML_ERR_CUDA);                                               \
+    }                                                                            \
+  } while (0)
+  ALLOC(h->a1, b * 6272);
+  ALLOC(h->i1, b * 6272);
+  ALLOC(h->a2, b * 3136);
+  ALLOC(h->i2, b * 3136);
+  ALLOC(h->ds, b * NCLS);
+  ALLOC(h->lossn, b);
+  ALLOC(h->da2, b * 3136);
+  ALLOC(h->dz2, b * 12544);
+  ALLOC(h->da1, b * 6272);
+  ALLOC(h->dz1, b * 25088);
+  ALLOC(h->part3, (int64_t)h->dw3_chunks * (NCLS * D3 + NCLS));
+  ALLOC(h->loss_dev, 1);
+  ALLOC(h->lab_dev, b);
+  if (!h->csr) ALLOC(h->x_dev, b * 784);
+  // workspace: max over the conv calls of the step
+  size_t need = 0, w = 0;
+  const sysml_conv_desc c1 = conv1_desc(max_local_batch, math), c2 = conv2_desc(max_local_batch, math);
+  const sysml_pool_desc p1 = pool1_desc(max_local_batch), p2 = pool2_desc(max_local_batch);
+  sysml_status s;
+  if ((s = conv_fwd_ws(c1, &p1, h->csr, &w)) != SYSML_OK) return fail(s);
+  need = std::max(need, w);
+  if ((s = conv_fwd_ws(c2, &p2, 0, &w)) != SYSML_OK) return fail(s);
+  need = std::max(need, w);
+  if ((s = conv_bwd_filter_ws(c2, 0, &w)) != SYSML_OK) return fail(s);
+  need = std::max(need, w);
+  if ((s = conv_bwd_data_ws(c2, &w)) != SYSML_OK) return fail(s);
+  need = std::max(need, w);
+  if ((s = conv_bwd_filter_ws(c1, h->csr, &w)) != SYSML_OK) return fail(s);
+  need = std::max(need, w);
+  h->ws_bytes = need;
+  if (need) {
+    cudaError_t e = cudaMalloc(&h->ws, need);
+    if (e != cudaSuccess) {
+      set_error("cudaMalloc(workspace %zu) failed: %s", need, cudaGetErrorString(e));
+      return fail(SYSML_ERR_CUDA);
+    }
+  }
+#undef ALLOC
+  *out = h;
+  return SYSML_OK;
+}
+
+sysml_status sysml_lenet_destroy(sysml_lenet *h) {
+  if (!h) return SYSML_OK;
+  cudaFree(h->a1); cudaFree(h->i1); cudaFree(h->a2); cudaFree(h->i2); cudaFree(h->ds);
+  cudaFree(h->lossn); cudaFree(h->da2); cudaFree(h->dz2); cudaFree(h->da1); cudaFree(h->dz1);
+  cudaFree(h->part3); cudaFree(h->loss_dev); cudaFree(h->lab_dev); cudaFree(h->x_dev);
+  cudaFree(h->ws);
+  for (auto &e : h->pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  for (int i = 0; i < NSTAGES; ++i)
+    for (auto &e : h->pending[i]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  delete h;
+  return SYSML_OK;
+}
+
+sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysml_input *x,
+                                 const int32_t *labels, int32_t n_local, int64_t n_global,
+                                 float *grads, float *loss_sum, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(h && params && x && labels && grads, "NULL argument to sysml_lenet_fwd_bwd");
+  SYSML_CHECK_ARG(n_local >= 1 && n_local <= h->max_b,
+                  "n_local %d out of range [1, max_local_batch=%d]", n_local, h->max_b);
+  SYSML_CHECK_ARG(n_global >= n_local, "n_global %lld < n_local %d", (long long)n_global, n_local);
+  SYSML_CHECK_ARG((x->is_csr != 0) == (h->csr != 0),
+                  "input is_csr=%d but the handle was created with input_is_csr=%d", x->is_csr,
+                  h->csr);
+  if (x->is_csr) {
+    SYSML_CHECK_SHAPE(x->csr.rows == n_local && x->csr.cols == 784,
+                      "CSR input %lldx%lld must be n_local x 784 = %dx784",
+                      (long long)x->csr.rows, (long long)x->csr.cols, n_local);
+    SYSML_CHECK_SHAPE(x->csr.nnz <= h->max_nnz, "CSR nnz %lld exceeds max_nnz %lld",
+                      (long long)x->csr.nnz, (long long)h->max_nnz);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = n_local;
+  const float inv_ng = (float)(1.0 / (double)n_global);
+  const sysml_conv_desc c1 = conv1_desc(n, h->math), c2 = conv2_desc(n, h->math);
+  const sysml_pool_desc p1 = pool1_desc(n), p2 = pool2_desc(n);
+  StageTimer T(h, st);
+  int launches0 = 0;
+
+  // F1
+  SYSML_TRY(T.begin(0));
+  SYSML_TRY(conv_fwd_dispatch(c1, *x, params + OFF_F1, params + OFF_B1, nullptr, &p1, h->a1, h->i1,
+                              h->ws, h->ws_bytes, st));
+  SYSML_TRY(T.end());
+  // F2
+  SYSML_TRY(T.begin(1));
+  sysml_input a1in{0, h->a1, {}};
+  SYSML_TRY(conv_fwd_dispatch(c2, a1in, params + OFF_F2, params + OFF_B2, nullptr, &p2, h->a2,
+                              h->i2, h->ws, h->ws_bytes, st));
+  SYSML_TRY(T.end());
+  // F3
+  SYSML_TRY(T.begin(2));
+  affine_softmax_ce_kernel<<<(unsigned)ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(
+      n, inv_ng, h->a2, params + OFF_W3, params + OFF_B3, labels, h->ds, h->lossn);
+  SYSML_LAUNCH_CHECK();
+  if (loss_sum) {
+    ordered_total_kernel<<<1, 1024, 0, st>>>(h->lossn, n, loss_sum);
+    SYSML_LAUNCH_CHECK();
+  }
+  SYSML_TRY(T.end());
+  // B3
+  SYSML_TRY(T.begin(3));
+  {
+    const int chunks = std::min(h->dw3_chunks, dw3_chunks_for(n));
+    const int npc = (int)ceil_div(n, chunks);
+    const int used = (int)ceil_div(n, npc);
+    dw3_partial_kernel<<<dim3((unsigned)ceil_div(D3, DW3_THREADS), used), DW3_THREADS, 0, st>>>(
+        n, npc, h->ds, h->a2, h->part3);
+    SYSML_LAUNCH_CHECK();
+    // grads W3 and b3 are contiguous: [W3 (10*3136)][b3 (10)] == part layout
+    chunk_sum_kernel<<<(unsigned)ceil_div(NCLS * D3 + NCLS, 256), 256, 0, st>>>(
+        h->part3, used, NCLS * D3 + NCLS, grads + OFF_W3);
+    SYSML_LAUNCH_CHECK();
+    da2_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)n * D3, 256), 16 * sm_count()), 256,
+                 0, st>>>(n, h->ds, params + OFF_W3, h->da2);
+    SYSML_LAUNCH_CHECK();
+  }
+  SYSML_TRY(T.end());
+  // B2p
+  SYSML_TRY(T.begin(4));
+  {
+    ConvGeom g;
+    SYSML_TRY(validate_pool(&p2, &g));
+    SYSML_TRY(launch_maxpool_bwd(pool_args(g, 1), h->i2, h->da2, h->a2, h->dz2, st));
+  }
+  SYSML_TRY(T.end());
+  // B2f
+  SYSML_TRY(T.begin(5));
+  SYSML_TRY(conv_bwd_filter_dispatch(c2, a1in, h->dz2, grads + OFF_F2, grads + OFF_B2, h->ws,
+                                     h->ws_bytes, st));
+  SYSML_TRY(T.end());
+  // B2d
+  SYSML_TRY(T.begin(6));
+  SYSML_TRY(conv_bwd_data_dispatch(c2, params + OFF_F2, h->dz2, h->da1, h->ws, h->ws_bytes, st));
+  SYSML_TRY(T.end());
+  // B1p
+  SYSML_TRY(T.begin(7));
+  {
+    ConvGeom g;
+    SYSML_TRY(validate_pool(&p1, &g));
+    SYSML_TRY(launch_maxpool_bwd(pool_args(g, 1), h->i1, h->da1, h->a1, h->dz1, st));
+  }
+  SYSML_TRY(T.end());
+  // B1f
+  SYSML_TRY(T.begin(8));
+  SYSML_TRY(conv_bwd_filter_dispatch(c1, *x, h->dz1, grads + OFF_F1, grads + OFF_B1, h->ws,
+                                     h->ws_bytes, st));
+  SYSML_TRY(T.end());
+  (void)launches0;
+  return SYSML_OK;
+}
+
+sysml_status sysml_sgd_update(float *params, const float *grads, int64_t n, float lr,
+                              sysml_stream_t stream) {
+  SYSML_CHECK_ARG(params && grads && n >= 0, "bad arguments to sysml_sgd_update");
+  if (n == 0) return SYSML_OK;
+  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), 4 * sm_count());
+  sgd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(params, grads, n, lr);
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
+}
+
+sysml_status sysml_lenet_step(sysml_lenet *h, float *params, float *grads, const sysml_input *x,
+                              const int32_t *labels, int32_t n_local, int64_t n_global,
+                              float lr, void *nccl_comm, float *loss_sum, sysml_stream_t stream) {
+  SYSML_TRY(sysml_lenet_fwd_bwd(h, params, x, labels, n_local, n_global, grads, loss_sum, stream));
+  if (nccl_comm) {
+    NcclSyms &s = nccl_syms();
+    if (!s.allreduce) {
+      set_error("ncclAllReduce could not be resolved (libnccl.so.2 not loaded in this process)");
+      return SYSML_ERR_NCCL;
+    }
+    const int r = s.allreduce(grads, grads, (size_t)NUM_PARAMS, /*ncclFloat32*/ 7, /*ncclSum*/ 0,
+                              nccl_comm, (cudaStream_t)stream);
+    if (r != 0) {
+      set_error("ncclAllReduce failed: %s", s.errstr ? s.errstr(r) : "?");
+      return SYSML_ERR_NCCL;
+    }
+  }
+  return sysml_sgd_update(params, grads, NUM_PARAMS, lr, stream);
+}
+
+sysml_status sysml_lenet_step_host(sysml_lenet *h, float *params, float *grads,
+                                   const float *x_host, const int32_t *labels_host,
+                                   int32_t n_local, int64_t n_global, float lr, void *nccl_comm,
+                                   float *loss_host, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(h && x_host && labels_host && loss_host, "NULL argument to sysml_lenet_step_host");
+  SYSML_CHECK_ARG(!h->csr, "sysml_lenet_step_host takes dense host input (handle is CSR)");
+  SYSML_CHECK_ARG(n_local >= 1 && n_local <= h->max_b, "n_local %d out of range", n_local);
+  cudaStream_t st = (cudaStream_t)stream;
+  SYSML_CUDA(cudaMemcpyAsync(h->x_dev, x_host, sizeof(float) * (size_t)n_local * 784,
+                             cudaMemcpyHostToDevice, st));
+  SYSML_CUDA(cudaMemcpyAsync(h->lab_dev, labels_host, sizeof(int32_t) * (size_t)n_local,
+                             cudaMemcpyHostToDevice, st));
+  sysml_input xin{0, h->x_dev, {}};
+  SYSML_TRY(sysml_lenet_step(h, params, grads, &xin, h->lab_dev, n_local, n_global, lr, nccl_comm,
+                             h->loss_dev, stream));
+  SYSML_CUDA(cudaMemcpyAsync(loss_host, h->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
+  SYSML_CUDA(cudaStreamSynchronize(st));
+  return SYSML_OK;
+}
+
+sysml_status sysml_lenet_set_timing(sysml_lenet *h, int32_t enable) {
+  SYSML_CHECK_ARG(h, "NULL handle");
+  h->timing = enable != 0;
+  return SYSML_OK;
+}
+
+sysml_status sysml_lenet_get_timing(sysml_lenet *h, int32_t max_stages, int32_t *n_stages,
+                                    double *ms, int64_t *calls, const char **names) {
+  SYSML_CHECK_ARG(h, "NULL handle");
+  for (int s = 0; s < NSTAGES; ++s) {
+    for (auto &e : h->pending[s]) {
+      SYSML_CUDA(cudaEventSynchronize(e.second));
+      float t = 0.f;
+      SYSML_CUDA(cudaEventElapsedTime(&t, e.first, e.second));
+      h->ms[s] += t;
+      h->calls[s] += 1;
+      h->pool.push_back(e);
+    }
+    h->pending[s].clear();
+  }
+  if (n_stages) *n_stages = NSTAGES;
+  for (int s = 0; s < NSTAGES && s < max_stages; ++s) {
+    if (ms) ms[s] = h->ms[s];
+    if (calls) calls[s] = h->calls[s];
+    if (names) names[s] = STAGE_NAMES[s];
+  }
+  if (max_stages < 0) {  // reset
+    for (int s = 0; s < NSTAGES; ++s) { h->ms[s] = 0; h->calls[s] = 0; }
+  }
+  return SYSML_OK;
+}
+
+}  // extern "C"

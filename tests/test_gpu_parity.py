@@ -1,0 +1,312 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element,
+on identical seeded inputs (synth/).  Tolerances (BJ north_star):
+  fp32 CUDA-core kernels  max|gpu - ref| <= 1e-4 * max|ref|
+  TF32 tensor-core kernels max|gpu - ref| <= 5e-3 * max|ref|
+  pooling argmax / index outputs: bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-4, "tf32": 5e-3}
+
+
+@pytest.fixture(scope="module")
+def S():
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    import paper_1802_04647_b200 as s
+    s.lib()
+    return s
+
+
+def dev(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def assert_close(gpu, ref, tol, what=""):
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    assert gpu.shape == ref.shape, (gpu.shape, ref.shape)
+    scale = max(np.abs(ref).max(initial=0.0), 1e-30)
+    err = np.abs(gpu - ref).max(initial=0.0)
+    assert err <= tol * scale, f"{what}: max|err| {err:.3e} > {tol:g} * max|ref| {scale:.3e}"
+
+
+# N, C, H, W, K, R, S, stride, pad  -- several tiles + ragged tails, plus the BJ layer shapes
+CONV_SHAPES = [
+    (8, 1, 28, 28, 32, 5, 5, 1, 2),      # BJ cfg 1: LeNet conv1
+    (5, 32, 14, 14, 64, 5, 5, 1, 2),     # LeNet conv2
+    (3, 5, 11, 9, 7, 3, 3, 2, 1),        # ragged, stride 2
+    (2, 3, 10, 13, 70, 3, 2, 1, (1, 0)), # K > 64 tile, rectangular kernel
+    (2, 256, 14, 14, 256, 3, 3, 1, 1),   # BJ cfg 4 (i) 3x3 C=K=256 at N=2
+    (2, 1024, 14, 14, 256, 1, 1, 1, 0),  # BJ cfg 4 (ii) 1x1 1024->256 at N=2
+    (1, 2, 5, 5, 3, 5, 5, 1, 0),         # P = Q = 1
+]
+
+
+def _conv_case(shape, seed):
+    N, C, H, W, K, R, S_, st, pd = shape
+    pd = pd if isinstance(pd, tuple) else (pd, pd)
+    st = (st, st)
+    P = oracle.out_extent(H, pd[0], R, st[0])
+    Q = oracle.out_extent(W, pd[1], S_, st[1])
+    x, f, b, dy = synth.conv_problem_U(N, C, H, W, K, R, S_, P, Q, seed=(seed,))
+    return (N, C, H, W, K, R, S_, st, pd, P, Q), x, f, b, dy
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("shape", CONV_SHAPES)
+def test_conv_fwd_bwd_parity(S, shape, math):
+    (N, C, H, W, K, R, S_, st, pd, P, Q), x, f, b, dy = _conv_case(shape, 100)
+    d = S.conv_desc(N, C, H, W, K, R, S_, st, pd, math)
+    y = S.sysml_conv2d(dev(x), dev(f), d, bias=dev(b))
+    yref = oracle.conv2d_fwd(x, f, N, C, H, W, K, R, S_, st, pd, bias=b)
+    assert_close(host(y), yref, TOL[math], "fwd")
+    y0 = S.sysml_conv2d(dev(x), dev(f), d)
+    assert_close(host(y0), oracle.conv2d_fwd(x, f, N, C, H, W, K, R, S_, st, pd), TOL[math], "fwd nobias")
+    df, db = S.sysml_conv2d_bwd_filter(dev(x), dev(dy), d)
+    dfr, dbr = oracle.conv2d_bwd_filter(x, dy, N, C, H, W, K, R, S_, st, pd)
+    assert_close(host(df), dfr, TOL[math], "bwd_filter")
+    assert_close(host(db), dbr, 1e-4, "db")
+    dx = S.sysml_conv2d_bwd_data(dev(f), dev(dy), d)
+    assert_close(host(dx), oracle.conv2d_bwd_data(f, dy, N, C, H, W, K, R, S_, st, pd), TOL[math], "bwd_data")
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+def test_conv_dyadic_grid_exact(S, math):
+    # family G: every partial sum is exact in fp32 and TF32 -> bit-exact vs fp64
+    N, C, H, W, K, R, S_ = 2, 64, 14, 14, 64, 3, 3
+    x, f, b, dy = synth.conv_problem_G(N, C, H, W, K, R, S_, 14, 14)
+    d = S.conv_desc(N, C, H, W, K, R, S_, 1, 1, math)
+    y = host(S.sysml_conv2d(dev(x), dev(f), d, bias=dev(b)))
+    assert np.array_equal(y, oracle.conv2d_fwd(x, f, N, C, H, W, K, R, S_, (1, 1), (1, 1), bias=b))
+    df, db = S.sysml_conv2d_bwd_filter(dev(x), dev(dy), d)
+    dfr, dbr = oracle.conv2d_bwd_filter(x, dy, N, C, H, W, K, R, S_, (1, 1), (1, 1))
+    assert np.array_equal(host(df), dfr) and np.array_equal(host(db), dbr)
+    dx = host(S.sysml_conv2d_bwd_data(dev(f), dev(dy), d))
+    assert np.array_equal(dx, oracle.conv2d_bwd_data(f, dy, N, C, H, W, K, R, S_, (1, 1), (1, 1)))
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+def test_conv_determinism(S, math):
+    (N, C, H, W, K, R, S_, st, pd, P, Q), x, f, b, dy = _conv_case(CONV_SHAPES[1], 7)
+    d = S.conv_desc(N, C, H, W, K, R, S_, st, pd, math)
+    outs = []
+    for _ in range(2):
+        y = S.sysml_conv2d(dev(x), dev(f), d, bias=dev(b))
+        df, db = S.sysml_conv2d_bwd_filter(dev(x), dev(dy), d)
+        dx = S.sysml_conv2d_bwd_data(dev(f), dev(dy), d)
+        outs.append([host(t).tobytes() for t in (y, df, db, dx)])
+    assert outs[0] == outs[1]
+
+
+POOL_CASES = [
+    # N, C, H, W, R, S, stride, pad
+    (4, 32, 28, 28, 2, 2, 2, 0),
+    (3, 5, 7, 9, 3, 3, 2, 1),   # overlapping + padding
+    (2, 3, 6, 7, 2, 3, (1, 2), (1, 1)),
+    (2, 4, 7, 7, 2, 2, 2, 0),   # trailing row/col not covered
+]
+
+
+@pytest.mark.parametrize("relu", [True, False])
+@pytest.mark.parametrize("case", POOL_CASES)
+def test_relu_maxpool_and_bwd_bit_exact(S, case, relu):
+    N, C, H, W, R, S_, st, pd = case
+    st = st if isinstance(st, tuple) else (st, st)
+    pd = pd if isinstance(pd, tuple) else (pd, pd)
+    rng = synth.rng(200)
+    for x in (synth.uniform((N, C * H * W), seed=(201,)),
+              (rng.integers(-1, 2, size=(N, C * H * W)) / 2.0).astype(np.float32)):  # ties + zeros
+        d = S.pool_desc(N, C, H, W, R, S_, st, pd, relu)
+        out, arg = S.sysml_relu_maxpool(dev(x), d)
+        oref, aref = oracle.relu_maxpool(x, N, C, H, W, R, S_, st, pd, relu=relu)
+        assert np.array_equal(host(arg), aref)
+        assert np.array_equal(host(out).astype(np.float64) + 0.0, oref + 0.0)  # +-0 canonicalised
+        P, Q = d.P, d.Q
+        dout = synth.normal((N, C * P * Q), seed=(202,))
+        for mask in (None, out):
+            dx = S.sysml_maxpool_bwd(arg, dev(dout), d, out_mask=mask)
+            dxr = oracle.maxpool_bwd(aref, dout, N, C, H, W, P, Q,
+                                     out_mask=None if mask is None else oref)
+            if st[0] >= R and st[1] >= S_:
+                assert np.array_equal(host(dx).astype(np.float64), dxr)  # one term per element
+            else:
+                assert_close(host(dx), dxr, 1e-6, "maxpool_bwd overlap")
+
+
+def test_bias_add(S):
+    y = synth.uniform((3, 7 * 30), seed=(300,))
+    b = synth.uniform((7,), seed=(301,))
+    t = dev(y)
+    S.sysml_bias_add(t, dev(b), 3, 7, 30)
+    assert_close(host(t), oracle.bias_add(y, b, 3, 7, 30), 1e-7, "bias_add")
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+def test_fused_conv_bias_relu_maxpool_dyadic_bit_exact(S, math):
+    # LeNet conv2 block on the dyadic grid: conv exact -> argmax bit-exact (SURVEY §8(c) protocol 2)
+    N = 6
+    x = synth.dyadic((N, 32 * 14 * 14), 0, 4, 4, seed=(400,))
+    f = synth.dyadic((64, 800), -3, 3, 64, seed=(401,))
+    b = synth.dyadic((64,), -3, 3, 16, seed=(402,))
+    cd = S.conv_desc(N, 32, 14, 14, 64, 5, 5, 1, 2, math)
+    pd = S.pool_desc(N, 64, 14, 14, 2, 2, 2, 0, True)
+    out, arg = S.sysml_conv2d_bias_relu_maxpool(dev(x), dev(f), dev(b), cd, pd)
+    z = oracle.conv2d_fwd(x, f, N, 32, 14, 14, 64, 5, 5, (1, 1), (2, 2), bias=b)
+    oref, aref = oracle.relu_maxpool(z, N, 64, 14, 14, 2, 2, (2, 2), (0, 0), relu=True)
+    assert np.array_equal(host(arg), aref)
+    assert np.array_equal(host(out).astype(np.float64), oref)
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+def test_fused_conv_pool_continuous_valid_argmax(S, math):
+    N = 5
+    x = synth.mnist_like(N, seed=(410,))
+    f = synth.normal((32, 25), np.sqrt(2 / 25), seed=(411,))
+    b = synth.normal((32,), 0.1, seed=(412,))
+    cd = S.conv_desc(N, 1, 28, 28, 32, 5, 5, 1, 2, math)
+    pd = S.pool_desc(N, 32, 28, 28, 2, 2, 2, 0, True)
+    out, arg = S.sysml_conv2d_bias_relu_maxpool(dev(x), dev(f), dev(b), cd, pd)
+    z = oracle.conv2d_fwd(x, f, N, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2), bias=b)
+    oref, aref = oracle.relu_maxpool(z, N, 32, 28, 28, 2, 2, (2, 2), (0, 0), relu=True)
+    assert_close(host(out), oref, TOL[math], "pooled")
+    # valid argmax: the oracle's relu(z) at the GPU index is within tolerance of the oracle max
+    a = host(arg)
+    zr = np.maximum(z, 0.0)
+    picked = np.take_along_axis(zr, a.astype(np.int64), axis=1)
+    assert np.abs(picked - oref).max() <= TOL[math] * np.abs(oref).max()
+    if math == "fp32":
+        assert (a != aref).mean() < 1e-3
+
+
+# ---------------------------------------------------------------------------- CSR
+
+def _csr_dev(S, dense):
+    rp, ci, v = synth.to_csr(dense)
+    return S.CSR(dev(rp, torch.int32), dev(ci, torch.int32), dev(v), dense.shape[0], dense.shape[1]), (rp, ci, v)
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+def test_csr_conv_fwd_bwd_filter(S, math):
+    N = 12
+    x = synth.mnist_like(N, seed=(500,))
+    x[0] = 0.0                                    # empty row
+    x[1] = synth.uniform((784,), 0.01, 1.0, seed=(501,))  # fully dense row
+    x[2, [0, 27, 28 * 27, 783]] = [0.5, 0.25, 0.75, 1.0]   # border non-zeros
+    m, (rp, ci, v) = _csr_dev(S, x)
+    assert S.sysml_csr_check(m) == 0
+    xd = oracle.csr_densify(rp, ci, v, N, 784)
+    f = synth.normal((32, 25), np.sqrt(2 / 25), seed=(502,))
+    b = synth.normal((32,), 0.1, seed=(503,))
+    dy = synth.normal((N, 32 * 784), seed=(504,))
+    d = S.conv_desc(N, 1, 28, 28, 32, 5, 5, 1, 2, math)
+    y = S.sysml_conv2d(m, dev(f), d, bias=dev(b))
+    assert_close(host(y), oracle.conv2d_fwd(xd, f, N, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2), bias=b), 1e-4, "csr fwd")
+    df, db = S.sysml_conv2d_bwd_filter(m, dev(dy), d)
+    dfr, dbr = oracle.conv2d_bwd_filter(xd, dy, N, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2))
+    assert_close(host(df), dfr, 1e-4, "csr bwd_filter")
+    assert_close(host(db), dbr, 1e-4, "csr db")
+    pd = S.pool_desc(N, 32, 28, 28, 2, 2, 2, 0, True)
+    out, arg = S.sysml_conv2d_bias_relu_maxpool(m, dev(f), dev(b), d, pd)
+    z = oracle.conv2d_fwd(xd, f, N, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2), bias=b)
+    oref, aref = oracle.relu_maxpool(z, N, 32, 28, 28, 2, 2, (2, 2), (0, 0))
+    assert_close(host(out), oref, 1e-4, "csr fused")
+    assert (host(arg) != aref).mean() < 1e-3
+
+
+def test_csr_dyadic_fused_bit_exact(S):
+    N = 9
+    x = synth.mnist_like_dyadic(N, seed=(510,))
+    m, (rp, ci, v) = _csr_dev(S, x)
+    f = synth.dyadic((32, 25), -3, 3, 16, seed=(511,))
+    b = synth.dyadic((32,), -3, 3, 16, seed=(512,))
+    d = S.conv_desc(N, 1, 28, 28, 32, 5, 5, 1, 2, "tf32")
+    pd = S.pool_desc(N, 32, 28, 28, 2, 2, 2, 0, True)
+    out, arg = S.sysml_conv2d_bias_relu_maxpool(m, dev(f), dev(b), d, pd)
+    z = oracle.conv2d_fwd(x, f, N, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2), bias=b)
+    oref, aref = oracle.relu_maxpool(z, N, 32, 28, 28, 2, 2, (2, 2), (0, 0))
+    assert np.array_equal(host(arg), aref) and np.array_equal(host(out).astype(np.float64), oref)
+
+
+def test_csr_check_flags_violations(S):
+    rp = np.array([0, 2, 3], np.int32)
+    ci = np.array([3, 1, 0], np.int32)   # row 0 unsorted
+    v = np.array([1.0, 2.0, 0.0], np.float32)  # row 1 explicit zero
+    m = S.CSR(dev(rp, torch.int32), dev(ci, torch.int32), dev(v), 2, 4)
+    assert S.sysml_csr_check(m) == 2
+
+
+# ---------------------------------------------------------------------------- errors
+
+def test_shape_errors_name_shapes(S):
+    d = S.conv_desc(2, 1, 3, 3, 1, 5, 5, 1, 0, "fp32")
+    with pytest.raises(S.SysmlError) as e:
+        S.sysml_conv2d(torch.zeros(2, 9, device="cuda"), torch.zeros(1, 25, device="cuda"), d,
+                       out=torch.zeros(2, 1, device="cuda"))
+    assert e.value.status == 2 and "3x3" in str(e.value)
+    pd = S.pool_desc(1, 1, 4, 4, 2, 2, 2, (2, 0))
+    with pytest.raises(S.SysmlError) as e:
+        S.sysml_relu_maxpool(torch.zeros(1, 16, device="cuda"), pd, out=torch.zeros(1, 16, device="cuda"))
+    assert e.value.status == 2
+
+
+# ---------------------------------------------------------------------------- LeNet step
+
+def _lenet_case(n, dyadic=False, seed=600):
+    if dyadic:
+        x = synth.mnist_like_dyadic(n, seed=(seed,))
+        prm = synth.lenet_params(seed=(seed + 1,), dyadic_grid=True)
+    else:
+        x = synth.mnist_like(n, seed=(seed,))
+        prm = synth.lenet_params(seed=(seed + 1,)) + synth.normal((83466,), 0.01, seed=(seed + 2,))
+    y = synth.labels(n, seed=(seed + 3,))
+    return x, y, prm.astype(np.float32)
+
+
+@pytest.mark.parametrize("csr", [False, True])
+@pytest.mark.parametrize("math,dyadic", [("fp32", False), ("tf32", True), ("fp32", True)])
+def test_lenet_fwd_bwd_parity(S, math, dyadic, csr):
+    n = 10
+    x, y, prm = _lenet_case(n, dyadic)
+    g_ref, loss_ref = oracle.lenet_fwd_bwd(x, y, prm, n_global=32)
+    net = S.LeNet(16, math=math, csr=csr, max_nnz=n * 784)
+    xin = _csr_dev(S, x)[0] if csr else dev(x)
+    grads = torch.empty(83466, device="cuda")
+    loss = torch.empty(1, device="cuda")
+    net.fwd_bwd(dev(prm), xin, dev(y, torch.int32), 32, grads, loss)
+    g = host(grads)
+    offs = np.cumsum([0] + [int(np.prod(s)) for _, s in synth.LENET_PARAM_SHAPES])
+    for i, (name, _) in enumerate(synth.LENET_PARAM_SHAPES):
+        assert_close(g[offs[i]:offs[i + 1]], g_ref[offs[i]:offs[i + 1]], TOL[math], name)
+    assert abs(host(loss)[0] - loss_ref) <= 1e-5 * abs(loss_ref)
+
+
+def test_lenet_step_sgd_and_determinism(S):
+    n = 8
+    x, y, prm = _lenet_case(n, seed=700)
+    net = S.LeNet(n, math="tf32")
+    results = []
+    for _ in range(2):
+        p = dev(prm)
+        g = torch.empty(83466, device="cuda")
+        net.step(p, g, dev(x), dev(y, torch.int32), n, lr=0.01)
+        results.append((host(p).tobytes(), host(g)))
+    assert results[0][0] == results[1][0]
+    p_ref = oracle.sgd_update(prm, results[0][1], 0.01)
+    assert_close(np.frombuffer(results[0][0], np.float32), p_ref, 1e-7, "sgd")
+    # host-input end-to-end entry point gives the same parameters
+    p = dev(prm)
+    g = torch.empty(83466, device="cuda")
+    loss = net.step_host(p, g, torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory(), n)
+    assert host(p).tobytes() == results[0][0]
+    assert np.isfinite(loss)
