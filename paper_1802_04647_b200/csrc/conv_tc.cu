@@ -1,27 +1,943 @@
-// conv_tc.cu -- tcgen05 TF32 implicit-GEMM convolution (placeholder until bring-up).
+// conv_tc.cu -- tcgen05 TF32 implicit-GEMM convolution for sm_100a:
+//   K3 forward (+ fused bias / relu / max-pool epilogue), K6 bwd_data, K5 bwd_filter.
+//
+// The paper's GPU backend lowers conv2d to GEMMs via im2col (cuDNN);
+// here the lowering is implicit and "shifted-window": no im2col is built, not even
+// in shared memory.
+//
+// Frame.  Output positions are laid out in a stacked, padded frame: image n owns
+// Hs rows of Wf = W + pw columns (Hs >= H + ph), so output (n,p,q) is frame
+// position g = (n*Hs + p)*Wf + q, and the input value feeding it through tap (r,s)
+// sits at frame position g + (r*Wf + s) of the input frame (same geometry; zero
+// padding comes from frame rows/columns that decode outside the image: the right
+// padding of a row is the left padding of the next row, the bottom padding of an
+// image is the top padding of the next).  Every tap of the convolution is the SAME
+// matrix shifted by a constant number of rows.
+//
+// Forward GEMM.  D[m = position][n = out channel] += sum_{tap,c} A[m + d_tap][c] B[n][(tap,c)]
+//   A: a halo of the input frame for 8 channels, staged once per K-chunk in shared
+//      memory in the UMMA K-major no-swizzle layout [channel quad][position][4 ch]
+//      (16 B per position).  Tap t is the same bytes with the descriptor start
+//      advanced by 16*d_tap, so each staged element feeds R*S MMAs.  The 8-row
+//      group stride (SBO) is 16 B x 8 in "linear" M-tiles (128 consecutive
+//      positions) or one frame row (16 B x Wf) in "2-D" M-tiles (16 rows x 8
+//      columns), which puts each 2x2 pool window inside one warp (lanes l, l+1,
+//      l+8, l+9) so the fused max-pool is four shuffles.
+//   B: filters, repacked once into [filter tile][chunk][tap][quad][filter][4 ch] and
+//      streamed per chunk with one bulk async copy (cp.async.bulk, TMA 1-D).
+//   D: fp32 accumulators in TMEM; MT M-tiles share every B chunk (MT*NF <= 512 cols).
+//   Roles (256 threads, persistent, 1 CTA/SM): warps 0-3 stage A and issue the B
+//   copy; warp 4 lane 0 issues tcgen05.mma; warps 4-7 drain TMEM in the epilogue.
+// bwd_data = the forward kernel on dY with the filter bank transposed and
+// rotated 180 degrees, padding R-1-ph (stride 1).
+//
+// bwd_filter GEMM.  For tap (r,s): D_rs[k][c] = sum_g dY[k][g] X[c][g + d_rs]
+//   over output frame positions g.  M = filters: A = dY chunk, K-major [pos quad]
+//   [row][4 pos]; when K < 128 the 128 TMEM lanes hold 128/K copies of the filters,
+//   copy j being dY shifted by j*Wf, so one MMA yields taps (r,s),(r+1,s),... (the
+//   shift by a frame row moves the tap down one row).  N = channels: B = the X halo
+//   in the MN-major layout [channel quad][position][4 ch], the tap shift again being
+//   a descriptor offset.  One accumulator per tap group; the position range is split
+//   over CTAs and the partials are summed in a fixed order (deterministic).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
 
 namespace sysml {
-bool tc_fwd_supported(const ConvArgs &, const PoolArgs *) { return false; }
-size_t tc_fwd_ws(const ConvArgs &) { return 0; }
-sysml_status tc_conv_fwd(const ConvArgs &, const float *, const float *, const float *, float *,
-                         const PoolArgs *, float *, int32_t *, void *, cudaStream_t) {
-  set_error("tcgen05 forward kernel not available");
-  return SYSML_ERR_UNSUPPORTED;
+
+namespace {
+
+constexpr int TC_THREADS = 256;
+constexpr int SMEM_BUDGET = 225 * 1024;
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
 }
-bool tc_bwd_data_supported(const ConvArgs &) { return false; }
-size_t tc_bwd_data_ws(const ConvArgs &) { return 0; }
-sysml_status tc_conv_bwd_data(const ConvArgs &, const float *, const float *, float *, void *,
-                              cudaStream_t) {
-  set_error("tcgen05 bwd_data kernel not available");
-  return SYSML_ERR_UNSUPPORTED;
+
+// =====================================================================================
+// Forward kernel
+// =====================================================================================
+struct TcFwdParams {
+  const float *x;
+  const float *fp;    // packed filters
+  const float *bias;  // may be null
+  float *y;           // plain output (N x K*P*Q) or null
+  float *pout;        // pooled output or null
+  int32_t *parg;      // pooled argmax or null
+  int N, C, H, W, K, R, S, ph, pw, P, Q;
+  int Wf, Hs, Lf;
+  int64_t G;
+  int NFpad, nft, nchunk;
+  int MT, HALO, nstage;
+  int tile2d;          // 0: linear 128-position M-tiles; 1: 16x8 2-D M-tiles
+  int CT, BB;          // 2-D: column tiles per band, bands per CTA tile (MT = CT*BB)
+  int64_t cta_pos;     // positions advanced per CTA tile (linear: MT*128; 2-D: BB*16*Wf)
+  int pool, PR, PS, Pp, Qp;
+  uint32_t a_bytes, b_bytes, stage_bytes, a_sbo;
+  int64_t ntiles;
+  uint32_t tmem_cols;
+};
+
+struct TcPlan {
+  TcFwdParams p;
+  size_t smem;
+  size_t fp_bytes;
+  bool ok;
+};
+
+__device__ __forceinline__ int tile_origin(const TcFwdParams &p, int i) {
+  // position offset (relative to the CTA tile origin) of M-tile i
+  if (!p.tile2d) return i * 128;
+  const int bb = i / p.CT, ct = i - bb * p.CT;
+  return bb * 16 * p.Wf + ct * 8;
 }
-bool tc_bwd_filter_supported(const ConvArgs &) { return false; }
-size_t tc_bwd_filter_ws(const ConvArgs &) { return 0; }
-sysml_status tc_conv_bwd_filter(const ConvArgs &, const float *, const float *, float *, float *,
-                                void *, cudaStream_t) {
-  set_error("tcgen05 bwd_filter kernel not available");
-  return SYSML_ERR_UNSUPPORTED;
+
+__global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_fwd_kernel(const TcFwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t *stage_base = smem;
+  int *src_off = reinterpret_cast<int *>(smem + (size_t)p.nstage * p.stage_bytes);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(
+      (reinterpret_cast<uintptr_t>(src_off + p.HALO) + 15) & ~(uintptr_t)15);
+  uint64_t *full = bars;
+  uint64_t *empty = bars + p.nstage;
+  uint64_t *accf = bars + 2 * p.nstage;
+  uint64_t *acce = accf + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.nstage; ++s) {
+      ptx::mbar_init(full + s, 4 + 1);  // 4 producer warps + the expect_tx arrival
+      ptx::mbar_init(empty + s, 1);     // tcgen05.commit
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::mbar_init(acce, 4);            // 4 epilogue warps
+    ptx::fence_mbar_init();
+  }
+  if (warp == 4) ptx::tmem_alloc(tmem_slot, p.tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int HW = p.H * p.W, RS = p.R * p.S;
+
+  if (warp < 4) {
+    // ================= producers: A halo (ld.global -> st.shared) + B chunk (bulk copy)
+    const int tid = threadIdx.x;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+      const int ft = (int)(tile % p.nft);
+      const int64_t g0 = (tile / p.nft) * p.cta_pos;
+      ptx::named_bar_sync(1, 128);
+      for (int pos = tid; pos < p.HALO; pos += 128) {
+        const int64_t gi = g0 + pos;
+        int off = -1;
+        if (gi < p.G) {
+          const int n = (int)(gi / p.Lf);
+          const int rem = (int)(gi - (int64_t)n * p.Lf);
+          const int hh = rem / p.Wf, ww = rem - hh * p.Wf;
+          const int h = hh - p.ph, w = ww - p.pw;
+          if (h >= 0 && h < p.H && w >= 0 && w < p.W) off = n * p.C * HW + h * p.W + w;
+        }
+        src_off[pos] = off;
+      }
+      ptx::named_bar_sync(1, 128);
+      for (int ch = 0; ch < p.nchunk; ++ch) {
+        ptx::mbar_wait(empty + stage, phase ^ 1);
+        uint8_t *A = stage_base + (size_t)stage * p.stage_bytes;
+        uint8_t *B = A + p.a_bytes;
+        if (tid == 0) {
+          ptx::mbar_arrive_expect_tx(full + stage, p.b_bytes);
+          ptx::bulk_g2s(B, p.fp + ((size_t)ft * p.nchunk + ch) * (p.b_bytes / 4), p.b_bytes,
+                        full + stage);
+        }
+        const int c0 = ch * 8;
+        const uint32_t a0 = ptx::smem_u32(A);
+        const uint32_t a1 = a0 + (uint32_t)p.HALO * 16;
+        const int nc = min(8, p.C - c0);
+        const float *xc = p.x + (size_t)c0 * HW;
+        // 4 positions per iteration: all loads in flight before the stores
+        for (int pb = tid; pb < p.HALO; pb += 4 * 128) {
+          float v[4][8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int pos = pb + u * 128;
+            const int off = pos < p.HALO ? src_off[pos] : -1;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              v[u][j] = (off >= 0 && j < nc) ? __ldg(xc + off + (size_t)j * HW) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int pos = pb + u * 128;
+            if (pos < p.HALO) {
+              st_shared_v4(a0 + pos * 16, v[u][0], v[u][1], v[u][2], v[u][3]);
+              st_shared_v4(a1 + pos * 16, v[u][4], v[u][5], v[u][6], v[u][7]);
+            }
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(full + stage);
+        if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // ================= MMA issuer (warp 4 lane 0) + epilogue (warps 4-7)
+    const int qd = warp - 4;
+    const uint32_t idesc = ptx::make_idesc_tf32(128, p.NFpad);
+    int stage = 0;
+    uint32_t phase = 0, tphase = 0;
+    const int PQ = p.P * p.Q;
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+      const int ft = (int)(tile % p.nft);
+      const int64_t g0 = (tile / p.nft) * p.cta_pos;
+      if (warp == 4) {
+        // whole warp runs the issue loop (warp-uniform descriptors stay in uniform
+        // registers); one elected lane issues each tcgen05.mma / commit
+        ptx::mbar_wait(acce, tphase ^ 1);
+        ptx::tc_fence_after();
+        // M-tile origins: nested (outer: bands / linear tiles, inner: column tiles)
+        const int n_outer = p.tile2d ? p.BB : p.MT;
+        const int n_inner = p.tile2d ? p.CT : 1;
+        const uint32_t step_outer = p.tile2d ? (uint32_t)(16 * p.Wf) : 128u;
+        const uint32_t step_inner = 8u;
+        const uint32_t tmem_step = (uint32_t)p.NFpad;
+        for (int ch = 0; ch < p.nchunk; ++ch) {
+          ptx::mbar_wait(full + stage, phase);
+          ptx::tc_fence_after();
+          const uint32_t A = ptx::smem_u32(stage_base + (size_t)stage * p.stage_bytes);
+          const uint32_t B = A + p.a_bytes;
+          const uint64_t adesc0 = ptx::make_desc(A, p.HALO * 16, p.a_sbo);
+          uint64_t bdesc = ptx::make_desc(B, p.NFpad * 16, 128);
+          uint32_t acc = ch != 0 ? 1u : 0u;
+          uint32_t dt = 0;  // tap shift in positions (= 16-B descriptor units)
+          for (int r = 0; r < p.R; ++r) {
+            for (int s_ = 0; s_ < p.S; ++s_) {
+              uint32_t org_o = dt, tm = tmem_base;
+              for (int io = 0; io < n_outer; ++io) {
+                uint32_t org = org_o;
+                for (int ii = 0; ii < n_inner; ++ii) {
+                  if (ptx::elect_one()) ptx::mma_tf32(tm, adesc0 + org, bdesc, idesc, acc);
+                  __syncwarp();
+                  org += step_inner;
+                  tm += tmem_step;
+                }
+                org_o += step_outer;
+              }
+              acc = 1u;
+              bdesc += (uint64_t)(2 * p.NFpad);  // next tap: 2 quads x NFpad x 16 B
+              dt += 1;
+            }
+            dt += (uint32_t)(p.Wf - p.S);
+          }
+          if (ptx::elect_one()) ptx::mma_commit(empty + stage);
+          __syncwarp();
+          if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+        }
+        if (ptx::elect_one()) ptx::mma_commit(accf);
+        __syncwarp();
+      }
+      __syncwarp();
+      ptx::mbar_wait(accf, tphase);
+      __syncwarp();
+      ptx::tc_fence_after();
+      for (int i = 0; i < p.MT; ++i) {
+        const uint32_t trow = tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(i * p.NFpad);
+        if (!p.pool) {
+          // linear or 2-D M-tile: lane -> position
+          int64_t g;
+          if (!p.tile2d) g = g0 + i * 128 + qd * 32 + lane;
+          else g = g0 + tile_origin(p, i) + (qd * 4 + (lane >> 3)) * p.Wf + (lane & 7);
+          bool valid = g < p.G;
+          int64_t ybase = 0;
+          if (valid) {
+            const int n = (int)(g / p.Lf);
+            const int rem = (int)(g - (int64_t)n * p.Lf);
+            const int hh = rem / p.Wf, q = rem - hh * p.Wf;
+            valid = hh < p.P && q < p.Q;
+            ybase = (int64_t)n * p.K * PQ + (int64_t)hh * p.Q + q;
+          }
+          for (int c16 = 0; c16 < p.NFpad / 16; ++c16) {
+            float v[16];
+            ptx::tmem_ld16(trow + c16 * 16, v);
+            if (valid) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int k = ft * p.NFpad + c16 * 16 + j;
+                if (k < p.K) p.y[ybase + (int64_t)k * PQ] = v[j] + (p.bias ? __ldg(p.bias + k) : 0.f);
+              }
+            }
+          }
+        } else {
+          // 2-D M-tile (16 rows x 8 cols): lane (rl = qd*4 + lane/8, cl = lane%8)
+          const int bb = i / p.CT, ct = i - bb * p.CT;
+          const int rl = qd * 4 + (lane >> 3), cl = lane & 7;
+          const int64_t grow = g0 / p.Wf + bb * 16 + rl;  // global frame row
+          const int col = ct * 8 + cl;
+          const int n = (int)(grow / p.Hs);
+          const int hh = (int)(grow - (int64_t)n * p.Hs);
+          const bool leader = (rl % p.PR) == 0 && (cl % p.PS) == 0;
+          const int pp = hh / p.PR, pc = col / p.PS;
+          const bool store = leader && n < p.N && pp < p.Pp && pc < p.Qp;
+          const int PpQp = p.Pp * p.Qp;
+          const int64_t obase = (int64_t)n * p.K * PpQp + (int64_t)pp * p.Qp + pc;
+          for (int c16 = 0; c16 < p.NFpad / 16; ++c16) {
+            float v[16];
+            ptx::tmem_ld16(trow + c16 * 16, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int k = ft * p.NFpad + c16 * 16 + j;
+              const float bk = (p.bias && k < p.K) ? __ldg(p.bias + k) : 0.f;
+              float z = v[j] + bk;
+              z = z > 0.f ? z : 0.f;  // relu, +0.0 for non-positive (reading R7)
+              int idx = (k * p.P + hh) * p.Q + col;
+              // first-occurrence max over the window (r outer, s inner; strict '>')
+              for (int d = 1; d < p.PS; d <<= 1) {
+                const float z2 = __shfl_down_sync(0xffffffffu, z, d);
+                const int i2 = __shfl_down_sync(0xffffffffu, idx, d);
+                if (z2 > z) { z = z2; idx = i2; }
+              }
+              for (int d = 8; d < 8 * p.PR; d <<= 1) {
+                const float z2 = __shfl_down_sync(0xffffffffu, z, d);
+                const int i2 = __shfl_down_sync(0xffffffffu, idx, d);
+                if (z2 > z) { z = z2; idx = i2; }
+              }
+              if (store && k < p.K) {
+                p.pout[obase + (int64_t)k * PpQp] = z;
+                if (p.parg) p.parg[obase + (int64_t)k * PpQp] = idx;
+              }
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(acce);
+      tphase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, p.tmem_cols);
+  }
 }
+
+// Repack filters into [ftile][chunk][tap][quad][NFpad][4] (zero padded).
+//  flip == 0: packed(k, c, t) = F[k][c][t]        (F is Kout x (Cin*RS))
+//  flip == 1: packed(k, c, t) = F[c][k][RS-1-t]   (F is Cin x (Kout*RS): bwd_data)
+__global__ void tc_pack_filters_kernel(const float *__restrict__ f, float *__restrict__ fp, int Kout,
+                                       int Cin, int RS, int NFpad, int nft, int nchunk, int flip) {
+  const int64_t total = (int64_t)nft * nchunk * RS * 2 * NFpad * 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int e = (int)(t % 4); t /= 4;
+    const int j = (int)(t % NFpad); t /= NFpad;
+    const int g = (int)(t % 2); t /= 2;
+    const int tap = (int)(t % RS); t /= RS;
+    const int ch = (int)(t % nchunk); t /= nchunk;
+    const int f_ = (int)t;
+    const int k = f_ * NFpad + j, c = ch * 8 + g * 4 + e;
+    float v = 0.f;
+    if (k < Kout && c < Cin)
+      v = flip ? f[((int64_t)c * Kout + k) * RS + (RS - 1 - tap)] : f[((int64_t)k * Cin + c) * RS + tap];
+    fp[i] = v;
+  }
+}
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+// Plan the forward kernel for a stride-1 conv: input (N,C,H,W), K output channels.
+TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
+                const PoolArgs *pool) {
+  TcPlan pl{};
+  TcFwdParams &p = pl.p;
+  p.N = N; p.C = C; p.H = H; p.W = W; p.K = K; p.R = R; p.S = S; p.ph = ph; p.pw = pw;
+  p.P = H + 2 * ph - R + 1;
+  p.Q = W + 2 * pw - S + 1;
+  pl.ok = false;
+  if (p.P < 1 || p.Q < 1) return pl;
+  p.Wf = W + pw;
+  p.pool = pool ? 1 : 0;
+  p.PR = pool ? pool->R : 1;
+  p.PS = pool ? pool->S : 1;
+  if (pool) {
+    // 2-D tiles: window rows must tile the 16-row tile and columns the 8-column tile
+    if (!(p.PR == 1 || p.PR == 2 || p.PR == 4 || p.PR == 8 || p.PR == 16)) return pl;
+    if (!(p.PS == 1 || p.PS == 2 || p.PS == 4 || p.PS == 8)) return pl;
+    p.Pp = pool->P;
+    p.Qp = pool->Q;
+  }
+  p.Hs = round_up(H + ph, p.PR);
+  p.Lf = p.Hs * p.Wf;
+  p.G = (int64_t)N * p.Lf;
+  if (p.G + 4096 >= (1ll << 31)) return pl;
+  p.tile2d = pool ? 1 : 0;
+  if (K <= 256) {
+    p.NFpad = std::max(16, round_up(K, 16));
+    p.nft = 1;
+  } else {
+    p.NFpad = 256;
+    p.nft = (K + 255) / 256;
+  }
+  p.nchunk = (C + 7) / 8;
+  const int RS = R * S;
+  p.b_bytes = (uint32_t)(RS * 2 * p.NFpad * 16);
+  const int nsm = sm_count();
+  const int64_t rows_total = (int64_t)N * p.Hs;
+  int mt_cap = std::min(16, 512 / p.NFpad);
+  p.CT = (p.Q + 7) / 8;
+  if (p.tile2d && p.CT > mt_cap) return pl;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    int mt = mt_cap;
+    for (; mt >= 1; --mt) {
+      int bb = 1, halo;
+      int64_t cta_pos, ntiles;
+      if (p.tile2d) {
+        bb = mt / p.CT;
+        if (bb < 1) continue;
+        cta_pos = (int64_t)bb * 16 * p.Wf;
+        halo = (bb - 1) * 16 * p.Wf + (p.CT - 1) * 8 + 15 * p.Wf + 7 + (R - 1) * p.Wf + (S - 1) + 1;
+        ntiles = ceil_div(rows_total, (int64_t)bb * 16) * p.nft;
+      } else {
+        cta_pos = (int64_t)mt * 128;
+        halo = mt * 128 + (R - 1) * p.Wf + (S - 1);
+        ntiles = ceil_div(p.G, cta_pos) * p.nft;
+      }
+      if (attempt == 0 && mt > 1 && ntiles < nsm) continue;  // keep the SMs busy first
+      const uint32_t a_bytes = (uint32_t)(2 * halo * 16);
+      const uint32_t stage = a_bytes + p.b_bytes;
+      const size_t fixed = (size_t)halo * 4 + 16 + 8 * 20 + 16;
+      const int nst = (int)((SMEM_BUDGET - (int64_t)fixed) / (int64_t)stage);
+      if (nst < 2) continue;
+      p.MT = p.tile2d ? bb * p.CT : mt;
+      p.BB = bb;
+      p.HALO = halo;
+      p.cta_pos = cta_pos;
+      p.ntiles = ntiles;
+      p.a_bytes = a_bytes;
+      p.stage_bytes = stage;
+      p.nstage = std::min(nst, 8);
+      p.a_sbo = p.tile2d ? (uint32_t)(p.Wf * 16) : 128u;
+      pl.smem = (size_t)p.nstage * stage + fixed + 8 * (2 * p.nstage + 2);
+      pl.ok = true;
+      break;
+    }
+    if (pl.ok) break;
+  }
+  if (!pl.ok) return pl;
+  if (p.tile2d && (uint32_t)p.Wf * 16 >= (1u << 18)) { pl.ok = false; return pl; }
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(p.MT * p.NFpad)) cols <<= 1;
+  p.tmem_cols = cols;
+  pl.fp_bytes = align_up((size_t)p.nft * p.nchunk * RS * 8 * p.NFpad * sizeof(float), 256);
+  return pl;
+}
+
+template <class K>
+sysml_status set_smem_attr(K kernel, size_t bytes, int &cache) {
+  if ((int)bytes > cache) {
+    SYSML_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cache = (int)bytes;
+  }
+  return SYSML_OK;
+}
+
+sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f_cin,
+                     const float *bias, float *y, float *pout, int32_t *parg, void *ws,
+                     cudaStream_t st) {
+  TcFwdParams p = pl.p;
+  float *fp = reinterpret_cast<float *>(ws);
+  {
+    const int64_t total = (int64_t)p.nft * p.nchunk * p.R * p.S * 2 * p.NFpad * 4;
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * sm_count());
+    tc_pack_filters_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, f_cin, p.R * p.S, p.NFpad, p.nft,
+                                                   p.nchunk, flip);
+    SYSML_LAUNCH_CHECK();
+  }
+  p.x = x;
+  p.fp = fp;
+  p.bias = bias;
+  p.y = y;
+  p.pout = pout;
+  p.parg = parg;
+  static int attr = 0;
+  SYSML_TRY(set_smem_attr(tc_conv_fwd_kernel, pl.smem, attr));
+  const int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
+  tc_conv_fwd_kernel<<<grid, TC_THREADS, pl.smem, st>>>(p);
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
+}
+
+bool pool_fusable(const PoolArgs *pool) {
+  return !pool || (pool->sh == pool->R && pool->sw == pool->S && pool->ph == 0 && pool->pw == 0);
+}
+
+// =====================================================================================
+// bwd_filter (weight gradient) kernel
+// =====================================================================================
+// Frame width Wf4 = round_up(W + pw, 4), so a tap shift d = rg*copies*Wf4 + s splits
+// into a whole number of 4-position quads (a = d >> 2) plus a phase (s mod 4): the X
+// halo is staged K-major ([pos quad][channel][4 pos]) once per phase (X shifted by
+// phi = 0..nph-1 positions) and every tap is a descriptor offset into its phase copy.
+struct TcWgParams {
+  const float *x, *dy;
+  float *part;    // [split][wt][tgc][128][NC]
+  float *dbpart;  // [split][K] (or null)
+  int N, C, H, W, K, R, S, ph, pw, P, Q;
+  int Wf, Hs, Lf;
+  int64_t G, Gext;
+  int Kc, copies, nkt;   // filters per copy, copies (128/Kc), filter tiles of 128
+  int NC, nct;           // channels per tile (mult of 16), channel tiles
+  int RG, TGt, TGc, ntg; // tap row groups, tap groups total / per CTA, tap-group tiles
+  int nwt;               // work types = nkt*nct*ntg
+  int splits;
+  int64_t pos_per_split;
+  int KC;                // positions per stage (multiple of 8)
+  int nph, HBq, XT;      // phases, B quads per phase, X offset table length
+  int dmax;              // max tap shift
+  int YT;                // dY offset table length = KC + (copies-1)*Wf
+  int nstage;
+  uint32_t a_bytes, b_bytes, phase_bytes, stage_bytes;
+  uint32_t tmem_cols;
+};
+
+struct TcWgPlan {
+  TcWgParams p;
+  size_t smem, part_bytes, dbpart_bytes;
+  bool ok;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_wgrad_kernel(const TcWgParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t *stage_base = smem;
+  int *ytab = reinterpret_cast<int *>(smem + (size_t)p.nstage * p.stage_bytes);  // [nstage][YT]
+  int *xtab = ytab + p.nstage * p.YT;                                            // [nstage][XT]
+  float *dbs = reinterpret_cast<float *>(xtab + p.nstage * p.XT);                 // [128]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(
+      (reinterpret_cast<uintptr_t>(dbs + 128) + 15) & ~(uintptr_t)15);
+  uint64_t *full = bars;
+  uint64_t *empty = bars + p.nstage;
+  uint64_t *accf = bars + 2 * p.nstage;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // work decomposition: blockIdx.x = split * nwt + wt; wt = (kt * nct + ct) * ntg + tgt
+  const int wt = blockIdx.x % p.nwt;
+  const int split = blockIdx.x / p.nwt;
+  const int tgt = wt % p.ntg;
+  const int ct = (wt / p.ntg) % p.nct;
+  const int kt = wt / (p.ntg * p.nct);
+  const int tg0 = tgt * p.TGc;
+  const int tgn = min(p.TGc, p.TGt - tg0);
+  const int64_t gs = (int64_t)split * p.pos_per_split;
+  const int64_t ge = min(p.Gext, gs + p.pos_per_split);
+  const int64_t span = ge > gs ? ge - gs : 0;
+  const int nchunks = (int)((span + p.KC - 1) / p.KC);
+  const bool do_db = p.dbpart != nullptr && ct == 0 && tgt == 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.nstage; ++s) {
+      ptx::mbar_init(full + s, 4);
+      ptx::mbar_init(empty + s, 1);
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 4) ptx::tmem_alloc(tmem_slot, p.tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int HW = p.H * p.W, PQ = p.P * p.Q;
+
+  if (warp < 4) {
+    // ================= producers
+    const int tid = threadIdx.x;
+    // A row owned by this thread: copy j = tid / Kc, filter k = kt*128 + tid % Kc
+    const int arow = tid;
+    const int aj = arow / p.Kc;
+    const int ak = kt * 128 + (arow - aj * p.Kc);
+    const bool arow_ok = aj < p.copies && ak < p.K;
+    float db_acc = 0.f;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int64_t u0 = gs + (int64_t)ch * p.KC;
+      ptx::mbar_wait(empty + stage, phase ^ 1);
+      int *yt = ytab + stage * p.YT;
+      int *xt = xtab + stage * p.XT;
+      // dY offsets for output-frame positions u0 - (copies-1)*Wf + e, e < YT
+      for (int e = tid; e < p.YT; e += 128) {
+        const int64_t g = u0 - (int64_t)(p.copies - 1) * p.Wf + e;
+        int off = -1;
+        if (g >= 0 && g < p.G) {
+          const int n = (int)(g / p.Lf);
+          const int rem = (int)(g - (int64_t)n * p.Lf);
+          const int hh = rem / p.Wf, q = rem - hh * p.Wf;
+          if (hh < p.P && q < p.Q) off = n * p.K * PQ + hh * p.Q + q;
+        }
+        yt[e] = off;
+      }
+      // X offsets for input-frame positions u0 + e, e < XT
+      for (int e = tid; e < p.XT; e += 128) {
+        const int64_t gi = u0 + e;
+        int off = -1;
+        if (gi < p.G) {
+          const int n = (int)(gi / p.Lf);
+          const int rem = (int)(gi - (int64_t)n * p.Lf);
+          const int hh = rem / p.Wf, ww = rem - hh * p.Wf;
+          const int h = hh - p.ph, w = ww - p.pw;
+          if (h >= 0 && h < p.H && w >= 0 && w < p.W) off = n * p.C * HW + h * p.W + w;
+        }
+        xt[e] = off;
+      }
+      ptx::named_bar_sync(1, 128);
+      const uint32_t A = ptx::smem_u32(stage_base + (size_t)stage * p.stage_bytes);
+      const uint32_t B = A + p.a_bytes;
+      // ---- A: row = (copy j, filter k); K-major [pos quad][128 rows][4 pos]
+      {
+        const int shift = (p.copies - 1 - aj) * p.Wf;  // yt index of position u0 + u - j*Wf
+        const float *dyk = p.dy + (size_t)(arow_ok ? ak : 0) * PQ;
+        for (int qb = 0; qb < p.KC / 4; qb += 4) {
+          float v[4][4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int u = (qb + a) * 4 + e;
+              // positions at or past this CTA's range end belong to the next CTA
+              const int off = (arow_ok && qb + a < p.KC / 4 && u0 + u < ge) ? yt[shift + u] : -1;
+              v[a][e] = off >= 0 ? __ldg(dyk + off) : 0.f;
+            }
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            if (qb + a < p.KC / 4) {
+              st_shared_v4(A + (uint32_t)(((qb + a) * 128 + arow) * 16), v[a][0], v[a][1], v[a][2], v[a][3]);
+              if (do_db && aj == 0) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) db_acc += v[a][e];
+              }
+            }
+          }
+        }
+      }
+      // ---- B: X halo, K-major per phase: [phase][pos quad][NC][4 pos]
+      {
+        const int c0 = ct * p.NC;
+        const int ntask = p.NC * p.HBq;
+        for (int t0 = tid; t0 < ntask; t0 += 2 * 128) {
+          float v[2][7];
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            const int t = t0 + a * 128;
+            const int cq = t / p.HBq;  // channel (within tile)
+            const int qd_ = t - cq * p.HBq;
+            const int c = c0 + cq;
+            const bool ok = t < ntask && c < p.C;
+            const float *xc = p.x + (size_t)(ok ? c : 0) * HW;
+#pragma unroll
+            for (int e = 0; e < 7; ++e) {
+              const int off = (ok && e < 3 + p.nph) ? xt[qd_ * 4 + e] : -1;
+              v[a][e] = off >= 0 ? __ldg(xc + off) : 0.f;
+            }
+          }
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            const int t = t0 + a * 128;
+            if (t < ntask) {
+              const int cq = t / p.HBq;
+              const int qd_ = t - cq * p.HBq;
+              const uint32_t dst = B + (uint32_t)((qd_ * p.NC + cq) * 16);
+#pragma unroll
+              for (int f = 0; f < 4; ++f)
+                if (f < p.nph)
+                  st_shared_v4(dst + f * p.phase_bytes, v[a][f], v[a][f + 1], v[a][f + 2], v[a][f + 3]);
+            }
+          }
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 128);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(full + stage);
+      if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+    }
+    if (do_db) {
+      // fixed-order reduction: thread arow (copy 0 rows only) owns filter ak
+      dbs[arow] = db_acc;
+      ptx::named_bar_sync(1, 128);
+      if (tid < p.Kc && ak < p.K) p.dbpart[(size_t)split * p.K + ak] = dbs[tid];
+    }
+  } else {
+    const int qd = warp - 4;
+    if (warp == 4) {
+      const uint32_t idesc = ptx::make_idesc_tf32(128, p.NC);  // A, B K-major
+      int stage = 0;
+      uint32_t phase = 0;
+      // tap groups handled by this CTA, in (rg, s) order from tg0
+      const int rg0 = tg0 / p.S, s0 = tg0 - rg0 * p.S;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        ptx::mbar_wait(full + stage, phase);
+        ptx::tc_fence_after();
+        const uint32_t A = ptx::smem_u32(stage_base + (size_t)stage * p.stage_bytes);
+        const uint32_t B = A + p.a_bytes;
+        const uint64_t adesc0 = ptx::make_desc(A, 128 * 16, 128);
+        const uint64_t bdesc0 = ptx::make_desc(B, (uint32_t)p.NC * 16, 128);
+        for (int kk = 0; kk < p.KC / 8; ++kk) {
+          const uint64_t adesc = adesc0 + (uint64_t)(kk * 2 * 128);  // 2 pos quads x 2048 B
+          int rg = rg0, s_ = s0;
+          uint32_t tm = tmem_base;
+          const uint32_t acc = (ch | kk) != 0 ? 1u : 0u;
+          for (int tl = 0; tl < tgn; ++tl) {
+            const uint32_t d = (uint32_t)(rg * p.copies * p.Wf + s_);
+            const uint64_t bdesc = bdesc0 + (uint64_t)((d & 3u) * (p.phase_bytes >> 4)) +
+                                   (uint64_t)((2 * kk + (int)(d >> 2)) * p.NC);
+            if (ptx::elect_one()) ptx::mma_tf32(tm, adesc, bdesc, idesc, acc);
+            __syncwarp();
+            tm += (uint32_t)p.NC;
+            if (++s_ == p.S) { s_ = 0; ++rg; }
+          }
+        }
+        if (ptx::elect_one()) ptx::mma_commit(empty + stage);
+        __syncwarp();
+        if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+      }
+      if (ptx::elect_one()) ptx::mma_commit(accf);
+      __syncwarp();
+    }
+    ptx::mbar_wait(accf, 0);
+    __syncwarp();
+    ptx::tc_fence_after();
+    // epilogue: partial[split][wt][tl][row][NC]; zero if no chunk ran
+    const int row = qd * 32 + lane;
+    float *dst = p.part + (((size_t)split * p.nwt + wt) * p.TGc) * 128 * p.NC;
+    for (int tl = 0; tl < p.TGc; ++tl) {
+      for (int c16 = 0; c16 < p.NC / 16; ++c16) {
+        float v[16];
+        if (tl < tgn && nchunks > 0) {
+          ptx::tmem_ld16(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(tl * p.NC + c16 * 16), v);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        }
+        float4 *o = reinterpret_cast<float4 *>(dst + ((size_t)tl * 128 + row) * p.NC + c16 * 16);
+        o[0] = make_float4(v[0], v[1], v[2], v[3]);
+        o[1] = make_float4(v[4], v[5], v[6], v[7]);
+        o[2] = make_float4(v[8], v[9], v[10], v[11]);
+        o[3] = make_float4(v[12], v[13], v[14], v[15]);
+      }
+    }
+    ptx::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+// dF[k][c][r][s] = sum_{split} part[split][wt(k,c,r,s)][tl][row][col]  (split ascending)
+__global__ void tc_wgrad_reduce_kernel(const TcWgParams p, float *__restrict__ df,
+                                       float *__restrict__ db) {
+  const int RS = p.R * p.S;
+  const int64_t total = (int64_t)p.K * p.C * RS;
+  const size_t split_stride = (size_t)p.nwt * p.TGc * 128 * p.NC;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i / ((int64_t)p.C * RS));
+    const int rem = (int)(i - (int64_t)k * p.C * RS);
+    const int c = rem / RS, t = rem - c * RS, r = t / p.S, s = t - r * p.S;
+    const int kt = k / 128, kk = k - kt * 128;
+    const int ct = c / p.NC, col = c - ct * p.NC;
+    const int rg = r / p.copies, j = r - rg * p.copies;
+    const int tg = rg * p.S + s;
+    const int tgt = tg / p.TGc, tl = tg - tgt * p.TGc;
+    const int wt = (kt * p.nct + ct) * p.ntg + tgt;
+    const int row = j * p.Kc + kk;
+    const size_t off = (((size_t)wt * p.TGc + tl) * 128 + row) * p.NC + col;
+    float acc = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp) acc += p.part[(size_t)sp * split_stride + off];
+    df[i] = acc;
+  }
+  if (db) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < p.K;
+         k += (int64_t)gridDim.x * blockDim.x) {
+      float acc = 0.f;
+      for (int sp = 0; sp < p.splits; ++sp) acc += p.dbpart[(size_t)sp * p.K + k];
+      db[k] = acc;
+    }
+  }
+}
+
+TcWgPlan plan_wgrad(const ConvArgs &a) {
+  TcWgPlan pl{};
+  TcWgParams &p = pl.p;
+  pl.ok = false;
+  if (a.sh != 1 || a.sw != 1) return pl;
+  p.N = a.N; p.C = a.C; p.H = a.H; p.W = a.W; p.K = a.K; p.R = a.R; p.S = a.S;
+  p.ph = a.ph; p.pw = a.pw; p.P = a.P; p.Q = a.Q;
+  p.Wf = round_up(a.W + a.pw, 4);
+  p.Hs = a.H + a.ph;
+  p.Lf = p.Hs * p.Wf;
+  p.G = (int64_t)a.N * p.Lf;
+  if (p.G + 8192 >= (1ll << 31)) return pl;
+  if (a.K >= 128) { p.Kc = 128; p.copies = 1; p.nkt = (a.K + 127) / 128; }
+  else {
+    p.Kc = a.K <= 16 ? 16 : a.K <= 32 ? 32 : a.K <= 64 ? 64 : 128;
+    p.copies = 128 / p.Kc;
+    if (p.copies > a.R) p.copies = std::max(1, a.R);  // extra copies would compute nothing
+    while (128 % (p.Kc * p.copies) != 0) --p.copies;
+    p.nkt = 1;
+  }
+  p.nph = std::min(a.S, 4);
+  p.RG = (a.R + p.copies - 1) / p.copies;
+  p.TGt = p.RG * a.S;
+  p.dmax = (p.RG - 1) * p.copies * p.Wf + (a.S - 1);
+  p.Gext = p.G + (int64_t)(p.copies - 1) * p.Wf;
+  // channel tile: as wide as TMEM allows for >= min(TGt, 8) tap groups, >= 16
+  int nc = std::min(256, round_up(std::max(a.C, 16), 16));
+  while (nc > 16 && std::min(p.TGt, 8) * nc > 512) nc -= 16;
+  bool planned = false;
+  for (; nc >= 16 && !planned; nc -= 16) {
+    p.NC = nc;
+    p.nct = (a.C + p.NC - 1) / p.NC;
+    p.TGc = std::min(p.TGt, 512 / p.NC);
+    p.ntg = (p.TGt + p.TGc - 1) / p.TGc;
+    p.nwt = p.nkt * p.nct * p.ntg;
+    for (p.KC = 64; p.KC >= 8; p.KC /= 2) {
+      p.HBq = p.KC / 4 + (p.dmax >> 2);
+      p.XT = p.HBq * 4 + 4;
+      p.YT = p.KC + (p.copies - 1) * p.Wf;
+      p.a_bytes = (uint32_t)(p.KC * 128 * 4);
+      p.phase_bytes = (uint32_t)(p.HBq * p.NC * 16);
+      p.b_bytes = (uint32_t)p.nph * p.phase_bytes;
+      p.stage_bytes = p.a_bytes + p.b_bytes;
+      const size_t per_stage = p.stage_bytes + 4 * (size_t)(p.YT + p.XT);
+      const size_t fixed = 128 * 4 + 16 + 8 * 20 + 16;
+      const int nst = (int)((SMEM_BUDGET - (int64_t)fixed) / (int64_t)per_stage);
+      if (nst >= 2) {
+        p.nstage = std::min(nst, 4);
+        pl.smem = (size_t)p.nstage * per_stage + fixed + 8 * (2 * p.nstage + 1);
+        planned = true;
+        break;
+      }
+    }
+  }
+  if (!planned) return pl;
+  // split the position range: ~2 CTAs per SM worth of work items
+  const int64_t target = 2ll * sm_count();
+  int64_t splits = std::max<int64_t>(1, target / p.nwt);
+  const int64_t max_splits = std::max<int64_t>(1, ceil_div(p.Gext, 4 * p.KC));
+  splits = std::min(splits, max_splits);
+  p.pos_per_split = align_up((size_t)ceil_div(p.Gext, splits), (size_t)p.KC);
+  p.splits = (int)ceil_div(p.Gext, p.pos_per_split);
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(p.TGc * p.NC)) cols <<= 1;
+  if (cols > 512) return pl;
+  p.tmem_cols = cols;
+  pl.part_bytes = align_up((size_t)p.splits * p.nwt * p.TGc * 128 * p.NC * sizeof(float), 256);
+  pl.dbpart_bytes = align_up((size_t)p.splits * p.K * sizeof(float), 256);
+  pl.ok = true;
+  return pl;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ forward (K3)
+bool tc_fwd_supported(const ConvArgs &a, const PoolArgs *pool) {
+  if (device_cc_major() != 10) return false;
+  if (a.sh != 1 || a.sw != 1 || !pool_fusable(pool)) return false;
+  return plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool).ok;
+}
+
+size_t tc_fwd_ws(const ConvArgs &a) {
+  // the packed filter bank only depends on (K, C, R, S)
+  const int nfpad = a.K <= 256 ? std::max(16, round_up(a.K, 16)) : 256;
+  const int nft = a.K <= 256 ? 1 : (a.K + 255) / 256;
+  return align_up((size_t)nft * ((a.C + 7) / 8) * a.R * a.S * 8 * nfpad * sizeof(float), 256);
+}
+
+sysml_status tc_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
+                         float *y, const PoolArgs *pool, float *pout, int32_t *parg, void *ws,
+                         cudaStream_t st) {
+  TcPlan pl = plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool);
+  if (!pl.ok) {
+    set_error("tcgen05 forward: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  return run_fwd(pl, x, f, 0, a.C, bias, pool ? nullptr : y, pout, parg, ws, st);
+}
+
+// ------------------------------------------------------------------ bwd_data (K6)
+static TcPlan plan_bwd_data(const ConvArgs &a) {
+  // dX = conv(dY, rot180(F)^T), pad R-1-ph; input (N, K, P, Q) -> output (N, C, H, W)
+  return plan_fwd(a.N, a.K, a.P, a.Q, a.C, a.R, a.S, a.R - 1 - a.ph, a.S - 1 - a.pw, nullptr);
+}
+
+bool tc_bwd_data_supported(const ConvArgs &a) {
+  if (device_cc_major() != 10) return false;
+  if (a.sh != 1 || a.sw != 1 || a.ph > a.R - 1 || a.pw > a.S - 1) return false;
+  TcPlan pl = plan_bwd_data(a);
+  return pl.ok && pl.p.P == a.H && pl.p.Q == a.W;
+}
+
+size_t tc_bwd_data_ws(const ConvArgs &a) {
+  TcPlan pl = plan_bwd_data(a);
+  return pl.ok ? pl.fp_bytes : 0;
+}
+
+sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
+                              void *ws, cudaStream_t st) {
+  TcPlan pl = plan_bwd_data(a);
+  if (!pl.ok) {
+    set_error("tcgen05 bwd_data: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  // filter bank F is (K x C*RS) = (Cin_of_this_conv x Kout*RS) -> flip = 1
+  return run_fwd(pl, dy, f, 1, a.K, nullptr, dx, nullptr, nullptr, ws, st);
+}
+
+// ------------------------------------------------------------------ bwd_filter (K5)
+bool tc_bwd_filter_supported(const ConvArgs &a) {
+  if (device_cc_major() != 10) return false;
+  if (a.C < 8) return false;  // tiny channel counts waste N; CUDA-core / CSR kernels instead
+  return plan_wgrad(a).ok;
+}
+
+size_t tc_bwd_filter_ws(const ConvArgs &a) {
+  TcWgPlan pl = plan_wgrad(a);
+  return pl.ok ? pl.part_bytes + pl.dbpart_bytes : 0;
+}
+
+sysml_status tc_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,
+                                float *db, void *ws, cudaStream_t st) {
+  TcWgPlan pl = plan_wgrad(a);
+  if (!pl.ok) {
+    set_error("tcgen05 bwd_filter: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  TcWgParams p = pl.p;
+  p.x = x;
+  p.dy = dy;
+  p.part = reinterpret_cast<float *>(ws);
+  p.dbpart = db ? reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + pl.part_bytes) : nullptr;
+  static int attr = 0;
+  SYSML_TRY(set_smem_attr(tc_conv_wgrad_kernel, pl.smem, attr));
+  tc_conv_wgrad_kernel<<<p.splits * p.nwt, TC_THREADS, pl.smem, st>>>(p);
+  SYSML_LAUNCH_CHECK();
+  const int64_t total = (int64_t)a.K * a.C * a.R * a.S;
+  const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 8 * sm_count());
+  tc_wgrad_reduce_kernel<<<blocks, 256, 0, st>>>(p, df, db);
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
+}
+
 }  // namespace sysml

@@ -56,7 +56,7 @@ sysml_status csr_densify(const sysml_csr &x, float *dense, cudaStream_t st);
 sysml_status csr_check(const sysml_csr &m, int64_t *violations, cudaStream_t st);
 
 // conv_tc.cu : tcgen05 TF32 implicit GEMM (SYSML_MATH_TF32)
-struct TcPlan;  // opaque
+
 bool tc_fwd_supported(const ConvArgs &a, const PoolArgs *pool);
 size_t tc_fwd_ws(const ConvArgs &a);
 sysml_status tc_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
