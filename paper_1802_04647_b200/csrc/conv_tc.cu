@@ -39,6 +39,9 @@
 //   in the MN-major layout [channel quad][position][4 ch], the tap shift again being
 //   a descriptor offset.  One accumulator per tap group; the position range is split
 //   over CTAs and the partials are summed in a fixed order (deterministic).
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -49,7 +52,8 @@ namespace sysml {
 
 namespace {
 
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 256;      // bwd_filter kernel: 4 producer warps + MMA/epilogue warps
+constexpr int TC_FWD_THREADS = 288;  // forward kernel: 4 producer, 1 MMA, 4 epilogue warps
 constexpr int SMEM_BUDGET = 225 * 1024;
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
@@ -68,6 +72,7 @@ struct TcFwdParams {
   float *y;           // plain output (N x K*P*Q) or null
   float *pout;        // pooled output or null
   int32_t *parg;      // pooled argmax or null
+  long long *clk;     // optional per-CTA cycle counters (SYSML_TC_PROFILE instrumentation)
   int N, C, H, W, K, R, S, ph, pw, P, Q;
   int Wf, Hs, Lf;
   int64_t G;
@@ -77,6 +82,7 @@ struct TcFwdParams {
   int CT, BB;          // 2-D: column tiles per band, bands per CTA tile (MT = CT*BB)
   int64_t cta_pos;     // positions advanced per CTA tile (linear: MT*128; 2-D: BB*16*Wf)
   int pool, PR, PS, Pp, Qp;
+  int bias_smem;       // bias staged in shared memory (K floats)
   uint32_t a_bytes, b_bytes, stage_bytes, a_sbo;
   int64_t ntiles;
   uint32_t tmem_cols;
@@ -89,41 +95,43 @@ struct TcPlan {
   bool ok;
 };
 
-__device__ __forceinline__ int tile_origin(const TcFwdParams &p, int i) {
-  // position offset (relative to the CTA tile origin) of M-tile i
-  if (!p.tile2d) return i * 128;
-  const int bb = i / p.CT, ct = i - bb * p.CT;
-  return bb * 16 * p.Wf + ct * 8;
-}
+constexpr uint32_t TMEM_BUF = 256;  // accumulator double buffer: columns [0,256) and [256,512)
 
-__global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_fwd_kernel(const TcFwdParams p) {
+__global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const TcFwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t *stage_base = smem;
   int *src_off = reinterpret_cast<int *>(smem + (size_t)p.nstage * p.stage_bytes);
+  float *bias_s = reinterpret_cast<float *>(src_off + p.HALO);
   uint64_t *bars = reinterpret_cast<uint64_t *>(
-      (reinterpret_cast<uintptr_t>(src_off + p.HALO) + 15) & ~(uintptr_t)15);
+      (reinterpret_cast<uintptr_t>(bias_s + (p.bias_smem ? p.K : 0)) + 15) & ~(uintptr_t)15);
   uint64_t *full = bars;
   uint64_t *empty = bars + p.nstage;
-  uint64_t *accf = bars + 2 * p.nstage;
-  uint64_t *acce = accf + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 1);
+  uint64_t *accf = bars + 2 * p.nstage;  // [2]
+  uint64_t *acce = accf + 2;             // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index via shuffle: provably warp-uniform, so role branches keep the uniform datapath
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nstage; ++s) {
       ptx::mbar_init(full + s, 4 + 1);  // 4 producer warps + the expect_tx arrival
       ptx::mbar_init(empty + s, 1);     // tcgen05.commit
     }
-    ptx::mbar_init(accf, 1);
-    ptx::mbar_init(acce, 4);            // 4 epilogue warps
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(accf + b, 1);
+      ptx::mbar_init(acce + b, 4);      // 4 epilogue warps
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 4) ptx::tmem_alloc(tmem_slot, p.tmem_cols);
+  if (p.bias_smem)
+    for (int k = threadIdx.x; k < p.K; k += blockDim.x) bias_s[k] = p.bias[k];
+  if (warp == 4) ptx::tmem_alloc(tmem_slot, p.tmem_cols);  // warp 4 = MMA warp
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int HW = p.H * p.W, RS = p.R * p.S;
+  const int HW = p.H * p.W;
+  const long long t_kernel0 = clock64();
 
   if (warp < 4) {
     // ================= producers: A halo (ld.global -> st.shared) + B chunk (bulk copy)
@@ -148,7 +156,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_fwd_kernel(const TcFwdP
       }
       ptx::named_bar_sync(1, 128);
       for (int ch = 0; ch < p.nchunk; ++ch) {
-        ptx::mbar_wait(empty + stage, phase ^ 1);
+        const long long t_e0 = clock64();
+        ptx::mbar_wait_sleep(empty + stage, phase ^ 1);
+        const long long t_f0 = clock64();
+        if (p.clk && tid == 0) p.clk[blockIdx.x * 8 + 0] += t_f0 - t_e0;
         uint8_t *A = stage_base + (size_t)stage * p.stage_bytes;
         uint8_t *B = A + p.a_bytes;
         if (tid == 0) {
@@ -184,76 +195,89 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_fwd_kernel(const TcFwdP
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(full + stage);
+        if (p.clk && tid == 0) p.clk[blockIdx.x * 8 + 1] += clock64() - t_f0;
         if (++stage == p.nstage) { stage = 0; phase ^= 1; }
       }
     }
   } else {
-    // ================= MMA issuer (warp 4 lane 0) + epilogue (warps 4-7)
-    const int qd = warp - 4;
+    // ================= MMA issuer (warp 4) | epilogue (warps 5-8, TMEM quadrant warp % 4)
+    const int qd = warp & 3;
     const uint32_t idesc = ptx::make_idesc_tf32(128, p.NFpad);
     int stage = 0;
-    uint32_t phase = 0, tphase = 0;
+    uint32_t phase = 0;
     const int PQ = p.P * p.Q;
-    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    const int nc16 = p.NFpad / 16;
+    uint32_t tcount = 0;
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++tcount) {
       const int ft = (int)(tile % p.nft);
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
+      const uint32_t buf = tcount & 1u, bphase = (tcount >> 1) & 1u;
       if (warp == 4) {
-        // whole warp runs the issue loop (warp-uniform descriptors stay in uniform
-        // registers); one elected lane issues each tcgen05.mma / commit
-        ptx::mbar_wait(acce, tphase ^ 1);
+        // Whole warp runs the issue loop: descriptors stay warp-uniform (uniform
+        // registers, no per-MMA conversions).  TMEM columns are addressed from 0:
+        // the CTA owns all 512 columns (1 CTA / SM); buffer `buf` = [buf*256, +256).
+        const long long t_a0 = clock64();
+        ptx::mbar_wait(acce + buf, bphase ^ 1);
+        const long long t_a1 = clock64();
+        if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 3] += t_a1 - t_a0;
         ptx::tc_fence_after();
-        // M-tile origins: nested (outer: bands / linear tiles, inner: column tiles)
-        const int n_outer = p.tile2d ? p.BB : p.MT;
         const int n_inner = p.tile2d ? p.CT : 1;
         const uint32_t step_outer = p.tile2d ? (uint32_t)(16 * p.Wf) : 128u;
-        const uint32_t step_inner = 8u;
-        const uint32_t tmem_step = (uint32_t)p.NFpad;
+        const uint32_t jump_outer = step_outer - 8u * (uint32_t)(n_inner - 1);
+        const uint32_t nf = (uint32_t)p.NFpad;
+        const uint32_t sbase = ptx::smem_u32(stage_base);
         for (int ch = 0; ch < p.nchunk; ++ch) {
+          const long long t_w1 = clock64();
           ptx::mbar_wait(full + stage, phase);
+          if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 2] += clock64() - t_w1;
           ptx::tc_fence_after();
-          const uint32_t A = ptx::smem_u32(stage_base + (size_t)stage * p.stage_bytes);
-          const uint32_t B = A + p.a_bytes;
+          const uint32_t A = sbase + (uint32_t)stage * p.stage_bytes;
           const uint64_t adesc0 = ptx::make_desc(A, p.HALO * 16, p.a_sbo);
-          uint64_t bdesc = ptx::make_desc(B, p.NFpad * 16, 128);
+          uint64_t bdesc = ptx::make_desc(A + p.a_bytes, nf * 16, 128);
           uint32_t acc = ch != 0 ? 1u : 0u;
-          uint32_t dt = 0;  // tap shift in positions (= 16-B descriptor units)
-          for (int r = 0; r < p.R; ++r) {
+          uint32_t drow = 0;
+          for (int r = 0; r < p.R; ++r, drow += (uint32_t)p.Wf) {
             for (int s_ = 0; s_ < p.S; ++s_) {
-              uint32_t org_o = dt, tm = tmem_base;
-              for (int io = 0; io < n_outer; ++io) {
-                uint32_t org = org_o;
-                for (int ii = 0; ii < n_inner; ++ii) {
-                  if (ptx::elect_one()) ptx::mma_tf32(tm, adesc0 + org, bdesc, idesc, acc);
-                  __syncwarp();
-                  org += step_inner;
-                  tm += tmem_step;
-                }
-                org_o += step_outer;
+              uint64_t ad = adesc0 + (uint64_t)(drow + (uint32_t)s_);
+              uint32_t tm = buf * TMEM_BUF;
+              int ct = 0;
+              for (int i = 0; i < p.MT; ++i) {
+                if (ptx::elect_one()) ptx::mma_tf32(tm, ad, bdesc, idesc, acc);
+                __syncwarp();
+                tm += nf;
+                if (++ct == n_inner) { ct = 0; ad += (uint64_t)jump_outer; }
+                else ad += 8u;
               }
               acc = 1u;
-              bdesc += (uint64_t)(2 * p.NFpad);  // next tap: 2 quads x NFpad x 16 B
-              dt += 1;
+              bdesc += (uint64_t)(2 * nf);  // next tap: 2 quads x NFpad x 16 B
             }
-            dt += (uint32_t)(p.Wf - p.S);
           }
           if (ptx::elect_one()) ptx::mma_commit(empty + stage);
           __syncwarp();
           if (++stage == p.nstage) { stage = 0; phase ^= 1; }
         }
-        if (ptx::elect_one()) ptx::mma_commit(accf);
+        if (ptx::elect_one()) ptx::mma_commit(accf + buf);
         __syncwarp();
+        if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 6] += clock64() - t_a1;
+        continue;  // the MMA warp goes straight on to the next tile
       }
+      ptx::mbar_wait_sleep(accf + buf, bphase);
       __syncwarp();
-      ptx::mbar_wait(accf, tphase);
-      __syncwarp();
+      const long long t_epi0 = clock64();
       ptx::tc_fence_after();
       for (int i = 0; i < p.MT; ++i) {
-        const uint32_t trow = tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(i * p.NFpad);
+        const uint32_t trow = tmem_base + ((uint32_t)(qd * 32) << 16) + buf * TMEM_BUF +
+                              (uint32_t)(i * p.NFpad);
+        uint32_t r[2][16];
+        ptx::tmem_ld16_issue(trow, r[0]);
         if (!p.pool) {
-          // linear or 2-D M-tile: lane -> position
+          // lane -> position (linear or 2-D M-tile)
           int64_t g;
           if (!p.tile2d) g = g0 + i * 128 + qd * 32 + lane;
-          else g = g0 + tile_origin(p, i) + (qd * 4 + (lane >> 3)) * p.Wf + (lane & 7);
+          else {
+            const int bb = i / p.CT, ct = i - bb * p.CT;
+            g = g0 + (int64_t)bb * 16 * p.Wf + ct * 8 + (qd * 4 + (lane >> 3)) * p.Wf + (lane & 7);
+          }
           bool valid = g < p.G;
           int64_t ybase = 0;
           if (valid) {
@@ -263,15 +287,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_fwd_kernel(const TcFwdP
             valid = hh < p.P && q < p.Q;
             ybase = (int64_t)n * p.K * PQ + (int64_t)hh * p.Q + q;
           }
-          for (int c16 = 0; c16 < p.NFpad / 16; ++c16) {
-            float v[16];
-            ptx::tmem_ld16(trow + c16 * 16, v);
+          float *yp = p.y + ybase;
+          auto process = [&](const uint32_t(&cur)[16], int c16) {
+            const int k0 = ft * p.NFpad + c16 * 16;
             if (valid) {
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
-                const int k = ft * p.NFpad + c16 * 16 + j;
-                if (k < p.K) p.y[ybase + (int64_t)k * PQ] = v[j] + (p.bias ? __ldg(p.bias + k) : 0.f);
+                const int k = k0 + j;
+                if (k < p.K) {
+                  const float bk = p.bias ? (p.bias_smem ? bias_s[k] : __ldg(p.bias + k)) : 0.f;
+                  yp[(int64_t)k * PQ] = __uint_as_float(cur[j]) + bk;
+                }
               }
+            }
+          };
+          // two register buffers with static indices (no local memory); one TMEM load
+          // in flight while the previous 16 columns are stored
+          for (int c16 = 0; c16 < nc16; c16 += 2) {
+            ptx::tmem_ld_wait(r[0]);
+            if (c16 + 1 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 1) * 16, r[1]);
+            process(r[0], c16);
+            if (c16 + 1 < nc16) {
+              ptx::tmem_ld_wait(r[1]);
+              if (c16 + 2 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 2) * 16, r[0]);
+              process(r[1], c16 + 1);
             }
           }
         } else {
@@ -287,41 +326,68 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_fwd_kernel(const TcFwdP
           const bool store = leader && n < p.N && pp < p.Pp && pc < p.Qp;
           const int PpQp = p.Pp * p.Qp;
           const int64_t obase = (int64_t)n * p.K * PpQp + (int64_t)pp * p.Qp + pc;
-          for (int c16 = 0; c16 < p.NFpad / 16; ++c16) {
-            float v[16];
-            ptx::tmem_ld16(trow + c16 * 16, v);
+          const int idx0 = hh * p.Q + col;
+          auto process = [&](const uint32_t(&cur)[16], int c16) {
+            const int k0 = ft * p.NFpad + c16 * 16;
+            float z[16];
+            int idx[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const int k = ft * p.NFpad + c16 * 16 + j;
-              const float bk = (p.bias && k < p.K) ? __ldg(p.bias + k) : 0.f;
-              float z = v[j] + bk;
-              z = z > 0.f ? z : 0.f;  // relu, +0.0 for non-positive (reading R7)
-              int idx = (k * p.P + hh) * p.Q + col;
-              // first-occurrence max over the window (r outer, s inner; strict '>')
-              for (int d = 1; d < p.PS; d <<= 1) {
-                const float z2 = __shfl_down_sync(0xffffffffu, z, d);
-                const int i2 = __shfl_down_sync(0xffffffffu, idx, d);
-                if (z2 > z) { z = z2; idx = i2; }
+              const int k = k0 + j;
+              const float bk = (p.bias && k < p.K) ? (p.bias_smem ? bias_s[k] : __ldg(p.bias + k)) : 0.f;
+              const float t = __uint_as_float(cur[j]) + bk;
+              z[j] = t > 0.f ? t : 0.f;  // relu, +0.0 for non-positive (reading R7)
+              idx[j] = k * PQ + idx0;
+            }
+            // first-occurrence max over the window (r outer, s inner; strict '>'):
+            // combine with the later partner only when strictly greater
+            for (int d = 1; d < p.PS; d <<= 1) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float z2 = __shfl_down_sync(0xffffffffu, z[j], d);
+                const int i2 = __shfl_down_sync(0xffffffffu, idx[j], d);
+                if (z2 > z[j]) { z[j] = z2; idx[j] = i2; }
               }
-              for (int d = 8; d < 8 * p.PR; d <<= 1) {
-                const float z2 = __shfl_down_sync(0xffffffffu, z, d);
-                const int i2 = __shfl_down_sync(0xffffffffu, idx, d);
-                if (z2 > z) { z = z2; idx = i2; }
+            }
+            for (int d = 8; d < 8 * p.PR; d <<= 1) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float z2 = __shfl_down_sync(0xffffffffu, z[j], d);
+                const int i2 = __shfl_down_sync(0xffffffffu, idx[j], d);
+                if (z2 > z[j]) { z[j] = z2; idx[j] = i2; }
               }
-              if (store && k < p.K) {
-                p.pout[obase + (int64_t)k * PpQp] = z;
-                if (p.parg) p.parg[obase + (int64_t)k * PpQp] = idx;
+            }
+            if (store) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int k = k0 + j;
+                if (k < p.K) {
+                  p.pout[obase + (int64_t)k * PpQp] = z[j];
+                  if (p.parg) p.parg[obase + (int64_t)k * PpQp] = idx[j];
+                }
               }
+            }
+          };
+          for (int c16 = 0; c16 < nc16; c16 += 2) {
+            ptx::tmem_ld_wait(r[0]);
+            if (c16 + 1 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 1) * 16, r[1]);
+            process(r[0], c16);
+            if (c16 + 1 < nc16) {
+              ptx::tmem_ld_wait(r[1]);
+              if (c16 + 2 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 2) * 16, r[0]);
+              process(r[1], c16 + 1);
             }
           }
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(acce);
-      tphase ^= 1;
+      if (lane == 0) ptx::mbar_arrive(acce + buf);
+      if (p.clk && lane == 0 && warp == 5) p.clk[blockIdx.x * 8 + 4] += clock64() - t_epi0;
     }
   }
+  if (p.clk && threadIdx.x == 160) p.clk[blockIdx.x * 8 + 5] = clock64() - t_kernel0;
+  if (p.clk && threadIdx.x == 0) p.clk[blockIdx.x * 8 + 7] = clock64() - t_kernel0;
   __syncthreads();
   if (warp == 4) {
     ptx::tc_fence_after();
@@ -392,7 +458,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   p.b_bytes = (uint32_t)(RS * 2 * p.NFpad * 16);
   const int nsm = sm_count();
   const int64_t rows_total = (int64_t)N * p.Hs;
-  int mt_cap = std::min(16, 512 / p.NFpad);
+  int mt_cap = std::min(16, (int)TMEM_BUF / p.NFpad);  // TMEM double buffer
   p.CT = (p.Q + 7) / 8;
   if (p.tile2d && p.CT > mt_cap) return pl;
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -405,16 +471,18 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
         if (bb < 1) continue;
         cta_pos = (int64_t)bb * 16 * p.Wf;
         halo = (bb - 1) * 16 * p.Wf + (p.CT - 1) * 8 + 15 * p.Wf + 7 + (R - 1) * p.Wf + (S - 1) + 1;
+        halo = round_up(halo, 8);  // LBO multiple of 128 B
         ntiles = ceil_div(rows_total, (int64_t)bb * 16) * p.nft;
       } else {
         cta_pos = (int64_t)mt * 128;
-        halo = mt * 128 + (R - 1) * p.Wf + (S - 1);
+        halo = round_up(mt * 128 + (R - 1) * p.Wf + (S - 1), 8);  // LBO multiple of 128 B
         ntiles = ceil_div(p.G, cta_pos) * p.nft;
       }
       if (attempt == 0 && mt > 1 && ntiles < nsm) continue;  // keep the SMs busy first
       const uint32_t a_bytes = (uint32_t)(2 * halo * 16);
       const uint32_t stage = a_bytes + p.b_bytes;
-      const size_t fixed = (size_t)halo * 4 + 16 + 8 * 20 + 16;
+      p.bias_smem = K <= 4096 ? 1 : 0;
+      const size_t fixed = (size_t)halo * 4 + (p.bias_smem ? (size_t)K * 4 : 0) + 16 + 8 * 24 + 16;
       const int nst = (int)((SMEM_BUDGET - (int64_t)fixed) / (int64_t)stage);
       if (nst < 2) continue;
       p.MT = p.tile2d ? bb * p.CT : mt;
@@ -426,7 +494,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
       p.stage_bytes = stage;
       p.nstage = std::min(nst, 8);
       p.a_sbo = p.tile2d ? (uint32_t)(p.Wf * 16) : 128u;
-      pl.smem = (size_t)p.nstage * stage + fixed + 8 * (2 * p.nstage + 2);
+      pl.smem = (size_t)p.nstage * stage + fixed + 8 * (2 * p.nstage + 4);
       pl.ok = true;
       break;
     }
@@ -434,9 +502,8 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   }
   if (!pl.ok) return pl;
   if (p.tile2d && (uint32_t)p.Wf * 16 >= (1u << 18)) { pl.ok = false; return pl; }
-  uint32_t cols = 32;
-  while (cols < (uint32_t)(p.MT * p.NFpad)) cols <<= 1;
-  p.tmem_cols = cols;
+  if (p.MT * p.NFpad > (int)TMEM_BUF) { pl.ok = false; return pl; }
+  p.tmem_cols = 512;  // whole TMEM: base column 0 (1 CTA per SM), issue loops address from 0
   pl.fp_bytes = align_up((size_t)p.nft * p.nchunk * RS * 8 * p.NFpad * sizeof(float), 256);
   return pl;
 }
@@ -468,11 +535,31 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
   p.y = y;
   p.pout = pout;
   p.parg = parg;
+  if (!bias) p.bias_smem = 0;
   static int attr = 0;
   SYSML_TRY(set_smem_attr(tc_conv_fwd_kernel, pl.smem, attr));
   const int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
-  tc_conv_fwd_kernel<<<grid, TC_THREADS, pl.smem, st>>>(p);
+  static long long *dclk = nullptr;
+  const bool prof = getenv("SYSML_TC_PROFILE") != nullptr;
+  p.clk = nullptr;
+  if (prof) {
+    if (!dclk) cudaMalloc(&dclk, sizeof(long long) * 8 * 1024);
+    cudaMemsetAsync(dclk, 0, sizeof(long long) * 8 * 1024, st);
+    p.clk = dclk;
+  }
+  tc_conv_fwd_kernel<<<grid, TC_FWD_THREADS, pl.smem, st>>>(p);
   SYSML_LAUNCH_CHECK();
+  if (prof) {
+    long long h[8 * 1024];
+    cudaMemcpyAsync(h, dclk, sizeof(long long) * 8 * grid, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double a[8] = {0};
+    for (int b = 0; b < grid; ++b)
+      for (int j = 0; j < 8; ++j) a[j] += (double)h[b * 8 + j] / grid;
+    fprintf(stderr, "[tc_fwd N=%d C=%d K=%d MT=%d nstage=%d tiles=%lld] prod_wait_empty %.0f prod_fill %.0f "
+            "mma_wait_full %.0f mma_wait_acce %.0f epilogue %.0f total_warp4 %.0f mma_loop %.0f total_prod %.0f\n",
+            p.N, p.C, p.K, p.MT, p.nstage, (long long)p.ntiles, a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]);
+  }
   return SYSML_OK;
 }
 
@@ -528,7 +615,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_wgrad_kernel(const TcWg
   uint64_t *accf = bars + 2 * p.nstage;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accf + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index via shuffle: provably warp-uniform, so role branches keep the uniform datapath
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   // work decomposition: blockIdx.x = split * nwt + wt; wt = (kt * nct + ct) * ntg + tgt
   const int wt = blockIdx.x % p.nwt;
   const int split = blockIdx.x / p.nwt;
@@ -571,7 +659,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_wgrad_kernel(const TcWg
     uint32_t phase = 0;
     for (int ch = 0; ch < nchunks; ++ch) {
       const int64_t u0 = gs + (int64_t)ch * p.KC;
-      ptx::mbar_wait(empty + stage, phase ^ 1);
+      ptx::mbar_wait_sleep(empty + stage, phase ^ 1);
       int *yt = ytab + stage * p.YT;
       int *xt = xtab + stage * p.XT;
       // dY offsets for output-frame positions u0 - (copies-1)*Wf + e, e < YT
@@ -694,7 +782,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_wgrad_kernel(const TcWg
         for (int kk = 0; kk < p.KC / 8; ++kk) {
           const uint64_t adesc = adesc0 + (uint64_t)(kk * 2 * 128);  // 2 pos quads x 2048 B
           int rg = rg0, s_ = s0;
-          uint32_t tm = tmem_base;
+          uint32_t tm = 0;  // CTA owns all 512 TMEM columns
           const uint32_t acc = (ch | kk) != 0 ? 1u : 0u;
           for (int tl = 0; tl < tgn; ++tl) {
             const uint32_t d = (uint32_t)(rg * p.copies * p.Wf + s_);
@@ -713,7 +801,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_wgrad_kernel(const TcWg
       if (ptx::elect_one()) ptx::mma_commit(accf);
       __syncwarp();
     }
-    ptx::mbar_wait(accf, 0);
+    ptx::mbar_wait_sleep(accf, 0);
     __syncwarp();
     ptx::tc_fence_after();
     // epilogue: partial[split][wt][tl][row][NC]; zero if no chunk ran
@@ -842,7 +930,7 @@ TcWgPlan plan_wgrad(const ConvArgs &a) {
   uint32_t cols = 32;
   while (cols < (uint32_t)(p.TGc * p.NC)) cols <<= 1;
   if (cols > 512) return pl;
-  p.tmem_cols = cols;
+  p.tmem_cols = 512;  // whole TMEM: base column 0 (1 CTA per SM), issue loops address from 0
   pl.part_bytes = align_up((size_t)p.splits * p.nwt * p.TGc * 128 * p.NC * sizeof(float), 256);
   pl.dbpart_bytes = align_up((size_t)p.splits * p.K * sizeof(float), 256);
   pl.ok = true;
