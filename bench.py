@@ -61,6 +61,8 @@ STAGE_WORK = {
     "B2d_conv2_bwd_data": (2 * 64 * 800 * 196, 12544 * 4 + 6272 * 4, "tensor"),
     "B1p_maxpool_bwd1": (0, 6272 * 4 * 3 + 25088 * 4, "hbm"),
     "B1f_conv1_bwd_filter": (2 * 32 * 25 * 784, 784 * 4 + 25088 * 4, "hbm"),
+    # fused maxpool_bwd1 + conv1 bwd_filter: reads da1, i1, a1 (pooled) and X
+    "B1_fused_pool_bwd_conv1_wgrad": (2 * 32 * 25 * 196, 6272 * 4 * 3 + 784 * 4, "hbm"),
 }
 
 

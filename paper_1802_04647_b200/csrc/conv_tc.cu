@@ -97,6 +97,168 @@ struct TcPlan {
 
 constexpr uint32_t TMEM_BUF = 256;  // accumulator double buffer: columns [0,256) and [256,512)
 
+
+// ---------------------------------------------------------------- epilogues
+// Both drain the CTA tile's accumulators (MT M-tiles x NFpad columns) from TMEM in
+// 16-column chunks with one tcgen05.ld in flight while the previous chunk is stored.
+// Bias comes from shared memory as float4s; full chunks (all 16 filters < K) take a
+// branch-free path.
+
+__device__ __forceinline__ void load_bias16(const TcFwdParams &p, const float *bias_s, int k0,
+                                            float (&b)[16]) {
+  if (!p.bias) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) b[j] = 0.f;
+  } else if (p.bias_smem && k0 + 16 <= p.K && (k0 & 3) == 0) {
+    const float4 *b4 = reinterpret_cast<const float4 *>(bias_s + k0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 v = b4[j];
+      b[4 * j] = v.x; b[4 * j + 1] = v.y; b[4 * j + 2] = v.z; b[4 * j + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) b[j] = (k0 + j < p.K) ? __ldg(p.bias + k0 + j) : 0.f;
+  }
+}
+
+// plain conv output: lane -> position (linear or 2-D M-tile), 16 filters per chunk
+__device__ __forceinline__ void epi_plain(const TcFwdParams &p, uint32_t tbase, int64_t g0, int ft,
+                                          int qd, int lane, const float *bias_s) {
+  const int PQ = p.P * p.Q;
+  const int nc16 = p.NFpad / 16;
+  float *__restrict__ y = p.y;
+  for (int i = 0; i < p.MT; ++i) {
+    const uint32_t trow = tbase + (uint32_t)(i * p.NFpad);
+    uint32_t r0[16], r1[16];
+    ptx::tmem_ld16_issue(trow, r0);
+    int64_t g;
+    if (!p.tile2d) g = g0 + i * 128 + qd * 32 + lane;
+    else {
+      const int bb = i / p.CT, ct = i - bb * p.CT;
+      g = g0 + (int64_t)bb * 16 * p.Wf + ct * 8 + (qd * 4 + (lane >> 3)) * p.Wf + (lane & 7);
+    }
+    bool valid = g < p.G;
+    int64_t ybase = 0;
+    if (valid) {
+      const int n = (int)(g / p.Lf);
+      const int rem = (int)(g - (int64_t)n * p.Lf);
+      const int hh = rem / p.Wf, q = rem - hh * p.Wf;
+      valid = hh < p.P && q < p.Q;
+      ybase = (int64_t)n * p.K * PQ + (int64_t)hh * p.Q + q;
+    }
+    auto process = [&](const uint32_t(&cur)[16], int c16) {
+      const int k0 = ft * p.NFpad + c16 * 16;
+      float b[16];
+      load_bias16(p, bias_s, k0, b);
+      if (!valid) return;
+      float *yp = y + ybase + (int64_t)k0 * PQ;
+      if (k0 + 16 <= p.K) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) yp[(int64_t)j * PQ] = __uint_as_float(cur[j]) + b[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (k0 + j < p.K) yp[(int64_t)j * PQ] = __uint_as_float(cur[j]) + b[j];
+      }
+    };
+    for (int c16 = 0; c16 < nc16; c16 += 2) {
+      ptx::tmem_ld_wait(r0);
+      if (c16 + 1 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 1) * 16, r1);
+      process(r0, c16);
+      if (c16 + 1 < nc16) {
+        ptx::tmem_ld_wait(r1);
+        if (c16 + 2 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 2) * 16, r0);
+        process(r1, c16 + 1);
+      }
+    }
+  }
+}
+
+// fused bias + relu + 2x2/2 max-pool on a 2-D M-tile (16 rows x 8 cols): the window
+// of lane l is lanes l, l+1 (next column), l+8, l+9 (next row), all in this warp.
+// First-occurrence tie-break (r outer, s inner; strict '>', readings R5/R7): the
+// later partner replaces the current value only when strictly greater.
+__device__ __forceinline__ void epi_pool2(const TcFwdParams &p, uint32_t tbase, int64_t g0, int ft,
+                                          int qd, int lane, const float *bias_s) {
+  const int PQ = p.P * p.Q, PpQp = p.Pp * p.Qp;
+  const int nc16 = p.NFpad / 16;
+  const int rl = qd * 4 + (lane >> 3), cl = lane & 7;
+  const bool leader = ((rl | cl) & 1) == 0;
+  float *__restrict__ pout = p.pout;
+  int32_t *__restrict__ parg = p.parg;
+  for (int i = 0; i < p.MT; ++i) {
+    const uint32_t trow = tbase + (uint32_t)(i * p.NFpad);
+    uint32_t r0[16], r1[16];
+    ptx::tmem_ld16_issue(trow, r0);
+    const int bb = i / p.CT, ct = i - bb * p.CT;
+    const int64_t grow = g0 / p.Wf + bb * 16 + rl;  // global frame row
+    const int col = ct * 8 + cl;
+    const int n = (int)(grow / p.Hs);
+    const int hh = (int)(grow - (int64_t)n * p.Hs);
+    const int pp = hh >> 1, pc = col >> 1;
+    const bool store = leader && n < p.N && pp < p.Pp && pc < p.Qp;
+    const int64_t obase = store ? (int64_t)n * p.K * PpQp + (int64_t)pp * p.Qp + pc : 0;
+    float *const pout_t = pout + obase;
+    int32_t *const parg_t = parg ? parg + obase : nullptr;
+    const int idx0 = hh * p.Q + col;
+    auto process = [&](const uint32_t(&cur)[16], int c16) {
+      const int k0 = ft * p.NFpad + c16 * 16;
+      float b[16], z[16];
+      int off[16];
+      load_bias16(p, bias_s, k0, b);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float t = __uint_as_float(cur[j]) + b[j];
+        z[j] = t > 0.f ? t : 0.f;  // relu, +0.0 for non-positive (reading R7)
+        off[j] = 0;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {  // (r, s) -> (r, s+1)
+        const float z2 = __shfl_down_sync(0xffffffffu, z[j], 1);
+        if (z2 > z[j]) { z[j] = z2; off[j] = 1; }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {  // row r -> row r+1 (carry the partner's column choice)
+        const float z2 = __shfl_down_sync(0xffffffffu, z[j], 8);
+        const int o2 = __shfl_down_sync(0xffffffffu, off[j], 8);
+        if (z2 > z[j]) { z[j] = z2; off[j] = p.Q + o2; }
+      }
+      if (store) {
+        // 32-bit element offsets from per-M-tile base pointers (no 64-bit math per store)
+        float *po = pout_t + k0 * PpQp;
+        const int ib = k0 * PQ + idx0;
+        if (k0 + 16 <= p.K) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) po[j * PpQp] = z[j];
+          if (parg_t) {
+            int32_t *pa = parg_t + k0 * PpQp;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) pa[j * PpQp] = ib + j * PQ + off[j];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (k0 + j < p.K) {
+              po[j * PpQp] = z[j];
+              if (parg_t) parg_t[k0 * PpQp + j * PpQp] = ib + j * PQ + off[j];
+            }
+        }
+      }
+    };
+    for (int c16 = 0; c16 < nc16; c16 += 2) {
+      ptx::tmem_ld_wait(r0);
+      if (c16 + 1 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 1) * 16, r1);
+      process(r0, c16);
+      if (c16 + 1 < nc16) {
+        ptx::tmem_ld_wait(r1);
+        if (c16 + 2 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 2) * 16, r0);
+        process(r1, c16 + 1);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const TcFwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t *stage_base = smem;
@@ -265,121 +427,9 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       __syncwarp();
       const long long t_epi0 = clock64();
       ptx::tc_fence_after();
-      for (int i = 0; i < p.MT; ++i) {
-        const uint32_t trow = tmem_base + ((uint32_t)(qd * 32) << 16) + buf * TMEM_BUF +
-                              (uint32_t)(i * p.NFpad);
-        uint32_t r[2][16];
-        ptx::tmem_ld16_issue(trow, r[0]);
-        if (!p.pool) {
-          // lane -> position (linear or 2-D M-tile)
-          int64_t g;
-          if (!p.tile2d) g = g0 + i * 128 + qd * 32 + lane;
-          else {
-            const int bb = i / p.CT, ct = i - bb * p.CT;
-            g = g0 + (int64_t)bb * 16 * p.Wf + ct * 8 + (qd * 4 + (lane >> 3)) * p.Wf + (lane & 7);
-          }
-          bool valid = g < p.G;
-          int64_t ybase = 0;
-          if (valid) {
-            const int n = (int)(g / p.Lf);
-            const int rem = (int)(g - (int64_t)n * p.Lf);
-            const int hh = rem / p.Wf, q = rem - hh * p.Wf;
-            valid = hh < p.P && q < p.Q;
-            ybase = (int64_t)n * p.K * PQ + (int64_t)hh * p.Q + q;
-          }
-          float *yp = p.y + ybase;
-          auto process = [&](const uint32_t(&cur)[16], int c16) {
-            const int k0 = ft * p.NFpad + c16 * 16;
-            if (valid) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const int k = k0 + j;
-                if (k < p.K) {
-                  const float bk = p.bias ? (p.bias_smem ? bias_s[k] : __ldg(p.bias + k)) : 0.f;
-                  yp[(int64_t)k * PQ] = __uint_as_float(cur[j]) + bk;
-                }
-              }
-            }
-          };
-          // two register buffers with static indices (no local memory); one TMEM load
-          // in flight while the previous 16 columns are stored
-          for (int c16 = 0; c16 < nc16; c16 += 2) {
-            ptx::tmem_ld_wait(r[0]);
-            if (c16 + 1 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 1) * 16, r[1]);
-            process(r[0], c16);
-            if (c16 + 1 < nc16) {
-              ptx::tmem_ld_wait(r[1]);
-              if (c16 + 2 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 2) * 16, r[0]);
-              process(r[1], c16 + 1);
-            }
-          }
-        } else {
-          // 2-D M-tile (16 rows x 8 cols): lane (rl = qd*4 + lane/8, cl = lane%8)
-          const int bb = i / p.CT, ct = i - bb * p.CT;
-          const int rl = qd * 4 + (lane >> 3), cl = lane & 7;
-          const int64_t grow = g0 / p.Wf + bb * 16 + rl;  // global frame row
-          const int col = ct * 8 + cl;
-          const int n = (int)(grow / p.Hs);
-          const int hh = (int)(grow - (int64_t)n * p.Hs);
-          const bool leader = (rl % p.PR) == 0 && (cl % p.PS) == 0;
-          const int pp = hh / p.PR, pc = col / p.PS;
-          const bool store = leader && n < p.N && pp < p.Pp && pc < p.Qp;
-          const int PpQp = p.Pp * p.Qp;
-          const int64_t obase = (int64_t)n * p.K * PpQp + (int64_t)pp * p.Qp + pc;
-          const int idx0 = hh * p.Q + col;
-          auto process = [&](const uint32_t(&cur)[16], int c16) {
-            const int k0 = ft * p.NFpad + c16 * 16;
-            float z[16];
-            int idx[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int k = k0 + j;
-              const float bk = (p.bias && k < p.K) ? (p.bias_smem ? bias_s[k] : __ldg(p.bias + k)) : 0.f;
-              const float t = __uint_as_float(cur[j]) + bk;
-              z[j] = t > 0.f ? t : 0.f;  // relu, +0.0 for non-positive (reading R7)
-              idx[j] = k * PQ + idx0;
-            }
-            // first-occurrence max over the window (r outer, s inner; strict '>'):
-            // combine with the later partner only when strictly greater
-            for (int d = 1; d < p.PS; d <<= 1) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const float z2 = __shfl_down_sync(0xffffffffu, z[j], d);
-                const int i2 = __shfl_down_sync(0xffffffffu, idx[j], d);
-                if (z2 > z[j]) { z[j] = z2; idx[j] = i2; }
-              }
-            }
-            for (int d = 8; d < 8 * p.PR; d <<= 1) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const float z2 = __shfl_down_sync(0xffffffffu, z[j], d);
-                const int i2 = __shfl_down_sync(0xffffffffu, idx[j], d);
-                if (z2 > z[j]) { z[j] = z2; idx[j] = i2; }
-              }
-            }
-            if (store) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const int k = k0 + j;
-                if (k < p.K) {
-                  p.pout[obase + (int64_t)k * PpQp] = z[j];
-                  if (p.parg) p.parg[obase + (int64_t)k * PpQp] = idx[j];
-                }
-              }
-            }
-          };
-          for (int c16 = 0; c16 < nc16; c16 += 2) {
-            ptx::tmem_ld_wait(r[0]);
-            if (c16 + 1 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 1) * 16, r[1]);
-            process(r[0], c16);
-            if (c16 + 1 < nc16) {
-              ptx::tmem_ld_wait(r[1]);
-              if (c16 + 2 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 2) * 16, r[0]);
-              process(r[1], c16 + 1);
-            }
-          }
-        }
-      }
+      const uint32_t tbase = tmem_base + ((uint32_t)(qd * 32) << 16) + buf * TMEM_BUF;
+      if (p.pool) epi_pool2(p, tbase, g0, ft, qd, lane, bias_s);
+      else epi_plain(p, tbase, g0, ft, qd, lane, bias_s);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(acce + buf);
@@ -436,8 +486,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   p.PS = pool ? pool->S : 1;
   if (pool) {
     // 2-D tiles: window rows must tile the 16-row tile and columns the 8-column tile
-    if (!(p.PR == 1 || p.PR == 2 || p.PR == 4 || p.PR == 8 || p.PR == 16)) return pl;
-    if (!(p.PS == 1 || p.PS == 2 || p.PS == 4 || p.PS == 8)) return pl;
+    if (p.PR != 2 || p.PS != 2) return pl;  // the fused epilogue implements 2x2/2 windows
     p.Pp = pool->P;
     p.Qp = pool->Q;
   }

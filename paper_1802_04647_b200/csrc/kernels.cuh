@@ -71,4 +71,12 @@ size_t tc_bwd_filter_ws(const ConvArgs &a);
 sysml_status tc_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,
                                 float *db, void *ws, cudaStream_t st);
 
+// fused_bwd.cu : maxpool_bwd + conv2d_bwd_filter for single-channel conv layers
+bool fused_pool_bwd_wgrad_supported(const ConvArgs &c, const PoolArgs &pa);
+size_t fused_pool_bwd_wgrad_ws(const ConvArgs &c);
+sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const float *x,
+                                  const sysml_csr *xcsr, const float *dpool,
+                                  const int32_t *argmax, const float *mask, float *df, float *db,
+                                  void *ws, cudaStream_t st);
+
 }  // namespace sysml

@@ -204,8 +204,9 @@ NcclSyms &nccl_syms() {
 
 const char *STAGE_NAMES[] = {"F1_conv1_pool", "F2_conv2_pool", "F3_affine_softmax_ce",
                              "B3_affine_bwd", "B2p_maxpool_bwd2", "B2f_conv2_bwd_filter",
-                             "B2d_conv2_bwd_data", "B1p_maxpool_bwd1", "B1f_conv1_bwd_filter"};
-constexpr int NSTAGES = 9;
+                             "B2d_conv2_bwd_data", "B1p_maxpool_bwd1", "B1f_conv1_bwd_filter",
+                             "B1_fused_pool_bwd_conv1_wgrad"};
+constexpr int NSTAGES = 10;
 
 }  // namespace
 
@@ -227,6 +228,7 @@ struct sysml_lenet {
   int64_t calls[NSTAGES] = {0};
   int launches = 0;
   int dw3_chunks = 1;
+  bool fused_b1 = false;  // maxpool_bwd1 + conv1 bwd_filter in one kernel (fused_bwd.cu)
 };
 
 namespace {
@@ -334,6 +336,13 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
   need = std::max(need, w);
   if ((s = conv_bwd_filter_ws(c1, h->csr, &w)) != SYSML_OK) return fail(s);
   need = std::max(need, w);
+  {
+    ConvGeom g1, gp1;
+    if ((s = validate_conv(&c1, &g1)) != SYSML_OK) return fail(s);
+    if ((s = validate_pool(&p1, &gp1)) != SYSML_OK) return fail(s);
+    h->fused_b1 = fused_pool_bwd_wgrad_supported(conv_args(g1), pool_args(gp1, 1));
+    if (h->fused_b1) need = std::max(need, fused_pool_bwd_wgrad_ws(conv_args(g1)));
+  }
   h->ws_bytes = need;
   if (need) {
     cudaError_t e = cudaMalloc(&h->ws, need);
@@ -441,19 +450,31 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
   SYSML_TRY(T.begin(6));
   SYSML_TRY(conv_bwd_data_dispatch(c2, params + OFF_F2, h->dz2, h->da1, h->ws, h->ws_bytes, st));
   SYSML_TRY(T.end());
-  // B1p
-  SYSML_TRY(T.begin(7));
-  {
-    ConvGeom g;
-    SYSML_TRY(validate_pool(&p1, &g));
-    SYSML_TRY(launch_maxpool_bwd(pool_args(g, 1), h->i1, h->da1, h->a1, h->dz1, st));
+  if (h->fused_b1) {
+    // B1 fused: conv1 bwd_filter of maxpool_bwd(i1, da1, a1 > 0) without materialising dz1
+    SYSML_TRY(T.begin(9));
+    ConvGeom g1, gp1;
+    SYSML_TRY(validate_conv(&c1, &g1));
+    SYSML_TRY(validate_pool(&p1, &gp1));
+    SYSML_TRY(fused_pool_bwd_wgrad(conv_args(g1), pool_args(gp1, 1), x->is_csr ? nullptr : x->dense,
+                                   x->is_csr ? &x->csr : nullptr, h->da1, h->i1, h->a1,
+                                   grads + OFF_F1, grads + OFF_B1, h->ws, st));
+    SYSML_TRY(T.end());
+  } else {
+    // B1p
+    SYSML_TRY(T.begin(7));
+    {
+      ConvGeom g;
+      SYSML_TRY(validate_pool(&p1, &g));
+      SYSML_TRY(launch_maxpool_bwd(pool_args(g, 1), h->i1, h->da1, h->a1, h->dz1, st));
+    }
+    SYSML_TRY(T.end());
+    // B1f
+    SYSML_TRY(T.begin(8));
+    SYSML_TRY(conv_bwd_filter_dispatch(c1, *x, h->dz1, grads + OFF_F1, grads + OFF_B1, h->ws,
+                                       h->ws_bytes, st));
+    SYSML_TRY(T.end());
   }
-  SYSML_TRY(T.end());
-  // B1f
-  SYSML_TRY(T.begin(8));
-  SYSML_TRY(conv_bwd_filter_dispatch(c1, *x, h->dz1, grads + OFF_F1, grads + OFF_B1, h->ws,
-                                     h->ws_bytes, st));
-  SYSML_TRY(T.end());
   (void)launches0;
   return SYSML_OK;
 }
