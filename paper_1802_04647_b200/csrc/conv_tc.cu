@@ -83,6 +83,10 @@ struct TcFwdParams {
   int64_t cta_pos;     // positions advanced per CTA tile (linear: MT*128; 2-D: BB*16*Wf)
   int pool, PR, PS, Pp, Qp;
   int bias_smem;       // bias staged in shared memory (K floats)
+  int64_t in_plane;    // > 0: input is SPF [C][in_plane], stored position = frame pos + in_shift
+  int in_shift;
+  int64_t out_plane;   // > 0: pooled output to SPF [K][out_plane] at (pp+out_off)*out_Wf + pc+out_off
+  int out_Wf, out_Lf, out_off;
   uint32_t a_bytes, b_bytes, stage_bytes, a_sbo;
   int64_t ntiles;
   uint32_t tmem_cols;
@@ -199,7 +203,13 @@ __device__ __forceinline__ void epi_pool2(const TcFwdParams &p, uint32_t tbase, 
     const int pp = hh >> 1, pc = col >> 1;
     const bool store = leader && n < p.N && pp < p.Pp && pc < p.Qp;
     const int64_t obase = store ? (int64_t)n * p.K * PpQp + (int64_t)pp * p.Qp + pc : 0;
-    float *const pout_t = pout + obase;
+    // pooled values: NCHW, or SPF (channel stride out_plane) for the LeNet-internal layout
+    const int vstride = p.out_plane > 0 ? (int)p.out_plane : PpQp;
+    const int64_t vbase = !store ? 0
+                          : p.out_plane > 0 ? (int64_t)n * p.out_Lf + (int64_t)(pp + p.out_off) * p.out_Wf +
+                                                  (pc + p.out_off)
+                                            : obase;
+    float *const pout_t = pout + vbase;
     int32_t *const parg_t = parg ? parg + obase : nullptr;
     const int idx0 = hh * p.Q + col;
     auto process = [&](const uint32_t(&cur)[16], int c16) {
@@ -226,11 +236,11 @@ __device__ __forceinline__ void epi_pool2(const TcFwdParams &p, uint32_t tbase, 
       }
       if (store) {
         // 32-bit element offsets from per-M-tile base pointers (no 64-bit math per store)
-        float *po = pout_t + k0 * PpQp;
+        float *po = pout_t + (int64_t)k0 * vstride;
         const int ib = k0 * PQ + idx0;
         if (k0 + 16 <= p.K) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) po[j * PpQp] = z[j];
+          for (int j = 0; j < 16; ++j) po[j * vstride] = z[j];
           if (parg_t) {
             int32_t *pa = parg_t + k0 * PpQp;
 #pragma unroll
@@ -240,7 +250,7 @@ __device__ __forceinline__ void epi_pool2(const TcFwdParams &p, uint32_t tbase, 
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             if (k0 + j < p.K) {
-              po[j * PpQp] = z[j];
+              po[j * vstride] = z[j];
               if (parg_t) parg_t[k0 * PpQp + j * PpQp] = ib + j * PQ + off[j];
             }
         }
@@ -307,7 +317,10 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       for (int pos = tid; pos < p.HALO; pos += 128) {
         const int64_t gi = g0 + pos;
         int off = -1;
-        if (gi < p.G) {
+        if (p.in_plane > 0) {
+          const int64_t si = gi + p.in_shift;  // SPF: zeros are stored, no decoding
+          if (gi < p.G && si >= 0 && si < p.in_plane) off = (int)si;
+        } else if (gi < p.G) {
           const int n = (int)(gi / p.Lf);
           const int rem = (int)(gi - (int64_t)n * p.Lf);
           const int hh = rem / p.Wf, ww = rem - hh * p.Wf;
@@ -333,7 +346,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         const uint32_t a0 = ptx::smem_u32(A);
         const uint32_t a1 = a0 + (uint32_t)p.HALO * 16;
         const int nc = min(8, p.C - c0);
-        const float *xc = p.x + (size_t)c0 * HW;
+        const int64_t cstride = p.in_plane > 0 ? p.in_plane : (int64_t)HW;
+        const float *xc = p.x + c0 * cstride;
         // 4 positions per iteration: all loads in flight before the stores
         for (int pb = tid; pb < p.HALO; pb += 4 * 128) {
           float v[4][8];
@@ -343,7 +357,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
             const int off = pos < p.HALO ? src_off[pos] : -1;
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-              v[u][j] = (off >= 0 && j < nc) ? __ldg(xc + off + (size_t)j * HW) : 0.f;
+              v[u][j] = (off >= 0 && j < nc) ? __ldg(xc + off + j * cstride) : 0.f;
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -568,8 +582,16 @@ sysml_status set_smem_attr(K kernel, size_t bytes, int &cache) {
 
 sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f_cin,
                      const float *bias, float *y, float *pout, int32_t *parg, void *ws,
-                     cudaStream_t st) {
+                     cudaStream_t st, const TcSpfIO *io = nullptr) {
   TcFwdParams p = pl.p;
+  if (io) {
+    p.in_plane = io->in_plane;
+    p.in_shift = io->in_shift;
+    p.out_plane = io->out_plane;
+    p.out_Wf = io->out_Wf;
+    p.out_Lf = io->out_Lf;
+    p.out_off = io->out_off;
+  }
   float *fp = reinterpret_cast<float *>(ws);
   {
     const int64_t total = (int64_t)p.nft * p.nchunk * p.R * p.S * 2 * p.NFpad * 4;
@@ -986,6 +1008,274 @@ TcWgPlan plan_wgrad(const ConvArgs &a) {
   return pl;
 }
 
+// =====================================================================================
+// bwd_filter on stacked-planar-frame (SPF) tensors -- the LeNet step's internal layout
+// =====================================================================================
+// SPF: tensor [C][G] with G = N * Hs * Wf stacked frame positions (Wf % 4 == 0), zeros in
+// every padding / garbage position, plane stride a multiple of 4 floats.  Every 4
+// consecutive positions are one aligned float4, so producers stream with 16-byte loads
+// and no index decoding.
+//   A rows (j, k): dY[k][g - j*Wf]              (copy j -> tap row r + j)
+//   B rows (s, c): X[c][g + s]                  (all S column taps in one MMA: N = S*C)
+//   D_rg[(j,k)][(s,c)] += A . B shifted by rg*copies*Wf  ->  dF[k][c][rg*copies + j][s]
+// One K-step (8 positions) issues RG MMAs of N = S*C instead of R*S small ones.
+struct TcWgSpfParams {
+  const float *x, *dy;   // SPF planes
+  int64_t plane_x, plane_dy;
+  int x_shift, dy_shift;  // stored position = frame position + shift
+  float *part;            // [split][RG][128][NB]
+  float *dbpart;          // [split][K] or null
+  int64_t G, Gext;
+  int K, C, R, S, Wf;
+  int Kc, copies, RG, NB;
+  int KC, HBq, nstage;
+  int splits;
+  int64_t pos_per_split;
+  uint32_t a_bytes, b_bytes, stage_bytes;
+};
+
+constexpr int WG_THREADS = 288;  // 8 producer/epilogue warps + 1 MMA warp
+
+__device__ __forceinline__ float4 ld_f4(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
+
+template <int S_>
+__global__ void __launch_bounds__(WG_THREADS, 1) tc_wgrad_spf_kernel(const TcWgSpfParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t *stage_base = smem;
+  float *dbs = reinterpret_cast<float *>(smem + (size_t)p.nstage * p.stage_bytes);  // [256]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(dbs + 256);
+  uint64_t *full = bars;
+  uint64_t *empty = bars + p.nstage;
+  uint64_t *accf = bars + 2 * p.nstage;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accf + 1);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int split = blockIdx.x;
+  const int64_t gs = (int64_t)split * p.pos_per_split;
+  const int64_t ge = min(p.Gext, gs + p.pos_per_split);
+  const int64_t span = ge > gs ? ge - gs : 0;
+  const int nchunks = (int)((span + p.KC - 1) / p.KC);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.nstage; ++s) {
+      ptx::mbar_init(full + s, 8);
+      ptx::mbar_init(empty + s, 1);
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 8) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < 8) {
+    const int tid = threadIdx.x;
+    // A task: fixed row (tid / 2) and quad half (tid % 2) of the KC/4 quads
+    const int arow = tid >> 1, ahalf = tid & 1;
+    const int aj = arow / p.Kc, ak = arow - aj * p.Kc;
+    const bool arow_ok = aj < p.copies && ak < p.K;
+    const int nq = p.KC / 4, qper = (nq + 1) / 2;
+    const float *dyk = p.dy + (arow_ok ? (int64_t)ak * p.plane_dy : 0);
+    float db_acc = 0.f;
+    // B task: channel c, group of 4 quads
+    const int ngrp = (p.HBq + 3) / 4;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int64_t u0 = gs + (int64_t)ch * p.KC;
+      ptx::mbar_wait_sleep(empty + stage, phase ^ 1);
+      const uint32_t A = ptx::smem_u32(stage_base + (size_t)stage * p.stage_bytes);
+      const uint32_t B = A + p.a_bytes;
+      // ---- A
+      {
+        float4 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int q = ahalf * qper + i;
+          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (i < qper && q < nq && arow_ok) {
+            const int64_t pos = u0 + 4 * q;          // CTA-range position of this quad
+            const int64_t src = pos - (int64_t)aj * p.Wf;
+            if (pos < ge && src >= 0 && src < p.G) v[i] = ld_f4(dyk + src + p.dy_shift);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int q = ahalf * qper + i;
+          if (i < qper && q < nq) {
+            st_shared_v4(A + (uint32_t)((q * 128 + arow) * 16), v[i].x, v[i].y, v[i].z, v[i].w);
+            if (aj == 0) db_acc += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+          }
+        }
+      }
+      // ---- B: rows (s, c) = X[c][u0 + 4q + s .. +3]
+      for (int t = tid; t < p.C * ngrp; t += 256) {
+        const int c = t / ngrp, q0 = (t - c * ngrp) * 4;
+        const float *xc = p.x + (int64_t)c * p.plane_x + p.x_shift;
+        float w[20];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          const int64_t pos = u0 + 4 * (q0 + i);
+          float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (pos < p.G) f = ld_f4(xc + pos);
+          w[4 * i] = f.x; w[4 * i + 1] = f.y; w[4 * i + 2] = f.z; w[4 * i + 3] = f.w;
+        }
+#pragma unroll
+        for (int qi = 0; qi < 4; ++qi) {
+          const int q = q0 + qi;
+          if (q < p.HBq) {
+#pragma unroll
+            for (int s_ = 0; s_ < S_; ++s_)
+              st_shared_v4(B + (uint32_t)(((q * p.NB) + s_ * p.C + c) * 16), w[4 * qi + s_],
+                           w[4 * qi + s_ + 1], w[4 * qi + s_ + 2], w[4 * qi + s_ + 3]);
+          }
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(full + stage);
+      if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+    }
+    if (p.dbpart) {
+      dbs[tid] = db_acc;
+      ptx::named_bar_sync(1, 256);
+      if (tid < p.Kc && tid < p.K) p.dbpart[(int64_t)split * p.K + tid] = dbs[2 * tid] + dbs[2 * tid + 1];
+    }
+  } else {
+    // ================= MMA warp
+    const uint32_t idesc = ptx::make_idesc_tf32(128, p.NB);
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t sbase = ptx::smem_u32(stage_base);
+    const uint32_t rg_step = (uint32_t)(p.copies * p.Wf / 4 * p.NB);  // quads x NB rows (16-B units)
+    for (int ch = 0; ch < nchunks; ++ch) {
+      ptx::mbar_wait(full + stage, phase);
+      ptx::tc_fence_after();
+      const uint32_t A = sbase + (uint32_t)stage * p.stage_bytes;
+      uint64_t adesc = ptx::make_desc(A, 128 * 16, 128);
+      uint64_t bdesc = ptx::make_desc(A + p.a_bytes, (uint32_t)p.NB * 16, 128);
+      for (int kk = 0; kk < p.KC / 8; ++kk) {
+        uint64_t bd = bdesc;
+        uint32_t tm = 0;
+        const uint32_t acc = (ch | kk) != 0 ? 1u : 0u;
+        for (int rg = 0; rg < p.RG; ++rg) {
+          if (ptx::elect_one()) ptx::mma_tf32(tm, adesc, bd, idesc, acc);
+          __syncwarp();
+          tm += (uint32_t)p.NB;
+          bd += (uint64_t)rg_step;
+        }
+        adesc += 2 * 128;                 // 2 quads of 128 rows x 16 B
+        bdesc += (uint64_t)(2 * p.NB);    // 2 quads of NB rows x 16 B
+      }
+      if (ptx::elect_one()) ptx::mma_commit(empty + stage);
+      __syncwarp();
+      if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+    }
+    if (ptx::elect_one()) ptx::mma_commit(accf);
+    __syncwarp();
+  }
+  // ================= epilogue: warps 0-7 (quadrant warp % 4, column chunk parity warp / 4)
+  if (warp < 8) {
+    ptx::mbar_wait_sleep(accf, 0);
+    __syncwarp();
+    ptx::tc_fence_after();
+    const int qd = warp & 3, half = warp >> 2;
+    const int row = qd * 32 + lane;
+    float *dst = p.part + (int64_t)split * p.RG * 128 * p.NB;
+    const int nc16 = p.NB / 16;
+    for (int rg = 0; rg < p.RG; ++rg)
+      for (int c16 = half; c16 < nc16; c16 += 2) {
+        float v[16];
+        if (nchunks > 0) {
+          ptx::tmem_ld16(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(rg * p.NB + c16 * 16), v);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        }
+        float4 *o = reinterpret_cast<float4 *>(dst + ((int64_t)rg * 128 + row) * p.NB + c16 * 16);
+        o[0] = make_float4(v[0], v[1], v[2], v[3]);
+        o[1] = make_float4(v[4], v[5], v[6], v[7]);
+        o[2] = make_float4(v[8], v[9], v[10], v[11]);
+        o[3] = make_float4(v[12], v[13], v[14], v[15]);
+      }
+    ptx::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 8) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, 512);
+  }
+}
+
+__global__ void tc_wgrad_spf_reduce_kernel(const TcWgSpfParams p, float *__restrict__ df,
+                                           float *__restrict__ db) {
+  const int RS = p.R * p.S;
+  const int64_t total = (int64_t)p.K * p.C * RS;
+  const int64_t split_stride = (int64_t)p.RG * 128 * p.NB;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i / ((int64_t)p.C * RS));
+    const int rem = (int)(i - (int64_t)k * p.C * RS);
+    const int c = rem / RS, t = rem - c * RS, r = t / p.S, s = t - r * p.S;
+    const int rg = r / p.copies, j = r - rg * p.copies;
+    const int64_t off = ((int64_t)rg * 128 + j * p.Kc + k) * p.NB + s * p.C + c;
+    float acc = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp) acc += p.part[sp * split_stride + off];
+    df[i] = acc;
+  }
+  if (db) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < p.K;
+         k += (int64_t)gridDim.x * blockDim.x) {
+      float acc = 0.f;
+      for (int sp = 0; sp < p.splits; ++sp) acc += p.dbpart[(int64_t)sp * p.K + k];
+      db[k] = acc;
+    }
+  }
+}
+
+struct TcWgSpfPlan {
+  TcWgSpfParams p;
+  size_t smem, part_bytes, dbpart_bytes;
+  bool ok;
+};
+
+TcWgSpfPlan plan_wgrad_spf(const SpfConv &sc) {
+  TcWgSpfPlan pl{};
+  TcWgSpfParams &p = pl.p;
+  pl.ok = false;
+  p.K = sc.K; p.C = sc.C; p.R = sc.R; p.S = sc.S; p.Wf = sc.Wf;
+  p.G = sc.G;
+  p.plane_x = sc.plane_x; p.plane_dy = sc.plane_dy;
+  p.x_shift = sc.x_shift; p.dy_shift = sc.dy_shift;
+  if (sc.Wf % 4 || sc.plane_x % 4 || sc.plane_dy % 4 || sc.G % 4 || sc.x_shift % 4 || sc.dy_shift % 4) return pl;
+  if (!(sc.S == 5 || sc.S == 3) || sc.K > 128) return pl;
+  p.Kc = sc.K <= 16 ? 16 : sc.K <= 32 ? 32 : sc.K <= 64 ? 64 : 128;
+  p.copies = 128 / p.Kc;
+  if (p.copies > sc.R) p.copies = std::max(1, sc.R);
+  while (128 % (p.Kc * p.copies) != 0) --p.copies;
+  p.RG = (sc.R + p.copies - 1) / p.copies;
+  p.NB = sc.S * sc.C;
+  if (p.NB % 16 || p.NB > 256 || p.RG * p.NB > 512) return pl;
+  p.Gext = p.G + (int64_t)(p.copies - 1) * p.Wf;
+  p.KC = 32;
+  p.HBq = p.KC / 4 + (p.RG - 1) * p.copies * p.Wf / 4;
+  p.a_bytes = (uint32_t)(p.KC / 4 * 128 * 16);
+  p.b_bytes = (uint32_t)(p.HBq * p.NB * 16);
+  p.stage_bytes = p.a_bytes + p.b_bytes;
+  const size_t fixed = 256 * 4 + 8 * 12 + 16;
+  p.nstage = (int)std::min<int64_t>(4, (SMEM_BUDGET - (int64_t)fixed) / p.stage_bytes);
+  if (p.nstage < 2) return pl;
+  pl.smem = (size_t)p.nstage * p.stage_bytes + fixed;
+  const int64_t target = 2ll * sm_count();
+  int64_t splits = std::min<int64_t>(target, std::max<int64_t>(1, ceil_div(p.Gext, 8 * p.KC)));
+  p.pos_per_split = align_up((size_t)ceil_div(p.Gext, splits), (size_t)p.KC);
+  p.splits = (int)ceil_div(p.Gext, p.pos_per_split);
+  pl.part_bytes = align_up((size_t)p.splits * p.RG * 128 * p.NB * sizeof(float), 256);
+  pl.dbpart_bytes = align_up((size_t)p.splits * p.K * sizeof(float), 256);
+  pl.ok = true;
+  return pl;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ forward (K3)
@@ -1040,6 +1330,67 @@ sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy
   }
   // filter bank F is (K x C*RS) = (Cin_of_this_conv x Kout*RS) -> flip = 1
   return run_fwd(pl, dy, f, 1, a.K, nullptr, dx, nullptr, nullptr, ws, st);
+}
+
+// ------------------------------------------------------------------ SPF-layout entry points
+sysml_status tc_conv_fwd_spf(const ConvArgs &a, const TcSpfIO &io, const float *x, const float *f,
+                             const float *bias, float *y, const PoolArgs *pool, float *pout,
+                             int32_t *parg, void *ws, cudaStream_t st) {
+  TcPlan pl = plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool);
+  if (!pl.ok || a.sh != 1 || a.sw != 1) {
+    set_error("tcgen05 SPF forward: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  return run_fwd(pl, x, f, 0, a.C, bias, pool ? nullptr : y, pout, parg, ws, st, &io);
+}
+
+sysml_status tc_conv_bwd_data_spf(const ConvArgs &a, const TcSpfIO &io, const float *f,
+                                  const float *dy, float *dx, void *ws, cudaStream_t st) {
+  if (!tc_bwd_data_supported(a)) {
+    set_error("tcgen05 SPF bwd_data: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  TcPlan pl = plan_bwd_data(a);
+  return run_fwd(pl, dy, f, 1, a.K, nullptr, dx, nullptr, nullptr, ws, st, &io);
+}
+
+// ------------------------------------------------------------------ bwd_filter on SPF
+bool tc_wgrad_spf_supported(const SpfConv &sc) {
+  return device_cc_major() == 10 && plan_wgrad_spf(sc).ok;
+}
+
+size_t tc_wgrad_spf_ws(const SpfConv &sc) {
+  TcWgSpfPlan pl = plan_wgrad_spf(sc);
+  return pl.ok ? pl.part_bytes + pl.dbpart_bytes : 0;
+}
+
+sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy_spf, float *df,
+                          float *db, void *ws, cudaStream_t st) {
+  TcWgSpfPlan pl = plan_wgrad_spf(sc);
+  if (!pl.ok) {
+    set_error("tcgen05 SPF bwd_filter: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  TcWgSpfParams p = pl.p;
+  p.x = x_spf;
+  p.dy = dy_spf;
+  p.part = reinterpret_cast<float *>(ws);
+  p.dbpart = db ? reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + pl.part_bytes) : nullptr;
+  if (p.S == 5) {
+    static int attr = 0;
+    SYSML_TRY(set_smem_attr(tc_wgrad_spf_kernel<5>, pl.smem, attr));
+    tc_wgrad_spf_kernel<5><<<p.splits, WG_THREADS, pl.smem, st>>>(p);
+  } else {
+    static int attr = 0;
+    SYSML_TRY(set_smem_attr(tc_wgrad_spf_kernel<3>, pl.smem, attr));
+    tc_wgrad_spf_kernel<3><<<p.splits, WG_THREADS, pl.smem, st>>>(p);
+  }
+  SYSML_LAUNCH_CHECK();
+  const int64_t total = (int64_t)p.K * p.C * p.R * p.S;
+  const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 8 * sm_count());
+  tc_wgrad_spf_reduce_kernel<<<blocks, 256, 0, st>>>(p, df, db);
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
 }
 
 // ------------------------------------------------------------------ bwd_filter (K5)

@@ -32,6 +32,8 @@ struct FusedB1Args {
   int Hp, Wp;                                   // padded image in smem
   int tpk;                                      // threads per filter
   int n_per_cta;
+  int64_t mask_plane;                           // > 0: mask is SPF [K][mask_plane]
+  int mask_Wf, mask_Lf, mask_off;
 };
 
 template <int R_, int S_>
@@ -77,7 +79,15 @@ __global__ void __launch_bounds__(FB_THREADS)
     const int64_t base = (int64_t)n * a.K * PpQp + (int64_t)k * PpQp;
     for (int pp = j; pp < PpQp; pp += a.tpk) {
       const float g0 = __ldg(dpool + base + pp);
-      if (mask && !(__ldg(mask + base + pp) > 0.f)) continue;
+      if (mask) {
+        int64_t mi = base + pp;
+        if (a.mask_plane > 0) {
+          const int pr = pp / a.Qp, pc = pp - pr * a.Qp;
+          mi = (int64_t)k * a.mask_plane + (int64_t)n * a.mask_Lf + (pr + a.mask_off) * a.mask_Wf +
+               pc + a.mask_off;
+        }
+        if (!(__ldg(mask + mi) > 0.f)) continue;
+      }
       if (g0 == 0.f) continue;
       const int am = __ldg(argmax + base + pp) - k * PQ;  // position inside plane k
       if (am < 0 || am >= PQ) continue;
@@ -142,8 +152,14 @@ size_t fused_pool_bwd_wgrad_ws(const ConvArgs &c) {
 sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const float *x,
                                   const sysml_csr *xcsr, const float *dpool,
                                   const int32_t *argmax, const float *mask, float *df, float *db,
-                                  void *ws, cudaStream_t st) {
+                                  void *ws, cudaStream_t st, const TcSpfIO *mask_spf) {
   FusedB1Args a{};
+  if (mask_spf) {
+    a.mask_plane = mask_spf->out_plane;
+    a.mask_Wf = mask_spf->out_Wf;
+    a.mask_Lf = mask_spf->out_Lf;
+    a.mask_off = mask_spf->out_off;
+  }
   a.N = c.N; a.H = c.H; a.W = c.W; a.K = c.K; a.R = c.R; a.S = c.S; a.ph = c.ph; a.pw = c.pw;
   a.P = c.P; a.Q = c.Q; a.Pp = pa.P; a.Qp = pa.Q;
   a.Hp = c.H + 2 * c.ph;

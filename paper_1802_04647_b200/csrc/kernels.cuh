@@ -55,6 +55,22 @@ sysml_status csr_conv_bwd_filter(const ConvArgs &a, const sysml_csr &x, const fl
 sysml_status csr_densify(const sysml_csr &x, float *dense, cudaStream_t st);
 sysml_status csr_check(const sysml_csr &m, int64_t *violations, cudaStream_t st);
 
+// Stacked planar frame (SPF) conv geometry: tensors [C][G] (x) and [K][G] (dy) with
+// G = N*Hs*Wf frame positions; stored position = frame position + shift.
+struct SpfConv {
+  int K, C, R, S, Wf;
+  int64_t G, plane_x, plane_dy;
+  int x_shift, dy_shift;
+};
+
+// SPF input / pooled-output options of the tcgen05 forward kernel (LeNet-internal layout)
+struct TcSpfIO {
+  int64_t in_plane = 0;  // > 0: input SPF, channel stride in_plane, stored pos = frame pos + in_shift
+  int in_shift = 0;
+  int64_t out_plane = 0;  // > 0: pooled output to SPF planes (pp + out_off) * out_Wf + pc + out_off
+  int out_Wf = 0, out_Lf = 0, out_off = 0;
+};
+
 // conv_tc.cu : tcgen05 TF32 implicit GEMM (SYSML_MATH_TF32)
 
 bool tc_fwd_supported(const ConvArgs &a, const PoolArgs *pool);
@@ -66,6 +82,15 @@ bool tc_bwd_data_supported(const ConvArgs &a);
 size_t tc_bwd_data_ws(const ConvArgs &a);
 sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
                               void *ws, cudaStream_t st);
+sysml_status tc_conv_fwd_spf(const ConvArgs &a, const TcSpfIO &io, const float *x, const float *f,
+                             const float *bias, float *y, const PoolArgs *pool, float *pout,
+                             int32_t *parg, void *ws, cudaStream_t st);
+sysml_status tc_conv_bwd_data_spf(const ConvArgs &a, const TcSpfIO &io, const float *f,
+                                  const float *dy, float *dx, void *ws, cudaStream_t st);
+bool tc_wgrad_spf_supported(const SpfConv &sc);
+size_t tc_wgrad_spf_ws(const SpfConv &sc);
+sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy_spf, float *df,
+                          float *db, void *ws, cudaStream_t st);
 bool tc_bwd_filter_supported(const ConvArgs &a);
 size_t tc_bwd_filter_ws(const ConvArgs &a);
 sysml_status tc_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,
@@ -77,6 +102,16 @@ size_t fused_pool_bwd_wgrad_ws(const ConvArgs &c);
 sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const float *x,
                                   const sysml_csr *xcsr, const float *dpool,
                                   const int32_t *argmax, const float *mask, float *df, float *db,
-                                  void *ws, cudaStream_t st);
+                                  void *ws, cudaStream_t st, const TcSpfIO *mask_spf = nullptr);
+
+// pool.cu : LeNet-internal layout helpers
+// maxpool_bwd (non-overlapping windows) writing the unpooled gradient into SPF planes
+// [C][plane], position n*Lf + h*Wf + w (only the window positions are written).
+sysml_status launch_maxpool_bwd_spf(const PoolArgs &a, const int32_t *argmax, const float *dout,
+                                    const float *mask, float *dx_spf, int64_t plane, int Wf,
+                                    int Lf, cudaStream_t st);
+// NCHW (N x C*H*W) -> SPF planes [C][plane] at n*Lf + (h+off)*Wf + (w+off)
+sysml_status launch_nchw_to_spf(int N, int C, int H, int W, const float *x, float *spf,
+                                int64_t plane, int Wf, int Lf, int off, cudaStream_t st);
 
 }  // namespace sysml

@@ -229,6 +229,11 @@ struct sysml_lenet {
   int launches = 0;
   int dw3_chunks = 1;
   bool fused_b1 = false;  // maxpool_bwd1 + conv1 bwd_filter in one kernel (fused_bwd.cu)
+  // TF32 path: a1 and dz2 live in the stacked planar frame layout (SPF, 16x16 frames,
+  // zero padding stored) so the tcgen05 producers stream aligned float4s
+  bool spf = false;
+  int64_t spf_plane = 0;
+  float *a1s = nullptr, *dz2s = nullptr;
 };
 
 namespace {
@@ -343,6 +348,31 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
     h->fused_b1 = fused_pool_bwd_wgrad_supported(conv_args(g1), pool_args(gp1, 1));
     if (h->fused_b1) need = std::max(need, fused_pool_bwd_wgrad_ws(conv_args(g1)));
   }
+  if (math == SYSML_MATH_TF32 && h->fused_b1) {
+    ConvGeom g1, g2, gp1, gp2;
+    validate_conv(&c1, &g1); validate_conv(&c2, &g2);
+    validate_pool(&p1, &gp1); validate_pool(&p2, &gp2);
+    const ConvArgs a1a = conv_args(g1), a2a = conv_args(g2);
+    const PoolArgs pa1 = pool_args(gp1, 1), pa2 = pool_args(gp2, 1);
+    SpfConv sc{64, 32, 5, 5, 16, (int64_t)max_local_batch * 256, (int64_t)max_local_batch * 256,
+               (int64_t)max_local_batch * 256, 0, 0};
+    h->spf = (h->csr || tc_fwd_supported(a1a, &pa1)) && tc_fwd_supported(a2a, &pa2) &&
+             tc_bwd_data_supported(a2a) && tc_wgrad_spf_supported(sc);
+    if (h->spf) {
+      h->spf_plane = (int64_t)max_local_batch * 256;
+      need = std::max(need, tc_fwd_ws(a1a));
+      need = std::max(need, tc_fwd_ws(a2a));
+      need = std::max(need, tc_bwd_data_ws(a2a));
+      need = std::max(need, tc_wgrad_spf_ws(sc));
+      ALLOC(h->a1s, 32 * h->spf_plane);
+      ALLOC(h->dz2s, 64 * h->spf_plane);
+      if (cudaMemset(h->a1s, 0, sizeof(float) * 32 * h->spf_plane) != cudaSuccess ||
+          cudaMemset(h->dz2s, 0, sizeof(float) * 64 * h->spf_plane) != cudaSuccess) {
+        set_error("cudaMemset of the SPF activation buffers failed");
+        return fail(SYSML_ERR_CUDA);
+      }
+    }
+  }
   h->ws_bytes = need;
   if (need) {
     cudaError_t e = cudaMalloc(&h->ws, need);
@@ -362,6 +392,7 @@ sysml_status sysml_lenet_destroy(sysml_lenet *h) {
   cudaFree(h->lossn); cudaFree(h->da2); cudaFree(h->dz2); cudaFree(h->da1); cudaFree(h->dz1);
   cudaFree(h->part3); cudaFree(h->loss_dev); cudaFree(h->lab_dev); cudaFree(h->x_dev);
   cudaFree(h->ws);
+  cudaFree(h->a1s); cudaFree(h->dz2s);
   for (auto &e : h->pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (int i = 0; i < NSTAGES; ++i)
     for (auto &e : h->pending[i]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -394,16 +425,44 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
   StageTimer T(h, st);
   int launches0 = 0;
 
+  ConvGeom g1, g2, gp1, gp2;
+  SYSML_TRY(validate_conv(&c1, &g1));
+  SYSML_TRY(validate_conv(&c2, &g2));
+  SYSML_TRY(validate_pool(&p1, &gp1));
+  SYSML_TRY(validate_pool(&p2, &gp2));
+  const ConvArgs ca1 = conv_args(g1), ca2 = conv_args(g2);
+  const PoolArgs pa1 = pool_args(gp1, 1), pa2 = pool_args(gp2, 1);
+  // SPF geometry of conv2's 14x14 planes: 16x16 frames (pad 2 stored as zeros)
+  TcSpfIO a1_io;  // a1 written / read in conv2's input-frame convention
+  a1_io.out_plane = h->spf_plane;
+  a1_io.out_Wf = 16;
+  a1_io.out_Lf = 256;
+  a1_io.out_off = 2;
+  sysml_input a1in{0, h->a1, {}};
   // F1
   SYSML_TRY(T.begin(0));
-  SYSML_TRY(conv_fwd_dispatch(c1, *x, params + OFF_F1, params + OFF_B1, nullptr, &p1, h->a1, h->i1,
-                              h->ws, h->ws_bytes, st));
+  if (h->spf && !x->is_csr) {
+    SYSML_TRY(tc_conv_fwd_spf(ca1, a1_io, x->dense, params + OFF_F1, params + OFF_B1, nullptr, &pa1,
+                              h->a1s, h->i1, h->ws, st));
+  } else {
+    SYSML_TRY(conv_fwd_dispatch(c1, *x, params + OFF_F1, params + OFF_B1, nullptr, &p1, h->a1, h->i1,
+                                h->ws, h->ws_bytes, st));
+    if (h->spf)
+      SYSML_TRY(launch_nchw_to_spf(n, 32, 14, 14, h->a1, h->a1s, h->spf_plane, 16, 256, 2, st));
+  }
   SYSML_TRY(T.end());
   // F2
   SYSML_TRY(T.begin(1));
-  sysml_input a1in{0, h->a1, {}};
-  SYSML_TRY(conv_fwd_dispatch(c2, a1in, params + OFF_F2, params + OFF_B2, nullptr, &p2, h->a2,
-                              h->i2, h->ws, h->ws_bytes, st));
+  if (h->spf) {
+    TcSpfIO io;
+    io.in_plane = h->spf_plane;
+    io.in_shift = 0;
+    SYSML_TRY(tc_conv_fwd_spf(ca2, io, h->a1s, params + OFF_F2, params + OFF_B2, nullptr, &pa2, h->a2,
+                              h->i2, h->ws, st));
+  } else {
+    SYSML_TRY(conv_fwd_dispatch(c2, a1in, params + OFF_F2, params + OFF_B2, nullptr, &p2, h->a2,
+                                h->i2, h->ws, h->ws_bytes, st));
+  }
   SYSML_TRY(T.end());
   // F3
   SYSML_TRY(T.begin(2));
@@ -433,41 +492,50 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     SYSML_LAUNCH_CHECK();
   }
   SYSML_TRY(T.end());
-  // B2p
-  SYSML_TRY(T.begin(4));
-  {
-    ConvGeom g;
-    SYSML_TRY(validate_pool(&p2, &g));
-    SYSML_TRY(launch_maxpool_bwd(pool_args(g, 1), h->i2, h->da2, h->a2, h->dz2, st));
+  if (h->spf) {
+    // B2p: unpooled gradient straight into the SPF planes (output-frame convention)
+    SYSML_TRY(T.begin(4));
+    SYSML_TRY(launch_maxpool_bwd_spf(pa2, h->i2, h->da2, h->a2, h->dz2s, h->spf_plane, 16, 256, st));
+    SYSML_TRY(T.end());
+    // B2f
+    SYSML_TRY(T.begin(5));
+    SpfConv sc{64, 32, 5, 5, 16, (int64_t)n * 256, h->spf_plane, h->spf_plane, 0, 0};
+    SYSML_TRY(tc_wgrad_spf(sc, h->a1s, h->dz2s, grads + OFF_F2, grads + OFF_B2, h->ws, st));
+    SYSML_TRY(T.end());
+    // B2d: input frame (pad 2) position = stored output-frame position + 34
+    SYSML_TRY(T.begin(6));
+    TcSpfIO io;
+    io.in_plane = h->spf_plane;
+    io.in_shift = -(2 * 16 + 2);
+    SYSML_TRY(tc_conv_bwd_data_spf(ca2, io, params + OFF_F2, h->dz2s, h->da1, h->ws, st));
+    SYSML_TRY(T.end());
+  } else {
+    // B2p
+    SYSML_TRY(T.begin(4));
+    SYSML_TRY(launch_maxpool_bwd(pa2, h->i2, h->da2, h->a2, h->dz2, st));
+    SYSML_TRY(T.end());
+    // B2f
+    SYSML_TRY(T.begin(5));
+    SYSML_TRY(conv_bwd_filter_dispatch(c2, a1in, h->dz2, grads + OFF_F2, grads + OFF_B2, h->ws,
+                                       h->ws_bytes, st));
+    SYSML_TRY(T.end());
+    // B2d
+    SYSML_TRY(T.begin(6));
+    SYSML_TRY(conv_bwd_data_dispatch(c2, params + OFF_F2, h->dz2, h->da1, h->ws, h->ws_bytes, st));
+    SYSML_TRY(T.end());
   }
-  SYSML_TRY(T.end());
-  // B2f
-  SYSML_TRY(T.begin(5));
-  SYSML_TRY(conv_bwd_filter_dispatch(c2, a1in, h->dz2, grads + OFF_F2, grads + OFF_B2, h->ws,
-                                     h->ws_bytes, st));
-  SYSML_TRY(T.end());
-  // B2d
-  SYSML_TRY(T.begin(6));
-  SYSML_TRY(conv_bwd_data_dispatch(c2, params + OFF_F2, h->dz2, h->da1, h->ws, h->ws_bytes, st));
-  SYSML_TRY(T.end());
   if (h->fused_b1) {
     // B1 fused: conv1 bwd_filter of maxpool_bwd(i1, da1, a1 > 0) without materialising dz1
     SYSML_TRY(T.begin(9));
-    ConvGeom g1, gp1;
-    SYSML_TRY(validate_conv(&c1, &g1));
-    SYSML_TRY(validate_pool(&p1, &gp1));
-    SYSML_TRY(fused_pool_bwd_wgrad(conv_args(g1), pool_args(gp1, 1), x->is_csr ? nullptr : x->dense,
-                                   x->is_csr ? &x->csr : nullptr, h->da1, h->i1, h->a1,
-                                   grads + OFF_F1, grads + OFF_B1, h->ws, st));
+    SYSML_TRY(fused_pool_bwd_wgrad(ca1, pa1, x->is_csr ? nullptr : x->dense,
+                                   x->is_csr ? &x->csr : nullptr, h->da1, h->i1,
+                                   h->spf ? h->a1s : h->a1, grads + OFF_F1, grads + OFF_B1, h->ws,
+                                   st, h->spf ? &a1_io : nullptr));
     SYSML_TRY(T.end());
   } else {
     // B1p
     SYSML_TRY(T.begin(7));
-    {
-      ConvGeom g;
-      SYSML_TRY(validate_pool(&p1, &g));
-      SYSML_TRY(launch_maxpool_bwd(pool_args(g, 1), h->i1, h->da1, h->a1, h->dz1, st));
-    }
+    SYSML_TRY(launch_maxpool_bwd(pa1, h->i1, h->da1, h->a1, h->dz1, st));
     SYSML_TRY(T.end());
     // B1f
     SYSML_TRY(T.begin(8));

@@ -139,6 +139,52 @@ __global__ void bias_add_kernel(int32_t N, int32_t K, int32_t PQ, float *__restr
   }
 }
 
+// maxpool_bwd to SPF: one thread per pooled output writes its whole (disjoint) window.
+__global__ void maxpool_bwd_spf_kernel(PoolArgs a, const int32_t *__restrict__ argmax,
+                                       const float *__restrict__ dout,
+                                       const float *__restrict__ mask, float *__restrict__ dx,
+                                       int64_t plane, int Wf, int Lf) {
+  const int64_t total = (int64_t)a.N * a.C * a.P * a.Q;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(o % a.Q);
+    int64_t t = o / a.Q;
+    const int p = (int)(t % a.P);
+    t /= a.P;
+    const int c = (int)(t % a.C);
+    const int n = (int)(t / a.C);
+    const int am = __ldg(argmax + o);
+    float g = __ldg(dout + o);
+    if (mask && !(__ldg(mask + o) > 0.f)) g = 0.f;
+    float *dxp = dx + (int64_t)c * plane + (int64_t)n * Lf;
+    for (int r = 0; r < a.R; ++r) {
+      const int h = p * a.R + r;
+      if (h >= a.H) break;
+      for (int s = 0; s < a.S; ++s) {
+        const int w = q * a.S + s;
+        if (w >= a.W) break;
+        const int col = (c * a.H + h) * a.W + w;
+        dxp[h * Wf + w] = (col == am) ? g : 0.f;
+      }
+    }
+  }
+}
+
+__global__ void nchw_to_spf_kernel(int N, int C, int H, int W, const float *__restrict__ x,
+                                   float *__restrict__ spf, int64_t plane, int Wf, int Lf, int off) {
+  const int64_t total = (int64_t)N * C * H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int w = (int)(i % W);
+    int64_t t = i / W;
+    const int h = (int)(t % H);
+    t /= H;
+    const int c = (int)(t % C);
+    const int n = (int)(t / C);
+    spf[(int64_t)c * plane + (int64_t)n * Lf + (h + off) * Wf + (w + off)] = __ldg(x + i);
+  }
+}
+
 static inline int grid_for(int64_t total, int threads) {
   int64_t b = ceil_div(total, threads);
   int64_t cap = (int64_t)sm_count() * 16;
@@ -180,6 +226,24 @@ sysml_status launch_bias_add(int32_t N, int32_t K, int32_t PQ, float *y, const f
                              cudaStream_t st) {
   const int64_t total = (int64_t)N * K * PQ;
   bias_add_kernel<<<grid_for(total, 256), 256, 0, st>>>(N, K, PQ, y, bias);
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
+}
+
+sysml_status launch_maxpool_bwd_spf(const PoolArgs &a, const int32_t *argmax, const float *dout,
+                                    const float *mask, float *dx_spf, int64_t plane, int Wf,
+                                    int Lf, cudaStream_t st) {
+  const int64_t total = (int64_t)a.N * a.C * a.P * a.Q;
+  maxpool_bwd_spf_kernel<<<grid_for(total, 256), 256, 0, st>>>(a, argmax, dout, mask, dx_spf, plane,
+                                                               Wf, Lf);
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
+}
+
+sysml_status launch_nchw_to_spf(int N, int C, int H, int W, const float *x, float *spf,
+                                int64_t plane, int Wf, int Lf, int off, cudaStream_t st) {
+  const int64_t total = (int64_t)N * C * H * W;
+  nchw_to_spf_kernel<<<grid_for(total, 256), 256, 0, st>>>(N, C, H, W, x, spf, plane, Wf, Lf, off);
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;
 }
