@@ -279,17 +279,13 @@ def ours_arm(args, world, rank, local):
     params = torch.from_numpy(synth.lenet_params(seed=(6,))).cuda()
     grads = torch.empty_like(params)
     loss = torch.empty(1, device="cuda")
-    net = S.LeNet(b, math=math)
-    comm = None
-    if world > 1:
-        t = torch.ones(1, device="cuda")
-        dist.all_reduce(t)  # creates the NCCL communicator
-        comm = S.nccl_comm_ptr()
+    from paper_1802_04647_b200.dp import DataParallelLeNet
+    dp = DataParallelLeNet(GLOBAL_BATCH, math=math)  # rank r: rows [r*b, (r+1)*b)
+    net, comm = dp.net, dp.comm
     st = torch.cuda.current_stream()
 
     def step(i):
-        net.step(params, grads, xs[i % ROTATE], ys[i % ROTATE], GLOBAL_BATCH, lr=0.01,
-                 nccl_comm=comm, loss_sum=loss)
+        dp.step(params, grads, xs[i % ROTATE], ys[i % ROTATE], lr=0.01, loss_sum=loss)
 
     for i in range(args.warmup):
         step(i)
@@ -386,6 +382,8 @@ def ours_arm(args, world, rank, local):
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": b * 784 * 4 + b * 4,
                 "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches),
+        "allreduce": ("in-library ncclAllReduce (torch ProcessGroupNCCL communicator)" if dp.use_lib_nccl
+                      else ("torch.distributed.all_reduce" if world > 1 else "none (1 GPU)")),
         "clocks": clocks,
         "roofline": roof,
         "stages": stage_rows,

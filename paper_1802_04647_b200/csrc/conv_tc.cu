@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       ptx::named_bar_sync(1, 128);
       for (int ch = 0; ch < p.nchunk; ++ch) {
         const long long t_e0 = clock64();
-        ptx::mbar_wait_sleep(empty + stage, phase ^ 1);
+        ptx::mbar_wait(empty + stage, phase ^ 1);
         const long long t_f0 = clock64();
         if (p.clk && tid == 0) p.clk[blockIdx.x * 8 + 0] += t_f0 - t_e0;
         uint8_t *A = stage_base + (size_t)stage * p.stage_bytes;
@@ -1032,6 +1032,7 @@ struct TcWgSpfParams {
   int splits;
   int64_t pos_per_split;
   uint32_t a_bytes, b_bytes, stage_bytes;
+  long long *clk;  // optional per-CTA cycle counters (SYSML_TC_PROFILE)
 };
 
 constexpr int WG_THREADS = 288;  // 8 producer/epilogue warps + 1 MMA warp
@@ -1074,68 +1075,97 @@ __global__ void __launch_bounds__(WG_THREADS, 1) tc_wgrad_spf_kernel(const TcWgS
     const int arow = tid >> 1, ahalf = tid & 1;
     const int aj = arow / p.Kc, ak = arow - aj * p.Kc;
     const bool arow_ok = aj < p.copies && ak < p.K;
-    const int nq = p.KC / 4, qper = (nq + 1) / 2;
+    const int nq = p.KC / 4, qper = (nq + 1) / 2;  // KC <= 32: at most 4 quads per half
     const float *dyk = p.dy + (arow_ok ? (int64_t)ak * p.plane_dy : 0);
     float db_acc = 0.f;
     // B task: channel c, group of 4 quads
     const int ngrp = (p.HBq + 3) / 4;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int ch = 0; ch < nchunks; ++ch) {
+    const int ntask = p.C * ngrp;
+    struct Regs {
+      float4 va[4];
+      float vb[2][20];
+    };
+    // global -> registers for chunk ch (A: 4 float4, B: up to 2 x 5 float4)
+    auto load = [&](int ch, Regs &R) {
       const int64_t u0 = gs + (int64_t)ch * p.KC;
-      ptx::mbar_wait_sleep(empty + stage, phase ^ 1);
-      const uint32_t A = ptx::smem_u32(stage_base + (size_t)stage * p.stage_bytes);
-      const uint32_t B = A + p.a_bytes;
-      // ---- A
-      {
-        float4 v[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int q = ahalf * qper + i;
-          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (i < qper && q < nq && arow_ok) {
-            const int64_t pos = u0 + 4 * q;          // CTA-range position of this quad
-            const int64_t src = pos - (int64_t)aj * p.Wf;
-            if (pos < ge && src >= 0 && src < p.G) v[i] = ld_f4(dyk + src + p.dy_shift);
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int q = ahalf * qper + i;
-          if (i < qper && q < nq) {
-            st_shared_v4(A + (uint32_t)((q * 128 + arow) * 16), v[i].x, v[i].y, v[i].z, v[i].w);
-            if (aj == 0) db_acc += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-          }
+      for (int i = 0; i < 4; ++i) {
+        const int q = ahalf * qper + i;
+        R.va[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < qper && q < nq && arow_ok) {
+          const int64_t pos = u0 + 4 * q;          // CTA-range position of this quad
+          const int64_t src = pos - (int64_t)aj * p.Wf;
+          if (pos < ge && src >= 0 && src < p.G) R.va[i] = ld_f4(dyk + src + p.dy_shift);
         }
       }
-      // ---- B: rows (s, c) = X[c][u0 + 4q + s .. +3]
-      for (int t = tid; t < p.C * ngrp; t += 256) {
-        const int c = t / ngrp, q0 = (t - c * ngrp) * 4;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int t = tid + u * 256;
+        const int c = t % p.C, q0 = (t / p.C) * 4;
         const float *xc = p.x + (int64_t)c * p.plane_x + p.x_shift;
-        float w[20];
 #pragma unroll
         for (int i = 0; i < 5; ++i) {
           const int64_t pos = u0 + 4 * (q0 + i);
           float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (pos < p.G) f = ld_f4(xc + pos);
-          w[4 * i] = f.x; w[4 * i + 1] = f.y; w[4 * i + 2] = f.z; w[4 * i + 3] = f.w;
+          if (t < ntask && q0 + i < p.HBq + 1 && pos < p.G) f = ld_f4(xc + pos);
+          R.vb[u][4 * i] = f.x; R.vb[u][4 * i + 1] = f.y; R.vb[u][4 * i + 2] = f.z; R.vb[u][4 * i + 3] = f.w;
         }
+      }
+    };
+    // registers -> the stage's shared-memory operands (A rows (j,k); B rows (s,c) with
+    // lanes on consecutive channels: conflict-free 16-byte stores)
+    auto store = [&](const Regs &R, uint32_t A, uint32_t B) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int q = ahalf * qper + i;
+        if (i < qper && q < nq) {
+          st_shared_v4(A + (uint32_t)((q * 128 + arow) * 16), R.va[i].x, R.va[i].y, R.va[i].z, R.va[i].w);
+          if (aj == 0) db_acc += (R.va[i].x + R.va[i].y) + (R.va[i].z + R.va[i].w);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int t = tid + u * 256;
+        if (t >= ntask) continue;
+        const int c = t % p.C, q0 = (t / p.C) * 4;
 #pragma unroll
         for (int qi = 0; qi < 4; ++qi) {
           const int q = q0 + qi;
           if (q < p.HBq) {
 #pragma unroll
             for (int s_ = 0; s_ < S_; ++s_)
-              st_shared_v4(B + (uint32_t)(((q * p.NB) + s_ * p.C + c) * 16), w[4 * qi + s_],
-                           w[4 * qi + s_ + 1], w[4 * qi + s_ + 2], w[4 * qi + s_ + 3]);
+              st_shared_v4(B + (uint32_t)(((q * p.NB) + s_ * p.C + c) * 16), R.vb[u][4 * qi + s_],
+                           R.vb[u][4 * qi + s_ + 1], R.vb[u][4 * qi + s_ + 2], R.vb[u][4 * qi + s_ + 3]);
           }
         }
       }
+    };
+    int stage = 0;
+    uint32_t phase = 0;
+    auto publish = [&](const Regs &R) {
+      const long long t0 = clock64();
+      ptx::mbar_wait(empty + stage, phase ^ 1);
+      if (p.clk && tid == 0) p.clk[blockIdx.x * 8 + 0] += clock64() - t0;
+      const uint32_t A = ptx::smem_u32(stage_base + (size_t)stage * p.stage_bytes);
+      store(R, A, A + p.a_bytes);
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(full + stage);
       if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+    };
+    // software pipeline: the loads of chunk ch+1 are in flight while chunk ch is stored
+    Regs R0, R1;
+    const long long tp0 = clock64();
+    if (nchunks > 0) load(0, R0);
+    for (int ch = 0; ch < nchunks; ch += 2) {
+      if (ch + 1 < nchunks) load(ch + 1, R1);
+      publish(R0);
+      if (ch + 1 < nchunks) {
+        if (ch + 2 < nchunks) load(ch + 2, R0);
+        publish(R1);
+      }
     }
+    if (p.clk && tid == 0) p.clk[blockIdx.x * 8 + 1] = clock64() - tp0;
     if (p.dbpart) {
       dbs[tid] = db_acc;
       ptx::named_bar_sync(1, 256);
@@ -1148,8 +1178,11 @@ __global__ void __launch_bounds__(WG_THREADS, 1) tc_wgrad_spf_kernel(const TcWgS
     uint32_t phase = 0;
     const uint32_t sbase = ptx::smem_u32(stage_base);
     const uint32_t rg_step = (uint32_t)(p.copies * p.Wf / 4 * p.NB);  // quads x NB rows (16-B units)
+    const long long tm0 = clock64();
     for (int ch = 0; ch < nchunks; ++ch) {
+      const long long tw = clock64();
       ptx::mbar_wait(full + stage, phase);
+      if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 2] += clock64() - tw;
       ptx::tc_fence_after();
       const uint32_t A = sbase + (uint32_t)stage * p.stage_bytes;
       uint64_t adesc = ptx::make_desc(A, 128 * 16, 128);
@@ -1173,6 +1206,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) tc_wgrad_spf_kernel(const TcWgS
     }
     if (ptx::elect_one()) ptx::mma_commit(accf);
     __syncwarp();
+    if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 3] = clock64() - tm0;
   }
   // ================= epilogue: warps 0-7 (quadrant warp % 4, column chunk parity warp / 4)
   if (warp < 8) {
@@ -1262,6 +1296,7 @@ TcWgSpfPlan plan_wgrad_spf(const SpfConv &sc) {
   p.a_bytes = (uint32_t)(p.KC / 4 * 128 * 16);
   p.b_bytes = (uint32_t)(p.HBq * p.NB * 16);
   p.stage_bytes = p.a_bytes + p.b_bytes;
+  if ((int64_t)sc.C * ((p.HBq + 3) / 4) > 512) return pl;  // producer B tasks: <= 2 per thread
   const size_t fixed = 256 * 4 + 8 * 12 + 16;
   p.nstage = (int)std::min<int64_t>(4, (SMEM_BUDGET - (int64_t)fixed) / p.stage_bytes);
   if (p.nstage < 2) return pl;
@@ -1376,6 +1411,14 @@ sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy
   p.dy = dy_spf;
   p.part = reinterpret_cast<float *>(ws);
   p.dbpart = db ? reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + pl.part_bytes) : nullptr;
+  static long long *dclk = nullptr;
+  const bool prof = getenv("SYSML_TC_PROFILE") != nullptr;
+  p.clk = nullptr;
+  if (prof) {
+    if (!dclk) cudaMalloc(&dclk, sizeof(long long) * 8 * 4096);
+    cudaMemsetAsync(dclk, 0, sizeof(long long) * 8 * 4096, st);
+    p.clk = dclk;
+  }
   if (p.S == 5) {
     static int attr = 0;
     SYSML_TRY(set_smem_attr(tc_wgrad_spf_kernel<5>, pl.smem, attr));
@@ -1386,6 +1429,16 @@ sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy
     tc_wgrad_spf_kernel<3><<<p.splits, WG_THREADS, pl.smem, st>>>(p);
   }
   SYSML_LAUNCH_CHECK();
+  if (prof) {
+    static long long h[8 * 4096];
+    cudaMemcpyAsync(h, dclk, sizeof(long long) * 8 * p.splits, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double a[8] = {0};
+    for (int b = 0; b < p.splits; ++b)
+      for (int j = 0; j < 8; ++j) a[j] += (double)h[b * 8 + j] / p.splits;
+    fprintf(stderr, "[tc_wgrad_spf splits=%d nstage=%d KC=%d] prod_wait_empty %.0f prod_total %.0f "
+            "mma_wait_full %.0f mma_total %.0f\n", p.splits, p.nstage, p.KC, a[0], a[1], a[2], a[3]);
+  }
   const int64_t total = (int64_t)p.K * p.C * p.R * p.S;
   const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 8 * sm_count());
   tc_wgrad_spf_reduce_kernel<<<blocks, 256, 0, st>>>(p, df, db);

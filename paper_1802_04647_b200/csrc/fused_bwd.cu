@@ -77,27 +77,42 @@ __global__ void __launch_bounds__(FB_THREADS)
     __syncthreads();
     if (!kok) continue;
     const int64_t base = (int64_t)n * a.K * PpQp + (int64_t)k * PpQp;
-    for (int pp = j; pp < PpQp; pp += a.tpk) {
-      const float g0 = __ldg(dpool + base + pp);
-      if (mask) {
-        int64_t mi = base + pp;
-        if (a.mask_plane > 0) {
-          const int pr = pp / a.Qp, pc = pp - pr * a.Qp;
-          mi = (int64_t)k * a.mask_plane + (int64_t)n * a.mask_Lf + (pr + a.mask_off) * a.mask_Wf +
-               pc + a.mask_off;
+    // 8 pooled outputs per batch: all 24 global loads in flight before any use
+    for (int pb = j; pb < PpQp; pb += 8 * a.tpk) {
+      float gv[8], mv[8];
+      int av[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int pp = pb + u * a.tpk;
+        gv[u] = 0.f; mv[u] = 1.f; av[u] = -1;
+        if (pp < PpQp) {
+          gv[u] = __ldg(dpool + base + pp);
+          av[u] = __ldg(argmax + base + pp);
+          if (mask) {
+            int64_t mi = base + pp;
+            if (a.mask_plane > 0) {
+              const int pr = pp / a.Qp, pc = pp - pr * a.Qp;
+              mi = (int64_t)k * a.mask_plane + (int64_t)n * a.mask_Lf + (pr + a.mask_off) * a.mask_Wf +
+                   pc + a.mask_off;
+            }
+            mv[u] = __ldg(mask + mi);
+          }
         }
-        if (!(__ldg(mask + mi) > 0.f)) continue;
       }
-      if (g0 == 0.f) continue;
-      const int am = __ldg(argmax + base + pp) - k * PQ;  // position inside plane k
-      if (am < 0 || am >= PQ) continue;
-      const int h = am / a.Q, w = am - h * a.Q;
-      const float *win = img + h * a.Wp + w;  // padded coords of tap (0,0)
-      dbacc += g0;
 #pragma unroll
-      for (int r = 0; r < R_; ++r)
+      for (int u = 0; u < 8; ++u) {
+        const float g0 = gv[u];
+        if (!(mv[u] > 0.f) || g0 == 0.f) continue;  // masked (reading R9) or zero gradient
+        const int am = av[u] - k * PQ;               // position inside plane k
+        if (am < 0 || am >= PQ) continue;
+        const int h = am / a.Q, w = am - h * a.Q;
+        const float *win = img + h * a.Wp + w;       // padded coords of tap (0,0)
+        dbacc += g0;
 #pragma unroll
-        for (int s = 0; s < S_; ++s) acc[r * S_ + s] = fmaf(g0, win[r * a.Wp + s], acc[r * S_ + s]);
+        for (int r = 0; r < R_; ++r)
+#pragma unroll
+          for (int s = 0; s < S_; ++s) acc[r * S_ + s] = fmaf(g0, win[r * a.Wp + s], acc[r * S_ + s]);
+      }
     }
   }
   // fixed-order reduction of the tpk partials of each filter through shared memory
@@ -129,7 +144,7 @@ __global__ void fused_b1_reduce_kernel(const float *__restrict__ part, int parts
 }
 
 int fused_b1_ctas(int N) {
-  int ctas = 2 * sm_count();
+  int ctas = 4 * sm_count();
   if (ctas > N) ctas = N;
   return ctas < 1 ? 1 : ctas;
 }

@@ -44,7 +44,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
   uint32_t ns = 32;
   while (!mbar_try_wait(bar, parity)) {
     __nanosleep(ns);
-    ns = ns < 512 ? ns * 2 : 512;
+    ns = ns < 64 ? ns * 2 : 64;
   }
 }
 
