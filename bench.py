@@ -55,8 +55,9 @@ STAGE_WORK = {
     "F1_conv1_pool": (2 * 32 * 25 * 784, 784 * 4 + 6272 * 4 * 2, "hbm"),
     "F2_conv2_pool": (2 * 64 * 800 * 196, 6272 * 4 + 3136 * 4 * 2, "tensor"),
     "F3_affine_softmax_ce": (2 * 10 * 3136, 3136 * 4 + 10 * 4, "hbm"),
-    "B3_affine_bwd": (4 * 10 * 3136, 3136 * 4 * 2 + 10 * 4, "hbm"),
-    "B2p_maxpool_bwd2": (0, 3136 * 4 * 3 + 12544 * 4, "hbm"),
+    "B3_affine_bwd": (2 * 10 * 3136, 3136 * 4 + 10 * 4, "hbm"),  # dW3 = ds^T a2, db3
+    # TF32/SPF path: da2 = ds W3 fused with the max-pool routing (reads a2, i2; writes dz2)
+    "B2p_maxpool_bwd2": (2 * 10 * 3136, 3136 * 4 * 2 + 12544 * 4, "hbm"),
     "B2f_conv2_bwd_filter": (2 * 64 * 800 * 196, 6272 * 4 + 12544 * 4, "tensor"),
     "B2d_conv2_bwd_data": (2 * 64 * 800 * 196, 12544 * 4 + 6272 * 4, "tensor"),
     "B1p_maxpool_bwd1": (0, 6272 * 4 * 3 + 25088 * 4, "hbm"),

@@ -53,7 +53,8 @@ namespace sysml {
 namespace {
 
 constexpr int TC_THREADS = 256;      // bwd_filter kernel: 4 producer warps + MMA/epilogue warps
-constexpr int TC_FWD_THREADS = 288;  // forward kernel: 4 producer, 1 MMA, 4 epilogue warps
+constexpr int TC_FWD_THREADS = 416;  // forward kernel: 4 producer, 1 MMA, 8 epilogue warps
+constexpr int TC_EPI_WARPS = 8;      // two per TMEM lane quadrant; they split the M-tiles
 constexpr int SMEM_BUDGET = 225 * 1024;
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
@@ -128,11 +129,11 @@ __device__ __forceinline__ void load_bias16(const TcFwdParams &p, const float *b
 
 // plain conv output: lane -> position (linear or 2-D M-tile), 16 filters per chunk
 __device__ __forceinline__ void epi_plain(const TcFwdParams &p, uint32_t tbase, int64_t g0, int ft,
-                                          int qd, int lane, const float *bias_s) {
+                                          int qd, int lane, const float *bias_s, int i0, int istep) {
   const int PQ = p.P * p.Q;
   const int nc16 = p.NFpad / 16;
   float *__restrict__ y = p.y;
-  for (int i = 0; i < p.MT; ++i) {
+  for (int i = i0; i < p.MT; i += istep) {
     const uint32_t trow = tbase + (uint32_t)(i * p.NFpad);
     uint32_t r0[16], r1[16];
     ptx::tmem_ld16_issue(trow, r0);
@@ -184,14 +185,14 @@ __device__ __forceinline__ void epi_plain(const TcFwdParams &p, uint32_t tbase, 
 // First-occurrence tie-break (r outer, s inner; strict '>', readings R5/R7): the
 // later partner replaces the current value only when strictly greater.
 __device__ __forceinline__ void epi_pool2(const TcFwdParams &p, uint32_t tbase, int64_t g0, int ft,
-                                          int qd, int lane, const float *bias_s) {
+                                          int qd, int lane, const float *bias_s, int i0, int istep) {
   const int PQ = p.P * p.Q, PpQp = p.Pp * p.Qp;
   const int nc16 = p.NFpad / 16;
   const int rl = qd * 4 + (lane >> 3), cl = lane & 7;
   const bool leader = ((rl | cl) & 1) == 0;
   float *__restrict__ pout = p.pout;
   int32_t *__restrict__ parg = p.parg;
-  for (int i = 0; i < p.MT; ++i) {
+  for (int i = i0; i < p.MT; i += istep) {
     const uint32_t trow = tbase + (uint32_t)(i * p.NFpad);
     uint32_t r0[16], r1[16];
     ptx::tmem_ld16_issue(trow, r0);
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(accf + b, 1);
-      ptx::mbar_init(acce + b, 4);      // 4 epilogue warps
+      ptx::mbar_init(acce + b, TC_EPI_WARPS);
     }
     ptx::fence_mbar_init();
   }
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       }
     }
   } else {
-    // ================= MMA issuer (warp 4) | epilogue (warps 5-8, TMEM quadrant warp % 4)
+    // ================= MMA issuer (warp 4) | epilogue (warps 5-12, TMEM quadrant warp % 4)
     const int qd = warp & 3;
     const uint32_t idesc = ptx::make_idesc_tf32(128, p.NFpad);
     int stage = 0;
@@ -442,8 +443,9 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       const long long t_epi0 = clock64();
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(qd * 32) << 16) + buf * TMEM_BUF;
-      if (p.pool) epi_pool2(p, tbase, g0, ft, qd, lane, bias_s);
-      else epi_plain(p, tbase, g0, ft, qd, lane, bias_s);
+      const int eset = (warp - 5) >> 2;  // epilogue warp set 0 / 1 -> even / odd M-tiles
+      if (p.pool) epi_pool2(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
+      else epi_plain(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(acce + buf);

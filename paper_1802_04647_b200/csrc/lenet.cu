@@ -169,6 +169,36 @@ __global__ void da2_kernel(int n, const float *__restrict__ ds, const float *__r
   }
 }
 
+// B3+B2p fused (SPF path): da2 = ds W3 evaluated per pooled output and routed straight
+// through the 2x2 max-pool argmax (ReLU mask a2 > 0) into the unpooled gradient dz2 in
+// SPF planes [64][plane] (output frame 16x16, position n*256 + h*16 + w): the da2 tensor
+// is never materialised.  One thread per pooled output (n, k, pp, pc).
+__global__ void affine_bwd_route_spf_kernel(int n, const float *__restrict__ ds,
+                                            const float *__restrict__ W3,
+                                            const float *__restrict__ a2,
+                                            const int32_t *__restrict__ i2,
+                                            float *__restrict__ dz2s, int64_t plane) {
+  const int64_t total = (int64_t)n * D3;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(o / D3);
+    const int d = (int)(o - (int64_t)s * D3);  // = k*49 + pp*7 + pc
+    const int k = d / 49, r = d - k * 49, pp = r / 7, pc = r - pp * 7;
+    float g = 0.f;
+    if (__ldg(a2 + o) > 0.f) {
+#pragma unroll
+      for (int j = 0; j < NCLS; ++j) g = fmaf(__ldg(ds + s * NCLS + j), __ldg(W3 + j * D3 + d), g);
+    }
+    const int am = __ldg(i2 + o) - k * 196;  // position inside the 14x14 plane
+    float *base = dz2s + (int64_t)k * plane + (int64_t)s * 256 + (2 * pp) * 16 + 2 * pc;
+    const int a0 = (2 * pp) * 14 + 2 * pc;
+    float2 top = make_float2(am == a0 ? g : 0.f, am == a0 + 1 ? g : 0.f);
+    float2 bot = make_float2(am == a0 + 14 ? g : 0.f, am == a0 + 15 ? g : 0.f);
+    *reinterpret_cast<float2 *>(base) = top;
+    *reinterpret_cast<float2 *>(base + 16) = bot;
+  }
+}
+
 __global__ void sgd_kernel(float *__restrict__ p, const float *__restrict__ g, int64_t n,
                            float lr) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -487,15 +517,21 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     chunk_sum_kernel<<<(unsigned)ceil_div(NCLS * D3 + NCLS, 256), 256, 0, st>>>(
         h->part3, used, NCLS * D3 + NCLS, grads + OFF_W3);
     SYSML_LAUNCH_CHECK();
-    da2_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)n * D3, 256), 16 * sm_count()), 256,
-                 0, st>>>(n, h->ds, params + OFF_W3, h->da2);
-    SYSML_LAUNCH_CHECK();
+    if (!h->spf) {
+      da2_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)n * D3, 256), 16 * sm_count()), 256,
+                   0, st>>>(n, h->ds, params + OFF_W3, h->da2);
+      SYSML_LAUNCH_CHECK();
+    }
   }
   SYSML_TRY(T.end());
   if (h->spf) {
     // B2p: unpooled gradient straight into the SPF planes (output-frame convention)
     SYSML_TRY(T.begin(4));
-    SYSML_TRY(launch_maxpool_bwd_spf(pa2, h->i2, h->da2, h->a2, h->dz2s, h->spf_plane, 16, 256, st));
+    affine_bwd_route_spf_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)n * D3, 256),
+                                                               16 * sm_count()),
+                                  256, 0, st>>>(n, h->ds, params + OFF_W3, h->a2, h->i2, h->dz2s,
+                                                h->spf_plane);
+    SYSML_LAUNCH_CHECK();
     SYSML_TRY(T.end());
     // B2f
     SYSML_TRY(T.begin(5));
