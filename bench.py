@@ -370,7 +370,15 @@ def ours_arm(args, world, rank, local):
         achieved = by * b / avg_s / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm"], "unit": "GB/s",
                 "frac": round(achieved / peaks["hbm"], 4)}
-    roof.update({"kernel": dom, "traffic": None, "peak_src": peaks["src"]})
+    traffic = None
+    try:  # DRAM bytes of the dominant kernel from one ncu --set full capture (profiles/)
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(dom)
+        if t:
+            traffic = round(t["dram_bytes_per_image"] * b)
+    except (OSError, ValueError):
+        pass
+    roof.update({"kernel": dom, "traffic": traffic, "algorithmic_bytes": by * b,
+                 "peak_src": peaks["src"]})
 
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
