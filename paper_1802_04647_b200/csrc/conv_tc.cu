@@ -84,6 +84,9 @@ struct TcFwdParams {
   int64_t cta_pos;     // positions advanced per CTA tile (linear: MT*128; 2-D: BB*16*Wf)
   int pool, PR, PS, Pp, Qp;
   int bias_smem;       // bias staged in shared memory (K floats)
+  int ks;              // C == 1: the S column taps fill the MMA K slots (s = 4*half + e)
+  int is_csr;          // KS mode only: input rows are CSR (scattered straight into the operand)
+  sysml_csr csr;
   int64_t in_plane;    // > 0: input is SPF [C][in_plane], stored position = frame pos + in_shift
   int in_shift;
   int64_t out_plane;   // > 0: pooled output to SPF [K][out_plane] at (pp+out_off)*out_Wf + pc+out_off
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t *stage_base = smem;
   int *src_off = reinterpret_cast<int *>(smem + (size_t)p.nstage * p.stage_bytes);
-  float *bias_s = reinterpret_cast<float *>(src_off + p.HALO);
+  float *bias_s = reinterpret_cast<float *>(src_off + p.HALO + 8);
   uint64_t *bars = reinterpret_cast<uint64_t *>(
       (reinterpret_cast<uintptr_t>(bias_s + (p.bias_smem ? p.K : 0)) + 15) & ~(uintptr_t)15);
   uint64_t *full = bars;
@@ -315,7 +318,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       const int ft = (int)(tile % p.nft);
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
       ptx::named_bar_sync(1, 128);
-      for (int pos = tid; pos < p.HALO; pos += 128) {
+      const int ntab = p.ks ? p.HALO + 8 : p.HALO;
+      for (int pos = tid; pos < (p.is_csr ? 0 : ntab); pos += 128) {
         const int64_t gi = g0 + pos;
         int off = -1;
         if (p.in_plane > 0) {
@@ -343,9 +347,56 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           ptx::bulk_g2s(B, p.fp + ((size_t)ft * p.nchunk + ch) * (p.b_bytes / 4), p.b_bytes,
                         full + stage);
         }
-        const int c0 = ch * 8;
         const uint32_t a0 = ptx::smem_u32(A);
         const uint32_t a1 = a0 + (uint32_t)p.HALO * 16;
+        if (p.ks && p.is_csr) {
+          // CSR rows scattered straight into the KS operand: element (pos, s) = x(pos + s);
+          // zero-fill, then each stored non-zero lands in its S slots (work ~ nnz)
+          for (int i = tid; i < 2 * p.HALO; i += 128) st_shared_v4(a0 + i * 16, 0.f, 0.f, 0.f, 0.f);
+          ptx::named_bar_sync(1, 128);
+          const int64_t last = g0 + p.HALO + 7;
+          const int n_lo = (int)(g0 / p.Lf);
+          const int n_hi = (int)min((int64_t)p.N - 1, last / p.Lf);
+          float *Af = reinterpret_cast<float *>(A);
+          for (int n = n_lo; n <= n_hi; ++n) {
+            const int j0 = __ldg(p.csr.row_ptr + n), j1 = __ldg(p.csr.row_ptr + n + 1);
+            for (int jj = j0 + tid; jj < j1; jj += 128) {
+              const int col = __ldg(p.csr.col_idx + jj);
+              if (col < 0 || col >= HW) continue;
+              const float v = __ldg(p.csr.val + jj);
+              const int h = col / p.W, w = col - h * p.W;
+              const int64_t gi = (int64_t)n * p.Lf + (int64_t)(h + p.ph) * p.Wf + (w + p.pw);
+              for (int s_ = 0; s_ < p.S; ++s_) {
+                const int64_t pos = gi - g0 - s_;
+                if (pos >= 0 && pos < p.HALO)
+                  atomicAdd(Af + (s_ >> 2) * p.HALO * 4 + pos * 4 + (s_ & 3), v);  // duplicates summed
+              }
+            }
+          }
+        } else if (p.ks) {
+          // dense C == 1 input: element (pos, s) = x(pos + s) for s < S, 0 for S <= s < 8
+          for (int pb = tid; pb < p.HALO; pb += 2 * 128) {
+            float v[2][8];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int pos = pb + u * 128;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int off = (pos < p.HALO && e < p.S) ? src_off[pos + e] : -1;
+                v[u][e] = off >= 0 ? __ldg(p.x + off) : 0.f;
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int pos = pb + u * 128;
+              if (pos < p.HALO) {
+                st_shared_v4(a0 + pos * 16, v[u][0], v[u][1], v[u][2], v[u][3]);
+                st_shared_v4(a1 + pos * 16, v[u][4], v[u][5], v[u][6], v[u][7]);
+              }
+            }
+          }
+        } else {
+        const int c0 = ch * 8;
         const int nc = min(8, p.C - c0);
         const int64_t cstride = p.in_plane > 0 ? p.in_plane : (int64_t)HW;
         const float *xc = p.x + c0 * cstride;
@@ -368,6 +419,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
               st_shared_v4(a1 + pos * 16, v[u][4], v[u][5], v[u][6], v[u][7]);
             }
           }
+        }
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
@@ -413,8 +465,9 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           uint64_t bdesc = ptx::make_desc(A + p.a_bytes, nf * 16, 128);
           uint32_t acc = ch != 0 ? 1u : 0u;
           uint32_t drow = 0;
+          const int s_taps = p.ks ? 1 : p.S;  // KS: all S column taps are in the K slots
           for (int r = 0; r < p.R; ++r, drow += (uint32_t)p.Wf) {
-            for (int s_ = 0; s_ < p.S; ++s_) {
+            for (int s_ = 0; s_ < s_taps; ++s_) {
               uint64_t ad = adesc0 + (uint64_t)(drow + (uint32_t)s_);
               uint32_t tm = buf * TMEM_BUF;
               int ct = 0;
@@ -484,11 +537,27 @@ __global__ void tc_pack_filters_kernel(const float *__restrict__ f, float *__res
   }
 }
 
+// KS packing (C == 1): [ftile][r][half][NFpad][4] with packed(k, r, 4*half + e) = F[k][0][r][s]
+__global__ void tc_pack_filters_ks_kernel(const float *__restrict__ f, float *__restrict__ fp,
+                                          int Kout, int R, int S, int NFpad, int nft) {
+  const int64_t total = (int64_t)nft * R * 2 * NFpad * 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int e = (int)(t % 4); t /= 4;
+    const int j = (int)(t % NFpad); t /= NFpad;
+    const int g = (int)(t % 2); t /= 2;
+    const int r = (int)(t % R); t /= R;
+    const int k = (int)t * NFpad + j, s = g * 4 + e;
+    fp[i] = (k < Kout && s < S) ? f[((int64_t)k * R + r) * S + s] : 0.f;
+  }
+}
+
 int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 // Plan the forward kernel for a stride-1 conv: input (N,C,H,W), K output channels.
 TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
-                const PoolArgs *pool) {
+                const PoolArgs *pool, bool allow_ks = true) {
   TcPlan pl{};
   TcFwdParams &p = pl.p;
   p.N = N; p.C = C; p.H = H; p.W = W; p.K = K; p.R = R; p.S = S; p.ph = ph; p.pw = pw;
@@ -518,9 +587,12 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
     p.NFpad = 256;
     p.nft = (K + 255) / 256;
   }
-  p.nchunk = (C + 7) / 8;
+  p.ks = (allow_ks && C == 1 && S <= 8) ? 1 : 0;
+  p.nchunk = p.ks ? 1 : (C + 7) / 8;
   const int RS = R * S;
-  p.b_bytes = (uint32_t)(RS * 2 * p.NFpad * 16);
+  const int b_taps = p.ks ? R : RS;
+  const int s_halo = p.ks ? 0 : S - 1;  // KS: the S window lives inside each operand row
+  p.b_bytes = (uint32_t)(b_taps * 2 * p.NFpad * 16);
   const int nsm = sm_count();
   const int64_t rows_total = (int64_t)N * p.Hs;
   int mt_cap = std::min(16, (int)TMEM_BUF / p.NFpad);  // TMEM double buffer
@@ -535,19 +607,19 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
         bb = mt / p.CT;
         if (bb < 1) continue;
         cta_pos = (int64_t)bb * 16 * p.Wf;
-        halo = (bb - 1) * 16 * p.Wf + (p.CT - 1) * 8 + 15 * p.Wf + 7 + (R - 1) * p.Wf + (S - 1) + 1;
+        halo = (bb - 1) * 16 * p.Wf + (p.CT - 1) * 8 + 15 * p.Wf + 7 + (R - 1) * p.Wf + s_halo + 1;
         halo = round_up(halo, 8);  // LBO multiple of 128 B
         ntiles = ceil_div(rows_total, (int64_t)bb * 16) * p.nft;
       } else {
         cta_pos = (int64_t)mt * 128;
-        halo = round_up(mt * 128 + (R - 1) * p.Wf + (S - 1), 8);  // LBO multiple of 128 B
+        halo = round_up(mt * 128 + (R - 1) * p.Wf + s_halo, 8);  // LBO multiple of 128 B
         ntiles = ceil_div(p.G, cta_pos) * p.nft;
       }
       if (attempt == 0 && mt > 1 && ntiles < nsm) continue;  // keep the SMs busy first
       const uint32_t a_bytes = (uint32_t)(2 * halo * 16);
       const uint32_t stage = a_bytes + p.b_bytes;
       p.bias_smem = K <= 4096 ? 1 : 0;
-      const size_t fixed = (size_t)halo * 4 + (p.bias_smem ? (size_t)K * 4 : 0) + 16 + 8 * 24 + 16;
+      const size_t fixed = (size_t)(halo + 8) * 4 + (p.bias_smem ? (size_t)K * 4 : 0) + 16 + 8 * 24 + 16;
       const int nst = (int)((SMEM_BUDGET - (int64_t)fixed) / (int64_t)stage);
       if (nst < 2) continue;
       p.MT = p.tile2d ? bb * p.CT : mt;
@@ -569,7 +641,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   if (p.tile2d && (uint32_t)p.Wf * 16 >= (1u << 18)) { pl.ok = false; return pl; }
   if (p.MT * p.NFpad > (int)TMEM_BUF) { pl.ok = false; return pl; }
   p.tmem_cols = 512;  // whole TMEM: base column 0 (1 CTA per SM), issue loops address from 0
-  pl.fp_bytes = align_up((size_t)p.nft * p.nchunk * RS * 8 * p.NFpad * sizeof(float), 256);
+  pl.fp_bytes = align_up((size_t)p.nft * p.nchunk * b_taps * 8 * p.NFpad * sizeof(float), 256);
   return pl;
 }
 
@@ -584,8 +656,16 @@ sysml_status set_smem_attr(K kernel, size_t bytes, int &cache) {
 
 sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f_cin,
                      const float *bias, float *y, float *pout, int32_t *parg, void *ws,
-                     cudaStream_t st, const TcSpfIO *io = nullptr) {
+                     cudaStream_t st, const TcSpfIO *io = nullptr, const sysml_csr *csr = nullptr) {
   TcFwdParams p = pl.p;
+  if (csr) {
+    if (!p.ks) {
+      set_error("tcgen05 forward: CSR input needs the single-channel (KS) mode");
+      return SYSML_ERR_UNSUPPORTED;
+    }
+    p.is_csr = 1;
+    p.csr = *csr;
+  }
   if (io) {
     p.in_plane = io->in_plane;
     p.in_shift = io->in_shift;
@@ -595,7 +675,16 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     p.out_off = io->out_off;
   }
   float *fp = reinterpret_cast<float *>(ws);
-  {
+  if (p.ks) {
+    if (flip) {
+      set_error("tcgen05 KS mode does not implement the flipped (bwd_data) packing");
+      return SYSML_ERR_UNSUPPORTED;
+    }
+    const int64_t total = (int64_t)p.nft * p.R * 2 * p.NFpad * 4;
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * sm_count());
+    tc_pack_filters_ks_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, p.R, p.S, p.NFpad, p.nft);
+    SYSML_LAUNCH_CHECK();
+  } else {
     const int64_t total = (int64_t)p.nft * p.nchunk * p.R * p.S * 2 * p.NFpad * 4;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * sm_count());
     tc_pack_filters_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, f_cin, p.R * p.S, p.NFpad, p.nft,
@@ -1316,6 +1405,8 @@ TcWgSpfPlan plan_wgrad_spf(const SpfConv &sc) {
 }  // namespace
 
 // ------------------------------------------------------------------ forward (K3)
+bool tc_fwd_ks(const ConvArgs &a) { return a.C == 1 && a.S <= 8; }
+
 bool tc_fwd_supported(const ConvArgs &a, const PoolArgs *pool) {
   if (device_cc_major() != 10) return false;
   if (a.sh != 1 || a.sw != 1 || !pool_fusable(pool)) return false;
@@ -1326,24 +1417,27 @@ size_t tc_fwd_ws(const ConvArgs &a) {
   // the packed filter bank only depends on (K, C, R, S)
   const int nfpad = a.K <= 256 ? std::max(16, round_up(a.K, 16)) : 256;
   const int nft = a.K <= 256 ? 1 : (a.K + 255) / 256;
+  if (a.C == 1 && a.S <= 8)  // KS packing: [ftile][r][2 halves][NFpad][4]
+    return align_up((size_t)nft * a.R * 8 * nfpad * sizeof(float), 256);
   return align_up((size_t)nft * ((a.C + 7) / 8) * a.R * a.S * 8 * nfpad * sizeof(float), 256);
 }
 
 sysml_status tc_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
                          float *y, const PoolArgs *pool, float *pout, int32_t *parg, void *ws,
-                         cudaStream_t st) {
+                         cudaStream_t st, const sysml_csr *csr) {
   TcPlan pl = plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool);
   if (!pl.ok) {
     set_error("tcgen05 forward: unsupported shape");
     return SYSML_ERR_UNSUPPORTED;
   }
-  return run_fwd(pl, x, f, 0, a.C, bias, pool ? nullptr : y, pout, parg, ws, st);
+  return run_fwd(pl, x, f, 0, a.C, bias, pool ? nullptr : y, pout, parg, ws, st, nullptr, csr);
 }
 
 // ------------------------------------------------------------------ bwd_data (K6)
 static TcPlan plan_bwd_data(const ConvArgs &a) {
   // dX = conv(dY, rot180(F)^T), pad R-1-ph; input (N, K, P, Q) -> output (N, C, H, W)
-  return plan_fwd(a.N, a.K, a.P, a.Q, a.C, a.R, a.S, a.R - 1 - a.ph, a.S - 1 - a.pw, nullptr);
+  return plan_fwd(a.N, a.K, a.P, a.Q, a.C, a.R, a.S, a.R - 1 - a.ph, a.S - 1 - a.pw, nullptr,
+                  /*allow_ks=*/false);
 }
 
 bool tc_bwd_data_supported(const ConvArgs &a) {
@@ -1372,13 +1466,13 @@ sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy
 // ------------------------------------------------------------------ SPF-layout entry points
 sysml_status tc_conv_fwd_spf(const ConvArgs &a, const TcSpfIO &io, const float *x, const float *f,
                              const float *bias, float *y, const PoolArgs *pool, float *pout,
-                             int32_t *parg, void *ws, cudaStream_t st) {
+                             int32_t *parg, void *ws, cudaStream_t st, const sysml_csr *csr) {
   TcPlan pl = plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool);
   if (!pl.ok || a.sh != 1 || a.sw != 1) {
     set_error("tcgen05 SPF forward: unsupported shape");
     return SYSML_ERR_UNSUPPORTED;
   }
-  return run_fwd(pl, x, f, 0, a.C, bias, pool ? nullptr : y, pout, parg, ws, st, &io);
+  return run_fwd(pl, x, f, 0, a.C, bias, pool ? nullptr : y, pout, parg, ws, st, &io, csr);
 }
 
 sysml_status tc_conv_bwd_data_spf(const ConvArgs &a, const TcSpfIO &io, const float *f,

@@ -74,17 +74,20 @@ struct TcSpfIO {
 // conv_tc.cu : tcgen05 TF32 implicit GEMM (SYSML_MATH_TF32)
 
 bool tc_fwd_supported(const ConvArgs &a, const PoolArgs *pool);
+// single-channel convs (C == 1, S <= 8) use the KS operand mode, which also reads CSR input
+bool tc_fwd_ks(const ConvArgs &a);
 size_t tc_fwd_ws(const ConvArgs &a);
 sysml_status tc_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
                          float *y, const PoolArgs *pool, float *pout, int32_t *parg, void *ws,
-                         cudaStream_t st);
+                         cudaStream_t st, const sysml_csr *csr = nullptr);
 bool tc_bwd_data_supported(const ConvArgs &a);
 size_t tc_bwd_data_ws(const ConvArgs &a);
 sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
                               void *ws, cudaStream_t st);
 sysml_status tc_conv_fwd_spf(const ConvArgs &a, const TcSpfIO &io, const float *x, const float *f,
                              const float *bias, float *y, const PoolArgs *pool, float *pout,
-                             int32_t *parg, void *ws, cudaStream_t st);
+                             int32_t *parg, void *ws, cudaStream_t st,
+                             const sysml_csr *csr = nullptr);
 sysml_status tc_conv_bwd_data_spf(const ConvArgs &a, const TcSpfIO &io, const float *f,
                                   const float *dy, float *dx, void *ws, cudaStream_t st);
 bool tc_wgrad_spf_supported(const SpfConv &sc);

@@ -386,7 +386,7 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
     const PoolArgs pa1 = pool_args(gp1, 1), pa2 = pool_args(gp2, 1);
     SpfConv sc{64, 32, 5, 5, 16, (int64_t)max_local_batch * 256, (int64_t)max_local_batch * 256,
                (int64_t)max_local_batch * 256, 0, 0};
-    h->spf = (h->csr || tc_fwd_supported(a1a, &pa1)) && tc_fwd_supported(a2a, &pa2) &&
+    h->spf = tc_fwd_supported(a1a, &pa1) && tc_fwd_supported(a2a, &pa2) &&
              tc_bwd_data_supported(a2a) && tc_wgrad_spf_supported(sc);
     if (h->spf) {
       h->spf_plane = (int64_t)max_local_batch * 256;
@@ -471,9 +471,11 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
   sysml_input a1in{0, h->a1, {}};
   // F1
   SYSML_TRY(T.begin(0));
-  if (h->spf && !x->is_csr) {
-    SYSML_TRY(tc_conv_fwd_spf(ca1, a1_io, x->dense, params + OFF_F1, params + OFF_B1, nullptr, &pa1,
-                              h->a1s, h->i1, h->ws, st));
+  if (h->spf) {
+    // dense or CSR (scattered straight into the KS operand): pooled a1 lands in SPF
+    SYSML_TRY(tc_conv_fwd_spf(ca1, a1_io, x->is_csr ? nullptr : x->dense, params + OFF_F1,
+                              params + OFF_B1, nullptr, &pa1, h->a1s, h->i1, h->ws, st,
+                              x->is_csr ? &x->csr : nullptr));
   } else {
     SYSML_TRY(conv_fwd_dispatch(c1, *x, params + OFF_F1, params + OFF_B1, nullptr, &p1, h->a1, h->i1,
                                 h->ws, h->ws_bytes, st));

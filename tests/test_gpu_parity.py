@@ -50,6 +50,9 @@ CONV_SHAPES = [
     (2, 256, 14, 14, 256, 3, 3, 1, 1),   # BJ cfg 4 (i) 3x3 C=K=256 at N=2
     (2, 1024, 14, 14, 256, 1, 1, 1, 0),  # BJ cfg 4 (ii) 1x1 1024->256 at N=2
     (1, 2, 5, 5, 3, 5, 5, 1, 0),         # P = Q = 1
+    (3, 1, 17, 23, 20, 7, 3, 1, (3, 1)), # C = 1 (KS operand mode), tall kernel, ragged
+    (2, 1, 9, 30, 5, 2, 8, 1, (0, 4)),   # C = 1, S = 8 (both K halves full)
+    (2, 4, 9, 9, 1, 3, 3, 1, 1),         # K = 1 (bwd_data input has one channel)
 ]
 
 
@@ -196,9 +199,9 @@ def _csr_dev(S, dense):
     return S.CSR(dev(rp, torch.int32), dev(ci, torch.int32), dev(v), dense.shape[0], dense.shape[1]), (rp, ci, v)
 
 
+@pytest.mark.parametrize("N", [12, 37])
 @pytest.mark.parametrize("math", ["fp32", "tf32"])
-def test_csr_conv_fwd_bwd_filter(S, math):
-    N = 12
+def test_csr_conv_fwd_bwd_filter(S, math, N):
     x = synth.mnist_like(N, seed=(500,))
     x[0] = 0.0                                    # empty row
     x[1] = synth.uniform((784,), 0.01, 1.0, seed=(501,))  # fully dense row
@@ -211,7 +214,7 @@ def test_csr_conv_fwd_bwd_filter(S, math):
     dy = synth.normal((N, 32 * 784), seed=(504,))
     d = S.conv_desc(N, 1, 28, 28, 32, 5, 5, 1, 2, math)
     y = S.sysml_conv2d(m, dev(f), d, bias=dev(b))
-    assert_close(host(y), oracle.conv2d_fwd(xd, f, N, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2), bias=b), 1e-4, "csr fwd")
+    assert_close(host(y), oracle.conv2d_fwd(xd, f, N, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2), bias=b), TOL[math], "csr fwd")
     df, db = S.sysml_conv2d_bwd_filter(m, dev(dy), d)
     dfr, dbr = oracle.conv2d_bwd_filter(xd, dy, N, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2))
     assert_close(host(df), dfr, 1e-4, "csr bwd_filter")
@@ -220,7 +223,7 @@ def test_csr_conv_fwd_bwd_filter(S, math):
     out, arg = S.sysml_conv2d_bias_relu_maxpool(m, dev(f), dev(b), d, pd)
     z = oracle.conv2d_fwd(xd, f, N, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2), bias=b)
     oref, aref = oracle.relu_maxpool(z, N, 32, 28, 28, 2, 2, (2, 2), (0, 0))
-    assert_close(host(out), oref, 1e-4, "csr fused")
+    assert_close(host(out), oref, TOL[math], "csr fused")
     assert (host(arg) != aref).mean() < 1e-3
 
 
