@@ -250,7 +250,13 @@ def layer_section(S, peaks, quick=False):
     fwd_bytes = 4 * (N + 1) + 8 * nnz + 4 * (800 + 32) + 4 * N * 32 * 784
     bwf_bytes = 4 * (N + 1) + 8 * nnz + 4 * N * 32 * 784 + 4 * 832
     res = {"nnz": int(nnz), "density": round(nnz / (N * 784), 4)}
+    pd = S.pool_desc(N, 32, 28, 28, 2, 2, 2, 0, True)
+    pout = torch.empty(N, 32 * 196, device="cuda")
+    parg = torch.empty(N, 32 * 196, dtype=torch.int32, device="cuda")
+    fused_bytes = 4 * (N + 1) + 8 * nnz + 4 * (800 + 32) + 8 * N * 32 * 196
     for op, fn, nbytes in (("fwd", lambda: S.sysml_conv2d(m, f, d, bias=b, out=y, workspace=ws), fwd_bytes),
+                           ("fwd_bias_relu_pool", lambda: S.sysml_conv2d_bias_relu_maxpool(
+                               m, f, b, d, pd, out=pout, argmax=parg, workspace=ws), fused_bytes),
                            ("bwd_filter", lambda: S.sysml_conv2d_bwd_filter(m, dy, d, df=df, db=db, workspace=ws), bwf_bytes)):
         med, mn = time_op(fn, reps, flush)
         gbs = nbytes / (med * 1e-3) / 1e9

@@ -227,6 +227,33 @@ def test_csr_conv_fwd_bwd_filter(S, math, N):
     assert (host(arg) != aref).mean() < 1e-3
 
 
+# (N, C, H, W, K, R, S, pad): the lane-per-filter K8 path (C=1, K<=32) and the fallback
+CSR_WGRAD_SHAPES = [
+    (5, 1, 12, 16, 20, 3, 3, 1),
+    (3, 1, 12, 16, 7, 5, 5, 0),
+    (4, 1, 9, 10, 32, 5, 5, 2),    # P*Q = 90: not a multiple of 4 -> fallback kernel
+    (3, 2, 8, 8, 5, 3, 3, 1),      # C = 2 -> fallback kernel
+]
+
+
+@pytest.mark.parametrize("shape", CSR_WGRAD_SHAPES)
+def test_csr_bwd_filter_shapes(S, shape):
+    N, C, H, W, K, R, S_, pd = shape
+    P, Q = H + 2 * pd - R + 1, W + 2 * pd - S_ + 1
+    x = synth.uniform((N, C * H * W), 0.0, 1.0, seed=(520,))
+    x[x < 0.7] = 0.0
+    x[0, :] = 0.0
+    m, (rp, ci, v) = _csr_dev(S, x)
+    dy = synth.normal((N, K * P * Q), seed=(521,))
+    d = S.conv_desc(N, C, H, W, K, R, S_, 1, pd, "fp32")
+    df, db = S.sysml_conv2d_bwd_filter(m, dev(dy), d)
+    dfr, dbr = oracle.conv2d_bwd_filter(x.astype(np.float64), dy, N, C, H, W, K, R, S_, (1, 1), (pd, pd))
+    assert_close(host(df), dfr, 1e-4, "csr bwd_filter")
+    assert_close(host(db), dbr, 1e-4, "csr db")
+    df2, db2 = S.sysml_conv2d_bwd_filter(m, dev(dy), d)
+    assert np.array_equal(host(df), host(df2)) and np.array_equal(host(db), host(db2))  # deterministic
+
+
 def test_csr_dyadic_fused_bit_exact(S):
     N = 9
     x = synth.mnist_like_dyadic(N, seed=(510,))
