@@ -276,66 +276,55 @@ __global__ void csr_check_kernel(sysml_csr m, unsigned long long *bad) {
 
 
 // ---------------------------------------------------------------- K8 fast path
-constexpr int WG_WARPS = 16;                   // compute warps
+constexpr int WG_WARPS = 16;                    // compute warps
 constexpr int WG_THREADS = (WG_WARPS + 1) * 32; // + producer warp
-constexpr int WG_GUARD = 16;                   // floats of zeroed guard around the planes
 
 struct WgK32 {
   int N, K, H, W, P, Q, ph, pw;
-  int stride;          // padded plane stride (floats)
-  int nbuf;            // 1 or 2 staging buffers
+  int stride;          // padded plane stride of the raw staging buffer (floats)
   int n_per_block;
   float invW;
-  int q4;              // Q % 4 == 0: interior non-zeros take the fixed-phase path
 };
 
 __device__ __forceinline__ float4 lds4(const float *p) {
   return *reinterpret_cast<const float4 *>(p);
 }
 
+// Per image: the producer bulk-copies the K dY planes into `raw` (plane stride padded
+// so lane-per-plane float4 reads are conflict free); the compute warps transpose raw
+// into T[pos][32] (filter-contiguous: one conflict-free 128-B wavefront per position
+// for lane = k) while summing db, release raw (the next image's copy then overlaps the
+// compute), and accumulate dF from T.
 template <int R_, int S_>
 __global__ void __launch_bounds__(WG_THREADS, 1)
     csr_wgrad_k32_kernel(WgK32 g, sysml_csr m, const float *__restrict__ dy,
                          float *__restrict__ part, float *__restrict__ dbpart) {
   extern __shared__ __align__(16) float sm[];
   const int PQ = g.P * g.Q;
-  const int bufsz = g.K * g.stride;
-  float *dys = sm + WG_GUARD;                                   // [nbuf][K][stride]
-  float *wpart = sm;  // [WG_WARPS][32][R_*S_ + 1], aliases the staging buffers after the loop
-  uint64_t *full = reinterpret_cast<uint64_t *>(dys + g.nbuf * bufsz + WG_GUARD);
-  uint64_t *empty = full + 2;
+  float *raw = sm;                          // [K][stride]
+  float *T = raw + g.K * g.stride;          // [PQ][32]
+  float *wpart = sm;                        // [WG_WARPS][32][R_*S_ + 1] (after the loop)
+  uint64_t *full = reinterpret_cast<uint64_t *>(T + PQ * 32);
+  uint64_t *empty = full + 1;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  // zero the staging region once: plane paddings and guards are read (and masked) but
-  // must hold finite values
-  {
-    float4 *z = reinterpret_cast<float4 *>(sm);
-    const int n4 = (g.nbuf * bufsz + 2 * WG_GUARD) / 4;
-    for (int i = threadIdx.x; i < n4; i += blockDim.x) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
   if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(full + b, 1);
-      ptx::mbar_init(empty + b, WG_WARPS);
-    }
+    ptx::mbar_init(full, 1);
+    ptx::mbar_init(empty, WG_WARPS);
     ptx::fence_mbar_init();
   }
-  ptx::fence_proxy_async_smem();
   __syncthreads();
   const int n0 = blockIdx.x * g.n_per_block, n1 = min(g.N, n0 + g.n_per_block);
 
   if (warp == WG_WARPS) {
     // ---------------- producer: one image's K dY planes per stage
     if (lane == 0) {
-      int buf = 0;
       uint32_t ph = 0;
-      for (int n = n0; n < n1; ++n) {
-        ptx::mbar_wait(empty + buf, ph ^ 1);
-        ptx::mbar_arrive_expect_tx(full + buf, (uint32_t)(g.K * PQ * 4));
+      for (int n = n0; n < n1; ++n, ph ^= 1) {
+        ptx::mbar_wait(empty, ph ^ 1);
+        ptx::mbar_arrive_expect_tx(full, (uint32_t)(g.K * PQ * 4));
         const float *src = dy + (int64_t)n * g.K * PQ;
-        float *dst = dys + buf * bufsz;
         for (int k = 0; k < g.K; ++k)
-          ptx::bulk_g2s(dst + k * g.stride, src + (int64_t)k * PQ, (uint32_t)(PQ * 4), full + buf);
-        if (++buf == g.nbuf) { buf = 0; ph ^= 1; }
+          ptx::bulk_g2s(raw + k * g.stride, src + (int64_t)k * PQ, (uint32_t)(PQ * 4), full);
       }
     }
     return;
@@ -349,13 +338,13 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 #pragma unroll
     for (int s_ = 0; s_ < S_; ++s_) acc[r][s_] = 0.f;
   float dbacc = 0.f;
-  // db slice of this warp: float4 groups [q0, q1) of the PQ/4 groups
   const int ng4 = PQ / 4;
   const int q0 = warp * ng4 / WG_WARPS, q1 = (warp + 1) * ng4 / WG_WARPS;
   const int HW = g.H * g.W;
+  const float *Tk = T + lane;
 
-  // non-zero j of image n is handled by warp (j - row_ptr[n]) % WG_WARPS; lane l holds the
-  // l-th of this warp's non-zeros of the round (prefetched one image ahead)
+  // non-zero j of image n is handled by warp (j - row_ptr[n]) % WG_WARPS; lane l holds
+  // the l-th of this warp's non-zeros of the round (prefetched one image ahead)
   int j0 = n0 < n1 ? __ldg(m.row_ptr + n0) : 0;
   int j1 = n0 < n1 ? __ldg(m.row_ptr + n0 + 1) : 0;
   int j2 = n0 + 1 < n1 ? __ldg(m.row_ptr + n0 + 2) : 0;
@@ -365,10 +354,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
     const int idx = j0 + warp + WG_WARPS * lane;
     if (n0 < n1 && idx < j1) { cur_col = __ldg(m.col_idx + idx); cur_val = __ldg(m.val + idx); }
   }
-  int buf = 0;
   uint32_t ph = 0;
-  for (int n = n0; n < n1; ++n) {
-    // prefetch the next image's first round of non-zeros and the row pointer after it
+  for (int n = n0; n < n1; ++n, ph ^= 1) {
     int nxt_col = -1;
     float nxt_val = 0.f;
     int j3 = 0;
@@ -377,53 +364,53 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
       if (idx < j2) { nxt_col = __ldg(m.col_idx + idx); nxt_val = __ldg(m.val + idx); }
       if (n + 2 < n1) j3 = __ldg(m.row_ptr + n + 3);
     }
-    ptx::mbar_wait(full + buf, ph);
-    const float *plane = dys + buf * bufsz + kk * g.stride;
-    // db[k] partial over this warp's slice (fixed order)
-    for (int q = q0; q < q1; ++q) {
-      const float4 e = lds4(plane + 4 * q);
-      dbacc += (e.x + e.y) + (e.z + e.w);
+    // T is free once every compute warp finished the previous image
+    ptx::named_bar_sync(1, WG_WARPS * 32);
+    ptx::mbar_wait(full, ph);
+    {
+      const float *plane = raw + kk * g.stride;
+      for (int q = q0; q < q1; ++q) {
+        const float4 e = lds4(plane + 4 * q);
+        dbacc += (e.x + e.y) + (e.z + e.w);  // db[k] partial, fixed order
+        float *t = T + (4 * q) * 32 + lane;
+        t[0] = e.x; t[32] = e.y; t[64] = e.z; t[96] = e.w;
+      }
     }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(empty);  // raw may be refilled (next image's copy)
+    ptx::named_bar_sync(1, WG_WARPS * 32);   // T complete
     const int mine = j1 - j0 > warp ? (j1 - j0 - warp + WG_WARPS - 1) / WG_WARPS : 0;
     for (int base = 0; base < mine; base += 32) {
       int bcol = cur_col;
       float bval = cur_val;
-      if (base > 0) {  // rare: more than 256 non-zeros in one image
+      if (base > 0) {  // rare: more than 32 * WG_WARPS non-zeros in one image
         const int idx = j0 + warp + WG_WARPS * (base + lane);
         bcol = idx < j1 ? __ldg(m.col_idx + idx) : -1;
         bval = idx < j1 ? __ldg(m.val + idx) : 0.f;
       }
       const int cnt = min(32, mine - base);
-      // lane-parallel decode of this round's non-zeros: code >= 0 -> interior non-zero
-      // (every tap in range) whose r = 0 window starts at dY position code; code <= -2 ->
-      // boundary non-zero with column -2 - code; -1 -> skip
+      // lane-parallel decode: code >= 0 -> interior non-zero (every tap in range) whose
+      // tap (0, S_-1) reads dY position code; code <= -2 -> boundary non-zero with column
+      // -2 - code; -1 -> skip
       int code = -1;
       if (bcol >= 0 && bcol < HW) {
         int h = __float2int_rz(((float)bcol + 0.5f) * g.invW);
         int w = bcol - h * g.W;
         if (w < 0) { --h; w += g.W; } else if (w >= g.W) { ++h; w -= g.W; }
         const int hp = h + g.ph, wp = w + g.pw;
-        const bool interior = g.q4 && hp >= R_ - 1 && hp < g.P && wp >= S_ - 1 && wp < g.Q;
+        const bool interior = hp >= R_ - 1 && hp < g.P && wp >= S_ - 1 && wp < g.Q;
         code = interior ? hp * g.Q + wp - (S_ - 1) : -2 - bcol;
       }
       for (int t = 0; t < cnt; ++t) {
         const int c = __shfl_sync(0xffffffffu, code, t);
         const float v = __shfl_sync(0xffffffffu, bval, t);
         if (c >= 0) {
-          // interior: all R_ x S_ taps valid; Q % 4 == 0 keeps the float4 phase o fixed
-          // across filter rows, so the tap -> register map is resolved once
-#define WG_FAST(O)                                                                \
-  case O: {                                                                       \
-    const float *p0 = plane + (c - O);                                            \
-    _Pragma("unroll") for (int r = 0; r < R_; ++r) {                              \
-      const float4 e0 = lds4(p0 - r * g.Q), e1 = lds4(p0 - r * g.Q + 4);          \
-      const float e[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};        \
-      _Pragma("unroll") for (int s_ = 0; s_ < S_; ++s_)                           \
-          acc[r][s_] = fmaf(v, e[O + S_ - 1 - s_], acc[r][s_]);                   \
-    }                                                                             \
-  } break;
-          switch (c & 3) { WG_FAST(0) WG_FAST(1) WG_FAST(2) WG_FAST(3) }
-#undef WG_FAST
+#pragma unroll
+          for (int r = 0; r < R_; ++r) {
+            const float *row = Tk + (c - r * g.Q) * 32;  // dY(p = hp - r, q = wp - (S_-1) + i)
+#pragma unroll
+            for (int s_ = 0; s_ < S_; ++s_) acc[r][s_] = fmaf(v, row[(S_ - 1 - s_) * 32], acc[r][s_]);
+          }
           continue;
         }
         if (c == -1) continue;  // out-of-range column: ignored
@@ -432,36 +419,24 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
         int w = col - h * g.W;
         if (w < 0) { --h; w += g.W; } else if (w >= g.W) { ++h; w -= g.W; }
         const int hp = h + g.ph, wp = w + g.pw;
-        float vs[S_];
-#pragma unroll
-        for (int s_ = 0; s_ < S_; ++s_) vs[s_] = (s_ <= wp && wp - s_ < g.Q) ? v : 0.f;
 #pragma unroll
         for (int r = 0; r < R_; ++r) {
           const int p = hp - r;
           if (p < 0 || p >= g.P) continue;
-          const int start = p * g.Q + wp - (S_ - 1);  // position of tap s = S_-1
-          const int a0 = start & ~3, o = start - a0;
-          const float4 e0 = lds4(plane + a0), e1 = lds4(plane + a0 + 4);
-          const float e[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
-          // dY position of tap s = start + (S_-1-s) -> e[o + S_-1-s]
-#define WG_CASE(O)                                                         \
-  case O:                                                                  \
-    _Pragma("unroll") for (int s_ = 0; s_ < S_; ++s_)                      \
-        acc[r][s_] = fmaf(vs[s_], e[O + S_ - 1 - s_], acc[r][s_]);         \
-    break;
-          switch (o) { WG_CASE(0) WG_CASE(1) WG_CASE(2) WG_CASE(3) }
-#undef WG_CASE
+#pragma unroll
+          for (int s_ = 0; s_ < S_; ++s_) {
+            const int q = wp - s_;
+            if (q < 0 || q >= g.Q) continue;
+            acc[r][s_] = fmaf(v, Tk[(p * g.Q + q) * 32], acc[r][s_]);
+          }
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(empty + buf);
-    if (++buf == g.nbuf) { buf = 0; ph ^= 1; }
     cur_col = nxt_col; cur_val = nxt_val;
     j0 = j1; j1 = j2; j2 = j3;
   }
-  // combine the warps' partials in a fixed order (staging buffers are free once every
-  // compute warp is past its last image)
+  // combine the warps' partials in a fixed order (the staging buffers are free once
+  // every compute warp is past its last image)
   ptx::named_bar_sync(1, WG_WARPS * 32);
   float *wp_ = wpart + (warp * 32 + lane) * (R_ * S_ + 1);
 #pragma unroll
@@ -484,15 +459,12 @@ WgK32 wgrad_k32_plan(const ConvArgs &a, int *blocks, size_t *smem) {
   WgK32 g{};
   g.N = a.N; g.K = a.K; g.H = a.H; g.W = a.W; g.P = a.P; g.Q = a.Q; g.ph = a.ph; g.pw = a.pw;
   const int PQ = a.P * a.Q;
-  int st = (PQ + 8 + 3) & ~3;
+  int st = (PQ + 3) & ~3;
   if (((st / 4) & 1) == 0) st += 4;  // stride/4 odd: lane-per-plane float4 reads conflict free
   g.stride = st;
   g.invW = 1.0f / (float)a.W;
-  g.q4 = (a.Q % 4) == 0;
-  const size_t fixed = sizeof(float) * 2 * WG_GUARD + 64;
-  const size_t per_buf = sizeof(float) * (size_t)a.K * st;
-  g.nbuf = fixed + 2 * per_buf <= 220 * 1024 ? 2 : 1;
-  *smem = std::max(fixed + g.nbuf * per_buf, sizeof(float) * WG_WARPS * 32 * (a.R * a.S + 1) + 64);
+  const size_t bytes = sizeof(float) * ((size_t)a.K * st + (size_t)PQ * 32) + 64;
+  *smem = std::max(bytes, sizeof(float) * WG_WARPS * 32 * (a.R * a.S + 1) + 64);
   int b = sm_count();
   if (b > a.N) b = a.N;
   if (b < 1) b = 1;
