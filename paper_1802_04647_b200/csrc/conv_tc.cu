@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nstage; ++s) {
-      ptx::mbar_init(full + s, 4 + 1);  // 4 producer warps + the expect_tx arrival
+      ptx::mbar_init(full + s, 128 + 1);  // 128 producer threads + the expect_tx arrival
       ptx::mbar_init(empty + s, 1);     // tcgen05.commit
     }
     for (int b = 0; b < 2; ++b) {
@@ -374,56 +374,37 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
             }
           }
         } else if (p.ks) {
-          // dense C == 1 input: element (pos, s) = x(pos + s) for s < S, 0 for S <= s < 8
-          for (int pb = tid; pb < p.HALO; pb += 2 * 128) {
-            float v[2][8];
+          // dense C == 1 input: element (pos, s) = x(pos + s) for s < S, 0 for S <= s < 8;
+          // 4-byte async copies (zero-filled where padded) -> no register round trip
+          for (int pos = tid; pos < p.HALO; pos += 128) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int pos = pb + u * 128;
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int off = (pos < p.HALO && e < p.S) ? src_off[pos + e] : -1;
-                v[u][e] = off >= 0 ? __ldg(p.x + off) : 0.f;
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int pos = pb + u * 128;
-              if (pos < p.HALO) {
-                st_shared_v4(a0 + pos * 16, v[u][0], v[u][1], v[u][2], v[u][3]);
-                st_shared_v4(a1 + pos * 16, v[u][4], v[u][5], v[u][6], v[u][7]);
-              }
+            for (int e = 0; e < 8; ++e) {
+              const int off = e < p.S ? src_off[pos + e] : -1;
+              ptx::cp_async4((e < 4 ? a0 : a1) + pos * 16 + (e & 3) * 4, off >= 0 ? p.x + off : p.x,
+                             off >= 0 ? 4u : 0u);
             }
           }
         } else {
-        const int c0 = ch * 8;
-        const int nc = min(8, p.C - c0);
-        const int64_t cstride = p.in_plane > 0 ? p.in_plane : (int64_t)HW;
-        const float *xc = p.x + c0 * cstride;
-        // 4 positions per iteration: all loads in flight before the stores
-        for (int pb = tid; pb < p.HALO; pb += 4 * 128) {
-          float v[4][8];
+          const int c0 = ch * 8;
+          const int nc = min(8, p.C - c0);
+          const int64_t cstride = p.in_plane > 0 ? p.in_plane : (int64_t)HW;
+          const float *xc = p.x + c0 * cstride;
+          for (int pos = tid; pos < p.HALO; pos += 128) {
+            const int off = src_off[pos];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int pos = pb + u * 128;
-            const int off = pos < p.HALO ? src_off[pos] : -1;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              v[u][j] = (off >= 0 && j < nc) ? __ldg(xc + off + j * cstride) : 0.f;
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int pos = pb + u * 128;
-            if (pos < p.HALO) {
-              st_shared_v4(a0 + pos * 16, v[u][0], v[u][1], v[u][2], v[u][3]);
-              st_shared_v4(a1 + pos * 16, v[u][4], v[u][5], v[u][6], v[u][7]);
+            for (int j = 0; j < 8; ++j) {
+              const bool ok = off >= 0 && j < nc;
+              ptx::cp_async4((j < 4 ? a0 : a1) + pos * 16 + (j & 3) * 4,
+                             ok ? xc + off + j * cstride : p.x, ok ? 4u : 0u);
             }
           }
         }
+        if (!p.is_csr) {
+          ptx::cp_async_mbar_arrive(full + stage);  // arrives when this thread's copies land
+        } else {
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(full + stage);
         }
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(full + stage);
         if (p.clk && tid == 0) p.clk[blockIdx.x * 8 + 1] += clock64() - t_f0;
         if (++stage == p.nstage) { stage = 0; phase ^= 1; }
       }
