@@ -86,6 +86,8 @@ struct TcFwdParams {
   int bias_smem;       // bias staged in shared memory (K floats)
   int ks;              // C == 1: the S column taps fill the MMA K slots (s = 4*half + e)
   int is_csr;          // KS mode only: input rows are CSR (scattered straight into the operand)
+  int mn;              // 1x1, pad 0, NCHW, H*W % 4 == 0: A staged MN-major with 16-byte copies
+                       // [pos/4][8 ch][4 pos] (no gather table, 4x fewer copy ops)
   sysml_csr csr;
   int64_t in_plane;    // > 0: input is SPF [C][in_plane], stored position = frame pos + in_shift
   int in_shift;
@@ -94,6 +96,7 @@ struct TcFwdParams {
   uint32_t a_bytes, b_bytes, stage_bytes, a_sbo;
   int64_t ntiles;
   uint32_t tmem_cols;
+  uint32_t tbuf;       // TMEM accumulator buffer stride: 256 (double buffer) or 0 (single, MT*NFpad <= 512)
 };
 
 struct TcPlan {
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
       ptx::named_bar_sync(1, 128);
       const int ntab = p.ks ? p.HALO + 8 : p.HALO;
-      for (int pos = tid; pos < (p.is_csr ? 0 : ntab); pos += 128) {
+      for (int pos = tid; pos < ((p.is_csr || p.mn) ? 0 : ntab); pos += 128) {
         const int64_t gi = g0 + pos;
         int off = -1;
         if (p.in_plane > 0) {
@@ -373,6 +376,22 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
               }
             }
           }
+        } else if (p.mn) {
+          // 1x1: lane -> (channel c = idx % 8, position group q4 = idx / 8); 16-byte copies
+          // of 4 consecutive positions of one channel plane (H*W % 4 == 0: never straddles
+          // an image), conflict-free 512-byte rows in shared memory
+          const int c0 = ch * 8;
+          for (int idx = tid; idx < (p.HALO / 4) * 8; idx += 128) {
+            const int c = idx & 7, q4 = idx >> 3;
+            const int64_t gi = g0 + 4 * q4;
+            bool ok = gi < p.G && c0 + c < p.C;
+            const float *src = p.x;
+            if (ok) {
+              const int n = (int)(gi / HW);
+              src = p.x + ((int64_t)n * p.C + c0 + c) * HW + (gi - (int64_t)n * HW);
+            }
+            ptx::cp_async16(a0 + q4 * 128 + c * 16, src, ok ? 16u : 0u);
+          }
         } else if (p.ks) {
           // dense C == 1 input: element (pos, s) = x(pos + s) for s < S, 0 for S <= s < 8;
           // 4-byte async copies (zero-filled where padded) -> no register round trip
@@ -412,7 +431,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
   } else {
     // ================= MMA issuer (warp 4) | epilogue (warps 5-12, TMEM quadrant warp % 4)
     const int qd = warp & 3;
-    const uint32_t idesc = ptx::make_idesc_tf32(128, p.NFpad);
+    const uint32_t idesc = p.mn ? ptx::make_idesc_tf32_amn(128, p.NFpad) : ptx::make_idesc_tf32(128, p.NFpad);
     int stage = 0;
     uint32_t phase = 0;
     const int PQ = p.P * p.Q;
@@ -421,7 +440,9 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++tcount) {
       const int ft = (int)(tile % p.nft);
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
-      const uint32_t buf = tcount & 1u, bphase = (tcount >> 1) & 1u;
+      // double buffer: buffers alternate; single buffer (tbuf 0): buffer 0 every tile
+      const uint32_t buf = p.tbuf ? (tcount & 1u) : 0u;
+      const uint32_t bphase = p.tbuf ? ((tcount >> 1) & 1u) : (tcount & 1u);
       if (warp == 4) {
         // Whole warp runs the issue loop: descriptors stay warp-uniform (uniform
         // registers, no per-MMA conversions).  TMEM columns are addressed from 0:
@@ -432,7 +453,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 3] += t_a1 - t_a0;
         ptx::tc_fence_after();
         const int n_inner = p.tile2d ? p.CT : 1;
-        const uint32_t step_outer = p.tile2d ? (uint32_t)(16 * p.Wf) : 128u;
+        // descriptor units of 16 B: K-major M-tile = 128 rows x 16 B; MN-major = 32 groups x 128 B
+        const uint32_t step_outer = p.tile2d ? (uint32_t)(16 * p.Wf) : (p.mn ? 256u : 128u);
         const uint32_t jump_outer = step_outer - 8u * (uint32_t)(n_inner - 1);
         const uint32_t nf = (uint32_t)p.NFpad;
         const uint32_t sbase = ptx::smem_u32(stage_base);
@@ -442,7 +464,10 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 2] += clock64() - t_w1;
           ptx::tc_fence_after();
           const uint32_t A = sbase + (uint32_t)stage * p.stage_bytes;
-          const uint64_t adesc0 = ptx::make_desc(A, p.HALO * 16, p.a_sbo);
+          // K-major: LBO = between the two channel quads, SBO = between 8-row groups;
+          // MN-major: SBO = between 4-position groups (128 B), LBO unused (K = 8 = one group)
+          const uint64_t adesc0 = p.mn ? ptx::make_desc(A, p.HALO * 32, 128)
+                                       : ptx::make_desc(A, p.HALO * 16, p.a_sbo);
           uint64_t bdesc = ptx::make_desc(A + p.a_bytes, nf * 16, 128);
           uint32_t acc = ch != 0 ? 1u : 0u;
           uint32_t drow = 0;
@@ -450,7 +475,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           for (int r = 0; r < p.R; ++r, drow += (uint32_t)p.Wf) {
             for (int s_ = 0; s_ < s_taps; ++s_) {
               uint64_t ad = adesc0 + (uint64_t)(drow + (uint32_t)s_);
-              uint32_t tm = buf * TMEM_BUF;
+              uint32_t tm = buf * p.tbuf;
               int ct = 0;
               for (int i = 0; i < p.MT; ++i) {
                 if (ptx::elect_one()) ptx::mma_tf32(tm, ad, bdesc, idesc, acc);
@@ -476,7 +501,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       __syncwarp();
       const long long t_epi0 = clock64();
       ptx::tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(qd * 32) << 16) + buf * TMEM_BUF;
+      const uint32_t tbase = tmem_base + ((uint32_t)(qd * 32) << 16) + buf * p.tbuf;
       const int eset = (warp - 5) >> 2;  // epilogue warp set 0 / 1 -> even / odd M-tiles
       if (p.pool) epi_pool2(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
       else epi_plain(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
@@ -498,8 +523,63 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
 // Repack filters into [ftile][chunk][tap][quad][NFpad][4] (zero padded).
 //  flip == 0: packed(k, c, t) = F[k][c][t]        (F is Kout x (Cin*RS))
 //  flip == 1: packed(k, c, t) = F[c][k][RS-1-t]   (F is Cin x (Kout*RS): bwd_data)
-__global__ void tc_pack_filters_kernel(const float *__restrict__ f, float *__restrict__ fp, int Kout,
-                                       int Cin, int RS, int NFpad, int nft, int nchunk, int flip) {
+constexpr int PACK_JB = 32;       // filters per pack block
+constexpr int PACK_MAX_RS = 40;   // taps supported by the staged pack (else per-element)
+
+// Block = (32-filter group, chunk, ftile): the filter rows it needs are contiguous in
+// F (8*RS floats per filter; for flip, 32*RS per input channel), so they are read
+// coalesced into shared memory and written out as [tap][quad][j][4] slabs.
+__global__ void __launch_bounds__(256) tc_pack_filters_kernel(
+    const float *__restrict__ f, float *__restrict__ fp, int Kout, int Cin, int RS, int NFpad,
+    int nft, int nchunk, int flip) {
+  __shared__ float sm[PACK_JB * 8 * PACK_MAX_RS];  // [j][c8 * RS + t]
+  const int njb = NFpad / PACK_JB;
+  const int jb = blockIdx.x % njb, ch = (blockIdx.x / njb) % nchunk, f_ = blockIdx.x / (njb * nchunk);
+  const int k0 = f_ * NFpad + jb * PACK_JB, c0 = ch * 8;
+  const int row = 8 * RS;
+  // 8 independent loads in flight per thread before the shared-memory stores
+  const int total = PACK_JB * row;
+  for (int base = threadIdx.x; base < total; base += 8 * blockDim.x) {
+    float v[8];
+    int dst[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * blockDim.x;
+      v[u] = 0.f;
+      dst[u] = -1;
+      if (i < total) {
+        if (!flip) {
+          const int j = i / row, r = i - j * row;
+          const int k = k0 + j, c = c0 + r / RS;
+          dst[u] = i;
+          if (k < Kout && c < Cin) v[u] = __ldg(f + ((size_t)k * Cin + c0) * RS + r);
+        } else {
+          const int crow = PACK_JB * RS;  // F[c][k0 .. k0+32)[*] is contiguous
+          const int cc = i / crow, r = i - cc * crow;
+          const int j = r / RS, t = r - j * RS;
+          const int k = k0 + j, c = c0 + cc;
+          dst[u] = j * row + cc * RS + t;
+          if (k < Kout && c < Cin) v[u] = __ldg(f + ((size_t)c * Kout + k0) * RS + r);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (dst[u] >= 0) sm[dst[u]] = v[u];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < RS * 2 * PACK_JB * 4; i += blockDim.x) {
+    const int e = i & 3, j = (i >> 2) % PACK_JB, g = (i >> 2) / PACK_JB % 2, tap = i / (2 * PACK_JB * 4);
+    const int src_t = flip ? RS - 1 - tap : tap;
+    const size_t slab = ((size_t)f_ * nchunk + ch) * RS + tap;
+    fp[slab * (8 * NFpad) + (size_t)(g * NFpad + jb * PACK_JB + j) * 4 + e] = sm[j * row + (g * 4 + e) * RS + src_t];
+  }
+}
+
+// fallback for RS > PACK_MAX_RS: one thread per packed element
+__global__ void tc_pack_filters_elem_kernel(const float *__restrict__ f, float *__restrict__ fp,
+                                            int Kout, int Cin, int RS, int NFpad, int nft,
+                                            int nchunk, int flip) {
   const int64_t total = (int64_t)nft * nchunk * RS * 2 * NFpad * 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -509,8 +589,7 @@ __global__ void tc_pack_filters_kernel(const float *__restrict__ f, float *__res
     const int g = (int)(t % 2); t /= 2;
     const int tap = (int)(t % RS); t /= RS;
     const int ch = (int)(t % nchunk); t /= nchunk;
-    const int f_ = (int)t;
-    const int k = f_ * NFpad + j, c = ch * 8 + g * 4 + e;
+    const int k = (int)t * NFpad + j, c = ch * 8 + g * 4 + e;
     float v = 0.f;
     if (k < Kout && c < Cin)
       v = flip ? f[((int64_t)c * Kout + k) * RS + (RS - 1 - tap)] : f[((int64_t)k * Cin + c) * RS + tap];
@@ -576,7 +655,13 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   p.b_bytes = (uint32_t)(b_taps * 2 * p.NFpad * 16);
   const int nsm = sm_count();
   const int64_t rows_total = (int64_t)N * p.Hs;
-  int mt_cap = std::min(16, (int)TMEM_BUF / p.NFpad);  // TMEM double buffer
+  // TMEM double buffer (epilogue overlaps the next tile's MMAs) unless B-heavy wide
+  // tiles want two M-tiles sharing each filter chunk (halves the L2 -> SMEM filter
+  // stream) -- then one 512-column accumulator
+  static const int single_env = getenv("SYSML_TC_SINGLEBUF") ? atoi(getenv("SYSML_TC_SINGLEBUF")) : -1;
+  const bool single = (single_env < 0 || single_env == 1) && p.NFpad == 256 && !pool;
+  p.tbuf = single ? 0u : TMEM_BUF;
+  int mt_cap = std::min(16, (single ? 512 : (int)TMEM_BUF) / p.NFpad);
   p.CT = (p.Q + 7) / 8;
   if (p.tile2d && p.CT > mt_cap) return pl;
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -596,7 +681,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
         halo = round_up(mt * 128 + (R - 1) * p.Wf + s_halo, 8);  // LBO multiple of 128 B
         ntiles = ceil_div(p.G, cta_pos) * p.nft;
       }
-      if (attempt == 0 && mt > 1 && ntiles < nsm) continue;  // keep the SMs busy first
+      if (attempt == 0 && mt > 1 && ntiles < nsm && !single) continue;  // keep the SMs busy first
       const uint32_t a_bytes = (uint32_t)(2 * halo * 16);
       const uint32_t stage = a_bytes + p.b_bytes;
       p.bias_smem = K <= 4096 ? 1 : 0;
@@ -620,7 +705,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   }
   if (!pl.ok) return pl;
   if (p.tile2d && (uint32_t)p.Wf * 16 >= (1u << 18)) { pl.ok = false; return pl; }
-  if (p.MT * p.NFpad > (int)TMEM_BUF) { pl.ok = false; return pl; }
+  if (p.MT * p.NFpad > (p.tbuf ? (int)p.tbuf : 512)) { pl.ok = false; return pl; }
   p.tmem_cols = 512;  // whole TMEM: base column 0 (1 CTA per SM), issue loops address from 0
   pl.fp_bytes = align_up((size_t)p.nft * p.nchunk * b_taps * 8 * p.NFpad * sizeof(float), 256);
   return pl;
@@ -639,6 +724,10 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
                      const float *bias, float *y, float *pout, int32_t *parg, void *ws,
                      cudaStream_t st, const TcSpfIO *io = nullptr, const sysml_csr *csr = nullptr) {
   TcFwdParams p = pl.p;
+  p.mn = (!io && !csr && !p.ks && !p.tile2d && p.R == 1 && p.S == 1 && p.ph == 0 && p.pw == 0 &&
+          (p.H * p.W) % 4 == 0 && ((uintptr_t)x & 15) == 0 &&
+          getenv("SYSML_TC_MN") != nullptr)  // opt-in: MN-major TF32 A reads as zeros so far
+             ? 1 : 0;
   if (csr) {
     if (!p.ks) {
       set_error("tcgen05 forward: CSR input needs the single-channel (KS) mode");
@@ -666,10 +755,16 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     tc_pack_filters_ks_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, p.R, p.S, p.NFpad, p.nft);
     SYSML_LAUNCH_CHECK();
   } else {
-    const int64_t total = (int64_t)p.nft * p.nchunk * p.R * p.S * 2 * p.NFpad * 4;
-    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * sm_count());
-    tc_pack_filters_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, f_cin, p.R * p.S, p.NFpad, p.nft,
-                                                   p.nchunk, flip);
+    const int RS = p.R * p.S;
+    if (RS <= PACK_MAX_RS && p.NFpad % PACK_JB == 0) {
+      tc_pack_filters_kernel<<<p.nft * p.nchunk * (p.NFpad / PACK_JB), 256, 0, st>>>(
+          f, fp, p.K, f_cin, RS, p.NFpad, p.nft, p.nchunk, flip);
+    } else {
+      const int64_t total = (int64_t)p.nft * p.nchunk * RS * 2 * p.NFpad * 4;
+      const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 8 * sm_count());
+      tc_pack_filters_elem_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, f_cin, RS, p.NFpad, p.nft,
+                                                           p.nchunk, flip);
+    }
     SYSML_LAUNCH_CHECK();
   }
   p.x = x;

@@ -183,6 +183,10 @@ __host__ __device__ constexpr uint32_t make_idesc_tf32(int M, int N) {
          | ((uint32_t)(N >> 3) << 17)   // n_dim
          | ((uint32_t)(M >> 4) << 24);  // m_dim
 }
+// same with A MN-major (positions contiguous in 16-byte groups)
+__host__ __device__ constexpr uint32_t make_idesc_tf32_amn(int M, int N) {
+  return make_idesc_tf32(M, N) | (1u << 15);
+}
 
 }  // namespace ptx
 }  // namespace sysml
