@@ -86,8 +86,6 @@ struct TcFwdParams {
   int bias_smem;       // bias staged in shared memory (K floats)
   int ks;              // C == 1: the S column taps fill the MMA K slots (s = 4*half + e)
   int is_csr;          // KS mode only: input rows are CSR (scattered straight into the operand)
-  int mn;              // 1x1, pad 0, NCHW, H*W % 4 == 0: A staged MN-major with 16-byte copies
-                       // [pos/4][8 ch][4 pos] (no gather table, 4x fewer copy ops)
   sysml_csr csr;
   int64_t in_plane;    // > 0: input is SPF [C][in_plane], stored position = frame pos + in_shift
   int in_shift;
@@ -322,7 +320,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
       ptx::named_bar_sync(1, 128);
       const int ntab = p.ks ? p.HALO + 8 : p.HALO;
-      for (int pos = tid; pos < ((p.is_csr || p.mn) ? 0 : ntab); pos += 128) {
+      for (int pos = tid; pos < (p.is_csr ? 0 : ntab); pos += 128) {
         const int64_t gi = g0 + pos;
         int off = -1;
         if (p.in_plane > 0) {
@@ -376,22 +374,6 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
               }
             }
           }
-        } else if (p.mn) {
-          // 1x1: lane -> (channel c = idx % 8, position group q4 = idx / 8); 16-byte copies
-          // of 4 consecutive positions of one channel plane (H*W % 4 == 0: never straddles
-          // an image), conflict-free 512-byte rows in shared memory
-          const int c0 = ch * 8;
-          for (int idx = tid; idx < (p.HALO / 4) * 8; idx += 128) {
-            const int c = idx & 7, q4 = idx >> 3;
-            const int64_t gi = g0 + 4 * q4;
-            bool ok = gi < p.G && c0 + c < p.C;
-            const float *src = p.x;
-            if (ok) {
-              const int n = (int)(gi / HW);
-              src = p.x + ((int64_t)n * p.C + c0 + c) * HW + (gi - (int64_t)n * HW);
-            }
-            ptx::cp_async16(a0 + q4 * 128 + c * 16, src, ok ? 16u : 0u);
-          }
         } else if (p.ks) {
           // dense C == 1 input: element (pos, s) = x(pos + s) for s < S, 0 for S <= s < 8;
           // 4-byte async copies (zero-filled where padded) -> no register round trip
@@ -431,7 +413,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
   } else {
     // ================= MMA issuer (warp 4) | epilogue (warps 5-12, TMEM quadrant warp % 4)
     const int qd = warp & 3;
-    const uint32_t idesc = p.mn ? ptx::make_idesc_tf32_amn(128, p.NFpad) : ptx::make_idesc_tf32(128, p.NFpad);
+    const uint32_t idesc = ptx::make_idesc_tf32(128, p.NFpad);
     int stage = 0;
     uint32_t phase = 0;
     const int PQ = p.P * p.Q;
@@ -453,8 +435,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 3] += t_a1 - t_a0;
         ptx::tc_fence_after();
         const int n_inner = p.tile2d ? p.CT : 1;
-        // descriptor units of 16 B: K-major M-tile = 128 rows x 16 B; MN-major = 32 groups x 128 B
-        const uint32_t step_outer = p.tile2d ? (uint32_t)(16 * p.Wf) : (p.mn ? 256u : 128u);
+        const uint32_t step_outer = p.tile2d ? (uint32_t)(16 * p.Wf) : 128u;
         const uint32_t jump_outer = step_outer - 8u * (uint32_t)(n_inner - 1);
         const uint32_t nf = (uint32_t)p.NFpad;
         const uint32_t sbase = ptx::smem_u32(stage_base);
@@ -464,10 +445,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 2] += clock64() - t_w1;
           ptx::tc_fence_after();
           const uint32_t A = sbase + (uint32_t)stage * p.stage_bytes;
-          // K-major: LBO = between the two channel quads, SBO = between 8-row groups;
-          // MN-major: SBO = between 4-position groups (128 B), LBO unused (K = 8 = one group)
-          const uint64_t adesc0 = p.mn ? ptx::make_desc(A, p.HALO * 32, 128)
-                                       : ptx::make_desc(A, p.HALO * 16, p.a_sbo);
+          const uint64_t adesc0 = ptx::make_desc(A, p.HALO * 16, p.a_sbo);
           uint64_t bdesc = ptx::make_desc(A + p.a_bytes, nf * 16, 128);
           uint32_t acc = ch != 0 ? 1u : 0u;
           uint32_t drow = 0;
@@ -724,10 +702,6 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
                      const float *bias, float *y, float *pout, int32_t *parg, void *ws,
                      cudaStream_t st, const TcSpfIO *io = nullptr, const sysml_csr *csr = nullptr) {
   TcFwdParams p = pl.p;
-  p.mn = (!io && !csr && !p.ks && !p.tile2d && p.R == 1 && p.S == 1 && p.ph == 0 && p.pw == 0 &&
-          (p.H * p.W) % 4 == 0 && ((uintptr_t)x & 15) == 0 &&
-          getenv("SYSML_TC_MN") != nullptr)  // opt-in: MN-major TF32 A reads as zeros so far
-             ? 1 : 0;
   if (csr) {
     if (!p.ks) {
       set_error("tcgen05 forward: CSR input needs the single-channel (KS) mode");
