@@ -73,6 +73,11 @@ struct TcSpfIO {
 
 // conv_tc.cu : tcgen05 TF32 implicit GEMM (SYSML_MATH_TF32)
 
+// K5 1x1 (stride 1, pad 0): TMA-fed GEMM over positions (wgrad_gemm.cu)
+bool tc_wgrad_1x1_supported(const ConvArgs &a);
+size_t tc_wgrad_1x1_ws(const ConvArgs &a);
+sysml_status tc_wgrad_1x1(const ConvArgs &a, const float *x, const float *dy, float *df,
+                          float *db, void *ws, cudaStream_t st);
 bool tc_fwd_supported(const ConvArgs &a, const PoolArgs *pool);
 // single-channel convs (C == 1, S <= 8) use the KS operand mode, which also reads CSR input
 bool tc_fwd_ks(const ConvArgs &a);

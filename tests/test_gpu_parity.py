@@ -53,6 +53,8 @@ CONV_SHAPES = [
     (3, 1, 17, 23, 20, 7, 3, 1, (3, 1)), # C = 1 (KS operand mode), tall kernel, ragged
     (2, 1, 9, 30, 5, 2, 8, 1, (0, 4)),   # C = 1, S = 8 (both K halves full)
     (2, 4, 9, 9, 1, 3, 3, 1, 1),         # K = 1 (bwd_data input has one channel)
+    (3, 48, 6, 6, 40, 1, 1, 1, 0),       # 1x1 TMA wgrad: one 128-filter tile, 48-channel tile
+    (2, 32, 4, 4, 300, 1, 1, 1, 0),      # 1x1 TMA wgrad: K > 256 (two filter-pair tiles), ragged
 ]
 
 

@@ -25,6 +25,19 @@ __device__ uint32_t a_off(int mode, int m, int k) {
       const uint32_t sw = lin ^ (((lin >> 7) & 1) << 4);
       return (m / 8) * 256 + sw + (m % 4) * 4;
     }
+    case 7: {  // K-major SW128: row m = 128 B (32 k), 16-B chunk ^= (m % 8); atoms of 8 rows at 1024 B
+      const int chunk = k / 4;
+      return m * 128 + ((chunk ^ (m % 8)) * 16) + (k % 4) * 4;
+    }
+    case 8: {  // K-major SW128, K offset 8 (second K-step inside the 128-B row): data at k+8
+      const int kk = k + 8, chunk = kk / 4;
+      return m * 128 + ((chunk ^ (m % 8)) * 16) + (kk % 4) * 4;
+    }
+    case 9: {  // K-major SW64: row m = 64 B (16 k), chunk ^= (m/2)%4 (Swizzle<2,4,3> on byte addr)
+      const uint32_t lin = m * 64 + (k / 4) * 16;
+      const uint32_t sw = lin ^ (((lin >> 7) & 3) << 4);
+      return sw + (k % 4) * 4;
+    }
     default: {  // SW64: atom 8 rows x 64 B (16 m), Swizzle<2,4,3>
       const int row = k % 8, chunk = (m % 16) / 4;
       const uint32_t lin = row * 64 + chunk * 16;
@@ -42,6 +55,9 @@ __device__ uint64_t a_desc(int mode, uint32_t A) {
     case 3: d = ptx::make_desc(A, 1024, 4096) | ((uint64_t)2 << 61); break;
     case 4: d = ptx::make_desc(A, 4096, 1024) | ((uint64_t)2 << 61); break;
     case 5: d = ptx::make_desc(A, 256, 4096) | ((uint64_t)6 << 61); break;
+    case 7: d = ptx::make_desc(A, 16, 1024) | ((uint64_t)2 << 61); break;
+    case 8: d = ptx::make_desc(A + 32, 16, 1024) | ((uint64_t)2 << 61); break;
+    case 9: d = ptx::make_desc(A, 16, 512) | ((uint64_t)4 << 61); break;
     default: d = ptx::make_desc(A, 512, 4096) | ((uint64_t)4 << 61); break;
   }
   return d;
@@ -70,7 +86,7 @@ __global__ void probe(int mode, float *D) {
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = tslot;
-  const uint32_t idesc = mode == 0 ? ptx::make_idesc_tf32(128, 16) : ptx::make_idesc_tf32_amn(128, 16);
+  const uint32_t idesc = (mode == 0 || mode >= 7) ? ptx::make_idesc_tf32(128, 16) : ptx::make_idesc_tf32_amn(128, 16);
   if (threadIdx.x == 0) {
     ptx::mma_tf32(tmem, a_desc(mode, A), ptx::make_desc(B, 16 * 16, 128), idesc, 0);
     ptx::mma_commit(&bar);
@@ -90,7 +106,7 @@ int main() {
   float *D;
   cudaMalloc(&D, 128 * 16 * 4);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  for (int mode = 0; mode < 7; ++mode) {
+  for (int mode = 0; mode < 10; ++mode) {
     cudaMemset(D, 0, 128 * 16 * 4);
     probe<<<1, 128, 64 * 1024>>>(mode, D);
     cudaError_t e = cudaDeviceSynchronize();
