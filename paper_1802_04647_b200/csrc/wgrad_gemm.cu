@@ -37,7 +37,10 @@ struct W1Params {
   int splits;
   int64_t iters;  // N * nblk
   float *part;    // [splits][K][C]
+  float *dbpart;  // [splits][K] (channel-tile-0 CTAs; nullptr: no db)
 };
+
+__device__ __forceinline__ void named_bar_sync_epi() { ptx::named_bar_sync(1, 128); }
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   // K-major, 128-byte swizzle: 8-row atoms of 1 KB (SBO), LBO unused
@@ -64,10 +67,11 @@ __global__ void __launch_bounds__(W1_THREADS, 1)
   const int k0 = mp * 256, c0 = nt * p.NB;
   const int64_t it0 = z * p.iters / p.splits, it1 = (z + 1) * p.iters / p.splits;
 
+  const bool do_db = p.dbpart != nullptr && nt == 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < W1_STAGES; ++s) {
       ptx::mbar_init(full + s, 1);
-      ptx::mbar_init(empty + s, 1);
+      ptx::mbar_init(empty + s, do_db ? 2 : 1);  // MMA commit (+ the db warp group)
     }
     ptx::mbar_init(accf, 1);
     ptx::fence_mbar_init();
@@ -121,8 +125,44 @@ __global__ void __launch_bounds__(W1_THREADS, 1)
     if (ptx::elect_one()) ptx::mma_commit(accf);
     __syncwarp();
   } else {
-    // epilogue: lane = filter row of this warp's TMEM quadrant, 16 channels per load
     const int qd = warp & 3;
+    const int et = threadIdx.x - 64;  // 0..127
+    // (1) while the MMAs run: db[k] partial = row sums of the staged dY tiles (channel
+    // tile 0 only; fixed order -> deterministic).  Thread et owns filter rows et and
+    // et + 128 of the A tile; a swizzled 128-byte row holds 32 positions.
+    float db0 = 0.f, db1 = 0.f;
+    if (do_db) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int64_t it = it0; it < it1; ++it) {
+        ptx::mbar_wait(full + stage, ph);
+        {
+          const float4 *row0 = reinterpret_cast<const float4 *>(smem + stage * stage_bytes + et * 128);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 v = row0[q];
+            db0 += (v.x + v.y) + (v.z + v.w);
+          }
+          if (p.mtiles > 1) {
+            const float4 *row1 = row0 + 128 * 8;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 v = row1[q];
+              db1 += (v.x + v.y) + (v.z + v.w);
+            }
+          }
+        }
+        named_bar_sync_epi();
+        if (et == 0) ptx::mbar_arrive(empty + stage);
+        if (++stage == W1_STAGES) { stage = 0; ph ^= 1; }
+      }
+    }
+    if (do_db) {
+      float *dbp = p.dbpart + (int64_t)z * p.K;
+      if (k0 + et < p.K) dbp[k0 + et] = db0;
+      if (p.mtiles > 1 && k0 + 128 + et < p.K) dbp[k0 + 128 + et] = db1;
+    }
+    // (2) epilogue: lane = filter row of this warp's TMEM quadrant, 16 channels per load
     const bool any = it1 > it0;
     if (any) ptx::mbar_wait_sleep(accf, 0);
     ptx::tc_fence_after();
@@ -160,19 +200,57 @@ __global__ void __launch_bounds__(W1_THREADS, 1)
   }
 }
 
-__global__ void w1_ordered_sum_kernel(const float *__restrict__ part, int parts, int64_t n,
-                                      float *__restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float acc = 0.f;
-    for (int z = 0; z < parts; ++z) acc += __ldg(part + (int64_t)z * n + i);
-    out[i] = acc;
+// Sum of the split partials (deterministic): each float4 output is owned by a group of
+// 4 lanes; lane q of the group sums splits z = q, q + 4, ... in increasing order and the
+// four partial sums are combined as (s0 + s1) + (s2 + s3).  Elements [0, n) are df,
+// [n, n + nb) are db (separate partial arrays).
+__global__ void w1_reduce_kernel(const float *__restrict__ part, const float *__restrict__ dbpart,
+                                 int parts, int64_t n, int nb, float *__restrict__ df,
+                                 float *__restrict__ db) {
+  const int64_t n4 = n / 4, nb4 = (nb + 3) / 4;
+  const int64_t total = n4 + (dbpart ? nb4 : 0) + (n % 4 ? 1 : 0);
+  const int q = threadIdx.x & 3;
+  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2; g < total;
+       g += ((int64_t)gridDim.x * blockDim.x) >> 2) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float *src;
+    int64_t stride, idx;
+    int cnt;
+    if (g < n4) { src = part; stride = n; idx = 4 * g; cnt = 4; }
+    else if (dbpart && g < n4 + nb4) { src = dbpart; stride = nb; idx = 4 * (g - n4); cnt = (int)(nb - idx < 4 ? nb - idx : 4); }
+    else { src = part; stride = n; idx = 4 * n4; cnt = (int)(n - 4 * n4); }
+    for (int z = q; z < parts; z += 4) {
+      const float *s = src + (int64_t)z * stride + idx;
+      if (cnt == 4 && src == part) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(s));
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      } else {
+        acc.x += __ldg(s);
+        if (cnt > 1) acc.y += __ldg(s + 1);
+        if (cnt > 2) acc.z += __ldg(s + 2);
+        if (cnt > 3) acc.w += __ldg(s + 3);
+      }
+    }
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {  // (s0 + s1) + (s2 + s3)
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+      acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
+      acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
+    }
+    if (q == 0) {
+      float *dst = (src == dbpart) ? db + idx : df + idx;
+      dst[0] = acc.x;
+      if (cnt > 1) dst[1] = acc.y;
+      if (cnt > 2) dst[2] = acc.z;
+      if (cnt > 3) dst[3] = acc.w;
+    }
   }
 }
 
 struct W1Plan {
   W1Params p;
-  size_t smem, part_bytes;
+  size_t smem, part_bytes, dbpart_bytes;
   int grid;
 };
 
@@ -194,6 +272,7 @@ W1Plan plan_w1(const ConvArgs &a) {
   const size_t stage = (size_t)p.mtiles * 128 * 128 + (size_t)p.NB * 128;
   pl.smem = 1024 + W1_STAGES * stage + 8 * (2 * W1_STAGES + 1) + 16;
   pl.part_bytes = align_up((size_t)splits * a.K * a.C * sizeof(float), 256);
+  pl.dbpart_bytes = align_up((size_t)splits * a.K * sizeof(float), 256);
   return pl;
 }
 
@@ -207,7 +286,8 @@ bool tc_wgrad_1x1_supported(const ConvArgs &a) {
 }
 
 size_t tc_wgrad_1x1_ws(const ConvArgs &a) {
-  return plan_w1(a).part_bytes + bias_grad_ws(a);
+  const W1Plan pl = plan_w1(a);
+  return pl.part_bytes + pl.dbpart_bytes;
 }
 
 sysml_status tc_wgrad_1x1(const ConvArgs &a, const float *x, const float *dy, float *df,
@@ -219,6 +299,7 @@ sysml_status tc_wgrad_1x1(const ConvArgs &a, const float *x, const float *dy, fl
   W1Plan pl = plan_w1(a);
   W1Params p = pl.p;
   p.part = reinterpret_cast<float *>(ws);
+  p.dbpart = db ? reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + pl.part_bytes) : nullptr;
   CUtensorMap tmA, tmB;
   const uint64_t hw = (uint64_t)p.HW;
   {
@@ -244,13 +325,10 @@ sysml_status tc_wgrad_1x1(const ConvArgs &a, const float *x, const float *dy, fl
   tc_wgrad_1x1_kernel<<<pl.grid, W1_THREADS, pl.smem, st>>>(tmA, tmB, p);
   SYSML_LAUNCH_CHECK();
   const int64_t total = (int64_t)a.K * a.C;
-  w1_ordered_sum_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 8 * sm_count()), 256, 0,
-                          st>>>(p.part, p.splits, total, df);
+  const int64_t groups = total / 4 + (db ? (a.K + 3) / 4 : 0) + 1;
+  w1_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(groups * 4, 256), 16 * sm_count()), 256, 0,
+                     st>>>(p.part, db ? p.dbpart : nullptr, p.splits, total, a.K, df, db);
   SYSML_LAUNCH_CHECK();
-  if (db) {
-    float *bpart = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + pl.part_bytes);
-    SYSML_TRY(launch_bias_grad(a, dy, db, bpart, st));
-  }
   return SYSML_OK;
 }
 
