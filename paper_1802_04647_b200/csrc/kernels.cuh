@@ -96,6 +96,11 @@ sysml_status tc_conv_fwd_spf(const ConvArgs &a, const TcSpfIO &io, const float *
 sysml_status tc_conv_bwd_data_spf(const ConvArgs &a, const TcSpfIO &io, const float *f,
                                   const float *dy, float *dx, void *ws, cudaStream_t st);
 bool tc_wgrad_spf_supported(const SpfConv &sc);
+// TMA-fed variant (wgrad_spf_tma.cu): ring of X atoms, no halo re-fetch
+bool tc_wgrad_spf_tma_supported(const SpfConv &sc);
+size_t tc_wgrad_spf_tma_ws(const SpfConv &sc);
+sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float *dy_spf,
+                              float *df, float *db, void *ws, cudaStream_t st);
 size_t tc_wgrad_spf_ws(const SpfConv &sc);
 sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy_spf, float *df,
                           float *db, void *ws, cudaStream_t st);

@@ -394,6 +394,7 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
       need = std::max(need, tc_fwd_ws(a2a));
       need = std::max(need, tc_bwd_data_ws(a2a));
       need = std::max(need, tc_wgrad_spf_ws(sc));
+      if (tc_wgrad_spf_tma_supported(sc)) need = std::max(need, tc_wgrad_spf_tma_ws(sc));
       ALLOC(h->a1s, 32 * h->spf_plane);
       ALLOC(h->dz2s, 64 * h->spf_plane);
       if (cudaMemset(h->a1s, 0, sizeof(float) * 32 * h->spf_plane) != cudaSuccess ||
@@ -538,7 +539,10 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     // B2f
     SYSML_TRY(T.begin(5));
     SpfConv sc{64, 32, 5, 5, 16, (int64_t)n * 256, h->spf_plane, h->spf_plane, 0, 0};
-    SYSML_TRY(tc_wgrad_spf(sc, h->a1s, h->dz2s, grads + OFF_F2, grads + OFF_B2, h->ws, st));
+    if (tc_wgrad_spf_tma_supported(sc))
+      SYSML_TRY(tc_wgrad_spf_tma(sc, h->a1s, h->dz2s, grads + OFF_F2, grads + OFF_B2, h->ws, st));
+    else
+      SYSML_TRY(tc_wgrad_spf(sc, h->a1s, h->dz2s, grads + OFF_F2, grads + OFF_B2, h->ws, st));
     SYSML_TRY(T.end());
     // B2d: input frame (pad 2) position = stored output-frame position + 34
     SYSML_TRY(T.begin(6));

@@ -1,0 +1,444 @@
+// wgrad_spf_tma.cu -- K5 conv2d_backward_filter on stacked-planar-frame (SPF) tensors
+// (the LeNet step's conv2 bwd_filter, §8(c) def. 4), fed by TMA.
+//
+//   dF[k][c][r][s] = sum_g dY[k][g] * X[c][g + r*Wf + s]        (g: frame position)
+//
+// GEMM over frame positions g (contiguous in SPF planes -> K-major tcgen05 operands
+// straight from HBM with 128-byte-swizzled TMA boxes of 32 positions = one "atom"):
+//   A rows (j, k): dY[k][g - j*Wf]          j < copies (= 128 / Kc): TMA box at g - j*Wf
+//   B rows (s, c): X[c][g + s]              s < S: one TMA box per s
+//   D_rb[(j,k)][(s,c)] = sum_g A . B(g + rb*copies*Wf)  ->  r = rb*copies + j
+// The rb shift (copies*Wf positions) is a whole number of atoms, so it is a descriptor
+// offset into a ring of B atoms: each X atom is loaded once and used by RG MMAs of
+// consecutive A atoms (no halo re-fetch).  All RG accumulators (RG * S*C columns) live
+// in TMEM; split-K over positions, partials reduced in a fixed order.
+//
+// Warp roles: warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 db (during the loop,
+// from the staged dY atoms) and epilogue (TMEM quadrant warp % 4).
+#include "common.cuh"
+#include "kernels.cuh"
+#include "tc_ptx.cuh"
+#include "tma.cuh"
+
+#include <algorithm>
+
+namespace sysml {
+
+namespace {
+
+constexpr int W2_NA = 4;          // A ring (dY atoms)
+constexpr int W2_THREADS = 224;  // + warp 6: B (X atom) producer
+constexpr int W2_ATOM = 32;       // positions per atom (128-byte swizzled row)
+
+struct W2Params {
+  int K, C, R, S, Wf;
+  int Kc, copies, RG, N;          // N = S*C
+  int rbstep;                     // atoms per rb shift (copies*Wf/32)
+  int nbr;                        // B ring slots
+  int64_t atoms;                  // ceil(G / 32)
+  int splits;
+  float *part;                    // [split][RG][128][N]
+  float *dbpart;                  // [split][K] or null
+  int dbg;                        // debug: 1 = skip the MMAs
+  const float *x;                 // X plane base (+ x_shift) for the shifted B rows
+  int64_t G, plane_x;
+  int ntma_s;                     // column taps s with s % 4 == 0 (TMA-loaded)
+  long long *clk;                 // optional per-CTA cycle counters (SYSML_TC_PROFILE)
+};
+
+__device__ __forceinline__ void st_shared_v4_w2(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
+  return ptx::make_desc(saddr, 16, 1024) | ((uint64_t)2 << 61);
+}
+
+__global__ void __launch_bounds__(W2_THREADS, 1)
+    tc_wgrad_spf_tma_kernel(const __grid_constant__ CUtensorMap tmDy,
+                            const __grid_constant__ CUtensorMap tmX, const W2Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const uint32_t a_slot = 128 * 128;                  // 16 KB
+  const uint32_t b_slot = (uint32_t)p.N * 128;        // N rows x 128 B
+  uint8_t *Aring = smem, *Bring = smem + W2_NA * a_slot;
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(Bring + p.nbr * b_slot);
+  uint64_t *emptyA = fullA + W2_NA;
+  uint64_t *fullB = emptyA + W2_NA;    // B atom complete (helper warps)
+  uint64_t *emptyB = fullB + p.nbr;
+  uint64_t *fullBt = emptyB + p.nbr;   // TMA part of a B atom landed
+  uint64_t *accf = fullBt + p.nbr;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(accf + 1);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int z = blockIdx.x;
+  const int64_t a0 = z * p.atoms / p.splits, a1 = (z + 1) * p.atoms / p.splits;
+  const int L = (p.RG - 1) * p.rbstep;  // B lookahead (atoms)
+  const bool do_db = p.dbpart != nullptr && !(p.dbg & 4);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < W2_NA; ++i) {
+      ptx::mbar_init(fullA + i, 1);
+      ptx::mbar_init(emptyA + i, do_db ? 2 : 1);
+    }
+    for (int i = 0; i < p.nbr; ++i) {
+      ptx::mbar_init(fullB + i, 4);   // the 4 helper warps (after they saw the TMA part)
+      ptx::mbar_init(fullBt + i, 1);  // expect_tx
+      ptx::mbar_init(emptyB + i, 1);
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::fence_mbar_init();
+    ptx::tma_prefetch_desc(&tmDy);
+    ptx::tma_prefetch_desc(&tmX);
+  }
+  if (warp == 1) ptx::tmem_alloc(tslot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t sA = ptx::smem_u32(Aring), sB = ptx::smem_u32(Bring);
+  const int64_t nA = a1 - a0, nB = a1 > a0 ? nA + L : 0;
+
+  const long long tk0 = clock64();
+  if (warp == 0) {
+    if (lane == 0) {
+      // B atom bi (= a0 + bi) goes to slot bi % nbr; A atom ai to slot ai % NA.  (No
+      // lambdas here: the tensor-map parameters must be addressed in param space.)
+      // A producer (dY atoms); the B producer is warp 6 so neither blocks the other.
+      // Ring cursors advance incrementally (no divisions in the issue loops).
+      int sa = 0;
+      uint32_t pa = 0;
+      for (int ia = 0; ia < (int)nA; ++ia) {
+        const long long t0 = clock64();
+        ptx::mbar_wait(emptyA + sa, pa ^ 1);
+        if (p.clk) p.clk[blockIdx.x * 8 + 4] += clock64() - t0;
+        ptx::mbar_arrive_expect_tx(fullA + sa, a_slot);
+        const int g = (int)((a0 + ia) * W2_ATOM);
+        for (int j = 0; j < p.copies; ++j)
+          ptx::tma_load_3d(sA + sa * a_slot + j * p.Kc * 128, &tmDy, g - j * p.Wf, 0, 0,
+                           ptx::smem_u32(fullA + sa));
+        if (++sa == W2_NA) { sa = 0; pa ^= 1; }
+      }
+    }
+  } else if (warp == 6) {
+    if (lane == 0) {
+      // B producer: the s % 4 == 0 column taps of X atoms 0 .. nB (atom nB feeds the
+      // tail of the last shifted rows) as fast as ring slots free up.  TMA needs
+      // 16-byte aligned inner coordinates, so the helper warps build the other shifts.
+      const int nBt = nA > 0 ? (int)nB + 1 : 0;
+      int sb = 0;
+      uint32_t pb = 0;
+      for (int ib = 0; ib < nBt; ++ib) {
+        const long long t0 = clock64();
+        ptx::mbar_wait(emptyB + sb, pb ^ 1);
+        if (p.clk) p.clk[blockIdx.x * 8 + 5] += clock64() - t0;
+        ptx::mbar_arrive_expect_tx(fullBt + sb, (uint32_t)(p.ntma_s * p.C * 128));
+        const int g = (int)((a0 + ib) * W2_ATOM);
+        for (int s = 0; s < p.S; s += 4)
+          ptx::tma_load_3d(sB + sb * b_slot + s * p.C * 128, &tmX, g + s, 0, 0,
+                           ptx::smem_u32(fullBt + sb));
+        if (++sb == p.nbr) { sb = 0; pb ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = ptx::make_idesc_tf32(128, p.N);
+    int sbw = 0;  // B ring cursor of the waits (atoms 0, 1, ... in order)
+    uint32_t pbw = 0;
+    for (int bi = 0; bi < (int)std::min<int64_t>(L, nB); ++bi) {
+      ptx::mbar_wait(fullB + sbw, pbw);
+      if (++sbw == p.nbr) { sbw = 0; pbw ^= 1; }
+    }
+    int sa = 0, s_ai = 0;  // A cursor; B slot of atom ai
+    uint32_t pa = 0;
+    for (int ai = 0; ai < (int)nA; ++ai) {
+      const long long t0 = clock64();
+      ptx::mbar_wait(fullA + sa, pa);
+      const long long t1 = clock64();
+      ptx::mbar_wait(fullB + sbw, pbw);  // newest B atom this group needs (ai + L)
+      if (++sbw == p.nbr) { sbw = 0; pbw ^= 1; }
+      if (p.clk && lane == 0) {
+        p.clk[blockIdx.x * 8 + 0] += t1 - t0;
+        p.clk[blockIdx.x * 8 + 1] += clock64() - t1;
+      }
+      ptx::tc_fence_after();
+      const uint32_t A = sA + sa * a_slot;
+      uint32_t Bslot[4];
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb) {
+        int sl = s_ai + rb * p.rbstep;
+        if (sl >= p.nbr) sl -= p.nbr;
+        Bslot[rb] = sB + (uint32_t)sl * b_slot;
+      }
+#pragma unroll
+      for (int kk = 0; kk < W2_ATOM / 8; ++kk) {
+        const uint64_t ad = sw128(A + kk * 32);
+        const uint32_t acc = (ai | kk) != 0 ? 1u : 0u;
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) {
+          if (rb < p.RG) {
+            if (!p.dbg && ptx::elect_one())
+              ptx::mma_tf32(tmem + rb * p.N, ad, sw128(Bslot[rb] + kk * 32), idesc, acc);
+            __syncwarp();
+          }
+        }
+      }
+      if (ptx::elect_one()) {
+        ptx::mma_commit(emptyA + sa);
+        ptx::mma_commit(emptyB + s_ai);  // B atom ai has no later user
+      }
+      __syncwarp();
+      if (++sa == W2_NA) { sa = 0; pa ^= 1; }
+      if (++s_ai == p.nbr) s_ai = 0;
+    }
+    if (ptx::elect_one()) ptx::mma_commit(accf);
+    __syncwarp();
+  } else {
+    const int et = threadIdx.x - 64;  // 0..127
+    const int qd = warp & 3;
+    // Merged loop in the producer's order: (1) the B rows of column taps s % 4 != 0 of
+    // atom bi -- X[c][g + s] from two aligned float4 loads, shifted in registers, stored
+    // into the 128-byte-swizzled row (16-byte chunk q ^ (row % 8)); (2) db[k] over this
+    // CTA's dY atoms (rows k of copy j = 0), two threads per row.
+    float dbv = 0.f;
+    const int npre = (int)std::min<int64_t>(L, nB);
+    const int drow = et >> 1, dhalf = et & 1;
+    // shift tasks (channel c, 16-byte chunk q) of this thread: t = et, et + 128 (C*8 <= 256).
+    // Source: the TMA-loaded s = 0 tile of atom bi (chunk q) and, for q = 7, chunk 0 of
+    // atom bi + 1 (next ring slot); both rows are 128-byte swizzled (chunk q at q ^ (c & 7)).
+    const int ntask = p.C * 8;
+    int sb = 0, sa = 0;
+    uint32_t pb = 0, pa = 0;
+    for (int step = -npre; step < (int)nA; ++step) {
+      const int bi = step + npre;
+      if (bi < nB) {
+        const int slot = sb, slot1 = sb + 1 == p.nbr ? 0 : sb + 1;
+        const uint32_t ph1 = sb + 1 == p.nbr ? pb ^ 1 : pb;
+        const long long t0 = clock64();
+        ptx::mbar_wait(fullBt + slot, pb);
+        ptx::mbar_wait(fullBt + slot1, ph1);
+        if (p.clk && et == 0) p.clk[blockIdx.x * 8 + 2] += clock64() - t0;
+        if (++sb == p.nbr) { sb = 0; pb ^= 1; }
+        const uint8_t *B0 = Bring + slot * b_slot, *B1 = Bring + slot1 * b_slot;
+        const uint32_t Bs = sB + slot * b_slot;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int t = et + u * 128;
+          if (t >= ntask) continue;
+          const int c = t >> 3, q = t & 7;
+          const float4 v0 = *reinterpret_cast<const float4 *>(B0 + c * 128 + ((q ^ (c & 7)) << 4));
+          const float4 v1 = q < 7 ? *reinterpret_cast<const float4 *>(B0 + c * 128 + (((q + 1) ^ (c & 7)) << 4))
+                                  : *reinterpret_cast<const float4 *>(B1 + c * 128 + ((c & 7) << 4));
+          const float e[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+          for (int s_ = 1; s_ < p.S; ++s_) {
+            if ((s_ & 3) == 0) continue;
+            const int row = s_ * p.C + c;
+            const uint32_t dst = Bs + row * 128 + ((q ^ (row & 7)) << 4);
+            const int o = s_ & 3;
+            float w0, w1, w2, w3;
+            if (o == 1) { w0 = e[1]; w1 = e[2]; w2 = e[3]; w3 = e[4]; }
+            else if (o == 2) { w0 = e[2]; w1 = e[3]; w2 = e[4]; w3 = e[5]; }
+            else { w0 = e[3]; w1 = e[4]; w2 = e[5]; w3 = e[6]; }
+            st_shared_v4_w2(dst, w0, w1, w2, w3);
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(fullB + slot);
+      }
+      if (step >= 0 && do_db) {
+        const int slotA = sa;
+        const long long t0 = clock64();
+        ptx::mbar_wait(fullA + slotA, pa);
+        if (++sa == W2_NA) { sa = 0; pa ^= 1; }
+        if (p.clk && et == 0) p.clk[blockIdx.x * 8 + 3] += clock64() - t0;
+        if (drow < p.Kc) {
+          const float4 *rp = reinterpret_cast<const float4 *>(Aring + slotA * a_slot + drow * 128) + dhalf * 4;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 v = rp[q];
+            dbv += (v.x + v.y) + (v.z + v.w);
+          }
+        }
+        ptx::named_bar_sync(1, 128);
+        if (et == 0) ptx::mbar_arrive(emptyA + slotA);
+      }
+    }
+    if (do_db) {
+      dbv += __shfl_xor_sync(0xffffffffu, dbv, 1);
+      if ((et & 1) == 0 && (et >> 1) < p.K) p.dbpart[(int64_t)z * p.K + (et >> 1)] = dbv;
+    }
+    if (nA > 0) ptx::mbar_wait_sleep(accf, 0);
+    ptx::tc_fence_after();
+    const int row = qd * 32 + lane;
+    float *dst = p.part + (int64_t)z * p.RG * 128 * p.N;
+    for (int rb = 0; rb < p.RG; ++rb)
+      for (int cb = 0; cb < p.N; cb += 16) {
+        float v[16];
+        if (nA > 0) {
+          ptx::tmem_ld16(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(rb * p.N + cb), v);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        }
+        float4 *o = reinterpret_cast<float4 *>(dst + ((int64_t)rb * 128 + row) * p.N + cb);
+        o[0] = make_float4(v[0], v[1], v[2], v[3]);
+        o[1] = make_float4(v[4], v[5], v[6], v[7]);
+        o[2] = make_float4(v[8], v[9], v[10], v[11]);
+        o[3] = make_float4(v[12], v[13], v[14], v[15]);
+      }
+  }
+  if (p.clk && threadIdx.x == 32) p.clk[blockIdx.x * 8 + 6] = clock64() - tk0;
+  if (p.clk && threadIdx.x == 64) p.clk[blockIdx.x * 8 + 7] = clock64() - tk0;
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+// dF[k][c][r][s] = sum over splits (fixed order) of D_rb[(j,k)][(s,c)], r = rb*copies + j
+__global__ void w2_reduce_kernel(const W2Params p, float *__restrict__ df, float *__restrict__ db) {
+  const int RS = p.R * p.S;
+  const int64_t total = (int64_t)p.K * p.C * RS;
+  const int64_t split_stride = (int64_t)p.RG * 128 * p.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i / ((int64_t)p.C * RS));
+    const int rem = (int)(i - (int64_t)k * p.C * RS);
+    const int c = rem / RS, t = rem - c * RS, r = t / p.S, s = t - r * p.S;
+    const int rb = r / p.copies, j = r - rb * p.copies;
+    const int64_t off = ((int64_t)rb * 128 + j * p.Kc + k) * p.N + s * p.C + c;
+    float acc = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp) acc += __ldg(p.part + sp * split_stride + off);
+    df[i] = acc;
+  }
+  if (db)
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < p.K;
+         k += (int64_t)gridDim.x * blockDim.x) {
+      float acc = 0.f;
+      for (int sp = 0; sp < p.splits; ++sp) acc += __ldg(p.dbpart + (int64_t)sp * p.K + k);
+      db[k] = acc;
+    }
+}
+
+struct W2Plan {
+  W2Params p;
+  size_t smem, part_bytes, dbpart_bytes;
+  bool ok;
+};
+
+W2Plan plan_w2(const SpfConv &sc) {
+  W2Plan pl{};
+  W2Params &p = pl.p;
+  pl.ok = false;
+  p.K = sc.K; p.C = sc.C; p.R = sc.R; p.S = sc.S; p.Wf = sc.Wf;
+  if (sc.K > 128 || sc.C % 8 || sc.C > 32 || sc.x_shift % 4 || sc.dy_shift % 4 || sc.plane_x % 4 ||
+      sc.plane_dy % 4 || sc.G <= 0)
+    return pl;
+  p.Kc = sc.K <= 16 ? 16 : sc.K <= 32 ? 32 : sc.K <= 64 ? 64 : 128;
+  p.copies = std::min(128 / p.Kc, sc.R);
+  while (p.copies > 1 && (p.copies * sc.Wf) % W2_ATOM) --p.copies;
+  if ((p.copies * sc.Wf) % W2_ATOM) return pl;
+  p.rbstep = p.copies * sc.Wf / W2_ATOM;
+  p.RG = (sc.R + p.copies - 1) / p.copies;
+  p.N = sc.S * sc.C;
+  if (p.N % 16 || p.N > 256 || p.RG * p.N > 512 || p.RG > 4) return pl;
+  // B ring: >= L + 2 (atom bi + 1 resident while bi is shifted) plus run-ahead slots
+  size_t smem = 0;
+  for (p.nbr = (p.RG - 1) * p.rbstep + 6; p.nbr >= (p.RG - 1) * p.rbstep + 3; --p.nbr) {
+    smem = 1024 + (size_t)W2_NA * 128 * 128 + (size_t)p.nbr * p.N * 128 +
+           8 * (2 * W2_NA + 3 * p.nbr + 1) + 16;
+    if (smem <= 227 * 1024) break;
+  }
+  if (smem > 227 * 1024) return pl;
+  p.atoms = ceil_div(sc.G, W2_ATOM);
+  int splits = sm_count();
+  if (splits > p.atoms) splits = (int)p.atoms;
+  p.splits = std::max(1, splits);
+  pl.smem = smem;
+  pl.part_bytes = align_up((size_t)p.splits * p.RG * 128 * p.N * sizeof(float), 256);
+  pl.dbpart_bytes = align_up((size_t)p.splits * p.K * sizeof(float), 256);
+  pl.ok = true;
+  return pl;
+}
+
+}  // namespace
+
+bool tc_wgrad_spf_tma_supported(const SpfConv &sc) {
+  return device_cc_major() == 10 && plan_w2(sc).ok && getenv("SYSML_NO_TMA_WGRAD") == nullptr;
+}
+
+size_t tc_wgrad_spf_tma_ws(const SpfConv &sc) {
+  const W2Plan pl = plan_w2(sc);
+  return pl.ok ? pl.part_bytes + pl.dbpart_bytes : 0;
+}
+
+sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float *dy_spf,
+                              float *df, float *db, void *ws, cudaStream_t st) {
+  W2Plan pl = plan_w2(sc);
+  if (!pl.ok) {
+    set_error("tcgen05 TMA SPF bwd_filter: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  const float *xb = x_spf + sc.x_shift, *dyb = dy_spf + sc.dy_shift;
+  if (((uintptr_t)xb & 15) || ((uintptr_t)dyb & 15)) {
+    set_error("tcgen05 TMA SPF bwd_filter: planes must be 16-byte aligned");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  W2Params p = pl.p;
+  p.dbg = getenv("SYSML_W2_DBG") ? atoi(getenv("SYSML_W2_DBG")) : 0;
+  p.x = xb;
+  p.G = sc.G;
+  p.plane_x = sc.plane_x;
+  p.ntma_s = (sc.S + 3) / 4;
+  p.part = reinterpret_cast<float *>(ws);
+  p.dbpart = db ? reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + pl.part_bytes) : nullptr;
+  CUtensorMap tmDy, tmX;
+  {
+    const uint64_t dims[3] = {(uint64_t)sc.G, (uint64_t)sc.K, 1};
+    const uint64_t strides[2] = {(uint64_t)sc.plane_dy * 4, (uint64_t)sc.plane_dy * 4 * sc.K};
+    const uint32_t box[3] = {W2_ATOM, (uint32_t)p.Kc, 1};
+    if (!tmap_encode_f32(&tmDy, dyb, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return SYSML_ERR_CUDA;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)sc.G, (uint64_t)sc.C, 1};
+    const uint64_t strides[2] = {(uint64_t)sc.plane_x * 4, (uint64_t)sc.plane_x * 4 * sc.C};
+    const uint32_t box[3] = {W2_ATOM, (uint32_t)sc.C, 1};
+    if (!tmap_encode_f32(&tmX, xb, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return SYSML_ERR_CUDA;
+  }
+  static int attr = 0;
+  if ((int)pl.smem > attr) {
+    SYSML_CUDA(cudaFuncSetAttribute(tc_wgrad_spf_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)pl.smem));
+    attr = (int)pl.smem;
+  }
+  static long long *dclk = nullptr;
+  const bool prof = getenv("SYSML_TC_PROFILE") != nullptr;
+  p.clk = nullptr;
+  if (prof) {
+    if (!dclk) cudaMalloc(&dclk, sizeof(long long) * 8 * 4096);
+    cudaMemsetAsync(dclk, 0, sizeof(long long) * 8 * 4096, st);
+    p.clk = dclk;
+  }
+  tc_wgrad_spf_tma_kernel<<<p.splits, W2_THREADS, pl.smem, st>>>(tmDy, tmX, p);
+  SYSML_LAUNCH_CHECK();
+  if (prof) {
+    static long long h[8 * 4096];
+    cudaMemcpyAsync(h, dclk, sizeof(long long) * 8 * p.splits, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double a[8] = {0};
+    for (int b = 0; b < p.splits; ++b)
+      for (int j = 0; j < 8; ++j) a[j] += (double)h[b * 8 + j] / p.splits;
+    fprintf(stderr, "[w2 splits=%d atoms/cta=%.0f] mma_wait_A %.0f mma_wait_B %.0f help_wait_emptyB %.0f "
+            "help_wait_fullA %.0f prod_wait_emptyA %.0f prod_wait_emptyB %.0f mma_total %.0f help_total %.0f\n",
+            p.splits, (double)p.atoms / p.splits, a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]);
+  }
+  const int64_t total = (int64_t)p.K * p.C * p.R * p.S;
+  w2_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 8 * sm_count()), 256, 0, st>>>(
+      p, df, db);
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
+}
+
+}  // namespace sysml
