@@ -73,6 +73,8 @@ struct TcFwdParams {
   float *y;           // plain output (N x K*P*Q) or null
   float *pout;        // pooled output or null
   int32_t *parg;      // pooled argmax or null
+  uint64_t *pcode;    // packed 4-bit window codes (LeNet-internal) or null: pcode[k/16][n*PpQp + pp*Qp + pc]
+  int64_t code_plane; // stride (64-bit words) of a 16-channel code group
   long long *clk;     // optional per-CTA cycle counters (SYSML_TC_PROFILE instrumentation)
   int N, C, H, W, K, R, S, ph, pw, P, Q;
   int Wf, Hs, Lf;
@@ -259,6 +261,99 @@ __device__ __forceinline__ void epi_pool2(const TcFwdParams &p, uint32_t tbase, 
               if (parg_t) parg_t[k0 * PpQp + j * PpQp] = ib + j * PQ + off[j];
             }
         }
+      }
+    };
+    for (int c16 = 0; c16 < nc16; c16 += 2) {
+      ptx::tmem_ld_wait(r0);
+      if (c16 + 1 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 1) * 16, r1);
+      process(r0, c16);
+      if (c16 + 1 < nc16) {
+        ptx::tmem_ld_wait(r1);
+        if (c16 + 2 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 2) * 16, r0);
+        process(r1, c16 + 1);
+      }
+    }
+  }
+}
+
+// Same fused bias + relu + 2x2/2 max-pool, LeNet-internal variant with a reduce-scatter
+// butterfly: round 1 (column partner, lane ^ 1) leaves each lane the pair-max of 8 of the
+// 16 channels, round 2 (row partner, lane ^ 8) the window max of 4 -- so each of the
+// window's four lanes owns 4 channels: 4 value stores and 16 bits of 4-bit codes
+// (positive*4 + dr*2 + ds, positive = window max > 0; ties -> the earlier position in
+// r-outer / s-inner order, readings R5/R7/R9).  relu'd values are >= +0.0, so they compare as unsigned integers; the later
+// position takes the partner's value when it is >= (u + 1 > u), the earlier when >.
+__device__ __forceinline__ void epi_pool2_code(const TcFwdParams &p, uint32_t tbase, int64_t g0,
+                                               int ft, int qd, int lane, const float *bias_s,
+                                               int i0, int istep) {
+  const int PpQp = p.Pp * p.Qp;
+  const int nc16 = p.NFpad / 16;
+  const int rl = qd * 4 + (lane >> 3), cl = lane & 7;
+  const uint32_t odd_c = cl & 1, odd_r = rl & 1;
+  const int cb = (int)(odd_c * 8 + odd_r * 4);  // first of the 4 channels this lane ends with
+  float *__restrict__ pout = p.pout;
+  for (int i = i0; i < p.MT; i += istep) {
+    const uint32_t trow = tbase + (uint32_t)(i * p.NFpad);
+    uint32_t r0[16], r1[16];
+    ptx::tmem_ld16_issue(trow, r0);
+    const int bb = i / p.CT, ct = i - bb * p.CT;
+    const int grow = (int)(g0 / p.Wf) + bb * 16 + rl;  // global frame row
+    const int col = ct * 8 + cl;
+    const int n = grow / p.Hs;
+    const int hh = grow - n * p.Hs;
+    const int pp = hh >> 1, pc = col >> 1;
+    const bool store = n < p.N && pp < p.Pp && pc < p.Qp;
+    const int vstride = p.out_plane > 0 ? (int)p.out_plane : PpQp;
+    const int64_t vbase = !store ? 0
+                          : p.out_plane > 0 ? (int64_t)n * p.out_Lf + (int64_t)(pp + p.out_off) * p.out_Wf +
+                                                  (pc + p.out_off)
+                                            : (int64_t)n * p.K * PpQp + (int64_t)pp * p.Qp + pc;
+    float *const pout_t = pout + vbase + (int64_t)cb * vstride;
+    uint16_t *const code_t = reinterpret_cast<uint16_t *>(p.pcode + (store ? (int64_t)n * PpQp + pp * p.Qp + pc : 0)) +
+                             (cb >> 2);
+    auto process = [&](const uint32_t(&cur)[16], int c16) {
+      const int k0 = ft * p.NFpad + c16 * 16;
+      float b[16];
+      uint32_t u[16];
+      load_bias16(p, bias_s, k0, b);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float t = __uint_as_float(cur[j]) + b[j];
+        u[j] = __float_as_uint(t > 0.f ? t : 0.f);  // relu, +0.0 for non-positive (reading R7)
+      }
+      // round 1: keep channels [8*odd_c, +8), send the other half to the column partner
+      uint32_t v8[8], sbit = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t send = odd_c ? u[j] : u[j + 8];
+        const uint32_t mine = odd_c ? u[j + 8] : u[j];
+        const uint32_t got = __shfl_xor_sync(0xffffffffu, send, 1);
+        const bool take = got + odd_c > mine;  // partner is the even (earlier) column iff odd_c
+        v8[j] = take ? got : mine;
+        sbit |= (odd_c ^ (uint32_t)take) << j;  // winner's column
+      }
+      // round 2: keep channels [cb, +4) of those 8, send the other 4 to the row partner
+      uint32_t v4[4];
+      const uint32_t psbit = __shfl_xor_sync(0xffffffffu, sbit, 8);
+      uint32_t code = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t send = odd_r ? v8[j] : v8[j + 4];
+        const uint32_t mine = odd_r ? v8[j + 4] : v8[j];
+        const uint32_t got = __shfl_xor_sync(0xffffffffu, send, 8);
+        const bool take = got + odd_r > mine;
+        v4[j] = take ? got : mine;
+        const int jj = (int)(odd_r * 4) + j;  // index among this lane's 8 channels
+        const uint32_t ds = ((take ? psbit : sbit) >> jj) & 1u;
+        const uint32_t pos = v4[j] != 0u;  // window max > 0: the relu/pool gradient mask (R9)
+        code |= ((pos << 2) | ((odd_r ^ (uint32_t)take) << 1) | ds) << (4 * j);
+      }
+      if (store) {
+        float *po = pout_t + (int64_t)k0 * vstride;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (k0 + cb + j < p.K) po[j * vstride] = __uint_as_float(v4[j]);
+        code_t[(int64_t)(k0 >> 4) * p.code_plane * 4] = (uint16_t)code;
       }
     };
     for (int c16 = 0; c16 < nc16; c16 += 2) {
@@ -481,7 +576,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(qd * 32) << 16) + buf * p.tbuf;
       const int eset = (warp - 5) >> 2;  // epilogue warp set 0 / 1 -> even / odd M-tiles
-      if (p.pool) epi_pool2(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
+      if (p.pool && p.pcode) epi_pool2_code(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
+      else if (p.pool) epi_pool2(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
       else epi_plain(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
       ptx::tc_fence_before();
       __syncwarp();
@@ -717,6 +813,12 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     p.out_Wf = io->out_Wf;
     p.out_Lf = io->out_Lf;
     p.out_off = io->out_off;
+    p.pcode = io->code;
+    p.code_plane = io->code_plane;
+    if (p.pcode && !(p.pool && p.tile2d)) {
+      set_error("tcgen05 forward: packed window codes need the fused 2x2 pool epilogue");
+      return SYSML_ERR_UNSUPPORTED;
+    }
   }
   float *fp = reinterpret_cast<float *>(ws);
   if (p.ks) {

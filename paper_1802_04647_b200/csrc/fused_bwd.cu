@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
 
 namespace sysml {
 
@@ -34,6 +35,8 @@ struct FusedB1Args {
   int n_per_cta;
   int64_t mask_plane;                           // > 0: mask is SPF [K][mask_plane]
   int mask_Wf, mask_Lf, mask_off;
+  const uint64_t *code;                         // non-null: argmax + mask as 4-bit window codes
+  int64_t code_plane;                           //   (TcSpfIO::code) -> the bulk kernel below
 };
 
 template <int R_, int S_>
@@ -48,6 +51,7 @@ __global__ void __launch_bounds__(FB_THREADS)
   const int k = t / a.tpk, j = t - k * a.tpk;
   const bool kok = k < a.K;
   const int PpQp = a.Pp * a.Qp, PQ = a.P * a.Q;
+  const float invQp = 1.0f / (float)a.Qp;  // exact floor for pp < 2^20 with the +0.5 offset
   float acc[RS];
 #pragma unroll
   for (int i = 0; i < RS; ++i) acc[i] = 0.f;
@@ -77,10 +81,12 @@ __global__ void __launch_bounds__(FB_THREADS)
     __syncthreads();
     if (!kok) continue;
     const int64_t base = (int64_t)n * a.K * PpQp + (int64_t)k * PpQp;
+    const int64_t mask_base = (int64_t)k * a.mask_plane + (int64_t)n * a.mask_Lf;
     // 8 pooled outputs per batch: all 24 global loads in flight before any use
     for (int pb = j; pb < PpQp; pb += 8 * a.tpk) {
       float gv[8], mv[8];
       int av[8];
+      // all global loads of the batch first; decoding happens after they are in flight
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int pp = pb + u * a.tpk;
@@ -91,9 +97,8 @@ __global__ void __launch_bounds__(FB_THREADS)
           if (mask) {
             int64_t mi = base + pp;
             if (a.mask_plane > 0) {
-              const int pr = pp / a.Qp, pc = pp - pr * a.Qp;
-              mi = (int64_t)k * a.mask_plane + (int64_t)n * a.mask_Lf + (pr + a.mask_off) * a.mask_Wf +
-                   pc + a.mask_off;
+              const int pr = __float2int_rz(((float)pp + 0.5f) * invQp), pc = pp - pr * a.Qp;
+              mi = mask_base + (pr + a.mask_off) * a.mask_Wf + pc + a.mask_off;
             }
             mv[u] = __ldg(mask + mi);
           }
@@ -128,6 +133,135 @@ __global__ void __launch_bounds__(FB_THREADS)
     float s = 0.f;
     for (int jj = 0; jj < a.tpk; ++jj) s += sred[i * FB_THREADS + kk * a.tpk + jj];
     part[(int64_t)blockIdx.x * nout + o] = s;
+  }
+}
+
+// Window-code variant (LeNet TF32 path, 2x2/2 pooling): the pool-gradient plane dpool[n]
+// (K x Pp*Qp, contiguous), the 4-bit window codes (positive*4 + dr*2 + ds: argmax and
+// relu mask, TcSpfIO::code) and the dense image x[n] are streamed into shared memory by
+// 1-D bulk async copies (2-stage ring, mbarrier completion) from a producer warp, so the
+// 256 compute threads only touch shared memory.  CSR images are scattered by the
+// compute threads from global memory.  Accumulation order as above (deterministic).
+constexpr int FBB_STAGES = 2;
+constexpr int FBB_THREADS = FB_THREADS + 32;
+
+template <int R_, int S_>
+__global__ void __launch_bounds__(FBB_THREADS)
+    pool_bwd_wgrad_c1_bulk_kernel(FusedB1Args a, const float *__restrict__ x, sysml_csr xcsr,
+                                  int is_csr, const float *__restrict__ dpool,
+                                  float *__restrict__ part) {
+  extern __shared__ __align__(16) uint8_t fbb_smem[];
+  constexpr int RS = R_ * S_;
+  const int PpQp = a.Pp * a.Qp, HW = a.H * a.W;
+  const int G = (a.K + 15) >> 4;
+  const uint32_t g_bytes = (uint32_t)(a.K * PpQp * 4), c_bytes = (uint32_t)(PpQp * 8),
+                 x_bytes = is_csr ? 0u : (uint32_t)(HW * 4);
+  const uint32_t stage_bytes = (g_bytes + G * c_bytes + x_bytes + 15) & ~15u;
+  float *img = reinterpret_cast<float *>(fbb_smem + FBB_STAGES * stage_bytes);  // Hp x Wp
+  uint64_t *full = reinterpret_cast<uint64_t *>(img + ((a.Hp * a.Wp + 3) & ~3));
+  uint64_t *empty = full + FBB_STAGES;
+  const int t = threadIdx.x;
+  const int warp = __shfl_sync(0xffffffffu, t >> 5, 0), lane = t & 31;
+  const int n0 = blockIdx.x * a.n_per_cta, n1 = min(a.N, n0 + a.n_per_cta);
+  for (int i = t; i < a.Hp * a.Wp; i += blockDim.x) img[i] = 0.f;  // zero border (= padding)
+  if (t == 0) {
+    for (int s_ = 0; s_ < FBB_STAGES; ++s_) {
+      ptx::mbar_init(full + s_, 1);
+      ptx::mbar_init(empty + s_, FB_THREADS / 32);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == FB_THREADS / 32) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int n = n0; n < n1; ++n) {
+        ptx::mbar_wait(empty + st, ph ^ 1);
+        ptx::mbar_arrive_expect_tx(full + st, g_bytes + G * c_bytes + x_bytes);
+        uint8_t *dst = fbb_smem + st * stage_bytes;
+        ptx::bulk_g2s(dst, dpool + (int64_t)n * a.K * PpQp, g_bytes, full + st);
+        for (int g = 0; g < G; ++g)
+          ptx::bulk_g2s(dst + g_bytes + g * c_bytes, a.code + g * a.code_plane + (int64_t)n * PpQp,
+                        c_bytes, full + st);
+        if (!is_csr)
+          ptx::bulk_g2s(dst + g_bytes + G * c_bytes, x + (int64_t)n * HW, x_bytes, full + st);
+        if (++st == FBB_STAGES) { st = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+  const int k = t / a.tpk, j = t - k * a.tpk;
+  const bool kok = k < a.K;
+  const float invQ = 1.0f / (float)a.Qp, invW = 1.0f / (float)a.W;
+  float acc[RS];
+#pragma unroll
+  for (int i = 0; i < RS; ++i) acc[i] = 0.f;
+  float dbacc = 0.f;
+  int st = 0;
+  uint32_t ph = 0;
+  for (int n = n0; n < n1; ++n) {
+    ptx::mbar_wait(full + st, ph);
+    const uint8_t *sb = fbb_smem + st * stage_bytes;
+    const float *gs = reinterpret_cast<const float *>(sb);
+    const unsigned long long *cs = reinterpret_cast<const unsigned long long *>(sb + g_bytes);
+    ptx::named_bar_sync(1, FB_THREADS);  // previous image's window reads are done
+    if (!is_csr) {
+      const float *xs = reinterpret_cast<const float *>(sb + g_bytes + G * c_bytes);
+      for (int i = t; i < HW; i += FB_THREADS) {
+        const int h = __float2int_rz(((float)i + 0.5f) * invW), w = i - h * a.W;
+        img[(h + a.ph) * a.Wp + w + a.pw] = xs[i];
+      }
+    } else {
+      for (int i = t; i < HW; i += FB_THREADS) {
+        const int h = __float2int_rz(((float)i + 0.5f) * invW), w = i - h * a.W;
+        img[(h + a.ph) * a.Wp + w + a.pw] = 0.f;
+      }
+      ptx::named_bar_sync(1, FB_THREADS);
+      const int j0 = __ldg(xcsr.row_ptr + n), j1 = __ldg(xcsr.row_ptr + n + 1);
+      for (int jj = j0 + t; jj < j1; jj += FB_THREADS) {
+        const int col = __ldg(xcsr.col_idx + jj);
+        if (col >= 0 && col < HW) {
+          const int h = col / a.W, w = col - h * a.W;
+          atomicAdd(img + (h + a.ph) * a.Wp + w + a.pw, __ldg(xcsr.val + jj));  // duplicates summed
+        }
+      }
+    }
+    ptx::named_bar_sync(1, FB_THREADS);  // image ready
+    if (kok) {
+      const float *gk = gs + k * PpQp;
+      const unsigned long long *ck = cs + (k >> 4) * PpQp;
+      const int sh = 4 * (k & 15);
+      for (int pp = j; pp < PpQp; pp += a.tpk) {
+        const float g0 = gk[pp];
+        const uint32_t cd = (uint32_t)(ck[pp] >> sh) & 15u;
+        if (!(cd & 4u) || g0 == 0.f) continue;  // masked (reading R9) or zero gradient
+        const int pr = __float2int_rz(((float)pp + 0.5f) * invQ), pc = pp - pr * a.Qp;
+        const float *win = img + (2 * pr + (int)((cd >> 1) & 1u)) * a.Wp + 2 * pc + (int)(cd & 1u);
+        dbacc += g0;
+#pragma unroll
+        for (int r = 0; r < R_; ++r)
+#pragma unroll
+          for (int s_ = 0; s_ < S_; ++s_) acc[r * S_ + s_] = fmaf(g0, win[r * a.Wp + s_], acc[r * S_ + s_]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(empty + st);
+    if (++st == FBB_STAGES) { st = 0; ph ^= 1; }
+  }
+  // fixed-order reduction of the tpk partials of each filter (reuses the stage ring)
+  ptx::named_bar_sync(1, FB_THREADS);
+  float *sred = reinterpret_cast<float *>(fbb_smem);
+#pragma unroll
+  for (int i = 0; i < RS; ++i) sred[i * FB_THREADS + t] = acc[i];
+  sred[RS * FB_THREADS + t] = dbacc;
+  ptx::named_bar_sync(1, FB_THREADS);
+  const int nout = a.K * (RS + 1);
+  for (int o = t; o < nout; o += FB_THREADS) {
+    const int kk = o / (RS + 1), i = o - kk * (RS + 1);
+    float sum = 0.f;
+    for (int jj = 0; jj < a.tpk; ++jj) sum += sred[i * FB_THREADS + kk * a.tpk + jj];
+    part[(int64_t)blockIdx.x * nout + o] = sum;
   }
 }
 
@@ -174,6 +308,8 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
     a.mask_Wf = mask_spf->out_Wf;
     a.mask_Lf = mask_spf->out_Lf;
     a.mask_off = mask_spf->out_off;
+    a.code = mask_spf->code;
+    a.code_plane = mask_spf->code_plane;
   }
   a.N = c.N; a.H = c.H; a.W = c.W; a.K = c.K; a.R = c.R; a.S = c.S; a.ph = c.ph; a.pw = c.pw;
   a.P = c.P; a.Q = c.Q; a.Pp = pa.P; a.Qp = pa.Q;
@@ -189,6 +325,28 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
   float *part = reinterpret_cast<float *>(ws);
   sysml_csr empty{};
   const sysml_csr &cs = xcsr ? *xcsr : empty;
+  if (a.code) {
+    if (pa.R != 2 || pa.S != 2 || ((uintptr_t)dpool & 15) || (!xcsr && ((uintptr_t)x & 15)) ||
+        ((int64_t)c.K * pa.P * pa.Q) % 4 || (pa.P * pa.Q) % 2 || (c.H * c.W) % 4) {
+      set_error("fused pool-bwd + conv1 wgrad: window codes need 2x2 pooling and 16-byte aligned planes");
+      return SYSML_ERR_UNSUPPORTED;
+    }
+    const int G = (c.K + 15) / 16;
+    const size_t stage = align_up((size_t)c.K * pa.P * pa.Q * 4 + (size_t)G * pa.P * pa.Q * 8 +
+                                      (xcsr ? 0 : (size_t)c.H * c.W * 4), 16);
+    const size_t smem_b = std::max(FBB_STAGES * stage, (size_t)FB_THREADS * (RS + 1) * 4) +
+                          align_up((size_t)a.Hp * a.Wp * 4, 16) + 8 * 2 * FBB_STAGES;
+    const size_t smem_bulk = FBB_STAGES * stage + align_up((size_t)a.Hp * a.Wp * 4, 16) + 8 * 2 * FBB_STAGES;
+    const size_t sm_need = std::max(smem_b, smem_bulk);
+    auto kern = RS == 25 ? pool_bwd_wgrad_c1_bulk_kernel<5, 5> : pool_bwd_wgrad_c1_bulk_kernel<3, 3>;
+    SYSML_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_need));
+    kern<<<used, FBB_THREADS, sm_need, st>>>(a, x, cs, xcsr != nullptr, dpool, part);
+    SYSML_LAUNCH_CHECK();
+    fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 256), 256, 0, st>>>(
+        part, used, c.K, RS, df, db);
+    SYSML_LAUNCH_CHECK();
+    return SYSML_OK;
+  }
   if (RS == 25) {
     static bool attr = false;
     if (!attr) {

@@ -69,6 +69,9 @@ struct TcSpfIO {
   int in_shift = 0;
   int64_t out_plane = 0;  // > 0: pooled output to SPF planes (pp + out_off) * out_Wf + pc + out_off
   int out_Wf = 0, out_Lf = 0, out_off = 0;
+  uint64_t *code = nullptr;  // pooled argmax + relu mask as packed 4-bit window codes
+  int64_t code_plane = 0;    // code[k/16][n*PpQp + pp*Qp + pc]: bits 4j..4j+3 of channel
+                             // 16g + j = positive*4 + dr*2 + ds (window winner (2pp+dr, 2pc+ds))
 };
 
 // conv_tc.cu : tcgen05 TF32 implicit GEMM (SYSML_MATH_TF32)

@@ -175,8 +175,7 @@ __global__ void da2_kernel(int n, const float *__restrict__ ds, const float *__r
 // is never materialised.  One thread per pooled output (n, k, pp, pc).
 __global__ void affine_bwd_route_spf_kernel(int n, const float *__restrict__ ds,
                                             const float *__restrict__ W3,
-                                            const float *__restrict__ a2,
-                                            const int32_t *__restrict__ i2,
+                                            const uint64_t *__restrict__ c2, int64_t cplane,
                                             float *__restrict__ dz2s, int64_t plane) {
   const int64_t total = (int64_t)n * D3;
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
@@ -184,16 +183,19 @@ __global__ void affine_bwd_route_spf_kernel(int n, const float *__restrict__ ds,
     const int s = (int)(o / D3);
     const int d = (int)(o - (int64_t)s * D3);  // = k*49 + pp*7 + pc
     const int k = d / 49, r = d - k * 49, pp = r / 7, pc = r - pp * 7;
+    // window code of the pool2 winner: positive*4 + dr*2 + ds (positive: a2 > 0, R9)
+    const uint32_t cd =
+        (uint32_t)(__ldg(reinterpret_cast<const unsigned long long *>(c2) + (int64_t)(k >> 4) * cplane +
+                         (int64_t)s * 49 + r) >> (4 * (k & 15))) & 15u;
     float g = 0.f;
-    if (__ldg(a2 + o) > 0.f) {
+    if (cd & 4u) {
 #pragma unroll
       for (int j = 0; j < NCLS; ++j) g = fmaf(__ldg(ds + s * NCLS + j), __ldg(W3 + j * D3 + d), g);
     }
-    const int am = __ldg(i2 + o) - k * 196;  // position inside the 14x14 plane
     float *base = dz2s + (int64_t)k * plane + (int64_t)s * 256 + (2 * pp) * 16 + 2 * pc;
-    const int a0 = (2 * pp) * 14 + 2 * pc;
-    float2 top = make_float2(am == a0 ? g : 0.f, am == a0 + 1 ? g : 0.f);
-    float2 bot = make_float2(am == a0 + 14 ? g : 0.f, am == a0 + 15 ? g : 0.f);
+    const uint32_t wp = cd & 3u;
+    float2 top = make_float2(wp == 0 ? g : 0.f, wp == 1 ? g : 0.f);
+    float2 bot = make_float2(wp == 2 ? g : 0.f, wp == 3 ? g : 0.f);
     *reinterpret_cast<float2 *>(base) = top;
     *reinterpret_cast<float2 *>(base + 16) = bot;
   }
@@ -264,6 +266,8 @@ struct sysml_lenet {
   bool spf = false;
   int64_t spf_plane = 0;
   float *a1s = nullptr, *dz2s = nullptr;
+  // TF32 path: pool argmax as packed 2-bit window codes, one u32 per (16 channels, window)
+  uint64_t *c1 = nullptr, *c2 = nullptr;  // [2][b*196], [4][b*49] (kernels.cuh TcSpfIO::code)
 };
 
 namespace {
@@ -396,6 +400,11 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
       need = std::max(need, tc_wgrad_spf_ws(sc));
       if (tc_wgrad_spf_tma_supported(sc)) need = std::max(need, tc_wgrad_spf_tma_ws(sc));
       ALLOC(h->a1s, 32 * h->spf_plane);
+      if (cudaMalloc(&h->c1, sizeof(uint64_t) * 2 * (size_t)max_local_batch * 196) != cudaSuccess ||
+          cudaMalloc(&h->c2, sizeof(uint64_t) * 4 * (size_t)max_local_batch * 49) != cudaSuccess) {
+        set_error("cudaMalloc failed for the window-code buffers");
+        return fail(SYSML_ERR_CUDA);
+      }
       ALLOC(h->dz2s, 64 * h->spf_plane);
       if (cudaMemset(h->a1s, 0, sizeof(float) * 32 * h->spf_plane) != cudaSuccess ||
           cudaMemset(h->dz2s, 0, sizeof(float) * 64 * h->spf_plane) != cudaSuccess) {
@@ -420,6 +429,7 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
 sysml_status sysml_lenet_destroy(sysml_lenet *h) {
   if (!h) return SYSML_OK;
   cudaFree(h->a1); cudaFree(h->i1); cudaFree(h->a2); cudaFree(h->i2); cudaFree(h->ds);
+  cudaFree(h->c1); cudaFree(h->c2);
   cudaFree(h->lossn); cudaFree(h->da2); cudaFree(h->dz2); cudaFree(h->da1); cudaFree(h->dz1);
   cudaFree(h->part3); cudaFree(h->loss_dev); cudaFree(h->lab_dev); cudaFree(h->x_dev);
   cudaFree(h->ws);
@@ -469,13 +479,15 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
   a1_io.out_Wf = 16;
   a1_io.out_Lf = 256;
   a1_io.out_off = 2;
+  a1_io.code = h->c1;
+  a1_io.code_plane = (int64_t)h->max_b * 196;
   sysml_input a1in{0, h->a1, {}};
   // F1
   SYSML_TRY(T.begin(0));
   if (h->spf) {
     // dense or CSR (scattered straight into the KS operand): pooled a1 lands in SPF
     SYSML_TRY(tc_conv_fwd_spf(ca1, a1_io, x->is_csr ? nullptr : x->dense, params + OFF_F1,
-                              params + OFF_B1, nullptr, &pa1, h->a1s, h->i1, h->ws, st,
+                              params + OFF_B1, nullptr, &pa1, h->a1s, nullptr, h->ws, st,
                               x->is_csr ? &x->csr : nullptr));
   } else {
     SYSML_TRY(conv_fwd_dispatch(c1, *x, params + OFF_F1, params + OFF_B1, nullptr, &p1, h->a1, h->i1,
@@ -490,8 +502,10 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     TcSpfIO io;
     io.in_plane = h->spf_plane;
     io.in_shift = 0;
+    io.code = h->c2;
+    io.code_plane = (int64_t)h->max_b * 49;
     SYSML_TRY(tc_conv_fwd_spf(ca2, io, h->a1s, params + OFF_F2, params + OFF_B2, nullptr, &pa2, h->a2,
-                              h->i2, h->ws, st));
+                              nullptr, h->ws, st));
   } else {
     SYSML_TRY(conv_fwd_dispatch(c2, a1in, params + OFF_F2, params + OFF_B2, nullptr, &p2, h->a2,
                                 h->i2, h->ws, h->ws_bytes, st));
@@ -532,8 +546,8 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     SYSML_TRY(T.begin(4));
     affine_bwd_route_spf_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)n * D3, 256),
                                                                16 * sm_count()),
-                                  256, 0, st>>>(n, h->ds, params + OFF_W3, h->a2, h->i2, h->dz2s,
-                                                h->spf_plane);
+                                  256, 0, st>>>(n, h->ds, params + OFF_W3, h->c2,
+                                                (int64_t)h->max_b * 49, h->dz2s, h->spf_plane);
     SYSML_LAUNCH_CHECK();
     SYSML_TRY(T.end());
     // B2f
