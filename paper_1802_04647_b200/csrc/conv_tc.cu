@@ -386,7 +386,9 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nstage; ++s) {
-      ptx::mbar_init(full + s, 128 + 1);  // 128 producer threads + the expect_tx arrival
+      // dense: 128 producer threads (cp.async arrivals) + the expect_tx arrival;
+      // CSR: one warp fills a whole stage and arrives once with the expect_tx
+      ptx::mbar_init(full + s, p.is_csr ? 1 : 128 + 1);
       ptx::mbar_init(empty + s, 1);     // tcgen05.commit
     }
     for (int b = 0; b < 2; ++b) {
@@ -405,7 +407,59 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
   const int HW = p.H * p.W;
   const long long t_kernel0 = clock64();
 
-  if (warp < 4) {
+  if (warp < 4 && p.is_csr) {
+    // ================= CSR producers (KS mode, one chunk per tile): each warp owns every
+    // 4th tile of this CTA and fills its stage alone -- zero-fill, scatter the non-zeros
+    // of the images overlapping the tile into their S slots, fence, then one arrival
+    // with the filter chunk's expect_tx.  Four tiles' load-latency chains overlap.
+    int tl = warp;  // CTA-local tile counter of this warp
+    for (int64_t tile = blockIdx.x + (int64_t)warp * gridDim.x; tile < p.ntiles;
+         tile += 4 * (int64_t)gridDim.x, tl += 4) {
+      const int ft = (int)(tile % p.nft);
+      const int64_t g0 = (tile / p.nft) * p.cta_pos;
+      const int stage = tl % p.nstage;
+      const uint32_t phase = (uint32_t)((tl / p.nstage) & 1);
+      ptx::mbar_wait(empty + stage, phase ^ 1);
+      uint8_t *A = stage_base + (size_t)stage * p.stage_bytes;
+      const uint32_t a0 = ptx::smem_u32(A);
+      // the row pointers of the (at most a few) images overlapping [g0, g0 + HALO + 8)
+      const int64_t last = g0 + p.HALO + 7;
+      const int n_lo = (int)(g0 / p.Lf);
+      const int n_hi = (int)min((int64_t)p.N - 1, last / p.Lf);
+      const int nimg = n_hi - n_lo + 1;
+      const int rp = lane <= nimg ? __ldg(p.csr.row_ptr + n_lo + lane) : 0;
+      for (int i = lane; i < 2 * p.HALO; i += 32) st_shared_v4(a0 + i * 16, 0.f, 0.f, 0.f, 0.f);
+      __syncwarp();
+      float *Af = reinterpret_cast<float *>(A);
+      for (int ii = 0; ii < nimg; ++ii) {
+        const int n = n_lo + ii;
+        int j0 = __shfl_sync(0xffffffffu, rp, ii & 31), j1 = __shfl_sync(0xffffffffu, rp, (ii + 1) & 31);
+        if (ii + 1 > 31) {  // more than 31 images in one tile (tiny images): direct loads
+          j0 = __ldg(p.csr.row_ptr + n);
+          j1 = __ldg(p.csr.row_ptr + n + 1);
+        }
+        for (int jj = j0 + lane; jj < j1; jj += 32) {
+          const int col = __ldg(p.csr.col_idx + jj);
+          const float v = __ldg(p.csr.val + jj);
+          if (col < 0 || col >= HW) continue;
+          const int h = col / p.W, w = col - h * p.W;
+          const int64_t gi = (int64_t)n * p.Lf + (int64_t)(h + p.ph) * p.Wf + (w + p.pw);
+          for (int s_ = 0; s_ < p.S; ++s_) {
+            const int64_t pos = gi - g0 - s_;
+            if (pos >= 0 && pos < p.HALO)
+              atomicAdd(Af + (s_ >> 2) * p.HALO * 4 + pos * 4 + (s_ & 3), v);  // duplicates summed
+          }
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::mbar_arrive_expect_tx(full + stage, p.b_bytes);
+        ptx::bulk_g2s(A + p.a_bytes, p.fp + (size_t)ft * p.nchunk * (p.b_bytes / 4), p.b_bytes,
+                      full + stage);
+      }
+    }
+  } else if (warp < 4) {
     // ================= producers: A halo (ld.global -> st.shared) + B chunk (bulk copy)
     const int tid = threadIdx.x;
     int stage = 0;
@@ -415,7 +469,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
       ptx::named_bar_sync(1, 128);
       const int ntab = p.ks ? p.HALO + 8 : p.HALO;
-      for (int pos = tid; pos < (p.is_csr ? 0 : ntab); pos += 128) {
+      for (int pos = tid; pos < ntab; pos += 128) {
         const int64_t gi = g0 + pos;
         int off = -1;
         if (p.in_plane > 0) {
@@ -445,31 +499,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         }
         const uint32_t a0 = ptx::smem_u32(A);
         const uint32_t a1 = a0 + (uint32_t)p.HALO * 16;
-        if (p.ks && p.is_csr) {
-          // CSR rows scattered straight into the KS operand: element (pos, s) = x(pos + s);
-          // zero-fill, then each stored non-zero lands in its S slots (work ~ nnz)
-          for (int i = tid; i < 2 * p.HALO; i += 128) st_shared_v4(a0 + i * 16, 0.f, 0.f, 0.f, 0.f);
-          ptx::named_bar_sync(1, 128);
-          const int64_t last = g0 + p.HALO + 7;
-          const int n_lo = (int)(g0 / p.Lf);
-          const int n_hi = (int)min((int64_t)p.N - 1, last / p.Lf);
-          float *Af = reinterpret_cast<float *>(A);
-          for (int n = n_lo; n <= n_hi; ++n) {
-            const int j0 = __ldg(p.csr.row_ptr + n), j1 = __ldg(p.csr.row_ptr + n + 1);
-            for (int jj = j0 + tid; jj < j1; jj += 128) {
-              const int col = __ldg(p.csr.col_idx + jj);
-              if (col < 0 || col >= HW) continue;
-              const float v = __ldg(p.csr.val + jj);
-              const int h = col / p.W, w = col - h * p.W;
-              const int64_t gi = (int64_t)n * p.Lf + (int64_t)(h + p.ph) * p.Wf + (w + p.pw);
-              for (int s_ = 0; s_ < p.S; ++s_) {
-                const int64_t pos = gi - g0 - s_;
-                if (pos >= 0 && pos < p.HALO)
-                  atomicAdd(Af + (s_ >> 2) * p.HALO * 4 + pos * 4 + (s_ & 3), v);  // duplicates summed
-              }
-            }
-          }
-        } else if (p.ks) {
+        if (p.ks) {
           // dense C == 1 input: element (pos, s) = x(pos + s) for s < S, 0 for S <= s < 8;
           // 4-byte async copies (zero-filled where padded) -> no register round trip
           for (int pos = tid; pos < p.HALO; pos += 128) {
@@ -495,12 +525,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
             }
           }
         }
-        if (!p.is_csr) {
-          ptx::cp_async_mbar_arrive(full + stage);  // arrives when this thread's copies land
-        } else {
-          ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive(full + stage);
-        }
+        ptx::cp_async_mbar_arrive(full + stage);  // arrives when this thread's copies land
         if (p.clk && tid == 0) p.clk[blockIdx.x * 8 + 1] += clock64() - t_f0;
         if (++stage == p.nstage) { stage = 0; phase ^= 1; }
       }
