@@ -186,104 +186,16 @@ __device__ __forceinline__ void epi_plain(const TcFwdParams &p, uint32_t tbase, 
   }
 }
 
-// fused bias + relu + 2x2/2 max-pool on a 2-D M-tile (16 rows x 8 cols): the window
-// of lane l is lanes l, l+1 (next column), l+8, l+9 (next row), all in this warp.
-// First-occurrence tie-break (r outer, s inner; strict '>', readings R5/R7): the
-// later partner replaces the current value only when strictly greater.
-__device__ __forceinline__ void epi_pool2(const TcFwdParams &p, uint32_t tbase, int64_t g0, int ft,
-                                          int qd, int lane, const float *bias_s, int i0, int istep) {
-  const int PQ = p.P * p.Q, PpQp = p.Pp * p.Qp;
-  const int nc16 = p.NFpad / 16;
-  const int rl = qd * 4 + (lane >> 3), cl = lane & 7;
-  const bool leader = ((rl | cl) & 1) == 0;
-  float *__restrict__ pout = p.pout;
-  int32_t *__restrict__ parg = p.parg;
-  for (int i = i0; i < p.MT; i += istep) {
-    const uint32_t trow = tbase + (uint32_t)(i * p.NFpad);
-    uint32_t r0[16], r1[16];
-    ptx::tmem_ld16_issue(trow, r0);
-    const int bb = i / p.CT, ct = i - bb * p.CT;
-    const int64_t grow = g0 / p.Wf + bb * 16 + rl;  // global frame row
-    const int col = ct * 8 + cl;
-    const int n = (int)(grow / p.Hs);
-    const int hh = (int)(grow - (int64_t)n * p.Hs);
-    const int pp = hh >> 1, pc = col >> 1;
-    const bool store = leader && n < p.N && pp < p.Pp && pc < p.Qp;
-    const int64_t obase = store ? (int64_t)n * p.K * PpQp + (int64_t)pp * p.Qp + pc : 0;
-    // pooled values: NCHW, or SPF (channel stride out_plane) for the LeNet-internal layout
-    const int vstride = p.out_plane > 0 ? (int)p.out_plane : PpQp;
-    const int64_t vbase = !store ? 0
-                          : p.out_plane > 0 ? (int64_t)n * p.out_Lf + (int64_t)(pp + p.out_off) * p.out_Wf +
-                                                  (pc + p.out_off)
-                                            : obase;
-    float *const pout_t = pout + vbase;
-    int32_t *const parg_t = parg ? parg + obase : nullptr;
-    const int idx0 = hh * p.Q + col;
-    auto process = [&](const uint32_t(&cur)[16], int c16) {
-      const int k0 = ft * p.NFpad + c16 * 16;
-      float b[16], z[16];
-      int off[16];
-      load_bias16(p, bias_s, k0, b);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float t = __uint_as_float(cur[j]) + b[j];
-        z[j] = t > 0.f ? t : 0.f;  // relu, +0.0 for non-positive (reading R7)
-        off[j] = 0;
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {  // (r, s) -> (r, s+1)
-        const float z2 = __shfl_down_sync(0xffffffffu, z[j], 1);
-        if (z2 > z[j]) { z[j] = z2; off[j] = 1; }
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {  // row r -> row r+1 (carry the partner's column choice)
-        const float z2 = __shfl_down_sync(0xffffffffu, z[j], 8);
-        const int o2 = __shfl_down_sync(0xffffffffu, off[j], 8);
-        if (z2 > z[j]) { z[j] = z2; off[j] = p.Q + o2; }
-      }
-      if (store) {
-        // 32-bit element offsets from per-M-tile base pointers (no 64-bit math per store)
-        float *po = pout_t + (int64_t)k0 * vstride;
-        const int ib = k0 * PQ + idx0;
-        if (k0 + 16 <= p.K) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) po[j * vstride] = z[j];
-          if (parg_t) {
-            int32_t *pa = parg_t + k0 * PpQp;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) pa[j * PpQp] = ib + j * PQ + off[j];
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (k0 + j < p.K) {
-              po[j * vstride] = z[j];
-              if (parg_t) parg_t[k0 * PpQp + j * PpQp] = ib + j * PQ + off[j];
-            }
-        }
-      }
-    };
-    for (int c16 = 0; c16 < nc16; c16 += 2) {
-      ptx::tmem_ld_wait(r0);
-      if (c16 + 1 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 1) * 16, r1);
-      process(r0, c16);
-      if (c16 + 1 < nc16) {
-        ptx::tmem_ld_wait(r1);
-        if (c16 + 2 < nc16) ptx::tmem_ld16_issue(trow + (c16 + 2) * 16, r0);
-        process(r1, c16 + 1);
-      }
-    }
-  }
-}
-
-// Same fused bias + relu + 2x2/2 max-pool, LeNet-internal variant with a reduce-scatter
-// butterfly: round 1 (column partner, lane ^ 1) leaves each lane the pair-max of 8 of the
+// Fused bias + relu + 2x2/2 max-pool on a 2-D M-tile (16 rows x 8 cols: the window of
+// lane l is lanes l, l^1 (next column), l^8 (next row), l^9, all in this warp) with a
+// reduce-scatter butterfly: round 1 (column partner, lane ^ 1) leaves each lane the pair-max of 8 of the
 // 16 channels, round 2 (row partner, lane ^ 8) the window max of 4 -- so each of the
-// window's four lanes owns 4 channels: 4 value stores and 16 bits of 4-bit codes
-// (positive*4 + dr*2 + ds, positive = window max > 0; ties -> the earlier position in
-// r-outer / s-inner order, readings R5/R7/R9).  relu'd values are >= +0.0, so they compare as unsigned integers; the later
+// window's four lanes owns 4 channels: 4 value stores plus either 4 int32 argmax
+// indices (column of the pool-input row, reading R6) or 16 bits of 4-bit codes
+// (LeNet-internal: positive*4 + dr*2 + ds, positive = window max > 0).  Ties -> the
+// earlier position in r-outer / s-inner order (readings R5/R7/R9).  relu'd values are >= +0.0, so they compare as unsigned integers; the later
 // position takes the partner's value when it is >= (u + 1 > u), the earlier when >.
-__device__ __forceinline__ void epi_pool2_code(const TcFwdParams &p, uint32_t tbase, int64_t g0,
+__device__ __forceinline__ void epi_pool2(const TcFwdParams &p, uint32_t tbase, int64_t g0,
                                                int ft, int qd, int lane, const float *bias_s,
                                                int i0, int istep) {
   const int PpQp = p.Pp * p.Qp;
@@ -309,8 +221,14 @@ __device__ __forceinline__ void epi_pool2_code(const TcFwdParams &p, uint32_t tb
                                                   (pc + p.out_off)
                                             : (int64_t)n * p.K * PpQp + (int64_t)pp * p.Qp + pc;
     float *const pout_t = pout + vbase + (int64_t)cb * vstride;
-    uint16_t *const code_t = reinterpret_cast<uint16_t *>(p.pcode + (store ? (int64_t)n * PpQp + pp * p.Qp + pc : 0)) +
-                             (cb >> 2);
+    uint16_t *const code_t = p.pcode ? reinterpret_cast<uint16_t *>(p.pcode + (store ? (int64_t)n * PpQp + pp * p.Qp + pc : 0)) +
+                                           (cb >> 2)
+                                     : nullptr;
+    // int32 argmax (NCHW pooled layout): plane index of the window's top-left conv output
+    int32_t *const parg_t = p.parg ? p.parg + (store ? (int64_t)n * p.K * PpQp + pp * p.Qp + pc : 0) +
+                                         (int64_t)cb * PpQp
+                                   : nullptr;
+    const int idx_tl = (2 * pp) * p.Q + 2 * pc;
     auto process = [&](const uint32_t(&cur)[16], int c16) {
       const int k0 = ft * p.NFpad + c16 * 16;
       float b[16];
@@ -353,7 +271,17 @@ __device__ __forceinline__ void epi_pool2_code(const TcFwdParams &p, uint32_t tb
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           if (k0 + cb + j < p.K) po[j * vstride] = __uint_as_float(v4[j]);
-        code_t[(int64_t)(k0 >> 4) * p.code_plane * 4] = (uint16_t)code;
+        if (code_t) code_t[(int64_t)(k0 >> 4) * p.code_plane * 4] = (uint16_t)code;
+        if (parg_t) {
+          const int PQ = p.P * p.Q;
+          int32_t *pa = parg_t + (int64_t)k0 * PpQp;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t cj = code >> (4 * j);
+            if (k0 + cb + j < p.K)
+              pa[j * PpQp] = (k0 + cb + j) * PQ + idx_tl + (int)((cj >> 1) & 1u) * p.Q + (int)(cj & 1u);
+          }
+        }
       }
     };
     for (int c16 = 0; c16 < nc16; c16 += 2) {
@@ -601,8 +529,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(qd * 32) << 16) + buf * p.tbuf;
       const int eset = (warp - 5) >> 2;  // epilogue warp set 0 / 1 -> even / odd M-tiles
-      if (p.pool && p.pcode) epi_pool2_code(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
-      else if (p.pool) epi_pool2(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
+      if (p.pool) epi_pool2(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
       else epi_plain(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
       ptx::tc_fence_before();
       __syncwarp();
