@@ -1650,12 +1650,14 @@ sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy
 bool tc_bwd_filter_supported(const ConvArgs &a) {
   if (device_cc_major() != 10) return false;
   if (tc_wgrad_1x1_supported(a)) return true;
+  if (tc_wgrad_frame_supported(a)) return true;
   if (a.C < 8) return false;  // tiny channel counts waste N; CUDA-core / CSR kernels instead
   return plan_wgrad(a).ok;
 }
 
 size_t tc_bwd_filter_ws(const ConvArgs &a) {
   if (tc_wgrad_1x1_supported(a)) return tc_wgrad_1x1_ws(a);
+  if (tc_wgrad_frame_supported(a)) return tc_wgrad_frame_ws(a);
   TcWgPlan pl = plan_wgrad(a);
   return pl.ok ? pl.part_bytes + pl.dbpart_bytes : 0;
 }
@@ -1663,6 +1665,7 @@ size_t tc_bwd_filter_ws(const ConvArgs &a) {
 sysml_status tc_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,
                                 float *db, void *ws, cudaStream_t st) {
   if (tc_wgrad_1x1_supported(a)) return tc_wgrad_1x1(a, x, dy, df, db, ws, st);
+  if (tc_wgrad_frame_supported(a)) return tc_wgrad_frame(a, x, dy, df, db, ws, st);
   TcWgPlan pl = plan_wgrad(a);
   if (!pl.ok) {
     set_error("tcgen05 bwd_filter: unsupported shape");

@@ -103,7 +103,13 @@ bool tc_wgrad_spf_supported(const SpfConv &sc);
 bool tc_wgrad_spf_tma_supported(const SpfConv &sc);
 size_t tc_wgrad_spf_tma_ws(const SpfConv &sc);
 sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float *dy_spf,
-                              float *df, float *db, void *ws, cudaStream_t st);
+                              float *df, float *db, void *ws, cudaStream_t st,
+                              const float *db_src = nullptr, int db_count = 0);
+// NCHW entry: framing pre-pass + the TMA kernel (stride 1, C % 8 == 0)
+bool tc_wgrad_frame_supported(const ConvArgs &a);
+size_t tc_wgrad_frame_ws(const ConvArgs &a);
+sysml_status tc_wgrad_frame(const ConvArgs &a, const float *x, const float *dy, float *df,
+                            float *db, void *ws, cudaStream_t st);
 size_t tc_wgrad_spf_ws(const SpfConv &sc);
 sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy_spf, float *df,
                           float *db, void *ws, cudaStream_t st);

@@ -32,8 +32,10 @@ constexpr int W2_ATOM = 32;       // positions per atom (128-byte swizzled row)
 
 struct W2Params {
   int K, C, R, S, Wf;
-  int Kc, copies, RG, N;          // N = S*C
-  int rbstep;                     // atoms per rb shift (copies*Wf/32)
+  int Kc, copies, RG, N;          // A rows per copy; N = S*Ct
+  int Ct, nct, nkt;               // channels per CTA tile, channel tiles, filter tiles
+  int shift;                      // positions per rb shift (copies*Wf, multiple of 8)
+  int L;                          // B lookahead in atoms
   int nbr;                        // B ring slots
   int64_t atoms;                  // ceil(G / 32)
   int splits;
@@ -55,6 +57,7 @@ __device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
   return ptx::make_desc(saddr, 16, 1024) | ((uint64_t)2 << 61);
 }
 
+template <int SHIFT>  // positions per rb shift (compile-time: 16 or 32), 0 = runtime p.shift
 __global__ void __launch_bounds__(W2_THREADS, 1)
     tc_wgrad_spf_tma_kernel(const __grid_constant__ CUtensorMap tmDy,
                             const __grid_constant__ CUtensorMap tmX, const W2Params p) {
@@ -71,10 +74,12 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   uint64_t *accf = fullBt + p.nbr;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(accf + 1);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int z = blockIdx.x;
+  const int z = blockIdx.x % p.splits;
+  const int ct = (blockIdx.x / p.splits) % p.nct, kt = blockIdx.x / (p.splits * p.nct);
+  const int k0 = kt * p.Kc, c0 = ct * p.Ct;
   const int64_t a0 = z * p.atoms / p.splits, a1 = (z + 1) * p.atoms / p.splits;
-  const int L = (p.RG - 1) * p.rbstep;  // B lookahead (atoms)
-  const bool do_db = p.dbpart != nullptr && !(p.dbg & 4);
+  const int L = p.L;  // B lookahead (atoms)
+  const bool do_db = p.dbpart != nullptr && !(p.dbg & 4) && ct == 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < W2_NA; ++i) {
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         ptx::mbar_arrive_expect_tx(fullA + sa, a_slot);
         const int g = (int)((a0 + ia) * W2_ATOM);
         for (int j = 0; j < p.copies; ++j)
-          ptx::tma_load_3d(sA + sa * a_slot + j * p.Kc * 128, &tmDy, g - j * p.Wf, 0, 0,
+          ptx::tma_load_3d(sA + sa * a_slot + j * p.Kc * 128, &tmDy, g - j * p.Wf, k0, 0,
                            ptx::smem_u32(fullA + sa));
         if (++sa == W2_NA) { sa = 0; pa ^= 1; }
       }
@@ -132,10 +137,10 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         const long long t0 = clock64();
         ptx::mbar_wait(emptyB + sb, pb ^ 1);
         if (p.clk) p.clk[blockIdx.x * 8 + 5] += clock64() - t0;
-        ptx::mbar_arrive_expect_tx(fullBt + sb, (uint32_t)(p.ntma_s * p.C * 128));
+        ptx::mbar_arrive_expect_tx(fullBt + sb, (uint32_t)(p.ntma_s * p.Ct * 128));
         const int g = (int)((a0 + ib) * W2_ATOM);
         for (int s = 0; s < p.S; s += 4)
-          ptx::tma_load_3d(sB + sb * b_slot + s * p.C * 128, &tmX, g + s, 0, 0,
+          ptx::tma_load_3d(sB + sb * b_slot + s * p.Ct * 128, &tmX, g + s, c0, 0,
                            ptx::smem_u32(fullBt + sb));
         if (++sb == p.nbr) { sb = 0; pb ^= 1; }
       }
@@ -150,6 +155,9 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
     }
     int sa = 0, s_ai = 0;  // A cursor; B slot of atom ai
     uint32_t pa = 0;
+    // per (kk, rb): the B atom offset and the 32-byte step inside the swizzled row of
+    // positions 8*kk + rb*shift (constant across atoms)
+    const int shift = SHIFT ? SHIFT : p.shift;
     for (int ai = 0; ai < (int)nA; ++ai) {
       const long long t0 = clock64();
       ptx::mbar_wait(fullA + sa, pa);
@@ -161,23 +169,26 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         p.clk[blockIdx.x * 8 + 1] += clock64() - t1;
       }
       ptx::tc_fence_after();
-      const uint32_t A = sA + sa * a_slot;
-      uint32_t Bslot[4];
+      // descriptors built once per atom; K-steps / sub-atom shifts are start-address
+      // increments (16-byte units) -- keeps the issue loop to a few uniform adds per MMA
+      const uint64_t adesc = sw128(sA + sa * a_slot);
+      uint64_t bdesc[4];
 #pragma unroll
-      for (int rb = 0; rb < 4; ++rb) {
-        int sl = s_ai + rb * p.rbstep;
+      for (int a = 0; a < 4; ++a) {
+        int sl = s_ai + a;
         if (sl >= p.nbr) sl -= p.nbr;
-        Bslot[rb] = sB + (uint32_t)sl * b_slot;
+        bdesc[a] = sw128(sB + (uint32_t)sl * b_slot);
       }
 #pragma unroll
       for (int kk = 0; kk < W2_ATOM / 8; ++kk) {
-        const uint64_t ad = sw128(A + kk * 32);
         const uint32_t acc = (ai | kk) != 0 ? 1u : 0u;
 #pragma unroll
         for (int rb = 0; rb < 4; ++rb) {
           if (rb < p.RG) {
+            const int t = 8 * kk + rb * shift;  // compile-time when SHIFT != 0
+            const uint64_t bd = bdesc[(t >> 5) & 3] + (uint64_t)((t & 31) >> 2);
             if (!p.dbg && ptx::elect_one())
-              ptx::mma_tf32(tmem + rb * p.N, ad, sw128(Bslot[rb] + kk * 32), idesc, acc);
+              ptx::mma_tf32(tmem + rb * p.N, adesc + (uint64_t)(kk * 2), bd, idesc, acc);
             __syncwarp();
           }
         }
@@ -201,11 +212,13 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
     // CTA's dY atoms (rows k of copy j = 0), two threads per row.
     float dbv = 0.f;
     const int npre = (int)std::min<int64_t>(L, nB);
-    const int drow = et >> 1, dhalf = et & 1;
+    // db rows: Kc <= 64 -> two threads per row (64-byte halves); Kc = 128 -> one per row
+    const bool dsplit = p.Kc <= 64;
+    const int drow = dsplit ? et >> 1 : et, dhalf = dsplit ? et & 1 : 0, dq = dsplit ? 4 : 8;
     // shift tasks (channel c, 16-byte chunk q) of this thread: t = et, et + 128 (C*8 <= 256).
     // Source: the TMA-loaded s = 0 tile of atom bi (chunk q) and, for q = 7, chunk 0 of
     // atom bi + 1 (next ring slot); both rows are 128-byte swizzled (chunk q at q ^ (c & 7)).
-    const int ntask = p.C * 8;
+    const int ntask = p.Ct * 8;
     int sb = 0, sa = 0;
     uint32_t pb = 0, pa = 0;
     for (int step = -npre; step < (int)nA; ++step) {
@@ -231,7 +244,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           const float e[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
           for (int s_ = 1; s_ < p.S; ++s_) {
             if ((s_ & 3) == 0) continue;
-            const int row = s_ * p.C + c;
+            const int row = s_ * p.Ct + c;
             const uint32_t dst = Bs + row * 128 + ((q ^ (row & 7)) << 4);
             const int o = s_ & 3;
             float w0, w1, w2, w3;
@@ -254,9 +267,11 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         if (drow < p.Kc) {
           const float4 *rp = reinterpret_cast<const float4 *>(Aring + slotA * a_slot + drow * 128) + dhalf * 4;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 v = rp[q];
-            dbv += (v.x + v.y) + (v.z + v.w);
+          for (int q = 0; q < 8; ++q) {
+            if (q < dq) {
+              const float4 v = rp[q];
+              dbv += (v.x + v.y) + (v.z + v.w);
+            }
           }
         }
         ptx::named_bar_sync(1, 128);
@@ -264,13 +279,14 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       }
     }
     if (do_db) {
-      dbv += __shfl_xor_sync(0xffffffffu, dbv, 1);
-      if ((et & 1) == 0 && (et >> 1) < p.K) p.dbpart[(int64_t)z * p.K + (et >> 1)] = dbv;
+      if (dsplit) dbv += __shfl_xor_sync(0xffffffffu, dbv, 1);
+      if ((!dsplit || (et & 1) == 0) && drow < p.Kc && k0 + drow < p.K)
+        p.dbpart[(int64_t)z * p.K + k0 + drow] = dbv;
     }
     if (nA > 0) ptx::mbar_wait_sleep(accf, 0);
     ptx::tc_fence_after();
     const int row = qd * 32 + lane;
-    float *dst = p.part + (int64_t)z * p.RG * 128 * p.N;
+    float *dst = p.part + (int64_t)blockIdx.x * p.RG * 128 * p.N;
     for (int rb = 0; rb < p.RG; ++rb)
       for (int cb = 0; cb < p.N; cb += 16) {
         float v[16];
@@ -297,27 +313,31 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   }
 }
 
-// dF[k][c][r][s] = sum over splits (fixed order) of D_rb[(j,k)][(s,c)], r = rb*copies + j
-__global__ void w2_reduce_kernel(const W2Params p, float *__restrict__ df, float *__restrict__ db) {
+// dF[k][c][r][s] = sum over splits (fixed order) of D_rb[(j,k')][(s,c')] of the CTA tile
+// (kt, ct) holding k = kt*Kc + k', c = ct*Ct + c', r = rb*copies + j
+__global__ void w2_reduce_kernel(const W2Params p, float *__restrict__ df, float *__restrict__ db,
+                                 const float *__restrict__ dbsrc, int dbcount) {
   const int RS = p.R * p.S;
   const int64_t total = (int64_t)p.K * p.C * RS;
-  const int64_t split_stride = (int64_t)p.RG * 128 * p.N;
+  const int64_t cta_stride = (int64_t)p.RG * 128 * p.N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(i / ((int64_t)p.C * RS));
     const int rem = (int)(i - (int64_t)k * p.C * RS);
     const int c = rem / RS, t = rem - c * RS, r = t / p.S, s = t - r * p.S;
     const int rb = r / p.copies, j = r - rb * p.copies;
-    const int64_t off = ((int64_t)rb * 128 + j * p.Kc + k) * p.N + s * p.C + c;
+    const int kt = k / p.Kc, kk = k - kt * p.Kc, ct = c / p.Ct, cc = c - ct * p.Ct;
+    const int64_t off = ((int64_t)rb * 128 + j * p.Kc + kk) * p.N + s * p.Ct + cc;
+    const float *src = p.part + ((int64_t)(kt * p.nct + ct) * p.splits) * cta_stride + off;
     float acc = 0.f;
-    for (int sp = 0; sp < p.splits; ++sp) acc += __ldg(p.part + sp * split_stride + off);
+    for (int sp = 0; sp < p.splits; ++sp) acc += __ldg(src + sp * cta_stride);
     df[i] = acc;
   }
   if (db)
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < p.K;
          k += (int64_t)gridDim.x * blockDim.x) {
       float acc = 0.f;
-      for (int sp = 0; sp < p.splits; ++sp) acc += __ldg(p.dbpart + (int64_t)sp * p.K + k);
+      for (int sp = 0; sp < dbcount; ++sp) acc += __ldg(dbsrc + (int64_t)sp * p.K + k);
       db[k] = acc;
     }
 }
@@ -325,6 +345,7 @@ __global__ void w2_reduce_kernel(const W2Params p, float *__restrict__ df, float
 struct W2Plan {
   W2Params p;
   size_t smem, part_bytes, dbpart_bytes;
+  int grid;
   bool ok;
 };
 
@@ -333,31 +354,43 @@ W2Plan plan_w2(const SpfConv &sc) {
   W2Params &p = pl.p;
   pl.ok = false;
   p.K = sc.K; p.C = sc.C; p.R = sc.R; p.S = sc.S; p.Wf = sc.Wf;
-  if (sc.K > 128 || sc.C % 8 || sc.C > 32 || sc.x_shift % 4 || sc.dy_shift % 4 || sc.plane_x % 4 ||
-      sc.plane_dy % 4 || sc.G <= 0)
+  if (sc.C % 8 || sc.x_shift % 4 || sc.dy_shift % 4 || sc.plane_x % 4 || sc.plane_dy % 4 ||
+      sc.G <= 0 || sc.Wf % 8 || sc.S > 8)
     return pl;
+  // A rows (j, k): Kc filters per copy, copies of dY shifted by j frame rows
   p.Kc = sc.K <= 16 ? 16 : sc.K <= 32 ? 32 : sc.K <= 64 ? 64 : 128;
   p.copies = std::min(128 / p.Kc, sc.R);
-  while (p.copies > 1 && (p.copies * sc.Wf) % W2_ATOM) --p.copies;
-  if ((p.copies * sc.Wf) % W2_ATOM) return pl;
-  p.rbstep = p.copies * sc.Wf / W2_ATOM;
+  p.nkt = (int)ceil_div(sc.K, p.Kc);
   p.RG = (sc.R + p.copies - 1) / p.copies;
-  p.N = sc.S * sc.C;
-  if (p.N % 16 || p.N > 256 || p.RG * p.N > 512 || p.RG > 4) return pl;
+  p.shift = p.copies * sc.Wf;
+  // channel tile: Ct <= 32 (helper tasks), S*Ct % 16 == 0, RG*S*Ct TMEM columns <= 512
+  p.Ct = 0;
+  for (int ct = std::min(32, sc.C); ct >= 8; ct -= 8)
+    if (sc.C % ct == 0 && (sc.S * ct) % 16 == 0 && sc.S * ct <= 256 && p.RG * sc.S * ct <= 512) {
+      p.Ct = ct;
+      break;
+    }
+  if (!p.Ct || p.RG > 4) return pl;
+  p.nct = sc.C / p.Ct;
+  p.N = sc.S * p.Ct;
+  p.L = (24 + (p.RG - 1) * p.shift) / W2_ATOM;
+  if (p.L > 3) return pl;  // B descriptors of atoms ai .. ai + 3
   // B ring: >= L + 2 (atom bi + 1 resident while bi is shifted) plus run-ahead slots
   size_t smem = 0;
-  for (p.nbr = (p.RG - 1) * p.rbstep + 6; p.nbr >= (p.RG - 1) * p.rbstep + 3; --p.nbr) {
+  for (p.nbr = p.L + 6; p.nbr >= p.L + 3; --p.nbr) {
     smem = 1024 + (size_t)W2_NA * 128 * 128 + (size_t)p.nbr * p.N * 128 +
            8 * (2 * W2_NA + 3 * p.nbr + 1) + 16;
     if (smem <= 227 * 1024) break;
   }
   if (smem > 227 * 1024) return pl;
   p.atoms = ceil_div(sc.G, W2_ATOM);
-  int splits = sm_count();
+  const int tiles = p.nkt * p.nct;
+  int splits = std::max(1, sm_count() / tiles);
   if (splits > p.atoms) splits = (int)p.atoms;
   p.splits = std::max(1, splits);
+  pl.grid = tiles * p.splits;
   pl.smem = smem;
-  pl.part_bytes = align_up((size_t)p.splits * p.RG * 128 * p.N * sizeof(float), 256);
+  pl.part_bytes = align_up((size_t)pl.grid * p.RG * 128 * p.N * sizeof(float), 256);
   pl.dbpart_bytes = align_up((size_t)p.splits * p.K * sizeof(float), 256);
   pl.ok = true;
   return pl;
@@ -375,7 +408,8 @@ size_t tc_wgrad_spf_tma_ws(const SpfConv &sc) {
 }
 
 sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float *dy_spf,
-                              float *df, float *db, void *ws, cudaStream_t st) {
+                              float *df, float *db, void *ws, cudaStream_t st,
+                              const float *db_src, int db_count) {
   W2Plan pl = plan_w2(sc);
   if (!pl.ok) {
     set_error("tcgen05 TMA SPF bwd_filter: unsupported shape");
@@ -393,26 +427,26 @@ sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float
   p.plane_x = sc.plane_x;
   p.ntma_s = (sc.S + 3) / 4;
   p.part = reinterpret_cast<float *>(ws);
-  p.dbpart = db ? reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + pl.part_bytes) : nullptr;
+  // db either from the staged dY atoms (dbpart) or precomputed per-image partials (db_src)
+  p.dbpart = (db && !db_src) ? reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + pl.part_bytes)
+                             : nullptr;
   CUtensorMap tmDy, tmX;
   {
     const uint64_t dims[3] = {(uint64_t)sc.G, (uint64_t)sc.K, 1};
     const uint64_t strides[2] = {(uint64_t)sc.plane_dy * 4, (uint64_t)sc.plane_dy * 4 * sc.K};
-    const uint32_t box[3] = {W2_ATOM, (uint32_t)p.Kc, 1};
+    const uint32_t box[3] = {W2_ATOM, (uint32_t)p.Kc, 1};  // rows beyond K: zero-filled
     if (!tmap_encode_f32(&tmDy, dyb, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return SYSML_ERR_CUDA;
   }
   {
     const uint64_t dims[3] = {(uint64_t)sc.G, (uint64_t)sc.C, 1};
     const uint64_t strides[2] = {(uint64_t)sc.plane_x * 4, (uint64_t)sc.plane_x * 4 * sc.C};
-    const uint32_t box[3] = {W2_ATOM, (uint32_t)sc.C, 1};
+    const uint32_t box[3] = {W2_ATOM, (uint32_t)p.Ct, 1};
     if (!tmap_encode_f32(&tmX, xb, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return SYSML_ERR_CUDA;
   }
-  static int attr = 0;
-  if ((int)pl.smem > attr) {
-    SYSML_CUDA(cudaFuncSetAttribute(tc_wgrad_spf_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)pl.smem));
-    attr = (int)pl.smem;
-  }
+  auto kern = p.shift == 32 ? tc_wgrad_spf_tma_kernel<32>
+              : p.shift == 16 ? tc_wgrad_spf_tma_kernel<16>
+                              : tc_wgrad_spf_tma_kernel<0>;
+  SYSML_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   static long long *dclk = nullptr;
   const bool prof = getenv("SYSML_TC_PROFILE") != nullptr;
   p.clk = nullptr;
@@ -421,24 +455,158 @@ sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float
     cudaMemsetAsync(dclk, 0, sizeof(long long) * 8 * 4096, st);
     p.clk = dclk;
   }
-  tc_wgrad_spf_tma_kernel<<<p.splits, W2_THREADS, pl.smem, st>>>(tmDy, tmX, p);
+  kern<<<pl.grid, W2_THREADS, pl.smem, st>>>(tmDy, tmX, p);
   SYSML_LAUNCH_CHECK();
   if (prof) {
     static long long h[8 * 4096];
-    cudaMemcpyAsync(h, dclk, sizeof(long long) * 8 * p.splits, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h, dclk, sizeof(long long) * 8 * pl.grid, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     double a[8] = {0};
-    for (int b = 0; b < p.splits; ++b)
-      for (int j = 0; j < 8; ++j) a[j] += (double)h[b * 8 + j] / p.splits;
+    for (int b = 0; b < pl.grid; ++b)
+      for (int j = 0; j < 8; ++j) a[j] += (double)h[b * 8 + j] / pl.grid;
     fprintf(stderr, "[w2 splits=%d atoms/cta=%.0f] mma_wait_A %.0f mma_wait_B %.0f help_wait_emptyB %.0f "
             "help_wait_fullA %.0f prod_wait_emptyA %.0f prod_wait_emptyB %.0f mma_total %.0f help_total %.0f\n",
             p.splits, (double)p.atoms / p.splits, a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]);
   }
   const int64_t total = (int64_t)p.K * p.C * p.R * p.S;
   w2_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 8 * sm_count()), 256, 0, st>>>(
-      p, df, db);
+      p, df, db_src ? db : (p.dbpart ? db : nullptr), db_src ? db_src : p.dbpart,
+      db_src ? db_count : p.splits);
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;
+}
+
+}  // namespace sysml
+
+// =====================================================================================
+// NCHW entry (public conv2d_backward_filter, K5): copy X and dY into stacked frames
+// (HBM-bound pre-pass) and run the TMA kernel above.
+//   X frame:  X_f[c][n*Hs*Wf + (h+ph)*Wf + (w+pw)] = X[n][c][h][w], zeros elsewhere
+//   dY frame: dY_f[k][n*Hs*Wf + p*Wf + q] = dY[n][k][p][q], zeros elsewhere
+// sum_g dY_f[g] X_f[g + r*Wf + s] equals the definition when the column /
+// row wrap lands in zero padding: Wf >= max(W + pw, Q + S - 1 - pw) and
+// Hs >= max(H + ph, P + R - 1 - ph); Wf is rounded up to a multiple of 8 so the tap-row
+// shifts are whole 32-byte steps of the swizzled rows.
+// =====================================================================================
+namespace sysml {
+namespace {
+
+// one float4 of a frame row per thread (Wf % 4 == 0); index decoding per float4
+__global__ void nchw_to_frame_kernel(const float *__restrict__ src, float *__restrict__ dst, int N,
+                                     int C, int H, int W, int Hs, int Wf, int oh, int ow,
+                                     int64_t plane) {
+  const int q4 = Wf >> 2;
+  const int NHs = N * Hs;
+  const int64_t total = (int64_t)C * NHs * q4;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / q4;
+    const int w0 = (int)(t - row * q4) * 4 - ow;
+    const int c = (int)(row / NHs);
+    const int rem = (int)(row - (int64_t)c * NHs);
+    const int n = rem / Hs, hh = rem - n * Hs;
+    const int h = hh - oh;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (h >= 0 && h < H) {
+      const float *srow = src + (((int64_t)n * C + c) * H + h) * W;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (w0 + e >= 0 && w0 + e < W) v[e] = __ldg(srow + w0 + e);
+    }
+    reinterpret_cast<float4 *>(dst + (int64_t)c * plane + (int64_t)rem * Wf)[t - row * q4] =
+        make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+// dY framing, one warp per (k, n) plane, also writing the plane's sum (db partial
+// psum[n][k], warp butterfly in a fixed order -> deterministic)
+__global__ void nchw_to_frame_sum_kernel(const float *__restrict__ src, float *__restrict__ dst,
+                                         float *__restrict__ psum, int N, int C, int H, int W,
+                                         int Hs, int Wf, int64_t plane) {
+  const int lane = threadIdx.x & 31;
+  const int q4 = Wf >> 2, nf4 = Hs * q4;
+  const int64_t planes = (int64_t)C * N;
+  const int64_t wstep = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t pl = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; pl < planes; pl += wstep) {
+    const int n = (int)(pl / C), c = (int)(pl - (int64_t)n * C);
+    const float *sp = src + ((int64_t)n * C + c) * H * W;
+    float *dp = dst + (int64_t)c * plane + (int64_t)n * Hs * Wf;
+    float sum = 0.f;
+    for (int f4 = lane; f4 < nf4; f4 += 32) {
+      const int hh = f4 / q4, w0 = (f4 - hh * q4) * 4;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (hh < H) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (w0 + e < W) v[e] = __ldg(sp + hh * W + w0 + e);
+      }
+      sum += (v[0] + v[1]) + (v[2] + v[3]);
+      reinterpret_cast<float4 *>(dp)[f4] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0 && psum) psum[(int64_t)n * C + c] = sum;
+  }
+}
+
+struct FramePlan {
+  int Hs, Wf;
+  int64_t G, plane;
+  SpfConv sc;
+  size_t x_bytes, dy_bytes;
+  bool ok;
+};
+
+FramePlan plan_frame(const ConvArgs &a) {
+  FramePlan f{};
+  f.ok = false;
+  if (a.sh != 1 || a.sw != 1 || a.C % 8 || a.R > 8 || a.S > 8) return f;
+  f.Wf = (int)std::max<int64_t>(a.W + a.pw, a.Q + a.S - 1 - a.pw);
+  f.Wf = (f.Wf + 7) / 8 * 8;
+  f.Hs = (int)std::max<int64_t>(a.H + a.ph, a.P + a.R - 1 - a.ph);
+  f.G = (int64_t)a.N * f.Hs * f.Wf;
+  f.plane = (f.G + 3) / 4 * 4;
+  if (f.G >= (1ll << 31)) return f;
+  f.sc = SpfConv{(int)a.K, (int)a.C, (int)a.R, (int)a.S, f.Wf, f.G, f.plane, f.plane, 0, 0};
+  f.x_bytes = align_up((size_t)a.C * f.plane * sizeof(float), 256);
+  f.dy_bytes = align_up((size_t)a.K * f.plane * sizeof(float), 256) +
+               align_up((size_t)a.N * a.K * sizeof(float), 256);  // + per-image db partials
+  f.ok = plan_w2(f.sc).ok;
+  return f;
+}
+
+}  // namespace
+
+bool tc_wgrad_frame_supported(const ConvArgs &a) {
+  if (device_cc_major() != 10 || getenv("SYSML_NO_TMA_WGRAD")) return false;
+  return plan_frame(a).ok;
+}
+
+size_t tc_wgrad_frame_ws(const ConvArgs &a) {
+  const FramePlan f = plan_frame(a);
+  return f.ok ? f.x_bytes + f.dy_bytes + tc_wgrad_spf_tma_ws(f.sc) : 0;
+}
+
+sysml_status tc_wgrad_frame(const ConvArgs &a, const float *x, const float *dy, float *df,
+                            float *db, void *ws, cudaStream_t st) {
+  const FramePlan f = plan_frame(a);
+  if (!f.ok) {
+    set_error("tcgen05 framed bwd_filter: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  float *xf = reinterpret_cast<float *>(ws);
+  float *dyf = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + f.x_bytes);
+  void *ws2 = reinterpret_cast<char *>(ws) + f.x_bytes + f.dy_bytes;
+  const int blocks = 8 * sm_count();
+  nchw_to_frame_kernel<<<blocks, 256, 0, st>>>(x, xf, (int)a.N, (int)a.C, (int)a.H, (int)a.W, f.Hs, f.Wf,
+                                               (int)a.ph, (int)a.pw, f.plane);
+  SYSML_LAUNCH_CHECK();
+  float *psum = reinterpret_cast<float *>(reinterpret_cast<char *>(dyf) +
+                                          align_up((size_t)a.K * f.plane * sizeof(float), 256));
+  nchw_to_frame_sum_kernel<<<blocks, 256, 0, st>>>(dy, dyf, db ? psum : nullptr, (int)a.N, (int)a.K,
+                                                   (int)a.P, (int)a.Q, f.Hs, f.Wf, f.plane);
+  SYSML_LAUNCH_CHECK();
+  return tc_wgrad_spf_tma(f.sc, xf, dyf, df, db, ws2, st, db ? psum : nullptr, (int)a.N);
 }
 
 }  // namespace sysml

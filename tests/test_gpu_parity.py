@@ -55,6 +55,8 @@ CONV_SHAPES = [
     (2, 4, 9, 9, 1, 3, 3, 1, 1),         # K = 1 (bwd_data input has one channel)
     (3, 48, 6, 6, 40, 1, 1, 1, 0),       # 1x1 TMA wgrad: one 128-filter tile, 48-channel tile
     (2, 32, 4, 4, 300, 1, 1, 1, 0),      # 1x1 TMA wgrad: K > 256 (two filter-pair tiles), ragged
+    (2, 16, 9, 11, 136, 3, 3, 1, 1),     # framed TMA wgrad: K > 128 (two filter tiles), 16-ch tile
+    (2, 32, 10, 12, 48, 3, 3, 1, 0),     # framed TMA wgrad: pad 0, rectangular
 ]
 
 
