@@ -51,19 +51,21 @@ def load_peaks():
 # Per-image algorithmic work of each step stage:
 # (flops, bytes, bound-if-tensor-math).  Bytes = fp32/int32 tensors each kernel must
 # read or write once; params are negligible.
-STAGE_WORK = {
-    "F1_conv1_pool": (2 * 32 * 25 * 784, 784 * 4 + 6272 * 4 * 2, "hbm"),
-    "F2_conv2_pool": (2 * 64 * 800 * 196, 6272 * 4 + 3136 * 4 * 2, "tensor"),
+STAGE_WORK = {  # per image: (algorithmic FLOPs, bytes the stage must move, bound)
+    # TF32 path: pooled a1 (SPF frame) + 4-bit window codes (argmax + relu mask, 8 B per
+    # 16 channels and window) written, x read
+    "F1_conv1_pool": (2 * 32 * 25 * 784, 784 * 4 + 6272 * 4 + 196 * 2 * 8, "hbm"),
+    "F2_conv2_pool": (2 * 64 * 800 * 196, 6272 * 4 + 3136 * 4 + 49 * 4 * 8, "tensor"),
     "F3_affine_softmax_ce": (2 * 10 * 3136, 3136 * 4 + 10 * 4, "hbm"),
     "B3_affine_bwd": (2 * 10 * 3136, 3136 * 4 + 10 * 4, "hbm"),  # dW3 = ds^T a2, db3
-    # TF32/SPF path: da2 = ds W3 fused with the max-pool routing (reads a2, i2; writes dz2)
-    "B2p_maxpool_bwd2": (2 * 10 * 3136, 3136 * 4 * 2 + 12544 * 4, "hbm"),
+    # da2 = ds W3 fused with the max-pool routing: reads the window codes, writes dz2
+    "B2p_maxpool_bwd2": (2 * 10 * 3136, 49 * 4 * 8 + 12544 * 4, "hbm"),
     "B2f_conv2_bwd_filter": (2 * 64 * 800 * 196, 6272 * 4 + 12544 * 4, "tensor"),
     "B2d_conv2_bwd_data": (2 * 64 * 800 * 196, 12544 * 4 + 6272 * 4, "tensor"),
     "B1p_maxpool_bwd1": (0, 6272 * 4 * 3 + 25088 * 4, "hbm"),
     "B1f_conv1_bwd_filter": (2 * 32 * 25 * 784, 784 * 4 + 25088 * 4, "hbm"),
-    # fused maxpool_bwd1 + conv1 bwd_filter: reads da1, i1, a1 (pooled) and X
-    "B1_fused_pool_bwd_conv1_wgrad": (2 * 32 * 25 * 196, 6272 * 4 * 3 + 784 * 4, "hbm"),
+    # fused maxpool_bwd1 + conv1 bwd_filter: reads da1, the window codes and X
+    "B1_fused_pool_bwd_conv1_wgrad": (2 * 32 * 25 * 196, 6272 * 4 + 196 * 2 * 8 + 784 * 4, "hbm"),
 }
 
 

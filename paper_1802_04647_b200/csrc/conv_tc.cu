@@ -97,6 +97,9 @@ struct TcFwdParams {
   int64_t ntiles;
   uint32_t tmem_cols;
   uint32_t tbuf;       // TMEM accumulator buffer stride: 256 (double buffer) or 0 (single, MT*NFpad <= 512)
+  int cl2;             // CTA-pair cluster: each CTA bulk-loads half of every filter chunk and
+                       // multicasts it to both (halves the L2 -> SMEM filter stream)
+  int64_t iters;       // tile iterations per CTA (cl2: equal in both CTAs, padded with empty tiles)
 };
 
 struct TcPlan {
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       // dense: 128 producer threads (cp.async arrivals) + the expect_tx arrival;
       // CSR: one warp fills a whole stage and arrives once with the expect_tx
       ptx::mbar_init(full + s, p.is_csr ? 1 : 128 + 1);
-      ptx::mbar_init(empty + s, 1);     // tcgen05.commit
+      ptx::mbar_init(empty + s, p.cl2 ? 2 : 1);  // tcgen05.commit (of both CTAs of a pair)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(accf + b, 1);
@@ -332,6 +335,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (p.cl2) ptx::cluster_sync();  // the peer's barriers are initialised before any multicast
+  const uint32_t crank = p.cl2 ? ptx::cluster_ctarank() : 0u;
   const int HW = p.H * p.W;
   const long long t_kernel0 = clock64();
 
@@ -340,6 +345,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     // 4th tile of this CTA and fills its stage alone -- zero-fill, scatter the non-zeros
     // of the images overlapping the tile into their S slots, fence, then one arrival
     // with the filter chunk's expect_tx.  Four tiles' load-latency chains overlap.
+    if (lane == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // packed filters ready
     int tl = warp;  // CTA-local tile counter of this warp
     for (int64_t tile = blockIdx.x + (int64_t)warp * gridDim.x; tile < p.ntiles;
          tile += 4 * (int64_t)gridDim.x, tl += 4) {
@@ -392,7 +398,12 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     const int tid = threadIdx.x;
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    // programmatic dependent launch: everything up to the first packed-filter read
+    // (barriers, TMEM, gather tables, A copies) overlaps the filter-pack kernel
+    if (tid == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int64_t it = 0; it < p.iters; ++it) {
+      const int64_t tile = blockIdx.x + it * gridDim.x;  // >= ntiles: empty (cl2 padding)
+      if (tile >= p.ntiles && !p.cl2) break;
       const int ft = (int)(tile % p.nft);
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
       ptx::named_bar_sync(1, 128);
@@ -422,8 +433,13 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         uint8_t *B = A + p.a_bytes;
         if (tid == 0) {
           ptx::mbar_arrive_expect_tx(full + stage, p.b_bytes);
-          ptx::bulk_g2s(B, p.fp + ((size_t)ft * p.nchunk + ch) * (p.b_bytes / 4), p.b_bytes,
-                        full + stage);
+          const float *bsrc = p.fp + ((size_t)ft * p.nchunk + ch) * (p.b_bytes / 4);
+          if (p.cl2) {
+            const uint32_t half = p.b_bytes / 2;
+            ptx::bulk_g2s_mc(B + crank * half, bsrc + crank * (half / 4), half, full + stage, 0x3);
+          } else {
+            ptx::bulk_g2s(B, bsrc, p.b_bytes, full + stage);
+          }
         }
         const uint32_t a0 = ptx::smem_u32(A);
         const uint32_t a1 = a0 + (uint32_t)p.HALO * 16;
@@ -467,7 +483,9 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     const int PQ = p.P * p.Q;
     const int nc16 = p.NFpad / 16;
     uint32_t tcount = 0;
-    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++tcount) {
+    for (int64_t it = 0; it < p.iters; ++it, ++tcount) {
+      const int64_t tile = blockIdx.x + it * gridDim.x;
+      if (tile >= p.ntiles && !p.cl2) break;
       const int ft = (int)(tile % p.nft);
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
       // double buffer: buffers alternate; single buffer (tbuf 0): buffer 0 every tile
@@ -514,7 +532,10 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
               bdesc += (uint64_t)(2 * nf);  // next tap: 2 quads x NFpad x 16 B
             }
           }
-          if (ptx::elect_one()) ptx::mma_commit(empty + stage);
+          if (ptx::elect_one()) {
+            if (p.cl2) ptx::mma_commit_mc(empty + stage, 0x3);  // frees the stage in both CTAs
+            else ptx::mma_commit(empty + stage);
+          }
           __syncwarp();
           if (++stage == p.nstage) { stage = 0; phase ^= 1; }
         }
@@ -544,6 +565,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, p.tmem_cols);
   }
+  if (p.cl2) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
 }
 
 // Repack filters into [ftile][chunk][tap][quad][NFpad][4] (zero padded).
@@ -558,6 +580,7 @@ constexpr int PACK_MAX_RS = 40;   // taps supported by the staged pack (else per
 __global__ void __launch_bounds__(256) tc_pack_filters_kernel(
     const float *__restrict__ f, float *__restrict__ fp, int Kout, int Cin, int RS, int NFpad,
     int nft, int nchunk, int flip) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL: the conv may start
   __shared__ float sm[PACK_JB * 8 * PACK_MAX_RS];  // [j][c8 * RS + t]
   const int njb = NFpad / PACK_JB;
   const int jb = blockIdx.x % njb, ch = (blockIdx.x / njb) % nchunk, f_ = blockIdx.x / (njb * nchunk);
@@ -606,6 +629,7 @@ __global__ void __launch_bounds__(256) tc_pack_filters_kernel(
 __global__ void tc_pack_filters_elem_kernel(const float *__restrict__ f, float *__restrict__ fp,
                                             int Kout, int Cin, int RS, int NFpad, int nft,
                                             int nchunk, int flip) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t total = (int64_t)nft * nchunk * RS * 2 * NFpad * 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -626,6 +650,7 @@ __global__ void tc_pack_filters_elem_kernel(const float *__restrict__ f, float *
 // KS packing (C == 1): [ftile][r][half][NFpad][4] with packed(k, r, 4*half + e) = F[k][0][r][s]
 __global__ void tc_pack_filters_ks_kernel(const float *__restrict__ f, float *__restrict__ fp,
                                           int Kout, int R, int S, int NFpad, int nft) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t total = (int64_t)nft * R * 2 * NFpad * 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -685,7 +710,11 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   // tiles want two M-tiles sharing each filter chunk (halves the L2 -> SMEM filter
   // stream) -- then one 512-column accumulator
   static const int single_env = getenv("SYSML_TC_SINGLEBUF") ? atoi(getenv("SYSML_TC_SINGLEBUF")) : -1;
-  const bool single = (single_env < 0 || single_env == 1) && p.NFpad == 256 && !pool;
+  static const int cluster_env = getenv("SYSML_TC_CLUSTER") ? atoi(getenv("SYSML_TC_CLUSTER")) : -1;
+  // 256-wide filter tiles: either a CTA pair sharing every filter chunk by multicast
+  // (double-buffered accumulators, MT = 1) or two M-tiles per CTA sharing it (single buffer)
+  p.cl2 = (cluster_env == 1) && p.NFpad == 256 && p.nft == 1 && !pool && !p.ks ? 1 : 0;
+  const bool single = !p.cl2 && (single_env < 0 || single_env == 1) && p.NFpad == 256 && !pool;
   p.tbuf = single ? 0u : TMEM_BUF;
   int mt_cap = std::min(16, (single ? 512 : (int)TMEM_BUF) / p.NFpad);
   p.CT = (p.Q + 7) / 8;
@@ -804,7 +833,12 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
   if (!bias) p.bias_smem = 0;
   static int attr = 0;
   SYSML_TRY(set_smem_attr(tc_conv_fwd_kernel, pl.smem, attr));
-  const int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
+  int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
+  if (p.cl2) {
+    if (grid < 2) p.cl2 = 0;
+    else grid &= ~1;
+  }
+  p.iters = ceil_div(p.ntiles, grid);
   static long long *dclk = nullptr;
   const bool prof = getenv("SYSML_TC_PROFILE") != nullptr;
   p.clk = nullptr;
@@ -813,7 +847,28 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     cudaMemsetAsync(dclk, 0, sizeof(long long) * 8 * 1024, st);
     p.clk = dclk;
   }
-  tc_conv_fwd_kernel<<<grid, TC_FWD_THREADS, pl.smem, st>>>(p);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(TC_FWD_THREADS);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the pack kernel
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+    if (p.cl2) {
+      at[na].id = cudaLaunchAttributeClusterDimension;
+      at[na].val.clusterDim.x = 2;
+      at[na].val.clusterDim.y = 1;
+      at[na].val.clusterDim.z = 1;
+      ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    SYSML_CUDA(cudaLaunchKernelEx(&cfg, tc_conv_fwd_kernel, p));
+  }
   SYSML_LAUNCH_CHECK();
   if (prof) {
     long long h[8 * 1024];
