@@ -265,15 +265,30 @@ __global__ void __launch_bounds__(FBB_THREADS)
   }
 }
 
+// block (32, 8): lane x owns output o, row y sums the y-th contiguous eighth of the CTA
+// partials in order; the row sums are added in row order (deterministic)
 __global__ void fused_b1_reduce_kernel(const float *__restrict__ part, int parts, int K, int RS,
                                        float *__restrict__ df, float *__restrict__ db) {
+  __shared__ float red[8][33];
   const int nout = K * (RS + 1);
-  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x) {
+  const int x = threadIdx.x, y = threadIdx.y;
+  const int c0 = y * parts / 8, c1 = (y + 1) * parts / 8;
+  for (int base = blockIdx.x * 32; base < nout; base += gridDim.x * 32) {
+    const int o = base + x;
     float s = 0.f;
-    for (int c = 0; c < parts; ++c) s += part[(int64_t)c * nout + o];
-    const int kk = o / (RS + 1), i = o - kk * (RS + 1);
-    if (i < RS) df[kk * RS + i] = s;
-    else if (db) db[kk] = s;
+    if (o < nout)
+      for (int c = c0; c < c1; ++c) s += __ldg(part + (int64_t)c * nout + o);
+    red[y][x] = s;
+    __syncthreads();
+    if (y == 0 && o < nout) {
+      float t = 0.f;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) t += red[g][x];
+      const int kk = o / (RS + 1), i = o - kk * (RS + 1);
+      if (i < RS) df[kk * RS + i] = t;
+      else if (db) db[kk] = t;
+    }
+    __syncthreads();
   }
 }
 
@@ -342,7 +357,7 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
     SYSML_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_need));
     kern<<<used, FBB_THREADS, sm_need, st>>>(a, x, cs, xcsr != nullptr, dpool, part);
     SYSML_LAUNCH_CHECK();
-    fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 256), 256, 0, st>>>(
+    fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 32), dim3(32, 8), 0, st>>>(
         part, used, c.K, RS, df, db);
     SYSML_LAUNCH_CHECK();
     return SYSML_OK;
@@ -367,7 +382,7 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
                                                                 argmax, mask, part);
   }
   SYSML_LAUNCH_CHECK();
-  fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 256), 256, 0, st>>>(
+  fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 32), dim3(32, 8), 0, st>>>(
       part, used, c.K, RS, df, db);
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;
