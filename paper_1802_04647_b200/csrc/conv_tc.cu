@@ -87,6 +87,9 @@ struct TcFwdParams {
   int pool, PR, PS, Pp, Qp;
   int bias_smem;       // bias staged in shared memory (K floats)
   int ks;              // C == 1: the S column taps fill the MMA K slots (s = 4*half + e)
+  int sn;              // narrow filter banks: the S column taps fold into N (D'[pos][(s,k)]),
+                       // the epilogue adds Y[pos][k] = sum_s D'[pos + s][(s,k)]
+  int NN;              // MMA N: NFpad, or S*NFpad in SN mode
   int is_csr;          // KS mode only: input rows are CSR (scattered straight into the operand)
   sysml_csr csr;
   int64_t in_plane;    // > 0: input is SPF [C][in_plane], stored position = frame pos + in_shift
@@ -300,13 +303,82 @@ __device__ __forceinline__ void epi_pool2(const TcFwdParams &p, uint32_t tbase, 
   }
 }
 
+constexpr int SN_MAXMT = 4;
+constexpr int SN_XCH_FLOATS = 2 * SN_MAXMT * 4 * 8 * 4 * 16;  // [set][M-tile][warp][s][row < S-1 <= 4][16]
+
+// SN epilogue (column taps in N, single-buffered MT M-tiles): accumulator row
+// l = i*128 + qd*32 + lane holds D'[g0 + l][(s, k)]; output
+// Y[g0 + l][k] = b[k] + sum_s D'[g0 + l + s][(s, k)] for l < cta_pos = MT*128 - (S-1)
+// (CTA tiles overlap by S-1 rows).  Rows l + s of the same warp come by shfl_down; the
+// first S-1 rows of the next 32-row group (next quadrant, or quadrant 0 of the next
+// M-tile) are dumped to shared memory first.  The two warp sets split the 16-channel
+// chunks.
+__device__ __forceinline__ void epi_sn(const TcFwdParams &p, uint32_t tbase, int64_t g0, int qd,
+                                       int lane, const float *bias_s, int eset, float *xch_all) {
+  const int PQ = p.P * p.Q;
+  const int nc16 = p.NFpad / 16;
+  float *__restrict__ y = p.y;
+  float *xch = xch_all + eset * (SN_MAXMT * 4 * 8 * 4 * 16);
+  auto xidx = [&](int i, int q, int s_, int row) { return (((i * 4 + q) * 8 + s_) * 4 + row) * 16; };
+  for (int c16 = eset; c16 < nc16; c16 += 2) {
+    // 1) dump the first S-1 rows of every 32-row group for s >= 1
+    for (int i = 0; i < p.MT; ++i)
+      for (int s_ = 1; s_ < p.S; ++s_) {
+        float t[16];
+        ptx::tmem_ld16(tbase + (uint32_t)(i * p.NN + s_ * p.NFpad + c16 * 16), t);
+        if (lane < p.S - 1) {
+          float *dst = xch + xidx(i, qd, s_, lane);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) dst[j] = t[j];
+        }
+      }
+    ptx::named_bar_sync(2 + eset, 128);
+    const int k0 = c16 * 16;
+    float b[16];
+    load_bias16(p, bias_s, k0, b);
+    // 2) shift-add per M-tile
+    for (int i = 0; i < p.MT; ++i) {
+      const int l = i * 128 + qd * 32 + lane;
+      const int ni = qd == 3 ? i + 1 : i, nq = (qd + 1) & 3;  // next 32-row group
+      float acc[16];
+      ptx::tmem_ld16(tbase + (uint32_t)(i * p.NN + c16 * 16), acc);
+      for (int s_ = 1; s_ < p.S; ++s_) {
+        float t[16];
+        ptx::tmem_ld16(tbase + (uint32_t)(i * p.NN + s_ * p.NFpad + c16 * 16), t);
+        const bool from_next = lane + s_ >= 32;
+        const float *src = xch + xidx(ni < p.MT ? ni : 0, nq, s_, from_next ? lane + s_ - 32 : 0);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float v = __shfl_down_sync(0xffffffffu, t[j], s_);
+          acc[j] += from_next ? src[j] : v;
+        }
+      }
+      const int64_t g = g0 + l;
+      if (l < (int)p.cta_pos && g < p.G) {
+        const int n = (int)(g / p.Lf);
+        const int rem = (int)(g - (int64_t)n * p.Lf);
+        const int hh = rem / p.Wf, q = rem - hh * p.Wf;
+        if (hh < p.P && q < p.Q) {
+          float *yp = y + (int64_t)n * p.K * PQ + (int64_t)hh * p.Q + q + (int64_t)k0 * PQ;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (k0 + j < p.K) yp[(int64_t)j * PQ] = acc[j] + b[j];
+        }
+      }
+    }
+    ptx::named_bar_sync(2 + eset, 128);  // before the next chunk overwrites the dump
+  }
+}
+
 __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const TcFwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t *stage_base = smem;
   int *src_off = reinterpret_cast<int *>(smem + (size_t)p.nstage * p.stage_bytes);
   float *bias_s = reinterpret_cast<float *>(src_off + p.HALO + 8);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(
+  // SN epilogue exchange: [set 2][warp 4][s 8][row 4][16] floats (rows 0..3 of each warp)
+  float *sn_xch = reinterpret_cast<float *>(
       (reinterpret_cast<uintptr_t>(bias_s + (p.bias_smem ? p.K : 0)) + 15) & ~(uintptr_t)15);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sn_xch + (p.sn ? SN_XCH_FLOATS : 0));
   uint64_t *full = bars;
   uint64_t *empty = bars + p.nstage;
   uint64_t *accf = bars + 2 * p.nstage;  // [2]
@@ -477,7 +549,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
   } else {
     // ================= MMA issuer (warp 4) | epilogue (warps 5-12, TMEM quadrant warp % 4)
     const int qd = warp & 3;
-    const uint32_t idesc = ptx::make_idesc_tf32(128, p.NFpad);
+    const uint32_t idesc = ptx::make_idesc_tf32(128, p.NN);
     int stage = 0;
     uint32_t phase = 0;
     const int PQ = p.P * p.Q;
@@ -503,7 +575,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         const int n_inner = p.tile2d ? p.CT : 1;
         const uint32_t step_outer = p.tile2d ? (uint32_t)(16 * p.Wf) : 128u;
         const uint32_t jump_outer = step_outer - 8u * (uint32_t)(n_inner - 1);
-        const uint32_t nf = (uint32_t)p.NFpad;
+        const uint32_t nf = (uint32_t)p.NN;
         const uint32_t sbase = ptx::smem_u32(stage_base);
         for (int ch = 0; ch < p.nchunk; ++ch) {
           const long long t_w1 = clock64();
@@ -515,7 +587,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           uint64_t bdesc = ptx::make_desc(A + p.a_bytes, nf * 16, 128);
           uint32_t acc = ch != 0 ? 1u : 0u;
           uint32_t drow = 0;
-          const int s_taps = p.ks ? 1 : p.S;  // KS: all S column taps are in the K slots
+          // KS: all S column taps are in the K slots; SN: in the N columns
+          const int s_taps = (p.ks || p.sn) ? 1 : p.S;
           for (int r = 0; r < p.R; ++r, drow += (uint32_t)p.Wf) {
             for (int s_ = 0; s_ < s_taps; ++s_) {
               uint64_t ad = adesc0 + (uint64_t)(drow + (uint32_t)s_);
@@ -550,8 +623,13 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(qd * 32) << 16) + buf * p.tbuf;
       const int eset = (warp - 5) >> 2;  // epilogue warp set 0 / 1 -> even / odd M-tiles
-      if (p.pool) epi_pool2(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
-      else epi_plain(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
+      if (p.sn) {
+        epi_sn(p, tbase, g0, qd, lane, bias_s, eset, sn_xch);
+      } else if (p.pool) {
+        epi_pool2(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
+      } else {
+        epi_plain(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
+      }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(acce + buf);
@@ -647,6 +725,31 @@ __global__ void tc_pack_filters_elem_kernel(const float *__restrict__ f, float *
   }
 }
 
+// SN packing: [chunk][r][quad][S*NFpad][4] with column n = s*NFpad + j:
+//  packed(j, c, r, s) = F[j][c][r][s] (flip 0) or F[c][j][R-1-r][S-1-s] (flip 1, bwd_data)
+__global__ void tc_pack_filters_sn_kernel(const float *__restrict__ f, float *__restrict__ fp,
+                                          int Kout, int Cin, int R, int S, int NFpad, int nchunk,
+                                          int flip) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int NN = S * NFpad;
+  const int64_t total = (int64_t)nchunk * R * 2 * NN * 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int e = (int)(t % 4); t /= 4;
+    const int n = (int)(t % NN); t /= NN;
+    const int g = (int)(t % 2); t /= 2;
+    const int r = (int)(t % R); t /= R;
+    const int ch = (int)t;
+    const int s_ = n / NFpad, j = n - s_ * NFpad, c = ch * 8 + g * 4 + e;
+    float v = 0.f;
+    if (j < Kout && c < Cin)
+      v = flip ? f[(((int64_t)c * Kout + j) * R + (R - 1 - r)) * S + (S - 1 - s_)]
+               : f[(((int64_t)j * Cin + c) * R + r) * S + s_];
+    fp[i] = v;
+  }
+}
+
 // KS packing (C == 1): [ftile][r][half][NFpad][4] with packed(k, r, 4*half + e) = F[k][0][r][s]
 __global__ void tc_pack_filters_ks_kernel(const float *__restrict__ f, float *__restrict__ fp,
                                           int Kout, int R, int S, int NFpad, int nft) {
@@ -699,11 +802,18 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
     p.nft = (K + 255) / 256;
   }
   p.ks = (allow_ks && C == 1 && S <= 8) ? 1 : 0;
+  // SN: narrow filter banks (N = NFpad <= 64 keeps the MMA SMEM-operand bound) fold
+  // the column taps into N when S * NFpad still fits one 256-column accumulator
+  static const int sn_env = getenv("SYSML_TC_SN") ? atoi(getenv("SYSML_TC_SN")) : -1;
+  p.sn = (sn_env != 0 && !p.ks && !pool && p.nft == 1 && S >= 2 && S <= 5 && p.NFpad <= 64 &&
+          S * p.NFpad <= 256 && p.NFpad % 16 == 0)
+             ? 1 : 0;
+  p.NN = p.sn ? S * p.NFpad : p.NFpad;
   p.nchunk = p.ks ? 1 : (C + 7) / 8;
   const int RS = R * S;
-  const int b_taps = p.ks ? R : RS;
-  const int s_halo = p.ks ? 0 : S - 1;  // KS: the S window lives inside each operand row
-  p.b_bytes = (uint32_t)(b_taps * 2 * p.NFpad * 16);
+  const int b_taps = (p.ks || p.sn) ? R : RS;
+  const int s_halo = (p.ks || p.sn) ? 0 : S - 1;  // KS / SN: the S window is in K / N
+  p.b_bytes = (uint32_t)(b_taps * 2 * p.NN * 16);
   const int nsm = sm_count();
   const int64_t rows_total = (int64_t)N * p.Hs;
   // TMEM double buffer (epilogue overlaps the next tile's MMAs) unless B-heavy wide
@@ -714,9 +824,9 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   // 256-wide filter tiles: either a CTA pair sharing every filter chunk by multicast
   // (double-buffered accumulators, MT = 1) or two M-tiles per CTA sharing it (single buffer)
   p.cl2 = (cluster_env == 1) && p.NFpad == 256 && p.nft == 1 && !pool && !p.ks ? 1 : 0;
-  const bool single = !p.cl2 && (single_env < 0 || single_env == 1) && p.NFpad == 256 && !pool;
+  const bool single = (!p.cl2 && (single_env < 0 || single_env == 1) && p.NFpad == 256 && !pool) || p.sn;
   p.tbuf = single ? 0u : TMEM_BUF;
-  int mt_cap = std::min(16, (single ? 512 : (int)TMEM_BUF) / p.NFpad);
+  int mt_cap = p.sn ? std::min(SN_MAXMT, 512 / p.NN) : std::min(16, (single ? 512 : (int)TMEM_BUF) / p.NFpad);
   p.CT = (p.Q + 7) / 8;
   if (p.tile2d && p.CT > mt_cap) return pl;
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -732,7 +842,8 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
         halo = round_up(halo, 8);  // LBO multiple of 128 B
         ntiles = ceil_div(rows_total, (int64_t)bb * 16) * p.nft;
       } else {
-        cta_pos = (int64_t)mt * 128;
+        // SN: tiles overlap by S-1 rows (output row l needs accumulator rows l .. l+S-1)
+        cta_pos = p.sn ? (int64_t)mt * 128 - (S - 1) : (int64_t)mt * 128;
         halo = round_up(mt * 128 + (R - 1) * p.Wf + s_halo, 8);  // LBO multiple of 128 B
         ntiles = ceil_div(p.G, cta_pos) * p.nft;
       }
@@ -740,7 +851,8 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
       const uint32_t a_bytes = (uint32_t)(2 * halo * 16);
       const uint32_t stage = a_bytes + p.b_bytes;
       p.bias_smem = K <= 4096 ? 1 : 0;
-      const size_t fixed = (size_t)(halo + 8) * 4 + (p.bias_smem ? (size_t)K * 4 : 0) + 16 + 8 * 24 + 16;
+      const size_t fixed = (size_t)(halo + 8) * 4 + (p.bias_smem ? (size_t)K * 4 : 0) + 16 + 8 * 24 + 16 +
+                           (p.sn ? (size_t)SN_XCH_FLOATS * 4 : 0);
       const int nst = (int)((SMEM_BUDGET - (int64_t)fixed) / (int64_t)stage);
       if (nst < 2) continue;
       p.MT = p.tile2d ? bb * p.CT : mt;
@@ -760,9 +872,9 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   }
   if (!pl.ok) return pl;
   if (p.tile2d && (uint32_t)p.Wf * 16 >= (1u << 18)) { pl.ok = false; return pl; }
-  if (p.MT * p.NFpad > (p.tbuf ? (int)p.tbuf : 512)) { pl.ok = false; return pl; }
+  if (p.MT * p.NN > (p.tbuf ? (int)p.tbuf : 512)) { pl.ok = false; return pl; }
   p.tmem_cols = 512;  // whole TMEM: base column 0 (1 CTA per SM), issue loops address from 0
-  pl.fp_bytes = align_up((size_t)p.nft * p.nchunk * b_taps * 8 * p.NFpad * sizeof(float), 256);
+  pl.fp_bytes = align_up((size_t)p.nft * p.nchunk * b_taps * 8 * p.NN * sizeof(float), 256);
   return pl;
 }
 
@@ -810,6 +922,11 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     const int64_t total = (int64_t)p.nft * p.R * 2 * p.NFpad * 4;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * sm_count());
     tc_pack_filters_ks_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, p.R, p.S, p.NFpad, p.nft);
+    SYSML_LAUNCH_CHECK();
+  } else if (p.sn) {
+    const int64_t total = (int64_t)p.nchunk * p.R * 2 * p.NN * 4;
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 8 * sm_count());
+    tc_pack_filters_sn_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, f_cin, p.R, p.S, p.NFpad, p.nchunk, flip);
     SYSML_LAUNCH_CHECK();
   } else {
     const int RS = p.R * p.S;
