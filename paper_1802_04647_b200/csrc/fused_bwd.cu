@@ -191,8 +191,11 @@ __global__ void __launch_bounds__(FBB_THREADS)
     }
     return;
   }
-  const int k = t / a.tpk, j = t - k * a.tpk;
+  // lane = filter k (K <= 32), warp w = every 8th pooled position: the window reads of a
+  // warp touch at most 4 distinct addresses (the 2x2 winners) -> broadcasts, no conflicts
+  const int k = lane, wq = warp;
   const bool kok = k < a.K;
+  const int kk = kok ? k : 0;
   const float invQ = 1.0f / (float)a.Qp, invW = 1.0f / (float)a.W;
   float acc[RS];
 #pragma unroll
@@ -228,21 +231,22 @@ __global__ void __launch_bounds__(FBB_THREADS)
       }
     }
     ptx::named_bar_sync(1, FB_THREADS);  // image ready
-    if (kok) {
-      const float *gk = gs + k * PpQp;
-      const unsigned long long *ck = cs + (k >> 4) * PpQp;
-      const int sh = 4 * (k & 15);
-      for (int pp = j; pp < PpQp; pp += a.tpk) {
+    {
+      const float *gk = gs + kk * PpQp;
+      const unsigned long long *ck = cs + (kk >> 4) * PpQp;
+      const int sh = 4 * (kk & 15);
+      for (int pp = wq; pp < PpQp; pp += FB_THREADS / 32) {
         const float g0 = gk[pp];
         const uint32_t cd = (uint32_t)(ck[pp] >> sh) & 15u;
-        if (!(cd & 4u) || g0 == 0.f) continue;  // masked (reading R9) or zero gradient
+        // masked (reading R9) lanes add g = 0: every lane stays on the same path
+        const float g = (kok && (cd & 4u)) ? g0 : 0.f;
         const int pr = __float2int_rz(((float)pp + 0.5f) * invQ), pc = pp - pr * a.Qp;
         const float *win = img + (2 * pr + (int)((cd >> 1) & 1u)) * a.Wp + 2 * pc + (int)(cd & 1u);
-        dbacc += g0;
+        dbacc += g;
 #pragma unroll
         for (int r = 0; r < R_; ++r)
 #pragma unroll
-          for (int s_ = 0; s_ < S_; ++s_) acc[r * S_ + s_] = fmaf(g0, win[r * a.Wp + s_], acc[r * S_ + s_]);
+          for (int s_ = 0; s_ < S_; ++s_) acc[r * S_ + s_] = fmaf(g, win[r * a.Wp + s_], acc[r * S_ + s_]);
       }
     }
     __syncwarp();
@@ -258,9 +262,9 @@ __global__ void __launch_bounds__(FBB_THREADS)
   ptx::named_bar_sync(1, FB_THREADS);
   const int nout = a.K * (RS + 1);
   for (int o = t; o < nout; o += FB_THREADS) {
-    const int kk = o / (RS + 1), i = o - kk * (RS + 1);
+    const int ko = o / (RS + 1), i = o - ko * (RS + 1);
     float sum = 0.f;
-    for (int jj = 0; jj < a.tpk; ++jj) sum += sred[i * FB_THREADS + kk * a.tpk + jj];
+    for (int w = 0; w < FB_THREADS / 32; ++w) sum += sred[i * FB_THREADS + w * 32 + ko];  // warp order
     part[(int64_t)blockIdx.x * nout + o] = sum;
   }
 }
@@ -341,7 +345,7 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
   sysml_csr empty{};
   const sysml_csr &cs = xcsr ? *xcsr : empty;
   if (a.code) {
-    if (pa.R != 2 || pa.S != 2 || ((uintptr_t)dpool & 15) || (!xcsr && ((uintptr_t)x & 15)) ||
+    if (c.K > 32 || pa.R != 2 || pa.S != 2 || ((uintptr_t)dpool & 15) || (!xcsr && ((uintptr_t)x & 15)) ||
         ((int64_t)c.K * pa.P * pa.Q) % 4 || (pa.P * pa.Q) % 2 || (c.H * c.W) % 4) {
       set_error("fused pool-bwd + conv1 wgrad: window codes need 2x2 pooling and 16-byte aligned planes");
       return SYSML_ERR_UNSUPPORTED;
