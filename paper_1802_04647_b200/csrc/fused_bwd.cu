@@ -350,6 +350,9 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
       set_error("fused pool-bwd + conv1 wgrad: window codes need 2x2 pooling and 16-byte aligned planes");
       return SYSML_ERR_UNSUPPORTED;
     }
+    // padded-image row pitch = 2 mod 32: the four 2x2-window candidates of a warp's window
+    // reads ((dr, ds) offsets 0, 1, pitch, pitch+1) fall in four different banks
+    a.Wp = (a.Wp + 31 - 2) / 32 * 32 + 2;
     const int G = (c.K + 15) / 16;
     const size_t stage = align_up((size_t)c.K * pa.P * pa.Q * 4 + (size_t)G * pa.P * pa.Q * 8 +
                                       (xcsr ? 0 : (size_t)c.H * c.W * 4), 16);
