@@ -173,31 +173,52 @@ __global__ void da2_kernel(int n, const float *__restrict__ ds, const float *__r
 // through the 2x2 max-pool argmax (ReLU mask a2 > 0) into the unpooled gradient dz2 in
 // SPF planes [64][plane] (output frame 16x16, position n*256 + h*16 + w): the da2 tensor
 // is never materialised.  One thread per pooled output (n, k, pp, pc).
-__global__ void affine_bwd_route_spf_kernel(int n, const float *__restrict__ ds,
-                                            const float *__restrict__ W3,
-                                            const uint64_t *__restrict__ c2, int64_t cplane,
-                                            float *__restrict__ dz2s, int64_t plane) {
-  const int64_t total = (int64_t)n * D3;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
-       o += (int64_t)gridDim.x * blockDim.x) {
-    const int s = (int)(o / D3);
-    const int d = (int)(o - (int64_t)s * D3);  // = k*49 + pp*7 + pc
-    const int k = d / 49, r = d - k * 49, pp = r / 7, pc = r - pp * 7;
-    // window code of the pool2 winner: positive*4 + dr*2 + ds (positive: a2 > 0, R9)
-    const uint32_t cd =
-        (uint32_t)(__ldg(reinterpret_cast<const unsigned long long *>(c2) + (int64_t)(k >> 4) * cplane +
-                         (int64_t)s * 49 + r) >> (4 * (k & 15))) & 15u;
-    float g = 0.f;
-    if (cd & 4u) {
+// B2p (TF32 path): da2 = ds W3 (P:58-84 affine backward) fused with the masked max-pool
+// routing (reading R9) into the dz2 SPF planes.  Block = 256 feature indices d
+// x a chunk of images: each thread keeps its W3 column (10 floats) in registers and walks
+// the chunk's images (ds rows staged in shared memory), so W3 is read once per block.
+constexpr int B2P_IMGS = 32;
+__global__ void __launch_bounds__(256) affine_bwd_route_spf_kernel(
+    int n, const float *__restrict__ ds, const float *__restrict__ W3,
+    const uint64_t *__restrict__ c2, int64_t cplane, float *__restrict__ dz2s, int64_t plane) {
+  __shared__ float dss[B2P_IMGS * NCLS];
+  const int d = blockIdx.x * 256 + threadIdx.x;  // = k*49 + pp*7 + pc
+  const int s0 = blockIdx.y * B2P_IMGS, s1 = min(n, s0 + B2P_IMGS);
+  for (int i = threadIdx.x; i < (s1 - s0) * NCLS; i += 256) dss[i] = __ldg(ds + (int64_t)s0 * NCLS + i);
+  __syncthreads();
+  if (d >= D3) return;
+  float w[NCLS];
 #pragma unroll
-      for (int j = 0; j < NCLS; ++j) g = fmaf(__ldg(ds + s * NCLS + j), __ldg(W3 + j * D3 + d), g);
+  for (int j = 0; j < NCLS; ++j) w[j] = __ldg(W3 + j * D3 + d);
+  const int k = d / 49, r = d - k * 49, pp = r / 7, pc = r - pp * 7;
+  const unsigned long long *cw = reinterpret_cast<const unsigned long long *>(c2) + (int64_t)(k >> 4) * cplane + r;
+  const int sh = 4 * (k & 15);
+  float *base = dz2s + (int64_t)k * plane + (2 * pp) * 16 + 2 * pc;
+  for (int sb = s0; sb < s1; sb += 4) {
+    uint32_t cd[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)  // the batch's code loads in flight together
+      cd[u] = sb + u < s1 ? (uint32_t)(__ldg(cw + (int64_t)(sb + u) * 49) >> sh) & 15u : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int s = sb + u;
+      if (s >= s1) break;
+      // window code of the pool2 winner: positive*4 + dr*2 + ds (positive: a2 > 0, R9)
+      float g = 0.f;
+      if (cd[u] & 4u) {
+        const float *dsr = dss + (s - s0) * NCLS;
+#pragma unroll
+        for (int j = 0; j < NCLS; ++j) g = fmaf(dsr[j], w[j], g);
+      }
+      const uint32_t wp = cd[u] & 3u;
+      float *bs = base + (int64_t)s * 256;
+      *reinterpret_cast<float2 *>(bs) = make_float2(wp == 0 ? g : 0.f, wp == 1 ? g : 0.f);
+      *reinterpret_cast<float2 *>(bs + 16) = make_float2(wp == 2 ? g : 0.f, wp == 3 ? g : 0.f);
+      if (pc == 6) {  // the frame's zero columns 14-15 too: whole 32-byte sectors written
+        *reinterpret_cast<float2 *>(bs + 2) = make_float2(0.f, 0.f);
+        *reinterpret_cast<float2 *>(bs + 18) = make_float2(0.f, 0.f);
+      }
     }
-    float *base = dz2s + (int64_t)k * plane + (int64_t)s * 256 + (2 * pp) * 16 + 2 * pc;
-    const uint32_t wp = cd & 3u;
-    float2 top = make_float2(wp == 0 ? g : 0.f, wp == 1 ? g : 0.f);
-    float2 bot = make_float2(wp == 2 ? g : 0.f, wp == 3 ? g : 0.f);
-    *reinterpret_cast<float2 *>(base) = top;
-    *reinterpret_cast<float2 *>(base + 16) = bot;
   }
 }
 
@@ -544,8 +565,7 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
   if (h->spf) {
     // B2p: unpooled gradient straight into the SPF planes (output-frame convention)
     SYSML_TRY(T.begin(4));
-    affine_bwd_route_spf_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)n * D3, 256),
-                                                               16 * sm_count()),
+    affine_bwd_route_spf_kernel<<<dim3((unsigned)ceil_div(D3, 256), (unsigned)ceil_div(n, B2P_IMGS)),
                                   256, 0, st>>>(n, h->ds, params + OFF_W3, h->c2,
                                                 (int64_t)h->max_b * 49, h->dz2s, h->spf_plane);
     SYSML_LAUNCH_CHECK();
