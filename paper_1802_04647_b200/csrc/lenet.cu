@@ -125,10 +125,17 @@ __global__ void dw3_partial_kernel(int n, int n_per_chunk, const float *__restri
     for (int i = threadIdx.x; i < cnt * NCLS; i += DW3_THREADS) dss[i] = ds[(int64_t)nb * NCLS + i];
     __syncthreads();
     if (d < D3) {
-      for (int i = 0; i < cnt; ++i) {
-        const float v = __ldg(a2 + (int64_t)(nb + i) * D3 + d);
+      for (int i0 = 0; i0 < cnt; i0 += 8) {
+        float v[8];
 #pragma unroll
-        for (int j = 0; j < NCLS; ++j) acc[j] = fmaf(dss[i * NCLS + j], v, acc[j]);
+        for (int u = 0; u < 8; ++u)  // 8 images' loads in flight
+          v[u] = i0 + u < cnt ? __ldg(a2 + (int64_t)(nb + i0 + u) * D3 + d) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (i0 + u >= cnt) break;
+#pragma unroll
+          for (int j = 0; j < NCLS; ++j) acc[j] = fmaf(dss[(i0 + u) * NCLS + j], v[u], acc[j]);
+        }
       }
     }
   }
