@@ -187,7 +187,8 @@ __global__ void da2_kernel(int n, const float *__restrict__ ds, const float *__r
 constexpr int B2P_IMGS = 32;
 __global__ void __launch_bounds__(256) affine_bwd_route_spf_kernel(
     int n, const float *__restrict__ ds, const float *__restrict__ W3,
-    const uint64_t *__restrict__ c2, int64_t cplane, float *__restrict__ dz2s, int64_t plane) {
+    const uint64_t *__restrict__ c2, int64_t cplane, float *__restrict__ dz2s, int64_t plane,
+    float *__restrict__ dbpart) {
   __shared__ float dss[B2P_IMGS * NCLS];
   const int d = blockIdx.x * 256 + threadIdx.x;  // = k*49 + pp*7 + pc
   const int s0 = blockIdx.y * B2P_IMGS, s1 = min(n, s0 + B2P_IMGS);
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(256) affine_bwd_route_spf_kernel(
   const unsigned long long *cw = reinterpret_cast<const unsigned long long *>(c2) + (int64_t)(k >> 4) * cplane + r;
   const int sh = 4 * (k & 15);
   float *base = dz2s + (int64_t)k * plane + (2 * pp) * 16 + 2 * pc;
+  float gsum = 0.f;  // db2 partial of this (k, window) over the chunk's images (image order)
   for (int sb = s0; sb < s1; sb += 4) {
     uint32_t cd[4];
 #pragma unroll
@@ -217,6 +219,7 @@ __global__ void __launch_bounds__(256) affine_bwd_route_spf_kernel(
 #pragma unroll
         for (int j = 0; j < NCLS; ++j) g = fmaf(dsr[j], w[j], g);
       }
+      gsum += g;
       const uint32_t wp = cd[u] & 3u;
       float *bs = base + (int64_t)s * 256;
       *reinterpret_cast<float2 *>(bs) = make_float2(wp == 0 ? g : 0.f, wp == 1 ? g : 0.f);
@@ -227,6 +230,29 @@ __global__ void __launch_bounds__(256) affine_bwd_route_spf_kernel(
       }
     }
   }
+  dbpart[(int64_t)blockIdx.y * D3 + d] = gsum;
+}
+
+// db2[k] = fixed-order sum of the B2p partials: block k, thread t sums chunks t, t + 256, ...
+// (each over the 49 windows in order), then a fixed shared-memory tree
+__global__ void __launch_bounds__(256) db2_reduce_kernel(const float *__restrict__ dbpart, int chunks,
+                                                         float *__restrict__ db) {
+  __shared__ float red[256];
+  const int k = blockIdx.x, t = threadIdx.x;
+  float acc = 0.f;
+  for (int c = t; c < chunks; c += 256) {
+    const float *pr = dbpart + (int64_t)c * D3 + k * 49;
+    float v = 0.f;
+    for (int r = 0; r < 49; ++r) v += __ldg(pr + r);
+    acc += v;
+  }
+  red[t] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (t < o) red[t] += red[t + o];
+    __syncthreads();
+  }
+  if (t == 0) db[k] = red[0];
 }
 
 __global__ void sgd_kernel(float *__restrict__ p, const float *__restrict__ g, int64_t n,
@@ -296,6 +322,7 @@ struct sysml_lenet {
   float *a1s = nullptr, *dz2s = nullptr;
   // TF32 path: pool argmax as packed 2-bit window codes, one u32 per (16 channels, window)
   uint64_t *c1 = nullptr, *c2 = nullptr;  // [2][b*196], [4][b*49] (kernels.cuh TcSpfIO::code)
+  float *db2part = nullptr;                // B2p's conv2 bias-gradient partials [chunks][3136]
 };
 
 namespace {
@@ -428,7 +455,9 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
       need = std::max(need, tc_wgrad_spf_ws(sc));
       if (tc_wgrad_spf_tma_supported(sc)) need = std::max(need, tc_wgrad_spf_tma_ws(sc));
       ALLOC(h->a1s, 32 * h->spf_plane);
-      if (cudaMalloc(&h->c1, sizeof(uint64_t) * 2 * (size_t)max_local_batch * 196) != cudaSuccess ||
+      if (cudaMalloc(&h->db2part, sizeof(float) * D3 * (size_t)ceil_div(max_local_batch, B2P_IMGS)) !=
+              cudaSuccess ||
+          cudaMalloc(&h->c1, sizeof(uint64_t) * 2 * (size_t)max_local_batch * 196) != cudaSuccess ||
           cudaMalloc(&h->c2, sizeof(uint64_t) * 4 * (size_t)max_local_batch * 49) != cudaSuccess) {
         set_error("cudaMalloc failed for the window-code buffers");
         return fail(SYSML_ERR_CUDA);
@@ -457,7 +486,7 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
 sysml_status sysml_lenet_destroy(sysml_lenet *h) {
   if (!h) return SYSML_OK;
   cudaFree(h->a1); cudaFree(h->i1); cudaFree(h->a2); cudaFree(h->i2); cudaFree(h->ds);
-  cudaFree(h->c1); cudaFree(h->c2);
+  cudaFree(h->c1); cudaFree(h->c2); cudaFree(h->db2part);
   cudaFree(h->lossn); cudaFree(h->da2); cudaFree(h->dz2); cudaFree(h->da1); cudaFree(h->dz1);
   cudaFree(h->part3); cudaFree(h->loss_dev); cudaFree(h->lab_dev); cudaFree(h->x_dev);
   cudaFree(h->ws);
@@ -574,15 +603,20 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     SYSML_TRY(T.begin(4));
     affine_bwd_route_spf_kernel<<<dim3((unsigned)ceil_div(D3, 256), (unsigned)ceil_div(n, B2P_IMGS)),
                                   256, 0, st>>>(n, h->ds, params + OFF_W3, h->c2,
-                                                (int64_t)h->max_b * 49, h->dz2s, h->spf_plane);
+                                                (int64_t)h->max_b * 49, h->dz2s, h->spf_plane,
+                                                h->db2part);
     SYSML_LAUNCH_CHECK();
     SYSML_TRY(T.end());
     // B2f
     SYSML_TRY(T.begin(5));
     SpfConv sc{64, 32, 5, 5, 16, (int64_t)n * 256, h->spf_plane, h->spf_plane, 0, 0};
     if (tc_wgrad_spf_tma_supported(sc))
-      SYSML_TRY(tc_wgrad_spf_tma(sc, h->a1s, h->dz2s, grads + OFF_F2, grads + OFF_B2, h->ws, st));
-    else
+    {
+      // db2 came out of B2p; the bwd_filter kernel computes dF2 only
+      SYSML_TRY(tc_wgrad_spf_tma(sc, h->a1s, h->dz2s, grads + OFF_F2, nullptr, h->ws, st));
+      db2_reduce_kernel<<<64, 256, 0, st>>>(h->db2part, (int)ceil_div(n, B2P_IMGS), grads + OFF_B2);
+      SYSML_LAUNCH_CHECK();
+    } else
       SYSML_TRY(tc_wgrad_spf(sc, h->a1s, h->dz2s, grads + OFF_F2, grads + OFF_B2, h->ws, st));
     SYSML_TRY(T.end());
     // B2d: input frame (pad 2) position = stored output-frame position + 34
