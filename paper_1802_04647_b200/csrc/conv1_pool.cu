@@ -1,0 +1,335 @@
+// conv1_pool.cu -- fused conv2d(C = 1) + bias + relu + 2x2/2 max-pool on tcgen05 with the
+// pooling window in the MMA's N dimension (LeNet conv1, BJ cfg 1-3; A1 + A3 of SURVEY §8).
+//
+// GEMM rows are POOLED windows m = (n, pp, pc).  The 2x2 window's conv outputs are
+//   y(2pp+dr, 2pc+ds, k) = sum_{r,s} F[k][r][s] * x_f(2pp + dr + r, 2pc + ds + s)
+// (x_f = zero-padded input).  With the row operand
+//   A_t[m][e] = x_f(2pp + t, 2pc + e),  e = 0..7  (8 consecutive inputs of one row)
+// and the filter operand  B_r[e][(ds, k)] = F[k][r][e - ds]  (0 <= e - ds < S),
+//   D_dr[m][(ds, k)] = sum_r A_{r+dr}[m] . B_r      (dr = 0, 1: 2*R MMAs, N = 2*Kp)
+// holds all four window values of every filter in ONE TMEM lane, so the epilogue's
+// bias + relu + max + first-occurrence argmax (readings R5/R7/R8) is lane-local -- no
+// shuffles -- and every lane stores one pooled output per filter.  No frame positions
+// are wasted (rows are exactly the pooled windows).
+//
+// Producer: A_t rows are 8-byte cp.async chunks straight from the NCHW image (pad even,
+// W even: a chunk is fully inside or fully padding -> zero-fill); B (all R taps, a few KB)
+// is bulk-copied once per CTA.  Warp roles as in conv_tc.cu: 4 producer warps, 1 MMA
+// warp, 8 epilogue warps (the two sets take the two M-tiles of a CTA tile).
+#include "common.cuh"
+#include "kernels.cuh"
+#include "tc_ptx.cuh"
+
+#include <algorithm>
+
+namespace sysml {
+
+namespace {
+
+constexpr int C1P_THREADS = 416;
+constexpr int C1P_MT = 2;  // M-tiles per CTA tile (one per epilogue warp set)
+
+struct C1pParams {
+  const float *x;
+  const float *fp;    // packed B: [r][quad][NN][4]
+  const float *bias;  // may be null
+  float *pout;        // pooled output (NCHW, or SPF planes when out_plane > 0)
+  int32_t *parg;      // int32 argmax (NCHW pooled layout) or null
+  uint64_t *pcode;    // 4-bit window codes (TcSpfIO::code) or null
+  int64_t code_plane;
+  int N, H, W, K, R, S, ph, pw, P, Q, Pp, Qp;
+  int Kp, NN;         // filters padded to 16 / 32; NN = 2*Kp
+  int T;              // A row blocks per M-tile = R + 1
+  int64_t nwin, ntiles;
+  int64_t out_plane;
+  int out_Wf, out_Lf, out_off;
+  int nstage;
+  uint32_t a_bytes, b_bytes;  // per stage (T blocks of 128 rows x 32 B), B total
+};
+
+__global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t *Bs = smem;                                // R taps x [quad][NN][4]
+  uint8_t *stages = smem + ((p.b_bytes + 1023) & ~1023u);
+  float *bias_s = reinterpret_cast<float *>(stages + (size_t)p.nstage * p.a_bytes);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(bias_s + 64);
+  uint64_t *full = bars, *empty = bars + p.nstage;
+  uint64_t *accf = bars + 2 * p.nstage, *acce = accf + 2, *bfull = acce + 2;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bfull + 1);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.nstage; ++s) {
+      ptx::mbar_init(full + s, 128);  // the producer threads' cp.async arrivals
+      ptx::mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(accf + b, 1);
+      ptx::mbar_init(acce + b, 8);
+    }
+    ptx::mbar_init(bfull, 1);
+    ptx::fence_mbar_init();
+  }
+  for (int k = threadIdx.x; k < 64; k += blockDim.x)
+    bias_s[k] = (p.bias && k < p.K) ? p.bias[k] : 0.f;
+  if (warp == 4) ptx::tmem_alloc(tslot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int PpQp = p.Pp * p.Qp;
+
+  if (warp < 4) {
+    // ---------------- producers: thread tid owns row m = tid of every stage
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // packed filters (PDL)
+      ptx::mbar_arrive_expect_tx(bfull, p.b_bytes);
+      ptx::bulk_g2s(Bs, p.fp, p.b_bytes, bfull);
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+      for (int i = 0; i < C1P_MT; ++i) {
+        ptx::mbar_wait(empty + stage, phase ^ 1);
+        const uint32_t A = ptx::smem_u32(stages + (size_t)stage * p.a_bytes);
+        const int64_t w = (tile * C1P_MT + i) * 128 + tid;
+        int n = 0, pp = 0, pc = 0;
+        const bool wok = w < p.nwin;
+        if (wok) {
+          n = (int)(w / PpQp);
+          const int rem = (int)(w - (int64_t)n * PpQp);
+          pp = rem / p.Qp;
+          pc = rem - pp * p.Qp;
+        }
+        const float *xn = p.x + (int64_t)n * p.H * p.W;
+        for (int t = 0; t < p.T; ++t) {
+          const int h = 2 * pp + t - p.ph;
+          const bool hok = wok && h >= 0 && h < p.H;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {  // 8-byte chunk j = inputs e = 2j, 2j + 1
+            const int c0 = 2 * pc - p.pw + 2 * j;
+            const bool ok = hok && c0 >= 0 && c0 + 1 < p.W;
+            const uint32_t dst = A + (uint32_t)(t * 4096 + (j >> 1) * 2048 + tid * 16 + (j & 1) * 8);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst),
+                         "l"(ok ? xn + (int64_t)h * p.W + c0 : p.x), "r"(ok ? 8u : 0u)
+                         : "memory");
+          }
+        }
+        ptx::cp_async_mbar_arrive(full + stage);
+        if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------- MMA issuer: D_dr[(ds, k)] = sum_r A_{r+dr} . B_r per M-tile
+    const uint32_t idesc = ptx::make_idesc_tf32(128, p.NN);
+    const uint32_t sB = ptx::smem_u32(Bs), sA0 = ptx::smem_u32(stages);
+    const uint32_t b_tap = (uint32_t)(2 * p.NN * 16);  // bytes per tap r
+    ptx::mbar_wait(bfull, 0);
+    int stage = 0;
+    uint32_t phase = 0, tcount = 0;
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++tcount) {
+      const uint32_t buf = tcount & 1u, bphase = (tcount >> 1) & 1u;
+      ptx::mbar_wait(acce + buf, bphase ^ 1);
+      ptx::tc_fence_after();
+      for (int i = 0; i < C1P_MT; ++i) {
+        ptx::mbar_wait(full + stage, phase);
+        ptx::tc_fence_after();
+        const uint32_t A = sA0 + (uint32_t)stage * p.a_bytes;
+        const uint64_t adesc = ptx::make_desc(A, 2048, 128);
+        const uint64_t bdesc = ptx::make_desc(sB, (uint32_t)p.NN * 16, 128);
+        for (int dr = 0; dr < 2; ++dr) {
+          const uint32_t tm = tmem + buf * 256 + i * 128 + dr * (uint32_t)p.NN;
+          for (int r = 0; r < p.R; ++r) {
+            if (ptx::elect_one())
+              ptx::mma_tf32(tm, adesc + (uint64_t)((r + dr) * 256), bdesc + (uint64_t)(r * (b_tap >> 4)),
+                            idesc, r > 0 ? 1u : 0u);
+            __syncwarp();
+          }
+        }
+        if (ptx::elect_one()) ptx::mma_commit(empty + stage);
+        __syncwarp();
+        if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+      }
+      if (ptx::elect_one()) ptx::mma_commit(accf + buf);
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue: set e = M-tile e of the CTA tile; lane = pooled window
+    const int qd = warp & 3, eset = (warp - 5) >> 2;
+    uint32_t tcount = 0;
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++tcount) {
+      const uint32_t buf = tcount & 1u, bphase = (tcount >> 1) & 1u;
+      ptx::mbar_wait_sleep(accf + buf, bphase);
+      __syncwarp();
+      ptx::tc_fence_after();
+      const int64_t w = (tile * C1P_MT + eset) * 128 + qd * 32 + lane;
+      const bool wok = w < p.nwin;
+      int n = 0, pp = 0, pc = 0;
+      if (wok) {
+        n = (int)(w / PpQp);
+        const int rem = (int)(w - (int64_t)n * PpQp);
+        pp = rem / p.Qp;
+        pc = rem - pp * p.Qp;
+      }
+      const int64_t vbase = p.out_plane > 0
+                                ? (int64_t)n * p.out_Lf + (int64_t)(pp + p.out_off) * p.out_Wf + pc + p.out_off
+                                : (int64_t)n * p.K * PpQp + (int64_t)pp * p.Qp + pc;
+      const int64_t vstride = p.out_plane > 0 ? p.out_plane : PpQp;
+      const int PQ = p.P * p.Q;
+      const int idx_tl = (2 * pp) * p.Q + 2 * pc;
+      const uint32_t tb = tmem + ((uint32_t)(qd * 32) << 16) + buf * 256 + eset * 128;
+      for (int k0 = 0; k0 < p.Kp; k0 += 16) {
+        uint32_t v00[16], v01[16], v10[16], v11[16];
+        ptx::tmem_ld16_issue(tb + (uint32_t)k0, v00);                       // (dr 0, ds 0)
+        ptx::tmem_ld16_issue(tb + (uint32_t)(p.Kp + k0), v01);              // (0, 1)
+        ptx::tmem_ld16_issue(tb + (uint32_t)(p.NN + k0), v10);              // (1, 0)
+        ptx::tmem_ld16_issue(tb + (uint32_t)(p.NN + p.Kp + k0), v11);       // (1, 1)
+        ptx::tmem_ld_wait(v00);  // each wait ties its registers to the completed load
+        ptx::tmem_ld_wait(v01);
+        ptx::tmem_ld_wait(v10);
+        ptx::tmem_ld_wait(v11);
+        uint64_t code = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float b = bias_s[k0 + j];
+          // relu (+0.0 for non-positive, R7) then the strict-'>' scan in r-outer / s-inner
+          // order (R5): non-negative floats compare as unsigned integers
+          const float z0 = __uint_as_float(v00[j]) + b, z1 = __uint_as_float(v01[j]) + b;
+          const float z2 = __uint_as_float(v10[j]) + b, z3 = __uint_as_float(v11[j]) + b;
+          uint32_t best = __float_as_uint(z0 > 0.f ? z0 : 0.f), c = 0;
+          const uint32_t u1 = __float_as_uint(z1 > 0.f ? z1 : 0.f);
+          const uint32_t u2 = __float_as_uint(z2 > 0.f ? z2 : 0.f);
+          const uint32_t u3 = __float_as_uint(z3 > 0.f ? z3 : 0.f);
+          if (u1 > best) { best = u1; c = 1; }
+          if (u2 > best) { best = u2; c = 2; }
+          if (u3 > best) { best = u3; c = 3; }
+          const int k = k0 + j;
+          if (wok && k < p.K) {
+            p.pout[vbase + (int64_t)k * vstride] = __uint_as_float(best);
+            if (p.parg)
+              p.parg[(int64_t)n * p.K * PpQp + (int64_t)k * PpQp + pp * p.Qp + pc] =
+                  k * PQ + idx_tl + (int)(c >> 1) * p.Q + (int)(c & 1);
+          }
+          code |= (uint64_t)(((best != 0u) ? 4u : 0u) | c) << (4 * j);
+        }
+        if (p.pcode && wok) p.pcode[(int64_t)(k0 >> 4) * p.code_plane + w] = code;
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(acce + buf);
+    }
+  }
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+// B_r[e][(ds, k)] = F[k][r][e - ds], packed [r][quad = e/4][NN][4]
+__global__ void conv1_pool_pack_kernel(const float *__restrict__ f, float *__restrict__ fp, int K,
+                                       int R, int S, int Kp) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int NN = 2 * Kp;
+  const int total = R * 2 * NN * 4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int e4 = i & 3, nn = (i >> 2) % NN, q = (i >> 2) / NN % 2, r = (i >> 2) / NN / 2;
+    const int e = q * 4 + e4, ds = nn / Kp, k = nn - ds * Kp, s = e - ds;
+    fp[i] = (k < K && s >= 0 && s < S) ? f[(k * R + r) * S + s] : 0.f;
+  }
+}
+
+struct C1pPlan {
+  C1pParams p;
+  size_t smem;
+  size_t fp_bytes;
+  bool ok;
+};
+
+C1pPlan plan_c1p(const ConvArgs &a, const PoolArgs *pool) {
+  C1pPlan pl{};
+  pl.ok = false;
+  C1pParams &p = pl.p;
+  if (!pool || a.C != 1 || a.sh != 1 || a.sw != 1 || a.K > 32 || a.R > 7 || a.S > 7) return pl;
+  if (pool->R != 2 || pool->S != 2 || pool->sh != 2 || pool->sw != 2 || pool->ph || pool->pw) return pl;
+  if ((a.pw & 1) || (a.W & 1)) return pl;  // 8-byte chunks fully inside or fully padding
+  p.N = a.N; p.H = a.H; p.W = a.W; p.K = a.K; p.R = a.R; p.S = a.S; p.ph = a.ph; p.pw = a.pw;
+  p.P = a.P; p.Q = a.Q; p.Pp = pool->P; p.Qp = pool->Q;
+  p.Kp = a.K <= 16 ? 16 : 32;
+  p.NN = 2 * p.Kp;
+  p.T = a.R + 1;
+  p.nwin = (int64_t)a.N * p.Pp * p.Qp;
+  p.ntiles = ceil_div(p.nwin, 128 * C1P_MT);
+  p.a_bytes = (uint32_t)(p.T * 4096);
+  p.b_bytes = (uint32_t)(a.R * 2 * p.NN * 16);
+  const size_t fixed = ((p.b_bytes + 1023) & ~1023u) + 64 * 4 + 8 * 24 + 64;
+  p.nstage = (int)std::min<size_t>(8, (225 * 1024 - fixed) / p.a_bytes);
+  if (p.nstage < 2) return pl;
+  pl.smem = fixed + (size_t)p.nstage * p.a_bytes + 1024;
+  pl.fp_bytes = align_up(p.b_bytes, 256);
+  pl.ok = true;
+  return pl;
+}
+
+}  // namespace
+
+bool conv1_pool_supported(const ConvArgs &a, const PoolArgs *pool) {
+  return device_cc_major() == 10 && plan_c1p(a, pool).ok && getenv("SYSML_NO_C1P") == nullptr;
+}
+
+size_t conv1_pool_ws(const ConvArgs &a, const PoolArgs *pool) {
+  const C1pPlan pl = plan_c1p(a, pool);
+  return pl.ok ? pl.fp_bytes : 0;
+}
+
+sysml_status conv1_pool(const ConvArgs &a, const PoolArgs *pool, const float *x, const float *f,
+                        const float *bias, float *pout, int32_t *parg, void *ws, cudaStream_t st,
+                        const TcSpfIO *io) {
+  C1pPlan pl = plan_c1p(a, pool);
+  if (!pl.ok) {
+    set_error("conv1+pool (pool-in-N) kernel: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  if ((uintptr_t)x & 7) {
+    set_error("conv1+pool kernel: input must be 8-byte aligned");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  C1pParams p = pl.p;
+  p.x = x;
+  p.fp = reinterpret_cast<const float *>(ws);
+  p.bias = bias;
+  p.pout = pout;
+  p.parg = parg;
+  if (io) {
+    p.out_plane = io->out_plane;
+    p.out_Wf = io->out_Wf;
+    p.out_Lf = io->out_Lf;
+    p.out_off = io->out_off;
+    p.pcode = io->code;
+    p.code_plane = io->code_plane;
+  }
+  conv1_pool_pack_kernel<<<8, 256, 0, st>>>(f, reinterpret_cast<float *>(ws), a.K, a.R, a.S, p.Kp);
+  SYSML_LAUNCH_CHECK();
+  static int attr = 0;
+  if ((int)pl.smem > attr) {
+    SYSML_CUDA(cudaFuncSetAttribute(conv1_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)pl.smem));
+    attr = (int)pl.smem;
+  }
+  const int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(C1P_THREADS);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SYSML_CUDA(cudaLaunchKernelEx(&cfg, conv1_pool_kernel, p));
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
+}
+
+}  // namespace sysml

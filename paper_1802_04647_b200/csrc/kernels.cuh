@@ -81,6 +81,12 @@ bool tc_wgrad_1x1_supported(const ConvArgs &a);
 size_t tc_wgrad_1x1_ws(const ConvArgs &a);
 sysml_status tc_wgrad_1x1(const ConvArgs &a, const float *x, const float *dy, float *df,
                           float *db, void *ws, cudaStream_t st);
+// fused conv(C = 1) + bias + relu + 2x2/2 pool with the window in N (conv1_pool.cu)
+bool conv1_pool_supported(const ConvArgs &a, const PoolArgs *pool);
+size_t conv1_pool_ws(const ConvArgs &a, const PoolArgs *pool);
+sysml_status conv1_pool(const ConvArgs &a, const PoolArgs *pool, const float *x, const float *f,
+                        const float *bias, float *pout, int32_t *parg, void *ws, cudaStream_t st,
+                        const TcSpfIO *io = nullptr);
 bool tc_fwd_supported(const ConvArgs &a, const PoolArgs *pool);
 // single-channel convs (C == 1, S <= 8) use the KS operand mode, which also reads CSR input
 bool tc_fwd_ks(const ConvArgs &a);

@@ -450,6 +450,7 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
     if (h->spf) {
       h->spf_plane = (int64_t)max_local_batch * 256;
       need = std::max(need, tc_fwd_ws(a1a));
+      need = std::max(need, conv1_pool_ws(a1a, &pa1));
       need = std::max(need, tc_fwd_ws(a2a));
       need = std::max(need, tc_bwd_data_ws(a2a));
       need = std::max(need, tc_wgrad_spf_ws(sc));
@@ -541,7 +542,11 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
   sysml_input a1in{0, h->a1, {}};
   // F1
   SYSML_TRY(T.begin(0));
-  if (h->spf) {
+  if (h->spf && !x->is_csr && conv1_pool_supported(ca1, &pa1)) {
+    // dense: pooling window in the MMA N dimension, lane-local pool epilogue
+    SYSML_TRY(conv1_pool(ca1, &pa1, x->dense, params + OFF_F1, params + OFF_B1, h->a1s, nullptr, h->ws,
+                         st, &a1_io));
+  } else if (h->spf) {
     // dense or CSR (scattered straight into the KS operand): pooled a1 lands in SPF
     SYSML_TRY(tc_conv_fwd_spf(ca1, a1_io, x->is_csr ? nullptr : x->dense, params + OFF_F1,
                               params + OFF_B1, nullptr, &pa1, h->a1s, nullptr, h->ws, st,
