@@ -175,6 +175,30 @@ def test_fused_conv_bias_relu_maxpool_dyadic_bit_exact(S, math):
     assert np.array_equal(host(out).astype(np.float64), oref)
 
 
+# (N, K, H, W, R, pad): C = 1 conv + pool with the 2x2 window in the MMA N dimension
+# (conv1_pool.cu): LeNet conv1, a 3x3 kernel with K <= 16, a tall 7x7 kernel, ragged
+# window count (N*Pp*Qp not a multiple of 256)
+C1P_SHAPES = [(7, 32, 28, 28, 5, 2), (3, 12, 10, 14, 3, 0), (2, 20, 16, 12, 7, 2)]
+
+
+@pytest.mark.parametrize("shape", C1P_SHAPES)
+def test_conv1_pool_dyadic_bit_exact(S, shape):
+    N, K, H, W, R, pd = shape
+    x = synth.dyadic((N, H * W), 0, 4, 4, seed=(410,))
+    x[x < 0.5] = 0.0  # zero-heavy: window ties at 0 exercise the first-occurrence rule
+    f = synth.dyadic((K, R * R), -3, 3, 16, seed=(411,))
+    b = synth.dyadic((K,), -3, 3, 16, seed=(412,))
+    P = H + 2 * pd - R + 1
+    Q = W + 2 * pd - R + 1
+    cd = S.conv_desc(N, 1, H, W, K, R, R, 1, pd, "tf32")
+    pdsc = S.pool_desc(N, K, P, Q, 2, 2, 2, 0, True)
+    out, arg = S.sysml_conv2d_bias_relu_maxpool(dev(x), dev(f), dev(b), cd, pdsc)
+    z = oracle.conv2d_fwd(x, f, N, 1, H, W, K, R, R, (1, 1), (pd, pd), bias=b)
+    oref, aref = oracle.relu_maxpool(z, N, K, P, Q, 2, 2, (2, 2), (0, 0), relu=True)
+    assert np.array_equal(host(arg), aref)
+    assert np.array_equal(host(out).astype(np.float64), oref)
+
+
 @pytest.mark.parametrize("math", ["fp32", "tf32"])
 def test_fused_conv_pool_continuous_valid_argmax(S, math):
     N = 5
