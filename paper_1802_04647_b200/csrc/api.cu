@@ -38,7 +38,7 @@ sysml_status conv_fwd_ws(const sysml_conv_desc &cd, const sysml_pool_desc *pd, i
     pa = pool_args(pg, 1);
     pap = &pa;
   }
-  if (!is_csr && use_tc && pap && conv1_pool_supported(a, pap)) {
+  if (use_tc && pap && conv1_pool_supported(a, pap)) {
     b += conv1_pool_ws(a, pap);  // C = 1 conv + pool: window in the MMA N dimension
   } else if (is_csr && use_tc && tc_fwd_ks(a) && tc_fwd_supported(a, pap)) {
     b += tc_fwd_ws(a);  // CSR rows scattered straight into the tcgen05 operand
@@ -96,9 +96,10 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
   WsCarve wc(ws, ws_bytes);
   const bool use_tc = cd.math == SYSML_MATH_TF32 && tc_fwd_supported(a, pap);
   const float *xd = x.dense;
-  if (!x.is_csr && cd.math == SYSML_MATH_TF32 && pap && conv1_pool_supported(a, pap)) {
+  if (cd.math == SYSML_MATH_TF32 && pap && conv1_pool_supported(a, pap)) {
     void *tws = wc.take<char>(conv1_pool_ws(a, pap));
-    return conv1_pool(a, pap, x.dense, f, bias, pout, parg, tws, st);
+    return conv1_pool(a, pap, x.is_csr ? nullptr : x.dense, f, bias, pout, parg, tws, st, nullptr,
+                      x.is_csr ? &x.csr : nullptr);
   }
   if (x.is_csr && use_tc && tc_fwd_ks(a)) {
     void *tws = wc.take<char>(tc_fwd_ws(a));

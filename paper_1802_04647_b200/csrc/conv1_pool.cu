@@ -45,7 +45,13 @@ struct C1pParams {
   int out_Wf, out_Lf, out_off;
   int nstage;
   uint32_t a_bytes, b_bytes;  // per stage (T blocks of 128 rows x 32 B), B total
+  int is_csr;                 // CSR input: non-zeros scattered straight into the A_t rows
+  sysml_csr csr;
 };
+
+__device__ __forceinline__ void st_shared_v4c1(uint32_t addr) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "f"(0.f) : "memory");
+}
 
 __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -59,7 +65,7 @@ __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pPar
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nstage; ++s) {
-      ptx::mbar_init(full + s, 128);  // the producer threads' cp.async arrivals
+      ptx::mbar_init(full + s, p.is_csr ? 1 : 128);  // cp.async arrivals / the filling warp
       ptx::mbar_init(empty + s, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -78,7 +84,84 @@ __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pPar
   const uint32_t tmem = *tslot;
   const int PpQp = p.Pp * p.Qp;
 
-  if (warp < 4) {
+  if (warp < 4 && p.is_csr) {
+    // ---------------- CSR producers: warp w fills every 4th M-tile alone -- zero the T
+    // row blocks, then each non-zero (h, w, v) of the overlapping images adds v to the
+    // (window, t, e) slots with 2pp + t = h + ph and 2pc + e = w + pw (work ~ nnz,
+    // P:168-170; duplicates summed, reading R15)
+    if (threadIdx.x == 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      ptx::mbar_arrive_expect_tx(bfull, p.b_bytes);
+      ptx::bulk_g2s(Bs, p.fp, p.b_bytes, bfull);
+    }
+    const int HW = p.H * p.W;
+    const float invW = 1.0f / (float)p.W;
+    int lm = warp;  // CTA-local M-tile counter of this warp
+    for (int64_t it = 0;; ++it) {
+      const int64_t tile = blockIdx.x + it * gridDim.x;
+      if (tile >= p.ntiles) break;
+      for (int i = 0; i < C1P_MT; ++i) {
+        const int mine = (int)(it * C1P_MT + i);
+        if ((mine & 3) != warp) continue;
+        const int stage = mine % p.nstage;
+        const uint32_t phase = (uint32_t)((mine / p.nstage) & 1);
+        ptx::mbar_wait(empty + stage, phase ^ 1);
+        uint8_t *As = stages + (size_t)stage * p.a_bytes;
+        const uint32_t A = ptx::smem_u32(As);
+        for (int q = lane; q < (int)(p.a_bytes / 16); q += 32) st_shared_v4c1(A + q * 16);
+        __syncwarp();
+        const int64_t w0 = (tile * C1P_MT + i) * 128;
+        if (w0 < p.nwin) {
+          const int n_lo = (int)(w0 / PpQp);
+          const int n_hi = (int)min((int64_t)p.N - 1, (w0 + 127) / PpQp);
+          float *Af = reinterpret_cast<float *>(As);
+          for (int n = n_lo; n <= n_hi; ++n) {
+            const int j0 = __ldg(p.csr.row_ptr + n), j1 = __ldg(p.csr.row_ptr + n + 1);
+            for (int base = j0; base < j1; base += 8 * 32) {
+              int cols[8];
+              float vals[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {  // the batch's loads in flight together
+                const int jj = base + lane + 32 * u;
+                cols[u] = jj < j1 ? __ldg(p.csr.col_idx + jj) : -1;
+                vals[u] = jj < j1 ? __ldg(p.csr.val + jj) : 0.f;
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int col = cols[u];
+                if (col < 0 || col >= HW) continue;
+                const float v = vals[u];
+                const int h = __float2int_rz(((float)col + 0.5f) * invW);
+                const int wc = col - h * p.W;
+                const int hf = h + p.ph, wf = wc + p.pw;
+                // window of slot (t, e): pp = (hf - t)/2, pc = (wf - e)/2 with t = hf & 1 + 2a,
+                // e = wf & 1 + 2b -> row offset m(a, b) = m00 - a*Qp - b
+                const int t0 = hf & 1, e0 = wf & 1;
+                const int pp0 = (hf - t0) >> 1, pc0 = (wf - e0) >> 1;
+                const int m00 = n * PpQp + pp0 * p.Qp + pc0 - (int)w0;
+#pragma unroll
+                for (int a_ = 0; a_ < 4; ++a_) {
+                  const int t = t0 + 2 * a_, pp = pp0 - a_;
+                  if (t >= p.T || pp < 0 || pp >= p.Pp) continue;
+#pragma unroll
+                  for (int b_ = 0; b_ < 4; ++b_) {
+                    const int e = e0 + 2 * b_, pc = pc0 - b_;
+                    const int m = m00 - a_ * p.Qp - b_;
+                    if (pc >= 0 && pc < p.Qp && m >= 0 && m < 128)
+                      atomicAdd(Af + t * 1024 + (e >> 2) * 512 + m * 4 + (e & 3), v);
+                  }
+                }
+              }
+            }
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(full + stage);
+      }
+    }
+    (void)lm;
+  } else if (warp < 4) {
     // ---------------- producers: thread tid owns row m = tid of every stage
     const int tid = threadIdx.x;
     if (tid == 0) {
@@ -284,18 +367,22 @@ size_t conv1_pool_ws(const ConvArgs &a, const PoolArgs *pool) {
 
 sysml_status conv1_pool(const ConvArgs &a, const PoolArgs *pool, const float *x, const float *f,
                         const float *bias, float *pout, int32_t *parg, void *ws, cudaStream_t st,
-                        const TcSpfIO *io) {
+                        const TcSpfIO *io, const sysml_csr *csr) {
   C1pPlan pl = plan_c1p(a, pool);
   if (!pl.ok) {
     set_error("conv1+pool (pool-in-N) kernel: unsupported shape");
     return SYSML_ERR_UNSUPPORTED;
   }
-  if ((uintptr_t)x & 7) {
+  if (!csr && ((uintptr_t)x & 7)) {
     set_error("conv1+pool kernel: input must be 8-byte aligned");
     return SYSML_ERR_UNSUPPORTED;
   }
   C1pParams p = pl.p;
   p.x = x;
+  if (csr) {
+    p.is_csr = 1;
+    p.csr = *csr;
+  }
   p.fp = reinterpret_cast<const float *>(ws);
   p.bias = bias;
   p.pout = pout;

@@ -86,7 +86,7 @@ bool conv1_pool_supported(const ConvArgs &a, const PoolArgs *pool);
 size_t conv1_pool_ws(const ConvArgs &a, const PoolArgs *pool);
 sysml_status conv1_pool(const ConvArgs &a, const PoolArgs *pool, const float *x, const float *f,
                         const float *bias, float *pout, int32_t *parg, void *ws, cudaStream_t st,
-                        const TcSpfIO *io = nullptr);
+                        const TcSpfIO *io = nullptr, const sysml_csr *csr = nullptr);
 bool tc_fwd_supported(const ConvArgs &a, const PoolArgs *pool);
 // single-channel convs (C == 1, S <= 8) use the KS operand mode, which also reads CSR input
 bool tc_fwd_ks(const ConvArgs &a);

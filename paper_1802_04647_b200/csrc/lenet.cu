@@ -542,10 +542,10 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
   sysml_input a1in{0, h->a1, {}};
   // F1
   SYSML_TRY(T.begin(0));
-  if (h->spf && !x->is_csr && conv1_pool_supported(ca1, &pa1)) {
-    // dense: pooling window in the MMA N dimension, lane-local pool epilogue
-    SYSML_TRY(conv1_pool(ca1, &pa1, x->dense, params + OFF_F1, params + OFF_B1, h->a1s, nullptr, h->ws,
-                         st, &a1_io));
+  if (h->spf && conv1_pool_supported(ca1, &pa1)) {
+    // dense or CSR: pooling window in the MMA N dimension, lane-local pool epilogue
+    SYSML_TRY(conv1_pool(ca1, &pa1, x->is_csr ? nullptr : x->dense, params + OFF_F1, params + OFF_B1,
+                         h->a1s, nullptr, h->ws, st, &a1_io, x->is_csr ? &x->csr : nullptr));
   } else if (h->spf) {
     // dense or CSR (scattered straight into the KS operand): pooled a1 lands in SPF
     SYSML_TRY(tc_conv_fwd_spf(ca1, a1_io, x->is_csr ? nullptr : x->dense, params + OFF_F1,
