@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
     // db rows: Kc <= 64 -> two threads per row (64-byte halves); Kc = 128 -> one per row
     const bool dsplit = p.Kc <= 64;
     const int drow = dsplit ? et >> 1 : et, dhalf = dsplit ? et & 1 : 0, dq = dsplit ? 4 : 8;
-    // shift tasks (channel c, 16-byte chunk q) of this thread: t = et, et + 128 (C*8 <= 256).
+    // shift tasks (channel c, 16-byte chunk q) of this thread: t = et + 128u (Ct*8 <= 384).
     // Source: the TMA-loaded s = 0 tile of atom bi (chunk q) and, for q = 7, chunk 0 of
     // atom bi + 1 (next ring slot); both rows are 128-byte swizzled (chunk q at q ^ (c & 7)).
     const int ntask = p.Ct * 8;
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         const uint8_t *B0 = Bring + slot * b_slot, *B1 = Bring + slot1 * b_slot;
         const uint32_t Bs = sB + slot * b_slot;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 3; ++u) {
           const int t = et + u * 128;
           if (t >= ntask) continue;
           const int c = t >> 3, q = t & 7;
@@ -413,15 +413,16 @@ W2Plan plan_w2(const SpfConv &sc) {
   p.nkt = (int)ceil_div(sc.K, p.Kc);
   p.RG = (sc.R + p.copies - 1) / p.copies;
   p.shift = p.copies * sc.Wf;
-  // channel tile: Ct <= 32 (helper tasks), S*Ct % 16 == 0, RG*S*Ct TMEM columns <= 512
+  // channel tile: Ct <= 48 (3 helper tasks per thread), S*Ct % 16 == 0, RG*S*Ct TMEM
+  // columns <= 512; the widest tile wins (the last one may be ragged: TMA zero-fills)
   p.Ct = 0;
-  for (int ct = std::min(32, sc.C); ct >= 8; ct -= 8)
-    if (sc.C % ct == 0 && (sc.S * ct) % 16 == 0 && sc.S * ct <= 256 && p.RG * sc.S * ct <= 512) {
+  for (int ct = std::min(48, (sc.C + 7) / 8 * 8); ct >= 8; ct -= 8)
+    if ((sc.S * ct) % 16 == 0 && sc.S * ct <= 256 && p.RG * sc.S * ct <= 512) {
       p.Ct = ct;
       break;
     }
   if (!p.Ct || p.RG > 4) return pl;
-  p.nct = sc.C / p.Ct;
+  p.nct = (int)ceil_div(sc.C, p.Ct);
   p.N = sc.S * p.Ct;
   p.L = (24 + (p.RG - 1) * p.shift) / W2_ATOM;
   if (p.L > 3) return pl;  // B descriptors of atoms ai .. ai + 3
