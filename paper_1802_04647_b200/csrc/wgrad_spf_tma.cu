@@ -548,30 +548,44 @@ sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float
 namespace sysml {
 namespace {
 
-// one float4 of a frame row per thread (Wf % 4 == 0); index decoding per float4
+// four float4s of frame rows per thread iteration (Wf % 4 == 0): independent loads in
+// flight; index decoding per float4
 __global__ void nchw_to_frame_kernel(const float *__restrict__ src, float *__restrict__ dst, int N,
                                      int C, int H, int W, int Hs, int Wf, int oh, int ow,
                                      int64_t plane) {
   const int q4 = Wf >> 2;
   const int NHs = N * Hs;
   const int64_t total = (int64_t)C * NHs * q4;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = t / q4;
-    const int w0 = (int)(t - row * q4) * 4 - ow;
-    const int c = (int)(row / NHs);
-    const int rem = (int)(row - (int64_t)c * NHs);
-    const int n = rem / Hs, hh = rem - n * Hs;
-    const int h = hh - oh;
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (h >= 0 && h < H) {
-      const float *srow = src + (((int64_t)n * C + c) * H + h) * W;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 < total; t0 += 4 * stride) {
+    float v[4][4];
+    int64_t dsti[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (w0 + e >= 0 && w0 + e < W) v[e] = __ldg(srow + w0 + e);
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = t0 + u * stride;
+      dsti[u] = -1;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[u][e] = 0.f;
+      if (t < total) {
+        const int64_t row = t / q4;
+        const int w0 = (int)(t - row * q4) * 4 - ow;
+        const int c = (int)(row / NHs);
+        const int rem = (int)(row - (int64_t)c * NHs);
+        const int n = rem / Hs, hh = rem - n * Hs;
+        const int h = hh - oh;
+        dsti[u] = (int64_t)c * plane + (int64_t)rem * Wf + (t - row * q4) * 4;
+        if (h >= 0 && h < H) {
+          const float *srow = src + (((int64_t)n * C + c) * H + h) * W;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (w0 + e >= 0 && w0 + e < W) v[u][e] = __ldg(srow + w0 + e);
+        }
+      }
     }
-    reinterpret_cast<float4 *>(dst + (int64_t)c * plane + (int64_t)rem * Wf)[t - row * q4] =
-        make_float4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (dsti[u] >= 0)
+        *reinterpret_cast<float4 *>(dst + dsti[u]) = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
   }
 }
 
