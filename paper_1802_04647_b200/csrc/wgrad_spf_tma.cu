@@ -331,7 +331,13 @@ __global__ void w2_reduce_kernel(const W2Params p, float *__restrict__ df, float
     const int64_t off = ((int64_t)rb * 128 + j * p.Kc + kk) * p.N + s * p.Ct + cc;
     const float *src = p.part + ((int64_t)(kt * p.nct + ct) * p.splits) * cta_stride + off;
     float acc = 0.f;
-    for (int sp = 0; sp < p.splits; ++sp) acc += __ldg(src + sp * cta_stride);
+    for (int sp0 = 0; sp0 < p.splits; sp0 += 8) {  // 8 loads in flight, summed in split order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = sp0 + u < p.splits ? __ldg(src + (sp0 + u) * cta_stride) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
     df[i] = acc;
   }
   if (db)
