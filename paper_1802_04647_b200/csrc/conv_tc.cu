@@ -930,7 +930,8 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     SYSML_LAUNCH_CHECK();
   } else {
     const int RS = p.R * p.S;
-    if (RS <= PACK_MAX_RS && p.NFpad % PACK_JB == 0) {
+    const int slab_blocks = p.nft * p.nchunk * (p.NFpad / PACK_JB);
+    if (RS <= PACK_MAX_RS && p.NFpad % PACK_JB == 0 && slab_blocks >= sm_count()) {
       tc_pack_filters_kernel<<<p.nft * p.nchunk * (p.NFpad / PACK_JB), 256, 0, st>>>(
           f, fp, p.K, f_cin, RS, p.NFpad, p.nft, p.nchunk, flip);
     } else {

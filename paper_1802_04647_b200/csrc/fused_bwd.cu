@@ -297,7 +297,9 @@ __global__ void fused_b1_reduce_kernel(const float *__restrict__ part, int parts
 }
 
 int fused_b1_ctas(int N) {
-  int ctas = 4 * sm_count();
+  // about 8 images per CTA at least (keeps the partial count, and the reduce, small at
+  // small batches), at most 4 CTAs per SM
+  int ctas = std::min(4 * sm_count(), (N + 7) / 8);
   if (ctas > N) ctas = N;
   return ctas < 1 ? 1 : ctas;
 }

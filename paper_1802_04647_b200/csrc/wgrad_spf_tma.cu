@@ -349,53 +349,43 @@ __global__ void w2_reduce_kernel(const W2Params p, float *__restrict__ df, float
     }
 }
 
-// many splits: block (32, 8): lane x owns output i, row y sums the y-th contiguous eighth
-// of the splits in order; the 8 row sums are added in row order (fixed association)
+// many splits: thread per partial offset o (the CTA-tile partial layout), so the reads of
+// one split are contiguous across threads; splits are summed in order, 8 loads in flight,
+// and the sum is scattered to dF[k][c][r][s] (valid rows / columns only)
 __global__ void w2_reduce_wide_kernel(const W2Params p, float *__restrict__ df, float *__restrict__ db,
                                       const float *__restrict__ dbsrc, int dbcount) {
-  __shared__ float red[8][33];
-  __shared__ int64_t offs[32];
-  const int RS = p.R * p.S;
-  const int64_t total = (int64_t)p.K * p.C * RS;
-  const int64_t cta_stride = (int64_t)p.RG * 128 * p.N;
-  const int x = threadIdx.x, y = threadIdx.y;
-  const int z0 = y * p.splits / 8, z1 = (y + 1) * p.splits / 8;
-  for (int64_t base = (int64_t)blockIdx.x * 32; base < total + p.K; base += (int64_t)gridDim.x * 32) {
-    const int64_t i = base + x;
-    if (y == 0) {  // partial-array offset of output i, decoded once per block
-      int64_t o = -1;
-      if (i < total) {
-        const int k = (int)(i / ((int64_t)p.C * RS));
-        const int rem = (int)(i - (int64_t)k * p.C * RS);
-        const int c = rem / RS, t = rem - c * RS, r = t / p.S, s = t - r * p.S;
-        const int rb = r / p.copies, j = r - rb * p.copies;
-        const int kt = k / p.Kc, kk = k - kt * p.Kc, ct = c / p.Ct, cc = c - ct * p.Ct;
-        o = ((int64_t)(kt * p.nct + ct) * p.splits) * cta_stride +
-            ((int64_t)rb * 128 + j * p.Kc + kk) * p.N + s * p.Ct + cc;
-      }
-      offs[x] = o;
-    }
-    __syncthreads();
+  const int64_t per_cta = (int64_t)p.RG * 128 * p.N;
+  const int64_t total = (int64_t)p.nkt * p.nct * per_cta;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int tile = (int)(o / per_cta);
+    const int64_t w = o - (int64_t)tile * per_cta;
+    const int rb = (int)(w / (128 * p.N));
+    const int rem = (int)(w - (int64_t)rb * 128 * p.N);
+    const int row = rem / p.N, col = rem - row * p.N;
+    const int j = row / p.Kc, kk = row - j * p.Kc;
+    const int s = col / p.Ct, cc = col - s * p.Ct;
+    const int kt = tile / p.nct, ct = tile - kt * p.nct;
+    const int k = kt * p.Kc + kk, c = ct * p.Ct + cc, r = rb * p.copies + j;
+    if (kk >= p.Kc || k >= p.K || c >= p.C || r >= p.R || j >= p.copies) continue;
+    const float *src = p.part + (int64_t)tile * p.splits * per_cta + w;
     float acc = 0.f;
-    if (i < total) {
-      const float *src = p.part + offs[x];
-      for (int sp = z0; sp < z1; ++sp) acc += __ldg(src + sp * cta_stride);
-    } else if (i < total + p.K && db) {
-      const int k = (int)(i - total);
-      const int d0 = y * dbcount / 8, d1 = (y + 1) * dbcount / 8;
-      for (int sp = d0; sp < d1; ++sp) acc += __ldg(dbsrc + (int64_t)sp * p.K + k);
-    }
-    red[y][x] = acc;
-    __syncthreads();
-    if (y == 0) {
-      float sum = 0.f;
+    for (int sp0 = 0; sp0 < p.splits; sp0 += 8) {
+      float v[8];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) sum += red[g][x];
-      if (i < total) df[i] = sum;
-      else if (i < total + p.K && db) db[i - total] = sum;
+      for (int u = 0; u < 8; ++u) v[u] = sp0 + u < p.splits ? __ldg(src + (int64_t)(sp0 + u) * per_cta) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
     }
-    __syncthreads();
+    df[(((int64_t)k * p.C + c) * p.R + r) * p.S + s] = acc;
   }
+  if (db)
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < p.K;
+         k += (int64_t)gridDim.x * blockDim.x) {
+      float acc = 0.f;
+      for (int sp = 0; sp < dbcount; ++sp) acc += __ldg(dbsrc + (int64_t)sp * p.K + k);
+      db[k] = acc;
+    }
 }
 
 struct W2Plan {
@@ -527,8 +517,9 @@ sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float
   }
   const int64_t total = (int64_t)p.K * p.C * p.R * p.S;
   if (p.splits >= 32)
-    w2_reduce_wide_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total + p.K, 32), 16 * sm_count()),
-                            dim3(32, 8), 0, st>>>(
+    w2_reduce_wide_kernel<<<(unsigned)std::min<int64_t>(
+                                ceil_div((int64_t)p.nkt * p.nct * p.RG * 128 * p.N, 256), 16 * sm_count()),
+                            256, 0, st>>>(
         p, df, db_src ? db : (p.dbpart ? db : nullptr), db_src ? db_src : p.dbpart,
         db_src ? db_count : p.splits);
   else
