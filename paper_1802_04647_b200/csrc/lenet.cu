@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
 
 namespace sysml {
 sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, const float *f,
@@ -45,49 +46,116 @@ constexpr int OFF_F1 = 0, OFF_B1 = OFF_F1 + 32 * 25, OFF_F2 = OFF_B1 + 32,
               NUM_PARAMS = OFF_B3 + 10;
 constexpr int D3 = 3136, NCLS = 10;
 
-// F3: one warp per sample: logits, max-shifted softmax, ds = (p - onehot)/Ng,
-// per-sample loss -log(max(p_y, 1e-15))/Ng.
-__global__ void affine_softmax_ce_kernel(int n, float inv_ng, const float *__restrict__ a2,
-                                         const float *__restrict__ W3, const float *__restrict__ b3,
-                                         const int32_t *__restrict__ labels,
-                                         float *__restrict__ ds, float *__restrict__ loss_n) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= n) return;
-  const float4 *row = reinterpret_cast<const float4 *>(a2 + (int64_t)warp * D3);
-  float acc[NCLS];
-#pragma unroll
-  for (int j = 0; j < NCLS; ++j) acc[j] = 0.f;
-  for (int d4 = lane; d4 < D3 / 4; d4 += 32) {
-    const float4 v = __ldg(row + d4);
-#pragma unroll
-    for (int j = 0; j < NCLS; ++j) {
-      const float4 w = __ldg(reinterpret_cast<const float4 *>(W3 + j * D3) + d4);
-      acc[j] = fmaf(v.x, w.x, fmaf(v.y, w.y, fmaf(v.z, w.z, fmaf(v.w, w.w, acc[j]))));
-    }
+// F3, persistent: each CTA stages W3 (125 KB) in shared memory once (1-D bulk copies), then
+// every warp takes samples two at a time -- lanes stride the 784 float4 columns, 8
+// iterations of a2 loads in flight, W3 from smem serving both samples.  The 2 x 10 partial
+// logits are summed over the warp by a halving reduce-scatter (masks 16, 8) and xor sums
+// (4, 2, 1) -- a fixed order; one lane per sample does the softmax/CE.
+constexpr int F3_THREADS = 512, F3_WARPS = F3_THREADS / 32;
+constexpr size_t F3_SMEM = (size_t)NCLS * D3 * 4 + (size_t)F3_WARPS * 2 * NCLS * 4;
+__global__ void __launch_bounds__(F3_THREADS) affine_softmax_ce_smem_kernel(
+    int n, float inv_ng, const float *__restrict__ a2, const float *__restrict__ W3,
+    const float *__restrict__ b3, const int32_t *__restrict__ labels, float *__restrict__ ds,
+    float *__restrict__ loss_n) {
+  extern __shared__ float4 f3s[];
+  float4 *w3s = f3s;  // [NCLS][D3/4]
+  float *lg = reinterpret_cast<float *>(f3s + NCLS * D3 / 4);
+  __shared__ __align__(8) uint64_t w3bar;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    ptx::mbar_init(&w3bar, 1);
+    ptx::fence_mbar_init();
+    ptx::mbar_arrive_expect_tx(&w3bar, NCLS * D3 * 4);
+#pragma unroll 1
+    for (int j = 0; j < NCLS; ++j) ptx::bulk_g2s(w3s + j * (D3 / 4), W3 + j * D3, D3 * 4, &w3bar);
   }
+  __syncthreads();
+  ptx::mbar_wait(&w3bar, 0);
+  float *mylg = lg + warp * 2 * NCLS;
+  const int npair = (n + 1) >> 1;
+  for (int pr = blockIdx.x * F3_WARPS + warp; pr < npair; pr += gridDim.x * F3_WARPS) {
+    const int i0 = 2 * pr;
+    const bool two = i0 + 1 < n;
+    const float4 *r0 = reinterpret_cast<const float4 *>(a2 + (int64_t)i0 * D3);
+    const float4 *r1 = two ? r0 + D3 / 4 : r0;
+    float v[2 * NCLS];
 #pragma unroll
-  for (int j = 0; j < NCLS; ++j)
+    for (int i = 0; i < 2 * NCLS; ++i) v[i] = 0.f;
+    // 8 iterations of loads in flight per batch (784 = 3 x 256 + 16 float4 columns)
+#pragma unroll 1
+    for (int base = 0; base < D3 / 4; base += 256) {
+      float4 xa[8], xb[8];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-  if (lane == 0) {
-    float m = -INFINITY;
+      for (int u = 0; u < 8; ++u) {
+        const int d4 = base + u * 32 + lane;
+        if (d4 < D3 / 4) {
+          xa[u] = __ldcs(r0 + d4);
+          xb[u] = __ldcs(r1 + d4);
+        } else {
+          xa[u] = xb[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
 #pragma unroll
-    for (int j = 0; j < NCLS; ++j) {
-      acc[j] += __ldg(b3 + j);
-      m = fmaxf(m, acc[j]);
+      for (int u = 0; u < 8; ++u) {
+        const int d4 = base + u * 32 + lane;
+        if (base + u * 32 < D3 / 4) {
+          const float4 x0 = xa[u], x1 = xb[u];
+#pragma unroll
+          for (int j = 0; j < NCLS; ++j) {
+            const float4 w = w3s[j * (D3 / 4) + min(d4, D3 / 4 - 1)];
+            v[j] = fmaf(x0.x, w.x, fmaf(x0.y, w.y, fmaf(x0.z, w.z, fmaf(x0.w, w.w, v[j]))));
+            v[NCLS + j] =
+                fmaf(x1.x, w.x, fmaf(x1.y, w.y, fmaf(x1.z, w.z, fmaf(x1.w, w.w, v[NCLS + j]))));
+          }
+        }
+      }
     }
-    float den = 0.f;
 #pragma unroll
-    for (int j = 0; j < NCLS; ++j) den += expf(acc[j] - m);
-    const int y = labels[warp];
-    float lossv = 0.f;
-#pragma unroll
-    for (int j = 0; j < NCLS; ++j) {
-      const float p = expf(acc[j] - m) / den;
-      ds[warp * NCLS + j] = (p - (j == y ? 1.f : 0.f)) * inv_ng;
-      if (j == y) lossv = -logf(fmaxf(p, 1e-15f)) * inv_ng;
+    for (int i = 0; i < NCLS; ++i) {
+      const bool hi = lane & 16;
+      const float r = __shfl_xor_sync(0xffffffffu, hi ? v[i] : v[i + NCLS], 16);
+      v[i] = (hi ? v[i + NCLS] : v[i]) + r;
     }
-    loss_n[warp] = lossv;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const bool hi = lane & 8;
+      const float r = __shfl_xor_sync(0xffffffffu, hi ? v[i] : v[i + 5], 8);
+      v[i] = (hi ? v[i + 5] : v[i]) + r;
+    }
+#pragma unroll
+    for (int m = 4; m > 0; m >>= 1)
+#pragma unroll
+      for (int i = 0; i < 5; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], m);
+    if ((lane & 7) == 0) {
+      const int base = ((lane & 16) ? NCLS : 0) + ((lane & 8) ? 5 : 0);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) mylg[base + i] = v[i];
+    }
+    __syncwarp();
+    if (lane < (two ? 2 : 1)) {
+      const float *a = mylg + lane * NCLS;
+      float z[NCLS];
+      float m = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < NCLS; ++j) {
+        z[j] = a[j] + __ldg(b3 + j);
+        m = fmaxf(m, z[j]);
+      }
+      float den = 0.f;
+#pragma unroll
+      for (int j = 0; j < NCLS; ++j) den += expf(z[j] - m);
+      const int img = i0 + lane;
+      const int y = labels[img];
+      float lossv = 0.f;
+#pragma unroll
+      for (int j = 0; j < NCLS; ++j) {
+        const float pj = expf(z[j] - m) / den;
+        ds[img * NCLS + j] = (pj - (j == y ? 1.f : 0.f)) * inv_ng;
+        if (j == y) lossv = -logf(fmaxf(pj, 1e-15f)) * inv_ng;
+      }
+      loss_n[img] = lossv;
+    }
+    __syncwarp();
   }
 }
 
@@ -575,8 +643,17 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
   SYSML_TRY(T.end());
   // F3
   SYSML_TRY(T.begin(2));
-  affine_softmax_ce_kernel<<<(unsigned)ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(
-      n, inv_ng, h->a2, params + OFF_W3, params + OFF_B3, labels, h->ds, h->lossn);
+  {
+    static bool attr = false;
+    if (!attr) {
+      SYSML_CUDA(cudaFuncSetAttribute(affine_softmax_ce_smem_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F3_SMEM));
+      attr = true;
+    }
+    const int ctas = (int)std::min<int64_t>(sm_count(), (n + 1) / 2);
+    affine_softmax_ce_smem_kernel<<<(unsigned)ctas, F3_THREADS, F3_SMEM, st>>>(
+        n, inv_ng, h->a2, params + OFF_W3, params + OFF_B3, labels, h->ds, h->lossn);
+  }
   SYSML_LAUNCH_CHECK();
   if (loss_sum) {
     ordered_total_kernel<<<1, 1024, 0, st>>>(h->lossn, n, loss_sum);

@@ -349,42 +349,78 @@ __global__ void w2_reduce_kernel(const W2Params p, float *__restrict__ df, float
     }
 }
 
-// many splits: thread per partial offset o (the CTA-tile partial layout), so the reads of
-// one split are contiguous across threads; splits are summed in order, 8 loads in flight,
-// and the sum is scattered to dF[k][c][r][s] (valid rows / columns only)
-__global__ void w2_reduce_wide_kernel(const W2Params p, float *__restrict__ df, float *__restrict__ db,
-                                      const float *__restrict__ dbsrc, int dbcount) {
-  const int64_t per_cta = (int64_t)p.RG * 128 * p.N;
-  const int64_t total = (int64_t)p.nkt * p.nct * per_cta;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
-       o += (int64_t)gridDim.x * blockDim.x) {
-    const int tile = (int)(o / per_cta);
-    const int64_t w = o - (int64_t)tile * per_cta;
-    const int rb = (int)(w / (128 * p.N));
-    const int rem = (int)(w - (int64_t)rb * 128 * p.N);
-    const int row = rem / p.N, col = rem - row * p.N;
-    const int j = row / p.Kc, kk = row - j * p.Kc;
-    const int s = col / p.Ct, cc = col - s * p.Ct;
-    const int kt = tile / p.nct, ct = tile - kt * p.nct;
-    const int k = kt * p.Kc + kk, c = ct * p.Ct + cc, r = rb * p.copies + j;
-    if (kk >= p.Kc || k >= p.K || c >= p.C || r >= p.R || j >= p.copies) continue;
-    const float *src = p.part + (int64_t)tile * p.splits * per_cta + w;
-    float acc = 0.f;
-    for (int sp0 = 0; sp0 < p.splits; sp0 += 8) {
-      float v[8];
+// many splits: a CTA covers 32 float4 groups of partial offsets (the CTA-tile partial
+// layout, so each split's reads are contiguous) x 8 eighths of the splits; thread (q, g)
+// sums its eighth in split order, 8 float4 loads in flight, then the eight partial sums are
+// added in order and scattered to dF[k][c][r][s] (valid rows / columns only).
+// Fixed order throughout: deterministic.
+constexpr int W2R_GROUPS = 32, W2R_Q = 8;
+__global__ void __launch_bounds__(W2R_GROUPS * W2R_Q) w2_reduce_wide_kernel(
+    const W2Params p, float *__restrict__ df, float *__restrict__ db, const float *__restrict__ dbsrc,
+    int dbcount) {
+  __shared__ float4 red[W2R_Q][W2R_GROUPS];
+  const int64_t per_cta = (int64_t)p.RG * 128 * p.N;  // multiple of 4
+  const int64_t groups = (int64_t)p.nkt * p.nct * per_cta / 4;
+  const int gl = threadIdx.x % W2R_GROUPS, q = threadIdx.x / W2R_GROUPS;
+  const int64_t g = blockIdx.x * (int64_t)W2R_GROUPS + gl;
+  const int sq = (p.splits + W2R_Q - 1) / W2R_Q;
+  const int sp_lo = q * sq, sp_hi = min(p.splits, sp_lo + sq);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int tile = 0;
+  int64_t w = 0;
+  if (g < groups) {
+    tile = (int)(g * 4 / per_cta);
+    w = g * 4 - (int64_t)tile * per_cta;
+    const float4 *src =
+        reinterpret_cast<const float4 *>(p.part + (int64_t)tile * p.splits * per_cta + w);
+    const int64_t stride4 = per_cta / 4;
+    for (int sp0 = sp_lo; sp0 < sp_hi; sp0 += 8) {
+      float4 v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = sp0 + u < p.splits ? __ldg(src + (int64_t)(sp0 + u) * per_cta) : 0.f;
+      for (int u = 0; u < 8; ++u)
+        v[u] = sp0 + u < sp_hi ? __ldg(src + (int64_t)(sp0 + u) * stride4) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc += v[u];
+      for (int u = 0; u < 8; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
     }
-    df[(((int64_t)k * p.C + c) * p.R + r) * p.S + s] = acc;
+  }
+  red[q][gl] = acc;
+  __syncthreads();
+  if (q == 0 && g < groups) {
+    float4 t = red[0][gl];
+#pragma unroll
+    for (int qq = 1; qq < W2R_Q; ++qq) {
+      const float4 u = red[qq][gl];
+      t.x += u.x;
+      t.y += u.y;
+      t.z += u.z;
+      t.w += u.w;
+    }
+    const float tv[4] = {t.x, t.y, t.z, t.w};
+    const int kt = tile / p.nct, ct = tile - kt * p.nct;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t we = w + e;
+      const int rb = (int)(we / (128 * p.N));
+      const int rem = (int)(we - (int64_t)rb * 128 * p.N);
+      const int row = rem / p.N, col = rem - row * p.N;
+      const int j = row / p.Kc, kk = row - j * p.Kc;
+      const int s = col / p.Ct, cc = col - s * p.Ct;
+      const int k = kt * p.Kc + kk, c = ct * p.Ct + cc, r = rb * p.copies + j;
+      if (kk >= p.Kc || k >= p.K || c >= p.C || r >= p.R || j >= p.copies || s >= p.S) continue;
+      df[(((int64_t)k * p.C + c) * p.R + r) * p.S + s] = tv[e];
+    }
   }
   if (db)
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < p.K;
          k += (int64_t)gridDim.x * blockDim.x) {
-      float acc = 0.f;
-      for (int sp = 0; sp < dbcount; ++sp) acc += __ldg(dbsrc + (int64_t)sp * p.K + k);
-      db[k] = acc;
+      float a = 0.f;
+      for (int sp = 0; sp < dbcount; ++sp) a += __ldg(dbsrc + (int64_t)sp * p.K + k);
+      db[k] = a;
     }
 }
 
@@ -517,9 +553,8 @@ sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float
   }
   const int64_t total = (int64_t)p.K * p.C * p.R * p.S;
   if (p.splits >= 32)
-    w2_reduce_wide_kernel<<<(unsigned)std::min<int64_t>(
-                                ceil_div((int64_t)p.nkt * p.nct * p.RG * 128 * p.N, 256), 16 * sm_count()),
-                            256, 0, st>>>(
+    w2_reduce_wide_kernel<<<(unsigned)ceil_div((int64_t)p.nkt * p.nct * p.RG * 128 * p.N / 4, W2R_GROUPS),
+                            W2R_GROUPS * W2R_Q, 0, st>>>(
         p, df, db_src ? db : (p.dbpart ? db : nullptr), db_src ? db_src : p.dbpart,
         db_src ? db_count : p.splits);
   else
