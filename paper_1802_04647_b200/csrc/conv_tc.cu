@@ -96,6 +96,7 @@ struct TcFwdParams {
   int in_shift;
   int64_t out_plane;   // > 0: pooled output to SPF [K][out_plane] at (pp+out_off)*out_Wf + pc+out_off
   int out_Wf, out_Lf, out_off;
+  int y_nhwc;          // SN epilogue: y written channel-minor [n][P*Q][K] (else NCHW)
   uint32_t a_bytes, b_bytes, stage_bytes, a_sbo;
   int64_t ntiles;
   uint32_t tmem_cols;
@@ -320,6 +321,7 @@ __device__ __forceinline__ void epi_sn(const TcFwdParams &p, uint32_t tbase, int
   float *__restrict__ y = p.y;
   float *xch = xch_all + eset * (SN_MAXMT * 4 * 8 * 4 * 16);
   auto xidx = [&](int i, int q, int s_, int row) { return (((i * 4 + q) * 8 + s_) * 4 + row) * 16; };
+  const bool g32 = p.G < (1ll << 31);
   for (int c16 = eset; c16 < nc16; c16 += 2) {
     // 1) dump the first S-1 rows of every 32-row group for s >= 1
     for (int i = 0; i < p.MT; ++i)
@@ -355,14 +357,30 @@ __device__ __forceinline__ void epi_sn(const TcFwdParams &p, uint32_t tbase, int
       }
       const int64_t g = g0 + l;
       if (l < (int)p.cta_pos && g < p.G) {
-        const int n = (int)(g / p.Lf);
-        const int rem = (int)(g - (int64_t)n * p.Lf);
+        int n, rem;
+        if (g32) {
+          n = (int)((uint32_t)g / (uint32_t)p.Lf);
+          rem = (int)((uint32_t)g - (uint32_t)n * (uint32_t)p.Lf);
+        } else {
+          n = (int)(g / p.Lf);
+          rem = (int)(g - (int64_t)n * p.Lf);
+        }
         const int hh = rem / p.Wf, q = rem - hh * p.Wf;
         if (hh < p.P && q < p.Q) {
-          float *yp = y + (int64_t)n * p.K * PQ + (int64_t)hh * p.Q + q + (int64_t)k0 * PQ;
+          if (p.y_nhwc) {
+            // channel-minor [n][P*Q][K]: 16 channels = 64 contiguous bytes per row
+            float4 *yp = reinterpret_cast<float4 *>(y + ((int64_t)n * PQ + (int64_t)hh * p.Q + q) * p.K + k0);
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (k0 + j < p.K) yp[(int64_t)j * PQ] = acc[j] + b[j];
+            for (int j4 = 0; j4 < 4; ++j4)
+              if (k0 + 4 * j4 + 4 <= p.K)
+                yp[j4] = make_float4(acc[4 * j4] + b[4 * j4], acc[4 * j4 + 1] + b[4 * j4 + 1],
+                                     acc[4 * j4 + 2] + b[4 * j4 + 2], acc[4 * j4 + 3] + b[4 * j4 + 3]);
+          } else {
+            float *yp = y + (int64_t)n * p.K * PQ + (int64_t)hh * p.Q + q + (int64_t)k0 * PQ;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (k0 + j < p.K) yp[(int64_t)j * PQ] = acc[j] + b[j];
+          }
         }
       }
     }
@@ -500,7 +518,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         const long long t_e0 = clock64();
         ptx::mbar_wait(empty + stage, phase ^ 1);
         const long long t_f0 = clock64();
-        if (p.clk && tid == 0) p.clk[blockIdx.x * 8 + 0] += t_f0 - t_e0;
+        if (p.clk && tid == 0) p.clk[blockIdx.x * 16 + 0] += t_f0 - t_e0;
         uint8_t *A = stage_base + (size_t)stage * p.stage_bytes;
         uint8_t *B = A + p.a_bytes;
         if (tid == 0) {
@@ -542,7 +560,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           }
         }
         ptx::cp_async_mbar_arrive(full + stage);  // arrives when this thread's copies land
-        if (p.clk && tid == 0) p.clk[blockIdx.x * 8 + 1] += clock64() - t_f0;
+        if (p.clk && tid == 0) p.clk[blockIdx.x * 16 + 1] += clock64() - t_f0;
         if (++stage == p.nstage) { stage = 0; phase ^= 1; }
       }
     }
@@ -570,7 +588,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         const long long t_a0 = clock64();
         ptx::mbar_wait(acce + buf, bphase ^ 1);
         const long long t_a1 = clock64();
-        if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 3] += t_a1 - t_a0;
+        if (p.clk && lane == 0) p.clk[blockIdx.x * 16 + 3] += t_a1 - t_a0;
         ptx::tc_fence_after();
         const int n_inner = p.tile2d ? p.CT : 1;
         const uint32_t step_outer = p.tile2d ? (uint32_t)(16 * p.Wf) : 128u;
@@ -580,7 +598,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         for (int ch = 0; ch < p.nchunk; ++ch) {
           const long long t_w1 = clock64();
           ptx::mbar_wait(full + stage, phase);
-          if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 2] += clock64() - t_w1;
+          if (p.clk && lane == 0) p.clk[blockIdx.x * 16 + 2] += clock64() - t_w1;
           ptx::tc_fence_after();
           const uint32_t A = sbase + (uint32_t)stage * p.stage_bytes;
           const uint64_t adesc0 = ptx::make_desc(A, p.HALO * 16, p.a_sbo);
@@ -614,7 +632,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         }
         if (ptx::elect_one()) ptx::mma_commit(accf + buf);
         __syncwarp();
-        if (p.clk && lane == 0) p.clk[blockIdx.x * 8 + 6] += clock64() - t_a1;
+        if (p.clk && lane == 0) p.clk[blockIdx.x * 16 + 6] += clock64() - t_a1;
         continue;  // the MMA warp goes straight on to the next tile
       }
       ptx::mbar_wait_sleep(accf + buf, bphase);
@@ -633,11 +651,11 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(acce + buf);
-      if (p.clk && lane == 0 && warp == 5) p.clk[blockIdx.x * 8 + 4] += clock64() - t_epi0;
+      if (p.clk && lane == 0 && warp == 5) p.clk[blockIdx.x * 16 + 4] += clock64() - t_epi0;
     }
   }
-  if (p.clk && threadIdx.x == 160) p.clk[blockIdx.x * 8 + 5] = clock64() - t_kernel0;
-  if (p.clk && threadIdx.x == 0) p.clk[blockIdx.x * 8 + 7] = clock64() - t_kernel0;
+  if (p.clk && threadIdx.x == 160) p.clk[blockIdx.x * 16 + 5] = clock64() - t_kernel0;
+  if (p.clk && threadIdx.x == 0) p.clk[blockIdx.x * 16 + 7] = clock64() - t_kernel0;
   __syncthreads();
   if (warp == 4) {
     ptx::tc_fence_after();
@@ -827,6 +845,8 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   const bool single = (!p.cl2 && (single_env < 0 || single_env == 1) && p.NFpad == 256 && !pool) || p.sn;
   p.tbuf = single ? 0u : TMEM_BUF;
   int mt_cap = p.sn ? std::min(SN_MAXMT, 512 / p.NN) : std::min(16, (single ? 512 : (int)TMEM_BUF) / p.NFpad);
+  static const int mtcap_env = getenv("SYSML_TC_MTCAP") ? atoi(getenv("SYSML_TC_MTCAP")) : 0;
+  if (mtcap_env > 0) mt_cap = std::min(mt_cap, mtcap_env);
   p.CT = (p.Q + 7) / 8;
   if (p.tile2d && p.CT > mt_cap) return pl;
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -908,6 +928,11 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     p.out_off = io->out_off;
     p.pcode = io->code;
     p.code_plane = io->code_plane;
+    p.y_nhwc = io->out_nhwc;
+    if (p.y_nhwc && (!p.sn || (p.K & 3) || ((uintptr_t)y & 15))) {
+      set_error("tcgen05 forward: channel-minor output needs the SN epilogue, K %% 4 == 0 and a 16-byte aligned y");
+      return SYSML_ERR_UNSUPPORTED;
+    }
     if (p.pcode && !(p.pool && p.tile2d)) {
       set_error("tcgen05 forward: packed window codes need the fused 2x2 pool epilogue");
       return SYSML_ERR_UNSUPPORTED;
@@ -961,8 +986,8 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
   const bool prof = getenv("SYSML_TC_PROFILE") != nullptr;
   p.clk = nullptr;
   if (prof) {
-    if (!dclk) cudaMalloc(&dclk, sizeof(long long) * 8 * 1024);
-    cudaMemsetAsync(dclk, 0, sizeof(long long) * 8 * 1024, st);
+    if (!dclk) cudaMalloc(&dclk, sizeof(long long) * 16 * 1024);
+    cudaMemsetAsync(dclk, 0, sizeof(long long) * 16 * 1024, st);
     p.clk = dclk;
   }
   {
@@ -989,15 +1014,18 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
   }
   SYSML_LAUNCH_CHECK();
   if (prof) {
-    long long h[8 * 1024];
-    cudaMemcpyAsync(h, dclk, sizeof(long long) * 8 * grid, cudaMemcpyDeviceToHost, st);
+    static long long h[16 * 1024];
+    cudaMemcpyAsync(h, dclk, sizeof(long long) * 16 * grid, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    double a[8] = {0};
+    double a[16] = {0};
     for (int b = 0; b < grid; ++b)
-      for (int j = 0; j < 8; ++j) a[j] += (double)h[b * 8 + j] / grid;
+      for (int j = 0; j < 16; ++j) a[j] += (double)h[b * 16 + j] / grid;
     fprintf(stderr, "[tc_fwd N=%d C=%d K=%d MT=%d nstage=%d tiles=%lld] prod_wait_empty %.0f prod_fill %.0f "
             "mma_wait_full %.0f mma_wait_acce %.0f epilogue %.0f total_warp4 %.0f mma_loop %.0f total_prod %.0f\n",
             p.N, p.C, p.K, p.MT, p.nstage, (long long)p.ntiles, a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]);
+    if (p.sn)
+      fprintf(stderr, "  [sn epi] dump %.0f bar1 %.0f tmem_ld %.0f shfl_add %.0f store %.0f bar2 %.0f\n", a[8], a[9],
+              a[10], a[11], a[12], a[13]);
   }
   return SYSML_OK;
 }
@@ -1129,7 +1157,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_conv_wgrad_kernel(const TcWg
       ptx::named_bar_sync(1, 128);
       const uint32_t A = ptx::smem_u32(stage_base + (size_t)stage * p.stage_bytes);
       const uint32_t B = A + p.a_bytes;
-      // ---- A: row = (copy j, filter k); K-major [pos quad][128 rows][4 pos]
+      
+// ---- A: row = (copy j, filter k); K-major [pos quad][128 rows][4 pos]
       {
         const int shift = (p.copies - 1 - aj) * p.Wf;  // yt index of position u0 + u - j*Wf
         const float *dyk = p.dy + (size_t)(arow_ok ? ak : 0) * PQ;
@@ -1750,6 +1779,12 @@ sysml_status tc_conv_fwd_spf(const ConvArgs &a, const TcSpfIO &io, const float *
     return SYSML_ERR_UNSUPPORTED;
   }
   return run_fwd(pl, x, f, 0, a.C, bias, pool ? nullptr : y, pout, parg, ws, st, &io, csr);
+}
+
+bool tc_conv_bwd_data_spf_nhwc_ok(const ConvArgs &a) {
+  if (!tc_bwd_data_supported(a)) return false;
+  const TcPlan pl = plan_bwd_data(a);
+  return pl.ok && pl.p.sn && (pl.p.K & 3) == 0;
 }
 
 sysml_status tc_conv_bwd_data_spf(const ConvArgs &a, const TcSpfIO &io, const float *f,

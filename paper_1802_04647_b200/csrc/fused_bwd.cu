@@ -37,6 +37,7 @@ struct FusedB1Args {
   int mask_Wf, mask_Lf, mask_off;
   const uint64_t *code;                         // non-null: argmax + mask as 4-bit window codes
   int64_t code_plane;                           //   (TcSpfIO::code) -> the bulk kernel below
+  int dpool_nhwc;                               // bulk kernel: dpool[n] is [Pp*Qp][K] (else [K][Pp*Qp])
 };
 
 template <int R_, int S_>
@@ -232,11 +233,13 @@ __global__ void __launch_bounds__(FBB_THREADS)
     }
     ptx::named_bar_sync(1, FB_THREADS);  // image ready
     {
-      const float *gk = gs + kk * PpQp;
+      // pooled gradient of (k, pp): [K][PpQp] or, channel-minor, [PpQp][K] (lanes contiguous)
+      const int gsk = a.dpool_nhwc ? 1 : PpQp, gsp = a.dpool_nhwc ? a.K : 1;
+      const float *gk = gs + kk * gsk;
       const unsigned long long *ck = cs + (kk >> 4) * PpQp;
       const int sh = 4 * (kk & 15);
       for (int pp = wq; pp < PpQp; pp += FB_THREADS / 32) {
-        const float g0 = gk[pp];
+        const float g0 = gk[pp * gsp];
         const uint32_t cd = (uint32_t)(ck[pp] >> sh) & 15u;
         // masked (reading R9) lanes add g = 0: every lane stays on the same path
         const float g = (kok && (cd & 4u)) ? g0 : 0.f;
@@ -322,8 +325,10 @@ size_t fused_pool_bwd_wgrad_ws(const ConvArgs &c) {
 sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const float *x,
                                   const sysml_csr *xcsr, const float *dpool,
                                   const int32_t *argmax, const float *mask, float *df, float *db,
-                                  void *ws, cudaStream_t st, const TcSpfIO *mask_spf) {
+                                  void *ws, cudaStream_t st, const TcSpfIO *mask_spf,
+                                  int dpool_nhwc) {
   FusedB1Args a{};
+  a.dpool_nhwc = dpool_nhwc;
   if (mask_spf) {
     a.mask_plane = mask_spf->out_plane;
     a.mask_Wf = mask_spf->out_Wf;
@@ -346,6 +351,10 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
   float *part = reinterpret_cast<float *>(ws);
   sysml_csr empty{};
   const sysml_csr &cs = xcsr ? *xcsr : empty;
+  if (dpool_nhwc && !a.code) {
+    set_error("fused pool-bwd + conv1 wgrad: a channel-minor pooled gradient needs the window-code path");
+    return SYSML_ERR_UNSUPPORTED;
+  }
   if (a.code) {
     if (c.K > 32 || pa.R != 2 || pa.S != 2 || ((uintptr_t)dpool & 15) || (!xcsr && ((uintptr_t)x & 15)) ||
         ((int64_t)c.K * pa.P * pa.Q) % 4 || (pa.P * pa.Q) % 2 || (c.H * c.W) % 4) {

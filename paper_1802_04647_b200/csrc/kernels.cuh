@@ -72,6 +72,7 @@ struct TcSpfIO {
   uint64_t *code = nullptr;  // pooled argmax + relu mask as packed 4-bit window codes
   int64_t code_plane = 0;    // code[k/16][n*PpQp + pp*Qp + pc]: bits 4j..4j+3 of channel
                              // 16g + j = positive*4 + dr*2 + ds (window winner (2pp+dr, 2pc+ds))
+  int out_nhwc = 0;          // SN epilogue (bwd_data): y channel-minor [n][P*Q][K], K % 4 == 0
 };
 
 // conv_tc.cu : tcgen05 TF32 implicit GEMM (SYSML_MATH_TF32)
@@ -102,6 +103,8 @@ sysml_status tc_conv_fwd_spf(const ConvArgs &a, const TcSpfIO &io, const float *
                              const float *bias, float *y, const PoolArgs *pool, float *pout,
                              int32_t *parg, void *ws, cudaStream_t st,
                              const sysml_csr *csr = nullptr);
+// true when the SN epilogue serves this bwd_data, so TcSpfIO::out_nhwc may be set
+bool tc_conv_bwd_data_spf_nhwc_ok(const ConvArgs &a);
 sysml_status tc_conv_bwd_data_spf(const ConvArgs &a, const TcSpfIO &io, const float *f,
                                   const float *dy, float *dx, void *ws, cudaStream_t st);
 bool tc_wgrad_spf_supported(const SpfConv &sc);
@@ -130,7 +133,8 @@ size_t fused_pool_bwd_wgrad_ws(const ConvArgs &c);
 sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const float *x,
                                   const sysml_csr *xcsr, const float *dpool,
                                   const int32_t *argmax, const float *mask, float *df, float *db,
-                                  void *ws, cudaStream_t st, const TcSpfIO *mask_spf = nullptr);
+                                  void *ws, cudaStream_t st, const TcSpfIO *mask_spf = nullptr,
+                                  int dpool_nhwc = 0);  // dpool [n][Pp*Qp][K] (window-code path)
 
 // pool.cu : LeNet-internal layout helpers
 // maxpool_bwd (non-overlapping windows) writing the unpooled gradient into SPF planes

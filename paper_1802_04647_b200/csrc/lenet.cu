@@ -366,6 +366,7 @@ constexpr int NSTAGES = 10;
 
 struct sysml_lenet {
   int max_b = 0, math = 0, csr = 0;
+  int da1_nhwc = 0;  // SPF path: B2d writes da1 as [n][196][32] for the fused B1 (codes)
   int64_t max_nnz = 0;
   float *a1 = nullptr, *a2 = nullptr, *ds = nullptr, *lossn = nullptr, *da2 = nullptr,
         *dz2 = nullptr, *da1 = nullptr, *dz1 = nullptr, *part3 = nullptr;
@@ -517,6 +518,8 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
              tc_bwd_data_supported(a2a) && tc_wgrad_spf_supported(sc);
     if (h->spf) {
       h->spf_plane = (int64_t)max_local_batch * 256;
+      static const int nhwc_env = getenv("SYSML_DA1_NHWC") ? atoi(getenv("SYSML_DA1_NHWC")) : 1;
+      h->da1_nhwc = nhwc_env && tc_conv_bwd_data_spf_nhwc_ok(a2a) ? 1 : 0;
       need = std::max(need, tc_fwd_ws(a1a));
       need = std::max(need, conv1_pool_ws(a1a, &pa1));
       need = std::max(need, tc_fwd_ws(a2a));
@@ -706,6 +709,7 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     TcSpfIO io;
     io.in_plane = h->spf_plane;
     io.in_shift = -(2 * 16 + 2);
+    io.out_nhwc = h->da1_nhwc;  // da1 channel-minor: whole-vector stores, read only by B1
     SYSML_TRY(tc_conv_bwd_data_spf(ca2, io, params + OFF_F2, h->dz2s, h->da1, h->ws, st));
     SYSML_TRY(T.end());
   } else {
@@ -729,7 +733,7 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     SYSML_TRY(fused_pool_bwd_wgrad(ca1, pa1, x->is_csr ? nullptr : x->dense,
                                    x->is_csr ? &x->csr : nullptr, h->da1, h->i1,
                                    h->spf ? h->a1s : h->a1, grads + OFF_F1, grads + OFF_B1, h->ws,
-                                   st, h->spf ? &a1_io : nullptr));
+                                   st, h->spf ? &a1_io : nullptr, h->spf ? h->da1_nhwc : 0));
     SYSML_TRY(T.end());
   } else {
     // B1p
