@@ -348,11 +348,22 @@ __device__ __forceinline__ void epi_sn(const TcFwdParams &p, uint32_t tbase, int
         float t[16];
         ptx::tmem_ld16(tbase + (uint32_t)(i * p.NN + s_ * p.NFpad + c16 * 16), t);
         const bool from_next = lane + s_ >= 32;
-        const float *src = xch + xidx(ni < p.MT ? ni : 0, nq, s_, from_next ? lane + s_ - 32 : 0);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const float v = __shfl_down_sync(0xffffffffu, t[j], s_);
-          acc[j] += from_next ? src[j] : v;
+          if (!from_next) acc[j] += v;
+        }
+        if (from_next) {  // the last s lanes: rows of the next 32-row group (4 x 16 B loads)
+          const float4 *src =
+              reinterpret_cast<const float4 *>(xch + xidx(ni < p.MT ? ni : 0, nq, s_, lane + s_ - 32));
+#pragma unroll
+          for (int j4 = 0; j4 < 4; ++j4) {
+            const float4 u = src[j4];
+            acc[4 * j4] += u.x;
+            acc[4 * j4 + 1] += u.y;
+            acc[4 * j4 + 2] += u.z;
+            acc[4 * j4 + 3] += u.w;
+          }
         }
       }
       const int64_t g = g0 + l;
