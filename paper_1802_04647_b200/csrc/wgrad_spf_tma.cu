@@ -26,6 +26,7 @@ namespace sysml {
 
 namespace {
 
+constexpr int W2_MAXS = 8;  // column taps (plan: S <= 8)
 constexpr int W2_NA = 4;          // A ring (dY atoms)
 constexpr int W2_THREADS = 224;  // + warp 6: B (X atom) producer
 constexpr int W2_ATOM = 32;       // positions per atom (128-byte swizzled row)
@@ -233,25 +234,32 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         if (++sb == p.nbr) { sb = 0; pb ^= 1; }
         const uint8_t *B0 = Bring + slot * b_slot, *B1 = Bring + slot1 * b_slot;
         const uint32_t Bs = sB + slot * b_slot;
+        // all six 16-byte loads of this thread's (up to) three tasks first, then the shifts
+        float4 v0[3], v1[3];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int t = et + u * 128;
+          if (t < ntask) {
+            const int c = t >> 3, q = t & 7;
+            v0[u] = *reinterpret_cast<const float4 *>(B0 + c * 128 + ((q ^ (c & 7)) << 4));
+            v1[u] = q < 7 ? *reinterpret_cast<const float4 *>(B0 + c * 128 + (((q + 1) ^ (c & 7)) << 4))
+                          : *reinterpret_cast<const float4 *>(B1 + c * 128 + ((c & 7) << 4));
+          }
+        }
 #pragma unroll
         for (int u = 0; u < 3; ++u) {
           const int t = et + u * 128;
           if (t >= ntask) continue;
           const int c = t >> 3, q = t & 7;
-          const float4 v0 = *reinterpret_cast<const float4 *>(B0 + c * 128 + ((q ^ (c & 7)) << 4));
-          const float4 v1 = q < 7 ? *reinterpret_cast<const float4 *>(B0 + c * 128 + (((q + 1) ^ (c & 7)) << 4))
-                                  : *reinterpret_cast<const float4 *>(B1 + c * 128 + ((c & 7) << 4));
-          const float e[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-          for (int s_ = 1; s_ < p.S; ++s_) {
-            if ((s_ & 3) == 0) continue;
+          const float e[8] = {v0[u].x, v0[u].y, v0[u].z, v0[u].w, v1[u].x, v1[u].y, v1[u].z, v1[u].w};
+          // taps unrolled to W2_MAXS with predication: the 1..3-position select is static
+#pragma unroll
+          for (int s_ = 1; s_ < W2_MAXS; ++s_) {
+            if (s_ >= p.S || (s_ & 3) == 0) continue;
             const int row = s_ * p.Ct + c;
             const uint32_t dst = Bs + row * 128 + ((q ^ (row & 7)) << 4);
             const int o = s_ & 3;
-            float w0, w1, w2, w3;
-            if (o == 1) { w0 = e[1]; w1 = e[2]; w2 = e[3]; w3 = e[4]; }
-            else if (o == 2) { w0 = e[2]; w1 = e[3]; w2 = e[4]; w3 = e[5]; }
-            else { w0 = e[3]; w1 = e[4]; w2 = e[5]; w3 = e[6]; }
-            st_shared_v4_w2(dst, w0, w1, w2, w3);
+            st_shared_v4_w2(dst, e[o], e[o + 1], e[o + 2], e[o + 3]);
           }
         }
         ptx::fence_proxy_async_smem();
