@@ -40,6 +40,9 @@
 //   a descriptor offset.  One accumulator per tap group; the position range is split
 //   over CTAs and the partials are summed in a fixed order (deterministic).
 #include <stdio.h>
+
+#include <cmath>
+#include <mutex>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -104,6 +107,10 @@ struct TcFwdParams {
   int cl2;             // CTA-pair cluster: each CTA bulk-loads half of every filter chunk and
                        // multicasts it to both (halves the L2 -> SMEM filter stream)
   int64_t iters;       // tile iterations per CTA (cl2: equal in both CTAs, padded with empty tiles)
+  int sk;              // stream-K: CTA b runs the global chunk iterations [b*I/G, (b+1)*I/G),
+                       //   I = ntiles*nchunk, G = grid; tiles split across CTAs are combined below
+  float *sk_part;      // stream-K partial accumulators [grid][MT][NN/16][128 rows][16] (workspace)
+  int *sk_flag;        // [grid] ready flags of this launch (library-owned, reset by their consumer)
 };
 
 struct TcPlan {
@@ -399,6 +406,101 @@ __device__ __forceinline__ void epi_sn(const TcFwdParams &p, uint32_t tbase, int
   }
 }
 
+// ---------------------------------------------------------------- work distribution
+// Round-robin whole tiles (tile = blockIdx.x + it*gridDim.x), or stream-K: the
+// ntiles*nchunk chunk iterations are cut into gridDim.x equal contiguous ranges, so a
+// tile may be split across consecutive CTAs.  A segment is (tile, chunks [c0, c1)).
+// The CTA holding a split tile's first segment (c0 = 0) computes it LAST in its range and
+// owns the tile: it adds the other segments' partial accumulators, which their CTAs
+// computed FIRST in their ranges and published (partial slot + release flag), in segment
+// order -- a fixed order, so results are deterministic -- then runs the normal epilogue.
+struct TcWork {
+  int64_t i, i1, it;
+};
+__device__ __forceinline__ int64_t sk_begin(const TcFwdParams &p, int b) {
+  return (int64_t)b * (p.ntiles * p.nchunk) / gridDim.x;
+}
+__device__ __forceinline__ TcWork tc_work_init(const TcFwdParams &p) {
+  TcWork w;
+  w.it = 0;
+  w.i = p.sk ? sk_begin(p, blockIdx.x) : 0;
+  w.i1 = p.sk ? sk_begin(p, blockIdx.x + 1) : 0;
+  return w;
+}
+__device__ __forceinline__ bool tc_next_raw(const TcFwdParams &p, TcWork &w, int64_t &tile, int &c0,
+                                            int &c1) {
+  if (p.sk) {
+    if (w.i >= w.i1) return false;
+    tile = w.i / p.nchunk;
+    c0 = (int)(w.i - tile * p.nchunk);
+    c1 = (int)min((int64_t)p.nchunk, (int64_t)c0 + (w.i1 - w.i));
+    w.i += c1 - c0;
+    return true;
+  }
+  if (w.it >= p.iters) return false;
+  tile = blockIdx.x + w.it * gridDim.x;  // >= ntiles: empty (cl2 padding)
+  ++w.it;
+  if (tile >= p.ntiles && !p.cl2) return false;
+  c0 = 0;
+  c1 = p.nchunk;
+  return true;
+}
+// the segment, broadcast from lane 0: provably warp-uniform, so the MMA issue loop keeps
+// its descriptors on the uniform datapath
+__device__ __forceinline__ bool tc_next(const TcFwdParams &p, TcWork &w, int64_t &tile, int &c0, int &c1) {
+  const bool ok = tc_next_raw(p, w, tile, c0, c1);
+  if (!__shfl_sync(0xffffffffu, (int)ok, 0)) return false;
+  tile = __shfl_sync(0xffffffffu, tile, 0);
+  c0 = __shfl_sync(0xffffffffu, c0, 0);
+  c1 = __shfl_sync(0xffffffffu, c1, 0);
+  return true;
+}
+
+// stream-K contributor: this thread's accumulator row (all MT x NN columns; the two warp
+// sets of a quadrant split the 16-column groups) -> the CTA's partial slot
+__device__ __forceinline__ void sk_dump(const TcFwdParams &p, uint32_t tb, int row, int eset) {
+  const int ng = p.NN / 16;
+  float *slot = p.sk_part + (size_t)blockIdx.x * p.MT * ng * 128 * 16;
+  for (int i = 0; i < p.MT; ++i)
+    for (int c16 = eset; c16 < ng; c16 += 2) {
+      float v[16];
+      ptx::tmem_ld16(tb + (uint32_t)(i * p.NN + c16 * 16), v);
+      float4 *o = reinterpret_cast<float4 *>(slot + ((size_t)(i * ng + c16) * 128 + row) * 16);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+}
+
+// stream-K owner: add the partials of the CTAs holding segments [c1, nchunk) of this tile
+// (CTAs blockIdx.x + 1, + 2, ... in segment order) into the accumulator in TMEM
+__device__ __forceinline__ void sk_fixup(const TcFwdParams &p, uint32_t tb, int row, int eset, int c1) {
+  const int ng = p.NN / 16;
+  int nj = 0;
+  for (int cur = c1, j = blockIdx.x + 1; cur < p.nchunk && j < (int)gridDim.x; ++j, ++nj) {
+    cur += (int)(sk_begin(p, j + 1) - sk_begin(p, j));
+    while (ptx::ld_acquire_gpu(p.sk_flag + j) == 0) __nanosleep(64);
+  }
+  for (int i = 0; i < p.MT; ++i)
+    for (int c16 = eset; c16 < ng; c16 += 2) {
+      float v[16];
+      ptx::tmem_ld16(tb + (uint32_t)(i * p.NN + c16 * 16), v);
+      for (int jj = 1; jj <= nj; ++jj) {
+        const float4 *src = reinterpret_cast<const float4 *>(
+            p.sk_part + (size_t)(blockIdx.x + jj) * p.MT * ng * 128 * 16 + ((size_t)(i * ng + c16) * 128 + row) * 16);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 u = __ldcg(src + j);
+          v[4 * j] += u.x;
+          v[4 * j + 1] += u.y;
+          v[4 * j + 2] += u.z;
+          v[4 * j + 3] += u.w;
+        }
+      }
+      ptx::tmem_st16(tb + (uint32_t)(i * p.NN + c16 * 16), v);
+    }
+  ptx::tmem_st_wait();
+}
+
 __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const TcFwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t *stage_base = smem;
@@ -502,9 +604,10 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     // programmatic dependent launch: everything up to the first packed-filter read
     // (barriers, TMEM, gather tables, A copies) overlaps the filter-pack kernel
     if (tid == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
-    for (int64_t it = 0; it < p.iters; ++it) {
-      const int64_t tile = blockIdx.x + it * gridDim.x;  // >= ntiles: empty (cl2 padding)
-      if (tile >= p.ntiles && !p.cl2) break;
+    TcWork wk = tc_work_init(p);
+    int64_t tile;
+    int c0, c1;
+    while (tc_next(p, wk, tile, c0, c1)) {
       const int ft = (int)(tile % p.nft);
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
       ptx::named_bar_sync(1, 128);
@@ -525,7 +628,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         src_off[pos] = off;
       }
       ptx::named_bar_sync(1, 128);
-      for (int ch = 0; ch < p.nchunk; ++ch) {
+      for (int ch = c0; ch < c1; ++ch) {
         const long long t_e0 = clock64();
         ptx::mbar_wait(empty + stage, phase ^ 1);
         const long long t_f0 = clock64();
@@ -584,9 +687,10 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     const int PQ = p.P * p.Q;
     const int nc16 = p.NFpad / 16;
     uint32_t tcount = 0;
-    for (int64_t it = 0; it < p.iters; ++it, ++tcount) {
-      const int64_t tile = blockIdx.x + it * gridDim.x;
-      if (tile >= p.ntiles && !p.cl2) break;
+    TcWork wk = tc_work_init(p);
+    int64_t tile;
+    int c0, c1;
+    for (; tc_next(p, wk, tile, c0, c1); ++tcount) {
       const int ft = (int)(tile % p.nft);
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
       // double buffer: buffers alternate; single buffer (tbuf 0): buffer 0 every tile
@@ -606,7 +710,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         const uint32_t jump_outer = step_outer - 8u * (uint32_t)(n_inner - 1);
         const uint32_t nf = (uint32_t)p.NN;
         const uint32_t sbase = ptx::smem_u32(stage_base);
-        for (int ch = 0; ch < p.nchunk; ++ch) {
+        for (int ch = c0; ch < c1; ++ch) {
           const long long t_w1 = clock64();
           ptx::mbar_wait(full + stage, phase);
           if (p.clk && lane == 0) p.clk[blockIdx.x * 16 + 2] += clock64() - t_w1;
@@ -614,7 +718,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           const uint32_t A = sbase + (uint32_t)stage * p.stage_bytes;
           const uint64_t adesc0 = ptx::make_desc(A, p.HALO * 16, p.a_sbo);
           uint64_t bdesc = ptx::make_desc(A + p.a_bytes, nf * 16, 128);
-          uint32_t acc = ch != 0 ? 1u : 0u;
+          uint32_t acc = ch != c0 ? 1u : 0u;
           uint32_t drow = 0;
           // KS: all S column taps are in the K slots; SN: in the N columns
           const int s_taps = (p.ks || p.sn) ? 1 : p.S;
@@ -652,6 +756,31 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(qd * 32) << 16) + buf * p.tbuf;
       const int eset = (warp - 5) >> 2;  // epilogue warp set 0 / 1 -> even / odd M-tiles
+      if (p.sk && (c0 > 0 || c1 < p.nchunk)) {
+        if (c0 > 0) {
+          // stream-K contributor: publish the raw partial accumulator, no epilogue
+          sk_dump(p, tbase, qd * 32 + lane, eset);
+          ptx::named_bar_sync(4, 32 * TC_EPI_WARPS);
+          if (warp == 5 && lane == 0) {
+            __threadfence();
+            ptx::st_release_gpu(p.sk_flag + blockIdx.x, 1);
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(acce + buf);
+          continue;
+        }
+        // stream-K owner: add the later segments' partials, then the normal epilogue
+        sk_fixup(p, tbase, qd * 32 + lane, eset, c1);
+        ptx::tc_fence_before();
+        ptx::named_bar_sync(4, 32 * TC_EPI_WARPS);  // both sets' columns are complete
+        ptx::tc_fence_after();
+        if (warp == 5 && lane == 0)  // reset the consumed flags for the next launch
+          for (int cur = c1, j = blockIdx.x + 1; cur < p.nchunk && j < (int)gridDim.x; ++j) {
+            cur += (int)(sk_begin(p, j + 1) - sk_begin(p, j));
+            p.sk_flag[j] = 0;
+          }
+      }
       if (p.sn) {
         epi_sn(p, tbase, g0, qd, lane, bias_s, eset, sn_xch);
       } else if (p.pool) {
@@ -918,6 +1047,35 @@ sysml_status set_smem_attr(K kernel, size_t bytes, int &cache) {
   return SYSML_OK;
 }
 
+// stream-K hand-off flags: per device a ring of TC_SK_SETS sets of TC_SK_MAX_GRID ints,
+// zeroed once; each launch takes the next set (a captured graph keeps its set, and its
+// replays on one stream are sequential); every flag is reset by the CTA that consumes it.
+constexpr int TC_SK_SETS = 64, TC_SK_MAX_GRID = 256;
+static int *sk_flag_set(cudaStream_t st) {
+  static std::mutex mu;
+  static int *base[64] = {};
+  static unsigned ctr[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!base[dev]) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    int *b = nullptr;
+    if (cudaMalloc(&b, sizeof(int) * TC_SK_SETS * TC_SK_MAX_GRID) != cudaSuccess) return nullptr;
+    if (cudaMemset(b, 0, sizeof(int) * TC_SK_SETS * TC_SK_MAX_GRID) != cudaSuccess) return nullptr;
+    base[dev] = b;
+  }
+  return base[dev] + (ctr[dev]++ % TC_SK_SETS) * TC_SK_MAX_GRID;
+}
+
+// workspace for the stream-K partial accumulators: one slot of <= 512 TMEM columns x 128
+// rows per CTA (behind the packed filters)
+static size_t sk_ws_bytes() {
+  static const bool on = getenv("SYSML_TC_SK") && atoi(getenv("SYSML_TC_SK")) == 1;
+  return on ? align_up((size_t)sm_count() * 512 * 128 * sizeof(float), 256) : 0;
+}
+
 sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f_cin,
                      const float *bias, float *y, float *pout, int32_t *parg, void *ws,
                      cudaStream_t st, const TcSpfIO *io = nullptr, const sysml_csr *csr = nullptr) {
@@ -988,6 +1146,28 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
   static int attr = 0;
   SYSML_TRY(set_smem_attr(tc_conv_fwd_kernel, pl.smem, attr));
   int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
+  // stream-K (opt-in, SYSML_TC_SK=1): even chunk-iteration ranges per CTA instead of whole
+  // tiles.  Measured slower on every shape of this build -- single-buffered accumulators
+  // serialise the contributor's partial dump with its next segment's MMAs, and short tiles
+  // (LeNet conv2: 4 chunks) pay a second halo prologue and epilogue per split tile -- so the
+  // default stays round-robin whole tiles.
+  p.sk = 0;
+  p.sk_part = nullptr;
+  p.sk_flag = nullptr;
+  {
+    static const int sk_env = getenv("SYSML_TC_SK") ? atoi(getenv("SYSML_TC_SK")) : 0;
+    const int nsm = sm_count();
+    if (sk_env == 1 && !p.cl2 && !p.is_csr &&
+        p.ntiles * (int64_t)p.nchunk >= 2 * nsm && nsm <= TC_SK_MAX_GRID) {
+      int *flags = sk_flag_set(st);
+      if (flags) {
+        p.sk = 1;
+        p.sk_flag = flags;
+        p.sk_part = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + align_up(pl.fp_bytes, 256));
+        grid = nsm;
+      }
+    }
+  }
   if (p.cl2) {
     if (grid < 2) p.cl2 = 0;
     else grid &= ~1;
@@ -1735,8 +1915,8 @@ size_t tc_fwd_ws(const ConvArgs &a) {
   const int nfpad = a.K <= 256 ? std::max(16, round_up(a.K, 16)) : 256;
   const int nft = a.K <= 256 ? 1 : (a.K + 255) / 256;
   if (a.C == 1 && a.S <= 8)  // KS packing: [ftile][r][2 halves][NFpad][4]
-    return align_up((size_t)nft * a.R * 8 * nfpad * sizeof(float), 256);
-  return align_up((size_t)nft * ((a.C + 7) / 8) * a.R * a.S * 8 * nfpad * sizeof(float), 256);
+    return align_up((size_t)nft * a.R * 8 * nfpad * sizeof(float), 256) + sk_ws_bytes();
+  return align_up((size_t)nft * ((a.C + 7) / 8) * a.R * a.S * 8 * nfpad * sizeof(float), 256) + sk_ws_bytes();
 }
 
 sysml_status tc_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
@@ -1766,7 +1946,7 @@ bool tc_bwd_data_supported(const ConvArgs &a) {
 
 size_t tc_bwd_data_ws(const ConvArgs &a) {
   TcPlan pl = plan_bwd_data(a);
-  return pl.ok ? pl.fp_bytes : 0;
+  return pl.ok ? align_up(pl.fp_bytes, 256) + sk_ws_bytes() : 0;
 }
 
 sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,

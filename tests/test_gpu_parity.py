@@ -368,3 +368,17 @@ def test_lenet_step_sgd_and_determinism(S):
     loss = net.step_host(p, g, torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory(), n)
     assert host(p).tobytes() == results[0][0]
     assert np.isfinite(loss)
+
+
+def test_stream_k_opt_in_parity():
+    """The opt-in stream-K schedule of the tcgen05 conv kernel (SYSML_TC_SK=1, read once per
+    process): the conv and LeNet parity tests above, re-run in a child process with it on."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, SYSML_TC_SK="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.abspath(__file__), "-k",
+                        "(test_conv_fwd_bwd_parity and tf32) or test_lenet_fwd_bwd_parity or determinism"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
