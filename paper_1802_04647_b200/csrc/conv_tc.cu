@@ -43,6 +43,7 @@
 
 #include <cmath>
 #include <mutex>
+#include <string.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -107,6 +108,9 @@ struct TcFwdParams {
   int cl2;             // CTA-pair cluster: each CTA bulk-loads half of every filter chunk and
                        // multicasts it to both (halves the L2 -> SMEM filter stream)
   int64_t iters;       // tile iterations per CTA (cl2: equal in both CTAs, padded with empty tiles)
+  int abulk;          // 1x1 / pad 0 / NCHW input: each chunk's 8 channel rows are staged MN-major
+                       //   ([8][HALO], 16-byte cp.async) behind the stage and transposed to the
+                       //   K-major A operand by the producer threads
   int sk;              // stream-K: CTA b runs the global chunk iterations [b*I/G, (b+1)*I/G),
                        //   I = ntiles*nchunk, G = grid; tiles split across CTAs are combined below
   float *sk_part;      // stream-K partial accumulators [grid][MT][NN/16][128 rows][16] (workspace)
@@ -514,7 +518,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
   uint64_t *empty = bars + p.nstage;
   uint64_t *accf = bars + 2 * p.nstage;  // [2]
   uint64_t *acce = accf + 2;             // [2]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
+  uint64_t *staged = acce + 2;           // [nstage] abulk: staging buffer filled
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(staged + p.nstage);
 
   // warp index via shuffle: provably warp-uniform, so role branches keep the uniform datapath
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -522,13 +527,14 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     for (int s = 0; s < p.nstage; ++s) {
       // dense: 128 producer threads (cp.async arrivals) + the expect_tx arrival;
       // CSR: one warp fills a whole stage and arrives once with the expect_tx
-      ptx::mbar_init(full + s, p.is_csr ? 1 : 128 + 1);
+      ptx::mbar_init(full + s, p.is_csr ? 1 : (p.abulk ? 64 : 128) + 1);
       ptx::mbar_init(empty + s, p.cl2 ? 2 : 1);  // tcgen05.commit (of both CTAs of a pair)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(accf + b, 1);
       ptx::mbar_init(acce + b, TC_EPI_WARPS);
     }
+    for (int s = 0; s < p.nstage; ++s) ptx::mbar_init(staged + s, 64);  // abulk: loader cp.async arrivals
     ptx::fence_mbar_init();
   }
   if (p.bias_smem)
@@ -607,9 +613,80 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     TcWork wk = tc_work_init(p);
     int64_t tile;
     int c0, c1;
+    int ist = 0;  // abulk issuer (tid 0): stage cursor, runs up to L chunks ahead
+    uint32_t iph = 0;
     while (tc_next(p, wk, tile, c0, c1)) {
       const int ft = (int)(tile % p.nft);
       const int64_t g0 = (tile / p.nft) * p.cta_pos;
+      if (p.abulk) {
+        // ---- 1x1 / pad 0: frame position = image position g = n*HW + hw.  Warps 0-1 stage
+        // chunk ch's 8 channel rows MN-major ([8][HALO]) by 16-byte cp.async of 4-position
+        // groups (groups never straddle an image as HW % 4 == 0; lanes take consecutive
+        // groups: coalesced, conflict-free) plus the filter chunk, running ahead on the
+        // empty barriers; warps 2-3 transpose staging -> A[quad][pos][4 ch] (4-byte reads
+        // of consecutive positions, 16-byte row writes: conflict-free), fence generic ->
+        // async proxy (their own stores only: a fence behind in-flight cp.async of the same
+        // thread would wait for them), and arrive on the stage's full barrier.
+        const int ngrp = p.HALO / 4;
+        if (tid < 64) {
+          // per-segment group offsets n*C*HW + hw (int: N*C*H*W < 2^31, plan), -1 past G
+          ptx::named_bar_sync(5, 64);  // the previous segment's copies have read the table
+          for (int gq = tid; gq < ngrp; gq += 64) {
+            const int64_t g = g0 + 4 * gq;
+            int off = -1;
+            if (g < p.G) {
+              const int64_t n = g / HW;
+              off = (int)(n * p.C * HW + (g - n * HW));
+            }
+            src_off[gq] = off;
+          }
+          ptx::named_bar_sync(5, 64);
+          for (int ch = c0; ch < c1; ++ch) {
+            ptx::mbar_wait(empty + ist, iph ^ 1);
+            uint8_t *A = stage_base + (size_t)ist * p.stage_bytes;
+            uint8_t *B = A + p.a_bytes;
+            const uint32_t stg = ptx::smem_u32(B + p.b_bytes);
+            if (tid == 0) {
+              ptx::mbar_arrive_expect_tx(full + ist, p.b_bytes);
+              ptx::bulk_g2s(B, p.fp + ((size_t)ft * p.nchunk + ch) * (p.b_bytes / 4), p.b_bytes, full + ist);
+            }
+            const int cc0 = ch * 8, nc = min(8, p.C - cc0);
+            const float *xc = p.x + (int64_t)cc0 * HW;
+            // item = (channel half jh, group gq): four channel rows share offset and address
+            for (int base = tid; base < 2 * ngrp; base += 64) {
+              const int jh = base >= ngrp ? 1 : 0, gq = base - jh * ngrp;
+              const int off = src_off[gq];
+              const uint32_t dst = stg + (uint32_t)(4 * jh * p.HALO + 4 * gq) * 4;
+              const float *src = xc + off + (int64_t)(4 * jh) * HW;
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const bool ok = off >= 0 && 4 * jh + jj < nc;
+                ptx::cp_async16(dst + (uint32_t)(jj * p.HALO) * 4, ok ? src + (int64_t)jj * HW : p.x, ok ? 16u : 0u);
+              }
+            }
+            ptx::cp_async_mbar_arrive(staged + ist);
+            if (++ist == p.nstage) { ist = 0; iph ^= 1; }
+          }
+        } else {
+          const int tt = tid - 64;
+          for (int ch = c0; ch < c1; ++ch) {
+            ptx::mbar_wait(staged + stage, phase);
+            const uint8_t *A = stage_base + (size_t)stage * p.stage_bytes;
+            const float *stg = reinterpret_cast<const float *>(A + p.a_bytes + p.b_bytes);
+            const uint32_t a0 = ptx::smem_u32(A);
+            for (int it = tt; it < 2 * p.HALO; it += 64) {
+              const int q = it >= p.HALO ? 1 : 0, pos = it - q * p.HALO;
+              st_shared_v4(a0 + (uint32_t)(q * p.HALO + pos) * 16, stg[(4 * q) * p.HALO + pos],
+                           stg[(4 * q + 1) * p.HALO + pos], stg[(4 * q + 2) * p.HALO + pos],
+                           stg[(4 * q + 3) * p.HALO + pos]);
+            }
+            ptx::fence_proxy_async_smem();
+            ptx::mbar_arrive(full + stage);
+            if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+          }
+        }
+        continue;
+      }
       ptx::named_bar_sync(1, 128);
       const int ntab = p.ks ? p.HALO + 8 : p.HALO;
       for (int pos = tid; pos < ntab; pos += 128) {
@@ -952,6 +1029,9 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   p.G = (int64_t)N * p.Lf;
   if (p.G + 4096 >= (1ll << 31)) return pl;
   p.tile2d = pool ? 1 : 0;
+  static const int abulk_env = getenv("SYSML_TC_ABULK") ? atoi(getenv("SYSML_TC_ABULK")) : -1;
+  p.abulk = (abulk_env != 0 && !pool && R == 1 && S == 1 && ph == 0 && pw == 0 &&
+             ((int64_t)H * W) % 4 == 0 && C > 1 && (int64_t)N * C * H * W < (1ll << 31)) ? 1 : 0;
   if (K <= 256) {
     p.NFpad = std::max(16, round_up(K, 16));
     p.nft = 1;
@@ -1009,7 +1089,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
       }
       if (attempt == 0 && mt > 1 && ntiles < nsm && !single) continue;  // keep the SMs busy first
       const uint32_t a_bytes = (uint32_t)(2 * halo * 16);
-      const uint32_t stage = a_bytes + p.b_bytes;
+      const uint32_t stage = a_bytes + p.b_bytes + (p.abulk ? (uint32_t)(8 * halo * 4) : 0u);
       p.bias_smem = K <= 4096 ? 1 : 0;
       const size_t fixed = (size_t)(halo + 8) * 4 + (p.bias_smem ? (size_t)K * 4 : 0) + 16 + 8 * 24 + 16 +
                            (p.sn ? (size_t)SN_XCH_FLOATS * 4 : 0);
@@ -1024,7 +1104,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
       p.stage_bytes = stage;
       p.nstage = std::min(nst, 8);
       p.a_sbo = p.tile2d ? (uint32_t)(p.Wf * 16) : 128u;
-      pl.smem = (size_t)p.nstage * stage + fixed + 8 * (2 * p.nstage + 4);
+      pl.smem = (size_t)p.nstage * stage + fixed + 8 * (3 * p.nstage + 4);
       pl.ok = true;
       break;
     }
@@ -1107,6 +1187,8 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
       return SYSML_ERR_UNSUPPORTED;
     }
   }
+  if (p.abulk && (p.cl2 || p.in_plane > 0 || p.is_csr || ((uintptr_t)x & 15))) p.abulk = 0;  // NCHW only
+
   float *fp = reinterpret_cast<float *>(ws);
   if (p.ks) {
     if (flip) {
