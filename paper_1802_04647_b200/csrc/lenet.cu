@@ -175,43 +175,51 @@ __global__ void ordered_total_kernel(const float *__restrict__ v, int n, float *
   if (threadIdx.x == 0) *out = red[0];
 }
 
-// B3 stage 1: partial dW3/db3 over a chunk of samples.  Thread owns column d (all
-// 10 classes); part[chunk][j][d] (j < 10) and part[chunk][10][j] for db3.
-constexpr int DW3_THREADS = 256;
-__global__ void dw3_partial_kernel(int n, int n_per_chunk, const float *__restrict__ ds,
-                                   const float *__restrict__ a2, float *__restrict__ part) {
-  const int d = blockIdx.x * DW3_THREADS + threadIdx.x;
+// B3 stage 1: partial dW3/db3 over a chunk of samples.  Block (196 threads) x = a quarter
+// of the 784 float4 columns of a2 (thread owns 4 columns x 10 classes), y = sample chunk;
+// 8 samples' float4 loads in flight per thread.  part[chunk][j][d] (j < 10), and
+// part[chunk][10][j] = db3 partial (sum of ds over the chunk).
+constexpr int DW3_T = 196;                                 // 4 x 196 = 784 float4 columns
+constexpr int DW3_LEN = NCLS * D3 + NCLS;                 // W3 then b3 (the grads layout)
+constexpr int DW3_STRIDE = (DW3_LEN + 3) / 4 * 4;         // partial stride: float4 aligned
+__global__ void __launch_bounds__(DW3_T) dw3_partial_kernel(int n, int n_per_chunk, const float *__restrict__ ds,
+                                                            const float *__restrict__ a2,
+                                                            float *__restrict__ part) {
+  const int d4 = blockIdx.x * DW3_T + threadIdx.x;  // < 784
   const int chunk = blockIdx.y;
   const int n0 = chunk * n_per_chunk, n1 = min(n, n0 + n_per_chunk);
   __shared__ float dss[64 * NCLS];
-  float acc[NCLS];
+  float4 acc[NCLS];
 #pragma unroll
-  for (int j = 0; j < NCLS; ++j) acc[j] = 0.f;
+  for (int j = 0; j < NCLS; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 *a24 = reinterpret_cast<const float4 *>(a2) + d4;
   for (int nb = n0; nb < n1; nb += 64) {
     const int cnt = min(64, n1 - nb);
     __syncthreads();
-    for (int i = threadIdx.x; i < cnt * NCLS; i += DW3_THREADS) dss[i] = ds[(int64_t)nb * NCLS + i];
+    for (int i = threadIdx.x; i < cnt * NCLS; i += DW3_T) dss[i] = ds[(int64_t)nb * NCLS + i];
     __syncthreads();
-    if (d < D3) {
-      for (int i0 = 0; i0 < cnt; i0 += 8) {
-        float v[8];
+    for (int i0 = 0; i0 < cnt; i0 += 8) {
+      float4 v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)  // 8 images' loads in flight
-          v[u] = i0 + u < cnt ? __ldg(a2 + (int64_t)(nb + i0 + u) * D3 + d) : 0.f;
+      for (int u = 0; u < 8; ++u)
+        v[u] = i0 + u < cnt ? __ldg(a24 + (int64_t)(nb + i0 + u) * (D3 / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (i0 + u >= cnt) break;
+      for (int u = 0; u < 8; ++u) {
+        if (i0 + u >= cnt) break;
 #pragma unroll
-          for (int j = 0; j < NCLS; ++j) acc[j] = fmaf(dss[(i0 + u) * NCLS + j], v[u], acc[j]);
+        for (int j = 0; j < NCLS; ++j) {
+          const float w = dss[(i0 + u) * NCLS + j];
+          acc[j].x = fmaf(w, v[u].x, acc[j].x);
+          acc[j].y = fmaf(w, v[u].y, acc[j].y);
+          acc[j].z = fmaf(w, v[u].z, acc[j].z);
+          acc[j].w = fmaf(w, v[u].w, acc[j].w);
         }
       }
     }
   }
-  float *pc = part + (int64_t)chunk * (NCLS * D3 + NCLS);
-  if (d < D3) {
+  float *pc = part + (int64_t)chunk * DW3_STRIDE;
 #pragma unroll
-    for (int j = 0; j < NCLS; ++j) pc[j * D3 + d] = acc[j];
-  }
+  for (int j = 0; j < NCLS; ++j) reinterpret_cast<float4 *>(pc + j * D3)[d4] = acc[j];
   if (blockIdx.x == 0 && threadIdx.x < NCLS) {
     float s = 0.f;
     for (int i = n0; i < n1; ++i) s += ds[(int64_t)i * NCLS + threadIdx.x];
@@ -219,17 +227,59 @@ __global__ void dw3_partial_kernel(int n, int n_per_chunk, const float *__restri
   }
 }
 
-__global__ void chunk_sum_kernel(const float *__restrict__ part, int chunks, int64_t len,
-                                 float *__restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
-       i += (int64_t)gridDim.x * blockDim.x) {
+// B3 stage 2: out[i] = sum over chunks (fixed order) of part[c][i].  Block (32 float4
+// groups x 8 eighths of the chunks): thread (e, g) sums its eighth in chunk order, the
+// eighths are added in order (deterministic); the len % 4 scalar tail by block 0.
+__global__ void __launch_bounds__(256) dw3_reduce_kernel(const float *__restrict__ part, int chunks,
+                                                         int64_t stride, int64_t len, float *__restrict__ out) {
+  __shared__ float4 red[8][32];
+  const int gl = threadIdx.x & 31, e = threadIdx.x >> 5;
+  const int64_t g = blockIdx.x * 32 + gl, ng = len / 4;
+  const int per = (chunks + 7) / 8, c0 = e * per, c1 = min(chunks, c0 + per);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (g < ng)
+    for (int cb = c0; cb < c1; cb += 8) {  // 8 loads in flight, summed in chunk order
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = cb + u < c1 ? __ldg(reinterpret_cast<const float4 *>(part + (int64_t)(cb + u) * stride) + g)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
+    }
+  red[e][gl] = acc;
+  __syncthreads();
+  if (e == 0 && g < ng) {
+    float4 t = red[0][gl];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+      t.x += red[k][gl].x;
+      t.y += red[k][gl].y;
+      t.z += red[k][gl].z;
+      t.w += red[k][gl].w;
+    }
+    if (((uintptr_t)out & 15) == 0) {
+      reinterpret_cast<float4 *>(out)[g] = t;
+    } else {  // caller's gradient buffer not 16-byte aligned
+      out[4 * g] = t.x;
+      out[4 * g + 1] = t.y;
+      out[4 * g + 2] = t.z;
+      out[4 * g + 3] = t.w;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < len - 4 * ng) {
+    const int64_t i = 4 * ng + threadIdx.x;
     float s = 0.f;
-    for (int c = 0; c < chunks; ++c) s += part[(int64_t)c * len + i];
+    for (int c = 0; c < chunks; ++c) s += part[(int64_t)c * stride + i];
     out[i] = s;
   }
 }
 
-// da2[n,d] = sum_j ds[n,j] W3[j,d]
 __global__ void da2_kernel(int n, const float *__restrict__ ds, const float *__restrict__ W3,
                            float *__restrict__ da2) {
   const int64_t total = (int64_t)n * D3;
@@ -406,8 +456,8 @@ sysml_pool_desc pool1_desc(int n) { return sysml_pool_desc{n, 32, 28, 28, 2, 2, 
 sysml_pool_desc pool2_desc(int n) { return sysml_pool_desc{n, 64, 14, 14, 2, 2, 2, 2, 0, 0, 1}; }
 
 int dw3_chunks_for(int n) {
-  int64_t c = ceil_div(2 * sm_count(), ceil_div(D3, DW3_THREADS));
-  if (c > ceil_div(n, 16)) c = ceil_div(n, 16);
+  // about 16 samples per chunk, at most one chunk per SM (x 4 column blocks)
+  int64_t c = std::min<int64_t>(sm_count(), ceil_div(n, 16));
   return (int)(c < 1 ? 1 : c);
 }
 
@@ -480,7 +530,7 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
   ALLOC(h->dz2, b * 12544);
   ALLOC(h->da1, b * 6272);
   ALLOC(h->dz1, b * 25088);
-  ALLOC(h->part3, (int64_t)h->dw3_chunks * (NCLS * D3 + NCLS));
+  ALLOC(h->part3, (int64_t)h->dw3_chunks * DW3_STRIDE);
   ALLOC(h->loss_dev, 1);
   ALLOC(h->lab_dev, b);
   if (!h->csr) ALLOC(h->x_dev, b * 784);
@@ -669,12 +719,11 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     const int chunks = std::min(h->dw3_chunks, dw3_chunks_for(n));
     const int npc = (int)ceil_div(n, chunks);
     const int used = (int)ceil_div(n, npc);
-    dw3_partial_kernel<<<dim3((unsigned)ceil_div(D3, DW3_THREADS), used), DW3_THREADS, 0, st>>>(
-        n, npc, h->ds, h->a2, h->part3);
+    dw3_partial_kernel<<<dim3(D3 / 4 / DW3_T, used), DW3_T, 0, st>>>(n, npc, h->ds, h->a2, h->part3);
     SYSML_LAUNCH_CHECK();
     // grads W3 and b3 are contiguous: [W3 (10*3136)][b3 (10)] == part layout
-    chunk_sum_kernel<<<(unsigned)ceil_div(NCLS * D3 + NCLS, 256), 256, 0, st>>>(
-        h->part3, used, NCLS * D3 + NCLS, grads + OFF_W3);
+    dw3_reduce_kernel<<<(unsigned)ceil_div(DW3_LEN / 4, 32), 256, 0, st>>>(h->part3, used, DW3_STRIDE,
+                                                                          DW3_LEN, grads + OFF_W3);
     SYSML_LAUNCH_CHECK();
     if (!h->spf) {
       da2_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)n * D3, 256), 16 * sm_count()), 256,
