@@ -337,11 +337,12 @@ def sysml_version() -> str:
     return lib().sysml_version().decode()
 
 
-def nccl_comm_ptr(group=None) -> Optional[int]:
-    """ncclComm_t of torch's ProcessGroupNCCL (created lazily; run one collective first)."""
+def nccl_comm_ptr(group=None, allow_single: bool = False) -> Optional[int]:
+    """ncclComm_t of torch's ProcessGroupNCCL (created lazily; run one collective first).
+    None for a single rank unless allow_single (tests of the in-library allreduce path)."""
     torch = _torch()
     import torch.distributed as dist
-    if not dist.is_initialized() or dist.get_world_size() == 1:
+    if not dist.is_initialized() or (dist.get_world_size() == 1 and not allow_single):
         return None
     pg = group or dist.distributed_c10d._get_default_group()
     be = pg._get_backend(torch.device("cuda"))

@@ -417,6 +417,12 @@ constexpr int NSTAGES = 10;
 struct sysml_lenet {
   int max_b = 0, math = 0, csr = 0;
   int da1_nhwc = 0;  // SPF path: B2d writes da1 as [n][196][32] for the fused B1 (codes)
+  // data-parallel gradient exchange overlapped with the tail of the backward pass: the
+  // {F2, b2, W3, b3} bucket is all-reduced on ar_stream as soon as conv2 bwd_filter is done
+  // (while conv2 bwd_data and the conv1 backward run), {F1, b1} after the conv1 backward
+  void *ar_comm = nullptr;  // set by sysml_lenet_step for the duration of the call
+  cudaStream_t ar_stream = nullptr;
+  cudaEvent_t ev_b2 = nullptr, ev_b1 = nullptr, ev_ar = nullptr;
   int64_t max_nnz = 0;
   float *a1 = nullptr, *a2 = nullptr, *ds = nullptr, *lossn = nullptr, *da2 = nullptr,
         *dz2 = nullptr, *da1 = nullptr, *dz1 = nullptr, *part3 = nullptr;
@@ -503,6 +509,14 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
   SYSML_CHECK_ARG(!input_is_csr || max_nnz >= 0, "max_nnz must be >= 0");
   sysml_lenet *h = new sysml_lenet();
   h->max_b = max_local_batch;
+  if (cudaStreamCreateWithFlags(&h->ar_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_b2, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_b1, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_ar, cudaEventDisableTiming) != cudaSuccess) {
+    set_error("creating the allreduce stream / events failed");
+    delete h;
+    return SYSML_ERR_CUDA;
+  }
   h->math = math;
   h->csr = input_is_csr ? 1 : 0;
   h->max_nnz = max_nnz;
@@ -607,6 +621,10 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
 
 sysml_status sysml_lenet_destroy(sysml_lenet *h) {
   if (!h) return SYSML_OK;
+  if (h->ar_stream) cudaStreamDestroy(h->ar_stream);
+  if (h->ev_b2) cudaEventDestroy(h->ev_b2);
+  if (h->ev_b1) cudaEventDestroy(h->ev_b1);
+  if (h->ev_ar) cudaEventDestroy(h->ev_ar);
   cudaFree(h->a1); cudaFree(h->i1); cudaFree(h->a2); cudaFree(h->i2); cudaFree(h->ds);
   cudaFree(h->c1); cudaFree(h->c2); cudaFree(h->db2part);
   cudaFree(h->lossn); cudaFree(h->da2); cudaFree(h->dz2); cudaFree(h->da1); cudaFree(h->dz1);
@@ -617,6 +635,25 @@ sysml_status sysml_lenet_destroy(sysml_lenet *h) {
   for (int i = 0; i < NSTAGES; ++i)
     for (auto &e : h->pending[i]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   delete h;
+  return SYSML_OK;
+}
+
+// all-reduce (sum) of grads[0, count) on the handle's allreduce stream once the main stream
+// reaches this point (event `ev`); no-op unless a communicator is set for this step
+static sysml_status ar_bucket(sysml_lenet *h, float *g, size_t count, cudaEvent_t ev, cudaStream_t st) {
+  if (!h->ar_comm) return SYSML_OK;
+  NcclSyms &s = nccl_syms();
+  if (!s.allreduce) {
+    set_error("ncclAllReduce could not be resolved (libnccl.so.2 not loaded in this process)");
+    return SYSML_ERR_NCCL;
+  }
+  SYSML_CUDA(cudaEventRecord(ev, st));
+  SYSML_CUDA(cudaStreamWaitEvent(h->ar_stream, ev, 0));
+  const int r = s.allreduce(g, g, count, /*ncclFloat32*/ 7, /*ncclSum*/ 0, h->ar_comm, h->ar_stream);
+  if (r != 0) {
+    set_error("ncclAllReduce failed: %s", s.errstr ? s.errstr(r) : "?");
+    return SYSML_ERR_NCCL;
+  }
   return SYSML_OK;
 }
 
@@ -753,6 +790,7 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     } else
       SYSML_TRY(tc_wgrad_spf(sc, h->a1s, h->dz2s, grads + OFF_F2, grads + OFF_B2, h->ws, st));
     SYSML_TRY(T.end());
+    SYSML_TRY(ar_bucket(h, grads + OFF_F2, NUM_PARAMS - OFF_F2, h->ev_b2, st));
     // B2d: input frame (pad 2) position = stored output-frame position + 34
     SYSML_TRY(T.begin(6));
     TcSpfIO io;
@@ -771,6 +809,7 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     SYSML_TRY(conv_bwd_filter_dispatch(c2, a1in, h->dz2, grads + OFF_F2, grads + OFF_B2, h->ws,
                                        h->ws_bytes, st));
     SYSML_TRY(T.end());
+    SYSML_TRY(ar_bucket(h, grads + OFF_F2, NUM_PARAMS - OFF_F2, h->ev_b2, st));
     // B2d
     SYSML_TRY(T.begin(6));
     SYSML_TRY(conv_bwd_data_dispatch(c2, params + OFF_F2, h->dz2, h->da1, h->ws, h->ws_bytes, st));
@@ -796,6 +835,11 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     SYSML_TRY(T.end());
   }
   (void)launches0;
+  if (h->ar_comm) {  // {F1, b1}, then the main stream joins the allreduce stream
+    SYSML_TRY(ar_bucket(h, grads, OFF_F2, h->ev_b1, st));
+    SYSML_CUDA(cudaEventRecord(h->ev_ar, h->ar_stream));
+    SYSML_CUDA(cudaStreamWaitEvent(st, h->ev_ar, 0));
+  }
   return SYSML_OK;
 }
 
@@ -812,6 +856,15 @@ sysml_status sysml_sgd_update(float *params, const float *grads, int64_t n, floa
 sysml_status sysml_lenet_step(sysml_lenet *h, float *params, float *grads, const sysml_input *x,
                               const int32_t *labels, int32_t n_local, int64_t n_global,
                               float lr, void *nccl_comm, float *loss_sum, sysml_stream_t stream) {
+  // overlapped bucketed allreduce unless SYSML_AR_OVERLAP=0 (read per call)
+  const char *ov = getenv("SYSML_AR_OVERLAP");
+  if (nccl_comm && !(ov && ov[0] == '0')) {
+    h->ar_comm = nccl_comm;
+    const sysml_status r = sysml_lenet_fwd_bwd(h, params, x, labels, n_local, n_global, grads, loss_sum, stream);
+    h->ar_comm = nullptr;
+    SYSML_TRY(r);
+    return sysml_sgd_update(params, grads, NUM_PARAMS, lr, stream);
+  }
   SYSML_TRY(sysml_lenet_fwd_bwd(h, params, x, labels, n_local, n_global, grads, loss_sum, stream));
   if (nccl_comm) {
     NcclSyms &s = nccl_syms();

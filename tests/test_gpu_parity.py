@@ -382,3 +382,57 @@ def test_stream_k_opt_in_parity():
                         "(test_conv_fwd_bwd_parity and tf32) or test_lenet_fwd_bwd_parity or determinism"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_lenet_step_nccl_bucketed_allreduce(S):
+    """sysml_lenet_step with a communicator: the bucketed allreduce overlapped on the handle's
+    side stream ({F2,b2,W3,b3} after conv2 bwd_filter, {F1,b1} at the end) gives bitwise the
+    same parameters as the single end-of-step allreduce and as no communicator (one rank: the
+    sum is the identity), eagerly and replayed from a captured CUDA graph."""
+    import os
+    import socket
+    import torch.distributed as dist
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        t = torch.ones(1, device="cuda")
+        dist.all_reduce(t)
+        comm = S.nccl_comm_ptr(allow_single=True)
+        assert comm
+        n = 24
+        x, y, prm = _lenet_case(n, seed=910)
+        net = S.LeNet(n, math="tf32")
+        out = {}
+        for mode in ("none", "single", "overlap"):
+            os.environ["SYSML_AR_OVERLAP"] = "0" if mode == "single" else "1"
+            p, g = dev(prm), torch.empty(83466, device="cuda")
+            for _ in range(2):
+                net.step(p, g, dev(x), dev(y, torch.int32), 64, lr=0.01,
+                         nccl_comm=None if mode == "none" else comm)
+            torch.cuda.synchronize()
+            out[mode] = host(p).tobytes()
+        assert out["overlap"] == out["single"] == out["none"]
+        # captured graph (side-stream fork / join inside the capture)
+        os.environ["SYSML_AR_OVERLAP"] = "1"
+        p, g = dev(prm), torch.empty(83466, device="cuda")
+        xd, yd = dev(x), dev(y, torch.int32)
+        net.step(p, g, xd, yd, 64, lr=0.01, nccl_comm=comm)  # warm-up (plans, attributes)
+        p.copy_(dev(prm))
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=cs):
+            net.step(p, g, xd, yd, 64, lr=0.01, nccl_comm=comm)
+        torch.cuda.current_stream().wait_stream(cs)
+        p.copy_(dev(prm))
+        torch.cuda.synchronize()
+        for _ in range(2):
+            gr.replay()
+        torch.cuda.synchronize()
+        assert host(p).tobytes() == out["overlap"]
+    finally:
+        os.environ.pop("SYSML_AR_OVERLAP", None)
+        dist.destroy_process_group()
