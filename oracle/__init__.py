@@ -59,6 +59,7 @@ def lib():
         _lib.oracle_lenet_forward.argtypes = [i64, dp, dp, dp, ip, dp, ip, dp]
         _lib.oracle_lenet_fwd_bwd.argtypes = [i64, i64, dp, ip, dp, dp, dp]
         _lib.oracle_sgd_update.argtypes = [i64, dp, dp, ctypes.c_double]
+        _lib.oracle_optimizer_update.argtypes = [i64, i64, dp, dp, dp] + [ctypes.c_double] * 6 + [i64]
     return _lib
 
 
@@ -165,6 +166,23 @@ def lenet_fwd_bwd(x, labels, params, n_global=None):
     lib().oracle_lenet_fwd_bwd(n, n_global, _p(x), _p(lab), _p(prm), _p(g),
                                ctypes.cast(ctypes.pointer(loss), ctypes.POINTER(ctypes.c_double)))
     return g, loss.value
+
+
+OPTIMIZERS = {"sgd": 0, "momentum": 1, "nesterov": 2, "adagrad": 3, "rmsprop": 4, "adam": 5}
+OPT_STATE = {"sgd": 0, "momentum": 1, "nesterov": 1, "adagrad": 1, "rmsprop": 1, "adam": 2}
+
+
+def optimizer_update(kind, params, grads, state, t=1, lr=0.01, mu=0.9, rho=0.99, eps=1e-8,
+                     beta1=0.9, beta2=0.999):
+    """One update of the named optimizer; returns (params', state').
+    state: float64[OPT_STATE[kind] * n] (adam: m then v); t: adam timestep (>= 1)."""
+    p = _d(params).copy()
+    g = _d(grads)
+    st = _d(state).copy() if OPT_STATE[kind] else np.zeros(1)
+    assert st.size == max(1, OPT_STATE[kind] * p.size)
+    lib().oracle_optimizer_update(OPTIMIZERS[kind], p.size, _p(p), _p(g), _p(st), lr, mu, rho, eps,
+                                  beta1, beta2, int(t))
+    return p, (st if OPT_STATE[kind] else np.zeros(0))
 
 
 def sgd_update(params, grads, lr=0.01):

@@ -338,3 +338,50 @@ EXPORT void oracle_lenet_fwd_bwd(int64_t n, int64_t n_global, const double *x,
 EXPORT void oracle_sgd_update(int64_t n, double *params, const double *grads, double lr) {
   for (int64_t i = 0; i < n; ++i) params[i] = params[i] - lr * grads[i];
 }
+
+/* The six optimizers of the NN library ("6 optimizers (namely Adagrad, Adam, RMSprop,
+ * SGD, SGD with momentum, and SGD with Nesterov momentum)"; S:282-290 optimizer_update).
+ * kind: 0 sgd, 1 sgd_momentum, 2 sgd_nesterov, 3 adagrad, 4 rmsprop, 5 adam.
+ * state: kinds 1-4 one accumulator per parameter (velocity v / squared-gradient cache);
+ * adam two, first moments m[0..n) then second moments v[n..2n).  t = adam timestep of
+ * this update (>= 1).  One update, written out in the order of the rules:
+ *   sgd       p <- p - lr g
+ *   momentum  v <- mu v - lr g;  p <- p + v
+ *   nesterov  v_prev <- v;  v <- mu v - lr g;  p <- p - mu v_prev + (1 + mu) v
+ *             (the look-ahead form of momentum; reading R19)
+ *   adagrad   c <- c + g^2;  p <- p - lr g / (sqrt(c) + eps)
+ *   rmsprop   c <- rho c + (1 - rho) g^2;  p <- p - lr g / (sqrt(c) + eps)
+ *   adam      m <- b1 m + (1 - b1) g;  v <- b2 v + (1 - b2) g^2;
+ *             mh = m / (1 - b1^t);  vh = v / (1 - b2^t);  p <- p - lr mh / (sqrt(vh) + eps)
+ *             (bias-corrected moments; eps outside the correction as in S:290's
+ *             worked example p = -lr * 1 / (sqrt(1) + eps) at t = 1)                    */
+EXPORT void oracle_optimizer_update(int64_t kind, int64_t n, double *p, const double *g, double *state,
+                                    double lr, double mu, double rho, double eps, double b1, double b2,
+                                    int64_t t) {
+  for (int64_t i = 0; i < n; ++i) {
+    const double gi = g[i];
+    if (kind == 0) {
+      p[i] = p[i] - lr * gi;
+    } else if (kind == 1) {
+      state[i] = mu * state[i] - lr * gi;
+      p[i] = p[i] + state[i];
+    } else if (kind == 2) {
+      const double v_prev = state[i];
+      state[i] = mu * state[i] - lr * gi;
+      p[i] = p[i] - mu * v_prev + (1.0 + mu) * state[i];
+    } else if (kind == 3) {
+      state[i] = state[i] + gi * gi;
+      p[i] = p[i] - lr * gi / (sqrt(state[i]) + eps);
+    } else if (kind == 4) {
+      state[i] = rho * state[i] + (1.0 - rho) * gi * gi;
+      p[i] = p[i] - lr * gi / (sqrt(state[i]) + eps);
+    } else {
+      double *m = state, *v = state + n;
+      m[i] = b1 * m[i] + (1.0 - b1) * gi;
+      v[i] = b2 * v[i] + (1.0 - b2) * gi * gi;
+      const double mh = m[i] / (1.0 - pow(b1, (double)t));
+      const double vh = v[i] / (1.0 - pow(b2, (double)t));
+      p[i] = p[i] - lr * mh / (sqrt(vh) + eps);
+    }
+  }
+}
