@@ -222,6 +222,41 @@ SYSML_API sysml_status sysml_lenet_step(sysml_lenet *h, float *params, float *gr
                               const int32_t *labels, int32_t n_local, int64_t n_global,
                               float lr, void *nccl_comm, float *loss_sum, sysml_stream_t stream);
 
+/* The six optimizers of the NN library ("Adagrad, Adam, RMSprop, SGD, SGD with
+ * momentum, and SGD with Nesterov momentum"; S:282-290 optimizer_update).  One update of
+ * params[0, n) with grads (device fp32).  `state` (device, caller-owned, zero before the
+ * first update; NULL for SGD) holds sysml_optimizer_state_floats(kind) * n floats: the
+ * velocity (momentum, nesterov), the squared-gradient cache (adagrad, rmsprop), or the
+ * first moments then the second moments (adam).  t = adam timestep of this update, >= 1
+ * (ignored by the others).  Rules, elementwise in fp32 (oracle: oracle_optimizer_update):
+ *   sgd       p -= lr g
+ *   momentum  v = mu v - lr g;  p += v
+ *   nesterov  v' = mu v - lr g;  p += -mu v + (1 + mu) v'
+ *   adagrad   c += g^2;  p -= lr g / (sqrt(c) + eps)
+ *   rmsprop   c = rho c + (1 - rho) g^2;  p -= lr g / (sqrt(c) + eps)
+ *   adam      m = b1 m + (1 - b1) g;  v = b2 v + (1 - b2) g^2;
+ *             p -= lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
+ * Errors: SYSML_ERR_ARG for an unknown kind, NULL pointers, n < 0, t < 1 (adam). */
+typedef enum {
+  SYSML_OPT_SGD = 0, SYSML_OPT_MOMENTUM = 1, SYSML_OPT_NESTEROV = 2,
+  SYSML_OPT_ADAGRAD = 3, SYSML_OPT_RMSPROP = 4, SYSML_OPT_ADAM = 5
+} sysml_optimizer_kind;
+typedef struct {
+  int32_t kind;
+  float lr, mu, rho, eps, beta1, beta2;
+} sysml_optimizer_desc;
+SYSML_API int32_t sysml_optimizer_state_floats(int32_t kind); /* 0, 1 or 2 per parameter; -1 unknown */
+SYSML_API sysml_status sysml_optimizer_update(const sysml_optimizer_desc *d, float *params,
+                                              const float *grads, float *state, int64_t n, int64_t t,
+                                              sysml_stream_t stream);
+
+/* sysml_lenet_step with any of the six optimizers: fwd_bwd + (if nccl_comm) the bucketed
+ * gradient allreduce + sysml_optimizer_update(d, params, grads, state, 83466, t).        */
+SYSML_API sysml_status sysml_lenet_step_opt(sysml_lenet *h, float *params, float *grads, float *state,
+                                  const sysml_optimizer_desc *d, int64_t t, const sysml_input *x,
+                                  const int32_t *labels, int32_t n_local, int64_t n_global,
+                                  void *nccl_comm, float *loss_sum, sysml_stream_t stream);
+
 /* End-to-end variant with HOST inputs: x_host (dense fp32 n_local x 784, pinned
  * for overlap) and labels_host are copied into handle-owned device buffers on
  * `stream`, the step runs as sysml_lenet_step, and the loss is copied back to

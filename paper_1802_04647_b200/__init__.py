@@ -43,6 +43,7 @@ EXPORTS = (
     "sysml_lenet_num_params", "sysml_lenet_create", "sysml_lenet_destroy", "sysml_lenet_fwd_bwd",
     "sysml_sgd_update", "sysml_lenet_step", "sysml_lenet_step_host",
     "sysml_lenet_set_timing", "sysml_lenet_get_timing",
+    "sysml_optimizer_state_floats", "sysml_optimizer_update", "sysml_lenet_step_opt",
 )
 
 
@@ -76,6 +77,21 @@ class PoolDesc(ctypes.Structure):
     @property
     def Q(self):
         return (self.W + 2 * self.pad_w - self.S) // self.stride_w + 1
+
+
+class OptimizerDesc(ctypes.Structure):
+    """sysml_optimizer_desc (include/sysml.h): the six NN-library optimizers."""
+    _fields_ = [("kind", ctypes.c_int32), ("lr", ctypes.c_float), ("mu", ctypes.c_float),
+                ("rho", ctypes.c_float), ("eps", ctypes.c_float), ("beta1", ctypes.c_float),
+                ("beta2", ctypes.c_float)]
+
+
+OPTIMIZERS = {"sgd": 0, "momentum": 1, "nesterov": 2, "adagrad": 3, "rmsprop": 4, "adam": 5}
+
+
+def optimizer_desc(kind, lr=0.01, mu=0.9, rho=0.99, eps=1e-8, beta1=0.9, beta2=0.999) -> OptimizerDesc:
+    """Defaults: S:285 (eps 1e-8, mu 0.9, rho 0.99, beta1 0.9, beta2 0.999) and lr 0.01."""
+    return OptimizerDesc(OPTIMIZERS[kind], lr, mu, rho, eps, beta1, beta2)
 
 
 class _Csr(ctypes.Structure):
@@ -155,6 +171,10 @@ def lib(build_if_missing: bool = False):
         "sysml_lenet_step": (c_i32, [vp, vp, vp, IN, vp, c_i32, c_i64, ctypes.c_float, vp, vp, vp]),
         "sysml_lenet_step_host": (c_i32, [vp, vp, vp, vp, vp, c_i32, c_i64, ctypes.c_float, vp, vp, vp]),
         "sysml_lenet_set_timing": (c_i32, [vp, c_i32]),
+        "sysml_optimizer_state_floats": (c_i32, [c_i32]),
+        "sysml_optimizer_update": (c_i32, [ctypes.POINTER(OptimizerDesc), vp, vp, vp, c_i64, c_i64, vp]),
+        "sysml_lenet_step_opt": (c_i32, [vp, vp, vp, vp, ctypes.POINTER(OptimizerDesc), c_i64, IN, vp, c_i32,
+                                         c_i64, vp, vp, vp]),
         "sysml_lenet_get_timing": (c_i32, [vp, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(c_i64), ctypes.POINTER(ctypes.c_char_p)]),
     }
@@ -329,6 +349,15 @@ def sysml_sgd_update(params, grads, lr=0.01, stream=None):
     return params
 
 
+def sysml_optimizer_update(desc, params, grads, state, t=1, stream=None):
+    """One in-place optimizer update (sysml_optimizer_update)."""
+    torch = _torch()
+    _check(lib().sysml_optimizer_update(ctypes.byref(desc), _ptr(params, torch.float32, "params"),
+                                        _ptr(grads, torch.float32, "grads"), _ptr(state, torch.float32, "state"),
+                                        params.numel(), int(t), _stream(stream)))
+    return params
+
+
 def sysml_launch_counter() -> int:
     return int(lib().sysml_launch_counter())
 
@@ -390,6 +419,19 @@ class LeNet:
                                       ctypes.byref(inp), _ptr(labels, torch.int32, "labels"), int(n), int(n_global),
                                       ctypes.c_float(lr), ctypes.c_void_p(nccl_comm) if nccl_comm else None,
                                       _ptr(loss_sum, torch.float32, "loss_sum"), _stream(stream)))
+
+    def step_opt(self, params, grads, state, desc, t, x, labels, n_global, nccl_comm=None, loss_sum=None,
+                 stream=None):
+        """One step with any of the six optimizers (sysml_lenet_step_opt); state: device fp32
+        [sysml_optimizer_state_floats(kind) * 83466] (None for SGD), t: adam timestep >= 1."""
+        torch = _torch()
+        inp = _input(x)
+        n = x.rows if isinstance(x, CSR) else x.shape[0]
+        _check(lib().sysml_lenet_step_opt(self.h, _ptr(params, torch.float32, "params"), _ptr(grads, torch.float32, "grads"),
+                                          _ptr(state, torch.float32, "state"), ctypes.byref(desc), int(t),
+                                          ctypes.byref(inp), _ptr(labels, torch.int32, "labels"), int(n), int(n_global),
+                                          ctypes.c_void_p(nccl_comm) if nccl_comm else None,
+                                          _ptr(loss_sum, torch.float32, "loss_sum"), _stream(stream)))
 
     def step_host(self, params, grads, x_host, labels_host, n_global, lr=0.01, nccl_comm=None, stream=None) -> float:
         """End-to-end step from HOST (ideally pinned) float32 / int32 CPU tensors."""

@@ -13,6 +13,9 @@
 //   B1p dz1 = maxpool_bwd(i1, da1, a1 > 0); B1f dF1, db1 = bwd_filter(X, dz1)
 #include <dlfcn.h>
 
+#include <algorithm>
+#include <cmath>
+
 #include <mutex>
 #include <string>
 #include <vector>
@@ -371,6 +374,44 @@ __global__ void __launch_bounds__(256) db2_reduce_kernel(const float *__restrict
     __syncthreads();
   }
   if (t == 0) db[k] = red[0];
+}
+
+// The six optimizers (include/sysml.h): elementwise fp32, one thread per
+// parameter; kind is a template argument so the loop carries no dispatch.  Adam's bias
+// corrections arrive as reciprocals c1 = 1/(1 - b1^t), c2 = 1/(1 - b2^t) (host, in double).
+template <int KIND>
+__global__ void optimizer_kernel(float *__restrict__ p, const float *__restrict__ g, float *__restrict__ st,
+                                 int64_t n, float lr, float mu, float rho, float eps, float b1, float b2,
+                                 float c1, float c2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    if (KIND == SYSML_OPT_SGD) {
+      p[i] = p[i] - lr * gi;
+    } else if (KIND == SYSML_OPT_MOMENTUM) {
+      const float v = mu * st[i] - lr * gi;
+      st[i] = v;
+      p[i] = p[i] + v;
+    } else if (KIND == SYSML_OPT_NESTEROV) {
+      const float v_prev = st[i];
+      const float v = mu * v_prev - lr * gi;
+      st[i] = v;
+      p[i] = p[i] - mu * v_prev + (1.f + mu) * v;
+    } else if (KIND == SYSML_OPT_ADAGRAD) {
+      const float c = st[i] + gi * gi;
+      st[i] = c;
+      p[i] = p[i] - lr * gi / (sqrtf(c) + eps);
+    } else if (KIND == SYSML_OPT_RMSPROP) {
+      const float c = rho * st[i] + (1.f - rho) * gi * gi;
+      st[i] = c;
+      p[i] = p[i] - lr * gi / (sqrtf(c) + eps);
+    } else {
+      const float m = b1 * st[i] + (1.f - b1) * gi;
+      const float v = b2 * st[n + i] + (1.f - b2) * gi * gi;
+      st[i] = m;
+      st[n + i] = v;
+      p[i] = p[i] - lr * (m * c1) / (sqrtf(v * c2) + eps);
+    }
+  }
 }
 
 __global__ void sgd_kernel(float *__restrict__ p, const float *__restrict__ g, int64_t n,
@@ -853,6 +894,47 @@ sysml_status sysml_sgd_update(float *params, const float *grads, int64_t n, floa
   return SYSML_OK;
 }
 
+int32_t sysml_optimizer_state_floats(int32_t kind) {
+  switch (kind) {
+    case SYSML_OPT_SGD: return 0;
+    case SYSML_OPT_MOMENTUM: case SYSML_OPT_NESTEROV: case SYSML_OPT_ADAGRAD: case SYSML_OPT_RMSPROP: return 1;
+    case SYSML_OPT_ADAM: return 2;
+    default: return -1;
+  }
+}
+
+sysml_status sysml_optimizer_update(const sysml_optimizer_desc *d, float *params, const float *grads,
+                                    float *state, int64_t n, int64_t t, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(d && params && grads, "NULL argument to sysml_optimizer_update");
+  const int nst = sysml_optimizer_state_floats(d->kind);
+  SYSML_CHECK_ARG(nst >= 0, "unknown optimizer kind %d", d->kind);
+  SYSML_CHECK_ARG(nst == 0 || state, "optimizer kind %d needs a state buffer", d->kind);
+  SYSML_CHECK_ARG(n >= 0, "n = %lld < 0", (long long)n);
+  SYSML_CHECK_ARG(d->kind != SYSML_OPT_ADAM || t >= 1, "adam timestep t = %lld < 1", (long long)t);
+  if (n == 0) return SYSML_OK;
+  double c1 = 1.0, c2 = 1.0;
+  if (d->kind == SYSML_OPT_ADAM) {
+    c1 = 1.0 / (1.0 - pow((double)d->beta1, (double)t));
+    c2 = 1.0 / (1.0 - pow((double)d->beta2, (double)t));
+  }
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * sm_count());
+  cudaStream_t st = (cudaStream_t)stream;
+#define SYSML_OPT_LAUNCH(K)                                                                       \
+  optimizer_kernel<K><<<blocks, 256, 0, st>>>(params, grads, state, n, d->lr, d->mu, d->rho, d->eps, \
+                                              d->beta1, d->beta2, (float)c1, (float)c2)
+  switch (d->kind) {
+    case SYSML_OPT_SGD: SYSML_OPT_LAUNCH(SYSML_OPT_SGD); break;
+    case SYSML_OPT_MOMENTUM: SYSML_OPT_LAUNCH(SYSML_OPT_MOMENTUM); break;
+    case SYSML_OPT_NESTEROV: SYSML_OPT_LAUNCH(SYSML_OPT_NESTEROV); break;
+    case SYSML_OPT_ADAGRAD: SYSML_OPT_LAUNCH(SYSML_OPT_ADAGRAD); break;
+    case SYSML_OPT_RMSPROP: SYSML_OPT_LAUNCH(SYSML_OPT_RMSPROP); break;
+    default: SYSML_OPT_LAUNCH(SYSML_OPT_ADAM); break;
+  }
+#undef SYSML_OPT_LAUNCH
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
+}
+
 sysml_status sysml_lenet_step(sysml_lenet *h, float *params, float *grads, const sysml_input *x,
                               const int32_t *labels, int32_t n_local, int64_t n_global,
                               float lr, void *nccl_comm, float *loss_sum, sysml_stream_t stream) {
@@ -880,6 +962,19 @@ sysml_status sysml_lenet_step(sysml_lenet *h, float *params, float *grads, const
     }
   }
   return sysml_sgd_update(params, grads, NUM_PARAMS, lr, stream);
+}
+
+sysml_status sysml_lenet_step_opt(sysml_lenet *h, float *params, float *grads, float *state,
+                                  const sysml_optimizer_desc *d, int64_t t, const sysml_input *x,
+                                  const int32_t *labels, int32_t n_local, int64_t n_global,
+                                  void *nccl_comm, float *loss_sum, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(h && d, "NULL argument to sysml_lenet_step_opt");
+  SYSML_CHECK_ARG(sysml_optimizer_state_floats(d->kind) >= 0, "unknown optimizer kind %d", d->kind);
+  h->ar_comm = nccl_comm;  // bucketed allreduce overlapped with the backward tail (may be NULL)
+  const sysml_status r = sysml_lenet_fwd_bwd(h, params, x, labels, n_local, n_global, grads, loss_sum, stream);
+  h->ar_comm = nullptr;
+  SYSML_TRY(r);
+  return sysml_optimizer_update(d, params, grads, state, NUM_PARAMS, t, stream);
 }
 
 sysml_status sysml_lenet_step_host(sysml_lenet *h, float *params, float *grads,

@@ -436,3 +436,51 @@ def test_lenet_step_nccl_bucketed_allreduce(S):
     finally:
         os.environ.pop("SYSML_AR_OVERLAP", None)
         dist.destroy_process_group()
+
+
+OPT_KINDS = ["sgd", "momentum", "nesterov", "adagrad", "rmsprop", "adam"]
+
+
+@pytest.mark.parametrize("kind", OPT_KINDS)
+def test_optimizer_update_vs_oracle(S, kind):
+    """sysml_optimizer_update (fp32) against oracle_optimizer_update (fp64), three steps from a
+    non-zero state, n ragged (not a multiple of the block), hyper-parameters off their defaults."""
+    rng = np.random.default_rng(20 + OPT_KINDS.index(kind))
+    n = 1000003
+    hp = dict(lr=0.013, mu=0.85, rho=0.95, eps=1e-6, beta1=0.8, beta2=0.99)
+    p = rng.normal(size=n)
+    nst = oracle.OPT_STATE[kind]
+    st = np.abs(rng.normal(size=nst * n)) if nst else np.zeros(0)
+    desc = S.optimizer_desc(kind, **hp)
+    assert S.lib().sysml_optimizer_state_floats(desc.kind) == nst
+    pd = dev(p)
+    sd = dev(st) if nst else None
+    p_ref, st_ref = p.astype(np.float32).astype(np.float64), st.astype(np.float32).astype(np.float64)
+    for t in range(1, 4):
+        g = rng.normal(size=n).astype(np.float32)
+        S.sysml_optimizer_update(desc, pd, dev(g), sd, t=t)
+        p_ref, st_ref = oracle.optimizer_update(kind, p_ref, g, st_ref if nst else np.zeros(0), t=t, **hp)
+    assert_close(host(pd), p_ref, 1e-5, f"{kind} params")
+    if nst:
+        assert_close(host(sd), st_ref, 1e-5, f"{kind} state")
+
+
+@pytest.mark.parametrize("kind", ["momentum", "adam"])
+def test_lenet_step_opt_vs_oracle_update(S, kind):
+    """sysml_lenet_step_opt = fwd_bwd + optimizer update: the parameters after the step equal
+    the oracle optimizer applied to the gradients of the same GPU fwd_bwd."""
+    n = 16
+    x, y, prm = _lenet_case(n, seed=930)
+    net = S.LeNet(n, math="tf32")
+    desc = S.optimizer_desc(kind, lr=0.02)
+    nst = oracle.OPT_STATE[kind]
+    g = torch.empty(83466, device="cuda")
+    net.fwd_bwd(dev(prm), dev(x), dev(y, torch.int32), 64, g)
+    g_h = host(g)
+    p = dev(prm)
+    st = torch.zeros(nst * 83466, device="cuda")
+    net.step_opt(p, torch.empty(83466, device="cuda"), st, desc, 1, dev(x), dev(y, torch.int32), 64)
+    p_ref, st_ref = oracle.optimizer_update(kind, prm.astype(np.float64), g_h, np.zeros(nst * 83466), t=1,
+                                            lr=0.02)
+    assert_close(host(p), p_ref, 1e-5, f"{kind} step params")
+    assert_close(host(st), st_ref, 1e-5, f"{kind} step state")
