@@ -484,3 +484,76 @@ def test_lenet_step_opt_vs_oracle_update(S, kind):
                                             lr=0.02)
     assert_close(host(p), p_ref, 1e-5, f"{kind} step params")
     assert_close(host(st), st_ref, 1e-5, f"{kind} step state")
+
+
+def test_lenet_full_batch_bench_config(S):
+    """BJ configs[4] at full size, in the launch configuration bench.py times (local batch 8192,
+    TF32): the 8192 images are 8 distinct images repeated 1024 times, so the oracle needs only
+    the 8 -- grads = 1024 x the 8-image oracle gradient sum, both scaled by 1/8192."""
+    k, rep = 8, 1024
+    x8, y8, prm = _lenet_case(k, dyadic=True, seed=960)  # TF32-exact: no argmax near-tie flips
+    g8, loss8 = oracle.lenet_fwd_bwd(x8, y8, prm, n_global=k * rep)
+    x = np.tile(x8, (rep, 1))
+    y = np.tile(y8, rep)
+    net = S.LeNet(k * rep, math="tf32")
+    grads = torch.empty(83466, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    net.fwd_bwd(dev(prm), dev(x), dev(y, torch.int32), k * rep, grads, loss)
+    g = host(grads)
+    offs = np.cumsum([0] + [int(np.prod(s)) for _, s in synth.LENET_PARAM_SHAPES])
+    for i, (name, _) in enumerate(synth.LENET_PARAM_SHAPES):
+        assert_close(g[offs[i]:offs[i + 1]], rep * g8[offs[i]:offs[i + 1]], TOL["tf32"], name + " @8192")
+    assert abs(host(loss)[0] - rep * loss8) <= 1e-4 * abs(rep * loss8)
+
+
+@pytest.mark.parametrize("layer", [(128, 256, 14, 14, 256, 3, 1), (128, 1024, 14, 14, 256, 1, 0)])
+def test_resnet_layer_full_size_sampled(S, layer):
+    """BJ configs[3] ResNet-style layers at full N = 128 (TF32): fwd and bwd_data checked on two
+    sampled images (the oracle per image), bwd_filter on 96 sampled (k, c, r, s) entries, each
+    the exact fp64 sum over all 128 images and P*Q positions."""
+    N, C, H, W, K, R, pd = layer
+    P = Q = H + 2 * pd - R + 1
+    x, f, b, dy = synth.conv_problem_U(N, C, H, W, K, R, R, P, Q, seed=(970,))
+    d = S.conv_desc(N, C, H, W, K, R, R, 1, pd, "tf32")
+    y = host(S.sysml_conv2d(dev(x), dev(f), d, bias=dev(b))).reshape(N, -1)
+    dx = host(S.sysml_conv2d_bwd_data(dev(f), dev(dy), d)).reshape(N, -1)
+    df, db = S.sysml_conv2d_bwd_filter(dev(x), dev(dy), d)
+    df, db = host(df).reshape(K, C, R, R), host(db)
+    for n in (0, N - 1):
+        yr = oracle.conv2d_fwd(x[n:n + 1], f, 1, C, H, W, K, R, R, (1, 1), (pd, pd), bias=b)
+        assert_close(y[n:n + 1], yr, TOL["tf32"], f"fwd image {n}")
+        dxr = oracle.conv2d_bwd_data(f, dy[n:n + 1], 1, C, H, W, K, R, R, (1, 1), (pd, pd))
+        assert_close(dx[n:n + 1], dxr, TOL["tf32"], f"bwd_data image {n}")
+    rng = np.random.default_rng(971)
+    X = np.pad(x.astype(np.float64).reshape(N, C, H, W), ((0, 0), (0, 0), (pd, pd), (pd, pd)))
+    DY = dy.astype(np.float64).reshape(N, K, P, Q)
+    idx = [(rng.integers(K), rng.integers(C), rng.integers(R), rng.integers(R)) for _ in range(96)]
+    ref = np.array([np.sum(DY[:, k] * X[:, c, r:r + P, s:s + Q]) for k, c, r, s in idx])
+    got = np.array([df[k, c, r, s] for k, c, r, s in idx])
+    assert_close(got, ref, TOL["tf32"], "bwd_filter sampled")
+    assert_close(db, DY.sum(axis=(0, 2, 3)), 1e-4, "db")
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+def test_csr_all_empty_matrix(S, math):
+    """Degenerate CSR input: nnz = 0 (every image empty) -> conv = bias, fused conv+pool =
+    relu(bias) with the first window position as argmax, bwd_filter = 0 (db still = sum dY)."""
+    N = 6
+    x = np.zeros((N, 784), np.float32)
+    m, _ = _csr_dev(S, x)
+    assert m.nnz == 0
+    f = synth.normal((32, 25), 0.2, seed=(980,))
+    b = synth.normal((32,), 0.1, seed=(981,))
+    d = S.conv_desc(N, 1, 28, 28, 32, 5, 5, 1, 2, math)
+    y = host(S.sysml_conv2d(m, dev(f), d, bias=dev(b)))
+    assert_close(y, np.repeat(b.astype(np.float64), 784)[None, :].repeat(N, 0), TOL[math], "empty csr fwd")
+    dy = synth.normal((N, 32 * 784), seed=(982,))
+    df, db = S.sysml_conv2d_bwd_filter(m, dev(dy), d)
+    assert not np.any(host(df))
+    assert_close(host(db), dy.astype(np.float64).reshape(N, 32, 784).sum(axis=(0, 2)), 1e-4, "empty csr db")
+    pd = S.pool_desc(N, 32, 28, 28, 2, 2, 2, 0, True)
+    out, arg = S.sysml_conv2d_bias_relu_maxpool(m, dev(f), dev(b), d, pd)
+    z = np.repeat(b.astype(np.float64), 784)[None, :].repeat(N, 0)
+    oref, aref = oracle.relu_maxpool(z, N, 32, 28, 28, 2, 2, (2, 2), (0, 0))
+    assert_close(host(out), oref, TOL[math], "empty csr fused")
+    assert np.array_equal(host(arg), aref)
