@@ -266,6 +266,20 @@ SYSML_API sysml_status sysml_lenet_step_host(sysml_lenet *h, float *params, floa
                                    int32_t n_local, int64_t n_global, float lr, void *nccl_comm,
                                    float *loss_host, sysml_stream_t stream);
 
+/* Pipelined variant of sysml_lenet_step_host for a training loop over host batches: the
+ * step on (x_host, labels_host) runs while the NEXT batch (x_host_next, labels_host_next,
+ * n_next; NULL = none) is copied host->device on the handle's copy stream into its second
+ * input buffer.  A call whose batch is the one the previous call prefetched (same host
+ * pointers and size) only waits for that copy; otherwise it copies now.  The next batch's
+ * host memory (pinned for overlap) must stay unchanged until the following call.  Every
+ * call performs one batch H2D and reads the loss back; synchronizes `stream` on return.  */
+SYSML_API sysml_status sysml_lenet_step_host_pipelined(sysml_lenet *h, float *params, float *grads,
+                                             const float *x_host, const int32_t *labels_host,
+                                             int32_t n_local, const float *x_host_next,
+                                             const int32_t *labels_host_next, int32_t n_next,
+                                             int64_t n_global, float lr, void *nccl_comm,
+                                             float *loss_host, sysml_stream_t stream);
+
 /* Per-stage device timing of the step (bench instrumentation).  When enabled,
  * fwd_bwd records CUDA events around each stage on `stream`; get_timing returns
  * accumulated milliseconds, launch counts and stage names (stage i < *n_stages),

@@ -44,6 +44,7 @@ EXPORTS = (
     "sysml_sgd_update", "sysml_lenet_step", "sysml_lenet_step_host",
     "sysml_lenet_set_timing", "sysml_lenet_get_timing",
     "sysml_optimizer_state_floats", "sysml_optimizer_update", "sysml_lenet_step_opt",
+    "sysml_lenet_step_host_pipelined",
 )
 
 
@@ -172,6 +173,8 @@ def lib(build_if_missing: bool = False):
         "sysml_lenet_step_host": (c_i32, [vp, vp, vp, vp, vp, c_i32, c_i64, ctypes.c_float, vp, vp, vp]),
         "sysml_lenet_set_timing": (c_i32, [vp, c_i32]),
         "sysml_optimizer_state_floats": (c_i32, [c_i32]),
+        "sysml_lenet_step_host_pipelined": (c_i32, [vp, vp, vp, vp, vp, c_i32, vp, vp, c_i32, c_i64,
+                                                    ctypes.c_float, vp, vp, vp]),
         "sysml_optimizer_update": (c_i32, [ctypes.POINTER(OptimizerDesc), vp, vp, vp, c_i64, c_i64, vp]),
         "sysml_lenet_step_opt": (c_i32, [vp, vp, vp, vp, ctypes.POINTER(OptimizerDesc), c_i64, IN, vp, c_i32,
                                          c_i64, vp, vp, vp]),
@@ -444,6 +447,28 @@ class LeNet:
                                            int(x_host.shape[0]), int(n_global), ctypes.c_float(lr),
                                            ctypes.c_void_p(nccl_comm) if nccl_comm else None,
                                            ctypes.byref(loss), _stream(stream)))
+        return loss.value
+
+    def step_host_pipelined(self, params, grads, x_host, labels_host, n_global, next_x=None, next_labels=None,
+                            lr=0.01, nccl_comm=None, stream=None) -> float:
+        """step_host for a loop over host batches: the next batch (pinned, unchanged until the
+        next call) is copied to the device while this step computes
+        (sysml_lenet_step_host_pipelined)."""
+        torch = _torch()
+        loss = ctypes.c_float(0.0)
+        for t in (x_host, labels_host) + ((next_x, next_labels) if next_x is not None else ()):
+            if t.is_cuda:
+                raise TypeError("step_host_pipelined takes CPU (pinned) tensors")
+        if x_host.dtype != torch.float32 or labels_host.dtype != torch.int32:
+            raise TypeError("step_host_pipelined takes float32 / int32 CPU tensors")
+        nxt = next_x is not None
+        _check(lib().sysml_lenet_step_host_pipelined(
+            self.h, _ptr(params, torch.float32), _ptr(grads, torch.float32),
+            ctypes.c_void_p(x_host.data_ptr()), ctypes.c_void_p(labels_host.data_ptr()), int(x_host.shape[0]),
+            ctypes.c_void_p(next_x.data_ptr()) if nxt else None,
+            ctypes.c_void_p(next_labels.data_ptr()) if nxt else None, int(next_x.shape[0]) if nxt else 0,
+            int(n_global), ctypes.c_float(lr), ctypes.c_void_p(nccl_comm) if nccl_comm else None,
+            ctypes.byref(loss), _stream(stream)))
         return loss.value
 
     def set_timing(self, enable: bool):

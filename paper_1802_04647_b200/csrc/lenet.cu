@@ -473,6 +473,14 @@ struct sysml_lenet {
   // host-input path buffers
   float *x_dev = nullptr, *loss_dev = nullptr;
   int32_t *lab_dev = nullptr;
+  // pipelined host input (sysml_lenet_step_host_pipelined): a second input buffer filled on
+  // copy_stream while the current step computes; slot 0 = x_dev / lab_dev, slot 1 = below
+  float *x_dev2 = nullptr;
+  int32_t *lab_dev2 = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+  const void *pf_x = nullptr, *pf_lab = nullptr;  // host batch prefetched into slot pf_slot
+  int pf_slot = -1, pf_n = 0;
   // timing
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool, pending[NSTAGES];
@@ -589,6 +597,18 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
   ALLOC(h->loss_dev, 1);
   ALLOC(h->lab_dev, b);
   if (!h->csr) ALLOC(h->x_dev, b * 784);
+  if (!h->csr) {
+    ALLOC(h->x_dev2, b * 784);
+    ALLOC(h->lab_dev2, b);
+    if (cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_copied[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_copied[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_consumed[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_consumed[1], cudaEventDisableTiming) != cudaSuccess) {
+      set_error("creating the input copy stream / events failed");
+      return fail(SYSML_ERR_CUDA);
+    }
+  }
   // workspace: max over the conv calls of the step
   size_t need = 0, w = 0;
   const sysml_conv_desc c1 = conv1_desc(max_local_batch, math), c2 = conv2_desc(max_local_batch, math);
@@ -670,6 +690,12 @@ sysml_status sysml_lenet_destroy(sysml_lenet *h) {
   cudaFree(h->c1); cudaFree(h->c2); cudaFree(h->db2part);
   cudaFree(h->lossn); cudaFree(h->da2); cudaFree(h->dz2); cudaFree(h->da1); cudaFree(h->dz1);
   cudaFree(h->part3); cudaFree(h->loss_dev); cudaFree(h->lab_dev); cudaFree(h->x_dev);
+  cudaFree(h->x_dev2); cudaFree(h->lab_dev2);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
+    if (h->ev_consumed[i]) cudaEventDestroy(h->ev_consumed[i]);
+  }
   cudaFree(h->ws);
   cudaFree(h->a1s); cudaFree(h->dz2s);
   for (auto &e : h->pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -985,6 +1011,11 @@ sysml_status sysml_lenet_step_host(sysml_lenet *h, float *params, float *grads,
   SYSML_CHECK_ARG(!h->csr, "sysml_lenet_step_host takes dense host input (handle is CSR)");
   SYSML_CHECK_ARG(n_local >= 1 && n_local <= h->max_b, "n_local %d out of range", n_local);
   cudaStream_t st = (cudaStream_t)stream;
+  if (h->copy_stream) {  // a pipelined prefetch may still target slot 0: let it land first
+    SYSML_CUDA(cudaStreamWaitEvent(st, h->ev_copied[0], 0));
+    SYSML_CUDA(cudaStreamWaitEvent(st, h->ev_copied[1], 0));
+    h->pf_slot = -1;
+  }
   SYSML_CUDA(cudaMemcpyAsync(h->x_dev, x_host, sizeof(float) * (size_t)n_local * 784,
                              cudaMemcpyHostToDevice, st));
   SYSML_CUDA(cudaMemcpyAsync(h->lab_dev, labels_host, sizeof(int32_t) * (size_t)n_local,
@@ -992,6 +1023,58 @@ sysml_status sysml_lenet_step_host(sysml_lenet *h, float *params, float *grads,
   sysml_input xin{0, h->x_dev, {}};
   SYSML_TRY(sysml_lenet_step(h, params, grads, &xin, h->lab_dev, n_local, n_global, lr, nccl_comm,
                              h->loss_dev, stream));
+  SYSML_CUDA(cudaMemcpyAsync(loss_host, h->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
+  SYSML_CUDA(cudaStreamSynchronize(st));
+  return SYSML_OK;
+}
+
+sysml_status sysml_lenet_step_host_pipelined(sysml_lenet *h, float *params, float *grads,
+                                             const float *x_host, const int32_t *labels_host,
+                                             int32_t n_local, const float *x_host_next,
+                                             const int32_t *labels_host_next, int32_t n_next,
+                                             int64_t n_global, float lr, void *nccl_comm,
+                                             float *loss_host, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(h && x_host && labels_host && loss_host, "NULL argument to sysml_lenet_step_host_pipelined");
+  SYSML_CHECK_ARG(!h->csr, "sysml_lenet_step_host_pipelined takes dense host input (handle is CSR)");
+  SYSML_CHECK_ARG(n_local >= 1 && n_local <= h->max_b, "n_local %d out of range", n_local);
+  SYSML_CHECK_ARG(!x_host_next || (labels_host_next && n_next >= 1 && n_next <= h->max_b),
+                  "next batch: labels NULL or n_next %d out of range", n_next);
+  cudaStream_t st = (cudaStream_t)stream;
+  float *xs[2] = {h->x_dev, h->x_dev2};
+  int32_t *ls[2] = {h->lab_dev, h->lab_dev2};
+  int slot;
+  if (h->pf_slot >= 0 && h->pf_x == x_host && h->pf_lab == labels_host && h->pf_n == n_local) {
+    slot = h->pf_slot;  // prefetched by the previous call: wait for its copy only
+  } else {
+    slot = h->pf_slot >= 0 ? 1 - h->pf_slot : 0;  // miss: copy now on the copy stream
+    SYSML_CUDA(cudaStreamWaitEvent(h->copy_stream, h->ev_consumed[slot], 0));
+    SYSML_CUDA(cudaMemcpyAsync(xs[slot], x_host, sizeof(float) * (size_t)n_local * 784,
+                               cudaMemcpyHostToDevice, h->copy_stream));
+    SYSML_CUDA(cudaMemcpyAsync(ls[slot], labels_host, sizeof(int32_t) * (size_t)n_local,
+                               cudaMemcpyHostToDevice, h->copy_stream));
+    SYSML_CUDA(cudaEventRecord(h->ev_copied[slot], h->copy_stream));
+  }
+  SYSML_CUDA(cudaStreamWaitEvent(st, h->ev_copied[slot], 0));
+  h->pf_slot = -1;
+  if (x_host_next) {
+    // the next batch goes to the other slot once the step that last read it is done; the
+    // copy overlaps this step's kernels.  The host buffers must stay unchanged until then.
+    const int ns = 1 - slot;
+    SYSML_CUDA(cudaStreamWaitEvent(h->copy_stream, h->ev_consumed[ns], 0));
+    SYSML_CUDA(cudaMemcpyAsync(xs[ns], x_host_next, sizeof(float) * (size_t)n_next * 784,
+                               cudaMemcpyHostToDevice, h->copy_stream));
+    SYSML_CUDA(cudaMemcpyAsync(ls[ns], labels_host_next, sizeof(int32_t) * (size_t)n_next,
+                               cudaMemcpyHostToDevice, h->copy_stream));
+    SYSML_CUDA(cudaEventRecord(h->ev_copied[ns], h->copy_stream));
+    h->pf_slot = ns;
+    h->pf_x = x_host_next;
+    h->pf_lab = labels_host_next;
+    h->pf_n = n_next;
+  }
+  sysml_input xin{0, xs[slot], {}};
+  SYSML_TRY(sysml_lenet_step(h, params, grads, &xin, ls[slot], n_local, n_global, lr, nccl_comm,
+                             h->loss_dev, stream));
+  SYSML_CUDA(cudaEventRecord(h->ev_consumed[slot], st));
   SYSML_CUDA(cudaMemcpyAsync(loss_host, h->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
   SYSML_CUDA(cudaStreamSynchronize(st));
   return SYSML_OK;

@@ -557,3 +557,31 @@ def test_csr_all_empty_matrix(S, math):
     oref, aref = oracle.relu_maxpool(z, N, 32, 28, 28, 2, 2, (2, 2), (0, 0))
     assert_close(host(out), oref, TOL[math], "empty csr fused")
     assert np.array_equal(host(arg), aref)
+
+
+def test_lenet_step_host_pipelined_matches_step_host(S):
+    """The pipelined host-input step (next batch copied while this step computes) gives bitwise
+    the same parameters and losses as the plain host step, over rotating batches and with a
+    prefetch miss (a batch other than the one prefetched)."""
+    n = 32
+    batches = []
+    for k in range(3):
+        x, y, prm = _lenet_case(n, seed=990 + 10 * k)
+        batches.append((torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory()))
+    prm = _lenet_case(n, seed=990)[2]
+    order = [0, 1, 2, 0]  # step 3 runs batch 0 while batch 2 was... prefetched as the next of step 2
+    net = S.LeNet(n, math="tf32")
+    p1, g1 = dev(prm), torch.empty(83466, device="cuda")
+    l1 = [net.step_host(p1, g1, batches[b][0], batches[b][1], n) for b in order]
+    net2 = S.LeNet(n, math="tf32")
+    p2, g2 = dev(prm), torch.empty(83466, device="cuda")
+    l2 = []
+    for i, b in enumerate(order):
+        nb = order[i + 1] if i + 1 < len(order) else None
+        if i == 2:
+            nb = 1  # prefetch a batch the next call does not use -> a miss at step 3
+        l2.append(net2.step_host_pipelined(p2, g2, batches[b][0], batches[b][1], n,
+                                           next_x=batches[nb][0] if nb is not None else None,
+                                           next_labels=batches[nb][1] if nb is not None else None))
+    assert l1 == l2
+    assert host(p1).tobytes() == host(p2).tobytes()
