@@ -170,8 +170,14 @@ __device__ __forceinline__ void epi_plain(const TcFwdParams &p, uint32_t tbase, 
     bool valid = g < p.G;
     int64_t ybase = 0;
     if (valid) {
-      const int n = (int)(g / p.Lf);
-      const int rem = (int)(g - (int64_t)n * p.Lf);
+      int n, rem;
+      if (p.G < (1ll << 31)) {  // 32-bit position arithmetic (the common case)
+        n = (int)((uint32_t)g / (uint32_t)p.Lf);
+        rem = (int)((uint32_t)g - (uint32_t)n * (uint32_t)p.Lf);
+      } else {
+        n = (int)(g / p.Lf);
+        rem = (int)(g - (int64_t)n * p.Lf);
+      }
       const int hh = rem / p.Wf, q = rem - hh * p.Wf;
       valid = hh < p.P && q < p.Q;
       ybase = (int64_t)n * p.K * PQ + (int64_t)hh * p.Q + q;
@@ -574,6 +580,39 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       for (int i = lane; i < 2 * p.HALO; i += 32) st_shared_v4(a0 + i * 16, 0.f, 0.f, 0.f, 0.f);
       __syncwarp();
       float *Af = reinterpret_cast<float *>(A);
+      if (nimg <= 31) {
+        // the overlapping images' non-zeros are one contiguous CSR range: 4 (col, val)
+        // pairs per lane in flight, each entry's image from the row pointers (uniform loop)
+        const int jA = __shfl_sync(0xffffffffu, rp, 0), jB = __shfl_sync(0xffffffffu, rp, nimg);
+        for (int base = jA; base < jB; base += 128) {
+          int col[4], img[4];
+          float val[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int jj = base + u * 32 + lane;
+            const bool ok = jj < jB;
+            col[u] = ok ? __ldg(p.csr.col_idx + jj) : -1;
+            val[u] = ok ? __ldg(p.csr.val + jj) : 0.f;
+            img[u] = 0;
+          }
+          for (int ii = 1; ii < nimg; ++ii) {
+            const int b = __shfl_sync(0xffffffffu, rp, ii);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) img[u] += (base + u * 32 + lane >= b) ? 1 : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (col[u] < 0 || col[u] >= HW) continue;
+            const int h = col[u] / p.W, w = col[u] - h * p.W;
+            const int64_t gi = (int64_t)(n_lo + img[u]) * p.Lf + (int64_t)(h + p.ph) * p.Wf + (w + p.pw);
+            for (int s_ = 0; s_ < p.S; ++s_) {
+              const int64_t pos = gi - g0 - s_;
+              if (pos >= 0 && pos < p.HALO)
+                atomicAdd(Af + (s_ >> 2) * p.HALO * 4 + pos * 4 + (s_ & 3), val[u]);  // duplicates summed
+            }
+          }
+        }
+      } else
       for (int ii = 0; ii < nimg; ++ii) {
         const int n = n_lo + ii;
         int j0 = __shfl_sync(0xffffffffu, rp, ii & 31), j1 = __shfl_sync(0xffffffffu, rp, (ii + 1) & 31);
