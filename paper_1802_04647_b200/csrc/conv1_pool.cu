@@ -53,6 +53,35 @@ __device__ __forceinline__ void st_shared_v4c1(uint32_t addr) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "f"(0.f) : "memory");
 }
 
+// One 16-channel group of the pooled epilogue (kept small: the argmax variant is a
+// template, not a branch in the unrolled loop, so the executing loop stays compact)
+template <bool PARG>
+__device__ __forceinline__ void c1p_group(const C1pParams &p, const uint32_t (&v00)[16], const uint32_t (&v01)[16],
+                                          const uint32_t (&v10)[16], const uint32_t (&v11)[16],
+                                          const float *bias_s, int k0, bool wok, float *poutp, int64_t vstride,
+                                          int32_t *pargp, int PpQp, int argbase, int PQ, uint64_t &code) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float b = bias_s[k0 + j];
+    // relu (+0.0 for non-positive, R7) then the strict-'>' scan in r-outer / s-inner
+    // order (R5): non-negative floats compare as unsigned integers
+    const float z0 = __uint_as_float(v00[j]) + b, z1 = __uint_as_float(v01[j]) + b;
+    const float z2 = __uint_as_float(v10[j]) + b, z3 = __uint_as_float(v11[j]) + b;
+    uint32_t best = __float_as_uint(z0 > 0.f ? z0 : 0.f), c = 0;
+    const uint32_t u1 = __float_as_uint(z1 > 0.f ? z1 : 0.f);
+    const uint32_t u2 = __float_as_uint(z2 > 0.f ? z2 : 0.f);
+    const uint32_t u3 = __float_as_uint(z3 > 0.f ? z3 : 0.f);
+    if (u1 > best) { best = u1; c = 1; }
+    if (u2 > best) { best = u2; c = 2; }
+    if (u3 > best) { best = u3; c = 3; }
+    if (wok && k0 + j < p.K) {
+      poutp[(int64_t)j * vstride] = __uint_as_float(best);
+      if (PARG) pargp[(int64_t)j * PpQp] = argbase + j * PQ + (int)(c >> 1) * p.Q + (int)(c & 1);
+    }
+    code |= (uint64_t)(((best != 0u) ? 4u : 0u) | c) << (4 * j);
+  }
+}
+
 __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t *Bs = smem;                                // R taps x [quad][NN][4]
@@ -272,29 +301,12 @@ __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pPar
         ptx::tmem_ld_wait(v10);
         ptx::tmem_ld_wait(v11);
         uint64_t code = 0;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float b = bias_s[k0 + j];
-          // relu (+0.0 for non-positive, R7) then the strict-'>' scan in r-outer / s-inner
-          // order (R5): non-negative floats compare as unsigned integers
-          const float z0 = __uint_as_float(v00[j]) + b, z1 = __uint_as_float(v01[j]) + b;
-          const float z2 = __uint_as_float(v10[j]) + b, z3 = __uint_as_float(v11[j]) + b;
-          uint32_t best = __float_as_uint(z0 > 0.f ? z0 : 0.f), c = 0;
-          const uint32_t u1 = __float_as_uint(z1 > 0.f ? z1 : 0.f);
-          const uint32_t u2 = __float_as_uint(z2 > 0.f ? z2 : 0.f);
-          const uint32_t u3 = __float_as_uint(z3 > 0.f ? z3 : 0.f);
-          if (u1 > best) { best = u1; c = 1; }
-          if (u2 > best) { best = u2; c = 2; }
-          if (u3 > best) { best = u3; c = 3; }
-          const int k = k0 + j;
-          if (wok && k < p.K) {
-            p.pout[vbase + (int64_t)k * vstride] = __uint_as_float(best);
-            if (p.parg)
-              p.parg[(int64_t)n * p.K * PpQp + (int64_t)k * PpQp + pp * p.Qp + pc] =
-                  k * PQ + idx_tl + (int)(c >> 1) * p.Q + (int)(c & 1);
-          }
-          code |= (uint64_t)(((best != 0u) ? 4u : 0u) | c) << (4 * j);
-        }
+        float *poutp = p.pout + vbase + (int64_t)k0 * vstride;
+        if (p.parg)
+          c1p_group<true>(p, v00, v01, v10, v11, bias_s, k0, wok, poutp, vstride,
+                          p.parg + ((int64_t)n * p.K + k0) * PpQp + pp * p.Qp + pc, PpQp, k0 * PQ + idx_tl, PQ, code);
+        else
+          c1p_group<false>(p, v00, v01, v10, v11, bias_s, k0, wok, poutp, vstride, nullptr, PpQp, 0, PQ, code);
         if (p.pcode && wok) p.pcode[(int64_t)(k0 >> 4) * p.code_plane + w] = code;
       }
       ptx::tc_fence_before();
