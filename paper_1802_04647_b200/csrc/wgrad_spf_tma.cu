@@ -27,8 +27,9 @@ namespace sysml {
 namespace {
 
 constexpr int W2_MAXS = 8;  // column taps (plan: S <= 8)
-constexpr int W2_NA = 4;          // A ring (dY atoms)
-constexpr int W2_THREADS = 224;  // + warp 6: B (X atom) producer
+constexpr int W2_NA = 6;          // A ring (dY atoms)
+constexpr int W2_THREADS = 352;  // warps 0 A producer, 1 MMA, 2-5 + 7-10 helpers, 6 B producer
+constexpr int W2_HELP_WARPS = 8;
 constexpr int W2_ATOM = 32;       // positions per atom (128-byte swizzled row)
 
 struct W2Params {
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       ptx::mbar_init(emptyA + i, do_db ? 2 : 1);
     }
     for (int i = 0; i < p.nbr; ++i) {
-      ptx::mbar_init(fullB + i, 4);   // the 4 helper warps (after they saw the TMA part)
+      ptx::mbar_init(fullB + i, W2_HELP_WARPS);  // the helper warps (after they saw the TMA part)
       ptx::mbar_init(fullBt + i, 1);  // expect_tx
       ptx::mbar_init(emptyB + i, 1);
     }
@@ -205,7 +206,9 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
     if (ptx::elect_one()) ptx::mma_commit(accf);
     __syncwarp();
   } else {
-    const int et = threadIdx.x - 64;  // 0..127
+    // helpers: warps 2-5 (et 0..127: also db and the epilogue) and 7-10 (et 128..255)
+    const bool main_helper = warp <= 5;
+    const int et = main_helper ? (int)threadIdx.x - 64 : 128 + (int)threadIdx.x - 224;
     const int qd = warp & 3;
     // Merged loop in the producer's order: (1) the B rows of column taps s % 4 != 0 of
     // atom bi -- X[c][g + s] from two aligned float4 loads, shifted in registers, stored
@@ -235,10 +238,10 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         const uint8_t *B0 = Bring + slot * b_slot, *B1 = Bring + slot1 * b_slot;
         const uint32_t Bs = sB + slot * b_slot;
         // all six 16-byte loads of this thread's (up to) three tasks first, then the shifts
-        float4 v0[3], v1[3];
+        float4 v0[2], v1[2];
 #pragma unroll
-        for (int u = 0; u < 3; ++u) {
-          const int t = et + u * 128;
+        for (int u = 0; u < 2; ++u) {
+          const int t = et + u * 256;
           if (t < ntask) {
             const int c = t >> 3, q = t & 7;
             v0[u] = *reinterpret_cast<const float4 *>(B0 + c * 128 + ((q ^ (c & 7)) << 4));
@@ -247,8 +250,8 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           }
         }
 #pragma unroll
-        for (int u = 0; u < 3; ++u) {
-          const int t = et + u * 128;
+        for (int u = 0; u < 2; ++u) {
+          const int t = et + u * 256;
           if (t >= ntask) continue;
           const int c = t >> 3, q = t & 7;
           const float e[8] = {v0[u].x, v0[u].y, v0[u].z, v0[u].w, v1[u].x, v1[u].y, v1[u].z, v1[u].w};
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(fullB + slot);
       }
-      if (step >= 0 && do_db) {
+      if (step >= 0 && do_db && main_helper) {
         const int slotA = sa;
         const long long t0 = clock64();
         ptx::mbar_wait(fullA + slotA, pa);
@@ -286,11 +289,12 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         if (et == 0) ptx::mbar_arrive(emptyA + slotA);
       }
     }
-    if (do_db) {
+    if (do_db && main_helper) {
       if (dsplit) dbv += __shfl_xor_sync(0xffffffffu, dbv, 1);
       if ((!dsplit || (et & 1) == 0) && drow < p.Kc && k0 + drow < p.K)
         p.dbpart[(int64_t)z * p.K + k0 + drow] = dbv;
     }
+    if (main_helper) {
     if (nA > 0) ptx::mbar_wait_sleep(accf, 0);
     ptx::tc_fence_after();
     const int row = qd * 32 + lane;
@@ -310,6 +314,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         o[2] = make_float4(v[8], v[9], v[10], v[11]);
         o[3] = make_float4(v[12], v[13], v[14], v[15]);
       }
+    }
   }
   if (p.clk && threadIdx.x == 32) p.clk[blockIdx.x * 8 + 6] = clock64() - tk0;
   if (p.clk && threadIdx.x == 64) p.clk[blockIdx.x * 8 + 7] = clock64() - tk0;
