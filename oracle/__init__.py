@@ -60,6 +60,9 @@ def lib():
         _lib.oracle_lenet_fwd_bwd.argtypes = [i64, i64, dp, ip, dp, dp, dp]
         _lib.oracle_sgd_update.argtypes = [i64, dp, dp, ctypes.c_double]
         _lib.oracle_optimizer_update.argtypes = [i64, i64, dp, dp, dp] + [ctypes.c_double] * 6 + [i64]
+        _lib.oracle_conv2d_fwd_csr_filter.argtypes = [i64] * 11 + [dp, ip, ip, dp, dp, dp]
+        _lib.oracle_count_nonzeros.restype = i64
+        _lib.oracle_count_nonzeros.argtypes = [i64, dp]
     return _lib
 
 
@@ -183,6 +186,31 @@ def optimizer_update(kind, params, grads, state, t=1, lr=0.01, mu=0.9, rho=0.99,
     lib().oracle_optimizer_update(OPTIMIZERS[kind], p.size, _p(p), _p(g), _p(st), lr, mu, rho, eps,
                                   beta1, beta2, int(t))
     return p, (st if OPT_STATE[kind] else np.zeros(0))
+
+
+def conv2d_fwd_csr_filter(x, f_row_ptr, f_col_idx, f_val, N, C, H, W, K, R, S, stride=(1, 1), pad=(0, 0),
+                          bias=None):
+    """Dense input / sparse (CSR, K x C*R*S) filter convolution."""
+    P = out_extent(H, pad[0], R, stride[0])
+    Q = out_extent(W, pad[1], S, stride[1])
+    x = _d(x)
+    y = np.empty((N, K * P * Q), dtype=np.float64)
+    b = None if bias is None else _d(bias)
+    rp, ci, v = _i(f_row_ptr), _i(f_col_idx), _d(f_val)  # kept alive across the call
+    assert rp.size == K + 1
+    lib().oracle_conv2d_fwd_csr_filter(N, C, H, W, K, R, S, stride[0], stride[1], pad[0], pad[1], _p(x),
+                                       _p(rp), _p(ci), _p(v), _p(b), _p(y))
+    return y
+
+
+SPARSITY_THRESHOLD = 0.4  # S:88-92 design decision (the paper gives no threshold)
+
+
+def decide_format(a, threshold=SPARSITY_THRESHOLD):
+    """'sparse' iff nnz / (rows * cols) <= threshold, else 'dense'."""
+    a = _d(a)
+    nnz = lib().oracle_count_nonzeros(a.size, _p(a))
+    return ("sparse" if a.size and nnz / a.size <= threshold else "dense"), int(nnz)
 
 
 def sgd_update(params, grads, lr=0.01):

@@ -385,3 +385,50 @@ EXPORT void oracle_optimizer_update(int64_t kind, int64_t n, double *p, const do
     }
   }
 }
+
+/* Dense input / sparse filter convolution (the third of the four physical
+ * convolution operators): the filter bank is CSR with K rows and C*R*S columns
+ * (column (c*R + r)*S + s, the row-major index of S:100), and only its stored non-zeros
+ * contribute: y[n,k,p,q] = b[k] + sum over stored (col, v) of row k of
+ *                          v * x(n, c, p*sh - ph + r, q*sw - pw + s)   (0 outside).
+ * Duplicate columns of a row are summed (reading R15).  Sparse input / sparse filter is
+ * this with x densified (oracle_csr_densify).                                         */
+EXPORT void oracle_conv2d_fwd_csr_filter(int64_t N, int64_t C, int64_t H, int64_t W, int64_t K,
+                                         int64_t R, int64_t S, int64_t sh, int64_t sw, int64_t ph,
+                                         int64_t pw, const double *x, const int32_t *f_row_ptr,
+                                         const int32_t *f_col_idx, const double *f_val,
+                                         const double *bias, double *y) {
+  const int64_t P = out_extent(H, ph, R, sh), Q = out_extent(W, pw, S, sw);
+  const int64_t CHW = C * H * W, KPQ = K * P * Q;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t n = 0; n < N; ++n) {
+    for (int64_t k = 0; k < K; ++k) {
+      double *plane = y + n * KPQ + k * P * Q;
+      const double b0 = bias ? bias[k] : 0.0;
+      for (int64_t i = 0; i < P * Q; ++i) plane[i] = b0;
+      for (int64_t j = f_row_ptr[k]; j < f_row_ptr[k + 1]; ++j) {
+        const int64_t col = f_col_idx[j];
+        const int64_t c = col / (R * S), r = (col / S) % R, s = col % S;
+        const double v = f_val[j];
+        for (int64_t p = 0; p < P; ++p) {
+          const int64_t h = p * sh - ph + r;
+          if (h < 0 || h >= H) continue;
+          for (int64_t q = 0; q < Q; ++q) {
+            const int64_t w = q * sw - pw + s;
+            if (w < 0 || w >= W) continue;
+            plane[p * Q + q] += v * x[n * CHW + (c * H + h) * W + w];
+          }
+        }
+      }
+    }
+  }
+}
+
+/* decide_format ("decides upon dense or sparse formats"): a matrix is
+ * stored sparse iff nnz / (rows * cols) <= threshold (0.4 by default, S's design decision).
+ * Returns the number of non-zeros (exact zeros, +0.0 and -0.0, are not stored).          */
+EXPORT int64_t oracle_count_nonzeros(int64_t n, const double *a) {
+  int64_t nnz = 0;
+  for (int64_t i = 0; i < n; ++i) nnz += a[i] != 0.0;
+  return nnz;
+}
