@@ -183,6 +183,29 @@ SYSML_API sysml_status sysml_conv2d_bias_relu_maxpool(const sysml_conv_desc *cd,
  * `stream`; *violations receives the number of offending rows (0 = valid).       */
 SYSML_API sysml_status sysml_csr_check(const sysml_csr *m, int64_t *violations, sysml_stream_t stream);
 
+/* Sparse-filter convolution: the third and fourth of the paper's physical convolution
+ * operators ("dense input / sparse filter and sparse input / sparse filter").
+ * f: the filter bank as CSR, f->rows = K, f->cols = C*R*S, column (c*R + r)*S + s;
+ * only stored entries contribute, duplicate columns are summed (R15).  x: dense
+ * N x (C*H*W) or CSR (then C*H*W <= 49152: each image is densified in shared memory).
+ * y (device, N x (K*P*Q)) = conv2d(x, densify(f)) (+ bias[K] if non-NULL), fp32, each
+ * output summed in the filter's stored order (deterministic).  Errors: SYSML_ERR_SHAPE
+ * for mismatched extents, SYSML_ERR_UNSUPPORTED for a CSR image larger than the limit.  */
+SYSML_API sysml_status sysml_conv2d_csr_filter(const sysml_conv_desc *d, const sysml_input *x,
+                                               const sysml_csr *f, const float *bias, float *y,
+                                               sysml_stream_t stream);
+
+/* Format decision ("decides upon dense or sparse formats"): a matrix
+ * is stored sparse iff nnz / (rows*cols) <= 0.4.  sysml_count_nonzeros counts the entries
+ * != 0 (+0.0 and -0.0 are not stored) of x[0, n) and synchronizes `stream`.
+ * sysml_dense_to_csr encodes the dense rows x cols matrix x as CSR: row_ptr int32[rows+1],
+ * col_idx int32 / val fp32 [nnz] (sized by sysml_count_nonzeros), columns ascending per row
+ * (deterministic); rows*cols < 2^31.  Caller-owned device buffers.                      */
+SYSML_API sysml_status sysml_count_nonzeros(const float *x, int64_t n, int64_t *nnz_host,
+                                            sysml_stream_t stream);
+SYSML_API sysml_status sysml_dense_to_csr(const float *x, int64_t rows, int64_t cols, int32_t *row_ptr,
+                                          int32_t *col_idx, float *val, sysml_stream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* Minibatch SGD-step driver (Listing 1: batch -> forward -> backward ->
  * sgd::update, lr = 0.01; P:142 LeNet; P:187-192 data-parallel plan).

@@ -45,6 +45,7 @@ EXPORTS = (
     "sysml_lenet_set_timing", "sysml_lenet_get_timing",
     "sysml_optimizer_state_floats", "sysml_optimizer_update", "sysml_lenet_step_opt",
     "sysml_lenet_step_host_pipelined",
+    "sysml_conv2d_csr_filter", "sysml_count_nonzeros", "sysml_dense_to_csr",
 )
 
 
@@ -173,6 +174,9 @@ def lib(build_if_missing: bool = False):
         "sysml_lenet_step_host": (c_i32, [vp, vp, vp, vp, vp, c_i32, c_i64, ctypes.c_float, vp, vp, vp]),
         "sysml_lenet_set_timing": (c_i32, [vp, c_i32]),
         "sysml_optimizer_state_floats": (c_i32, [c_i32]),
+        "sysml_conv2d_csr_filter": (c_i32, [CD, IN, CS, vp, vp, vp]),
+        "sysml_count_nonzeros": (c_i32, [vp, c_i64, ctypes.POINTER(c_i64), vp]),
+        "sysml_dense_to_csr": (c_i32, [vp, c_i64, c_i64, vp, vp, vp, vp]),
         "sysml_lenet_step_host_pipelined": (c_i32, [vp, vp, vp, vp, vp, c_i32, vp, vp, c_i32, c_i64,
                                                     ctypes.c_float, vp, vp, vp]),
         "sysml_optimizer_update": (c_i32, [ctypes.POINTER(OptimizerDesc), vp, vp, vp, c_i64, c_i64, vp]),
@@ -350,6 +354,54 @@ def sysml_sgd_update(params, grads, lr=0.01, stream=None):
     _check(lib().sysml_sgd_update(_ptr(params, torch.float32, "params"), _ptr(grads, torch.float32, "grads"),
                                   params.numel(), ctypes.c_float(lr), _stream(stream)))
     return params
+
+
+def _csr_struct(m):
+    torch = _torch()
+    return _Csr(m.rows, m.cols, m.nnz, _ptr(m.row_ptr, torch.int32).value,
+                _ptr(m.col_idx, torch.int32).value if m.nnz else None, _ptr(m.val, torch.float32).value if m.nnz else None)
+
+
+def sysml_conv2d_csr_filter(x, f: "CSR", d, bias=None, out=None, stream=None):
+    """Convolution with a CSR filter bank (K x C*R*S): dense input / sparse filter, or sparse /
+    sparse when x is a CSR."""
+    torch = _torch()
+    y = out if out is not None else torch.empty(d.N, d.K * d.P * d.Q, device="cuda", dtype=torch.float32)
+    inp = _input(x)
+    fc = _csr_struct(f)
+    _check(lib().sysml_conv2d_csr_filter(ctypes.byref(d), ctypes.byref(inp), ctypes.byref(fc),
+                                         _ptr(bias, torch.float32, "bias"), _ptr(y, torch.float32, "y"), _stream(stream)))
+    return y
+
+
+SPARSITY_THRESHOLD = 0.4  # S:88-92
+
+
+def sysml_count_nonzeros(x, stream=None) -> int:
+    torch = _torch()
+    n = ctypes.c_int64(0)
+    _check(lib().sysml_count_nonzeros(_ptr(x, torch.float32, "x"), x.numel(), ctypes.byref(n), _stream(stream)))
+    return n.value
+
+
+def dense_to_csr(x, stream=None) -> "CSR":
+    """GPU dense (rows x cols, fp32) -> CSR, columns ascending per row (sysml_dense_to_csr)."""
+    torch = _torch()
+    rows, cols = x.shape
+    nnz = sysml_count_nonzeros(x, stream)
+    rp = torch.empty(rows + 1, device="cuda", dtype=torch.int32)
+    ci = torch.empty(max(nnz, 1), device="cuda", dtype=torch.int32)
+    v = torch.empty(max(nnz, 1), device="cuda", dtype=torch.float32)
+    _check(lib().sysml_dense_to_csr(_ptr(x, torch.float32, "x"), rows, cols, _ptr(rp), _ptr(ci), _ptr(v), _stream(stream)))
+    return CSR(rp, ci[:nnz], v[:nnz], rows, cols)
+
+
+def decide_format(x, threshold=SPARSITY_THRESHOLD, stream=None):
+    """P:163-165 / S:88-96: the CSR form of x if nnz / (rows*cols) <= threshold, else x itself."""
+    nnz = sysml_count_nonzeros(x, stream)
+    if x.numel() and nnz / x.numel() <= threshold:
+        return dense_to_csr(x, stream)
+    return x
 
 
 def sysml_optimizer_update(desc, params, grads, state, t=1, stream=None):

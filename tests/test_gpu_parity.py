@@ -585,3 +585,64 @@ def test_lenet_step_host_pipelined_matches_step_host(S):
                                            next_labels=batches[nb][1] if nb is not None else None))
     assert l1 == l2
     assert host(p1).tobytes() == host(p2).tobytes()
+
+
+SF_SHAPES = [  # N, C, H, W, K, R, S, stride, pad, filter density
+    (6, 1, 28, 28, 32, 5, 5, 1, 2, 0.3),
+    (3, 4, 9, 7, 6, 3, 3, 2, 1, 0.5),
+    (2, 16, 8, 8, 40, 1, 1, 1, 0, 0.2),
+    (2, 2, 6, 5, 3, 4, 2, 1, (2, 0), 1.0),
+    (2, 64, 14, 14, 20, 3, 3, 1, 1, 0.05),   # > SF_CHUNK-sized filter rows are not needed: 576 cols
+]
+
+
+@pytest.mark.parametrize("csr_input", [False, True])
+@pytest.mark.parametrize("shape", SF_SHAPES)
+def test_conv2d_csr_filter_vs_oracle(S, shape, csr_input):
+    """Dense input / sparse filter and sparse input / sparse filter against
+    oracle_conv2d_fwd_csr_filter (fp32 tolerance); includes an empty filter row."""
+    N, C, H, W, K, R, S_, st, pd, dens = shape
+    pd = pd if isinstance(pd, tuple) else (pd, pd)
+    rng = np.random.default_rng(40 + SF_SHAPES.index(shape))
+    x = synth.uniform((N, C * H * W), -1.0, 1.0, seed=(41,))
+    if csr_input:
+        x[rng.random(x.shape) > 0.25] = 0.0
+    f = rng.normal(size=(K, C * R * S_)).astype(np.float32)
+    f[rng.random(f.shape) > dens] = 0.0
+    f[0] = 0.0
+    b = rng.normal(size=K).astype(np.float32)
+    frp, fci, fv = synth.to_csr(f)
+    fc = S.CSR(dev(frp, torch.int32), dev(fci, torch.int32), dev(fv), K, C * R * S_)
+    xin = _csr_dev(S, x)[0] if csr_input else dev(x)
+    d = S.conv_desc(N, C, H, W, K, R, S_, st, pd, "fp32")
+    y = S.sysml_conv2d_csr_filter(xin, fc, d, bias=dev(b))
+    ref = oracle.conv2d_fwd_csr_filter(x.astype(np.float32).astype(np.float64), frp, fci, fv, N, C, H, W, K,
+                                       R, S_, (st, st), pd, bias=b)
+    assert_close(host(y), ref, 1e-4, "sparse-filter conv")
+    y2 = S.sysml_conv2d_csr_filter(xin, fc, d, bias=dev(b))
+    assert np.array_equal(host(y), host(y2))  # stored-order sums: deterministic
+
+
+def test_decide_format_and_dense_to_csr(S):
+    """GPU non-zero count and dense -> CSR: bit-exact against the
+    re-encoding in synth, the 0.4 threshold, empty rows, and the densify round trip."""
+    x = synth.mnist_like(37, seed=(700,))
+    x[3] = 0.0
+    x[5, :] = -0.0
+    nnz = int(np.count_nonzero(x))
+    xd = dev(x)
+    assert S.sysml_count_nonzeros(xd) == nnz == oracle.decide_format(x)[1]
+    m = S.dense_to_csr(xd)
+    rp, ci, v = synth.to_csr(x)
+    assert np.array_equal(host(m.row_ptr), rp) and np.array_equal(host(m.col_idx), ci)
+    assert np.array_equal(host(m.val), v)
+    assert np.array_equal(oracle.csr_densify(host(m.row_ptr), host(m.col_idx), host(m.val), 37, 784),
+                          x.astype(np.float64))
+    assert isinstance(S.decide_format(xd), S.CSR) and oracle.decide_format(x)[0] == "sparse"  # MNIST ~0.19
+    dense = dev(synth.uniform((8, 50), 0.5, 1.0, seed=(701,)))
+    assert S.decide_format(dense) is dense
+    a = np.zeros((10, 10), np.float32)
+    a.flat[:40] = 1.0
+    assert isinstance(S.decide_format(dev(a)), S.CSR)  # nnz/size = 0.4 -> sparse
+    a.flat[40] = 1.0
+    assert not isinstance(S.decide_format(dev(a)), S.CSR)
