@@ -391,6 +391,26 @@ def ours_arm(args, world, rank, local):
         ms_e2e = float(t.item())
     e2e_value = GLOBAL_BATCH * args.steps / (ms_e2e * 1e-3)
 
+    # ---- scoring (P:193-202 parfor-style row-partitioned scoring): forward + softmax/argmax of
+    # the local rows through sysml_lenet_predict; replicas, no collective
+    for i in range(3):
+        net.predict(params, xs[i % ROTATE])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e4 = torch.cuda.Event(enable_timing=True); e5 = torch.cuda.Event(enable_timing=True)
+    e4.record(st)
+    for i in range(args.steps):
+        net.predict(params, xs[i % ROTATE])
+    e5.record(st)
+    torch.cuda.synchronize()
+    ms_score = e4.elapsed_time(e5)
+    if world > 1:
+        t = torch.tensor([ms_score], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_score = float(t.item())
+    score_value = GLOBAL_BATCH * args.steps / (ms_score * 1e-3)
+
     # ---- roofline of the dominant stage
     tf32_sus = peaks["bf16_sus"] * 0.5
     fp32_alu = 148 * 128 * 2 * peaks["sm_max"] * 1e6 / 1e12
@@ -438,6 +458,8 @@ def ours_arm(args, world, rank, local):
                    "global_batch": GLOBAL_BATCH, "local_batch": b, "input": "dense MNIST-shaped (density ~0.19)",
                    "parallelism": f"dp{world}", "l2": f"{ROTATE} rotating input batches + ~0.6 GB/step activations >> 126 MB L2",
                    "launch": graph_note},
+        "scoring": {"value": round(score_value, 1), "unit": UNIT,
+                    "mode": "sysml_lenet_predict: forward + softmax / argmax of the local rows, row-partitioned replicas (no collective), device-resident batches"},
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": b * 784 * 4 + b * 4,
                 "d2h_bytes_per_step": 4, "mode": "sysml_lenet_step_host_pipelined: pinned host batches, batch i+1 copied H2D while step i computes, loss read back every step"},
         "gpu_launches": int(launches),

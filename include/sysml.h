@@ -233,6 +233,14 @@ SYSML_API sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, 
                                  const int32_t *labels, int32_t n_local, int64_t n_global,
                                  float *grads, float *loss_sum, sysml_stream_t stream);
 
+/* Scoring (parfor-style row-partitioned scoring; replicas need no collective):
+ * the forward of the local rows (conv-relu-pool x2, affine) -> pred int32[n_local] = the
+ * first maximal class (nullable) and probs fp32[n_local x 10] = softmax (nullable; one of
+ * the two required).  x: dense or CSR as the handle was created.                      */
+SYSML_API sysml_status sysml_lenet_predict(sysml_lenet *h, const float *params, const sysml_input *x,
+                                           int32_t n_local, int32_t *pred, float *probs,
+                                           sysml_stream_t stream);
+
 /* SGD (S:282-290 sgd: p - lr*g): params[i] -= lr * grads[i], i < n.              */
 SYSML_API sysml_status sysml_sgd_update(float *params, const float *grads, int64_t n, float lr,
                               sysml_stream_t stream);

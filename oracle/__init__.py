@@ -159,6 +159,13 @@ def lenet_forward(x, params):
     return dict(a1=a1, i1=i1, a2=a2, i2=i2, scores=sc)
 
 
+def lenet_predict(x, params):
+    """Scoring: softmax of the oracle forward's scores and the first maximal class."""
+    sc = lenet_forward(x, params)["scores"]
+    e = np.exp(sc - sc.max(axis=1, keepdims=True))
+    return np.argmax(sc, axis=1).astype(np.int32), e / e.sum(axis=1, keepdims=True)
+
+
 def lenet_fwd_bwd(x, labels, params, n_global=None):
     """Returns (grads float64[83466] pre-scaled by 1/n_global, loss_sum)."""
     n = x.shape[0]

@@ -45,7 +45,7 @@ EXPORTS = (
     "sysml_lenet_set_timing", "sysml_lenet_get_timing",
     "sysml_optimizer_state_floats", "sysml_optimizer_update", "sysml_lenet_step_opt",
     "sysml_lenet_step_host_pipelined",
-    "sysml_conv2d_csr_filter", "sysml_count_nonzeros", "sysml_dense_to_csr",
+    "sysml_conv2d_csr_filter", "sysml_count_nonzeros", "sysml_dense_to_csr", "sysml_lenet_predict",
 )
 
 
@@ -175,6 +175,7 @@ def lib(build_if_missing: bool = False):
         "sysml_lenet_set_timing": (c_i32, [vp, c_i32]),
         "sysml_optimizer_state_floats": (c_i32, [c_i32]),
         "sysml_conv2d_csr_filter": (c_i32, [CD, IN, CS, vp, vp, vp]),
+        "sysml_lenet_predict": (c_i32, [vp, vp, IN, c_i32, vp, vp, vp]),
         "sysml_count_nonzeros": (c_i32, [vp, c_i64, ctypes.POINTER(c_i64), vp]),
         "sysml_dense_to_csr": (c_i32, [vp, c_i64, c_i64, vp, vp, vp, vp]),
         "sysml_lenet_step_host_pipelined": (c_i32, [vp, vp, vp, vp, vp, c_i32, vp, vp, c_i32, c_i64,
@@ -465,6 +466,18 @@ class LeNet:
                                          _ptr(labels, torch.int32, "labels"), int(n), int(n_global),
                                          _ptr(grads, torch.float32, "grads"), _ptr(loss_sum, torch.float32, "loss_sum"),
                                          _stream(stream)))
+
+    def predict(self, params, x, probs=False, stream=None):
+        """Scoring (sysml_lenet_predict): predicted labels (int32[n]) and, if probs, the softmax
+        probabilities (fp32[n, 10])."""
+        torch = _torch()
+        inp = _input(x)
+        n = x.rows if isinstance(x, CSR) else x.shape[0]
+        pred = torch.empty(n, device="cuda", dtype=torch.int32)
+        pr = torch.empty(n, 10, device="cuda", dtype=torch.float32) if probs else None
+        _check(lib().sysml_lenet_predict(self.h, _ptr(params, torch.float32, "params"), ctypes.byref(inp), int(n),
+                                         _ptr(pred), _ptr(pr), _stream(stream)))
+        return (pred, pr) if probs else pred
 
     def step(self, params, grads, x, labels, n_global, lr=0.01, nccl_comm=None, loss_sum=None, stream=None):
         torch = _torch()

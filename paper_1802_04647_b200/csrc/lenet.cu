@@ -162,6 +162,52 @@ __global__ void __launch_bounds__(F3_THREADS) affine_softmax_ce_smem_kernel(
   }
 }
 
+// Scoring (P:193-202 parfor-style row-partitioned scoring): warp per sample, logits =
+// a2 . W3^T + b3 (lanes stride the 784 float4 columns, xor-tree reduction), then the
+// max-shifted softmax probabilities and the first maximum as the predicted label.
+__global__ void lenet_predict_kernel(int n, const float *__restrict__ a2, const float *__restrict__ W3,
+                                     const float *__restrict__ b3, int32_t *__restrict__ pred,
+                                     float *__restrict__ probs) {
+  const int sample = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (sample >= n) return;
+  const float4 *row = reinterpret_cast<const float4 *>(a2 + (int64_t)sample * D3);
+  float acc[NCLS];
+#pragma unroll
+  for (int j = 0; j < NCLS; ++j) acc[j] = 0.f;
+  for (int d4 = lane; d4 < D3 / 4; d4 += 32) {
+    const float4 v = __ldg(row + d4);
+#pragma unroll
+    for (int j = 0; j < NCLS; ++j) {
+      const float4 w = __ldg(reinterpret_cast<const float4 *>(W3 + j * D3) + d4);
+      acc[j] = fmaf(v.x, w.x, fmaf(v.y, w.y, fmaf(v.z, w.z, fmaf(v.w, w.w, acc[j]))));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NCLS; ++j)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+  if (lane == 0) {
+    float m = -INFINITY;
+    int best = 0;
+#pragma unroll
+    for (int j = 0; j < NCLS; ++j) {
+      acc[j] += __ldg(b3 + j);
+      if (acc[j] > m) {  // strict: the first maximum wins
+        m = acc[j];
+        best = j;
+      }
+    }
+    if (pred) pred[sample] = best;
+    if (probs) {
+      float den = 0.f;
+#pragma unroll
+      for (int j = 0; j < NCLS; ++j) den += expf(acc[j] - m);
+#pragma unroll
+      for (int j = 0; j < NCLS; ++j) probs[(int64_t)sample * NCLS + j] = expf(acc[j] - m) / den;
+    }
+  }
+}
+
 // ordered sum of v[0..n) into *out (single block, fixed tree)
 __global__ void ordered_total_kernel(const float *__restrict__ v, int n, float *__restrict__ out) {
   __shared__ float red[1024];
@@ -724,10 +770,13 @@ static sysml_status ar_bucket(sysml_lenet *h, float *g, size_t count, cudaEvent_
   return SYSML_OK;
 }
 
-sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysml_input *x,
-                                 const int32_t *labels, int32_t n_local, int64_t n_global,
-                                 float *grads, float *loss_sum, sysml_stream_t stream) {
-  SYSML_CHECK_ARG(h && params && x && labels && grads, "NULL argument to sysml_lenet_fwd_bwd");
+// the forward (+ backward) of the local shard; predict mode (pred or probs non-NULL) stops
+// after conv2 + pool and scores instead
+static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_input *x,
+                              const int32_t *labels, int32_t n_local, int64_t n_global,
+                              float *grads, float *loss_sum, sysml_stream_t stream, int32_t *pred,
+                              float *probs) {
+  SYSML_CHECK_ARG(h && params && x && ((labels && grads) || pred || probs), "NULL argument to sysml_lenet_fwd_bwd / predict");
   SYSML_CHECK_ARG(n_local >= 1 && n_local <= h->max_b,
                   "n_local %d out of range [1, max_local_batch=%d]", n_local, h->max_b);
   SYSML_CHECK_ARG(n_global >= n_local, "n_global %lld < n_local %d", (long long)n_global, n_local);
@@ -798,6 +847,12 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
                                 h->i2, h->ws, h->ws_bytes, st));
   }
   SYSML_TRY(T.end());
+  if (pred || probs) {  // scoring: logits, softmax, argmax
+    lenet_predict_kernel<<<(unsigned)ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(n, h->a2, params + OFF_W3,
+                                                                               params + OFF_B3, pred, probs);
+    SYSML_LAUNCH_CHECK();
+    return SYSML_OK;
+  }
   // F3
   SYSML_TRY(T.begin(2));
   {
@@ -908,6 +963,19 @@ sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysm
     SYSML_CUDA(cudaStreamWaitEvent(st, h->ev_ar, 0));
   }
   return SYSML_OK;
+}
+
+sysml_status sysml_lenet_fwd_bwd(sysml_lenet *h, const float *params, const sysml_input *x,
+                                 const int32_t *labels, int32_t n_local, int64_t n_global,
+                                 float *grads, float *loss_sum, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(labels && grads, "NULL labels / grads argument to sysml_lenet_fwd_bwd");
+  return lenet_run(h, params, x, labels, n_local, n_global, grads, loss_sum, stream, nullptr, nullptr);
+}
+
+sysml_status sysml_lenet_predict(sysml_lenet *h, const float *params, const sysml_input *x, int32_t n_local,
+                                 int32_t *pred, float *probs, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(pred || probs, "sysml_lenet_predict needs pred and/or probs");
+  return lenet_run(h, params, x, nullptr, n_local, n_local, nullptr, nullptr, stream, pred, probs);
 }
 
 sysml_status sysml_sgd_update(float *params, const float *grads, int64_t n, float lr,

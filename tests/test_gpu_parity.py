@@ -646,3 +646,19 @@ def test_decide_format_and_dense_to_csr(S):
     assert isinstance(S.decide_format(dev(a)), S.CSR)  # nnz/size = 0.4 -> sparse
     a.flat[40] = 1.0
     assert not isinstance(S.decide_format(dev(a)), S.CSR)
+
+
+@pytest.mark.parametrize("csr", [False, True])
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+def test_lenet_predict_vs_oracle(S, math, csr):
+    """Scoring (sysml_lenet_predict) against the oracle forward's softmax / argmax: dyadic
+    inputs, so TF32 logits are exact and the labels must match exactly."""
+    n = 40
+    x, _, prm = _lenet_case(n, dyadic=True, seed=1010)
+    net = S.LeNet(64, math=math, csr=csr, max_nnz=n * 784)
+    xin = _csr_dev(S, x)[0] if csr else dev(x)
+    pred, probs = net.predict(dev(prm), xin, probs=True)
+    pred_ref, probs_ref = oracle.lenet_predict(x, prm)
+    assert np.array_equal(host(pred), pred_ref)
+    assert_close(host(probs), probs_ref, TOL[math], "probs")
+    assert np.array_equal(host(net.predict(dev(prm), xin)), pred_ref)

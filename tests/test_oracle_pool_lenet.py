@@ -202,3 +202,18 @@ def test_dyadic_lenet_forward_is_exact_in_fp32():
     fw = oracle.lenet_forward(x, prm)
     for k in ("a1", "a2"):
         assert np.array_equal(fw[k].astype(np.float32).astype(np.float64), fw[k])
+
+
+def test_lenet_predict_properties():
+    """Scoring oracle: probabilities sum to 1, the label is the argmax of the
+    (pinned) forward scores, and a common shift of the logits (added to every b3 entry)
+    leaves the probabilities unchanged (softmax shift invariance)."""
+    rng = np.random.default_rng(5)
+    x = rng.random((6, 784))
+    prm = synth.lenet_params(seed=(31,)).astype(np.float64)
+    pred, probs = oracle.lenet_predict(x, prm)
+    assert np.allclose(probs.sum(axis=1), 1.0, rtol=0, atol=1e-14)
+    assert np.array_equal(pred, np.argmax(oracle.lenet_forward(x, prm)["scores"], axis=1))
+    prm2 = prm.copy()
+    prm2[-10:] += 3.25
+    assert np.allclose(oracle.lenet_predict(x, prm2)[1], probs, rtol=0, atol=1e-12)
