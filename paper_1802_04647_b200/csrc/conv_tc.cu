@@ -81,6 +81,7 @@ struct TcFwdParams {
   int64_t code_plane; // stride (64-bit words) of a 16-channel code group
   long long *clk;     // optional per-CTA cycle counters (SYSML_TC_PROFILE instrumentation)
   int N, C, H, W, K, R, S, ph, pw, P, Q;
+  int sh, sw;          // stride: 1, or > 1 for 1x1 filters (frame = the output grid)
   int Wf, Hs, Lf;
   int64_t G;
   int NFpad, nft, nchunk;
@@ -738,7 +739,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           const int n = (int)(gi / p.Lf);
           const int rem = (int)(gi - (int64_t)n * p.Lf);
           const int hh = rem / p.Wf, ww = rem - hh * p.Wf;
-          const int h = hh - p.ph, w = ww - p.pw;
+          const int h = hh * p.sh - p.ph, w = ww * p.sw - p.pw;  // stride > 1: output-grid frame
           if (h >= 0 && h < p.H && w >= 0 && w < p.W) off = n * p.C * HW + h * p.W + w;
         }
         src_off[pos] = off;
@@ -1045,15 +1046,19 @@ int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 // Plan the forward kernel for a stride-1 conv: input (N,C,H,W), K output channels.
 TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
-                const PoolArgs *pool, bool allow_ks = true) {
+                const PoolArgs *pool, bool allow_ks = true, int sh = 1, int sw = 1) {
   TcPlan pl{};
   TcFwdParams &p = pl.p;
   p.N = N; p.C = C; p.H = H; p.W = W; p.K = K; p.R = R; p.S = S; p.ph = ph; p.pw = pw;
-  p.P = H + 2 * ph - R + 1;
-  p.Q = W + 2 * pw - S + 1;
+  p.sh = sh; p.sw = sw;
   pl.ok = false;
-  if (p.P < 1 || p.Q < 1) return pl;
-  p.Wf = W + pw;
+  const bool strided = sh != 1 || sw != 1;
+  // a strided conv has no shifted-window reuse: only 1x1 filters, on the output grid
+  if (sh < 1 || sw < 1 || (strided && (R != 1 || S != 1 || pool))) return pl;
+  p.P = (H + 2 * ph - R) / sh + 1;
+  p.Q = (W + 2 * pw - S) / sw + 1;
+  if (H + 2 * ph - R < 0 || W + 2 * pw - S < 0 || p.P < 1 || p.Q < 1) return pl;
+  p.Wf = strided ? p.Q : W + pw;
   p.pool = pool ? 1 : 0;
   p.PR = pool ? pool->R : 1;
   p.PS = pool ? pool->S : 1;
@@ -1063,13 +1068,13 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
     p.Pp = pool->P;
     p.Qp = pool->Q;
   }
-  p.Hs = round_up(H + ph, p.PR);
+  p.Hs = strided ? p.P : round_up(H + ph, p.PR);
   p.Lf = p.Hs * p.Wf;
   p.G = (int64_t)N * p.Lf;
   if (p.G + 4096 >= (1ll << 31)) return pl;
   p.tile2d = pool ? 1 : 0;
   static const int abulk_env = getenv("SYSML_TC_ABULK") ? atoi(getenv("SYSML_TC_ABULK")) : -1;
-  p.abulk = (abulk_env != 0 && !pool && R == 1 && S == 1 && ph == 0 && pw == 0 &&
+  p.abulk = (abulk_env != 0 && !pool && R == 1 && S == 1 && ph == 0 && pw == 0 && !strided &&
              ((int64_t)H * W) % 4 == 0 && C > 1 && (int64_t)N * C * H * W < (1ll << 31)) ? 1 : 0;
   if (K <= 256) {
     p.NFpad = std::max(16, round_up(K, 16));
@@ -2027,8 +2032,8 @@ bool tc_fwd_ks(const ConvArgs &a) { return a.C == 1 && a.S <= 8; }
 
 bool tc_fwd_supported(const ConvArgs &a, const PoolArgs *pool) {
   if (device_cc_major() != 10) return false;
-  if (a.sh != 1 || a.sw != 1 || !pool_fusable(pool)) return false;
-  return plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool).ok;
+  if (((a.sh != 1 || a.sw != 1) && (a.R != 1 || a.S != 1 || pool)) || !pool_fusable(pool)) return false;
+  return plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool, true, a.sh, a.sw).ok;
 }
 
 size_t tc_fwd_ws(const ConvArgs &a) {
@@ -2043,7 +2048,7 @@ size_t tc_fwd_ws(const ConvArgs &a) {
 sysml_status tc_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
                          float *y, const PoolArgs *pool, float *pout, int32_t *parg, void *ws,
                          cudaStream_t st, const sysml_csr *csr) {
-  TcPlan pl = plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool);
+  TcPlan pl = plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool, true, a.sh, a.sw);
   if (!pl.ok) {
     set_error("tcgen05 forward: unsupported shape");
     return SYSML_ERR_UNSUPPORTED;

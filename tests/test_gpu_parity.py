@@ -57,6 +57,8 @@ CONV_SHAPES = [
     (2, 32, 4, 4, 300, 1, 1, 1, 0),      # 1x1 TMA wgrad: K > 256 (two filter-pair tiles), ragged
     (2, 16, 9, 11, 136, 3, 3, 1, 1),     # framed TMA wgrad: K > 128 (two filter tiles), 16-ch tile
     (2, 32, 10, 12, 48, 3, 3, 1, 0),     # framed TMA wgrad: pad 0, rectangular
+    (4, 64, 14, 14, 96, 1, 1, 2, 0),     # 1x1 stride 2 (ResNet downsample): tcgen05 on the output grid
+    (2, 24, 9, 11, 40, 1, 1, 2, 0),      # 1x1 stride 2, odd extents (floor)
 ]
 
 
