@@ -82,6 +82,8 @@ struct TcFwdParams {
   long long *clk;     // optional per-CTA cycle counters (SYSML_TC_PROFILE instrumentation)
   int N, C, H, W, K, R, S, ph, pw, P, Q;
   int sh, sw;          // stride: 1, or > 1 for 1x1 filters (frame = the output grid)
+  int yH, yW, ysh, ysw;  // plain epilogue: output image yH x yW, row (p, q) -> (p*ysh, q*ysw)
+                         // (strided 1x1 bwd_data writes every ysh-th row / ysw-th column)
   int Wf, Hs, Lf;
   int64_t G;
   int NFpad, nft, nchunk;
@@ -155,7 +157,7 @@ __device__ __forceinline__ void load_bias16(const TcFwdParams &p, const float *b
 // plain conv output: lane -> position (linear or 2-D M-tile), 16 filters per chunk
 __device__ __forceinline__ void epi_plain(const TcFwdParams &p, uint32_t tbase, int64_t g0, int ft,
                                           int qd, int lane, const float *bias_s, int i0, int istep) {
-  const int PQ = p.P * p.Q;
+  const int64_t PQ = (int64_t)p.yH * p.yW;  // output plane (= P*Q unless strided bwd_data)
   const int nc16 = p.NFpad / 16;
   float *__restrict__ y = p.y;
   for (int i = i0; i < p.MT; i += istep) {
@@ -181,7 +183,7 @@ __device__ __forceinline__ void epi_plain(const TcFwdParams &p, uint32_t tbase, 
       }
       const int hh = rem / p.Wf, q = rem - hh * p.Wf;
       valid = hh < p.P && q < p.Q;
-      ybase = (int64_t)n * p.K * PQ + (int64_t)hh * p.Q + q;
+      ybase = (int64_t)n * p.K * PQ + (int64_t)hh * p.ysh * p.yW + (int64_t)q * p.ysw;
     }
     auto process = [&](const uint32_t(&cur)[16], int c16) {
       const int k0 = ft * p.NFpad + c16 * 16;
@@ -1051,6 +1053,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   TcFwdParams &p = pl.p;
   p.N = N; p.C = C; p.H = H; p.W = W; p.K = K; p.R = R; p.S = S; p.ph = ph; p.pw = pw;
   p.sh = sh; p.sw = sw;
+  p.ysh = p.ysw = 1;
   pl.ok = false;
   const bool strided = sh != 1 || sw != 1;
   // a strided conv has no shifted-window reuse: only 1x1 filters, on the output grid
@@ -1059,6 +1062,8 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   p.Q = (W + 2 * pw - S) / sw + 1;
   if (H + 2 * ph - R < 0 || W + 2 * pw - S < 0 || p.P < 1 || p.Q < 1) return pl;
   p.Wf = strided ? p.Q : W + pw;
+  p.yH = p.P;
+  p.yW = p.Q;
   p.pool = pool ? 1 : 0;
   p.PR = pool ? pool->R : 1;
   p.PS = pool ? pool->S : 1;
@@ -2057,7 +2062,21 @@ sysml_status tc_conv_fwd(const ConvArgs &a, const float *x, const float *f, cons
 }
 
 // ------------------------------------------------------------------ bwd_data (K6)
+static bool strided_1x1(const ConvArgs &a) {
+  return (a.sh != 1 || a.sw != 1) && a.R == 1 && a.S == 1 && a.ph == 0 && a.pw == 0;
+}
+
 static TcPlan plan_bwd_data(const ConvArgs &a) {
+  if (strided_1x1(a)) {
+    // strided 1x1: dX[n, c, p*sh, q*sw] = sum_k F[k, c] dY[n, k, p, q], zero elsewhere -- a
+    // stride-1 1x1 "forward" on dY's grid whose rows land on every sh-th row / sw-th column
+    TcPlan pl = plan_fwd(a.N, a.K, a.P, a.Q, a.C, 1, 1, 0, 0, nullptr, /*allow_ks=*/false);
+    pl.p.yH = a.H;
+    pl.p.yW = a.W;
+    pl.p.ysh = a.sh;
+    pl.p.ysw = a.sw;
+    return pl;
+  }
   // dX = conv(dY, rot180(F)^T), pad R-1-ph; input (N, K, P, Q) -> output (N, C, H, W)
   return plan_fwd(a.N, a.K, a.P, a.Q, a.C, a.R, a.S, a.R - 1 - a.ph, a.S - 1 - a.pw, nullptr,
                   /*allow_ks=*/false);
@@ -2065,6 +2084,7 @@ static TcPlan plan_bwd_data(const ConvArgs &a) {
 
 bool tc_bwd_data_supported(const ConvArgs &a) {
   if (device_cc_major() != 10) return false;
+  if (strided_1x1(a)) return plan_bwd_data(a).ok && !plan_bwd_data(a).p.sn;
   if (a.sh != 1 || a.sw != 1 || a.ph > a.R - 1 || a.pw > a.S - 1) return false;
   TcPlan pl = plan_bwd_data(a);
   return pl.ok && pl.p.P == a.H && pl.p.Q == a.W;
@@ -2082,6 +2102,8 @@ sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy
     set_error("tcgen05 bwd_data: unsupported shape");
     return SYSML_ERR_UNSUPPORTED;
   }
+  if (strided_1x1(a))  // positions off the stride grid receive no contribution
+    SYSML_CUDA(cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)a.N * a.C * a.H * a.W, st));
   // filter bank F is (K x C*RS) = (Cin_of_this_conv x Kout*RS) -> flip = 1
   return run_fwd(pl, dy, f, 1, a.K, nullptr, dx, nullptr, nullptr, ws, st);
 }
@@ -2172,8 +2194,29 @@ sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy
 }
 
 // ------------------------------------------------------------------ bwd_filter (K5)
+// strided 1x1 bwd_filter: dF[k][c] = sum_{n,p,q} dY[n,k,p,q] X[n,c,p*sh,q*sw] is the stride-1
+// 1x1 bwd_filter of the subsampled X (N x C x P x Q, gathered into the workspace first)
+static ConvArgs subsampled_1x1(const ConvArgs &a) {
+  ConvArgs b = a;
+  b.H = a.P;
+  b.W = a.Q;
+  b.sh = b.sw = 1;
+  return b;
+}
+
+__global__ void subsample_kernel(const float *__restrict__ x, float *__restrict__ xs, int64_t NC, int H, int W,
+                                 int P, int Q, int sh, int sw) {
+  const int64_t total = NC * P * Q;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nc = i / (P * Q);
+    const int pq = (int)(i - nc * P * Q), pp = pq / Q, qq = pq - pp * Q;
+    xs[i] = __ldg(x + nc * H * W + (int64_t)pp * sh * W + (int64_t)qq * sw);
+  }
+}
+
 bool tc_bwd_filter_supported(const ConvArgs &a) {
   if (device_cc_major() != 10) return false;
+  if (strided_1x1(a)) return tc_wgrad_1x1_supported(subsampled_1x1(a));
   if (tc_wgrad_1x1_supported(a)) return true;
   if (tc_wgrad_frame_supported(a)) return true;
   if (a.C < 8) return false;  // tiny channel counts waste N; CUDA-core / CSR kernels instead
@@ -2181,6 +2224,8 @@ bool tc_bwd_filter_supported(const ConvArgs &a) {
 }
 
 size_t tc_bwd_filter_ws(const ConvArgs &a) {
+  if (strided_1x1(a))
+    return align_up((size_t)a.N * a.C * a.P * a.Q * sizeof(float), 256) + tc_wgrad_1x1_ws(subsampled_1x1(a));
   if (tc_wgrad_1x1_supported(a)) return tc_wgrad_1x1_ws(a);
   if (tc_wgrad_frame_supported(a)) return tc_wgrad_frame_ws(a);
   TcWgPlan pl = plan_wgrad(a);
@@ -2189,6 +2234,20 @@ size_t tc_bwd_filter_ws(const ConvArgs &a) {
 
 sysml_status tc_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,
                                 float *db, void *ws, cudaStream_t st) {
+  if (strided_1x1(a)) {
+    const ConvArgs b = subsampled_1x1(a);
+    if (!tc_wgrad_1x1_supported(b)) {
+      set_error("tcgen05 bwd_filter: unsupported strided 1x1 shape");
+      return SYSML_ERR_UNSUPPORTED;
+    }
+    float *xs = reinterpret_cast<float *>(ws);
+    const int64_t total = (int64_t)a.N * a.C * a.P * a.Q;
+    subsample_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 16 * sm_count()), 256, 0, st>>>(
+        x, xs, (int64_t)a.N * a.C, a.H, a.W, a.P, a.Q, a.sh, a.sw);
+    SYSML_LAUNCH_CHECK();
+    return tc_wgrad_1x1(b, xs, dy, df, db,
+                        reinterpret_cast<char *>(ws) + align_up((size_t)total * sizeof(float), 256), st);
+  }
   if (tc_wgrad_1x1_supported(a)) return tc_wgrad_1x1(a, x, dy, df, db, ws, st);
   if (tc_wgrad_frame_supported(a)) return tc_wgrad_frame(a, x, dy, df, db, ws, st);
   TcWgPlan pl = plan_wgrad(a);

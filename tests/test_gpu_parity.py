@@ -59,6 +59,7 @@ CONV_SHAPES = [
     (2, 32, 10, 12, 48, 3, 3, 1, 0),     # framed TMA wgrad: pad 0, rectangular
     (4, 64, 14, 14, 96, 1, 1, 2, 0),     # 1x1 stride 2 (ResNet downsample): tcgen05 on the output grid
     (2, 24, 9, 11, 40, 1, 1, 2, 0),      # 1x1 stride 2, odd extents (floor)
+    (2, 32, 16, 16, 48, 1, 1, 2, 0),     # 1x1 stride 2, P*Q % 4 == 0: strided TMA bwd_filter
 ]
 
 
