@@ -389,11 +389,11 @@ __global__ void __launch_bounds__(256) affine_bwd_route_spf_kernel(
       gsum += g;
       const uint32_t wp = cd[u] & 3u;
       float *bs = base + (int64_t)s * 256;
-      *reinterpret_cast<float2 *>(bs) = make_float2(wp == 0 ? g : 0.f, wp == 1 ? g : 0.f);
-      *reinterpret_cast<float2 *>(bs + 16) = make_float2(wp == 2 ? g : 0.f, wp == 3 ? g : 0.f);
+      __stcs(reinterpret_cast<float2 *>(bs), make_float2(wp == 0 ? g : 0.f, wp == 1 ? g : 0.f));  // streaming
+      __stcs(reinterpret_cast<float2 *>(bs + 16), make_float2(wp == 2 ? g : 0.f, wp == 3 ? g : 0.f));
       if (pc == 6) {  // the frame's zero columns 14-15 too: whole 32-byte sectors written
-        *reinterpret_cast<float2 *>(bs + 2) = make_float2(0.f, 0.f);
-        *reinterpret_cast<float2 *>(bs + 18) = make_float2(0.f, 0.f);
+        __stcs(reinterpret_cast<float2 *>(bs + 2), make_float2(0.f, 0.f));
+        __stcs(reinterpret_cast<float2 *>(bs + 18), make_float2(0.f, 0.f));
       }
     }
   }
