@@ -119,7 +119,9 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         const long long t0 = clock64();
         ptx::mbar_wait(emptyA + sa, pa ^ 1);
         if (p.clk) p.clk[blockIdx.x * 8 + 4] += clock64() - t0;
-        ptx::mbar_arrive_expect_tx(fullA + sa, a_slot);
+        // the bytes the copies below deliver: copies x Kc rows (< 128 rows when copies*Kc < 128;
+        // the slot's other rows only feed accumulator rows the reduce skips)
+        ptx::mbar_arrive_expect_tx(fullA + sa, (uint32_t)(p.copies * p.Kc * 128));
         const int g = (int)((a0 + ia) * W2_ATOM);
         for (int j = 0; j < p.copies; ++j)
           ptx::tma_load_3d(sA + sa * a_slot + j * p.Kc * 128, &tmDy, g - j * p.Wf, k0, 0,

@@ -665,3 +665,39 @@ def test_lenet_predict_vs_oracle(S, math, csr):
     assert np.array_equal(host(pred), pred_ref)
     assert_close(host(probs), probs_ref, TOL[math], "probs")
     assert np.array_equal(host(net.predict(dev(prm), xin)), pred_ref)
+
+
+def _random_conv_shapes(count, seed):
+    rng = np.random.default_rng(seed)
+    shapes = []
+    while len(shapes) < count:
+        N = int(rng.integers(1, 5))
+        C = int(rng.choice([1, 2, 3, 8, 13, 16, 24, 40, 64]))
+        K = int(rng.choice([1, 5, 16, 17, 32, 48, 64, 96, 130]))
+        R = int(rng.choice([1, 2, 3, 5]))
+        S_ = int(rng.choice([1, 3, 5])) if rng.random() < 0.7 else R
+        st = int(rng.choice([1, 1, 1, 2]))
+        ph, pw = int(rng.integers(0, R)), int(rng.integers(0, S_))
+        H, W = int(rng.integers(R, 19)), int(rng.integers(S_, 19))
+        if (H + 2 * ph - R) // st + 1 < 1 or (W + 2 * pw - S_) // st + 1 < 1:
+            continue
+        shapes.append((N, C, H, W, K, R, S_, st, (ph, pw)))
+    return shapes
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("shape", _random_conv_shapes(24, 2026))
+def test_conv_random_shape_sweep(S, shape, math):
+    """Seeded random sweep over conv shapes (strides, pads, rectangular kernels, odd sizes,
+    channel / filter counts around tile boundaries): fwd (+bias), bwd_filter (+db) and bwd_data
+    against the oracle -- guards the plan / dispatch corners of every kernel family."""
+    (N, C, H, W, K, R, S_, st, pd, P, Q), x, f, b, dy = _conv_case(shape, 77)
+    d = S.conv_desc(N, C, H, W, K, R, S_, st, pd, math)
+    y = S.sysml_conv2d(dev(x), dev(f), d, bias=dev(b))
+    assert_close(host(y), oracle.conv2d_fwd(x, f, N, C, H, W, K, R, S_, st, pd, bias=b), TOL[math], "fwd")
+    df, db = S.sysml_conv2d_bwd_filter(dev(x), dev(dy), d)
+    dfr, dbr = oracle.conv2d_bwd_filter(x, dy, N, C, H, W, K, R, S_, st, pd)
+    assert_close(host(df), dfr, TOL[math], "bwd_filter")
+    assert_close(host(db), dbr, 1e-4, "db")
+    dx = S.sysml_conv2d_bwd_data(dev(f), dev(dy), d)
+    assert_close(host(dx), oracle.conv2d_bwd_data(f, dy, N, C, H, W, K, R, S_, st, pd), TOL[math], "bwd_data")
