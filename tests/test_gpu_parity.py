@@ -701,3 +701,68 @@ def test_conv_random_shape_sweep(S, shape, math):
     assert_close(host(db), dbr, 1e-4, "db")
     dx = S.sysml_conv2d_bwd_data(dev(f), dev(dy), d)
     assert_close(host(dx), oracle.conv2d_bwd_data(f, dy, N, C, H, W, K, R, S_, st, pd), TOL[math], "bwd_data")
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("shape", _random_conv_shapes(32, 4242))
+def test_conv_random_shape_sweep_b(S, shape, math):
+    """Second seed of the random conv-shape sweep."""
+    test_conv_random_shape_sweep(S, shape, math)
+
+
+def _random_pool_shapes(count, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        N = int(rng.integers(1, 5))
+        C = int(rng.choice([1, 3, 8, 16, 32]))
+        K = int(rng.choice([5, 16, 32, 48, 64]))
+        R = int(rng.choice([3, 5]))
+        pad = R // 2
+        H, W = 2 * int(rng.integers(2, 10)), 2 * int(rng.integers(2, 10))
+        out.append((N, C, H, W, K, R, pad))
+    return out
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("shape", _random_pool_shapes(16, 99))
+def test_fused_conv_pool_random_sweep(S, shape, math):
+    """Random fused conv + bias + relu + 2x2/2 max-pool shapes on dyadic inputs (exact in TF32):
+    pooled values and int32 argmax bit-exact against the oracle."""
+    N, C, H, W, K, R, pad = shape
+    x = synth.dyadic((N, C * H * W), -2, 2, 8, seed=(91,))
+    f = synth.dyadic((K, C * R * R), -2, 2, 8, seed=(92,))
+    b = synth.dyadic((K,), -2, 2, 8, seed=(93,))
+    d = S.conv_desc(N, C, H, W, K, R, R, 1, pad, math)
+    pd = S.pool_desc(N, K, H, W, 2, 2, 2, 0, True)
+    out, arg = S.sysml_conv2d_bias_relu_maxpool(dev(x), dev(f), dev(b), d, pd)
+    z = oracle.conv2d_fwd(x, f, N, C, H, W, K, R, R, (1, 1), (pad, pad), bias=b)
+    oref, aref = oracle.relu_maxpool(z, N, K, H, W, 2, 2, (2, 2), (0, 0))
+    assert np.array_equal(host(out).astype(np.float64), oref)
+    assert np.array_equal(host(arg), aref)
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("N,K,R", [(1, 5, 3), (7, 16, 5), (33, 32, 5), (5, 32, 3), (130, 32, 5)])
+def test_csr_conv1_random_sweep(S, N, K, R, math):
+    """CSR conv1-style inputs (C = 1, 28x28, ~19% dense) over batch sizes and filter counts:
+    fwd, bwd_filter and the fused conv+pool against the oracle."""
+    x = synth.mnist_like(N, seed=(95, N))
+    m, (rp, ci, v) = _csr_dev(S, x)
+    xd = oracle.csr_densify(rp, ci, v, N, 784)
+    pad = R // 2
+    f = synth.normal((K, R * R), 0.3, seed=(96,))
+    b = synth.normal((K,), 0.1, seed=(97,))
+    d = S.conv_desc(N, 1, 28, 28, K, R, R, 1, pad, math)
+    y = S.sysml_conv2d(m, dev(f), d, bias=dev(b))
+    assert_close(host(y), oracle.conv2d_fwd(xd, f, N, 1, 28, 28, K, R, R, (1, 1), (pad, pad), bias=b), TOL[math], "fwd")
+    dy = synth.normal((N, K * 784), seed=(98,))
+    df, db = S.sysml_conv2d_bwd_filter(m, dev(dy), d)
+    dfr, dbr = oracle.conv2d_bwd_filter(xd, dy, N, 1, 28, 28, K, R, R, (1, 1), (pad, pad))
+    assert_close(host(df), dfr, 1e-4, "bwd_filter")
+    assert_close(host(db), dbr, 1e-4, "db")
+    pd = S.pool_desc(N, K, 28, 28, 2, 2, 2, 0, True)
+    out, arg = S.sysml_conv2d_bias_relu_maxpool(m, dev(f), dev(b), d, pd)
+    z = oracle.conv2d_fwd(xd, f, N, 1, 28, 28, K, R, R, (1, 1), (pad, pad), bias=b)
+    oref, aref = oracle.relu_maxpool(z, N, K, 28, 28, 2, 2, (2, 2), (0, 0))
+    assert_close(host(out), oref, TOL[math], "fused")
