@@ -766,3 +766,20 @@ def test_csr_conv1_random_sweep(S, N, K, R, math):
     z = oracle.conv2d_fwd(xd, f, N, 1, 28, 28, K, R, R, (1, 1), (pad, pad), bias=b)
     oref, aref = oracle.relu_maxpool(z, N, K, 28, 28, 2, 2, (2, 2), (0, 0))
     assert_close(host(out), oref, TOL[math], "fused")
+
+
+@pytest.mark.parametrize("n", [1, 3, 31, 33, 65, 130])
+def test_lenet_fwd_bwd_batch_sweep(S, n):
+    """LeNet fwd_bwd (TF32, dyadic) over ragged local batch sizes: odd counts (F3 sample pairs),
+    non-multiples of 32 (B2p chunks, B1 CTAs, dW3 chunks) and a handle larger than the batch."""
+    x, y, prm = _lenet_case(n, dyadic=True, seed=1100 + n)
+    g_ref, loss_ref = oracle.lenet_fwd_bwd(x, y, prm, n_global=2 * n)
+    net = S.LeNet(n + 7, math="tf32")
+    grads = torch.empty(83466, device="cuda")
+    loss = torch.empty(1, device="cuda")
+    net.fwd_bwd(dev(prm), dev(x), dev(y, torch.int32), 2 * n, grads, loss)
+    g = host(grads)
+    offs = np.cumsum([0] + [int(np.prod(s)) for _, s in synth.LENET_PARAM_SHAPES])
+    for i, (name, _) in enumerate(synth.LENET_PARAM_SHAPES):
+        assert_close(g[offs[i]:offs[i + 1]], g_ref[offs[i]:offs[i + 1]], TOL["tf32"], f"{name} n={n}")
+    assert abs(host(loss)[0] - loss_ref) <= 1e-5 * abs(loss_ref)
