@@ -210,19 +210,23 @@ def layer_section(S, peaks, quick=False):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
     out = {}
     reps = 5 if quick else 20
-    for name, (N, C, H, W, K, R, S_, pd) in {
-        "resnet3x3_C256_K256_14x14_N128": (128, 256, 14, 14, 256, 3, 3, 1),
-        "resnet1x1_C1024_K256_14x14_N128": (128, 1024, 14, 14, 256, 1, 1, 0),
-        "lenet_conv2_C32_K64_14x14_N8192": (8192, 32, 14, 14, 64, 5, 5, 2),
+    for name, (N, C, H, W, K, R, S_, st, pd) in {
+        "resnet3x3_C256_K256_14x14_N128": (128, 256, 14, 14, 256, 3, 3, 1, 1),
+        "resnet1x1_C1024_K256_14x14_N128": (128, 1024, 14, 14, 256, 1, 1, 1, 0),
+        "lenet_conv2_C32_K64_14x14_N8192": (8192, 32, 14, 14, 64, 5, 5, 1, 2),
+        # ResNet-50 strided convs (NEXT-2, phase split onto the stride-1 tcgen05 kernels)
+        "resnet50_stem7x7s2_C3_K64_224_N128": (128, 3, 224, 224, 64, 7, 7, 2, 3),
+        "resnet50_3x3s2_C128_K128_56_N128": (128, 128, 56, 56, 128, 3, 3, 2, 1),
     }.items():
-        P = Q = H
+        P = (H + 2 * pd - R) // st + 1
+        Q = (W + 2 * pd - S_) // st + 1
         x, f, b, dy = synth.conv_problem_U(N, C, H, W, K, R, S_, P, Q, seed=(1000,))
         x, f, b, dy = (torch.from_numpy(t).cuda() for t in (x, f, b, dy))
-        d = S.conv_desc(N, C, H, W, K, R, S_, 1, pd, "tf32")
+        d = S.conv_desc(N, C, H, W, K, R, S_, st, pd, "tf32")
         y = torch.empty(N, K * P * Q, device="cuda")
         dx = torch.empty(N, C * H * W, device="cuda")
         df = torch.empty(K, C * R * S_, device="cuda"); db = torch.empty(K, device="cuda")
-        ws = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+        ws = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
         flops = 2.0 * N * K * C * R * S_ * P * Q
         res = {}
         for op, fn, nbytes in (

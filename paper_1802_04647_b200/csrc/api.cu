@@ -5,6 +5,8 @@
 // Dispatch:
 //   dense conv fwd / bwd_data / bwd_filter:
 //     math == TF32 and the tcgen05 kernel covers the shape -> conv_tc.cu (K3/K5/K6)
+//     TF32, strided with R or S > 1, stride-1 image covered -> phase.cu (phase split +
+//                                                              the tcgen05 stride-1 kernels)
 //     otherwise                                             -> conv_simt.cu (fp32 FMA)
 //   CSR input: fwd -> csr.cu K7 (fused epilogue optional); bwd_filter -> csr.cu K8;
 //     shapes beyond K7/K8's shared-memory budget are densified into the workspace
@@ -46,10 +48,13 @@ sysml_status conv_fwd_ws(const sysml_conv_desc &cd, const sysml_pool_desc *pd, i
     if (!csr_fwd_supported(a)) {
       b += align_up((size_t)g.N * g.CHW() * sizeof(float), 256);  // densified input
       if (use_tc && tc_fwd_supported(a, pap)) b += tc_fwd_ws(a);
+      else if (use_tc && !pap && phase_fwd_supported(a)) b += phase_fwd_ws(a);
       else if (pd) b += align_up((size_t)g.N * g.KPQ() * sizeof(float), 256);
     }
   } else if (use_tc && tc_fwd_supported(a, pap)) {
     b += tc_fwd_ws(a);
+  } else if (use_tc && !pap && phase_fwd_supported(a)) {
+    b += phase_fwd_ws(a);
   } else if (pd) {
     b += align_up((size_t)g.N * g.KPQ() * sizeof(float), 256);  // unfused z
   }
@@ -115,6 +120,8 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
     void *tws = wc.take<char>(tc_fwd_ws(a));
     return tc_conv_fwd(a, xd, f, bias, y, pap, pout, parg, tws, st);
   }
+  if (cd.math == SYSML_MATH_TF32 && !pap && phase_fwd_supported(a))
+    return phase_conv_fwd(a, xd, f, bias, y, wc.take<char>(phase_fwd_ws(a)), st);
   if (pap) {
     float *z = wc.take<float>((size_t)g.N * g.KPQ());
     SYSML_TRY(simt_conv_fwd(a, xd, f, bias, z, st));
@@ -133,6 +140,7 @@ sysml_status conv_bwd_filter_ws(const sysml_conv_desc &cd, int is_csr, size_t *b
   } else {
     if (is_csr) b += align_up((size_t)g.N * g.CHW() * sizeof(float), 256);
     if (cd.math == SYSML_MATH_TF32 && tc_bwd_filter_supported(a)) b += tc_bwd_filter_ws(a);
+    else if (cd.math == SYSML_MATH_TF32 && phase_bwd_filter_supported(a)) b += phase_bwd_filter_ws(a);
     else b += simt_bwd_filter_ws(a);
   }
   *bytes = b;
@@ -165,6 +173,8 @@ sysml_status conv_bwd_filter_dispatch(const sysml_conv_desc &cd, const sysml_inp
     void *tws = wc.take<char>(tc_bwd_filter_ws(a));
     return tc_conv_bwd_filter(a, xd, dy, df, db, tws, st);
   }
+  if (cd.math == SYSML_MATH_TF32 && phase_bwd_filter_supported(a))
+    return phase_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(phase_bwd_filter_ws(a)), st);
   void *sws = wc.take<char>(simt_bwd_filter_ws(a));
   return simt_conv_bwd_filter(a, xd, dy, df, db, sws, st);
 }
@@ -173,7 +183,9 @@ sysml_status conv_bwd_data_ws(const sysml_conv_desc &cd, size_t *bytes) {
   ConvGeom g;
   SYSML_TRY(validate_conv(&cd, &g));
   const ConvArgs a = conv_args(g);
-  *bytes = (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a)) ? tc_bwd_data_ws(a) : 0;
+  *bytes = 0;
+  if (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a)) *bytes = tc_bwd_data_ws(a);
+  else if (cd.math == SYSML_MATH_TF32 && phase_bwd_data_supported(a)) *bytes = phase_bwd_data_ws(a);
   return SYSML_OK;
 }
 
@@ -191,6 +203,8 @@ sysml_status conv_bwd_data_dispatch(const sysml_conv_desc &cd, const float *f, c
   }
   if (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a))
     return tc_conv_bwd_data(a, f, dy, dx, ws, st);
+  if (cd.math == SYSML_MATH_TF32 && phase_bwd_data_supported(a))
+    return phase_conv_bwd_data(a, f, dy, dx, ws, st);
   return simt_conv_bwd_data(a, f, dy, dx, st);
 }
 

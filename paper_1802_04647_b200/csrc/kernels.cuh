@@ -95,6 +95,20 @@ size_t tc_fwd_ws(const ConvArgs &a);
 sysml_status tc_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
                          float *y, const PoolArgs *pool, float *pout, int32_t *parg, void *ws,
                          cudaStream_t st, const sysml_csr *csr = nullptr);
+// phase.cu : strided convs with R or S > 1 as stride-1 tcgen05 convs over the phase-split
+// input (space-to-depth); DESIGN.md §7 "Strided convolutions"
+bool phase_fwd_supported(const ConvArgs &a);
+size_t phase_fwd_ws(const ConvArgs &a);
+sysml_status phase_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
+                            float *y, void *ws, cudaStream_t st);
+bool phase_bwd_data_supported(const ConvArgs &a);
+size_t phase_bwd_data_ws(const ConvArgs &a);
+sysml_status phase_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
+                                 void *ws, cudaStream_t st);
+bool phase_bwd_filter_supported(const ConvArgs &a);
+size_t phase_bwd_filter_ws(const ConvArgs &a);
+sysml_status phase_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,
+                                   float *db, void *ws, cudaStream_t st);
 bool tc_bwd_data_supported(const ConvArgs &a);
 size_t tc_bwd_data_ws(const ConvArgs &a);
 sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,

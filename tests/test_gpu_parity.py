@@ -60,13 +60,20 @@ CONV_SHAPES = [
     (4, 64, 14, 14, 96, 1, 1, 2, 0),     # 1x1 stride 2 (ResNet downsample): tcgen05 on the output grid
     (2, 24, 9, 11, 40, 1, 1, 2, 0),      # 1x1 stride 2, odd extents (floor)
     (2, 32, 16, 16, 48, 1, 1, 2, 0),     # 1x1 stride 2, P*Q % 4 == 0: strided TMA bwd_filter
+    # strided R, S > 1 (TF32: phase split + stride-1 tcgen05 kernels, phase.cu)
+    (2, 3, 32, 30, 64, 7, 7, 2, 3),      # ResNet-50 stem 7x7/2 pad 3, small image
+    (2, 64, 15, 15, 64, 3, 3, 2, 1),     # 3x3/2 odd extent (floor drops the last row)
+    (2, 128, 16, 16, 128, 3, 3, 2, 1),   # ResNet-50 stage-transition 3x3/2
+    (2, 8, 11, 13, 24, 5, 3, 3, (2, 1)), # stride 3, rectangular kernel, asymmetric pad
+    (2, 16, 12, 10, 32, 3, 3, (2, 1), 1),  # asymmetric stride
+    (3, 12, 9, 9, 20, 2, 2, 2, 0),       # 2x2/2 (phase split has R' = S' = 1)
 ]
 
 
 def _conv_case(shape, seed):
     N, C, H, W, K, R, S_, st, pd = shape
     pd = pd if isinstance(pd, tuple) else (pd, pd)
-    st = (st, st)
+    st = st if isinstance(st, tuple) else (st, st)
     P = oracle.out_extent(H, pd[0], R, st[0])
     Q = oracle.out_extent(W, pd[1], S_, st[1])
     x, f, b, dy = synth.conv_problem_U(N, C, H, W, K, R, S_, P, Q, seed=(seed,))
@@ -532,6 +539,37 @@ def test_resnet_layer_full_size_sampled(S, layer):
     DY = dy.astype(np.float64).reshape(N, K, P, Q)
     idx = [(rng.integers(K), rng.integers(C), rng.integers(R), rng.integers(R)) for _ in range(96)]
     ref = np.array([np.sum(DY[:, k] * X[:, c, r:r + P, s:s + Q]) for k, c, r, s in idx])
+    got = np.array([df[k, c, r, s] for k, c, r, s in idx])
+    assert_close(got, ref, TOL["tf32"], "bwd_filter sampled")
+    assert_close(db, DY.sum(axis=(0, 2, 3)), 1e-4, "db")
+
+
+@pytest.mark.parametrize("layer", [(32, 3, 224, 224, 64, 7, 2, 3),    # ResNet-50 stem
+                                   (32, 128, 56, 56, 128, 3, 2, 1),   # conv3_1 3x3/2 (v1.5)
+                                   (32, 512, 14, 14, 512, 3, 2, 1)])  # conv5_1 3x3/2
+def test_resnet50_strided_full_size_sampled(S, layer):
+    """NEXT-2: the ResNet-50 strided convs at ImageNet size, N = 32 (TF32, phase path).  fwd and
+    bwd_data on two sampled images against the per-image oracle; bwd_filter on 64 sampled
+    entries, each the exact fp64 sum over all images and output positions."""
+    N, C, H, W, K, R, st, pd = layer
+    P = Q = (H + 2 * pd - R) // st + 1
+    x, f, b, dy = synth.conv_problem_U(N, C, H, W, K, R, R, P, Q, seed=(975,))
+    d = S.conv_desc(N, C, H, W, K, R, R, st, pd, "tf32")
+    y = host(S.sysml_conv2d(dev(x), dev(f), d, bias=dev(b))).reshape(N, -1)
+    dx = host(S.sysml_conv2d_bwd_data(dev(f), dev(dy), d)).reshape(N, -1)
+    df, db = S.sysml_conv2d_bwd_filter(dev(x), dev(dy), d)
+    df, db = host(df).reshape(K, C, R, R), host(db)
+    for n in (0, N - 1):
+        yr = oracle.conv2d_fwd(x[n:n + 1], f, 1, C, H, W, K, R, R, (st, st), (pd, pd), bias=b)
+        assert_close(y[n:n + 1], yr, TOL["tf32"], f"fwd image {n}")
+        dxr = oracle.conv2d_bwd_data(f, dy[n:n + 1], 1, C, H, W, K, R, R, (st, st), (pd, pd))
+        assert_close(dx[n:n + 1], dxr, TOL["tf32"], f"bwd_data image {n}")
+    rng = np.random.default_rng(976)
+    X = np.pad(x.astype(np.float64).reshape(N, C, H, W), ((0, 0), (0, 0), (pd, pd), (pd, pd)))
+    DY = dy.astype(np.float64).reshape(N, K, P, Q)
+    idx = [(rng.integers(K), rng.integers(C), rng.integers(R), rng.integers(R)) for _ in range(64)]
+    e = (P - 1) * st + 1
+    ref = np.array([np.sum(DY[:, k] * X[:, c, r:r + e:st, s:s + e:st]) for k, c, r, s in idx])
     got = np.array([df[k, c, r, s] for k, c, r, s in idx])
     assert_close(got, ref, TOL["tf32"], "bwd_filter sampled")
     assert_close(db, DY.sum(axis=(0, 2, 3)), 1e-4, "db")
