@@ -82,6 +82,12 @@ struct TcFwdParams {
   long long *clk;     // optional per-CTA cycle counters (SYSML_TC_PROFILE instrumentation)
   int N, C, H, W, K, R, S, ph, pw, P, Q;
   int sh, sw;          // stride: 1, or > 1 for 1x1 filters (frame = the output grid)
+  // phase-split mode (phase.cu; phs > 0): this is the stride-1 pad-0 problem over the phase
+  // planes X'[n][(a*phw + b)*phC + c][h'][w'] = X[n][c][h'*phs + a - php][w'*phw + b - phpw] of an
+  // original phH x phW image with phC channels.  in_phase: the producer gathers X' straight from
+  // the original X (fwd); out_phase: the plain epilogue writes channel (ab, c), position
+  // (h', w') to dX[n][c][h'*phs + a - php][w'*phw + b - phpw] (bwd_data)
+  int phs, phw, phC, phH, phW, php, phpw, in_phase, out_phase;
   int yH, yW, ysh, ysw;  // plain epilogue: output image yH x yW, row (p, q) -> (p*ysh, q*ysw)
                          // (strided 1x1 bwd_data writes every ysh-th row / ysw-th column)
   int Wf, Hs, Lf;
@@ -154,7 +160,33 @@ __device__ __forceinline__ void load_bias16(const TcFwdParams &p, const float *b
   }
 }
 
+// phase mode gather offset of frame position gi (phase-problem frame, pad 0) for phase ab:
+// n*phC*phH*phW + h*phW + w of the original image, -1 outside it (zero-filled)
+__device__ __forceinline__ int phase_off(const TcFwdParams &p, int64_t gi, int ab) {
+  if (gi >= p.G || ab >= p.phs * p.phw) return -1;
+  const int n = (int)(gi / p.Lf), rem = (int)(gi - (int64_t)n * p.Lf);
+  const int hh = rem / p.Wf, ww = rem - hh * p.Wf;
+  const int a = ab / p.phw, b = ab - a * p.phw;
+  const int h = hh * p.phs + a - p.php, w = ww * p.phw + b - p.phpw;
+  if (hh >= p.H || ww >= p.W || h < 0 || h >= p.phH || w < 0 || w >= p.phW) return -1;
+  return (n * p.phC) * p.phH * p.phW + h * p.phW + w;
+}
+
+// phase-split bwd_data epilogue store (out of line: keeps the common epilogue's registers)
+__device__ __forceinline__ void phase_store16(const TcFwdParams &p, int64_t g, int a, int bb, int c,
+                                              const float *v) {
+  const int n = (int)(g / p.Lf), r2 = (int)(g - (int64_t)n * p.Lf), hh = r2 / p.Wf, q = r2 - hh * p.Wf;
+  const int h = hh * p.phs + a - p.php, w = q * p.phw + bb - p.phpw;
+  if (h < 0 || h >= p.phH || w < 0 || w >= p.phW) return;
+  const int64_t HWo = (int64_t)p.phH * p.phW;
+  float *yo = p.y + ((int64_t)n * p.phC + c) * HWo + (int64_t)h * p.phW + w;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) yo[(int64_t)j * HWo] = v[j];
+}
+
 // plain conv output: lane -> position (linear or 2-D M-tile), 16 filters per chunk
+template <bool PH>  // PH: phase-split modes compiled in (a separate kernel instance, so the
+                   // common instance keeps its register allocation)
 __device__ __forceinline__ void epi_plain(const TcFwdParams &p, uint32_t tbase, int64_t g0, int ft,
                                           int qd, int lane, const float *bias_s, int i0, int istep) {
   const int64_t PQ = (int64_t)p.yH * p.yW;  // output plane (= P*Q unless strided bwd_data)
@@ -191,6 +223,15 @@ __device__ __forceinline__ void epi_plain(const TcFwdParams &p, uint32_t tbase, 
       load_bias16(p, bias_s, k0, b);
       if (!valid) return;
       float *yp = y + ybase + (int64_t)k0 * PQ;
+      if (PH && p.out_phase) {  // phase-split bwd_data: 16 channels of one phase (phC % 16 == 0)
+        const int ab = k0 / p.phC, c = k0 - ab * p.phC, a = ab / p.phw, bb = ab - a * p.phw;
+        if (ab >= p.phs * p.phw) return;  // pad channels
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(cur[j]) + b[j];
+        phase_store16(p, g, a, bb, c, v);
+        return;
+      }
       if (k0 + 16 <= p.K) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) yp[(int64_t)j * PQ] = __uint_as_float(cur[j]) + b[j];
@@ -514,6 +555,7 @@ __device__ __forceinline__ void sk_fixup(const TcFwdParams &p, uint32_t tb, int 
   ptx::tmem_st_wait();
 }
 
+template <bool PH>
 __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const TcFwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t *stage_base = smem;
@@ -731,10 +773,15 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       }
       ptx::named_bar_sync(1, 128);
       const int ntab = p.ks ? p.HALO + 8 : p.HALO;
+      // phase mode: the table holds the gather offsets of phase cur_ab (recomputed below when
+      // the chunk loop crosses into the next phase's channels)
+      int cur_ab = (PH && p.in_phase) ? (c0 * 8) / p.phC : 0;
       for (int pos = tid; pos < ntab; pos += 128) {
         const int64_t gi = g0 + pos;
         int off = -1;
-        if (p.in_plane > 0) {
+        if (PH && p.in_phase) {
+          off = phase_off(p, gi, cur_ab);
+        } else if (p.in_plane > 0) {
           const int64_t si = gi + p.in_shift;  // SPF: zeros are stored, no decoding
           if (gi < p.G && si >= 0 && si < p.in_plane) off = (int)si;
         } else if (gi < p.G) {
@@ -778,9 +825,21 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
             }
           }
         } else {
-          const int c0 = ch * 8;
-          const int nc = min(8, p.C - c0);
-          const int64_t cstride = p.in_plane > 0 ? p.in_plane : (int64_t)HW;
+          int c0 = ch * 8;
+          int nc = min(8, p.C - c0);
+          int64_t cstride = p.in_plane > 0 ? p.in_plane : (int64_t)HW;
+          if (PH && p.in_phase) {
+            const int ab = c0 / p.phC;
+            if (ab != cur_ab) {  // next phase: every producer has issued from the old table
+              ptx::named_bar_sync(1, 128);
+              for (int pos = tid; pos < p.HALO; pos += 128) src_off[pos] = phase_off(p, g0 + pos, ab);
+              ptx::named_bar_sync(1, 128);
+              cur_ab = ab;
+            }
+            c0 -= ab * p.phC;  // channel of the original image (phC % 8 == 0)
+            nc = ab < p.phs * p.phw ? 8 : 0;  // pad channels: zero-fill
+            cstride = (int64_t)p.phH * p.phW;
+          }
           const float *xc = p.x + c0 * cstride;
           for (int pos = tid; pos < p.HALO; pos += 128) {
             const int off = src_off[pos];
@@ -905,7 +964,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       } else if (p.pool) {
         epi_pool2(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
       } else {
-        epi_plain(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
+        epi_plain<PH>(p, tbase, g0, ft, qd, lane, bias_s, eset, 2);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -1275,7 +1334,13 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
   p.parg = parg;
   if (!bias) p.bias_smem = 0;
   static int attr = 0;
-  SYSML_TRY(set_smem_attr(tc_conv_fwd_kernel, pl.smem, attr));
+  const bool ph = p.in_phase || p.out_phase;
+  if (ph) {
+    static int attr_ph = 0;
+    SYSML_TRY(set_smem_attr(tc_conv_fwd_kernel<true>, pl.smem, attr_ph));
+  } else {
+    SYSML_TRY(set_smem_attr(tc_conv_fwd_kernel<false>, pl.smem, attr));
+  }
   int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
   // stream-K (opt-in, SYSML_TC_SK=1): even chunk-iteration ranges per CTA instead of whole
   // tiles.  Measured slower on every shape of this build -- single-buffered accumulators
@@ -1332,7 +1397,7 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
-    SYSML_CUDA(cudaLaunchKernelEx(&cfg, tc_conv_fwd_kernel, p));
+    SYSML_CUDA(cudaLaunchKernelEx(&cfg, ph ? tc_conv_fwd_kernel<true> : tc_conv_fwd_kernel<false>, p));
   }
   SYSML_LAUNCH_CHECK();
   if (prof) {
@@ -2106,6 +2171,53 @@ sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy
     SYSML_CUDA(cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)a.N * a.C * a.H * a.W, st));
   // filter bank F is (K x C*RS) = (Cin_of_this_conv x Kout*RS) -> flip = 1
   return run_fwd(pl, dy, f, 1, a.K, nullptr, dx, nullptr, nullptr, ws, st);
+}
+
+// ------------------------------------------------------------------ phase-split entry points
+// (phase.cu): `b` is the stride-1 pad-0 phase problem of the strided conv `a`; X' is gathered
+// from X by the producer (fwd) and dX' scattered to dX by the epilogue (bwd_data), so neither
+// phase tensor exists in HBM.
+static void set_phase(TcFwdParams &p, const ConvArgs &a) {
+  p.phs = a.sh; p.phw = a.sw; p.phC = a.C; p.phH = a.H; p.phW = a.W; p.php = a.ph; p.phpw = a.pw;
+}
+
+bool tc_fwd_phase_fused_ok(const ConvArgs &a, const ConvArgs &b) {
+  if (a.C % 8 || (int64_t)a.N * a.C * a.H * a.W >= (1ll << 31)) return false;
+  const TcPlan pl = plan_fwd(b.N, b.C, b.H, b.W, b.K, b.R, b.S, 0, 0, nullptr, true);
+  return pl.ok && !pl.p.ks && !pl.p.abulk;
+}
+
+sysml_status tc_conv_fwd_phase(const ConvArgs &a, const ConvArgs &b, const float *x, const float *fp,
+                               const float *bias, float *y, void *ws, cudaStream_t st) {
+  TcPlan pl = plan_fwd(b.N, b.C, b.H, b.W, b.K, b.R, b.S, 0, 0, nullptr, true);
+  if (!pl.ok || pl.p.ks || pl.p.abulk) {
+    set_error("tcgen05 phase forward: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  set_phase(pl.p, a);
+  pl.p.in_phase = 1;
+  return run_fwd(pl, x, fp, 0, b.C, bias, y, nullptr, nullptr, ws, st);
+}
+
+bool tc_bwd_data_phase_fused_ok(const ConvArgs &a, const ConvArgs &b) {
+  if (a.C % 16 || (int64_t)a.N * a.C * a.H * a.W >= (1ll << 31) || !tc_bwd_data_supported(b)) return false;
+  const TcPlan pl = plan_bwd_data(b);
+  return pl.ok && !pl.p.sn && !pl.p.tile2d && !pl.p.pool;
+}
+
+sysml_status tc_conv_bwd_data_phase(const ConvArgs &a, const ConvArgs &b, const float *fp, const float *dy,
+                                    float *dx, void *ws, cudaStream_t st) {
+  TcPlan pl = plan_bwd_data(b);
+  if (!pl.ok || pl.p.sn || pl.p.tile2d) {
+    set_error("tcgen05 phase bwd_data: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  // positions no phase cell reaches (floor extent) receive no contribution
+  if ((int64_t)b.H * a.sh - a.ph < a.H || (int64_t)b.W * a.sw - a.pw < a.W)
+    SYSML_CUDA(cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)a.N * a.C * a.H * a.W, st));
+  set_phase(pl.p, a);
+  pl.p.out_phase = 1;
+  return run_fwd(pl, dy, fp, 1, b.K, nullptr, dx, nullptr, nullptr, ws, st);
 }
 
 // ------------------------------------------------------------------ SPF-layout entry points

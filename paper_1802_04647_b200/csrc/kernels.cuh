@@ -95,6 +95,14 @@ size_t tc_fwd_ws(const ConvArgs &a);
 sysml_status tc_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
                          float *y, const PoolArgs *pool, float *pout, int32_t *parg, void *ws,
                          cudaStream_t st, const sysml_csr *csr = nullptr);
+// phase-split modes of the forward kernel (conv_tc.cu): a = the strided conv, b = its
+// stride-1 pad-0 phase problem (phase.cu); the gather / scatter of X' / dX' happens in-kernel
+bool tc_fwd_phase_fused_ok(const ConvArgs &a, const ConvArgs &b);
+sysml_status tc_conv_fwd_phase(const ConvArgs &a, const ConvArgs &b, const float *x, const float *fp,
+                               const float *bias, float *y, void *ws, cudaStream_t st);
+bool tc_bwd_data_phase_fused_ok(const ConvArgs &a, const ConvArgs &b);
+sysml_status tc_conv_bwd_data_phase(const ConvArgs &a, const ConvArgs &b, const float *fp, const float *dy,
+                                    float *dx, void *ws, cudaStream_t st);
 // phase.cu : strided convs with R or S > 1 as stride-1 tcgen05 convs over the phase-split
 // input (space-to-depth); DESIGN.md §7 "Strided convolutions"
 bool phase_fwd_supported(const ConvArgs &a);
@@ -131,8 +139,11 @@ sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float
 // NCHW entry: framing pre-pass + the TMA kernel (stride 1, C % 8 == 0)
 bool tc_wgrad_frame_supported(const ConvArgs &a);
 size_t tc_wgrad_frame_ws(const ConvArgs &a);
+// x_framed: x is already in the frame layout of tc_wgrad_frame_geom (planes [c][plane],
+// image n at n*Hs*Wf, pixel (h, w) at (h + ph)*Wf + w + pw, zeros elsewhere)
 sysml_status tc_wgrad_frame(const ConvArgs &a, const float *x, const float *dy, float *df,
-                            float *db, void *ws, cudaStream_t st);
+                            float *db, void *ws, cudaStream_t st, bool x_framed = false);
+void tc_wgrad_frame_geom(const ConvArgs &a, int *Hs, int *Wf, int64_t *plane);
 size_t tc_wgrad_spf_ws(const SpfConv &sc);
 sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy_spf, float *df,
                           float *db, void *ws, cudaStream_t st);

@@ -24,16 +24,20 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
 
 namespace sysml {
 
 namespace {
 
+constexpr int PH_SMEM_FLOATS = 8192;  // 32 KB of staged rows per block (gather kernels)
+
 ConvArgs phase_args(const ConvArgs &a) {
   ConvArgs b{};
   b.N = a.N;
   b.K = a.K;
-  b.C = a.sh * a.sw * a.C;
+  b.C = (a.sh * a.sw * a.C + 7) / 8 * 8;  // pad channels (zero planes / zero filters): the
+                                         // frame bwd_filter and the 8-channel chunks want C % 8 == 0
   b.R = (a.R + a.sh - 1) / a.sh;
   b.S = (a.S + a.sw - 1) / a.sw;
   b.P = a.P;
@@ -47,37 +51,88 @@ ConvArgs phase_args(const ConvArgs &a) {
 
 bool is_phase_shape(const ConvArgs &a) {
   static const bool off = getenv("SYSML_NO_PHASE") != nullptr;  // A/B switch: FP32 SIMT instead
-  return !off && (a.sh > 1 || a.sw > 1) && (a.R > 1 || a.S > 1) && a.sh <= 4 && a.sw <= 4;
+  if (off || !((a.sh > 1 || a.sw > 1) && (a.R > 1 || a.S > 1)) || a.sh > 4 || a.sw > 4) return false;
+  // the gathers stage sh input rows / sh*sw phase rows per block in shared memory
+  const ConvArgs b = phase_args(a);
+  return (int64_t)a.sh * a.W <= PH_SMEM_FLOATS && (int64_t)a.sh * a.sw * b.W <= PH_SMEM_FLOATS;
+}
+
+// SYSML_PHASE_FUSED=0: materialise X' / dX' with the gather kernels instead of the in-kernel
+// gather / scatter (A/B switch; also exercises the unfused path in tests)
+bool fused_ok() {
+  static const bool on = [] {
+    const char *e = getenv("SYSML_PHASE_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 int grid_for(int64_t total) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 16ll * sm_count()));
 }
 
-// X (N x C*H*W) -> X' (N x C'*H'*W'), one write per X' element, zero outside the padded image
-__global__ void phase_split_x_kernel(const float *__restrict__ x, float *__restrict__ xp, int C, int H,
-                                     int W, int sh, int sw, int ph, int pw, int C2, int H2, int W2,
-                                     int64_t total) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int w2 = (int)(i % W2);
-    int64_t t = i / W2;
-    const int h2 = (int)(t % H2);
-    t /= H2;
-    const int c2 = (int)(t % C2);
-    const int64_t n = t / C2;
-    const int c = c2 % C, ab = c2 / C, a = ab / sw, b = ab - a * sw;
-    const int h = h2 * sh + a - ph, w = w2 * sw + b - pw;
-    float v = 0.f;
-    if (h >= 0 && h < H && w >= 0 && w < W) v = __ldg(x + ((n * C + c) * H + h) * (int64_t)W + w);
-    xp[i] = v;
+// X (N x C*H*W) -> X' (N x C'*H'*W'), zero outside the padded image and in the pad channels.
+// Block (n*C + c, chunk of `rows` h' rows) stages the input rows it needs, [h0*sh - ph,
+// (h0 + rows)*sh - ph), in shared memory with coalesced loads, then writes every phase row
+// (a, b, h') of the chunk with coalesced stores (the stride-sw reads hit shared memory).
+// Pad-channel planes (C' rounded up to 8) are extra blocks past N*C that only write zeros.
+// Output element (n, c', h', w') lives at c'*cstride + n*nstride + h'*Wrow + w' (NCHW: cstride =
+// H'W', nstride = C'H'W', Wrow = W'; the framed bwd_filter layout: cstride = plane, nstride =
+// H'*Wf, Wrow = Wf); columns W' .. Wrow-1 are written as zeros.
+
+template <int SW>  // the column stride sw, compile-time so w <-> (w', b) needs no division
+__global__ void __launch_bounds__(256) phase_split_x_kernel(const float *__restrict__ x, float *__restrict__ xp,
+                                                            int N, int C, int H, int W, int sh, int ph,
+                                                            int pw, int C2, int H2, int W2, int rows,
+                                                            int64_t cstride, int64_t nstride, int Wrow) {
+  __shared__ float srow[PH_SMEM_FLOATS];
+  constexpr int sw = SW;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int h0 = blockIdx.y * rows, nrows = min(rows, H2 - h0);
+  const int Cph = sh * sw * C;
+  if (blockIdx.x >= (unsigned)N * C) {  // zero plane of a pad channel
+    const int i = blockIdx.x - N * C, npad = C2 - Cph, n = i / npad, c2 = Cph + i % npad;
+    float *dst = xp + c2 * cstride + n * nstride + (int64_t)h0 * Wrow;
+    for (int e = tid; e < nrows * Wrow; e += 256) dst[e] = 0.f;
+    return;
+  }
+  const int n = blockIdx.x / C, c = blockIdx.x - n * C;
+  const float *xs = x + (int64_t)blockIdx.x * H * W;
+  // stage input rows hin = h0*sh - ph + j, j < nrows*sh (zero rows outside the image): a warp
+  // per row, lanes over w -- no per-element index division (the kernel is issue-bound otherwise)
+  // 4-byte cp.async (zero-fill outside the image): every copy of the thread is in flight at
+  // once (plain load -> st.shared chains left the kernel latency-bound at ~2 loads per warp)
+  const int hbase = h0 * sh - ph;
+  const uint32_t sbase = ptx::smem_u32(srow);
+  for (int j = threadIdx.y; j < nrows * sh; j += 8) {
+    const int h = hbase + j;
+    const bool ok = h >= 0 && h < H;
+    const float *src = ok ? xs + (int64_t)h * W : xs;
+    for (int w = threadIdx.x; w < W; w += 32)
+      ptx::cp_async4(sbase + 4u * (j * W + w), ok ? src + w : xs, ok ? 4u : 0u);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  // a warp per output row (a, b, h'), lanes over w'; nested loops keep index divisions out of
+  // the row loop (rows are short, so per-row overhead is what the kernel issues)
+  for (int ab = 0; ab < sh * sw; ++ab) {
+    const int a = ab / sw, b = ab - a * sw;
+    float *dst0 = xp + (ab * C + c) * cstride + n * nstride + (int64_t)h0 * Wrow;
+    const float *s0 = srow + a * W + b - pw;
+    for (int hl = threadIdx.y; hl < nrows; hl += 8) {
+      const float *src = s0 + hl * sh * W;
+      float *dst = dst0 + (int64_t)hl * Wrow;
+      for (int w2 = threadIdx.x; w2 < Wrow; w2 += 32) {
+        const int w = w2 * sw + b - pw;
+        dst[w2] = (w2 < W2 && (unsigned)w < (unsigned)W) ? src[w2 * sw] : 0.f;
+      }
+    }
   }
 }
 
-// F (K x C*R*S) -> F' (K x C'*R'*S'), zero for the padded taps
+// F (K x C*R*S) -> F' (K x C'*R'*S'), zero for the padded taps and the pad channels
 __global__ void phase_split_f_kernel(const float *__restrict__ f, float *__restrict__ fp, int C, int R,
-                                     int S, int sh, int sw, int R2, int S2, int64_t total) {
-  const int C2 = sh * sw * C;
+                                     int S, int sh, int sw, int C2, int R2, int S2, int64_t total) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int s2 = (int)(i % S2);
@@ -88,36 +143,54 @@ __global__ void phase_split_f_kernel(const float *__restrict__ f, float *__restr
     const int64_t k = t / C2;
     const int c = c2 % C, ab = c2 / C, a = ab / sw, b = ab - a * sw;
     const int r = r2 * sh + a, s = s2 * sw + b;
-    fp[i] = (r < R && s < S) ? __ldg(f + ((k * C + c) * R + r) * (int64_t)S + s) : 0.f;
+    fp[i] = (ab < sh * sw && r < R && s < S) ? __ldg(f + ((k * C + c) * R + r) * (int64_t)S + s) : 0.f;
   }
 }
 
 // dX'(N x C'*H'*W') -> dX (N x C*H*W): the transpose of phase_split_x (a gather, each Xp
-// position belongs to exactly one phase cell)
-__global__ void phase_merge_dx_kernel(const float *__restrict__ dxp, float *__restrict__ dx, int C, int H,
-                                      int W, int sh, int sw, int ph, int pw, int C2, int H2, int W2,
-                                      int64_t total) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int w = (int)(i % W);
-    int64_t t = i / W;
-    const int h = (int)(t % H);
-    t /= H;
-    const int c = (int)(t % C);
-    const int64_t n = t / C;
-    const int hp = h + ph, wp = w + pw;
-    const int h2 = hp / sh, a = hp - h2 * sh, w2 = wp / sw, b = wp - w2 * sw;
-    float v = 0.f;
-    if (h2 < H2 && w2 < W2)
-      v = __ldg(dxp + ((n * C2 + (int64_t)(a * sw + b) * C + c) * H2 + h2) * (int64_t)W2 + w2);
-    dx[i] = v;
+// position belongs to exactly one phase cell).  Block (n*C + c, chunk of `rows` dX rows,
+// rows % sh == 0 and (h0 + ph) % sh == 0 unless clipped) stages the phase rows it needs, h' in
+// [(h0 + ph)/sh, .. + rows/sh), from all sh*sw phase planes with coalesced loads, then writes
+// the dX rows coalesced.
+template <int SW>
+__global__ void __launch_bounds__(256) phase_merge_dx_kernel(const float *__restrict__ dxp, float *__restrict__ dx,
+                                                             int C, int H, int W, int sh, int ph, int pw,
+                                                             int C2, int H2, int W2, int rows) {
+  __shared__ float srow[PH_SMEM_FLOATS];
+  constexpr int sw = SW;
+  // chunk in padded-row space: hp in [blockIdx.y*rows, +rows), rows a multiple of sh
+  const int hp0 = blockIdx.y * rows, h2b = hp0 / sh, nh2 = min(rows / sh, H2 - h2b);
+  const int n = blockIdx.x / C, c = blockIdx.x - n * C;
+  // stage [ab][h2 - h2b][w2] for the sh*sw phase planes of channel c: a warp per phase row
+  const int per = nh2 > 0 ? nh2 * W2 : 0;
+  const uint32_t sbase = ptx::smem_u32(srow);
+  for (int ab = 0; ab < sh * sw; ++ab) {
+    const float *src0 = dxp + ((int64_t)(n * C2 + ab * C + c) * H2 + h2b) * W2;
+    const uint32_t dst0 = sbase + 4u * (ab * per);
+    for (int hl = threadIdx.y; hl < nh2; hl += 8)
+      for (int w2 = threadIdx.x; w2 < W2; w2 += 32)
+        ptx::cp_async4(dst0 + 4u * (hl * W2 + w2), src0 + hl * W2 + w2, 4u);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  float *out = dx + (int64_t)blockIdx.x * H * W;
+  for (int a = 0; a < sh; ++a) {
+    for (int hl = threadIdx.y; hl * sh < rows; hl += 8) {
+      const int h = hp0 + hl * sh + a - ph;
+      if (h < 0 || h >= H) continue;
+      const float *src = srow + a * sw * per + hl * W2;
+      float *o = out + (int64_t)h * W;
+      for (int w = threadIdx.x; w < W; w += 32) {
+        const int wp = w + pw, w2 = wp / sw, b = wp - w2 * sw;
+        o[w] = (hl < nh2 && w2 < W2) ? src[b * per + w2] : 0.f;
+      }
+    }
   }
 }
 
 // dF' (K x C'*R'*S') -> dF (K x C*R*S)
 __global__ void phase_merge_df_kernel(const float *__restrict__ dfp, float *__restrict__ df, int C, int R,
-                                      int S, int sh, int sw, int R2, int S2, int64_t total) {
-  const int C2 = sh * sw * C;
+                                      int S, int sh, int sw, int C2, int R2, int S2, int64_t total) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int s = (int)(i % S);
@@ -132,23 +205,52 @@ __global__ void phase_merge_df_kernel(const float *__restrict__ dfp, float *__re
 }
 
 size_t x2_bytes(const ConvArgs &b) {
-  return align_up((size_t)b.N * b.C * b.H * b.W * sizeof(float), 256);
+  size_t n = (size_t)b.N * b.C * b.H * b.W;
+  if (tc_wgrad_frame_supported(b)) {  // bwd_filter may write the framed layout (>= NCHW size)
+    int Hs, Wf;
+    int64_t plane;
+    tc_wgrad_frame_geom(b, &Hs, &Wf, &plane);
+    n = std::max(n, (size_t)b.C * plane);
+  }
+  return align_up(n * sizeof(float), 256);
 }
 size_t f2_bytes(const ConvArgs &b) {
   return align_up((size_t)b.K * b.C * b.R * b.S * sizeof(float), 256);
 }
 
-sysml_status split_x(const ConvArgs &a, const ConvArgs &b, const float *x, float *xp, cudaStream_t st) {
-  const int64_t total = (int64_t)b.N * b.C * b.H * b.W;
-  phase_split_x_kernel<<<grid_for(total), 256, 0, st>>>(x, xp, a.C, a.H, a.W, a.sh, a.sw, a.ph, a.pw,
-                                                        b.C, b.H, b.W, total);
+// frame: write the framed bwd_filter layout (tc_wgrad_frame_geom) instead of NCHW
+sysml_status split_x(const ConvArgs &a, const ConvArgs &b, const float *x, float *xp, cudaStream_t st,
+                     bool frame = false) {
+  int64_t cstride = (int64_t)b.H * b.W, nstride = (int64_t)b.C * b.H * b.W;
+  int Wrow = b.W;
+  if (frame) {
+    int Hs, Wf;
+    int64_t plane;
+    tc_wgrad_frame_geom(b, &Hs, &Wf, &plane);
+    cstride = plane;
+    nstride = (int64_t)Hs * Wf;
+    Wrow = Wf;
+  }
+  const int rows = std::max(1, std::min(b.H, PH_SMEM_FLOATS / (a.sh * a.W)));
+  const dim3 grid((unsigned)((int64_t)b.N * (b.C - a.sh * a.sw * a.C) + (int64_t)a.N * a.C),
+                  (unsigned)ceil_div(b.H, rows));
+#define SYSML_PH_SPLIT(SWV)                                                                            \
+  phase_split_x_kernel<SWV><<<grid, dim3(32, 8), 0, st>>>(x, xp, a.N, a.C, a.H, a.W, a.sh, a.ph, a.pw, b.C, b.H, \
+                                                          b.W, rows, cstride, nstride, Wrow)
+  switch (a.sw) {
+    case 1: SYSML_PH_SPLIT(1); break;
+    case 2: SYSML_PH_SPLIT(2); break;
+    case 3: SYSML_PH_SPLIT(3); break;
+    default: SYSML_PH_SPLIT(4); break;
+  }
+#undef SYSML_PH_SPLIT
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;
 }
 
 sysml_status split_f(const ConvArgs &a, const ConvArgs &b, const float *f, float *fp, cudaStream_t st) {
   const int64_t total = (int64_t)b.K * b.C * b.R * b.S;
-  phase_split_f_kernel<<<grid_for(total), 256, 0, st>>>(f, fp, a.C, a.R, a.S, a.sh, a.sw, b.R, b.S,
+  phase_split_f_kernel<<<grid_for(total), 256, 0, st>>>(f, fp, a.C, a.R, a.S, a.sh, a.sw, b.C, b.R, b.S,
                                                         total);
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;
@@ -173,8 +275,10 @@ sysml_status phase_conv_fwd(const ConvArgs &a, const float *x, const float *f, c
   float *xp = wc.take<float>((size_t)b.N * b.C * b.H * b.W);
   float *fp = wc.take<float>((size_t)b.K * b.C * b.R * b.S);
   void *tws = wc.take<char>(tc_fwd_ws(b));
-  SYSML_TRY(split_x(a, b, x, xp, st));
   SYSML_TRY(split_f(a, b, f, fp, st));
+  if (fused_ok() && tc_fwd_phase_fused_ok(a, b))  // X' gathered by the conv kernel's producer
+    return tc_conv_fwd_phase(a, b, x, fp, bias, y, tws, st);
+  SYSML_TRY(split_x(a, b, x, xp, st));
   return tc_conv_fwd(b, xp, fp, bias, y, nullptr, nullptr, nullptr, tws, st);
 }
 
@@ -196,10 +300,22 @@ sysml_status phase_conv_bwd_data(const ConvArgs &a, const float *f, const float 
   float *fp = wc.take<float>((size_t)b.K * b.C * b.R * b.S);
   void *tws = wc.take<char>(tc_bwd_data_ws(b));
   SYSML_TRY(split_f(a, b, f, fp, st));
+  if (fused_ok() && tc_bwd_data_phase_fused_ok(a, b))  // dX' scattered by the conv epilogue
+    return tc_conv_bwd_data_phase(a, b, fp, dy, dx, tws, st);
   SYSML_TRY(tc_conv_bwd_data(b, fp, dy, dxp, tws, st));
-  const int64_t total = (int64_t)a.N * a.C * a.H * a.W;
-  phase_merge_dx_kernel<<<grid_for(total), 256, 0, st>>>(dxp, dx, a.C, a.H, a.W, a.sh, a.sw, a.ph, a.pw,
-                                                         b.C, b.H, b.W, total);
+  // rows of padded-image space per block: a multiple of sh whose phase rows fit in smem
+  const int rows = a.sh * std::max(1, std::min((a.H + a.ph + a.sh - 1) / a.sh, PH_SMEM_FLOATS / (a.sh * a.sw * b.W)));
+  const dim3 grid((unsigned)((int64_t)a.N * a.C), (unsigned)ceil_div(a.H + a.ph, rows));
+#define SYSML_PH_MERGE(SWV)                                                                          \
+  phase_merge_dx_kernel<SWV><<<grid, dim3(32, 8), 0, st>>>(dxp, dx, a.C, a.H, a.W, a.sh, a.ph, a.pw, b.C, b.H, \
+                                                           b.W, rows)
+  switch (a.sw) {
+    case 1: SYSML_PH_MERGE(1); break;
+    case 2: SYSML_PH_MERGE(2); break;
+    case 3: SYSML_PH_MERGE(3); break;
+    default: SYSML_PH_MERGE(4); break;
+  }
+#undef SYSML_PH_MERGE
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;
 }
@@ -218,13 +334,18 @@ sysml_status phase_conv_bwd_filter(const ConvArgs &a, const float *x, const floa
                                    float *db, void *ws, cudaStream_t st) {
   const ConvArgs b = phase_args(a);
   WsCarve wc(ws, (size_t)-1);
-  float *xp = wc.take<float>((size_t)b.N * b.C * b.H * b.W);
+  float *xp = reinterpret_cast<float *>(wc.take<char>(x2_bytes(b)));
   float *dfp = wc.take<float>((size_t)b.K * b.C * b.R * b.S);
   void *tws = wc.take<char>(tc_bwd_filter_ws(b));
-  SYSML_TRY(split_x(a, b, x, xp, st));
-  SYSML_TRY(tc_conv_bwd_filter(b, xp, dy, dfp, db, tws, st));
+  if (tc_wgrad_frame_supported(b)) {  // X' written straight into the frame (no second pass)
+    SYSML_TRY(split_x(a, b, x, xp, st, /*frame=*/true));
+    SYSML_TRY(tc_wgrad_frame(b, xp, dy, dfp, db, tws, st, /*x_framed=*/true));
+  } else {
+    SYSML_TRY(split_x(a, b, x, xp, st));
+    SYSML_TRY(tc_conv_bwd_filter(b, xp, dy, dfp, db, tws, st));
+  }
   const int64_t total = (int64_t)a.K * a.C * a.R * a.S;
-  phase_merge_df_kernel<<<grid_for(total), 256, 0, st>>>(dfp, df, a.C, a.R, a.S, a.sh, a.sw, b.R, b.S,
+  phase_merge_df_kernel<<<grid_for(total), 256, 0, st>>>(dfp, df, a.C, a.R, a.S, a.sh, a.sw, b.C, b.R, b.S,
                                                          total);
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;

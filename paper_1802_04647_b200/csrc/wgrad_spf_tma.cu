@@ -705,8 +705,15 @@ size_t tc_wgrad_frame_ws(const ConvArgs &a) {
   return f.ok ? f.x_bytes + f.dy_bytes + tc_wgrad_spf_tma_ws(f.sc) : 0;
 }
 
+void tc_wgrad_frame_geom(const ConvArgs &a, int *Hs, int *Wf, int64_t *plane) {
+  const FramePlan f = plan_frame(a);
+  *Hs = f.Hs;
+  *Wf = f.Wf;
+  *plane = f.plane;
+}
+
 sysml_status tc_wgrad_frame(const ConvArgs &a, const float *x, const float *dy, float *df,
-                            float *db, void *ws, cudaStream_t st) {
+                            float *db, void *ws, cudaStream_t st, bool x_framed) {
   const FramePlan f = plan_frame(a);
   if (!f.ok) {
     set_error("tcgen05 framed bwd_filter: unsupported shape");
@@ -716,9 +723,13 @@ sysml_status tc_wgrad_frame(const ConvArgs &a, const float *x, const float *dy, 
   float *dyf = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + f.x_bytes);
   void *ws2 = reinterpret_cast<char *>(ws) + f.x_bytes + f.dy_bytes;
   const int blocks = 8 * sm_count();
-  nchw_to_frame_kernel<<<blocks, 256, 0, st>>>(x, xf, (int)a.N, (int)a.C, (int)a.H, (int)a.W, f.Hs, f.Wf,
-                                               (int)a.ph, (int)a.pw, f.plane);
-  SYSML_LAUNCH_CHECK();
+  if (x_framed) {
+    xf = const_cast<float *>(x);  // caller wrote X in the frame layout already (phase.cu)
+  } else {
+    nchw_to_frame_kernel<<<blocks, 256, 0, st>>>(x, xf, (int)a.N, (int)a.C, (int)a.H, (int)a.W, f.Hs,
+                                                 f.Wf, (int)a.ph, (int)a.pw, f.plane);
+    SYSML_LAUNCH_CHECK();
+  }
   float *psum = reinterpret_cast<float *>(reinterpret_cast<char *>(dyf) +
                                           align_up((size_t)a.K * f.plane * sizeof(float), 256));
   nchw_to_frame_sum_kernel<<<blocks, 256, 0, st>>>(dy, dyf, db ? psum : nullptr, (int)a.N, (int)a.K,

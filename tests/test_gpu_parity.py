@@ -394,6 +394,22 @@ def test_stream_k_opt_in_parity():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+def test_phase_unfused_parity():
+    """Strided R, S > 1 convs with the phase tensors materialised (SYSML_PHASE_FUSED=0: the
+    X' / dX' gather kernels instead of the in-kernel gather / scatter), and with the phase path
+    off (SYSML_NO_PHASE=1: the FP32-SIMT kernels under TF32), re-run in child processes."""
+    import os
+    import subprocess
+    import sys
+    for var, val in (("SYSML_PHASE_FUSED", "0"), ("SYSML_NO_PHASE", "1")):
+        env = dict(os.environ, **{var: val})
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                            os.path.abspath(__file__), "-k",
+                            "(test_conv_fwd_bwd_parity and tf32) or resnet50 or (random and tf32)"],
+                           env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, var + ": " + r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_lenet_step_nccl_bucketed_allreduce(S):
     """sysml_lenet_step with a communicator: the bucketed allreduce overlapped on the handle's
     side stream ({F2,b2,W3,b3} after conv2 bwd_filter, {F1,b1} at the end) gives bitwise the
