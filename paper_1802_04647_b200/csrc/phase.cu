@@ -84,8 +84,8 @@ template <int SW>  // the column stride sw, compile-time so w <-> (w', b) needs 
 __global__ void __launch_bounds__(256) phase_split_x_kernel(const float *__restrict__ x, float *__restrict__ xp,
                                                             int N, int C, int H, int W, int sh, int ph,
                                                             int pw, int C2, int H2, int W2, int rows,
-                                                            int64_t cstride, int64_t nstride, int Wrow) {
-  __shared__ float srow[PH_SMEM_FLOATS];
+                                                            int64_t cstride, int64_t nstride, int Wrow, int vec) {
+  __shared__ __align__(16) float srow[PH_SMEM_FLOATS];
   constexpr int sw = SW;
   const int tid = threadIdx.y * 32 + threadIdx.x;
   const int h0 = blockIdx.y * rows, nrows = min(rows, H2 - h0);
@@ -104,15 +104,47 @@ __global__ void __launch_bounds__(256) phase_split_x_kernel(const float *__restr
   // once (plain load -> st.shared chains left the kernel latency-bound at ~2 loads per warp)
   const int hbase = h0 * sh - ph;
   const uint32_t sbase = ptx::smem_u32(srow);
-  for (int j = threadIdx.y; j < nrows * sh; j += 8) {
-    const int h = hbase + j;
-    const bool ok = h >= 0 && h < H;
-    const float *src = ok ? xs + (int64_t)h * W : xs;
-    for (int w = threadIdx.x; w < W; w += 32)
-      ptx::cp_async4(sbase + 4u * (j * W + w), ok ? src + w : xs, ok ? 4u : 0u);
+  if (vec) {
+    // W % 4 == 0, 16-byte aligned planes: the staged rows are one contiguous span of the
+    // plane, copied as 16-byte chunks (rows outside the image zero-filled)
+    const int nq = nrows * sh * W / 4, q4w = W / 4;
+    for (int e = tid; e < nq; e += 256) {
+      const int j = e / q4w, h = hbase + j;
+      const bool ok = h >= 0 && h < H;
+      ptx::cp_async16(sbase + 16u * e, ok ? xs + (int64_t)h * W + 4 * (e - j * q4w) : xs, ok ? 16u : 0u);
+    }
+  } else {
+    for (int j = threadIdx.y; j < nrows * sh; j += 8) {
+      const int h = hbase + j;
+      const bool ok = h >= 0 && h < H;
+      const float *src = ok ? xs + (int64_t)h * W : xs;
+      for (int w = threadIdx.x; w < W; w += 32)
+        ptx::cp_async4(sbase + 4u * (j * W + w), ok ? src + w : xs, ok ? 4u : 0u);
+    }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if (vec && (Wrow & 3) == 0) {
+    // 16-byte stores: thread -> (phase row, 4 consecutive w'); 4 strided shared reads each
+    const int nq = Wrow / 4, per_ab = nrows * nq;
+    for (int ab = 0; ab < sh * sw; ++ab) {
+      const int a = ab / sw, b = ab - a * sw;
+      float *dst0 = xp + (ab * C + c) * cstride + n * nstride + (int64_t)h0 * Wrow;
+      const float *s0 = srow + a * W + b - pw;
+      for (int e = tid; e < per_ab; e += 256) {
+        const int hl = e / nq, q4 = e - hl * nq;
+        const float *src = s0 + hl * sh * W;
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int w2 = 4 * q4 + k, w = w2 * sw + b - pw;
+          v[k] = (w2 < W2 && (unsigned)w < (unsigned)W) ? src[w2 * sw] : 0.f;
+        }
+        *reinterpret_cast<float4 *>(dst0 + (int64_t)hl * Wrow + 4 * q4) = make_float4(v[0], v[1], v[2], v[3]);
+      }
+    }
+    return;
+  }
   // a warp per output row (a, b, h'), lanes over w'; nested loops keep index divisions out of
   // the row loop (rows are short, so per-row overhead is what the kernel issues)
   for (int ab = 0; ab < sh * sw; ++ab) {
@@ -234,9 +266,13 @@ sysml_status split_x(const ConvArgs &a, const ConvArgs &b, const float *x, float
   const int rows = std::max(1, std::min(b.H, PH_SMEM_FLOATS / (a.sh * a.W)));
   const dim3 grid((unsigned)((int64_t)b.N * (b.C - a.sh * a.sw * a.C) + (int64_t)a.N * a.C),
                   (unsigned)ceil_div(b.H, rows));
+  // 16-byte paths: input rows 16-byte aligned; output rows too (frame: Wf % 8 == 0, plane % 4
+  // == 0; NCHW: W' % 4 == 0 and H'W' % 4 == 0)
+  const int vec = (a.W % 4 == 0) && (((uintptr_t)x & 15) == 0) && (((uintptr_t)xp & 15) == 0) &&
+                  (Wrow % 4 == 0) && (cstride % 4 == 0) && (nstride % 4 == 0);
 #define SYSML_PH_SPLIT(SWV)                                                                            \
   phase_split_x_kernel<SWV><<<grid, dim3(32, 8), 0, st>>>(x, xp, a.N, a.C, a.H, a.W, a.sh, a.ph, a.pw, b.C, b.H, \
-                                                          b.W, rows, cstride, nstride, Wrow)
+                                                          b.W, rows, cstride, nstride, Wrow, vec)
   switch (a.sw) {
     case 1: SYSML_PH_SPLIT(1); break;
     case 2: SYSML_PH_SPLIT(2); break;
