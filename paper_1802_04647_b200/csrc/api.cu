@@ -7,6 +7,7 @@
 //     math == TF32 and the tcgen05 kernel covers the shape -> conv_tc.cu (K3/K5/K6)
 //     TF32, strided with R or S > 1, stride-1 image covered -> phase.cu (phase split +
 //                                                              the tcgen05 stride-1 kernels)
+//     TF32 bwd_filter, C < 8, P*Q % 4 == 0                   -> phase.cu im2col + 1x1 TMA GEMM
 //     otherwise                                             -> conv_simt.cu (fp32 FMA)
 //   CSR input: fwd -> csr.cu K7 (fused epilogue optional); bwd_filter -> csr.cu K8;
 //     shapes beyond K7/K8's shared-memory budget are densified into the workspace
@@ -140,6 +141,7 @@ sysml_status conv_bwd_filter_ws(const sysml_conv_desc &cd, int is_csr, size_t *b
   } else {
     if (is_csr) b += align_up((size_t)g.N * g.CHW() * sizeof(float), 256);
     if (cd.math == SYSML_MATH_TF32 && tc_bwd_filter_supported(a)) b += tc_bwd_filter_ws(a);
+    else if (cd.math == SYSML_MATH_TF32 && im2col_bwd_filter_supported(a)) b += im2col_bwd_filter_ws(a);
     else if (cd.math == SYSML_MATH_TF32 && phase_bwd_filter_supported(a)) b += phase_bwd_filter_ws(a);
     else b += simt_bwd_filter_ws(a);
   }
@@ -173,6 +175,8 @@ sysml_status conv_bwd_filter_dispatch(const sysml_conv_desc &cd, const sysml_inp
     void *tws = wc.take<char>(tc_bwd_filter_ws(a));
     return tc_conv_bwd_filter(a, xd, dy, df, db, tws, st);
   }
+  if (cd.math == SYSML_MATH_TF32 && im2col_bwd_filter_supported(a))
+    return im2col_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(im2col_bwd_filter_ws(a)), st);
   if (cd.math == SYSML_MATH_TF32 && phase_bwd_filter_supported(a))
     return phase_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(phase_bwd_filter_ws(a)), st);
   void *sws = wc.take<char>(simt_bwd_filter_ws(a));

@@ -292,7 +292,134 @@ sysml_status split_f(const ConvArgs &a, const ConvArgs &b, const float *f, float
   return SYSML_OK;
 }
 
+// ---------------------------------------------------------------- im2col bwd_filter (C < 8)
+// For tiny channel counts (the ResNet-50 stem, C = 3) the shifted-window / frame kernels have
+// too little reuse per staged row, so bwd_filter is lowered explicitly (P:171-174's im2col):
+//   Xcol[n][(c,r,s)][p*Q + q] = Xp[n][c][p*sh + r][q*sw + s]
+//   dF[k][(c,r,s)] = sum_{n,p,q} dY[n][k][p*Q + q] Xcol[n][(c,r,s)][p*Q + q]
+// which is exactly the 1x1 bwd_filter (K x CRS, positions contiguous in both operands) of the
+// TMA-fed tcgen05 GEMM (wgrad_gemm.cu).  Images are processed in chunks that bound Xcol to
+// im2col_ws_cap(); chunk partials are summed in chunk order (deterministic).
+// Xcol bound per chunk: 512 MB (SYSML_IM2COL_WS_MB overrides; tests force many chunks)
+size_t im2col_ws_cap() {
+  static const size_t cap = [] {
+    const char *e = getenv("SYSML_IM2COL_WS_MB");
+    const long mb = e ? atol(e) : 512;
+    return (size_t)std::max(1l, mb) << 20;
+  }();
+  return cap;
+}
+
+__global__ void __launch_bounds__(256) im2col_kernel(const float *__restrict__ x, float *__restrict__ xcol, int C,
+                                                     int H, int W, int R, int S, int sh, int sw, int ph, int pw,
+                                                     int P, int Q, int rows) {
+  // block (n*CRS + crs, chunk of `rows` output rows), a warp per row, lanes over q
+  const int CRS = C * R * S;
+  const int n = blockIdx.x / CRS, crs = blockIdx.x - n * CRS;
+  const int c = crs / (R * S), rs = crs - c * R * S, r = rs / S, s = rs - r * S;
+  const float *xs = x + ((int64_t)n * C + c) * H * W;
+  float *dst0 = xcol + (int64_t)blockIdx.x * P * Q;
+  const int p0 = blockIdx.y * rows, p1 = min(P, p0 + rows);
+  for (int pp = p0 + threadIdx.y; pp < p1; pp += 8) {
+    const int h = pp * sh + r - ph;
+    const bool rowok = h >= 0 && h < H;
+    const float *src = xs + (int64_t)h * W;
+    float *dst = dst0 + (int64_t)pp * Q;
+    for (int q = threadIdx.x; q < Q; q += 32) {
+      const int w = q * sw + s - pw;
+      dst[q] = (rowok && w >= 0 && w < W) ? __ldg(src + w) : 0.f;
+    }
+  }
+}
+
+__global__ void chunk_sum_kernel(const float *__restrict__ part, float *__restrict__ out, int64_t len,
+                                 int nchunks) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < nchunks; ++k) acc += part[(int64_t)k * len + i];
+    out[i] = acc;
+  }
+}
+
+struct Im2colPlan {
+  int nb, nchunks;
+  ConvArgs g;  // the 1x1 GEMM of one chunk: N = nb, C = CRS, H*W = P*Q
+  size_t col_bytes, part_bytes, dbpart_bytes, gemm_ws;
+  bool ok;
+};
+
+Im2colPlan plan_im2col(const ConvArgs &a) {
+  Im2colPlan pl{};
+  pl.ok = false;
+  const int64_t CRS = (int64_t)a.C * a.R * a.S, PQ = (int64_t)a.P * a.Q;
+  const int64_t per_img = CRS * PQ * sizeof(float);
+  if (per_img > (int64_t)im2col_ws_cap()) return pl;
+  pl.nb = (int)std::min<int64_t>(a.N, (int64_t)im2col_ws_cap() / per_img);
+  pl.nchunks = (a.N + pl.nb - 1) / pl.nb;
+  ConvArgs g{};
+  g.N = pl.nb; g.C = (int)CRS; g.K = a.K; g.R = g.S = 1; g.sh = g.sw = 1; g.ph = g.pw = 0;
+  g.H = a.P; g.W = a.Q; g.P = a.P; g.Q = a.Q;
+  pl.g = g;
+  if (!tc_wgrad_1x1_supported(g)) return pl;
+  pl.col_bytes = align_up((size_t)pl.nb * per_img, 256);
+  pl.part_bytes = pl.nchunks > 1 ? align_up((size_t)pl.nchunks * a.K * CRS * sizeof(float), 256) : 0;
+  pl.dbpart_bytes = pl.nchunks > 1 ? align_up((size_t)pl.nchunks * a.K * sizeof(float), 256) : 0;
+  pl.gemm_ws = align_up(tc_wgrad_1x1_ws(g), 256);
+  pl.ok = true;
+  return pl;
+}
+
 }  // namespace
+
+bool im2col_bwd_filter_supported(const ConvArgs &a) {
+  static const bool off = getenv("SYSML_NO_IM2COL") != nullptr;  // A/B switch
+  if (off || a.C >= 8 || (int64_t)a.C * a.R * a.S < 16 || ((int64_t)a.P * a.Q) % 4) return false;
+  return plan_im2col(a).ok;
+}
+
+size_t im2col_bwd_filter_ws(const ConvArgs &a) {
+  const Im2colPlan pl = plan_im2col(a);
+  return pl.ok ? pl.col_bytes + pl.part_bytes + pl.dbpart_bytes + pl.gemm_ws : 0;
+}
+
+sysml_status im2col_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df, float *db,
+                                    void *ws, cudaStream_t st) {
+  const Im2colPlan pl = plan_im2col(a);
+  if (!pl.ok) {
+    set_error("im2col bwd_filter: unsupported shape");
+    return SYSML_ERR_UNSUPPORTED;
+  }
+  WsCarve wc(ws, (size_t)-1);
+  float *xcol = reinterpret_cast<float *>(wc.take<char>(pl.col_bytes));
+  float *dfp = pl.part_bytes ? reinterpret_cast<float *>(wc.take<char>(pl.part_bytes)) : nullptr;
+  float *dbp = pl.dbpart_bytes ? reinterpret_cast<float *>(wc.take<char>(pl.dbpart_bytes)) : nullptr;
+  void *gws = wc.take<char>(pl.gemm_ws);
+  const int CRS = a.C * a.R * a.S;
+  const int64_t PQ = (int64_t)a.P * a.Q;
+  for (int i = 0; i < pl.nchunks; ++i) {
+    ConvArgs g = pl.g;
+    g.N = std::min(pl.nb, a.N - i * pl.nb);
+    const float *xi = x + (int64_t)i * pl.nb * a.C * a.H * a.W;
+    const float *dyi = dy + (int64_t)i * pl.nb * a.K * PQ;
+    const int rows = std::max(1, std::min(a.P, 4096 / std::max(1, a.Q)));
+    const dim3 grid((unsigned)((int64_t)g.N * CRS), (unsigned)ceil_div(a.P, rows));
+    im2col_kernel<<<grid, dim3(32, 8), 0, st>>>(xi, xcol, a.C, a.H, a.W, a.R, a.S, a.sh, a.sw, a.ph, a.pw, a.P,
+                                                a.Q, rows);
+    SYSML_LAUNCH_CHECK();
+    float *dfo = pl.nchunks > 1 ? dfp + (int64_t)i * a.K * CRS : df;
+    float *dbo = db ? (pl.nchunks > 1 ? dbp + (int64_t)i * a.K : db) : nullptr;
+    SYSML_TRY(tc_wgrad_1x1(g, xcol, dyi, dfo, dbo, gws, st));
+  }
+  if (pl.nchunks > 1) {
+    chunk_sum_kernel<<<grid_for((int64_t)a.K * CRS), 256, 0, st>>>(dfp, df, (int64_t)a.K * CRS, pl.nchunks);
+    SYSML_LAUNCH_CHECK();
+    if (db) {
+      chunk_sum_kernel<<<grid_for(a.K), 256, 0, st>>>(dbp, db, a.K, pl.nchunks);
+      SYSML_LAUNCH_CHECK();
+    }
+  }
+  return SYSML_OK;
+}
 
 // ---------------------------------------------------------------- forward
 bool phase_fwd_supported(const ConvArgs &a) {

@@ -221,7 +221,7 @@ __global__ void w1_reduce_kernel(const float *__restrict__ part, const float *__
     else { src = part; stride = n; idx = 4 * n4; cnt = (int)(n - 4 * n4); }
     for (int z = q; z < parts; z += 4) {
       const float *s = src + (int64_t)z * stride + idx;
-      if (cnt == 4 && src == part) {
+      if (cnt == 4 && src == part && (n & 3) == 0) {  // split partials 16-byte aligned
         const float4 v = __ldg(reinterpret_cast<const float4 *>(s));
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       } else {

@@ -396,12 +396,14 @@ def test_stream_k_opt_in_parity():
 
 def test_phase_unfused_parity():
     """Strided R, S > 1 convs with the phase tensors materialised (SYSML_PHASE_FUSED=0: the
-    X' / dX' gather kernels instead of the in-kernel gather / scatter), and with the phase path
-    off (SYSML_NO_PHASE=1: the FP32-SIMT kernels under TF32), re-run in child processes."""
+    X' / dX' gather kernels instead of the in-kernel gather / scatter), with the phase path
+    off (SYSML_NO_PHASE=1: the FP32-SIMT kernels under TF32), with the C < 8 im2col bwd_filter
+    split into 1 MB chunks (summed in chunk order) and with it off, re-run in child processes."""
     import os
     import subprocess
     import sys
-    for var, val in (("SYSML_PHASE_FUSED", "0"), ("SYSML_NO_PHASE", "1")):
+    for var, val in (("SYSML_PHASE_FUSED", "0"), ("SYSML_NO_PHASE", "1"), ("SYSML_IM2COL_WS_MB", "1"),
+                     ("SYSML_NO_IM2COL", "1")):
         env = dict(os.environ, **{var: val})
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                             os.path.abspath(__file__), "-k",
