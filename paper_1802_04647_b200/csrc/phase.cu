@@ -320,6 +320,24 @@ __global__ void __launch_bounds__(256) im2col_kernel(const float *__restrict__ x
   const float *xs = x + ((int64_t)n * C + c) * H * W;
   float *dst0 = xcol + (int64_t)blockIdx.x * P * Q;
   const int p0 = blockIdx.y * rows, p1 = min(P, p0 + rows);
+  if ((Q & 3) == 0) {
+    // float4 stores: thread -> 4 consecutive q of one row (one division per 4 outputs)
+    const int nq = Q / 4, tid = threadIdx.y * 32 + threadIdx.x;
+    for (int e = tid; e < (p1 - p0) * nq; e += 256) {
+      const int pr = e / nq, q0 = 4 * (e - pr * nq), pp = p0 + pr;
+      const int h = pp * sh + r - ph;
+      const bool rowok = h >= 0 && h < H;
+      const float *src = xs + (int64_t)h * W;
+      float v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int w = (q0 + k) * sw + s - pw;
+        v[k] = (rowok && w >= 0 && w < W) ? __ldg(src + w) : 0.f;
+      }
+      *reinterpret_cast<float4 *>(dst0 + (int64_t)pp * Q + q0) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    return;
+  }
   for (int pp = p0 + threadIdx.y; pp < p1; pp += 8) {
     const int h = pp * sh + r - ph;
     const bool rowok = h >= 0 && h < H;
