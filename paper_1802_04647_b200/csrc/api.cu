@@ -190,6 +190,7 @@ sysml_status conv_bwd_data_ws(const sysml_conv_desc &cd, size_t *bytes) {
   *bytes = 0;
   if (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a)) *bytes = tc_bwd_data_ws(a);
   else if (cd.math == SYSML_MATH_TF32 && phase_bwd_data_supported(a)) *bytes = phase_bwd_data_ws(a);
+  else if (phase_simt_bwd_data_supported(a)) *bytes = phase_simt_bwd_data_ws(a);
   return SYSML_OK;
 }
 
@@ -209,6 +210,7 @@ sysml_status conv_bwd_data_dispatch(const sysml_conv_desc &cd, const float *f, c
     return tc_conv_bwd_data(a, f, dy, dx, ws, st);
   if (cd.math == SYSML_MATH_TF32 && phase_bwd_data_supported(a))
     return phase_conv_bwd_data(a, f, dy, dx, ws, st);
+  if (phase_simt_bwd_data_supported(a)) return phase_simt_conv_bwd_data(a, f, dy, dx, ws, st);
   return simt_conv_bwd_data(a, f, dy, dx, st);
 }
 

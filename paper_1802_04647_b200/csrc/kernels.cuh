@@ -118,6 +118,10 @@ bool im2col_bwd_filter_supported(const ConvArgs &a);
 size_t im2col_bwd_filter_ws(const ConvArgs &a);
 sysml_status im2col_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df, float *db,
                                     void *ws, cudaStream_t st);
+bool phase_simt_bwd_data_supported(const ConvArgs &a);
+size_t phase_simt_bwd_data_ws(const ConvArgs &a);
+sysml_status phase_simt_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
+                                      void *ws, cudaStream_t st);
 bool phase_bwd_filter_supported(const ConvArgs &a);
 size_t phase_bwd_filter_ws(const ConvArgs &a);
 sysml_status phase_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,

@@ -387,6 +387,24 @@ Im2colPlan plan_im2col(const ConvArgs &a) {
   return pl;
 }
 
+sysml_status merge_dx(const ConvArgs &a, const ConvArgs &b, const float *dxp, float *dx, cudaStream_t st) {
+  // rows of padded-image space per block: a multiple of sh whose phase rows fit in smem
+  const int rows = a.sh * std::max(1, std::min((a.H + a.ph + a.sh - 1) / a.sh, PH_SMEM_FLOATS / (a.sh * a.sw * b.W)));
+  const dim3 grid((unsigned)((int64_t)a.N * a.C), (unsigned)ceil_div(a.H + a.ph, rows));
+#define SYSML_PH_MERGE(SWV)                                                                          \
+  phase_merge_dx_kernel<SWV><<<grid, dim3(32, 8), 0, st>>>(dxp, dx, a.C, a.H, a.W, a.sh, a.ph, a.pw, b.C, b.H, \
+                                                           b.W, rows)
+  switch (a.sw) {
+    case 1: SYSML_PH_MERGE(1); break;
+    case 2: SYSML_PH_MERGE(2); break;
+    case 3: SYSML_PH_MERGE(3); break;
+    default: SYSML_PH_MERGE(4); break;
+  }
+#undef SYSML_PH_MERGE
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
+}
+
 }  // namespace
 
 bool im2col_bwd_filter_supported(const ConvArgs &a) {
@@ -484,21 +502,28 @@ sysml_status phase_conv_bwd_data(const ConvArgs &a, const float *f, const float 
   if (fused_ok() && tc_bwd_data_phase_fused_ok(a, b))  // dX' scattered by the conv epilogue
     return tc_conv_bwd_data_phase(a, b, fp, dy, dx, tws, st);
   SYSML_TRY(tc_conv_bwd_data(b, fp, dy, dxp, tws, st));
-  // rows of padded-image space per block: a multiple of sh whose phase rows fit in smem
-  const int rows = a.sh * std::max(1, std::min((a.H + a.ph + a.sh - 1) / a.sh, PH_SMEM_FLOATS / (a.sh * a.sw * b.W)));
-  const dim3 grid((unsigned)((int64_t)a.N * a.C), (unsigned)ceil_div(a.H + a.ph, rows));
-#define SYSML_PH_MERGE(SWV)                                                                          \
-  phase_merge_dx_kernel<SWV><<<grid, dim3(32, 8), 0, st>>>(dxp, dx, a.C, a.H, a.W, a.sh, a.ph, a.pw, b.C, b.H, \
-                                                           b.W, rows)
-  switch (a.sw) {
-    case 1: SYSML_PH_MERGE(1); break;
-    case 2: SYSML_PH_MERGE(2); break;
-    case 3: SYSML_PH_MERGE(3); break;
-    default: SYSML_PH_MERGE(4); break;
-  }
-#undef SYSML_PH_MERGE
-  SYSML_LAUNCH_CHECK();
-  return SYSML_OK;
+  return merge_dx(a, b, dxp, dx, st);
+}
+
+// FP32 math (no tensor cores): the same split onto the stride-1 SIMT bwd_data.  The strided
+// SIMT gather tests every (k, r, s) term for stride divisibility and skips (sh*sw - 1)/(sh*sw)
+// of them; over the phases every term is real.
+bool phase_simt_bwd_data_supported(const ConvArgs &a) { return is_phase_shape(a); }
+
+size_t phase_simt_bwd_data_ws(const ConvArgs &a) {
+  const ConvArgs b = phase_args(a);
+  return align_up((size_t)b.N * b.C * b.H * b.W * sizeof(float), 256) + f2_bytes(b);
+}
+
+sysml_status phase_simt_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
+                                      void *ws, cudaStream_t st) {
+  const ConvArgs b = phase_args(a);
+  WsCarve wc(ws, (size_t)-1);
+  float *dxp = wc.take<float>((size_t)b.N * b.C * b.H * b.W);
+  float *fp = wc.take<float>((size_t)b.K * b.C * b.R * b.S);
+  SYSML_TRY(split_f(a, b, f, fp, st));
+  SYSML_TRY(simt_conv_bwd_data(b, fp, dy, dxp, st));
+  return merge_dx(a, b, dxp, dx, st);
 }
 
 // ---------------------------------------------------------------- bwd_filter
