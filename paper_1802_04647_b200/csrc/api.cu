@@ -7,7 +7,7 @@
 //     math == TF32 and the tcgen05 kernel covers the shape -> conv_tc.cu (K3/K5/K6)
 //     TF32, strided with R or S > 1, stride-1 image covered -> phase.cu (phase split +
 //                                                              the tcgen05 stride-1 kernels)
-//     TF32 bwd_filter, C < 8, P*Q % 4 == 0                   -> phase.cu im2col + 1x1 TMA GEMM
+//     TF32 bwd_filter outside the TMA kernels' shapes             -> phase.cu im2col + 1x1 TMA GEMM
 //     otherwise                                             -> conv_simt.cu (fp32 FMA)
 //   CSR input: fwd -> csr.cu K7 (fused epilogue optional); bwd_filter -> csr.cu K8;
 //     shapes beyond K7/K8's shared-memory budget are densified into the workspace
@@ -131,6 +131,24 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
   return simt_conv_fwd(a, xd, f, bias, y, st);
 }
 
+// TF32 dense bwd_filter route, best first: the dedicated TMA kernels; the phase
+// split when its stride-1 problem fits the frame kernel; im2col + the 1x1 GEMM (tiny channel
+// counts, 7x7 planes, frames too wide for the frame kernel); the generic tcgen05 kernel; the
+// phase split onto it; else FP32 SIMT.
+enum class WgRoute { TC, PHASE, IM2COL, SIMT };
+
+static WgRoute wgrad_route(const sysml_conv_desc &cd, const ConvArgs &a) {
+  if (cd.math != SYSML_MATH_TF32) return WgRoute::SIMT;
+  if (tc_bwd_filter_fast_supported(a)) return WgRoute::TC;
+  if (phase_bwd_filter_frame_ok(a)) return WgRoute::PHASE;
+  // im2col after the frame kernels: measured on the ResNet-50 sweep, it loses wherever a frame
+  // kernel applies (its split-K partials scale with K x CRS), and wins by 4-7x where none does
+  if (im2col_bwd_filter_supported(a)) return WgRoute::IM2COL;
+  if (tc_bwd_filter_supported(a)) return WgRoute::TC;
+  if (phase_bwd_filter_supported(a)) return WgRoute::PHASE;
+  return WgRoute::SIMT;
+}
+
 sysml_status conv_bwd_filter_ws(const sysml_conv_desc &cd, int is_csr, size_t *bytes) {
   ConvGeom g;
   SYSML_TRY(validate_conv(&cd, &g));
@@ -140,10 +158,12 @@ sysml_status conv_bwd_filter_ws(const sysml_conv_desc &cd, int is_csr, size_t *b
     b = csr_bwd_filter_ws(a);
   } else {
     if (is_csr) b += align_up((size_t)g.N * g.CHW() * sizeof(float), 256);
-    if (cd.math == SYSML_MATH_TF32 && tc_bwd_filter_supported(a)) b += tc_bwd_filter_ws(a);
-    else if (cd.math == SYSML_MATH_TF32 && im2col_bwd_filter_supported(a)) b += im2col_bwd_filter_ws(a);
-    else if (cd.math == SYSML_MATH_TF32 && phase_bwd_filter_supported(a)) b += phase_bwd_filter_ws(a);
-    else b += simt_bwd_filter_ws(a);
+    switch (wgrad_route(cd, a)) {
+      case WgRoute::TC: b += tc_bwd_filter_ws(a); break;
+      case WgRoute::PHASE: b += phase_bwd_filter_ws(a); break;
+      case WgRoute::IM2COL: b += im2col_bwd_filter_ws(a); break;
+      case WgRoute::SIMT: b += simt_bwd_filter_ws(a); break;
+    }
   }
   *bytes = b;
   return SYSML_OK;
@@ -171,14 +191,14 @@ sysml_status conv_bwd_filter_dispatch(const sysml_conv_desc &cd, const sysml_inp
     SYSML_TRY(csr_densify(x.csr, dense, st));
     xd = dense;
   }
-  if (cd.math == SYSML_MATH_TF32 && tc_bwd_filter_supported(a)) {
-    void *tws = wc.take<char>(tc_bwd_filter_ws(a));
-    return tc_conv_bwd_filter(a, xd, dy, df, db, tws, st);
+  switch (wgrad_route(cd, a)) {
+    case WgRoute::TC: return tc_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(tc_bwd_filter_ws(a)), st);
+    case WgRoute::PHASE:
+      return phase_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(phase_bwd_filter_ws(a)), st);
+    case WgRoute::IM2COL:
+      return im2col_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(im2col_bwd_filter_ws(a)), st);
+    case WgRoute::SIMT: break;
   }
-  if (cd.math == SYSML_MATH_TF32 && im2col_bwd_filter_supported(a))
-    return im2col_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(im2col_bwd_filter_ws(a)), st);
-  if (cd.math == SYSML_MATH_TF32 && phase_bwd_filter_supported(a))
-    return phase_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(phase_bwd_filter_ws(a)), st);
   void *sws = wc.take<char>(simt_bwd_filter_ws(a));
   return simt_conv_bwd_filter(a, xd, dy, df, db, sws, st);
 }

@@ -2326,6 +2326,13 @@ __global__ void subsample_kernel(const float *__restrict__ x, float *__restrict_
   }
 }
 
+// the dedicated TMA kernels (1x1 GEMM, strided 1x1 via subsampling, framed shifted rows)
+bool tc_bwd_filter_fast_supported(const ConvArgs &a) {
+  if (device_cc_major() != 10) return false;
+  if (strided_1x1(a)) return tc_wgrad_1x1_supported(subsampled_1x1(a));
+  return tc_wgrad_1x1_supported(a) || tc_wgrad_frame_supported(a);
+}
+
 bool tc_bwd_filter_supported(const ConvArgs &a) {
   if (device_cc_major() != 10) return false;
   if (strided_1x1(a)) return tc_wgrad_1x1_supported(subsampled_1x1(a));

@@ -122,10 +122,12 @@ bool phase_simt_bwd_data_supported(const ConvArgs &a);
 size_t phase_simt_bwd_data_ws(const ConvArgs &a);
 sysml_status phase_simt_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
                                       void *ws, cudaStream_t st);
+bool phase_bwd_filter_frame_ok(const ConvArgs &a);  // the phase problem fits the TMA frame kernel
 bool phase_bwd_filter_supported(const ConvArgs &a);
 size_t phase_bwd_filter_ws(const ConvArgs &a);
 sysml_status phase_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,
                                    float *db, void *ws, cudaStream_t st);
+bool tc_bwd_filter_fast_supported(const ConvArgs &a);  // 1x1 / strided 1x1 / framed TMA kernels
 bool tc_bwd_data_supported(const ConvArgs &a);
 size_t tc_bwd_data_ws(const ConvArgs &a);
 sysml_status tc_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,

@@ -312,14 +312,15 @@ size_t im2col_ws_cap() {
 
 __global__ void __launch_bounds__(256) im2col_kernel(const float *__restrict__ x, float *__restrict__ xcol, int C,
                                                      int H, int W, int R, int S, int sh, int sw, int ph, int pw,
-                                                     int P, int Q, int rows) {
+                                                     int P, int Q, int rows, int PQp) {
   // block (n*CRS + crs, chunk of `rows` output rows), a warp per row, lanes over q
   const int CRS = C * R * S;
   const int n = blockIdx.x / CRS, crs = blockIdx.x - n * CRS;
   const int c = crs / (R * S), rs = crs - c * R * S, r = rs / S, s = rs - r * S;
   const float *xs = x + ((int64_t)n * C + c) * H * W;
-  float *dst0 = xcol + (int64_t)blockIdx.x * P * Q;
+  float *dst0 = xcol + (int64_t)blockIdx.x * PQp;  // rows padded to PQp (% 4 == 0) with zeros
   const int p0 = blockIdx.y * rows, p1 = min(P, p0 + rows);
+  if (blockIdx.y == 0 && threadIdx.y == 0 && threadIdx.x < PQp - P * Q) dst0[P * Q + threadIdx.x] = 0.f;
   if ((Q & 3) == 0) {
     // float4 stores: thread -> 4 consecutive q of one row (one division per 4 outputs)
     const int nq = Q / 4, tid = threadIdx.y * 32 + threadIdx.x;
@@ -350,6 +351,17 @@ __global__ void __launch_bounds__(256) im2col_kernel(const float *__restrict__ x
   }
 }
 
+// dY (rows of P*Q) -> dYp (rows of PQp, zero tail) for the 16-byte TMA strides of the GEMM
+__global__ void pad_rows_kernel(const float *__restrict__ src, float *__restrict__ dst, int64_t rows, int L,
+                                int Lp) {
+  const int64_t total = rows * Lp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / Lp;
+    const int e = (int)(i - r * Lp);
+    dst[i] = e < L ? __ldg(src + r * L + e) : 0.f;
+  }
+}
+
 __global__ void chunk_sum_kernel(const float *__restrict__ part, float *__restrict__ out, int64_t len,
                                  int nchunks) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
@@ -362,24 +374,27 @@ __global__ void chunk_sum_kernel(const float *__restrict__ part, float *__restri
 struct Im2colPlan {
   int nb, nchunks;
   ConvArgs g;  // the 1x1 GEMM of one chunk: N = nb, C = CRS, H*W = P*Q
-  size_t col_bytes, part_bytes, dbpart_bytes, gemm_ws;
+  int PQp;  // P*Q rounded up to a multiple of 4 (TMA strides); > P*Q pads dY too
+  size_t col_bytes, dyp_bytes, part_bytes, dbpart_bytes, gemm_ws;
   bool ok;
 };
 
 Im2colPlan plan_im2col(const ConvArgs &a) {
   Im2colPlan pl{};
   pl.ok = false;
-  const int64_t CRS = (int64_t)a.C * a.R * a.S, PQ = (int64_t)a.P * a.Q;
-  const int64_t per_img = CRS * PQ * sizeof(float);
+  const int64_t CRS = (int64_t)a.C * a.R * a.S, PQ = (int64_t)a.P * a.Q, PQp = (PQ + 3) / 4 * 4;
+  const int64_t per_img = CRS * PQp * sizeof(float);
+  pl.PQp = (int)PQp;
   if (per_img > (int64_t)im2col_ws_cap()) return pl;
   pl.nb = (int)std::min<int64_t>(a.N, (int64_t)im2col_ws_cap() / per_img);
   pl.nchunks = (a.N + pl.nb - 1) / pl.nb;
   ConvArgs g{};
   g.N = pl.nb; g.C = (int)CRS; g.K = a.K; g.R = g.S = 1; g.sh = g.sw = 1; g.ph = g.pw = 0;
-  g.H = a.P; g.W = a.Q; g.P = a.P; g.Q = a.Q;
+  g.H = g.P = 1; g.W = g.Q = (int)PQp;
   pl.g = g;
   if (!tc_wgrad_1x1_supported(g)) return pl;
   pl.col_bytes = align_up((size_t)pl.nb * per_img, 256);
+  pl.dyp_bytes = PQp != PQ ? align_up((size_t)pl.nb * a.K * PQp * sizeof(float), 256) : 0;
   pl.part_bytes = pl.nchunks > 1 ? align_up((size_t)pl.nchunks * a.K * CRS * sizeof(float), 256) : 0;
   pl.dbpart_bytes = pl.nchunks > 1 ? align_up((size_t)pl.nchunks * a.K * sizeof(float), 256) : 0;
   pl.gemm_ws = align_up(tc_wgrad_1x1_ws(g), 256);
@@ -409,13 +424,13 @@ sysml_status merge_dx(const ConvArgs &a, const ConvArgs &b, const float *dxp, fl
 
 bool im2col_bwd_filter_supported(const ConvArgs &a) {
   static const bool off = getenv("SYSML_NO_IM2COL") != nullptr;  // A/B switch
-  if (off || a.C >= 8 || (int64_t)a.C * a.R * a.S < 16 || ((int64_t)a.P * a.Q) % 4) return false;
+  if (off || (int64_t)a.C * a.R * a.S < 16) return false;
   return plan_im2col(a).ok;
 }
 
 size_t im2col_bwd_filter_ws(const ConvArgs &a) {
   const Im2colPlan pl = plan_im2col(a);
-  return pl.ok ? pl.col_bytes + pl.part_bytes + pl.dbpart_bytes + pl.gemm_ws : 0;
+  return pl.ok ? pl.col_bytes + pl.dyp_bytes + pl.part_bytes + pl.dbpart_bytes + pl.gemm_ws : 0;
 }
 
 sysml_status im2col_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df, float *db,
@@ -427,6 +442,7 @@ sysml_status im2col_conv_bwd_filter(const ConvArgs &a, const float *x, const flo
   }
   WsCarve wc(ws, (size_t)-1);
   float *xcol = reinterpret_cast<float *>(wc.take<char>(pl.col_bytes));
+  float *dyp = pl.dyp_bytes ? reinterpret_cast<float *>(wc.take<char>(pl.dyp_bytes)) : nullptr;
   float *dfp = pl.part_bytes ? reinterpret_cast<float *>(wc.take<char>(pl.part_bytes)) : nullptr;
   float *dbp = pl.dbpart_bytes ? reinterpret_cast<float *>(wc.take<char>(pl.dbpart_bytes)) : nullptr;
   void *gws = wc.take<char>(pl.gemm_ws);
@@ -436,12 +452,18 @@ sysml_status im2col_conv_bwd_filter(const ConvArgs &a, const float *x, const flo
     ConvArgs g = pl.g;
     g.N = std::min(pl.nb, a.N - i * pl.nb);
     const float *xi = x + (int64_t)i * pl.nb * a.C * a.H * a.W;
-    const float *dyi = dy + (int64_t)i * pl.nb * a.K * PQ;
+    const float *dyi = dy + (int64_t)i * pl.nb * a.K * PQ;  // 16-byte aligned when PQ % 4 == 0
     const int rows = std::max(1, std::min(a.P, 4096 / std::max(1, a.Q)));
     const dim3 grid((unsigned)((int64_t)g.N * CRS), (unsigned)ceil_div(a.P, rows));
     im2col_kernel<<<grid, dim3(32, 8), 0, st>>>(xi, xcol, a.C, a.H, a.W, a.R, a.S, a.sh, a.sw, a.ph, a.pw, a.P,
-                                                a.Q, rows);
+                                                a.Q, rows, pl.PQp);
     SYSML_LAUNCH_CHECK();
+    if (dyp) {
+      pad_rows_kernel<<<grid_for((int64_t)g.N * a.K * pl.PQp), 256, 0, st>>>(dyi, dyp, (int64_t)g.N * a.K, (int)PQ,
+                                                                            pl.PQp);
+      SYSML_LAUNCH_CHECK();
+      dyi = dyp;
+    }
     float *dfo = pl.nchunks > 1 ? dfp + (int64_t)i * a.K * CRS : df;
     float *dbo = db ? (pl.nchunks > 1 ? dbp + (int64_t)i * a.K : db) : nullptr;
     SYSML_TRY(tc_wgrad_1x1(g, xcol, dyi, dfo, dbo, gws, st));
@@ -527,6 +549,10 @@ sysml_status phase_simt_conv_bwd_data(const ConvArgs &a, const float *f, const f
 }
 
 // ---------------------------------------------------------------- bwd_filter
+bool phase_bwd_filter_frame_ok(const ConvArgs &a) {
+  return is_phase_shape(a) && tc_wgrad_frame_supported(phase_args(a));
+}
+
 bool phase_bwd_filter_supported(const ConvArgs &a) {
   return is_phase_shape(a) && tc_bwd_filter_supported(phase_args(a));
 }

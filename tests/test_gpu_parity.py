@@ -593,6 +593,34 @@ def test_resnet50_strided_full_size_sampled(S, layer):
     assert_close(db, DY.sum(axis=(0, 2, 3)), 1e-4, "db")
 
 
+def _resnet50_shapes():
+    import importlib.util, os
+    spec = importlib.util.spec_from_file_location(
+        "resnet50_sweep", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "resnet50_sweep.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m.RESNET50
+
+
+@pytest.mark.parametrize("name", list(_resnet50_shapes()))
+def test_resnet50_every_layer_shape(S, name):
+    """NEXT-2 sweep: every distinct ResNet-50 conv shape (stem, 1x1 / 3x3, stride-2 3x3 and
+    1x1 downsamples, 56/28/14/7 planes) at N = 2, TF32, all three operators vs the oracle."""
+    C, H, K, R, st, pd = _resnet50_shapes()[name]
+    N = 2
+    P = (H + 2 * pd - R) // st + 1
+    x, f, b, dy = synth.conv_problem_U(N, C, H, H, K, R, R, P, P, seed=(980,))
+    d = S.conv_desc(N, C, H, H, K, R, R, st, pd, "tf32")
+    y = S.sysml_conv2d(dev(x), dev(f), d, bias=dev(b))
+    assert_close(host(y), oracle.conv2d_fwd(x, f, N, C, H, H, K, R, R, (st, st), (pd, pd), bias=b), TOL["tf32"], "fwd")
+    df, db = S.sysml_conv2d_bwd_filter(dev(x), dev(dy), d)
+    dfr, dbr = oracle.conv2d_bwd_filter(x, dy, N, C, H, H, K, R, R, (st, st), (pd, pd))
+    assert_close(host(df), dfr, TOL["tf32"], "bwd_filter")
+    assert_close(host(db), dbr, 1e-4, "db")
+    dx = S.sysml_conv2d_bwd_data(dev(f), dev(dy), d)
+    assert_close(host(dx), oracle.conv2d_bwd_data(f, dy, N, C, H, H, K, R, R, (st, st), (pd, pd)), TOL["tf32"], "bwd_data")
+
+
 @pytest.mark.parametrize("math", ["fp32", "tf32"])
 def test_csr_all_empty_matrix(S, math):
     """Degenerate CSR input: nnz = 0 (every image empty) -> conv = bias, fused conv+pool =
