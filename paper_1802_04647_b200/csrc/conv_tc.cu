@@ -1151,7 +1151,11 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   // SN: narrow filter banks (N = NFpad <= 64 keeps the MMA SMEM-operand bound) fold
   // the column taps into N when S * NFpad still fits one 256-column accumulator
   static const int sn_env = getenv("SYSML_TC_SN") ? atoi(getenv("SYSML_TC_SN")) : -1;
-  p.sn = (sn_env != 0 && !p.ks && !pool && p.nft == 1 && S >= 2 && S <= 5 && p.NFpad <= 64 &&
+  // (NFpad <= 32 by default: at NFpad = 64 the N = 64 MMAs are only 1.5x SMEM-bound and the
+  // SN epilogue costs more than it saves -- ResNet-50 stem (phase) fwd 528 -> 235 us without it;
+  // SYSML_TC_SN=2 restores the 64-wide rule)
+  const int sn_max = sn_env == 2 ? 64 : 32;
+  p.sn = (sn_env != 0 && !p.ks && !pool && p.nft == 1 && S >= 2 && S <= 5 && p.NFpad <= sn_max &&
           S * p.NFpad <= 256 && p.NFpad % 16 == 0)
              ? 1 : 0;
   p.NN = p.sn ? S * p.NFpad : p.NFpad;
