@@ -155,7 +155,9 @@ __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pPar
                 cols[u] = jj < j1 ? __ldg(p.csr.col_idx + jj) : -1;
                 vals[u] = jj < j1 ? __ldg(p.csr.val + jj) : 0.f;
               }
-#pragma unroll
+              // not unrolled: the 8 x 16 guarded scatter body unrolled thrashed the
+              // instruction cache (ncu: 37% of stalls no_instructions, profiles/r01_ncu_csr_pool.txt)
+#pragma unroll 1
               for (int u = 0; u < 8; ++u) {
                 const int col = cols[u];
                 if (col < 0 || col >= HW) continue;
