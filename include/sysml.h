@@ -12,8 +12,11 @@
  * ---------------------------------------
  *  * Pointers named x, f, bias, y, dy, dx, df, db, out, argmax, workspace, params,
  *    grads, labels and the sysml_csr arrays are DEVICE pointers (cudaMalloc /
- *    torch CUDA tensors) on the current CUDA device, 16-byte aligned unless
- *    stated.  The caller owns every buffer; the library never frees them.
+ *    torch CUDA tensors) on the current CUDA device.  fp32 tensors, argmax
+ *    outputs and workspaces must be 16-byte aligned; int32 index arrays (the
+ *    sysml_csr arrays, labels, pred) and the loss scalar need 4-byte alignment.
+ *    A pointer that breaks this returns SYSML_ERR_UNSUPPORTED (nothing is
+ *    launched).  The caller owns every buffer; the library never frees them.
  *  * Outputs are fully overwritten (never accumulated into), except
  *    sysml_bias_add, which updates y in place.  Inputs are not modified and
  *    must not alias outputs.
@@ -24,7 +27,7 @@
  *    returns.
  *  * Results are bitwise run-to-run reproducible for fixed inputs, device and
  *    math mode (no floating-point atomics; split reductions are summed in a
- *    fixed order).
+ *    fixed order; duplicate CSR columns are summed in stored order).
  *  * Errors: a non-zero sysml_status; sysml_last_error() returns a
  *    thread-local message naming the offending argument / both shapes
  *    ("shape error naming both shapes").  Nothing is launched on error.
@@ -205,6 +208,12 @@ SYSML_API sysml_status sysml_count_nonzeros(const float *x, int64_t n, int64_t *
                                             sysml_stream_t stream);
 SYSML_API sysml_status sysml_dense_to_csr(const float *x, int64_t rows, int64_t cols, int32_t *row_ptr,
                                           int32_t *col_idx, float *val, sysml_stream_t stream);
+/* The decision itself: *is_sparse = 1 iff n > 0 and
+ * nnz / n <= threshold (threshold <= 0 selects the default SYSML_SPARSITY_THRESHOLD),
+ * else 0; *nnz_host = nnz of x[0, n).  Synchronizes `stream` (a host decision).         */
+#define SYSML_SPARSITY_THRESHOLD 0.4
+SYSML_API sysml_status sysml_decide_format(const float *x, int64_t n, double threshold, int32_t *is_sparse,
+                                           int64_t *nnz_host, sysml_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Minibatch SGD-step driver (Listing 1: batch -> forward -> backward ->

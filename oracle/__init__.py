@@ -58,6 +58,7 @@ def lib():
         _lib.oracle_lenet_num_params.restype = i64
         _lib.oracle_lenet_forward.argtypes = [i64, dp, dp, dp, ip, dp, ip, dp]
         _lib.oracle_lenet_fwd_bwd.argtypes = [i64, i64, dp, ip, dp, dp, dp]
+        _lib.oracle_lenet_predict.argtypes = [i64, dp, dp, ip, dp]
         _lib.oracle_sgd_update.argtypes = [i64, dp, dp, ctypes.c_double]
         _lib.oracle_optimizer_update.argtypes = [i64, i64, dp, dp, dp] + [ctypes.c_double] * 6 + [i64]
         _lib.oracle_conv2d_fwd_csr_filter.argtypes = [i64] * 11 + [dp, ip, ip, dp, dp, dp]
@@ -160,10 +161,14 @@ def lenet_forward(x, params):
 
 
 def lenet_predict(x, params):
-    """Scoring: softmax of the oracle forward's scores and the first maximal class."""
-    sc = lenet_forward(x, params)["scores"]
-    e = np.exp(sc - sc.max(axis=1, keepdims=True))
-    return np.argmax(sc, axis=1).astype(np.int32), e / e.sum(axis=1, keepdims=True)
+    """Scoring: (first maximal class, softmax probabilities) of the oracle
+    forward's scores, computed in oracle.c (oracle_lenet_predict)."""
+    n = x.shape[0]
+    x, prm = _d(x), _d(params)
+    pred = np.empty(n, dtype=np.int32)
+    probs = np.empty((n, 10), dtype=np.float64)
+    lib().oracle_lenet_predict(n, _p(x), _p(prm), _p(pred), _p(probs))
+    return pred, probs
 
 
 def lenet_fwd_bwd(x, labels, params, n_global=None):

@@ -276,6 +276,30 @@ EXPORT void oracle_lenet_forward(int64_t n, const double *x, const double *prm, 
   free(z2);
 }
 
+/* Scoring (P:193-202 parfor-style scoring; Listing 1 "probs = softmax::forward(scores)",
+ * S:252-258 softmax with the max shift): probs[i,j] = exp(s_ij - m_i) / sum_j' exp(s_ij' - m_i),
+ * m_i = max_j s_ij; pred[i] = the first j with s_ij == m_i (first maximal class).          */
+EXPORT void oracle_lenet_predict(int64_t n, const double *x, const double *prm, int32_t *pred,
+                                 double *probs) {
+  double *a1 = (double *)malloc(sizeof(double) * (size_t)(n * 6272));
+  double *a2 = (double *)malloc(sizeof(double) * (size_t)(n * 3136));
+  int32_t *i1 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n * 6272));
+  int32_t *i2 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n * 3136));
+  double *sc = (double *)malloc(sizeof(double) * (size_t)(n * 10));
+  oracle_lenet_forward(n, x, prm, a1, i1, a2, i2, sc);
+  for (int64_t i = 0; i < n; ++i) {
+    double m = sc[i * 10];
+    int32_t arg = 0;
+    for (int j = 1; j < 10; ++j)
+      if (sc[i * 10 + j] > m) { m = sc[i * 10 + j]; arg = j; }
+    double den = 0.0;
+    for (int j = 0; j < 10; ++j) den += exp(sc[i * 10 + j] - m);
+    for (int j = 0; j < 10; ++j) probs[i * 10 + j] = exp(sc[i * 10 + j] - m) / den;
+    pred[i] = arg;
+  }
+  free(a1); free(a2); free(i1); free(i2); free(sc);
+}
+
 EXPORT void oracle_lenet_fwd_bwd(int64_t n, int64_t n_global, const double *x,
                                  const int32_t *labels, const double *prm, double *grads,
                                  double *loss_sum) {

@@ -15,6 +15,7 @@ of that shape (any contiguous shape with the right numel is accepted).
 from __future__ import annotations
 
 import ctypes
+import threading
 import os
 from dataclasses import dataclass
 from typing import Optional
@@ -178,6 +179,8 @@ def lib(build_if_missing: bool = False):
         "sysml_lenet_predict": (c_i32, [vp, vp, IN, c_i32, vp, vp, vp]),
         "sysml_count_nonzeros": (c_i32, [vp, c_i64, ctypes.POINTER(c_i64), vp]),
         "sysml_dense_to_csr": (c_i32, [vp, c_i64, c_i64, vp, vp, vp, vp]),
+        "sysml_decide_format": (c_i32, [vp, c_i64, ctypes.c_double, ctypes.POINTER(c_i32),
+                                        ctypes.POINTER(c_i64), vp]),
         "sysml_lenet_step_host_pipelined": (c_i32, [vp, vp, vp, vp, vp, c_i32, vp, vp, c_i32, c_i64,
                                                     ctypes.c_float, vp, vp, vp]),
         "sysml_optimizer_update": (c_i32, [ctypes.POINTER(OptimizerDesc), vp, vp, vp, c_i64, c_i64, vp]),
@@ -233,14 +236,25 @@ def _input(x) -> _Input:
     return _Input(0, _ptr(x, torch.float32, "x").value, _Csr())
 
 
-def _workspace(nbytes: int, workspace=None, device=None):
+_ws_keep = threading.local()
+
+
+def _workspace(nbytes: int, workspace=None, stream=None):
+    """The caller's workspace if large enough, else a fresh buffer allocated on the stream the
+    kernel runs on (so the caching allocator orders its reuse after that kernel), kept alive
+    per thread and stream until the next call on them."""
     torch = _torch()
     if nbytes == 0:
         return None, 0
     if workspace is not None and workspace.numel() * workspace.element_size() >= nbytes:
         return ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size()
-    buf = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
-    _workspace.keep = buf  # keep alive until the next call (stream-ordered reuse)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    with torch.cuda.stream(s):
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=s.device)
+    keep = getattr(_ws_keep, "bufs", None)
+    if keep is None:
+        keep = _ws_keep.bufs = {}
+    keep[(s.device.index, s.cuda_stream)] = buf
     return ctypes.c_void_p(buf.data_ptr()), nbytes
 
 
@@ -259,7 +273,7 @@ def sysml_conv2d(x, f, d: ConvDesc, bias=None, out=None, workspace=None, stream=
     if out is None:
         out = torch.empty((d.N, d.K * d.P * d.Q), dtype=torch.float32, device="cuda")
     nb = _ws_size(L.sysml_conv2d_workspace_size, ctypes.byref(d), inp.is_csr)
-    ws, wsb = _workspace(nb, workspace)
+    ws, wsb = _workspace(nb, workspace, stream)
     _check(L.sysml_conv2d(ctypes.byref(d), ctypes.byref(inp), _ptr(f, torch.float32, "f"),
                           _ptr(bias, torch.float32, "bias"), _ptr(out, torch.float32, "out"),
                           ws, wsb, _stream(stream)))
@@ -275,7 +289,7 @@ def sysml_conv2d_bwd_filter(x, dy, d: ConvDesc, df=None, db=None, want_db=True, 
     if db is None and want_db:
         db = torch.empty((d.K,), dtype=torch.float32, device="cuda")
     nb = _ws_size(L.sysml_conv2d_bwd_filter_workspace_size, ctypes.byref(d), inp.is_csr)
-    ws, wsb = _workspace(nb, workspace)
+    ws, wsb = _workspace(nb, workspace, stream)
     _check(L.sysml_conv2d_bwd_filter(ctypes.byref(d), ctypes.byref(inp), _ptr(dy, torch.float32, "dy"),
                                      _ptr(df, torch.float32, "df"), _ptr(db, torch.float32, "db"),
                                      ws, wsb, _stream(stream)))
@@ -288,7 +302,7 @@ def sysml_conv2d_bwd_data(f, dy, d: ConvDesc, dx=None, workspace=None, stream=No
     if dx is None:
         dx = torch.empty((d.N, d.C * d.H * d.W), dtype=torch.float32, device="cuda")
     nb = _ws_size(L.sysml_conv2d_bwd_data_workspace_size, ctypes.byref(d))
-    ws, wsb = _workspace(nb, workspace)
+    ws, wsb = _workspace(nb, workspace, stream)
     _check(L.sysml_conv2d_bwd_data(ctypes.byref(d), _ptr(f, torch.float32, "f"), _ptr(dy, torch.float32, "dy"),
                                    _ptr(dx, torch.float32, "dx"), ws, wsb, _stream(stream)))
     return dx
@@ -332,7 +346,7 @@ def sysml_conv2d_bias_relu_maxpool(x, f, bias, cd: ConvDesc, pd: PoolDesc, out=N
     if argmax is None:
         argmax = torch.empty((pd.N, pd.C * pd.P * pd.Q), dtype=torch.int32, device="cuda")
     nb = _ws_size(L.sysml_conv2d_bias_relu_maxpool_workspace_size, ctypes.byref(cd), ctypes.byref(pd), inp.is_csr)
-    ws, wsb = _workspace(nb, workspace)
+    ws, wsb = _workspace(nb, workspace, stream)
     _check(L.sysml_conv2d_bias_relu_maxpool(ctypes.byref(cd), ctypes.byref(pd), ctypes.byref(inp),
                                             _ptr(f, torch.float32, "f"), _ptr(bias, torch.float32, "bias"),
                                             _ptr(out, torch.float32, "out"), _ptr(argmax, torch.int32, "argmax"),
@@ -398,11 +412,14 @@ def dense_to_csr(x, stream=None) -> "CSR":
 
 
 def decide_format(x, threshold=SPARSITY_THRESHOLD, stream=None):
-    """P:163-165 / S:88-96: the CSR form of x if nnz / (rows*cols) <= threshold, else x itself."""
-    nnz = sysml_count_nonzeros(x, stream)
-    if x.numel() and nnz / x.numel() <= threshold:
-        return dense_to_csr(x, stream)
-    return x
+    """P:163-165 / S:88-96: the CSR form of x if nnz / (rows*cols) <= threshold, else x itself
+    (the rule is sysml_decide_format in the C ABI)."""
+    torch = _torch()
+    sparse = ctypes.c_int32(0)
+    nnz = ctypes.c_int64(0)
+    _check(lib().sysml_decide_format(_ptr(x, torch.float32, "x"), x.numel(), float(threshold),
+                                     ctypes.byref(sparse), ctypes.byref(nnz), _stream(stream)))
+    return dense_to_csr(x, stream) if sparse.value else x
 
 
 def sysml_optimizer_update(desc, params, grads, state, t=1, stream=None):

@@ -71,6 +71,12 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
   SYSML_TRY(validate_conv(&cd, &g));
   SYSML_TRY(validate_input(&x, g));
   SYSML_CHECK_ARG(f != nullptr, "filter pointer is NULL");
+  SYSML_CHECK_ALIGN16(f, "filter");
+  SYSML_CHECK_ALIGN16(bias, "bias");
+  SYSML_CHECK_ALIGN16(y, "output");
+  SYSML_CHECK_ALIGN16(pout, "pooled output");
+  SYSML_CHECK_ALIGN16(parg, "argmax");
+  SYSML_CHECK_ALIGN16(ws, "workspace");
   const ConvArgs a = conv_args(g);
   PoolArgs pa{};
   const PoolArgs *pap = nullptr;
@@ -104,27 +110,35 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
   const float *xd = x.dense;
   if (cd.math == SYSML_MATH_TF32 && pap && conv1_pool_supported(a, pap)) {
     void *tws = wc.take<char>(conv1_pool_ws(a, pap));
+    SYSML_WS_FITS(wc);
     return conv1_pool(a, pap, x.is_csr ? nullptr : x.dense, f, bias, pout, parg, tws, st, nullptr,
                       x.is_csr ? &x.csr : nullptr);
   }
   if (x.is_csr && use_tc && tc_fwd_ks(a)) {
     void *tws = wc.take<char>(tc_fwd_ws(a));
+    SYSML_WS_FITS(wc);
     return tc_conv_fwd(a, nullptr, f, bias, y, pap, pout, parg, tws, st, &x.csr);
   }
   if (x.is_csr) {
     if (csr_fwd_supported(a)) return csr_conv_fwd(a, x.csr, f, bias, y, pap, pout, parg, st);
     float *dense = wc.take<float>((size_t)g.N * g.CHW());
+    SYSML_WS_FITS(wc);
     SYSML_TRY(csr_densify(x.csr, dense, st));
     xd = dense;
   }
   if (use_tc) {
     void *tws = wc.take<char>(tc_fwd_ws(a));
+    SYSML_WS_FITS(wc);
     return tc_conv_fwd(a, xd, f, bias, y, pap, pout, parg, tws, st);
   }
-  if (cd.math == SYSML_MATH_TF32 && !pap && phase_fwd_supported(a))
-    return phase_conv_fwd(a, xd, f, bias, y, wc.take<char>(phase_fwd_ws(a)), st);
+  if (cd.math == SYSML_MATH_TF32 && !pap && phase_fwd_supported(a)) {
+    void *pws = wc.take<char>(phase_fwd_ws(a));
+    SYSML_WS_FITS(wc);
+    return phase_conv_fwd(a, xd, f, bias, y, pws, st);
+  }
   if (pap) {
     float *z = wc.take<float>((size_t)g.N * g.KPQ());
+    SYSML_WS_FITS(wc);
     SYSML_TRY(simt_conv_fwd(a, xd, f, bias, z, st));
     return launch_relu_maxpool(*pap, z, pout, parg, st);
   }
@@ -176,6 +190,10 @@ sysml_status conv_bwd_filter_dispatch(const sysml_conv_desc &cd, const sysml_inp
   SYSML_TRY(validate_conv(&cd, &g));
   SYSML_TRY(validate_input(&x, g));
   SYSML_CHECK_ARG(dy && df, "dy/df pointer is NULL");
+  SYSML_CHECK_ALIGN16(dy, "dy");
+  SYSML_CHECK_ALIGN16(df, "df");
+  SYSML_CHECK_ALIGN16(db, "db");
+  SYSML_CHECK_ALIGN16(ws, "workspace");
   const ConvArgs a = conv_args(g);
   size_t need = 0;
   SYSML_TRY(conv_bwd_filter_ws(cd, x.is_csr, &need));
@@ -188,18 +206,26 @@ sysml_status conv_bwd_filter_dispatch(const sysml_conv_desc &cd, const sysml_inp
   if (x.is_csr) {
     if (csr_bwd_filter_supported(a)) return csr_conv_bwd_filter(a, x.csr, dy, df, db, ws, st);
     float *dense = wc.take<float>((size_t)g.N * g.CHW());
-    SYSML_TRY(csr_densify(x.csr, dense, st));
     xd = dense;
   }
-  switch (wgrad_route(cd, a)) {
-    case WgRoute::TC: return tc_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(tc_bwd_filter_ws(a)), st);
-    case WgRoute::PHASE:
-      return phase_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(phase_bwd_filter_ws(a)), st);
-    case WgRoute::IM2COL:
-      return im2col_conv_bwd_filter(a, xd, dy, df, db, wc.take<char>(im2col_bwd_filter_ws(a)), st);
+  const WgRoute route = wgrad_route(cd, a);
+  size_t route_ws = 0;
+  switch (route) {
+    case WgRoute::TC: route_ws = tc_bwd_filter_ws(a); break;
+    case WgRoute::PHASE: route_ws = phase_bwd_filter_ws(a); break;
+    case WgRoute::IM2COL: route_ws = im2col_bwd_filter_ws(a); break;
+    case WgRoute::SIMT: route_ws = simt_bwd_filter_ws(a); break;
+  }
+  void *rws = wc.take<char>(route_ws);
+  SYSML_WS_FITS(wc);
+  if (x.is_csr) SYSML_TRY(csr_densify(x.csr, const_cast<float *>(xd), st));
+  switch (route) {
+    case WgRoute::TC: return tc_conv_bwd_filter(a, xd, dy, df, db, rws, st);
+    case WgRoute::PHASE: return phase_conv_bwd_filter(a, xd, dy, df, db, rws, st);
+    case WgRoute::IM2COL: return im2col_conv_bwd_filter(a, xd, dy, df, db, rws, st);
     case WgRoute::SIMT: break;
   }
-  void *sws = wc.take<char>(simt_bwd_filter_ws(a));
+  void *sws = rws;
   return simt_conv_bwd_filter(a, xd, dy, df, db, sws, st);
 }
 
@@ -219,6 +245,10 @@ sysml_status conv_bwd_data_dispatch(const sysml_conv_desc &cd, const float *f, c
   ConvGeom g;
   SYSML_TRY(validate_conv(&cd, &g));
   SYSML_CHECK_ARG(f && dy && dx, "f/dy/dx pointer is NULL");
+  SYSML_CHECK_ALIGN16(f, "filter");
+  SYSML_CHECK_ALIGN16(dy, "dy");
+  SYSML_CHECK_ALIGN16(dx, "dx");
+  SYSML_CHECK_ALIGN16(ws, "workspace");
   const ConvArgs a = conv_args(g);
   size_t need = 0;
   SYSML_TRY(conv_bwd_data_ws(cd, &need));
@@ -289,6 +319,8 @@ sysml_status sysml_bias_add(int32_t N, int32_t K, int32_t PQ, float *y, const fl
   SYSML_CHECK_ARG(N >= 1 && K >= 1 && PQ >= 1, "bias_add dims must be >= 1 (N=%d K=%d PQ=%d)", N,
                   K, PQ);
   SYSML_CHECK_ARG(y && bias, "NULL pointer");
+  SYSML_CHECK_ALIGN16(y, "y");
+  SYSML_CHECK_ALIGN16(bias, "bias");
   return launch_bias_add(N, K, PQ, y, bias, (cudaStream_t)stream);
 }
 
@@ -297,6 +329,9 @@ sysml_status sysml_relu_maxpool(const sysml_pool_desc *d, const float *x, float 
   ConvGeom g;
   SYSML_TRY(validate_pool(d, &g));
   SYSML_CHECK_ARG(x && out, "NULL pointer");
+  SYSML_CHECK_ALIGN16(x, "x");
+  SYSML_CHECK_ALIGN16(out, "out");
+  SYSML_CHECK_ALIGN16(argmax, "argmax");
   return launch_relu_maxpool(pool_args(g, d->relu ? 1 : 0), x, out, argmax, (cudaStream_t)stream);
 }
 
@@ -306,6 +341,10 @@ sysml_status sysml_maxpool_bwd(const sysml_pool_desc *d, const int32_t *argmax,
   ConvGeom g;
   SYSML_TRY(validate_pool(d, &g));
   SYSML_CHECK_ARG(argmax && dout && dx, "NULL pointer");
+  SYSML_CHECK_ALIGN16(argmax, "argmax");
+  SYSML_CHECK_ALIGN16(dout, "dout");
+  SYSML_CHECK_ALIGN16(out_mask, "out_mask");
+  SYSML_CHECK_ALIGN16(dx, "dx");
   return launch_maxpool_bwd(pool_args(g, d->relu ? 1 : 0), argmax, dout, out_mask, dx,
                             (cudaStream_t)stream);
 }

@@ -1,7 +1,9 @@
 // common.cu -- error reporting, device queries and descriptor validation.
 #include <stdarg.h>
 
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "common.cuh"
 #include "tma.cuh"
@@ -24,6 +26,20 @@ static int query_attr(cudaDeviceAttr a) {
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&v, a, dev) != cudaSuccess) return 0;
   return v;
+}
+
+sysml_status ensure_smem_attr(const void *func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  SYSML_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t &cur = done[{func, dev}];
+  if (bytes > cur) {
+    SYSML_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
+  }
+  return SYSML_OK;
 }
 
 int sm_count() {
@@ -78,10 +94,14 @@ sysml_status validate_input(const sysml_input *x, const ConvGeom &g) {
   SYSML_CHECK_ARG(x != nullptr, "input is NULL");
   if (!x->is_csr) {
     SYSML_CHECK_ARG(x->dense != nullptr, "dense input pointer is NULL");
+    SYSML_CHECK_ALIGN16(x->dense, "dense input");
     return SYSML_OK;
   }
   const sysml_csr &m = x->csr;
   SYSML_CHECK_ARG(m.row_ptr && (m.nnz == 0 || (m.col_idx && m.val)), "CSR arrays are NULL");
+  SYSML_CHECK_ALIGN(m.row_ptr, 4, "CSR row_ptr");
+  SYSML_CHECK_ALIGN(m.col_idx, 4, "CSR col_idx");
+  SYSML_CHECK_ALIGN(m.val, 4, "CSR val");
   SYSML_CHECK_SHAPE(m.rows == g.N && m.cols == g.CHW(),
                     "CSR shape %lldx%lld does not match input N x (C*H*W) = %lldx%lld",
                     (long long)m.rows, (long long)m.cols, (long long)g.N, (long long)g.CHW());

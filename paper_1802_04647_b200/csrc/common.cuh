@@ -32,6 +32,19 @@ const char *get_error();
     }                                \
   } while (0)
 
+// sysml.h "Conventions": dense tensors and workspaces are 16-byte aligned (the kernels move
+// them with 16-byte vector, cp.async and bulk/TMA copies); int32 index arrays (CSR, labels)
+// need their natural 4-byte alignment.  A view that breaks this is rejected, not faulted on.
+#define SYSML_CHECK_ALIGN(ptr, bytes, name)                                                   \
+  do {                                                                                        \
+    if ((ptr) != nullptr && ((uintptr_t)(ptr) & ((bytes) - 1)) != 0) {                        \
+      ::sysml::set_error("%s pointer %p is not %d-byte aligned", name, (const void *)(ptr),    \
+                         (int)(bytes));                                                       \
+      return SYSML_ERR_UNSUPPORTED;                                                          \
+    }                                                                                         \
+  } while (0)
+#define SYSML_CHECK_ALIGN16(ptr, name) SYSML_CHECK_ALIGN(ptr, 16, name)
+
 #define SYSML_CUDA(call)                                                           \
   do {                                                                             \
     cudaError_t e_ = (call);                                                       \
@@ -67,6 +80,15 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline size_t align_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
 
 int sm_count();              // cached per device
+
+// Opt `func` (a __global__ function) into `bytes` of dynamic shared memory on the CURRENT
+// device.  The attribute is per device, so the cache is keyed by (function, device) and
+// guarded by a mutex (reentrant, multi-GPU processes).
+sysml_status ensure_smem_attr(const void *func, size_t bytes);
+template <class K>
+inline sysml_status smem_attr(K *kernel, size_t bytes) {
+  return ensure_smem_attr(reinterpret_cast<const void *>(kernel), bytes);
+}
 int device_cc_major();       // cached per device
 
 // Derived geometry of a conv descriptor.
@@ -96,6 +118,20 @@ struct WsCarve {
     return p;
   }
   size_t used() const { return align_up(off, 256); }
+  // false once the carved regions run past the declared size (a sizing/dispatch mismatch)
+  bool fits() const { return off <= size; }
 };
+
+// Carve check: every internal path that carves a caller workspace is given the size its
+// own *_ws() function declared and must stay inside it (sizing and dispatch
+// disagreed once and the kernel wrote past the caller's buffer).
+#define SYSML_WS_FITS(wc)                                                                  \
+  do {                                                                                     \
+    if (!(wc).fits()) {                                                                    \
+      ::sysml::set_error("internal: workspace carve %zu bytes exceeds declared %zu at %s:%d", \
+                         (wc).off, (wc).size, __FILE__, __LINE__);                          \
+      return SYSML_ERR_WORKSPACE;                                                          \
+    }                                                                                      \
+  } while (0)
 
 }  // namespace sysml

@@ -53,6 +53,36 @@ __device__ __forceinline__ void st_shared_v4c1(uint32_t addr) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "f"(0.f) : "memory");
 }
 
+// CSR producer: pixel `col` of image n (value v) into every (window, tap) slot of the M-tile
+// at window w0 it feeds.  Window of slot (t, e): pp = (hf - t)/2, pc = (wf - e)/2 with
+// t = hf & 1 + 2a, e = wf & 1 + 2b -> row offset m(a, b) = m00 - a*Qp - b.  ACC: add (the
+// stored-order rebuild of a row with duplicate columns) instead of store (one writer).
+template <bool ACC, class P>
+__device__ __forceinline__ void c1p_scatter(const P &p, float *Af, int col, float v, int n, int PpQp,
+                                            int64_t w0, float invW, int HW) {
+  if (col < 0 || col >= HW) return;
+  const int h = __float2int_rz(((float)col + 0.5f) * invW);
+  const int wc = col - h * p.W;
+  const int hf = h + p.ph, wf = wc + p.pw;
+  const int t0 = hf & 1, e0 = wf & 1;
+  const int pp0 = (hf - t0) >> 1, pc0 = (wf - e0) >> 1;
+  const int m00 = n * PpQp + pp0 * p.Qp + pc0 - (int)w0;
+#pragma unroll
+  for (int a_ = 0; a_ < 4; ++a_) {
+    const int t = t0 + 2 * a_, pp = pp0 - a_;
+    if (t >= p.T || pp < 0 || pp >= p.Pp) continue;
+#pragma unroll
+    for (int b_ = 0; b_ < 4; ++b_) {
+      const int e = e0 + 2 * b_, pc = pc0 - b_;
+      const int m = m00 - a_ * p.Qp - b_;
+      if (pc >= 0 && pc < p.Qp && m >= 0 && m < 128) {
+        float *d = Af + t * 1024 + (e >> 2) * 512 + m * 4 + (e & 3);
+        if (ACC) *d += v; else *d = v;
+      }
+    }
+  }
+}
+
 // One 16-channel group of the pooled epilogue (kept small: the argmax variant is a
 // template, not a branch in the unrolled loop, so the executing loop stays compact)
 template <bool PARG>
@@ -144,8 +174,14 @@ __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pPar
           const int n_lo = (int)(w0 / PpQp);
           const int n_hi = (int)min((int64_t)p.N - 1, (w0 + 127) / PpQp);
           float *Af = reinterpret_cast<float *>(As);
+          // one input pixel owns distinct (window, tap) slots, so a strictly increasing row
+          // has one writer per slot: plain stores.  Rows that are not (unsorted or
+          // duplicate columns, reading R15) flag the tile, which lane 0 then rebuilds by
+          // summing in stored order: deterministic, no float atomics.
+          bool bad = false;
           for (int n = n_lo; n <= n_hi; ++n) {
             const int j0 = __ldg(p.csr.row_ptr + n), j1 = __ldg(p.csr.row_ptr + n + 1);
+            int last = -1;
             for (int base = j0; base < j1; base += 8 * 32) {
               int cols[8];
               float vals[8];
@@ -155,35 +191,32 @@ __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pPar
                 cols[u] = jj < j1 ? __ldg(p.csr.col_idx + jj) : -1;
                 vals[u] = jj < j1 ? __ldg(p.csr.val + jj) : 0.f;
               }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int up = __shfl_up_sync(0xffffffffu, cols[u], 1);
+                const int prev = lane ? up : last;
+                last = __shfl_sync(0xffffffffu, cols[u], 31);
+                const int jj = base + lane + 32 * u;
+                if (jj < j1 && jj > j0 && prev >= cols[u]) bad = true;
+              }
               // not unrolled: the 8 x 16 guarded scatter body unrolled thrashed the
               // instruction cache (ncu: 37% of stalls no_instructions, profiles/r01_ncu_csr_pool.txt)
 #pragma unroll 1
-              for (int u = 0; u < 8; ++u) {
-                const int col = cols[u];
-                if (col < 0 || col >= HW) continue;
-                const float v = vals[u];
-                const int h = __float2int_rz(((float)col + 0.5f) * invW);
-                const int wc = col - h * p.W;
-                const int hf = h + p.ph, wf = wc + p.pw;
-                // window of slot (t, e): pp = (hf - t)/2, pc = (wf - e)/2 with t = hf & 1 + 2a,
-                // e = wf & 1 + 2b -> row offset m(a, b) = m00 - a*Qp - b
-                const int t0 = hf & 1, e0 = wf & 1;
-                const int pp0 = (hf - t0) >> 1, pc0 = (wf - e0) >> 1;
-                const int m00 = n * PpQp + pp0 * p.Qp + pc0 - (int)w0;
-#pragma unroll
-                for (int a_ = 0; a_ < 4; ++a_) {
-                  const int t = t0 + 2 * a_, pp = pp0 - a_;
-                  if (t >= p.T || pp < 0 || pp >= p.Pp) continue;
-#pragma unroll
-                  for (int b_ = 0; b_ < 4; ++b_) {
-                    const int e = e0 + 2 * b_, pc = pc0 - b_;
-                    const int m = m00 - a_ * p.Qp - b_;
-                    if (pc >= 0 && pc < p.Qp && m >= 0 && m < 128)
-                      atomicAdd(Af + t * 1024 + (e >> 2) * 512 + m * 4 + (e & 3), v);
-                  }
-                }
-              }
+              for (int u = 0; u < 8; ++u)
+                c1p_scatter<false>(p, Af, cols[u], vals[u], n, PpQp, w0, invW, HW);
             }
+          }
+          if (__any_sync(0xffffffffu, bad)) {  // rebuild in stored order (lane 0)
+            __syncwarp();
+            for (int q = lane; q < (int)(p.a_bytes / 16); q += 32) st_shared_v4c1(A + q * 16);
+            __syncwarp();
+            if (lane == 0)
+              for (int n = n_lo; n <= n_hi; ++n) {
+                const int j1 = __ldg(p.csr.row_ptr + n + 1);
+                for (int jj = __ldg(p.csr.row_ptr + n); jj < j1; ++jj)
+                  c1p_scatter<true>(p, Af, __ldg(p.csr.col_idx + jj), __ldg(p.csr.val + jj), n, PpQp, w0,
+                                    invW, HW);
+              }
           }
         }
         ptx::fence_proxy_async_smem();
@@ -411,12 +444,7 @@ sysml_status conv1_pool(const ConvArgs &a, const PoolArgs *pool, const float *x,
   }
   conv1_pool_pack_kernel<<<8, 256, 0, st>>>(f, reinterpret_cast<float *>(ws), a.K, a.R, a.S, p.Kp);
   SYSML_LAUNCH_CHECK();
-  static int attr = 0;
-  if ((int)pl.smem > attr) {
-    SYSML_CUDA(cudaFuncSetAttribute(conv1_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)pl.smem));
-    attr = (int)pl.smem;
-  }
+  SYSML_TRY(smem_attr(conv1_pool_kernel, pl.smem));
   const int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);

@@ -295,9 +295,10 @@ sysml_status simt_conv_bwd_filter(const ConvArgs &a, const float *x, const float
   const int64_t kg = (int64_t)a.N * a.P * a.Q;
   int k_per_split = (int)align_up((size_t)ceil_div(kg, splits), BK);
   const int used_splits = (int)ceil_div(kg, k_per_split);
-  WsCarve wc(ws, (size_t)-1);
+  WsCarve wc(ws, simt_bwd_filter_ws(a));
   float *part = wc.take<float>((size_t)splits * a.K * a.C * a.R * a.S);
   float *bpart = wc.take<float>((size_t)a.K * bias_grad_chunks(a));
+  SYSML_WS_FITS(wc);
   BwdFilterOp op{a, x, dy, used_splits == 1 ? df : part};
   dim3 grid((unsigned)ceil_div((int64_t)a.C * a.R * a.S, BN), (unsigned)ceil_div(a.K, BM),
             (unsigned)used_splits);

@@ -625,10 +625,17 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       for (int i = lane; i < 2 * p.HALO; i += 32) st_shared_v4(a0 + i * 16, 0.f, 0.f, 0.f, 0.f);
       __syncwarp();
       float *Af = reinterpret_cast<float *>(A);
+      // Every input position owns distinct (pos, s) slots, so a strictly increasing row (the
+      // S:31-32 contract) has one writer per slot: plain stores.  A row that is not strictly
+      // increasing (unsorted, or duplicate columns -- reading R15) flags the tile, which is
+      // then rebuilt by lane 0 summing in stored order: deterministic, no float atomics.
+      bool bad = false;
+      const int jA = __shfl_sync(0xffffffffu, rp, 0);
+      const int jB = nimg <= 31 ? __shfl_sync(0xffffffffu, rp, nimg) : __ldg(p.csr.row_ptr + n_hi + 1);
       if (nimg <= 31) {
         // the overlapping images' non-zeros are one contiguous CSR range: 4 (col, val)
         // pairs per lane in flight, each entry's image from the row pointers (uniform loop)
-        const int jA = __shfl_sync(0xffffffffu, rp, 0), jB = __shfl_sync(0xffffffffu, rp, nimg);
+        int last = -1;  // column of the entry before this batch (lane 31 of the last one)
         for (int base = jA; base < jB; base += 128) {
           int col[4], img[4];
           float val[4];
@@ -647,34 +654,63 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
+            const int up = __shfl_up_sync(0xffffffffu, col[u], 1);
+            const int prev = lane ? up : last;
+            last = __shfl_sync(0xffffffffu, col[u], 31);
+            const int rs = __shfl_sync(0xffffffffu, rp, img[u]);
+            const int jj = base + u * 32 + lane;
+            if (jj < jB && jj > rs && prev >= col[u]) bad = true;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
             if (col[u] < 0 || col[u] >= HW) continue;
             const int h = col[u] / p.W, w = col[u] - h * p.W;
             const int64_t gi = (int64_t)(n_lo + img[u]) * p.Lf + (int64_t)(h + p.ph) * p.Wf + (w + p.pw);
             for (int s_ = 0; s_ < p.S; ++s_) {
               const int64_t pos = gi - g0 - s_;
-              if (pos >= 0 && pos < p.HALO)
-                atomicAdd(Af + (s_ >> 2) * p.HALO * 4 + pos * 4 + (s_ & 3), val[u]);  // duplicates summed
+              if (pos >= 0 && pos < p.HALO) Af[(s_ >> 2) * p.HALO * 4 + pos * 4 + (s_ & 3)] = val[u];
             }
           }
         }
       } else
-      for (int ii = 0; ii < nimg; ++ii) {
+      for (int ii = 0; ii < nimg; ++ii) {  // more than 31 images in one tile (tiny images)
         const int n = n_lo + ii;
-        int j0 = __shfl_sync(0xffffffffu, rp, ii & 31), j1 = __shfl_sync(0xffffffffu, rp, (ii + 1) & 31);
-        if (ii + 1 > 31) {  // more than 31 images in one tile (tiny images): direct loads
-          j0 = __ldg(p.csr.row_ptr + n);
-          j1 = __ldg(p.csr.row_ptr + n + 1);
-        }
-        for (int jj = j0 + lane; jj < j1; jj += 32) {
-          const int col = __ldg(p.csr.col_idx + jj);
-          const float v = __ldg(p.csr.val + jj);
+        const int j0 = __ldg(p.csr.row_ptr + n), j1 = __ldg(p.csr.row_ptr + n + 1);
+        int last = -1;
+        for (int base = j0; base < j1; base += 32) {
+          const int jj = base + lane;
+          const int col = jj < j1 ? __ldg(p.csr.col_idx + jj) : -1;
+          const float v = jj < j1 ? __ldg(p.csr.val + jj) : 0.f;
+          const int up = __shfl_up_sync(0xffffffffu, col, 1);
+          const int prev = lane ? up : last;
+          last = __shfl_sync(0xffffffffu, col, 31);
+          if (jj < j1 && jj > j0 && prev >= col) bad = true;
           if (col < 0 || col >= HW) continue;
           const int h = col / p.W, w = col - h * p.W;
           const int64_t gi = (int64_t)n * p.Lf + (int64_t)(h + p.ph) * p.Wf + (w + p.pw);
           for (int s_ = 0; s_ < p.S; ++s_) {
             const int64_t pos = gi - g0 - s_;
-            if (pos >= 0 && pos < p.HALO)
-              atomicAdd(Af + (s_ >> 2) * p.HALO * 4 + pos * 4 + (s_ & 3), v);  // duplicates summed
+            if (pos >= 0 && pos < p.HALO) Af[(s_ >> 2) * p.HALO * 4 + pos * 4 + (s_ & 3)] = v;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, bad)) {  // rebuild the tile in stored order (lane 0)
+        __syncwarp();
+        for (int i = lane; i < 2 * p.HALO; i += 32) st_shared_v4(a0 + i * 16, 0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
+        if (lane == 0) {
+          int n = n_lo, jn = __ldg(p.csr.row_ptr + n_lo + 1);
+          for (int jj = jA; jj < jB; ++jj) {
+            while (jj >= jn) jn = __ldg(p.csr.row_ptr + (++n) + 1);
+            const int col = __ldg(p.csr.col_idx + jj);
+            if (col < 0 || col >= HW) continue;
+            const float v = __ldg(p.csr.val + jj);
+            const int h = col / p.W, w = col - h * p.W;
+            const int64_t gi = (int64_t)n * p.Lf + (int64_t)(h + p.ph) * p.Wf + (w + p.pw);
+            for (int s_ = 0; s_ < p.S; ++s_) {
+              const int64_t pos = gi - g0 - s_;
+              if (pos >= 0 && pos < p.HALO) Af[(s_ >> 2) * p.HALO * 4 + pos * 4 + (s_ & 3)] += v;
+            }
           }
         }
       }
@@ -1230,14 +1266,6 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   return pl;
 }
 
-template <class K>
-sysml_status set_smem_attr(K kernel, size_t bytes, int &cache) {
-  if ((int)bytes > cache) {
-    SYSML_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    cache = (int)bytes;
-  }
-  return SYSML_OK;
-}
 
 // stream-K hand-off flags: per device a ring of TC_SK_SETS sets of TC_SK_MAX_GRID ints,
 // zeroed once; each launch takes the next set (a captured graph keeps its set, and its
@@ -1337,13 +1365,11 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
   p.pout = pout;
   p.parg = parg;
   if (!bias) p.bias_smem = 0;
-  static int attr = 0;
   const bool ph = p.in_phase || p.out_phase;
   if (ph) {
-    static int attr_ph = 0;
-    SYSML_TRY(set_smem_attr(tc_conv_fwd_kernel<true>, pl.smem, attr_ph));
+    SYSML_TRY(smem_attr(tc_conv_fwd_kernel<true>, pl.smem));
   } else {
-    SYSML_TRY(set_smem_attr(tc_conv_fwd_kernel<false>, pl.smem, attr));
+    SYSML_TRY(smem_attr(tc_conv_fwd_kernel<false>, pl.smem));
   }
   int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
   // stream-K (opt-in, SYSML_TC_SK=1): even chunk-iteration ranges per CTA instead of whole
@@ -2283,12 +2309,10 @@ sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy
     p.clk = dclk;
   }
   if (p.S == 5) {
-    static int attr = 0;
-    SYSML_TRY(set_smem_attr(tc_wgrad_spf_kernel<5>, pl.smem, attr));
+      SYSML_TRY(smem_attr(tc_wgrad_spf_kernel<5>, pl.smem));
     tc_wgrad_spf_kernel<5><<<p.splits, WG_THREADS, pl.smem, st>>>(p);
   } else {
-    static int attr = 0;
-    SYSML_TRY(set_smem_attr(tc_wgrad_spf_kernel<3>, pl.smem, attr));
+      SYSML_TRY(smem_attr(tc_wgrad_spf_kernel<3>, pl.smem));
     tc_wgrad_spf_kernel<3><<<p.splits, WG_THREADS, pl.smem, st>>>(p);
   }
   SYSML_LAUNCH_CHECK();
@@ -2383,8 +2407,7 @@ sysml_status tc_conv_bwd_filter(const ConvArgs &a, const float *x, const float *
   p.dy = dy;
   p.part = reinterpret_cast<float *>(ws);
   p.dbpart = db ? reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + pl.part_bytes) : nullptr;
-  static int attr = 0;
-  SYSML_TRY(set_smem_attr(tc_conv_wgrad_kernel, pl.smem, attr));
+  SYSML_TRY(smem_attr(tc_conv_wgrad_kernel, pl.smem));
   tc_conv_wgrad_kernel<<<p.splits * p.nwt, TC_THREADS, pl.smem, st>>>(p);
   SYSML_LAUNCH_CHECK();
   const int64_t total = (int64_t)a.K * a.C * a.R * a.S;

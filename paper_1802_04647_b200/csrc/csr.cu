@@ -29,6 +29,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
+#include "csr_dev.cuh"
 
 #include <algorithm>
 
@@ -46,11 +47,10 @@ __device__ __forceinline__ void stage_row_dense(const sysml_csr &m, int64_t row,
   for (int i = threadIdx.x; i < chw; i += blockDim.x) img[i] = 0.f;
   __syncthreads();
   const int j0 = __ldg(m.row_ptr + row), j1 = __ldg(m.row_ptr + row + 1);
-  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-    const int col = __ldg(m.col_idx + j);
-    const float v = __ldg(m.val + j);
-    if (col >= 0 && col < chw) atomicAdd(img + col, v);  // duplicates summed (reading R15)
-  }
+  // duplicates summed in stored order (reading R15; csr_dev.cuh)
+  csr_scatter_row(m.col_idx, m.val, j0, j1, threadIdx.x, blockDim.x,
+                  [&](int col) { return col >= 0 && col < chw ? img + col : nullptr; },
+                  [](bool b) { return __syncthreads_or(b) != 0; });
   __syncthreads();
 }
 
@@ -251,10 +251,9 @@ __global__ void csr_densify_kernel(sysml_csr m, float *__restrict__ dense) {
     for (int64_t i = threadIdx.x; i < m.cols; i += blockDim.x) row[i] = 0.f;
     __syncthreads();
     const int j0 = m.row_ptr[r], j1 = m.row_ptr[r + 1];
-    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-      const int c = m.col_idx[j];
-      if (c >= 0 && c < m.cols) atomicAdd(row + c, m.val[j]);
-    }
+    csr_scatter_row(m.col_idx, m.val, j0, j1, threadIdx.x, blockDim.x,
+                    [&](int c) { return c >= 0 && c < m.cols ? row + c : nullptr; },
+                    [](bool b) { return __syncthreads_or(b) != 0; });
     __syncthreads();
   }
 }
@@ -516,20 +515,10 @@ sysml_status csr_conv_fwd(const ConvArgs &a, const sysml_csr &x, const float *f,
   const size_t smem = fwd_smem(a);
   int blocks = a.N < 8 * sm_count() ? a.N : 8 * sm_count();
   if (pool) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      SYSML_CUDA(cudaFuncSetAttribute(csr_fwd_pool_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-      attr_set = true;
-    }
+    SYSML_TRY(smem_attr(csr_fwd_pool_kernel, 96 * 1024));
     csr_fwd_pool_kernel<<<blocks, CSR_THREADS, smem, st>>>(a, *pool, x, f, bias, pout, parg);
   } else {
-    static bool attr_set = false;
-    if (!attr_set) {
-      SYSML_CUDA(cudaFuncSetAttribute(csr_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      96 * 1024));
-      attr_set = true;
-    }
+    SYSML_TRY(smem_attr(csr_fwd_kernel, 96 * 1024));
     csr_fwd_kernel<<<blocks, CSR_THREADS, smem, st>>>(a, x, f, bias, y);
   }
   SYSML_LAUNCH_CHECK();
@@ -542,14 +531,21 @@ bool csr_bwd_filter_supported(const ConvArgs &a) {
          (int64_t)a.K * a.C * a.R * a.S <= MAX_FILTER_FLOATS;
 }
 
-size_t csr_bwd_filter_ws(const ConvArgs &a) {
-  int blocks = bwf_blocks(a);
-  if (wgrad_k32_ok(a)) {
-    size_t smem;
-    wgrad_k32_plan(a, &blocks, &smem);
-  }
+static size_t csr_bwf_part_ws(const ConvArgs &a, int blocks) {
   return align_up((size_t)blocks * a.K * a.C * a.R * a.S * sizeof(float), 256) +
          align_up((size_t)blocks * a.K * sizeof(float), 256);
+}
+
+// both routes of csr_conv_bwd_filter fit (the K32 kernel also needs a 16-byte aligned dy)
+size_t csr_bwd_filter_ws(const ConvArgs &a) {
+  size_t b = csr_bwf_part_ws(a, bwf_blocks(a));
+  if (wgrad_k32_ok(a)) {
+    int blocks;
+    size_t smem;
+    wgrad_k32_plan(a, &blocks, &smem);
+    b = std::max(b, csr_bwf_part_ws(a, blocks));
+  }
+  return b;
 }
 
 sysml_status csr_conv_bwd_filter(const ConvArgs &a, const sysml_csr &x, const float *dy,
@@ -558,12 +554,13 @@ sysml_status csr_conv_bwd_filter(const ConvArgs &a, const sysml_csr &x, const fl
     int blocks;
     size_t smem;
     const WgK32 g = wgrad_k32_plan(a, &blocks, &smem);
-    WsCarve wc(ws, (size_t)-1);
+    WsCarve wc(ws, csr_bwd_filter_ws(a));
     const int64_t kcrs = (int64_t)a.K * a.R * a.S;
     float *part = wc.take<float>((size_t)blocks * kcrs);
     float *dbpart = wc.take<float>((size_t)blocks * a.K);
+    SYSML_WS_FITS(wc);
     auto kern = (a.R == 5) ? csr_wgrad_k32_kernel<5, 5> : csr_wgrad_k32_kernel<3, 3>;
-    SYSML_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SYSML_TRY(smem_attr(kern, smem));
     kern<<<blocks, WG_THREADS, smem, st>>>(g, x, dy, part, db ? dbpart : nullptr);
     SYSML_LAUNCH_CHECK();
     ordered_sum_kernel<<<(unsigned)ceil_div(kcrs, 256), 256, 0, st>>>(part, blocks, kcrs, df);
@@ -577,17 +574,13 @@ sysml_status csr_conv_bwd_filter(const ConvArgs &a, const sysml_csr &x, const fl
   const int blocks = bwf_blocks(a);
   const int npb = (int)ceil_div(a.N, blocks);
   const int used = (int)ceil_div(a.N, npb);
-  WsCarve wc(ws, (size_t)-1);
+  WsCarve wc(ws, csr_bwd_filter_ws(a));
   const int64_t kcrs = (int64_t)a.K * a.C * a.R * a.S;
   float *part = wc.take<float>((size_t)blocks * kcrs);
   float *dbpart = wc.take<float>((size_t)blocks * a.K);
+  SYSML_WS_FITS(wc);
   const size_t smem = bwf_smem(a);
-  static bool attr_set = false;
-  if (!attr_set) {
-    SYSML_CUDA(cudaFuncSetAttribute(csr_bwd_filter_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_set = true;
-  }
+  SYSML_TRY(smem_attr(csr_bwd_filter_kernel, 200 * 1024));
   csr_bwd_filter_kernel<<<used, CSR_THREADS, smem, st>>>(a, x, dy, npb, part, db ? dbpart : nullptr);
   SYSML_LAUNCH_CHECK();
   ordered_sum_kernel<<<(unsigned)ceil_div(kcrs, 256), 256, 0, st>>>(part, used, kcrs, df);

@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
+#include "csr_dev.cuh"
 
 namespace sysml {
 
@@ -71,13 +72,14 @@ __global__ void __launch_bounds__(FB_THREADS)
       }
     } else {
       const int j0 = __ldg(xcsr.row_ptr + n), j1 = __ldg(xcsr.row_ptr + n + 1);
-      for (int jj = j0 + t; jj < j1; jj += FB_THREADS) {
-        const int col = __ldg(xcsr.col_idx + jj);
-        if (col >= 0 && col < a.H * a.W) {
-          const int h = col / a.W, w = col - h * a.W;
-          atomicAdd(img + (h + a.ph) * a.Wp + w + a.pw, __ldg(xcsr.val + jj));  // duplicates summed
-        }
-      }
+      // duplicates summed in stored order (reading R15; csr_dev.cuh)
+      csr_scatter_row(xcsr.col_idx, xcsr.val, j0, j1, t, FB_THREADS,
+                      [&](int col) -> float * {
+                        if (col < 0 || col >= a.H * a.W) return nullptr;
+                        const int h = col / a.W, w = col - h * a.W;
+                        return img + (h + a.ph) * a.Wp + w + a.pw;
+                      },
+                      [](bool b) { return __syncthreads_or(b) != 0; });
     }
     __syncthreads();
     if (!kok) continue;
@@ -223,13 +225,14 @@ __global__ void __launch_bounds__(FBB_THREADS)
       }
       ptx::named_bar_sync(1, FB_THREADS);
       const int j0 = __ldg(xcsr.row_ptr + n), j1 = __ldg(xcsr.row_ptr + n + 1);
-      for (int jj = j0 + t; jj < j1; jj += FB_THREADS) {
-        const int col = __ldg(xcsr.col_idx + jj);
-        if (col >= 0 && col < HW) {
-          const int h = col / a.W, w = col - h * a.W;
-          atomicAdd(img + (h + a.ph) * a.Wp + w + a.pw, __ldg(xcsr.val + jj));  // duplicates summed
-        }
-      }
+      // duplicates summed in stored order (reading R15; csr_dev.cuh)
+      csr_scatter_row(xcsr.col_idx, xcsr.val, j0, j1, t, FB_THREADS,
+                      [&](int col) -> float * {
+                        if (col < 0 || col >= HW) return nullptr;
+                        const int h = col / a.W, w = col - h * a.W;
+                        return img + (h + a.ph) * a.Wp + w + a.pw;
+                      },
+                      [](bool b) { return named_bar_or(1, FB_THREADS, b); });
     }
     ptx::named_bar_sync(1, FB_THREADS);  // image ready
     {
@@ -372,7 +375,7 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
     const size_t smem_bulk = FBB_STAGES * stage + align_up((size_t)a.Hp * a.Wp * 4, 16) + 8 * 2 * FBB_STAGES;
     const size_t sm_need = std::max(smem_b, smem_bulk);
     auto kern = RS == 25 ? pool_bwd_wgrad_c1_bulk_kernel<5, 5> : pool_bwd_wgrad_c1_bulk_kernel<3, 3>;
-    SYSML_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_need));
+    SYSML_TRY(smem_attr(kern, sm_need));
     kern<<<used, FBB_THREADS, sm_need, st>>>(a, x, cs, xcsr != nullptr, dpool, part);
     SYSML_LAUNCH_CHECK();
     fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 32), dim3(32, 8), 0, st>>>(
@@ -381,21 +384,11 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
     return SYSML_OK;
   }
   if (RS == 25) {
-    static bool attr = false;
-    if (!attr) {
-      SYSML_CUDA(cudaFuncSetAttribute(pool_bwd_wgrad_c1_kernel<5, 5>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-      attr = true;
-    }
+    SYSML_TRY(smem_attr(pool_bwd_wgrad_c1_kernel<5, 5>, 64 * 1024));
     pool_bwd_wgrad_c1_kernel<5, 5><<<used, FB_THREADS, smem, st>>>(a, x, cs, xcsr != nullptr, dpool,
                                                                  argmax, mask, part);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      SYSML_CUDA(cudaFuncSetAttribute(pool_bwd_wgrad_c1_kernel<3, 3>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-      attr = true;
-    }
+    SYSML_TRY(smem_attr(pool_bwd_wgrad_c1_kernel<3, 3>, 64 * 1024));
     pool_bwd_wgrad_c1_kernel<3, 3><<<used, FB_THREADS, smem, st>>>(a, x, cs, xcsr != nullptr, dpool,
                                                                 argmax, mask, part);
   }

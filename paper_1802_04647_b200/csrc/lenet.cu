@@ -783,7 +783,17 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
   SYSML_CHECK_ARG((x->is_csr != 0) == (h->csr != 0),
                   "input is_csr=%d but the handle was created with input_is_csr=%d", x->is_csr,
                   h->csr);
+  SYSML_CHECK_ALIGN16(params, "params");
+  SYSML_CHECK_ALIGN16(grads, "grads");
+  SYSML_CHECK_ALIGN(labels, 4, "labels");
+  SYSML_CHECK_ALIGN(loss_sum, 4, "loss_sum");
+  SYSML_CHECK_ALIGN(pred, 4, "pred");
+  SYSML_CHECK_ALIGN16(probs, "probs");
+  if (!x->is_csr) SYSML_CHECK_ALIGN16(x->dense, "dense input");
   if (x->is_csr) {
+    SYSML_CHECK_ALIGN(x->csr.row_ptr, 4, "CSR row_ptr");
+    SYSML_CHECK_ALIGN(x->csr.col_idx, 4, "CSR col_idx");
+    SYSML_CHECK_ALIGN(x->csr.val, 4, "CSR val");
     SYSML_CHECK_SHAPE(x->csr.rows == n_local && x->csr.cols == 784,
                       "CSR input %lldx%lld must be n_local x 784 = %dx784",
                       (long long)x->csr.rows, (long long)x->csr.cols, n_local);
@@ -856,12 +866,7 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
   // F3
   SYSML_TRY(T.begin(2));
   {
-    static bool attr = false;
-    if (!attr) {
-      SYSML_CUDA(cudaFuncSetAttribute(affine_softmax_ce_smem_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F3_SMEM));
-      attr = true;
-    }
+    SYSML_TRY(smem_attr(affine_softmax_ce_smem_kernel, F3_SMEM));
     const int ctas = (int)std::min<int64_t>(sm_count(), (n + 1) / 2);
     affine_softmax_ce_smem_kernel<<<(unsigned)ctas, F3_THREADS, F3_SMEM, st>>>(
         n, inv_ng, h->a2, params + OFF_W3, params + OFF_B3, labels, h->ds, h->lossn);

@@ -440,12 +440,13 @@ sysml_status im2col_conv_bwd_filter(const ConvArgs &a, const float *x, const flo
     set_error("im2col bwd_filter: unsupported shape");
     return SYSML_ERR_UNSUPPORTED;
   }
-  WsCarve wc(ws, (size_t)-1);
+  WsCarve wc(ws, im2col_bwd_filter_ws(a));
   float *xcol = reinterpret_cast<float *>(wc.take<char>(pl.col_bytes));
   float *dyp = pl.dyp_bytes ? reinterpret_cast<float *>(wc.take<char>(pl.dyp_bytes)) : nullptr;
   float *dfp = pl.part_bytes ? reinterpret_cast<float *>(wc.take<char>(pl.part_bytes)) : nullptr;
   float *dbp = pl.dbpart_bytes ? reinterpret_cast<float *>(wc.take<char>(pl.dbpart_bytes)) : nullptr;
   void *gws = wc.take<char>(pl.gemm_ws);
+  SYSML_WS_FITS(wc);
   const int CRS = a.C * a.R * a.S;
   const int64_t PQ = (int64_t)a.P * a.Q;
   for (int i = 0; i < pl.nchunks; ++i) {
@@ -492,10 +493,11 @@ size_t phase_fwd_ws(const ConvArgs &a) {
 sysml_status phase_conv_fwd(const ConvArgs &a, const float *x, const float *f, const float *bias,
                             float *y, void *ws, cudaStream_t st) {
   const ConvArgs b = phase_args(a);
-  WsCarve wc(ws, (size_t)-1);
+  WsCarve wc(ws, phase_fwd_ws(a));
   float *xp = wc.take<float>((size_t)b.N * b.C * b.H * b.W);
   float *fp = wc.take<float>((size_t)b.K * b.C * b.R * b.S);
   void *tws = wc.take<char>(tc_fwd_ws(b));
+  SYSML_WS_FITS(wc);
   SYSML_TRY(split_f(a, b, f, fp, st));
   if (fused_ok() && tc_fwd_phase_fused_ok(a, b))  // X' gathered by the conv kernel's producer
     return tc_conv_fwd_phase(a, b, x, fp, bias, y, tws, st);
@@ -516,10 +518,11 @@ size_t phase_bwd_data_ws(const ConvArgs &a) {
 sysml_status phase_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
                                  void *ws, cudaStream_t st) {
   const ConvArgs b = phase_args(a);
-  WsCarve wc(ws, (size_t)-1);
+  WsCarve wc(ws, phase_bwd_data_ws(a));
   float *dxp = wc.take<float>((size_t)b.N * b.C * b.H * b.W);
   float *fp = wc.take<float>((size_t)b.K * b.C * b.R * b.S);
   void *tws = wc.take<char>(tc_bwd_data_ws(b));
+  SYSML_WS_FITS(wc);
   SYSML_TRY(split_f(a, b, f, fp, st));
   if (fused_ok() && tc_bwd_data_phase_fused_ok(a, b))  // dX' scattered by the conv epilogue
     return tc_conv_bwd_data_phase(a, b, fp, dy, dx, tws, st);
@@ -540,9 +543,10 @@ size_t phase_simt_bwd_data_ws(const ConvArgs &a) {
 sysml_status phase_simt_conv_bwd_data(const ConvArgs &a, const float *f, const float *dy, float *dx,
                                       void *ws, cudaStream_t st) {
   const ConvArgs b = phase_args(a);
-  WsCarve wc(ws, (size_t)-1);
+  WsCarve wc(ws, phase_simt_bwd_data_ws(a));
   float *dxp = wc.take<float>((size_t)b.N * b.C * b.H * b.W);
   float *fp = wc.take<float>((size_t)b.K * b.C * b.R * b.S);
+  SYSML_WS_FITS(wc);
   SYSML_TRY(split_f(a, b, f, fp, st));
   SYSML_TRY(simt_conv_bwd_data(b, fp, dy, dxp, st));
   return merge_dx(a, b, dxp, dx, st);
@@ -557,18 +561,25 @@ bool phase_bwd_filter_supported(const ConvArgs &a) {
   return is_phase_shape(a) && tc_bwd_filter_supported(phase_args(a));
 }
 
+// the inner stride-1 problem runs on the frame kernel whenever it supports it (same test as
+// phase_conv_bwd_filter below), else on tc_conv_bwd_filter's own route: size for that kernel
+static size_t phase_inner_wgrad_ws(const ConvArgs &b) {
+  return tc_wgrad_frame_supported(b) ? tc_wgrad_frame_ws(b) : tc_bwd_filter_ws(b);
+}
+
 size_t phase_bwd_filter_ws(const ConvArgs &a) {
   const ConvArgs b = phase_args(a);
-  return x2_bytes(b) + f2_bytes(b) + align_up(tc_bwd_filter_ws(b), 256);
+  return x2_bytes(b) + f2_bytes(b) + align_up(phase_inner_wgrad_ws(b), 256);
 }
 
 sysml_status phase_conv_bwd_filter(const ConvArgs &a, const float *x, const float *dy, float *df,
                                    float *db, void *ws, cudaStream_t st) {
   const ConvArgs b = phase_args(a);
-  WsCarve wc(ws, (size_t)-1);
+  WsCarve wc(ws, phase_bwd_filter_ws(a));
   float *xp = reinterpret_cast<float *>(wc.take<char>(x2_bytes(b)));
   float *dfp = wc.take<float>((size_t)b.K * b.C * b.R * b.S);
-  void *tws = wc.take<char>(tc_bwd_filter_ws(b));
+  void *tws = wc.take<char>(phase_inner_wgrad_ws(b));
+  SYSML_WS_FITS(wc);
   if (tc_wgrad_frame_supported(b)) {  // X' written straight into the frame (no second pass)
     SYSML_TRY(split_x(a, b, x, xp, st, /*frame=*/true));
     SYSML_TRY(tc_wgrad_frame(b, xp, dy, dfp, db, tws, st, /*x_framed=*/true));

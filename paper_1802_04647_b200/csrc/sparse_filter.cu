@@ -11,6 +11,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "csr_dev.cuh"
 
 namespace sysml {
 namespace {
@@ -45,10 +46,10 @@ __global__ void __launch_bounds__(SF_THREADS) conv_csr_filter_kernel(SfArgs a, c
     for (int64_t i = threadIdx.x; i < CHW; i += SF_THREADS) img[i] = 0.f;
     __syncthreads();
     const int j0 = xc.row_ptr[n], j1 = xc.row_ptr[n + 1];
-    for (int j = j0 + threadIdx.x; j < j1; j += SF_THREADS) {
-      const int col = xc.col_idx[j];
-      if (col >= 0 && col < CHW) atomicAdd(img + col, xc.val[j]);
-    }
+    // duplicates summed in stored order (reading R15; csr_dev.cuh)
+    csr_scatter_row(xc.col_idx, xc.val, j0, j1, threadIdx.x, SF_THREADS,
+                    [&](int col) { return col >= 0 && col < CHW ? img + col : nullptr; },
+                    [](bool b) { return __syncthreads_or(b) != 0; });
     xn = img;
   }
   const int RS = a.R * a.S, CRS = a.C * RS;
@@ -185,15 +186,7 @@ sysml_status sysml_conv2d_csr_filter(const sysml_conv_desc *d, const sysml_input
   a.nchunk = (int)ceil_div(g.P * g.Q, SF_THREADS);
   SYSML_CHECK_SHAPE((int64_t)a.nchunk * g.N < (1ll << 31) && g.K <= 65535, "sparse-filter conv grid too large");
   const size_t smem = sizeof(int4) * SF_CHUNK + (x->is_csr ? sizeof(float) * (size_t)(g.C * g.H * g.W) : 0);
-  static std::mutex mu;
-  static size_t attr = 0;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    if (smem > 48 * 1024 && smem > attr) {
-      SYSML_CUDA(cudaFuncSetAttribute(conv_csr_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
-  }
+  if (smem > 48 * 1024) SYSML_TRY(smem_attr(conv_csr_filter_kernel, smem));
   conv_csr_filter_kernel<<<dim3((unsigned)(a.nchunk * g.N), (unsigned)g.K), SF_THREADS, smem, (cudaStream_t)stream>>>(
       a, x->is_csr ? nullptr : x->dense, x->csr, x->is_csr, *f, bias, y);
   SYSML_LAUNCH_CHECK();
@@ -221,6 +214,15 @@ sysml_status sysml_count_nonzeros(const float *x, int64_t n, int64_t *nnz_host, 
   SYSML_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
   SYSML_CUDA(cudaStreamSynchronize(st));
   *nnz_host = (int64_t)h;
+  return SYSML_OK;
+}
+
+sysml_status sysml_decide_format(const float *x, int64_t n, double threshold, int32_t *is_sparse,
+                                 int64_t *nnz_host, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(is_sparse && nnz_host, "bad argument to sysml_decide_format");
+  SYSML_TRY(sysml_count_nonzeros(x, n, nnz_host, stream));
+  const double thr = threshold > 0.0 ? threshold : SYSML_SPARSITY_THRESHOLD;
+  *is_sparse = (n > 0 && (double)*nnz_host <= thr * (double)n) ? 1 : 0;
   return SYSML_OK;
 }
 

@@ -316,12 +316,7 @@ sysml_status tc_wgrad_1x1(const ConvArgs &a, const float *x, const float *dy, fl
     if (!tmap_encode_f32(&tmB, x, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return SYSML_ERR_CUDA;
   }
-  static int attr = 0;
-  if ((int)pl.smem > attr) {
-    SYSML_CUDA(cudaFuncSetAttribute(tc_wgrad_1x1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)pl.smem));
-    attr = (int)pl.smem;
-  }
+  SYSML_TRY(smem_attr(tc_wgrad_1x1_kernel, pl.smem));
   tc_wgrad_1x1_kernel<<<pl.grid, W1_THREADS, pl.smem, st>>>(tmA, tmB, p);
   SYSML_LAUNCH_CHECK();
   const int64_t total = (int64_t)a.K * a.C;

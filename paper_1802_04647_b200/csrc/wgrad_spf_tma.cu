@@ -544,7 +544,7 @@ sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float
   auto kern = p.shift == 32 ? tc_wgrad_spf_tma_kernel<32>
               : p.shift == 16 ? tc_wgrad_spf_tma_kernel<16>
                               : tc_wgrad_spf_tma_kernel<0>;
-  SYSML_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+  SYSML_TRY(smem_attr(kern, pl.smem));
   static long long *dclk = nullptr;
   const bool prof = getenv("SYSML_TC_PROFILE") != nullptr;
   p.clk = nullptr;

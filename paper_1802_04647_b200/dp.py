@@ -52,18 +52,21 @@ def allreduce_sum_(t, group=None):
 class DataParallelLeNet:
     """One rank of the data-parallel LeNet SGD step (global batch sharded by rows)."""
 
-    def __init__(self, global_batch: int, math: str = "tf32", group=None):
+    def __init__(self, global_batch: int, math: str = "tf32", group=None, net=None, sgd=None):
+        """net / sgd: the per-rank LeNet handle and SGD update (default: libsysml's); the CPU
+        multi-process tests pass stand-ins to exercise this host logic over gloo."""
         import torch.distributed as dist
-        from . import LeNet, nccl_comm_ptr
+        from . import LeNet, nccl_comm_ptr, sysml_sgd_update
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.shard = shard_rows(self.rank, self.world, global_batch)
         self.global_batch = global_batch
         self.group = group
-        self.net = LeNet(self.shard.size, math=math)
+        self.net = net if net is not None else LeNet(self.shard.size, math=math)
+        self.sgd = sgd if sgd is not None else sysml_sgd_update
         self.comm: Optional[int] = None
         self.use_lib_nccl = False
-        if self.world > 1:
+        if self.world > 1 and dist.get_backend(group) == "nccl":
             import torch
             t = torch.ones(1, device="cuda")
             dist.all_reduce(t, group=group)  # creates the communicator
@@ -71,7 +74,7 @@ class DataParallelLeNet:
             self.use_lib_nccl = self.comm is not None
 
     def step(self, params, grads, x_local, labels_local, lr=0.01, loss_sum=None):
-        from . import SysmlError, sysml_sgd_update
+        from . import SysmlError
         if self.world == 1 or self.use_lib_nccl:
             try:
                 self.net.step(params, grads, x_local, labels_local, self.global_batch, lr=lr,
@@ -82,5 +85,5 @@ class DataParallelLeNet:
                     raise
                 self.use_lib_nccl = False
         self.net.fwd_bwd(params, x_local, labels_local, self.global_batch, grads, loss_sum)
-        allreduce_sum_(grads, self.group)
-        sysml_sgd_update(params, grads, lr)
+        allreduce_sum_(grads, self.group)  # loss_sum stays this rank's share, as in the library path
+        self.sgd(params, grads, lr)

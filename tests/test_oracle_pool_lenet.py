@@ -217,3 +217,41 @@ def test_lenet_predict_properties():
     prm2 = prm.copy()
     prm2[-10:] += 3.25
     assert np.allclose(oracle.lenet_predict(x, prm2)[1], probs, rtol=0, atol=1e-12)
+
+
+def test_lenet_predict_vs_torch_softmax_fp64():
+    """oracle_lenet_predict's softmax against torch.softmax in fp64 on the
+    oracle's own forward scores (pinned above), and its label against torch.argmax
+    (first maximal index).  A base-2 exponential, a missing max shift that overflows, or a
+    wrong normalisation axis fails here."""
+    import torch
+    rng = np.random.default_rng(7)
+    x = rng.random((9, 784))
+    prm = synth.lenet_params(seed=(33,)).astype(np.float64)
+    prm[-10:] += rng.normal(0, 3.0, 10)        # spread the logits so the softmax is not flat
+    sc = torch.from_numpy(oracle.lenet_forward(x, prm)["scores"])
+    pred, probs = oracle.lenet_predict(x, prm)
+    ref = torch.softmax(sc, dim=1).numpy()
+    assert np.abs(probs - ref).max() <= 1e-14
+    assert np.array_equal(pred, torch.argmax(sc, dim=1).numpy().astype(np.int32))
+
+
+def test_lenet_predict_closed_forms():
+    """Closed forms of the scoring softmax: W3 = 0 makes the logits equal b3 for every image.
+    b3 = 0 -> p = 1/10 and label 0 (first maximal class of a ten-way tie);
+    b3 = (ln 2, 0, ..., 0) -> p0 = 2/11, pj = 1/11; b3 = 800 on class 7 only -> label 7, p7 ~ 1
+    without overflow (the max shift)."""
+    x = synth.mnist_like(3, seed=(34,)).astype(np.float64)
+    prm = synth.lenet_params(seed=(35,)).astype(np.float64)
+    prm[-10 - 31360:-10] = 0.0
+    prm[-10:] = 0.0
+    pred, probs = oracle.lenet_predict(x, prm)
+    assert np.array_equal(pred, [0, 0, 0]) and np.abs(probs - 0.1).max() <= 1e-15
+    prm[-10] = np.log(2.0)
+    pred, probs = oracle.lenet_predict(x, prm)
+    assert np.abs(probs[:, 0] - 2 / 11).max() <= 1e-15 and np.abs(probs[:, 1:] - 1 / 11).max() <= 1e-15
+    prm[-10:] = 0.0
+    prm[-3] = 800.0
+    pred, probs = oracle.lenet_predict(x, prm)
+    assert np.array_equal(pred, [7, 7, 7]) and np.all(np.isfinite(probs))
+    assert np.abs(probs[:, 7] - 1.0).max() <= 1e-15
