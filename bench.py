@@ -10,7 +10,15 @@ softmax + cross-entropy, maxpool_bwd, conv bwd_filter / bwd_data, the NCCL
 allreduce of dW/db (N > 1) and the SGD update -- all in libsysml kernels.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-  (N > 1: torchrun --nproc-per-node N ... bench.py --gpus N)
+  (N > 1 without WORLD_SIZE in the environment: re-executes itself under
+   torch.distributed.run with N local ranks; under torchrun it asserts WORLD_SIZE == N)
+
+Besides the headline (BJ configs[4]) the line carries one leg per other BASELINE config:
+cfg1 (conv1 fwd / bwd_filter / bwd_data latency at N = 8), cfg2 (dense LeNet step at
+N = 64), cfg3 (CSR LeNet step at N = 256 with the K7 / K8 CSR conv1 kernels against the
+6.6 us bar), cfg4 (`layers`: ResNet-style conv GFLOP/s vs the TF32 peak, with the route each
+op took), the per-rank step at local batch 1024 (one rank's share at N = 8), and the oracle
+timed on each config (`oracle_per_config`).
 
 Prints ONE JSON line (rank 0).  Timing: CUDA events on the launching stream,
 barrier + synchronize on both sides, max over ranks.  L2: each step reads one of
@@ -39,13 +47,72 @@ UNIT = "images/s"
 ROTATE = 8
 
 
+TF32_SPEC_TFLOPS = 1125.0  # nominal dense TF32 (B200_PROFILING.md), context only
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
-                    sm_max=d.get("sm_max_mhz", 1965.0), src="measured (MEASURED_PEAKS.json)")
-    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, sm_max=1965.0, src="fallback (B200_PROFILING.md)")
+        pk = dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                  sm_max=d.get("sm_max_mhz", 1965.0), src="measured (MEASURED_PEAKS.json)")
+    else:
+        pk = dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, sm_max=1965.0, src="fallback (B200_PROFILING.md)")
+    # a TF32 contraction takes the bf16 measured peak x the nominal tf32/bf16 ratio (1.125/2.25)
+    pk["tf32"], pk["tf32_sus"] = 0.5 * pk["bf16"], 0.5 * pk["bf16_sus"]
+    pk["fp32_alu"] = 148 * 128 * 2 * pk["sm_max"] * 1e6 / 1e12
+    return pk
+
+
+def tf32_cublas_peak(reps=10):
+    """cuBLAS TF32 GEMM (torch.matmul fp32 8192^3, allow_tf32), best of `reps`: the measured
+    TF32 peak BASELINE.md section 4 asks for, reported beside the bf16-derived denominator.
+    Library code is the measuring stick here only -- it is never on the product path."""
+    import torch
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        c = torch.empty(n, n, device="cuda")
+        for _ in range(3):
+            torch.matmul(a, b, out=c)
+        best = 1e9
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(); torch.matmul(a, b, out=c); e1.record(); e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b, c
+        return round(2.0 * n ** 3 / (best * 1e-3) / 1e12, 1)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+
+
+def regime(clocks, sm_max):
+    """Which measured peak applies: 'sustained' when the clock record shows the power-capped
+    regime (sw_power_cap active, or median SM clock below 90% of max), else 'burst'."""
+    mhz = clocks.get("sm_mhz")
+    if "sw_power_cap" in clocks.get("reasons", []) or (mhz is not None and mhz < 0.9 * sm_max):
+        return "sustained"
+    return "burst"
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # Per-image algorithmic work of each step stage (DESIGN.md "Roofline"):
@@ -128,6 +195,19 @@ def dist_env():
     return world, rank, local
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` run without torchrun: re-execute under torch.distributed.run with N
+    local ranks (one process per GPU, 127.0.0.1 rendezvous); rank 0 prints the line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def cpu_oracle_rate(target_s: float = 15.0, max_images: int = 4096):
     """Time the fp64 oracle LeNet step (fwd+bwd+SGD) on a bounded sample of the workload."""
     import oracle
@@ -179,7 +259,7 @@ def reference_arm(args, world, rank):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": "DP LeNet minibatch SGD (BJ configs[4])",
                                         "global_batch": GLOBAL_BATCH, "sample_per_step": per_step},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                          "sample": f"{per_step} images of the global-batch-{GLOBAL_BATCH} step per timed step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -201,12 +281,165 @@ def time_op(fn, reps, flush=None):
     return statistics.median(ts), min(ts)
 
 
+def time_graph(fn, reps, flush=None, warm=3):
+    """Capture fn into a CUDA graph and time each replay (L2 flushed before each when given)."""
+    import torch
+    st = torch.cuda.current_stream()
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(st)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cs):
+        fn()
+    st.wait_stream(cs)
+    torch.cuda.synchronize()
+    ts = []
+    for i in range(reps + 2):
+        if flush is not None:
+            flush.zero_()
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(st); g.replay(); b.record(st)
+        b.synchronize()
+        if i >= 2:
+            ts.append(a.elapsed_time(b))
+    return statistics.median(ts), min(ts)
+
+
+def config_legs(S, peaks, quick=False):
+    """BASELINE configs 1-3 and the per-rank step of the 8-GPU configuration, each op or step
+    timed alone on the device (CUDA events, L2 flushed between reps)."""
+    import torch
+    import synth
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    reps = 10 if quick else 50
+    out = {}
+    # ---- cfg1: single LeNet conv1 layer fwd + bwd, N = 8, dense, launch/latency-bound
+    N = 8
+    x, f, b, dy = synth.conv_problem_U(N, 1, 28, 28, 32, 5, 5, 28, 28, seed=(1100,))
+    x = synth.mnist_like(N, seed=(1101,))
+    x, f, b, dy = (torch.from_numpy(t).cuda() for t in (x, f, b, dy))
+    ws = torch.empty(1 << 26, dtype=torch.uint8, device="cuda")
+    c1 = {"N": N, "unit": "us", "note": "median per call, eager launch through the C ABI (ctypes), L2 flushed"}
+    for math in ("tf32", "fp32"):
+        d = S.conv_desc(N, 1, 28, 28, 32, 5, 5, 1, 2, math)
+        y = torch.empty(N, 32 * 784, device="cuda")
+        dx = torch.empty(N, 784, device="cuda")
+        df = torch.empty(32, 25, device="cuda"); db = torch.empty(32, device="cuda")
+        row = {}
+        for op, fn in (("fwd_bias", lambda: S.sysml_conv2d(x, f, d, bias=b, out=y, workspace=ws)),
+                       ("bwd_filter_db", lambda: S.sysml_conv2d_bwd_filter(x, dy, d, df=df, db=db, workspace=ws)),
+                       ("bwd_data", lambda: S.sysml_conv2d_bwd_data(f, dy, d, dx=dx, workspace=ws))):
+            med, mn = time_op(fn, reps, flush)
+            row[op] = {"us": round(1e3 * med, 2), "min_us": round(1e3 * mn, 2), "route": S.sysml_last_route()}
+        gmed, _ = time_graph(lambda: (S.sysml_conv2d(x, f, d, bias=b, out=y, workspace=ws),
+                                      S.sysml_conv2d_bwd_filter(x, dy, d, df=df, db=db, workspace=ws),
+                                      S.sysml_conv2d_bwd_data(f, dy, d, dx=dx, workspace=ws)), reps, flush)
+        row["fwd_bwd_graph_us"] = round(1e3 * gmed, 2)
+        c1[math] = row
+    out["cfg1_conv1_N8"] = c1
+    # ---- cfg2: LeNet step, N = 64, dense; cfg3: LeNet step, N = 256, CSR input
+    prm = torch.from_numpy(synth.lenet_params(seed=(6,))).cuda()
+    for name, n, csr in (("cfg2_lenet_step_N64_dense", 64, False), ("cfg3_lenet_step_N256_csr", 256, True)):
+        xh = synth.mnist_like(n, seed=(1102, n))
+        yl = torch.from_numpy(synth.labels(n, seed=(1103, n))).cuda()
+        if csr:
+            rp, ci, v = synth.to_csr(xh)
+            xin = S.CSR(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(), torch.from_numpy(v).cuda(), n, 784)
+        else:
+            xin = torch.from_numpy(xh).cuda()
+        row = {"N": n, "input": "CSR (density %.3f)" % (np.count_nonzero(xh) / xh.size) if csr else "dense"}
+        for math in ("tf32", "fp32"):
+            net = S.LeNet(n, math=math, csr=csr, max_nnz=n * 784)
+            p = prm.clone()
+            g = torch.empty_like(p)
+            med, mn = time_graph(lambda: net.step(p, g, xin, yl, n, lr=0.01), reps, flush)
+            row[math] = {"us_per_step": round(1e3 * med, 2), "images_per_s": round(n / (med * 1e-3), 1),
+                         "launch": "cuda_graph"}
+            del net
+        out[name] = row
+    # cfg3's CSR conv1 kernels alone at N = 256 (K7 fwd, K7 fused epilogue, K8 bwd_filter)
+    n = 256
+    xh = synth.mnist_like(n, seed=(1102, n))
+    rp, ci, v = synth.to_csr(xh)
+    m = S.CSR(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(), torch.from_numpy(v).cuda(), n, 784)
+    f = torch.from_numpy(synth.normal((32, 25), 0.28, seed=(1002,))).cuda()
+    b = torch.zeros(32, device="cuda")
+    dy = torch.from_numpy(synth.normal((n, 32 * 784), seed=(1104,))).cuda()
+    d = S.conv_desc(n, 1, 28, 28, 32, 5, 5, 1, 2, "tf32")
+    pd = S.pool_desc(n, 32, 28, 28, 2, 2, 2, 0, True)
+    y = torch.empty(n, 32 * 784, device="cuda")
+    pout = torch.empty(n, 32 * 196, device="cuda"); parg = torch.empty(n, 32 * 196, dtype=torch.int32, device="cuda")
+    df = torch.empty(32, 25, device="cuda"); db = torch.empty(32, device="cuda")
+    nnz = int(ci.size)
+    k7_bytes = 4 * (n + 1) + 8 * nnz + 4 * (800 + 32) + 4 * n * 32 * 784
+    k7f_bytes = 4 * (n + 1) + 8 * nnz + 4 * (800 + 32) + 8 * n * 32 * 196
+    k8_bytes = 4 * (n + 1) + 8 * nnz + 4 * n * 32 * 784 + 4 * 832
+    k = {"N": n, "nnz": nnz, "bar_us_K7_unfused": round(k7_bytes / (0.6 * peaks["hbm"] * 1e9) * 1e6, 2),
+         "bar_note": "SURVEY 8(d) cfg 3: K7 unfused at 60% of HBM"}
+    for op, fn, nb in (("K7_fwd", lambda: S.sysml_conv2d(m, f, d, bias=b, out=y, workspace=ws), k7_bytes),
+                       ("K7_fwd_bias_relu_pool", lambda: S.sysml_conv2d_bias_relu_maxpool(
+                           m, f, b, d, pd, out=pout, argmax=parg, workspace=ws), k7f_bytes),
+                       ("K8_bwd_filter", lambda: S.sysml_conv2d_bwd_filter(m, dy, d, df=df, db=db, workspace=ws), k8_bytes)):
+        med, mn = time_op(fn, reps, flush)
+        gmed, _ = time_graph(fn, reps, flush)
+        k[op] = {"us": round(1e3 * med, 2), "graph_us": round(1e3 * gmed, 2),
+                 "gbs_graph": round(nb / (gmed * 1e-3) / 1e9, 1), "route": S.sysml_last_route()}
+    out["cfg3_csr_conv1_kernels_N256"] = k
+    # ---- one rank's share of the 8-GPU step (local batch 1024, n_global 8192), graph replay
+    n = GLOBAL_BATCH // 8
+    xs = [torch.from_numpy(synth.mnist_like(n, seed=(1105, i))).cuda() for i in range(4)]
+    ys = [torch.from_numpy(synth.labels(n, seed=(1106, i))).cuda() for i in range(4)]
+    net = S.LeNet(n, math="tf32")
+    p = prm.clone()
+    g = torch.empty_like(p)
+    med, mn = time_graph(lambda: net.step(p, g, xs[0], ys[0], GLOBAL_BATCH, lr=0.01), reps, flush)
+    out["per_rank_step_local1024"] = {"us_per_step": round(1e3 * med, 2), "min_us": round(1e3 * mn, 2),
+                                      "note": "one rank's compute at N = 8 (no allreduce: 1 GPU); "
+                                              "8-GPU efficiency = t(8192) / (8 (t(1024) + t_allreduce))"}
+    return out
+
+
+def oracle_per_config():
+    """The fp64 oracle timed on each BASELINE config (bounded samples, scaled), host cores."""
+    import oracle
+    import synth
+    res = {"cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)), "cpu_model": cpu_model()}
+
+    def t(fn):
+        t0 = time.perf_counter(); fn(); return time.perf_counter() - t0
+    x = synth.mnist_like(8, seed=(1,)).astype(np.float64)
+    f = synth.normal((32, 25), 0.3, seed=(2,)).astype(np.float64)
+    dy = synth.normal((8, 32 * 784), seed=(3,)).astype(np.float64)
+    res["cfg1_conv1_N8_ms"] = {
+        "fwd": round(1e3 * t(lambda: oracle.conv2d_fwd(x, f, 8, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2))), 2),
+        "bwd_filter": round(1e3 * t(lambda: oracle.conv2d_bwd_filter(x, dy, 8, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2))), 2),
+        "bwd_data": round(1e3 * t(lambda: oracle.conv2d_bwd_data(f, dy, 8, 1, 28, 28, 32, 5, 5, (1, 1), (2, 2))), 2)}
+    prm = synth.lenet_params(seed=(6,)).astype(np.float64)
+    for name, n in (("cfg2_lenet_step_N64_s", 64), ("cfg3_lenet_step_N256_s", 256)):
+        xx = synth.mnist_like(n, seed=(4, n)); yy = synth.labels(n, seed=(5, n))
+        res[name] = round(t(lambda: oracle.sgd_update(prm, oracle.lenet_fwd_bwd(xx, yy, prm)[0], 0.01)), 3)
+    c4 = {}
+    for lname, (C, H, K, R, pd) in {"resnet3x3_C256_K256_14x14": (256, 14, 256, 3, 1),
+                                   "resnet1x1_C1024_K256_14x14": (1024, 14, 256, 1, 0)}.items():
+        ns = 2  # sample of the N = 128 layer, scaled x64
+        xx, ff, bb, dd = synth.conv_problem_U(ns, C, H, H, K, R, R, H, H, seed=(7,))
+        c4[lname] = {op: round(128 / ns * t(fn), 2) for op, fn in (
+            ("fwd", lambda: oracle.conv2d_fwd(xx, ff, ns, C, H, H, K, R, R, (1, 1), (pd, pd), bias=bb)),
+            ("bwd_filter", lambda: oracle.conv2d_bwd_filter(xx, dd, ns, C, H, H, K, R, R, (1, 1), (pd, pd))),
+            ("bwd_data", lambda: oracle.conv2d_bwd_data(ff, dd, ns, C, H, H, K, R, R, (1, 1), (pd, pd))))}
+    res["cfg4_layers_N128_s"] = c4
+    res["cfg4_note"] = "N = 2 sample scaled x64 to N = 128"
+    return res
+
+
 def layer_section(S, peaks, quick=False):
     """conv2d GFLOP/s vs TF32 peak on the BJ ResNet-style layers (cfg 4) and the CSR
     conv1 bandwidth case (cfg 3), each op timed alone with an L2 flush between reps."""
     import torch
     import synth
-    tf32_peak = peaks["bf16"] * 0.5  # nominal tf32/bf16 = 1.125/2.25
+    tf32_peak = peaks["tf32"]  # burst: each op is timed alone (bf16 measured x 1.125/2.25)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
     out = {}
     reps = 5 if quick else 20
@@ -236,8 +469,12 @@ def layer_section(S, peaks, quick=False):
         ):
             med, mn = time_op(fn, reps, flush)
             tfs = flops / (med * 1e-3) / 1e12
+            gbs = nbytes / (med * 1e-3) / 1e9
             res[op] = {"ms": round(med, 4), "tflops": round(tfs, 2), "frac_tf32_peak": round(tfs / tf32_peak, 4),
-                       "gbs": round(nbytes / (med * 1e-3) / 1e9, 1)}
+                       "gbs": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 4),
+                       "route": S.sysml_last_route()}
+            if peaks.get("tf32_cublas"):
+                res[op]["frac_tf32_cublas"] = round(tfs / peaks["tf32_cublas"], 4)
         out[name] = res
         del x, f, b, dy, y, dx
     # CSR conv1 (BJ cfg 3 shape, N = 16384 as the bandwidth headline)
@@ -266,8 +503,12 @@ def layer_section(S, peaks, quick=False):
                            ("bwd_filter", lambda: S.sysml_conv2d_bwd_filter(m, dy, d, df=df, db=db, workspace=ws), bwf_bytes)):
         med, mn = time_op(fn, reps, flush)
         gbs = nbytes / (med * 1e-3) / 1e9
-        res[op] = {"ms": round(med, 4), "gbs": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 4)}
+        res[op] = {"ms": round(med, 4), "gbs": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 4),
+                   "route": S.sysml_last_route()}
     out[f"csr_lenet_conv1_N{N}"] = res
+    out["peak_note"] = ("frac_tf32_peak: of the burst TF32 denominator (measured bf16 x 0.5 = %.1f TFLOP/s); "
+                        "frac_tf32_cublas: of cuBLAS TF32 measured live; frac_hbm: of measured HBM copy %.1f GB/s"
+                        % (tf32_peak, peaks["hbm"]))
     return out
 
 
@@ -415,30 +656,44 @@ def ours_arm(args, world, rank, local):
         ms_score = float(t.item())
     score_value = GLOBAL_BATCH * args.steps / (ms_score * 1e-3)
 
-    # ---- roofline of the dominant stage
-    tf32_sus = peaks["bf16_sus"] * 0.5
-    fp32_alu = 148 * 128 * 2 * peaks["sm_max"] * 1e6 / 1e12
+    # ---- roofline of the dominant stage.  One denominator for the whole line: the burst peak
+    # for a timed region that ran at full clocks (this ~40 ms step loop), the sustained one
+    # when the clock record shows the power-capped regime.
+    reg = regime(clocks, peaks["sm_max"])
+    tf32_pk = peaks["tf32"] if reg == "burst" else peaks["tf32_sus"]
     stage_rows = {}
     for name, (tot_ms, calls) in stages.items():
         if calls == 0:
             continue
         fl, by, bound = STAGE_WORK[name]
         avg = tot_ms / calls
-        stage_rows[name] = {"avg_ms": round(avg, 4), "share": round(tot_ms / max(ms, 1e-9), 4),
-                            "tflops": round(fl * b / (avg * 1e-3) / 1e12, 2),
-                            "gbs": round(by * b / (avg * 1e-3) / 1e9, 1)}
+        tfl = fl * b / (avg * 1e-3) / 1e12
+        gbs = by * b / (avg * 1e-3) / 1e9
+        row = {"avg_ms": round(avg, 4), "share": round(tot_ms / max(ms, 1e-9), 4),
+               "tflops": round(tfl, 2), "gbs": round(gbs, 1), "bound": bound}
+        if bound == "tensor" and math == "tf32":
+            row["frac"] = round(tfl / tf32_pk, 4)
+        elif bound == "tensor":
+            row["bound"] = "alu"
+            row["frac"] = round(tfl / peaks["fp32_alu"], 4)
+        else:
+            row["frac"] = round(gbs / peaks["hbm"], 4)
+        stage_rows[name] = row
     dom = max(stage_rows, key=lambda k: stage_rows[k]["avg_ms"])
     fl, by, bound = STAGE_WORK[dom]
     avg_s = stage_rows[dom]["avg_ms"] * 1e-3
     if bound == "tensor" and math == "tf32":
         achieved = fl * b / avg_s / 1e12
-        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(tf32_sus, 1), "unit": "TFLOP/s",
-                "frac": round(achieved / tf32_sus, 4),
-                "peak_note": "TF32 = measured bf16 sustained x 0.5 (nominal 1.125/2.25 PF)"}
+        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(tf32_pk, 1), "unit": "TFLOP/s",
+                "frac": round(achieved / tf32_pk, 4),
+                "peak_note": f"TF32 {reg} = measured bf16 {reg} x 0.5 (nominal 1.125/2.25 PF); regime from the clock record"}
+        if peaks.get("tf32_cublas"):
+            roof["frac_tf32_cublas"] = round(achieved / peaks["tf32_cublas"], 4)
+        roof["frac_tf32_spec"] = round(achieved / TF32_SPEC_TFLOPS, 4)
     elif bound == "tensor":
         achieved = fl * b / avg_s / 1e12
-        roof = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(fp32_alu, 1), "unit": "TFLOP/s",
-                "frac": round(achieved / fp32_alu, 4), "peak_note": "148 SM x 128 FFMA x 2 x sm_max_mhz"}
+        roof = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(peaks["fp32_alu"], 1), "unit": "TFLOP/s",
+                "frac": round(achieved / peaks["fp32_alu"], 4), "peak_note": "148 SM x 128 FFMA x 2 x sm_max_mhz"}
     else:
         achieved = by * b / avg_s / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm"], "unit": "GB/s",
@@ -450,8 +705,8 @@ def ours_arm(args, world, rank, local):
             traffic = round(t["dram_bytes_per_image"] * b)
     except (OSError, ValueError):
         pass
-    roof.update({"kernel": dom, "traffic": traffic, "algorithmic_bytes": by * b,
-                 "peak_src": peaks["src"]})
+    roof.update({"kernel": dom, "traffic": traffic, "algorithmic_bytes": by * b, "algorithmic_flops": fl * b,
+                 "regime": reg, "peak_src": peaks["src"]})
 
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -474,11 +729,31 @@ def ours_arm(args, world, rank, local):
         "stages": stage_rows,
     }
     if rank == 0 and world == 1 and not args.no_layers:
+        try:
+            peaks["tf32_cublas"] = tf32_cublas_peak()
+        except Exception as ex:  # the measuring stick is optional; the bf16-derived peak stays
+            peaks["tf32_cublas"] = None
+            result["tf32_cublas_error"] = f"{type(ex).__name__}: {ex}"
+        result["peaks"] = {"hbm_gbs": peaks["hbm"], "tf32_burst_tflops": round(peaks["tf32"], 1),
+                           "tf32_sustained_tflops": round(peaks["tf32_sus"], 1),
+                           "tf32_cublas_measured_tflops": peaks["tf32_cublas"],
+                           "tf32_spec_tflops": TF32_SPEC_TFLOPS, "fp32_alu_tflops": round(peaks["fp32_alu"], 1),
+                           "src": peaks["src"]}
+        if peaks["tf32_cublas"]:
+            result["roofline"]["frac_tf32_cublas"] = (round(result["roofline"]["achieved"] / peaks["tf32_cublas"], 4)
+                                                      if result["roofline"]["bound"] == "tensor" else None)
         result["layers"] = layer_section(S, peaks, quick=args.quick)
+        try:
+            for leg_name, leg in config_legs(S, peaks, quick=args.quick).items():
+                result[leg_name] = leg
+        except Exception as ex:  # keep the headline line even if a side leg fails
+            result["config_legs_error"] = f"{type(ex).__name__}: {ex}"
     if rank == 0 and world == 1 and not args.no_cpu:
         v, n, t, cores = cpu_oracle_rate()
         result["cpu_baseline"] = {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+                                  "cpu_model": cpu_model(),
                                   "sample": f"fp64 oracle LeNet fwd+bwd+SGD on {n} images ({t:.1f} s)"}
+        result["oracle_per_config"] = oracle_per_config()
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -498,7 +773,11 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying CUDA graphs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)  # does not return
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     if args.impl == "reference":
         reference_arm(args, world, rank)
         return

@@ -115,6 +115,10 @@ typedef struct {
 /* Library identity / diagnostics ------------------------------------------- */
 SYSML_API const char *sysml_version(void);
 SYSML_API const char *sysml_last_error(void); /* thread-local; never NULL               */
+/* Thread-local route of the last conv2d / conv2d_bias_relu_maxpool / bwd_filter /
+ * bwd_data call on this thread: the main kernels it launched, " + "-separated, with their
+ * operand mode (e.g. "tc_conv_fwd_kernel [tcgen05 TF32, SN, ...]").  Never NULL.        */
+SYSML_API const char *sysml_last_route(void);
 /* Number of SMs of the current device, as the kernels size their grids.      */
 SYSML_API int32_t sysml_device_sm_count(void);
 

@@ -34,7 +34,7 @@ STATUS = {0: "SYSML_OK", 1: "SYSML_ERR_ARG", 2: "SYSML_ERR_SHAPE", 3: "SYSML_ERR
 
 # every symbol include/sysml.h declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "sysml_version", "sysml_last_error", "sysml_device_sm_count", "sysml_launch_counter",
+    "sysml_version", "sysml_last_error", "sysml_last_route", "sysml_device_sm_count", "sysml_launch_counter",
     "sysml_conv2d_workspace_size", "sysml_conv2d",
     "sysml_conv2d_bwd_filter_workspace_size", "sysml_conv2d_bwd_filter",
     "sysml_conv2d_bwd_data_workspace_size", "sysml_conv2d_bwd_data",
@@ -45,7 +45,7 @@ EXPORTS = (
     "sysml_sgd_update", "sysml_lenet_step", "sysml_lenet_step_host",
     "sysml_lenet_set_timing", "sysml_lenet_get_timing",
     "sysml_optimizer_state_floats", "sysml_optimizer_update", "sysml_lenet_step_opt",
-    "sysml_lenet_step_host_pipelined",
+    "sysml_lenet_step_host_pipelined", "sysml_decide_format",
     "sysml_conv2d_csr_filter", "sysml_count_nonzeros", "sysml_dense_to_csr", "sysml_lenet_predict",
 )
 
@@ -152,6 +152,7 @@ def lib(build_if_missing: bool = False):
     sig = {
         "sysml_version": (ctypes.c_char_p, []),
         "sysml_last_error": (ctypes.c_char_p, []),
+        "sysml_last_route": (ctypes.c_char_p, []),
         "sysml_device_sm_count": (c_i32, []),
         "sysml_launch_counter": (c_i64, []),
         "sysml_conv2d_workspace_size": (c_i32, [CD, c_i32, psz]),
@@ -429,6 +430,11 @@ def sysml_optimizer_update(desc, params, grads, state, t=1, stream=None):
                                         _ptr(grads, torch.float32, "grads"), _ptr(state, torch.float32, "state"),
                                         params.numel(), int(t), _stream(stream)))
     return params
+
+
+def sysml_last_route() -> str:
+    """The kernels the last conv call on this thread launched (sysml_last_route)."""
+    return lib().sysml_last_route().decode()
 
 
 def sysml_launch_counter() -> int:

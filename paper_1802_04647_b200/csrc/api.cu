@@ -67,6 +67,7 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
                                const float *bias, float *y, const sysml_pool_desc *pd,
                                float *pout, int32_t *parg, void *ws, size_t ws_bytes,
                                cudaStream_t st) {
+  route_reset();
   ConvGeom g;
   SYSML_TRY(validate_conv(&cd, &g));
   SYSML_TRY(validate_input(&x, g));
@@ -121,6 +122,7 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
   }
   if (x.is_csr) {
     if (csr_fwd_supported(a)) return csr_conv_fwd(a, x.csr, f, bias, y, pap, pout, parg, st);
+    route_note("csr_densify_kernel");
     float *dense = wc.take<float>((size_t)g.N * g.CHW());
     SYSML_WS_FITS(wc);
     SYSML_TRY(csr_densify(x.csr, dense, st));
@@ -132,6 +134,7 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
     return tc_conv_fwd(a, xd, f, bias, y, pap, pout, parg, tws, st);
   }
   if (cd.math == SYSML_MATH_TF32 && !pap && phase_fwd_supported(a)) {
+    route_note("phase split");
     void *pws = wc.take<char>(phase_fwd_ws(a));
     SYSML_WS_FITS(wc);
     return phase_conv_fwd(a, xd, f, bias, y, pws, st);
@@ -140,6 +143,7 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
     float *z = wc.take<float>((size_t)g.N * g.KPQ());
     SYSML_WS_FITS(wc);
     SYSML_TRY(simt_conv_fwd(a, xd, f, bias, z, st));
+    route_note("relu_maxpool_kernel");
     return launch_relu_maxpool(*pap, z, pout, parg, st);
   }
   return simt_conv_fwd(a, xd, f, bias, y, st);
@@ -186,6 +190,7 @@ sysml_status conv_bwd_filter_ws(const sysml_conv_desc &cd, int is_csr, size_t *b
 sysml_status conv_bwd_filter_dispatch(const sysml_conv_desc &cd, const sysml_input &x,
                                       const float *dy, float *df, float *db, void *ws,
                                       size_t ws_bytes, cudaStream_t st) {
+  route_reset();
   ConvGeom g;
   SYSML_TRY(validate_conv(&cd, &g));
   SYSML_TRY(validate_input(&x, g));
@@ -209,6 +214,8 @@ sysml_status conv_bwd_filter_dispatch(const sysml_conv_desc &cd, const sysml_inp
     xd = dense;
   }
   const WgRoute route = wgrad_route(cd, a);
+  if (route == WgRoute::PHASE) route_note("phase split");
+  if (route == WgRoute::IM2COL) route_note("im2col_kernel");
   size_t route_ws = 0;
   switch (route) {
     case WgRoute::TC: route_ws = tc_bwd_filter_ws(a); break;
@@ -218,7 +225,10 @@ sysml_status conv_bwd_filter_dispatch(const sysml_conv_desc &cd, const sysml_inp
   }
   void *rws = wc.take<char>(route_ws);
   SYSML_WS_FITS(wc);
-  if (x.is_csr) SYSML_TRY(csr_densify(x.csr, const_cast<float *>(xd), st));
+  if (x.is_csr) {
+    route_note("csr_densify_kernel");
+    SYSML_TRY(csr_densify(x.csr, const_cast<float *>(xd), st));
+  }
   switch (route) {
     case WgRoute::TC: return tc_conv_bwd_filter(a, xd, dy, df, db, rws, st);
     case WgRoute::PHASE: return phase_conv_bwd_filter(a, xd, dy, df, db, rws, st);
@@ -242,6 +252,7 @@ sysml_status conv_bwd_data_ws(const sysml_conv_desc &cd, size_t *bytes) {
 
 sysml_status conv_bwd_data_dispatch(const sysml_conv_desc &cd, const float *f, const float *dy,
                                     float *dx, void *ws, size_t ws_bytes, cudaStream_t st) {
+  route_reset();
   ConvGeom g;
   SYSML_TRY(validate_conv(&cd, &g));
   SYSML_CHECK_ARG(f && dy && dx, "f/dy/dx pointer is NULL");
@@ -258,9 +269,14 @@ sysml_status conv_bwd_data_dispatch(const sysml_conv_desc &cd, const float *f, c
   }
   if (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a))
     return tc_conv_bwd_data(a, f, dy, dx, ws, st);
-  if (cd.math == SYSML_MATH_TF32 && phase_bwd_data_supported(a))
+  if (cd.math == SYSML_MATH_TF32 && phase_bwd_data_supported(a)) {
+    route_note("phase split");
     return phase_conv_bwd_data(a, f, dy, dx, ws, st);
-  if (phase_simt_bwd_data_supported(a)) return phase_simt_conv_bwd_data(a, f, dy, dx, ws, st);
+  }
+  if (phase_simt_bwd_data_supported(a)) {
+    route_note("phase split");
+    return phase_simt_conv_bwd_data(a, f, dy, dx, ws, st);
+  }
   return simt_conv_bwd_data(a, f, dy, dx, st);
 }
 
@@ -272,6 +288,7 @@ extern "C" {
 
 const char *sysml_version(void) { return "sysml-b200 0.1 (sm_100a; tcgen05 TF32 + fp32 SIMT + CSR)"; }
 const char *sysml_last_error(void) { return get_error(); }
+const char *sysml_last_route(void) { return route_get(); }
 int32_t sysml_device_sm_count(void) { return sm_count(); }
 int64_t sysml_launch_counter(void) { return g_launches; }
 

@@ -1,5 +1,6 @@
 // common.cu -- error reporting, device queries and descriptor validation.
 #include <stdarg.h>
+#include <string.h>
 
 #include <map>
 #include <mutex>
@@ -20,6 +21,25 @@ void set_error(const char *fmt, ...) {
 }
 
 const char *get_error() { return g_err; }
+
+static thread_local char g_route[512] = "";
+
+void route_reset() { g_route[0] = 0; }
+
+void route_note(const char *fmt, ...) {
+  size_t len = strlen(g_route);
+  if (len + 4 >= sizeof(g_route)) return;
+  if (len) {
+    strcpy(g_route + len, " + ");
+    len += 3;
+  }
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_route + len, sizeof(g_route) - len, fmt, ap);
+  va_end(ap);
+}
+
+const char *route_get() { return g_route; }
 
 static int query_attr(cudaDeviceAttr a) {
   int dev = 0, v = 0;

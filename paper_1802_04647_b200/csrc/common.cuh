@@ -12,6 +12,12 @@
 
 namespace sysml {
 
+// Thread-local route log (sysml_last_route): the main kernels the last dispatch launched,
+// so a bench line or test can report which implementation an op took.
+void route_reset();
+void route_note(const char *fmt, ...) __attribute__((format(printf, 1, 2)));
+const char *route_get();
+
 // Thread-local last error message (sysml_last_error).
 void set_error(const char *fmt, ...) __attribute__((format(printf, 1, 2)));
 const char *get_error();

@@ -456,6 +456,7 @@ sysml_status conv1_pool(const ConvArgs &a, const PoolArgs *pool, const float *x,
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  route_note("conv1_pool_kernel [tcgen05 TF32 pool-in-N%s]", p.is_csr ? ", CSR producer" : "");
   SYSML_CUDA(cudaLaunchKernelEx(&cfg, conv1_pool_kernel, p));
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;

@@ -252,6 +252,7 @@ sysml_status simt_conv_fwd(const ConvArgs &a, const float *x, const float *f, co
   FwdOp op{a, x, f, bias, y};
   const int64_t ng = (int64_t)a.N * a.P * a.Q;
   dim3 grid((unsigned)ceil_div(ng, BN), (unsigned)ceil_div(a.K, BM), 1);
+  route_note("igemm_kernel<Fwd> (FP32 SIMT)");
   igemm_kernel<FwdOp><<<grid, NT, 0, st>>>(op, a.C * a.R * a.S);
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;
@@ -262,6 +263,7 @@ sysml_status simt_conv_bwd_data(const ConvArgs &a, const float *f, const float *
   BwdDataOp op{a, f, dy, dx};
   const int64_t ng = (int64_t)a.N * a.H * a.W;
   dim3 grid((unsigned)ceil_div(ng, BN), (unsigned)ceil_div(a.C, BM), 1);
+  route_note("igemm_kernel<BwdData> (FP32 SIMT)");
   igemm_kernel<BwdDataOp><<<grid, NT, 0, st>>>(op, a.K * a.R * a.S);
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;
@@ -302,6 +304,7 @@ sysml_status simt_conv_bwd_filter(const ConvArgs &a, const float *x, const float
   BwdFilterOp op{a, x, dy, used_splits == 1 ? df : part};
   dim3 grid((unsigned)ceil_div((int64_t)a.C * a.R * a.S, BN), (unsigned)ceil_div(a.K, BM),
             (unsigned)used_splits);
+  route_note("igemm_kernel<BwdFilter> (FP32 SIMT, %d splits)", used_splits);
   igemm_kernel<BwdFilterOp><<<grid, NT, 0, st>>>(op, k_per_split);
   SYSML_LAUNCH_CHECK();
   if (used_splits > 1) {

@@ -1427,6 +1427,9 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
+    route_note("tc_conv_fwd_kernel%s [tcgen05 TF32, %s%s, MT=%d, N=%d, %d tiles on %d CTAs%s]", ph ? "<phase>" : "",
+               p.ks ? "KS" : p.sn ? "SN" : "standard", p.is_csr ? " CSR" : "", p.MT, p.NN, (int)p.ntiles, grid,
+               p.pool ? ", pool epilogue" : "");
     SYSML_CUDA(cudaLaunchKernelEx(&cfg, ph ? tc_conv_fwd_kernel<true> : tc_conv_fwd_kernel<false>, p));
   }
   SYSML_LAUNCH_CHECK();
@@ -2310,9 +2313,11 @@ sysml_status tc_wgrad_spf(const SpfConv &sc, const float *x_spf, const float *dy
   }
   if (p.S == 5) {
       SYSML_TRY(smem_attr(tc_wgrad_spf_kernel<5>, pl.smem));
+    route_note("tc_wgrad_spf_kernel<5> [tcgen05 TF32, %d splits]", p.splits);
     tc_wgrad_spf_kernel<5><<<p.splits, WG_THREADS, pl.smem, st>>>(p);
   } else {
       SYSML_TRY(smem_attr(tc_wgrad_spf_kernel<3>, pl.smem));
+    route_note("tc_wgrad_spf_kernel<3> [tcgen05 TF32, %d splits]", p.splits);
     tc_wgrad_spf_kernel<3><<<p.splits, WG_THREADS, pl.smem, st>>>(p);
   }
   SYSML_LAUNCH_CHECK();
@@ -2389,6 +2394,7 @@ sysml_status tc_conv_bwd_filter(const ConvArgs &a, const float *x, const float *
     }
     float *xs = reinterpret_cast<float *>(ws);
     const int64_t total = (int64_t)a.N * a.C * a.P * a.Q;
+    route_note("subsample_kernel");
     subsample_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 16 * sm_count()), 256, 0, st>>>(
         x, xs, (int64_t)a.N * a.C, a.H, a.W, a.P, a.Q, a.sh, a.sw);
     SYSML_LAUNCH_CHECK();
@@ -2408,6 +2414,7 @@ sysml_status tc_conv_bwd_filter(const ConvArgs &a, const float *x, const float *
   p.part = reinterpret_cast<float *>(ws);
   p.dbpart = db ? reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + pl.part_bytes) : nullptr;
   SYSML_TRY(smem_attr(tc_conv_wgrad_kernel, pl.smem));
+  route_note("tc_conv_wgrad_kernel [tcgen05 TF32, %d CTAs]", p.splits * p.nwt);
   tc_conv_wgrad_kernel<<<p.splits * p.nwt, TC_THREADS, pl.smem, st>>>(p);
   SYSML_LAUNCH_CHECK();
   const int64_t total = (int64_t)a.K * a.C * a.R * a.S;

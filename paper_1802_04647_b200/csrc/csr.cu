@@ -516,9 +516,11 @@ sysml_status csr_conv_fwd(const ConvArgs &a, const sysml_csr &x, const float *f,
   int blocks = a.N < 8 * sm_count() ? a.N : 8 * sm_count();
   if (pool) {
     SYSML_TRY(smem_attr(csr_fwd_pool_kernel, 96 * 1024));
+    route_note("csr_fwd_pool_kernel (FP32)");
     csr_fwd_pool_kernel<<<blocks, CSR_THREADS, smem, st>>>(a, *pool, x, f, bias, pout, parg);
   } else {
     SYSML_TRY(smem_attr(csr_fwd_kernel, 96 * 1024));
+    route_note("csr_fwd_kernel (FP32)");
     csr_fwd_kernel<<<blocks, CSR_THREADS, smem, st>>>(a, x, f, bias, y);
   }
   SYSML_LAUNCH_CHECK();
@@ -561,6 +563,7 @@ sysml_status csr_conv_bwd_filter(const ConvArgs &a, const sysml_csr &x, const fl
     SYSML_WS_FITS(wc);
     auto kern = (a.R == 5) ? csr_wgrad_k32_kernel<5, 5> : csr_wgrad_k32_kernel<3, 3>;
     SYSML_TRY(smem_attr(kern, smem));
+    route_note("csr_wgrad_k32_kernel<%d,%d> (FP32, %d CTAs)", a.R, a.S, blocks);
     kern<<<blocks, WG_THREADS, smem, st>>>(g, x, dy, part, db ? dbpart : nullptr);
     SYSML_LAUNCH_CHECK();
     ordered_sum_kernel<<<(unsigned)ceil_div(kcrs, 256), 256, 0, st>>>(part, blocks, kcrs, df);
@@ -581,6 +584,7 @@ sysml_status csr_conv_bwd_filter(const ConvArgs &a, const sysml_csr &x, const fl
   SYSML_WS_FITS(wc);
   const size_t smem = bwf_smem(a);
   SYSML_TRY(smem_attr(csr_bwd_filter_kernel, 200 * 1024));
+  route_note("csr_bwd_filter_kernel (FP32, %d CTAs)", used);
   csr_bwd_filter_kernel<<<used, CSR_THREADS, smem, st>>>(a, x, dy, npb, part, db ? dbpart : nullptr);
   SYSML_LAUNCH_CHECK();
   ordered_sum_kernel<<<(unsigned)ceil_div(kcrs, 256), 256, 0, st>>>(part, used, kcrs, df);

@@ -317,6 +317,7 @@ sysml_status tc_wgrad_1x1(const ConvArgs &a, const float *x, const float *dy, fl
       return SYSML_ERR_CUDA;
   }
   SYSML_TRY(smem_attr(tc_wgrad_1x1_kernel, pl.smem));
+  route_note("tc_wgrad_1x1_kernel [TMA + tcgen05 TF32, %d CTAs]", pl.grid);
   tc_wgrad_1x1_kernel<<<pl.grid, W1_THREADS, pl.smem, st>>>(tmA, tmB, p);
   SYSML_LAUNCH_CHECK();
   const int64_t total = (int64_t)a.K * a.C;

@@ -553,6 +553,7 @@ sysml_status tc_wgrad_spf_tma(const SpfConv &sc, const float *x_spf, const float
     cudaMemsetAsync(dclk, 0, sizeof(long long) * 8 * 4096, st);
     p.clk = dclk;
   }
+  route_note("tc_wgrad_spf_tma_kernel<%d> [TMA + tcgen05 TF32, %d CTAs]", p.shift, pl.grid);
   kern<<<pl.grid, W2_THREADS, pl.smem, st>>>(tmDy, tmX, p);
   SYSML_LAUNCH_CHECK();
   if (prof) {
