@@ -102,7 +102,11 @@ struct TcFwdParams {
   int ks;              // C == 1: the S column taps fill the MMA K slots (s = 4*half + e)
   int sn;              // narrow filter banks: the S column taps fold into N (D'[pos][(s,k)]),
                        // the epilogue adds Y[pos][k] = sum_s D'[pos + s][(s,k)]
-  int NN;              // MMA N: NFpad, or S*NFpad in SN mode
+  int snt;             // SN: taps s < snt in N (MMA 1, A unshifted); taps s = snt .. S-1 come
+                       // from MMA 2 with A shifted by snt positions, accumulated into columns
+                       // (s - snt, k).  snt == S: one MMA; snt < S: the accumulator is snt*NFpad
+                       // wide, so two tiles fit TMEM and the epilogue overlaps the MMAs
+  int NN;              // accumulator width per M-tile: NFpad, or snt*NFpad in SN mode
   int is_csr;          // KS mode only: input rows are CSR (scattered straight into the operand)
   sysml_csr csr;
   int64_t in_plane;    // > 0: input is SPF [C][in_plane], stored position = frame pos + in_shift
@@ -368,10 +372,9 @@ __device__ __forceinline__ void epi_pool2(const TcFwdParams &p, uint32_t tbase, 
 constexpr int SN_MAXMT = 4;
 constexpr int SN_XCH_FLOATS = 2 * SN_MAXMT * 4 * 8 * 4 * 16;  // [set][M-tile][warp][s][row < S-1 <= 4][16]
 
-// SN epilogue (column taps in N, single-buffered MT M-tiles): accumulator row
-// l = i*128 + qd*32 + lane holds D'[g0 + l][(s, k)]; output
-// Y[g0 + l][k] = b[k] + sum_s D'[g0 + l + s][(s, k)] for l < cta_pos = MT*128 - (S-1)
-// (CTA tiles overlap by S-1 rows).  Rows l + s of the same warp come by shfl_down; the
+// SN epilogue (column taps in N): accumulator row l = i*128 + qd*32 + lane holds
+// D'[g0 + l][(s', k)], s' < T = snt; output Y[g0 + l][k] = b[k] + sum_s' D'[g0 + l + s'][(s', k)]
+// for l < cta_pos = MT*128 - (T-1) (CTA tiles overlap by T-1 rows).  Rows l + s of the same warp come by shfl_down; the
 // first S-1 rows of the next 32-row group (next quadrant, or quadrant 0 of the next
 // M-tile) are dumped to shared memory first.  The two warp sets split the 16-channel
 // chunks.
@@ -386,10 +389,10 @@ __device__ __forceinline__ void epi_sn(const TcFwdParams &p, uint32_t tbase, int
   for (int c16 = eset; c16 < nc16; c16 += 2) {
     // 1) dump the first S-1 rows of every 32-row group for s >= 1
     for (int i = 0; i < p.MT; ++i)
-      for (int s_ = 1; s_ < p.S; ++s_) {
+      for (int s_ = 1; s_ < p.snt; ++s_) {
         float t[16];
         ptx::tmem_ld16(tbase + (uint32_t)(i * p.NN + s_ * p.NFpad + c16 * 16), t);
-        if (lane < p.S - 1) {
+        if (lane < p.snt - 1) {
           float *dst = xch + xidx(i, qd, s_, lane);
 #pragma unroll
           for (int j = 0; j < 16; ++j) dst[j] = t[j];
@@ -405,7 +408,7 @@ __device__ __forceinline__ void epi_sn(const TcFwdParams &p, uint32_t tbase, int
       const int ni = qd == 3 ? i + 1 : i, nq = (qd + 1) & 3;  // next 32-row group
       float acc[16];
       ptx::tmem_ld16(tbase + (uint32_t)(i * p.NN + c16 * 16), acc);
-      for (int s_ = 1; s_ < p.S; ++s_) {
+      for (int s_ = 1; s_ < p.snt; ++s_) {
         float t[16];
         ptx::tmem_ld16(tbase + (uint32_t)(i * p.NN + s_ * p.NFpad + c16 * 16), t);
         const bool from_next = lane + s_ >= 32;
@@ -934,6 +937,29 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
           uint64_t bdesc = ptx::make_desc(A + p.a_bytes, nf * 16, 128);
           uint32_t acc = ch != c0 ? 1u : 0u;
           uint32_t drow = 0;
+          if (p.sn && p.snt < p.S) {
+            // SN-T: per tap row, MMA 1 (taps s < T, N = T*NF, A unshifted) then MMA 2 (taps
+            // s >= T, N = (S-T)*NF, A shifted by T positions) into the same accumulator columns
+            const uint32_t n1 = (uint32_t)(p.snt * p.NFpad), n2 = (uint32_t)((p.S - p.snt) * p.NFpad);
+            const uint32_t idesc2 = ptx::make_idesc_tf32(128, (int)n2);
+            const uint32_t bsrow = A + p.a_bytes;
+            for (int r = 0; r < p.R; ++r, drow += (uint32_t)p.Wf) {
+              const uint32_t br = bsrow + (uint32_t)r * 2u * (n1 + n2) * 16u;
+              const uint64_t bd1 = ptx::make_desc(br, n1 * 16, 128);
+              const uint64_t bd2 = ptx::make_desc(br + 2u * n1 * 16u, n2 * 16, 128);
+              uint64_t ad = adesc0 + (uint64_t)drow;
+              uint32_t tm = buf * p.tbuf;
+              for (int i = 0; i < p.MT; ++i) {
+                if (ptx::elect_one()) ptx::mma_tf32(tm, ad, bd1, idesc, acc);
+                __syncwarp();
+                if (ptx::elect_one()) ptx::mma_tf32(tm, ad + (uint64_t)p.snt, bd2, idesc2, 1u);
+                __syncwarp();
+                tm += nf;
+                ad += (uint64_t)jump_outer;  // next M-tile: 128 positions (linear tiles)
+              }
+              acc = 1u;
+            }
+          } else {
           // KS: all S column taps are in the K slots; SN: in the N columns
           const int s_taps = (p.ks || p.sn) ? 1 : p.S;
           for (int r = 0; r < p.R; ++r, drow += (uint32_t)p.Wf) {
@@ -951,6 +977,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
               acc = 1u;
               bdesc += (uint64_t)(2 * nf);  // next tap: 2 quads x NFpad x 16 B
             }
+          }
           }
           if (ptx::elect_one()) {
             if (p.cl2) ptx::mma_commit_mc(empty + stage, 0x3);  // frees the stage in both CTAs
@@ -1097,23 +1124,26 @@ __global__ void tc_pack_filters_elem_kernel(const float *__restrict__ f, float *
   }
 }
 
-// SN packing: [chunk][r][quad][S*NFpad][4] with column n = s*NFpad + j:
+// SN packing: per (chunk, r) the taps s < T as [quad][T*NFpad][4] (column n = s*NFpad + j,
+// MMA 1), then the taps s >= T as [quad][(S-T)*NFpad][4] (column n = (s-T)*NFpad + j, MMA 2):
 //  packed(j, c, r, s) = F[j][c][r][s] (flip 0) or F[c][j][R-1-r][S-1-s] (flip 1, bwd_data)
 __global__ void tc_pack_filters_sn_kernel(const float *__restrict__ f, float *__restrict__ fp,
                                           int Kout, int Cin, int R, int S, int NFpad, int nchunk,
-                                          int flip) {
+                                          int flip, int T) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int NN = S * NFpad;
+  const int NN = S * NFpad, N1 = T * NFpad;
   const int64_t total = (int64_t)nchunk * R * 2 * NN * 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = i;
     const int e = (int)(t % 4); t /= 4;
-    const int n = (int)(t % NN); t /= NN;
-    const int g = (int)(t % 2); t /= 2;
+    int w = (int)(t % (2 * NN)); t /= 2 * NN;   // position inside the (chunk, r) block
     const int r = (int)(t % R); t /= R;
     const int ch = (int)t;
-    const int s_ = n / NFpad, j = n - s_ * NFpad, c = ch * 8 + g * 4 + e;
+    int g, n, s0;
+    if (w < 2 * N1) { g = w / N1; n = w - g * N1; s0 = 0; }                       // MMA 1 block
+    else { w -= 2 * N1; g = w / (NN - N1); n = w - g * (NN - N1); s0 = T; }       // MMA 2 block
+    const int s_ = s0 + n / NFpad, j = n % NFpad, c = ch * 8 + g * 4 + e;
     float v = 0.f;
     if (j < Kout && c < Cin)
       v = flip ? f[(((int64_t)c * Kout + j) * R + (R - 1 - r)) * S + (S - 1 - s_)]
@@ -1194,12 +1224,23 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   p.sn = (sn_env != 0 && !p.ks && !pool && p.nft == 1 && S >= 2 && S <= 5 && p.NFpad <= sn_max &&
           S * p.NFpad <= 256 && p.NFpad % 16 == 0)
              ? 1 : 0;
-  p.NN = p.sn ? S * p.NFpad : p.NFpad;
+  // SN-T (default): at most 96 accumulator columns per M-tile, so two tiles of 2+ M-tiles fit
+  // TMEM and the epilogue of one tile overlaps the MMAs of the next (B2d profile r02: the MMA
+  // warp waited 37% of the kernel on the single-buffered 480-column SN accumulator).
+  // SYSML_TC_SNT=0 restores all taps in N (single buffer); SYSML_TC_SNT=t forces t.
+  static const int snt_env = getenv("SYSML_TC_SNT") ? atoi(getenv("SYSML_TC_SNT")) : -1;
+  p.snt = S;
+  if (p.sn) {
+    if (snt_env < 0) p.snt = std::min(S, std::max(3, 96 / p.NFpad));
+    else if (snt_env >= 3) p.snt = std::min(S, snt_env);  // T = 2 (MT = 4) is not supported
+  }
+  p.NN = p.sn ? p.snt * p.NFpad : p.NFpad;
   p.nchunk = p.ks ? 1 : (C + 7) / 8;
   const int RS = R * S;
   const int b_taps = (p.ks || p.sn) ? R : RS;
-  const int s_halo = (p.ks || p.sn) ? 0 : S - 1;  // KS / SN: the S window is in K / N
-  p.b_bytes = (uint32_t)(b_taps * 2 * p.NN * 16);
+  // KS / SN: the S window is in K / N (SN-T: MMA 2 reads A shifted by snt positions)
+  const int s_halo = p.ks ? 0 : p.sn ? S - p.snt : S - 1;
+  p.b_bytes = (uint32_t)(b_taps * 2 * (p.sn ? S * p.NFpad : p.NN) * 16);
   const int nsm = sm_count();
   const int64_t rows_total = (int64_t)N * p.Hs;
   // TMEM double buffer (epilogue overlaps the next tile's MMAs) unless B-heavy wide
@@ -1210,9 +1251,11 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   // 256-wide filter tiles: either a CTA pair sharing every filter chunk by multicast
   // (double-buffered accumulators, MT = 1) or two M-tiles per CTA sharing it (single buffer)
   p.cl2 = (cluster_env == 1) && p.NFpad == 256 && p.nft == 1 && !pool && !p.ks ? 1 : 0;
-  const bool single = (!p.cl2 && (single_env < 0 || single_env == 1) && p.NFpad == 256 && !pool) || p.sn;
+  const bool single = (!p.cl2 && (single_env < 0 || single_env == 1) && p.NFpad == 256 && !pool) ||
+                      (p.sn && p.snt == S);
   p.tbuf = single ? 0u : TMEM_BUF;
-  int mt_cap = p.sn ? std::min(SN_MAXMT, 512 / p.NN) : std::min(16, (single ? 512 : (int)TMEM_BUF) / p.NFpad);
+  int mt_cap = p.sn ? std::min(SN_MAXMT, (single ? 512 : (int)TMEM_BUF) / p.NN)
+                    : std::min(16, (single ? 512 : (int)TMEM_BUF) / p.NFpad);
   static const int mtcap_env = getenv("SYSML_TC_MTCAP") ? atoi(getenv("SYSML_TC_MTCAP")) : 0;
   if (mtcap_env > 0) mt_cap = std::min(mt_cap, mtcap_env);
   p.CT = (p.Q + 7) / 8;
@@ -1230,8 +1273,8 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
         halo = round_up(halo, 8);  // LBO multiple of 128 B
         ntiles = ceil_div(rows_total, (int64_t)bb * 16) * p.nft;
       } else {
-        // SN: tiles overlap by S-1 rows (output row l needs accumulator rows l .. l+S-1)
-        cta_pos = p.sn ? (int64_t)mt * 128 - (S - 1) : (int64_t)mt * 128;
+        // SN: tiles overlap by T-1 rows (output row l needs accumulator rows l .. l+T-1)
+        cta_pos = p.sn ? (int64_t)mt * 128 - (p.snt - 1) : (int64_t)mt * 128;
         halo = round_up(mt * 128 + (R - 1) * p.Wf + s_halo, 8);  // LBO multiple of 128 B
         ntiles = ceil_div(p.G, cta_pos) * p.nft;
       }
@@ -1262,7 +1305,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   if (p.tile2d && (uint32_t)p.Wf * 16 >= (1u << 18)) { pl.ok = false; return pl; }
   if (p.MT * p.NN > (p.tbuf ? (int)p.tbuf : 512)) { pl.ok = false; return pl; }
   p.tmem_cols = 512;  // whole TMEM: base column 0 (1 CTA per SM), issue loops address from 0
-  pl.fp_bytes = align_up((size_t)p.nft * p.nchunk * b_taps * 8 * p.NN * sizeof(float), 256);
+  pl.fp_bytes = align_up((size_t)p.nft * p.nchunk * b_taps * 8 * (p.sn ? S * p.NFpad : p.NN) * sizeof(float), 256);
   return pl;
 }
 
@@ -1340,9 +1383,9 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     tc_pack_filters_ks_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, p.R, p.S, p.NFpad, p.nft);
     SYSML_LAUNCH_CHECK();
   } else if (p.sn) {
-    const int64_t total = (int64_t)p.nchunk * p.R * 2 * p.NN * 4;
+    const int64_t total = (int64_t)p.nchunk * p.R * 2 * p.S * p.NFpad * 4;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 8 * sm_count());
-    tc_pack_filters_sn_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, f_cin, p.R, p.S, p.NFpad, p.nchunk, flip);
+    tc_pack_filters_sn_kernel<<<blocks, 256, 0, st>>>(f, fp, p.K, f_cin, p.R, p.S, p.NFpad, p.nchunk, flip, p.snt);
     SYSML_LAUNCH_CHECK();
   } else {
     const int RS = p.R * p.S;
@@ -1428,7 +1471,7 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     cfg.attrs = at;
     cfg.numAttrs = na;
     route_note("tc_conv_fwd_kernel%s [tcgen05 TF32, %s%s, MT=%d, N=%d, %d tiles on %d CTAs%s]", ph ? "<phase>" : "",
-               p.ks ? "KS" : p.sn ? "SN" : "standard", p.is_csr ? " CSR" : "", p.MT, p.NN, (int)p.ntiles, grid,
+               p.ks ? "KS" : p.sn ? (p.snt < p.S ? "SN-T" : "SN") : "standard", p.is_csr ? " CSR" : "", p.MT, p.NN, (int)p.ntiles, grid,
                p.pool ? ", pool epilogue" : "");
     SYSML_CUDA(cudaLaunchKernelEx(&cfg, ph ? tc_conv_fwd_kernel<true> : tc_conv_fwd_kernel<false>, p));
   }
