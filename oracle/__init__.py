@@ -64,6 +64,17 @@ def lib():
         _lib.oracle_conv2d_fwd_csr_filter.argtypes = [i64] * 11 + [dp, ip, ip, dp, dp, dp]
         _lib.oracle_count_nonzeros.restype = i64
         _lib.oracle_count_nonzeros.argtypes = [i64, dp]
+        u64, u8p = ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint8)
+        _lib.oracle_philox_raw.argtypes = [u64, u64, i64, i64, ctypes.POINTER(ctypes.c_uint64)]
+        _lib.oracle_dropout_mask.argtypes = [u64, u64, i64, i64, i64, ctypes.c_double, u8p]
+        _lib.oracle_dropout_fwd.argtypes = [i64, dp, u8p, ctypes.c_double, dp]
+        _lib.oracle_dropout_bwd.argtypes = [i64, dp, u8p, ctypes.c_double, dp]
+        _lib.oracle_lenet512_num_params.restype = i64
+        _lib.oracle_lenet512_forward.argtypes = [i64, i64, dp, dp, i64, u64, u64, ctypes.c_double,
+                                                 dp, ip, dp, ip, dp, dp, u8p, dp]
+        _lib.oracle_lenet512_fwd_bwd.argtypes = [i64, i64, i64, dp, ip, dp, u64, u64, ctypes.c_double,
+                                                 dp, dp]
+        _lib.oracle_lenet512_predict.argtypes = [i64, dp, dp, ip, dp]
     return _lib
 
 
@@ -80,6 +91,10 @@ def _p(a):
         return None
     if a.dtype == np.int32:
         return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    if a.dtype == np.uint8:
+        return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+    if a.dtype == np.uint64:
+        return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
@@ -230,3 +245,81 @@ def sgd_update(params, grads, lr=0.01):
     g = _d(grads)
     lib().oracle_sgd_update(p.size, _p(p), _p(g), float(lr))
     return p
+
+
+# ---- NEXT-4: LeNet-512 + inverted dropout (oracle.c; R22-R24) ----------------
+
+LENET512_HIDDEN = 512
+
+
+def philox_raw(key0, key1, start, n):
+    """Raw 64-bit outputs start..start+n-1 of Philox4x64-10 with key (key0, key1), in
+    numpy.random.Philox's output order (oracle_philox_raw)."""
+    out = np.empty(n, dtype=np.uint64)
+    lib().oracle_philox_raw(int(key0), int(key1), int(start), int(n), _p(out))
+    return out
+
+
+def dropout_mask(seed, step, row0, rows, units, keep_p):
+    """uint8 [rows x units] keep mask of global rows row0.. (reading R23)."""
+    m = np.empty((rows, units), dtype=np.uint8)
+    lib().oracle_dropout_mask(int(seed), int(step), int(row0), int(rows), int(units), float(keep_p), _p(m))
+    return m
+
+
+def dropout_fwd(x, mask, keep_p):
+    x = _d(x)
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    assert m.size == x.size
+    out = np.empty_like(x)
+    lib().oracle_dropout_fwd(x.size, _p(x), _p(m), float(keep_p), _p(out))
+    return out
+
+
+def dropout_bwd(dout, mask, keep_p):
+    d = _d(dout)
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    assert m.size == d.size
+    dx = np.empty_like(d)
+    lib().oracle_dropout_bwd(d.size, _p(d), _p(m), float(keep_p), _p(dx))
+    return dx
+
+
+def lenet512_num_params() -> int:
+    return int(lib().oracle_lenet512_num_params())
+
+
+def lenet512_forward(x, params, train=False, seed=0, step=0, keep_p=1.0, row0=0):
+    n = x.shape[0]
+    x, prm = _d(x), _d(params)
+    H = LENET512_HIDDEN
+    a1 = np.empty((n, 6272)); i1 = np.empty((n, 6272), dtype=np.int32)
+    a2 = np.empty((n, 3136)); i2 = np.empty((n, 3136), dtype=np.int32)
+    z3 = np.empty((n, H)); h = np.empty((n, H)); mask = np.empty((n, H), dtype=np.uint8)
+    sc = np.empty((n, 10))
+    lib().oracle_lenet512_forward(n, int(row0), _p(x), _p(prm), int(bool(train)), int(seed), int(step),
+                                  float(keep_p), _p(a1), _p(i1), _p(a2), _p(i2), _p(z3), _p(h), _p(mask),
+                                  _p(sc))
+    return dict(a1=a1, i1=i1, a2=a2, i2=i2, z3=z3, h=h, mask=mask, scores=sc)
+
+
+def lenet512_fwd_bwd(x, labels, params, seed, step, keep_p, n_global=None, row0=0):
+    """Returns (grads float64[1663370] pre-scaled by 1/n_global, loss_sum)."""
+    n = x.shape[0]
+    n_global = n if n_global is None else n_global
+    x, lab, prm = _d(x), _i(labels), _d(params)
+    g = np.empty(prm.size, dtype=np.float64)
+    loss = ctypes.c_double(0.0)
+    lib().oracle_lenet512_fwd_bwd(n, int(n_global), int(row0), _p(x), _p(lab), _p(prm), int(seed), int(step),
+                                  float(keep_p), _p(g),
+                                  ctypes.cast(ctypes.pointer(loss), ctypes.POINTER(ctypes.c_double)))
+    return g, loss.value
+
+
+def lenet512_predict(x, params):
+    n = x.shape[0]
+    x, prm = _d(x), _d(params)
+    pred = np.empty(n, dtype=np.int32)
+    probs = np.empty((n, 10), dtype=np.float64)
+    lib().oracle_lenet512_predict(n, _p(x), _p(prm), _p(pred), _p(probs))
+    return pred, probs

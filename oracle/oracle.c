@@ -456,3 +456,241 @@ EXPORT int64_t oracle_count_nonzeros(int64_t n, const double *a) {
   for (int64_t i = 0; i < n; ++i) nnz += a[i] != 0.0;
   return nnz;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4: the SystemML LeNet with a 512-unit hidden affine layer and dropout
+ * ("20+ pre-implemented layers"; S:275-281 dropout; SURVEY §8(f) NEXT-4;
+ * DESIGN.md readings R22-R24).
+ *
+ * Dropout's random numbers come from a counter-based generator so that the GPU and this
+ * oracle draw the same mask without sharing code (R23): Philox4x64-10 (Salmon et al.,
+ * SC'11), the generator numpy exposes as numpy.random.Philox, in numpy's output order:
+ * raw 64-bit output e of key (k0, k1) is word e % 4 of the block for counter value
+ * (e / 4 + 1, 0, 0, 0).  (numpy increments the counter before each block.)           */
+static inline void philox_mulhilo(uint64_t a, uint64_t b, uint64_t *hi, uint64_t *lo) {
+  const unsigned __int128 p = (unsigned __int128)a * b;
+  *hi = (uint64_t)(p >> 64);
+  *lo = (uint64_t)p;
+}
+
+static void philox4x64_10(const uint64_t ctr_in[4], uint64_t k0, uint64_t k1, uint64_t out[4]) {
+  uint64_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+  for (int round = 0; round < 10; ++round) {
+    if (round > 0) { /* key schedule: Weyl sequence bump between rounds */
+      k0 += 0x9E3779B97F4A7C15ULL;
+      k1 += 0xBB67AE8584CAA73BULL;
+    }
+    uint64_t hi0, lo0, hi1, lo1;
+    philox_mulhilo(0xD2E7470EE14C6C93ULL, c0, &hi0, &lo0);
+    philox_mulhilo(0xCA5A826395121157ULL, c2, &hi1, &lo1);
+    const uint64_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* raw outputs e = start .. start + n - 1 of the stream with key (k0, k1) */
+EXPORT void oracle_philox_raw(uint64_t k0, uint64_t k1, int64_t start, int64_t n, uint64_t *out) {
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t e = (uint64_t)(start + i);
+    const uint64_t ctr[4] = {e / 4 + 1, 0, 0, 0};
+    uint64_t w[4];
+    philox4x64_10(ctr, k0, k1, w);
+    out[i] = w[e % 4];
+  }
+}
+
+/* Dropout keep mask ("Bernoulli(keep_p) mask from the seeded generator"; R23):
+ * unit j of global sample row g, step t: e = g * units + j, key = (seed, t);
+ * kept  <=>  (raw_e >> 32) < floor(keep_p * 2^32)   (keep_p in (0, 1]; keep_p = 1 keeps all). */
+static inline uint64_t keep_threshold(double keep_p) { return (uint64_t)floor(keep_p * 4294967296.0); }
+
+EXPORT void oracle_dropout_mask(uint64_t seed, uint64_t step, int64_t row0, int64_t rows, int64_t units,
+                                double keep_p, uint8_t *mask) {
+  const uint64_t T = keep_threshold(keep_p);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t j = 0; j < units; ++j) {
+      uint64_t raw;
+      oracle_philox_raw(seed, step, (row0 + i) * units + j, 1, &raw);
+      mask[i * units + j] = (raw >> 32) < T ? 1 : 0;
+    }
+}
+
+/* inverted dropout: out = x * mask / keep_p;  backward: dx = dout * mask / keep_p */
+EXPORT void oracle_dropout_fwd(int64_t n, const double *x, const uint8_t *mask, double keep_p, double *out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = mask[i] ? x[i] / keep_p : 0.0;
+}
+
+EXPORT void oracle_dropout_bwd(int64_t n, const double *dout, const uint8_t *mask, double keep_p, double *dx) {
+  for (int64_t i = 0; i < n; ++i) dx[i] = mask[i] ? dout[i] / keep_p : 0.0;
+}
+
+/* LeNet-512 (SystemML's mnist_lenet.dml topology, SURVEY §8(c) reading 12 [ext]; R22):
+ *   z1 = conv(X; F1,b1, 5x5 p2);  a1,i1 = relu_maxpool(z1, 2x2/2)
+ *   z2 = conv(a1; F2,b2, 5x5 p2); a2,i2 = relu_maxpool(z2, 2x2/2)
+ *   z3 = a2 W3^T + b3  (3136 -> 512);  r3 = relu(z3);  h = dropout(r3; mask, keep_p)
+ *   s  = h W4^T + b4   (512 -> 10);    p = softmax(s);  L = -(1/Ng) sum log(max(p[y], 1e-15))
+ * backward:  ds = (p - onehot(y)) / Ng;  dW4 = ds^T h;  db4 = colsum(ds);  dh = ds W4
+ *   dr3 = dropout_bwd(dh; mask);  dz3 = dr3 * [z3 > 0];  dW3 = dz3^T a2;  db3 = colsum(dz3)
+ *   da2 = dz3 W3;  then exactly the LeNet-min tail (dz2, dF2, db2, da1, dz1, dF1, db1).
+ * train = 0 (scoring) skips dropout (h = r3).  row0 = global index of local row 0 (the
+ * mask is a function of the global sample row, so any sharding draws the same masks).
+ * Flat parameter order: F1[32x25], b1[32], F2[64x800], b2[64], W3[512x3136], b3[512],
+ * W4[10x512], b4[10]  (1,663,370 floats).                                             */
+#define L5_H 512
+#define L5_F1 0
+#define L5_B1 (L5_F1 + 32 * 25)
+#define L5_F2 (L5_B1 + 32)
+#define L5_B2 (L5_F2 + 64 * 800)
+#define L5_W3 (L5_B2 + 64)
+#define L5_B3 (L5_W3 + L5_H * 3136)
+#define L5_W4 (L5_B3 + L5_H)
+#define L5_B4 (L5_W4 + 10 * L5_H)
+#define L5_NP (L5_B4 + 10)
+
+EXPORT int64_t oracle_lenet512_num_params(void) { return L5_NP; }
+
+/* forward; writes a1, i1, a2, i2 (as oracle_lenet_forward), z3 [n x 512], h [n x 512],
+ * mask [n x 512] (all ones when train = 0) and scores [n x 10]. */
+EXPORT void oracle_lenet512_forward(int64_t n, int64_t row0, const double *x, const double *prm,
+                                    int64_t train, uint64_t seed, uint64_t step, double keep_p,
+                                    double *a1, int32_t *i1, double *a2, int32_t *i2, double *z3,
+                                    double *h, uint8_t *mask, double *scores) {
+  double *z1 = (double *)malloc(sizeof(double) * (size_t)(n * 32 * 784));
+  double *z2 = (double *)malloc(sizeof(double) * (size_t)(n * 64 * 196));
+  double *r3 = (double *)malloc(sizeof(double) * (size_t)(n * L5_H));
+  oracle_conv2d_fwd(n, 1, 28, 28, 32, 5, 5, 1, 1, 2, 2, x, prm + L5_F1, prm + L5_B1, z1);
+  oracle_relu_maxpool(n, 32, 28, 28, 2, 2, 2, 2, 0, 0, 1, z1, a1, i1);
+  oracle_conv2d_fwd(n, 32, 14, 14, 64, 5, 5, 1, 1, 2, 2, a1, prm + L5_F2, prm + L5_B2, z2);
+  oracle_relu_maxpool(n, 64, 14, 14, 2, 2, 2, 2, 0, 0, 1, z2, a2, i2);
+  const double *W3 = prm + L5_W3, *b3 = prm + L5_B3, *W4 = prm + L5_W4, *b4 = prm + L5_B4;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t u = 0; u < L5_H; ++u) {
+      double acc = b3[u];
+      for (int64_t d = 0; d < 3136; ++d) acc += a2[i * 3136 + d] * W3[u * 3136 + d];
+      z3[i * L5_H + u] = acc;
+      r3[i * L5_H + u] = acc > 0.0 ? acc : 0.0; /* R7 */
+    }
+  if (train) {
+    oracle_dropout_mask(seed, step, row0, n, L5_H, keep_p, mask);
+    oracle_dropout_fwd(n * L5_H, r3, mask, keep_p, h);
+  } else {
+    memset(mask, 1, (size_t)(n * L5_H));
+    memcpy(h, r3, sizeof(double) * (size_t)(n * L5_H));
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < 10; ++j) {
+      double acc = b4[j];
+      for (int64_t u = 0; u < L5_H; ++u) acc += h[i * L5_H + u] * W4[j * L5_H + u];
+      scores[i * 10 + j] = acc;
+    }
+  free(z1); free(z2); free(r3);
+}
+
+EXPORT void oracle_lenet512_fwd_bwd(int64_t n, int64_t n_global, int64_t row0, const double *x,
+                                    const int32_t *labels, const double *prm, uint64_t seed,
+                                    uint64_t step, double keep_p, double *grads, double *loss_sum) {
+  double *a1 = (double *)malloc(sizeof(double) * (size_t)(n * 6272));
+  double *a2 = (double *)malloc(sizeof(double) * (size_t)(n * 3136));
+  int32_t *i1 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n * 6272));
+  int32_t *i2 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n * 3136));
+  double *z3 = (double *)malloc(sizeof(double) * (size_t)(n * L5_H));
+  double *h = (double *)malloc(sizeof(double) * (size_t)(n * L5_H));
+  uint8_t *mask = (uint8_t *)malloc((size_t)(n * L5_H));
+  double *sc = (double *)malloc(sizeof(double) * (size_t)(n * 10));
+  double *ds = (double *)malloc(sizeof(double) * (size_t)(n * 10));
+  double *dh = (double *)malloc(sizeof(double) * (size_t)(n * L5_H));
+  double *dz3 = (double *)malloc(sizeof(double) * (size_t)(n * L5_H));
+  double *da2 = (double *)malloc(sizeof(double) * (size_t)(n * 3136));
+  double *dz2 = (double *)malloc(sizeof(double) * (size_t)(n * 12544));
+  double *da1 = (double *)malloc(sizeof(double) * (size_t)(n * 6272));
+  double *dz1 = (double *)malloc(sizeof(double) * (size_t)(n * 25088));
+  oracle_lenet512_forward(n, row0, x, prm, 1, seed, step, keep_p, a1, i1, a2, i2, z3, h, mask, sc);
+
+  double loss = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double m = sc[i * 10];
+    for (int j = 1; j < 10; ++j) m = sc[i * 10 + j] > m ? sc[i * 10 + j] : m;
+    double den = 0.0;
+    for (int j = 0; j < 10; ++j) den += exp(sc[i * 10 + j] - m);
+    for (int j = 0; j < 10; ++j) {
+      const double pj = exp(sc[i * 10 + j] - m) / den;
+      ds[i * 10 + j] = (pj - (j == labels[i] ? 1.0 : 0.0)) / (double)n_global;
+      if (j == labels[i]) loss += -log(pj > 1e-15 ? pj : 1e-15);
+    }
+  }
+  if (loss_sum) *loss_sum = loss / (double)n_global;
+
+  const double *W3 = prm + L5_W3, *W4 = prm + L5_W4;
+  double *dW4 = grads + L5_W4, *db4 = grads + L5_B4, *dW3 = grads + L5_W3, *db3 = grads + L5_B3;
+  for (int j = 0; j < 10; ++j) {
+    double accb = 0.0;
+    for (int64_t i = 0; i < n; ++i) accb += ds[i * 10 + j];
+    db4[j] = accb;
+    for (int64_t u = 0; u < L5_H; ++u) {
+      double acc = 0.0;
+      for (int64_t i = 0; i < n; ++i) acc += ds[i * 10 + j] * h[i * L5_H + u];
+      dW4[j * L5_H + u] = acc;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t u = 0; u < L5_H; ++u) {
+      double acc = 0.0;
+      for (int j = 0; j < 10; ++j) acc += ds[i * 10 + j] * W4[j * L5_H + u];
+      dh[i * L5_H + u] = acc;
+    }
+  oracle_dropout_bwd(n * L5_H, dh, mask, keep_p, dz3);            /* dr3 */
+  for (int64_t e = 0; e < n * L5_H; ++e) dz3[e] = z3[e] > 0.0 ? dz3[e] : 0.0; /* relu' */
+#pragma omp parallel for schedule(static)
+  for (int64_t u = 0; u < L5_H; ++u) {
+    double accb = 0.0;
+    for (int64_t i = 0; i < n; ++i) accb += dz3[i * L5_H + u];
+    db3[u] = accb;
+    for (int64_t d = 0; d < 3136; ++d) {
+      double acc = 0.0;
+      for (int64_t i = 0; i < n; ++i) acc += dz3[i * L5_H + u] * a2[i * 3136 + d];
+      dW3[u * 3136 + d] = acc;
+    }
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t d = 0; d < 3136; ++d) {
+      double acc = 0.0;
+      for (int64_t u = 0; u < L5_H; ++u) acc += dz3[i * L5_H + u] * W3[u * 3136 + d];
+      da2[i * 3136 + d] = acc;
+    }
+  oracle_maxpool_bwd(n, 64, 14, 14, 7, 7, i2, da2, a2, dz2);
+  oracle_conv2d_bwd_filter(n, 32, 14, 14, 64, 5, 5, 1, 1, 2, 2, a1, dz2, grads + L5_F2, grads + L5_B2);
+  oracle_conv2d_bwd_data(n, 32, 14, 14, 64, 5, 5, 1, 1, 2, 2, prm + L5_F2, dz2, da1);
+  oracle_maxpool_bwd(n, 32, 28, 28, 14, 14, i1, da1, a1, dz1);
+  oracle_conv2d_bwd_filter(n, 1, 28, 28, 32, 5, 5, 1, 1, 2, 2, x, dz1, grads + L5_F1, grads + L5_B1);
+  free(a1); free(a2); free(i1); free(i2); free(z3); free(h); free(mask); free(sc); free(ds);
+  free(dh); free(dz3); free(da2); free(dz2); free(da1); free(dz1);
+}
+
+/* scoring of LeNet-512 (no dropout at inference): first maximal class + softmax */
+EXPORT void oracle_lenet512_predict(int64_t n, const double *x, const double *prm, int32_t *pred,
+                                    double *probs) {
+  double *a1 = (double *)malloc(sizeof(double) * (size_t)(n * 6272));
+  double *a2 = (double *)malloc(sizeof(double) * (size_t)(n * 3136));
+  int32_t *i1 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n * 6272));
+  int32_t *i2 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n * 3136));
+  double *z3 = (double *)malloc(sizeof(double) * (size_t)(n * L5_H));
+  double *h = (double *)malloc(sizeof(double) * (size_t)(n * L5_H));
+  uint8_t *mask = (uint8_t *)malloc((size_t)(n * L5_H));
+  double *sc = (double *)malloc(sizeof(double) * (size_t)(n * 10));
+  oracle_lenet512_forward(n, 0, x, prm, 0, 0, 0, 1.0, a1, i1, a2, i2, z3, h, mask, sc);
+  for (int64_t i = 0; i < n; ++i) {
+    double m = sc[i * 10];
+    int32_t arg = 0;
+    for (int j = 1; j < 10; ++j)
+      if (sc[i * 10 + j] > m) { m = sc[i * 10 + j]; arg = j; }
+    double den = 0.0;
+    for (int j = 0; j < 10; ++j) den += exp(sc[i * 10 + j] - m);
+    for (int j = 0; j < 10; ++j) probs[i * 10 + j] = exp(sc[i * 10 + j] - m) / den;
+    pred[i] = arg;
+  }
+  free(a1); free(a2); free(i1); free(i2); free(z3); free(h); free(mask); free(sc);
+}

@@ -39,6 +39,22 @@ LENET_PARAM_SHAPES = (
 LENET_NUM_PARAMS = sum(int(np.prod(s)) for _, s in LENET_PARAM_SHAPES)  # 83,466
 
 
+# LeNet-512: SystemML's mnist_lenet.dml topology (NEXT-4; reading R22):
+# ... -> affine(3136 -> 512) -> relu -> dropout -> affine(512 -> 10) -> softmax
+LENET512_HIDDEN = 512
+LENET512_PARAM_SHAPES = (
+    ("F1", (32, 1 * 5 * 5)),
+    ("b1", (32,)),
+    ("F2", (64, 32 * 5 * 5)),
+    ("b2", (64,)),
+    ("W3", (LENET512_HIDDEN, 64 * 7 * 7)),
+    ("b3", (LENET512_HIDDEN,)),
+    ("W4", (10, LENET512_HIDDEN)),
+    ("b4", (10,)),
+)
+LENET512_NUM_PARAMS = sum(int(np.prod(s)) for _, s in LENET512_PARAM_SHAPES)  # 1,663,370
+
+
 def rng(*seed: int) -> np.random.Generator:
     return np.random.default_rng([ROOT_SEED, *[int(s) for s in seed]])
 
@@ -169,6 +185,42 @@ def lenet_params(seed=(6,), dyadic_grid=False) -> np.ndarray:
 def split_lenet_params(flat: np.ndarray):
     out, o = {}, 0
     for name, shape in LENET_PARAM_SHAPES:
+        sz = int(np.prod(shape))
+        out[name] = flat[o:o + sz].reshape(shape)
+        o += sz
+    return out
+
+
+def lenet512_params(seed=(7,), dyadic_grid=False) -> np.ndarray:
+    """Flat float32[1,663,370] in the order F1,b1,F2,b2,W3,b3,W4,b4 (LeNet-512).
+
+    Default: Glorot-uniform weights, zero biases (as ``lenet_params``).  ``dyadic_grid``:
+    F1 {-3..3}/16, F2 {-3..3}/64, W3 {-3..3}/256, W4 {-3..3}/64, b {-3..3}/16."""
+    g = rng(*seed)
+    out = []
+    for name, shape in LENET512_PARAM_SHAPES:
+        if dyadic_grid:
+            denom = {"F1": 16, "F2": 64, "W3": 256, "W4": 64}.get(name, 16)
+            k = g.integers(-3, 4, size=shape)
+            out.append((k / denom).astype(np.float32).ravel())
+        elif name.startswith("b"):
+            out.append(np.zeros(shape, dtype=np.float32).ravel())
+        else:
+            fan_out, fan_in = shape[0], shape[1]
+            if name == "F1":
+                fan_out = 32 * 25
+            elif name == "F2":
+                fan_out = 64 * 25
+            lim = np.sqrt(6.0 / (fan_in + fan_out))
+            out.append(g.uniform(-lim, lim, size=shape).astype(np.float32).ravel())
+    flat = np.concatenate(out)
+    assert flat.size == LENET512_NUM_PARAMS
+    return flat
+
+
+def split_lenet512_params(flat: np.ndarray):
+    out, o = {}, 0
+    for name, shape in LENET512_PARAM_SHAPES:
         sz = int(np.prod(shape))
         out[name] = flat[o:o + sz].reshape(shape)
         o += sz
