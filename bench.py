@@ -398,7 +398,36 @@ def config_legs(S, peaks, quick=False):
     out["per_rank_step_local1024"] = {"us_per_step": round(1e3 * med, 2), "min_us": round(1e3 * mn, 2),
                                       "note": "one rank's compute at N = 8 (no allreduce: 1 GPU); "
                                               "8-GPU efficiency = t(8192) / (8 (t(1024) + t_allreduce))"}
+    del net
+    out["lenet512_step_N8192"] = lenet512_leg(S, peaks, flush, reps)
     return out
+
+
+def lenet512_leg(S, peaks, flush, reps):
+    """NEXT-4: the LeNet-512 step (affine 3136->512 + relu + dropout 0.5 + affine 512->10) at
+    batch 8192, TF32, graph replay, with its per-stage breakdown (untimed eager pass)."""
+    import torch
+    import synth
+    n = GLOBAL_BATCH
+    xs = [torch.from_numpy(synth.mnist_like(n, seed=(1107, i))).cuda() for i in range(2)]
+    ys = [torch.from_numpy(synth.labels(n, seed=(1108, i))).cuda() for i in range(2)]
+    prm = torch.from_numpy(synth.lenet512_params(seed=(7,))).cuda()
+    net = S.LeNet(n, math="tf32", model="lenet512", keep_p=0.5, seed=180204647)
+    g = torch.empty_like(prm)
+    med, mn = time_graph(lambda: net.step(prm, g, xs[0], ys[0], n, lr=0.01), reps, flush)
+    # hidden-layer FLOPs: 3 GEMMs of 2 * n * 3136 * 512
+    gemm_flop = 3 * 2.0 * n * 3136 * 512
+    net.set_timing(True)
+    for _ in range(3):
+        net.step(prm, g, xs[1], ys[1], n, lr=0.01)
+    torch.cuda.synchronize()
+    stages = {k: round(v[0] / max(1, v[1]), 4) for k, v in net.get_timing(reset=True).items() if v[1]}
+    net.set_timing(False)
+    return {"N": n, "us_per_step": round(1e3 * med, 2), "min_us": round(1e3 * mn, 2),
+            "images_per_s": round(n / (med * 1e-3), 1), "launch": "cuda_graph", "keep_p": 0.5,
+            "params": int(net.num_params), "stage_avg_ms": stages,
+            "hidden_gemm_flop_per_step": gemm_flop,
+            "note": "F3h = hidden GEMM + bias/relu/dropout epilogue; B3h = dz3, dW3 (transpose + TMA GEMM), da2 GEMM"}
 
 
 def oracle_per_config():

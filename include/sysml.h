@@ -236,6 +236,34 @@ SYSML_API sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math,
                                 int64_t max_nnz, sysml_lenet **out);
 SYSML_API sysml_status sysml_lenet_destroy(sysml_lenet *h);
 
+/* LeNet-512 (NEXT-4; SystemML's mnist_lenet topology, R22-R24; "20+
+ * pre-implemented layers", S:275-281 dropout):
+ *   [conv5x5(32,p2)+relu+pool2] -> [conv5x5(64,p2)+relu+pool2] -> affine(3136->512) -> relu
+ *   -> inverted dropout(keep_p) -> affine(512->10) -> softmax -> cross-entropy.
+ * Flat parameter order: F1[32x25], b1[32], F2[64x800], b2[64], W3[512x3136], b3[512],
+ * W4[10x512], b4[10] (1,663,370 floats).  The returned handle serves sysml_lenet_fwd_bwd /
+ * _predict / _step / _step_opt / _step_host* exactly as a LeNet-min handle, with this
+ * parameter vector.  Dropout mask (R23): unit j of GLOBAL sample row g is kept iff the high
+ * 32 bits of raw output e = g*512 + j of Philox4x64-10 with key (seed, t) are below
+ * floor(keep_p * 2^32) (numpy.random.Philox order), where t is the handle's device step
+ * counter: 0 at creation, +1 at the end of every sysml_lenet_step* call (so CUDA-graph
+ * replays draw fresh masks); fwd_bwd alone does not advance it.  Kept units are scaled by
+ * 1/keep_p.  Scoring (predict) applies no dropout.
+ * Errors: SYSML_ERR_ARG if keep_p is not in (0, 1]; others as sysml_lenet_create.        */
+SYSML_API int64_t sysml_lenet512_num_params(void);
+SYSML_API sysml_status sysml_lenet512_create(int32_t max_local_batch, int32_t math, int32_t input_is_csr,
+                                             int64_t max_nnz, float keep_p, uint64_t seed,
+                                             sysml_lenet **out);
+/* row0 = global index of the local shard's first row (rank * local batch in the
+ * data-parallel plan; the mask follows the global row, so sharding does not change it);
+ * step = new value of the device step counter, set on `stream`.  LeNet-512 handles only.  */
+SYSML_API sysml_status sysml_lenet_set_dropout(sysml_lenet *h, int64_t row0, int64_t step,
+                                               sysml_stream_t stream);
+/* Reads the device step counter (synchronous).                                           */
+SYSML_API sysml_status sysml_lenet_get_dropout_step(sysml_lenet *h, int64_t *step);
+/* Parameter count of this handle's model (83,466 or 1,663,370).                          */
+SYSML_API int64_t sysml_lenet_handle_num_params(const sysml_lenet *h);
+
 /* Forward + backward of the local shard (rows of the global batch):
  * grads (device, fp32[83466]) receive sum over local samples of dLoss/dtheta
  * with Loss = (1/n_global) sum_global CE, i.e. already scaled by 1/n_global

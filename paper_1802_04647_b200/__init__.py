@@ -46,6 +46,8 @@ EXPORTS = (
     "sysml_lenet_set_timing", "sysml_lenet_get_timing",
     "sysml_optimizer_state_floats", "sysml_optimizer_update", "sysml_lenet_step_opt",
     "sysml_lenet_step_host_pipelined", "sysml_decide_format",
+    "sysml_lenet512_num_params", "sysml_lenet512_create", "sysml_lenet_set_dropout",
+    "sysml_lenet_get_dropout_step", "sysml_lenet_handle_num_params",
     "sysml_conv2d_csr_filter", "sysml_count_nonzeros", "sysml_dense_to_csr", "sysml_lenet_predict",
 )
 
@@ -189,6 +191,12 @@ def lib(build_if_missing: bool = False):
                                          c_i64, vp, vp, vp]),
         "sysml_lenet_get_timing": (c_i32, [vp, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(c_i64), ctypes.POINTER(ctypes.c_char_p)]),
+        "sysml_lenet512_num_params": (c_i64, []),
+        "sysml_lenet512_create": (c_i32, [c_i32, c_i32, c_i32, c_i64, ctypes.c_float, ctypes.c_uint64,
+                                          ctypes.POINTER(vp)]),
+        "sysml_lenet_set_dropout": (c_i32, [vp, c_i64, c_i64, vp]),
+        "sysml_lenet_get_dropout_step": (c_i32, [vp, ctypes.POINTER(c_i64)]),
+        "sysml_lenet_handle_num_params": (c_i64, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -458,17 +466,42 @@ def nccl_comm_ptr(group=None, allow_single: bool = False) -> Optional[int]:
 
 
 class LeNet:
-    """Minibatch SGD-step driver (Listing 1; P:142 LeNet; P:187-192 data-parallel plan)."""
+    """Minibatch SGD-step driver (Listing 1; P:142 LeNet; P:187-192 data-parallel plan).
+
+    model="lenet-min" (default): conv-relu-pool x2, affine 3136->10 (83,466 parameters).
+    model="lenet512": SystemML's mnist_lenet topology with affine 3136->512, relu, inverted
+    dropout (keep_p, Philox mask stream ``seed``), affine 512->10 (1,663,370 parameters;
+    sysml_lenet512_create, NEXT-4)."""
 
     NUM_PARAMS = 83466
+    NUM_PARAMS_512 = 1663370
 
-    def __init__(self, max_local_batch: int, math="tf32", csr=False, max_nnz=0):
+    def __init__(self, max_local_batch: int, math="tf32", csr=False, max_nnz=0, model="lenet-min",
+                 keep_p=0.5, seed=0):
         L = lib()
         h = ctypes.c_void_p()
-        _check(L.sysml_lenet_create(int(max_local_batch), _MATH[math], int(bool(csr)), int(max_nnz), ctypes.byref(h)))
+        if model == "lenet-min":
+            _check(L.sysml_lenet_create(int(max_local_batch), _MATH[math], int(bool(csr)), int(max_nnz),
+                                        ctypes.byref(h)))
+        elif model == "lenet512":
+            _check(L.sysml_lenet512_create(int(max_local_batch), _MATH[math], int(bool(csr)), int(max_nnz),
+                                           ctypes.c_float(keep_p), ctypes.c_uint64(int(seed)), ctypes.byref(h)))
+        else:
+            raise ValueError(f"unknown model {model!r}")
         self.h = h
+        self.model = model
+        self.num_params = int(L.sysml_lenet_handle_num_params(h))
         self.max_local_batch = max_local_batch
         self.csr = bool(csr)
+
+    def set_dropout(self, row0=0, step=0, stream=None):
+        """LeNet-512: global row offset of the local shard and the device mask-step counter."""
+        _check(lib().sysml_lenet_set_dropout(self.h, int(row0), int(step), _stream(stream)))
+
+    def dropout_step(self) -> int:
+        v = ctypes.c_int64(0)
+        _check(lib().sysml_lenet_get_dropout_step(self.h, ctypes.byref(v)))
+        return v.value
 
     def close(self):
         if getattr(self, "h", None):

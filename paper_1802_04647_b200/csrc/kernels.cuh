@@ -182,4 +182,32 @@ sysml_status launch_maxpool_bwd_spf(const PoolArgs &a, const int32_t *argmax, co
 sysml_status launch_nchw_to_spf(int N, int C, int H, int W, const float *x, float *spf,
                                 int64_t plane, int Wf, int Lf, int off, cudaStream_t st);
 
+// affine_gemm.cu : the affine layers of the LeNet-512 step (NEXT-4)
+// Fused epilogue of tc_gemm: C = acc (+ bias[col]) (relu) (inverted dropout of unit col of
+// global row row0 + row: Philox4x64-10 stream (seed, *step), kept iff (raw >> 32) < keep_T)
+struct GemmEpi {
+  const float *bias = nullptr;
+  int relu = 0, dropout = 0;
+  uint64_t keep_T = 0;
+  float keep_p = 1.f;
+  uint64_t seed = 0;
+  const uint64_t *step = nullptr;  // device counter (advances once per training step)
+  int64_t row0 = 0;
+  int units = 0;                    // mask row length (= N)
+};
+bool tc_gemm_supported(int M, int N, int K, int64_t lda, int64_t ldb);
+// C[M][N] (row stride ldc) = A[M][K] (lda) . B[N][K]^T (ldb), tcgen05 TF32, fp32 accumulate
+sysml_status tc_gemm(int M, int N, int K, const float *A, int64_t lda, const float *B, int64_t ldb,
+                     float *C, int64_t ldc, const GemmEpi &e, cudaStream_t st);
+sysml_status launch_transpose(const float *in, int R, int Cc, int64_t ldi, float *out, int64_t ldo,
+                              cudaStream_t st);
+sysml_status launch_dz3(int n, int H, const float *ds, const float *W4, const float *h, float keep_p,
+                        float *dz3, float *dz3T, int64_t ldt, cudaStream_t st);
+sysml_status launch_relu_dropout(float *z, int n, int H, int64_t row0, uint64_t seed, const uint64_t *step,
+                                 uint64_t T, float keep_p, int dropout, cudaStream_t st);
+sysml_status launch_counter_inc(uint64_t *c, cudaStream_t st);
+int route_da2_chunks(int n);
+sysml_status launch_route_da2_spf(int n, const float *da2, const uint64_t *c2, int64_t cplane, float *dz2s,
+                                  int64_t plane, float *dbpart, cudaStream_t st);
+
 }  // namespace sysml

@@ -54,8 +54,10 @@ constexpr int D3 = 3136, NCLS = 10;
 // iterations of a2 loads in flight, W3 from smem serving both samples.  The 2 x 10 partial
 // logits are summed over the warp by a halving reduce-scatter (masks 16, 8) and xor sums
 // (4, 2, 1) -- a fixed order; one lane per sample does the softmax/CE.
+// D = input features of the output affine layer: 3136 (LeNet-min), 512 (LeNet-512).
 constexpr int F3_THREADS = 512, F3_WARPS = F3_THREADS / 32;
-constexpr size_t F3_SMEM = (size_t)NCLS * D3 * 4 + (size_t)F3_WARPS * 2 * NCLS * 4;
+constexpr size_t f3_smem(int D) { return (size_t)NCLS * D * 4 + (size_t)F3_WARPS * 2 * NCLS * 4; }
+template <int D3>
 __global__ void __launch_bounds__(F3_THREADS) affine_softmax_ce_smem_kernel(
     int n, float inv_ng, const float *__restrict__ a2, const float *__restrict__ W3,
     const float *__restrict__ b3, const int32_t *__restrict__ labels, float *__restrict__ ds,
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(F3_THREADS) affine_softmax_ce_smem_kernel(
 // Scoring (P:193-202 parfor-style row-partitioned scoring): warp per sample, logits =
 // a2 . W3^T + b3 (lanes stride the 784 float4 columns, xor-tree reduction), then the
 // max-shifted softmax probabilities and the first maximum as the predicted label.
+template <int D3>
 __global__ void lenet_predict_kernel(int n, const float *__restrict__ a2, const float *__restrict__ W3,
                                      const float *__restrict__ b3, int32_t *__restrict__ pred,
                                      float *__restrict__ probs) {
@@ -228,13 +231,17 @@ __global__ void ordered_total_kernel(const float *__restrict__ v, int n, float *
 // of the 784 float4 columns of a2 (thread owns 4 columns x 10 classes), y = sample chunk;
 // 8 samples' float4 loads in flight per thread.  part[chunk][j][d] (j < 10), and
 // part[chunk][10][j] = db3 partial (sum of ds over the chunk).
-constexpr int DW3_T = 196;                                 // 4 x 196 = 784 float4 columns
-constexpr int DW3_LEN = NCLS * D3 + NCLS;                 // W3 then b3 (the grads layout)
-constexpr int DW3_STRIDE = (DW3_LEN + 3) / 4 * 4;         // partial stride: float4 aligned
+// Templated on the feature width D3 (3136: 4 blocks of 196 threads; 512: one of 128).
+constexpr int dw3_threads(int D) { return D == 3136 ? 196 : D / 4; }
+constexpr int dw3_len(int D) { return NCLS * D + NCLS; }              // W then b (grads layout)
+constexpr int dw3_stride(int D) { return (dw3_len(D) + 3) / 4 * 4; }  // float4-aligned partials
+constexpr int DW3_LEN = dw3_len(D3), DW3_STRIDE = dw3_stride(D3);
+template <int D3, int DW3_T>
 __global__ void __launch_bounds__(DW3_T) dw3_partial_kernel(int n, int n_per_chunk, const float *__restrict__ ds,
                                                             const float *__restrict__ a2,
                                                             float *__restrict__ part) {
-  const int d4 = blockIdx.x * DW3_T + threadIdx.x;  // < 784
+  constexpr int DW3_STRIDE = dw3_stride(D3);
+  const int d4 = blockIdx.x * DW3_T + threadIdx.x;  // < D3 / 4
   const int chunk = blockIdx.y;
   const int n0 = chunk * n_per_chunk, n1 = min(n, n0 + n_per_chunk);
   __shared__ float dss[64 * NCLS];
@@ -496,8 +503,16 @@ NcclSyms &nccl_syms() {
 const char *STAGE_NAMES[] = {"F1_conv1_pool", "F2_conv2_pool", "F3_affine_softmax_ce",
                              "B3_affine_bwd", "B2p_maxpool_bwd2", "B2f_conv2_bwd_filter",
                              "B2d_conv2_bwd_data", "B1p_maxpool_bwd1", "B1f_conv1_bwd_filter",
-                             "B1_fused_pool_bwd_conv1_wgrad"};
-constexpr int NSTAGES = 10;
+                             "B1_fused_pool_bwd_conv1_wgrad", "F3h_affine_relu_dropout",
+                             "B3h_affine_hidden_bwd"};
+constexpr int NSTAGES = 12;
+
+// LeNet-512 (NEXT-4; R22): F1, b1, F2, b2, W3[512x3136], b3[512], W4[10x512], b4[10]
+constexpr int H5 = 512;
+constexpr int OFF5_W3 = OFF_B2 + 64, OFF5_B3 = OFF5_W3 + H5 * D3, OFF5_W4 = OFF5_B3 + H5,
+              OFF5_B4 = OFF5_W4 + NCLS * H5, NUM_PARAMS5 = OFF5_B4 + NCLS;
+
+__global__ void counter_set_kernel(uint64_t *c, uint64_t v) { *c = v; }
 
 }  // namespace
 
@@ -543,6 +558,14 @@ struct sysml_lenet {
   // TF32 path: pool argmax as packed 2-bit window codes, one u32 per (16 channels, window)
   uint64_t *c1 = nullptr, *c2 = nullptr;  // [2][b*196], [4][b*49] (kernels.cuh TcSpfIO::code)
   float *db2part = nullptr;                // B2p's conv2 bias-gradient partials [chunks][3136]
+  // LeNet-512 (hidden = 512; 0 = LeNet-min): affine 3136->512 + relu + inverted dropout
+  int hidden = 0;
+  int64_t num_params = NUM_PARAMS;
+  float keep_p = 1.f;
+  uint64_t seed = 0, keep_T = 0;
+  int64_t row0 = 0;                 // global index of local row 0 (the mask follows the global row)
+  uint64_t *drop_step = nullptr;    // device step counter of the mask stream (R23)
+  float *h3 = nullptr, *dz3 = nullptr, *dz3T = nullptr, *a2T = nullptr, *W3T = nullptr, *part4 = nullptr;
 };
 
 namespace {
@@ -596,8 +619,11 @@ extern "C" {
 
 int64_t sysml_lenet_num_params(void) { return NUM_PARAMS; }
 
-sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t input_is_csr,
-                                int64_t max_nnz, sysml_lenet **out) {
+}  // extern "C"
+
+static sysml_status lenet_create_impl(int32_t max_local_batch, int32_t math, int32_t input_is_csr,
+                                      int64_t max_nnz, int hidden, float keep_p, uint64_t seed,
+                                      sysml_lenet **out) {
   SYSML_CHECK_ARG(out != nullptr, "out is NULL");
   SYSML_CHECK_ARG(max_local_batch >= 1, "max_local_batch must be >= 1 (got %d)", max_local_batch);
   SYSML_CHECK_ARG(math == SYSML_MATH_FP32 || math == SYSML_MATH_TF32, "bad math %d", math);
@@ -614,6 +640,11 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
   }
   h->math = math;
   h->csr = input_is_csr ? 1 : 0;
+  h->hidden = hidden;
+  h->num_params = hidden ? NUM_PARAMS5 : NUM_PARAMS;
+  h->keep_p = keep_p;
+  h->seed = seed;
+  h->keep_T = (uint64_t)floor((double)keep_p * 4294967296.0);  // R23: kept iff (raw >> 32) < T
   h->max_nnz = max_nnz;
   const int64_t b = max_local_batch;
   h->dw3_chunks = dw3_chunks_for(max_local_batch);
@@ -655,8 +686,37 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
       return fail(SYSML_ERR_CUDA);
     }
   }
+  const int64_t ldt_max = (b + 3) / 4 * 4;
+  if (hidden) {
+    ALLOC(h->h3, b * H5);
+    ALLOC(h->dz3, b * H5);
+    ALLOC(h->dz3T, (int64_t)H5 * ldt_max);
+    ALLOC(h->a2T, (int64_t)D3 * ldt_max);
+    ALLOC(h->W3T, (int64_t)D3 * H5);
+    ALLOC(h->part4, (int64_t)h->dw3_chunks * dw3_stride(H5));
+    ALLOC(h->drop_step, 1);
+    if (cudaMemset(h->drop_step, 0, sizeof(uint64_t)) != cudaSuccess) {
+      set_error("cudaMemset of the dropout step counter failed");
+      return fail(SYSML_ERR_CUDA);
+    }
+  }
   // workspace: max over the conv calls of the step
   size_t need = 0, w = 0;
+  if (hidden) {
+    sysml_status s5;
+    if (math == SYSML_MATH_TF32) {
+      const ConvArgs wa{1, D3, 1, (int)ldt_max, H5, 1, 1, 1, 1, 0, 0, 1, (int)ldt_max};
+      need = std::max(need, tc_wgrad_1x1_ws(wa));
+    } else {
+      const sysml_conv_desc hd{(int32_t)b, D3, 1, 1, H5, 1, 1, 1, 1, 0, 0, math};
+      if ((s5 = conv_fwd_ws(hd, nullptr, 0, &w)) != SYSML_OK) return fail(s5);
+      need = std::max(need, w);
+      if ((s5 = conv_bwd_filter_ws(hd, 0, &w)) != SYSML_OK) return fail(s5);
+      need = std::max(need, w);
+      if ((s5 = conv_bwd_data_ws(hd, &w)) != SYSML_OK) return fail(s5);
+      need = std::max(need, w);
+    }
+  }
   const sysml_conv_desc c1 = conv1_desc(max_local_batch, math), c2 = conv2_desc(max_local_batch, math);
   const sysml_pool_desc p1 = pool1_desc(max_local_batch), p2 = pool2_desc(max_local_batch);
   sysml_status s;
@@ -726,6 +786,42 @@ sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t i
   return SYSML_OK;
 }
 
+extern "C" {
+
+sysml_status sysml_lenet_create(int32_t max_local_batch, int32_t math, int32_t input_is_csr,
+                                int64_t max_nnz, sysml_lenet **out) {
+  return lenet_create_impl(max_local_batch, math, input_is_csr, max_nnz, 0, 1.f, 0, out);
+}
+
+int64_t sysml_lenet512_num_params(void) { return NUM_PARAMS5; }
+
+sysml_status sysml_lenet512_create(int32_t max_local_batch, int32_t math, int32_t input_is_csr,
+                                   int64_t max_nnz, float keep_p, uint64_t seed, sysml_lenet **out) {
+  SYSML_CHECK_ARG(keep_p > 0.f && keep_p <= 1.f, "keep_p %g must be in (0, 1]", (double)keep_p);
+  return lenet_create_impl(max_local_batch, math, input_is_csr, max_nnz, H5, keep_p, seed, out);
+}
+
+sysml_status sysml_lenet_set_dropout(sysml_lenet *h, int64_t row0, int64_t step, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(h, "NULL handle");
+  SYSML_CHECK_ARG(h->hidden, "sysml_lenet_set_dropout: the handle has no dropout layer (LeNet-min)");
+  SYSML_CHECK_ARG(row0 >= 0 && step >= 0, "row0 / step must be >= 0");
+  h->row0 = row0;
+  counter_set_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(h->drop_step, (uint64_t)step);
+  SYSML_LAUNCH_CHECK();
+  return SYSML_OK;
+}
+
+sysml_status sysml_lenet_get_dropout_step(sysml_lenet *h, int64_t *step) {
+  SYSML_CHECK_ARG(h && step, "NULL argument");
+  SYSML_CHECK_ARG(h->hidden, "the handle has no dropout layer (LeNet-min)");
+  uint64_t v = 0;
+  SYSML_CUDA(cudaMemcpy(&v, h->drop_step, sizeof(v), cudaMemcpyDeviceToHost));
+  *step = (int64_t)v;
+  return SYSML_OK;
+}
+
+int64_t sysml_lenet_handle_num_params(const sysml_lenet *h) { return h ? h->num_params : -1; }
+
 sysml_status sysml_lenet_destroy(sysml_lenet *h) {
   if (!h) return SYSML_OK;
   if (h->ar_stream) cudaStreamDestroy(h->ar_stream);
@@ -744,6 +840,8 @@ sysml_status sysml_lenet_destroy(sysml_lenet *h) {
   }
   cudaFree(h->ws);
   cudaFree(h->a1s); cudaFree(h->dz2s);
+  cudaFree(h->h3); cudaFree(h->dz3); cudaFree(h->dz3T); cudaFree(h->a2T); cudaFree(h->W3T);
+  cudaFree(h->part4); cudaFree(h->drop_step);
   for (auto &e : h->pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (int i = 0; i < NSTAGES; ++i)
     for (auto &e : h->pending[i]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -857,19 +955,59 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
                                 h->i2, h->ws, h->ws_bytes, st));
   }
   SYSML_TRY(T.end());
+  const bool hid = h->hidden != 0;
+  const int OW = hid ? OFF5_W4 : OFF_W3, OB = hid ? OFF5_B4 : OFF_B3;  // output affine layer
+  const float *feat = hid ? h->h3 : h->a2;                            // its input features
+  const int64_t ldt = ((int64_t)n + 3) / 4 * 4;                       // batch-contiguous row stride
+  const sysml_conv_desc hd{n, D3, 1, 1, H5, 1, 1, 1, 1, 0, 0, h->math};  // affine as a 1x1 conv (FP32)
+  if (hid) {
+    // F3h: h = dropout(relu(a2 W3^T + b3)) (train) / relu(a2 W3^T + b3) (scoring)
+    const bool train = !(pred || probs);
+    SYSML_TRY(T.begin(10));
+    if (h->math == SYSML_MATH_TF32) {
+      GemmEpi e;
+      e.bias = params + OFF5_B3;
+      e.relu = 1;
+      e.dropout = train && h->keep_p < 1.f;
+      e.keep_T = h->keep_T;
+      e.keep_p = h->keep_p;
+      e.seed = h->seed;
+      e.step = h->drop_step;
+      e.row0 = h->row0;
+      e.units = H5;
+      SYSML_TRY(tc_gemm(n, H5, D3, h->a2, D3, params + OFF5_W3, D3, h->h3, H5, e, st));
+    } else {
+      sysml_input ain{0, h->a2, {}};
+      SYSML_TRY(conv_fwd_dispatch(hd, ain, params + OFF5_W3, params + OFF5_B3, h->h3, nullptr, nullptr,
+                                  nullptr, h->ws, h->ws_bytes, st));
+      SYSML_TRY(launch_relu_dropout(h->h3, n, H5, h->row0, h->seed, h->drop_step, h->keep_T, h->keep_p,
+                                    train && h->keep_p < 1.f, st));
+    }
+    SYSML_TRY(T.end());
+  }
   if (pred || probs) {  // scoring: logits, softmax, argmax
-    lenet_predict_kernel<<<(unsigned)ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(n, h->a2, params + OFF_W3,
-                                                                               params + OFF_B3, pred, probs);
+    if (hid)
+      lenet_predict_kernel<H5><<<(unsigned)ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(
+          n, feat, params + OW, params + OB, pred, probs);
+    else
+      lenet_predict_kernel<D3><<<(unsigned)ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(
+          n, feat, params + OW, params + OB, pred, probs);
     SYSML_LAUNCH_CHECK();
     return SYSML_OK;
   }
   // F3
   SYSML_TRY(T.begin(2));
   {
-    SYSML_TRY(smem_attr(affine_softmax_ce_smem_kernel, F3_SMEM));
     const int ctas = (int)std::min<int64_t>(sm_count(), (n + 1) / 2);
-    affine_softmax_ce_smem_kernel<<<(unsigned)ctas, F3_THREADS, F3_SMEM, st>>>(
-        n, inv_ng, h->a2, params + OFF_W3, params + OFF_B3, labels, h->ds, h->lossn);
+    if (hid) {
+      SYSML_TRY(smem_attr(affine_softmax_ce_smem_kernel<H5>, f3_smem(H5)));
+      affine_softmax_ce_smem_kernel<H5><<<(unsigned)ctas, F3_THREADS, f3_smem(H5), st>>>(
+          n, inv_ng, feat, params + OW, params + OB, labels, h->ds, h->lossn);
+    } else {
+      SYSML_TRY(smem_attr(affine_softmax_ce_smem_kernel<D3>, f3_smem(D3)));
+      affine_softmax_ce_smem_kernel<D3><<<(unsigned)ctas, F3_THREADS, f3_smem(D3), st>>>(
+          n, inv_ng, feat, params + OW, params + OB, labels, h->ds, h->lossn);
+    }
   }
   SYSML_LAUNCH_CHECK();
   if (loss_sum) {
@@ -883,27 +1021,62 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
     const int chunks = std::min(h->dw3_chunks, dw3_chunks_for(n));
     const int npc = (int)ceil_div(n, chunks);
     const int used = (int)ceil_div(n, npc);
-    dw3_partial_kernel<<<dim3(D3 / 4 / DW3_T, used), DW3_T, 0, st>>>(n, npc, h->ds, h->a2, h->part3);
-    SYSML_LAUNCH_CHECK();
-    // grads W3 and b3 are contiguous: [W3 (10*3136)][b3 (10)] == part layout
-    dw3_reduce_kernel<<<(unsigned)ceil_div(DW3_LEN / 4, 32), 256, 0, st>>>(h->part3, used, DW3_STRIDE,
-                                                                          DW3_LEN, grads + OFF_W3);
-    SYSML_LAUNCH_CHECK();
-    if (!h->spf) {
-      da2_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)n * D3, 256), 16 * sm_count()), 256,
-                   0, st>>>(n, h->ds, params + OFF_W3, h->da2);
+    if (hid) {  // dW4, db4
+      constexpr int T5 = dw3_threads(H5);
+      dw3_partial_kernel<H5, T5><<<dim3(H5 / 4 / T5, used), T5, 0, st>>>(n, npc, h->ds, feat, h->part4);
       SYSML_LAUNCH_CHECK();
+      dw3_reduce_kernel<<<(unsigned)ceil_div(dw3_len(H5) / 4, 32), 256, 0, st>>>(
+          h->part4, used, dw3_stride(H5), dw3_len(H5), grads + OFF5_W4);
+      SYSML_LAUNCH_CHECK();
+    } else {
+      constexpr int T3 = dw3_threads(D3);
+      dw3_partial_kernel<D3, T3><<<dim3(D3 / 4 / T3, used), T3, 0, st>>>(n, npc, h->ds, h->a2, h->part3);
+      SYSML_LAUNCH_CHECK();
+      // grads W3 and b3 are contiguous: [W3 (10*3136)][b3 (10)] == part layout
+      dw3_reduce_kernel<<<(unsigned)ceil_div(DW3_LEN / 4, 32), 256, 0, st>>>(h->part3, used, DW3_STRIDE,
+                                                                            DW3_LEN, grads + OFF_W3);
+      SYSML_LAUNCH_CHECK();
+      if (!h->spf) {
+        da2_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)n * D3, 256), 16 * sm_count()), 256,
+                     0, st>>>(n, h->ds, params + OFF_W3, h->da2);
+        SYSML_LAUNCH_CHECK();
+      }
     }
   }
   SYSML_TRY(T.end());
+  if (hid) {
+    // B3h: dz3 = (ds W4) [h > 0] / keep_p; dW3 = dz3^T a2, db3 = colsum dz3; da2 = dz3 W3
+    SYSML_TRY(T.begin(11));
+    SYSML_TRY(launch_dz3(n, H5, h->ds, params + OFF5_W4, h->h3, h->keep_p, h->dz3, h->dz3T, ldt, st));
+    if (h->math == SYSML_MATH_TF32) {
+      // contraction over the batch: both operands batch-contiguous (K-major) for the TMA GEMM
+      SYSML_TRY(launch_transpose(h->a2, n, D3, D3, h->a2T, ldt, st));
+      const ConvArgs wa{1, D3, 1, (int)ldt, H5, 1, 1, 1, 1, 0, 0, 1, (int)ldt};
+      SYSML_TRY(tc_wgrad_1x1(wa, h->a2T, h->dz3T, grads + OFF5_W3, grads + OFF5_B3, h->ws, st));
+      SYSML_TRY(launch_transpose(params + OFF5_W3, H5, D3, D3, h->W3T, H5, st));
+      SYSML_TRY(tc_gemm(n, D3, H5, h->dz3, H5, h->W3T, H5, h->da2, D3, GemmEpi{}, st));
+    } else {
+      sysml_input ain{0, h->a2, {}};
+      SYSML_TRY(conv_bwd_filter_dispatch(hd, ain, h->dz3, grads + OFF5_W3, grads + OFF5_B3, h->ws,
+                                         h->ws_bytes, st));
+      SYSML_TRY(conv_bwd_data_dispatch(hd, params + OFF5_W3, h->dz3, h->da2, h->ws, h->ws_bytes, st));
+    }
+    SYSML_TRY(T.end());
+  }
   if (h->spf) {
     // B2p: unpooled gradient straight into the SPF planes (output-frame convention)
     SYSML_TRY(T.begin(4));
-    affine_bwd_route_spf_kernel<<<dim3((unsigned)ceil_div(D3, 256), (unsigned)ceil_div(n, B2P_IMGS)),
-                                  256, 0, st>>>(n, h->ds, params + OFF_W3, h->c2,
-                                                (int64_t)h->max_b * 49, h->dz2s, h->spf_plane,
-                                                h->db2part);
-    SYSML_LAUNCH_CHECK();
+    if (hid) {
+      static_assert(B2P_IMGS == 32, "route_da2_spf_kernel chunks db2 partials by 32 images");
+      SYSML_TRY(launch_route_da2_spf(n, h->da2, h->c2, (int64_t)h->max_b * 49, h->dz2s, h->spf_plane,
+                                     h->db2part, st));
+    } else {
+      affine_bwd_route_spf_kernel<<<dim3((unsigned)ceil_div(D3, 256), (unsigned)ceil_div(n, B2P_IMGS)),
+                                    256, 0, st>>>(n, h->ds, params + OFF_W3, h->c2,
+                                                  (int64_t)h->max_b * 49, h->dz2s, h->spf_plane,
+                                                  h->db2part);
+      SYSML_LAUNCH_CHECK();
+    }
     SYSML_TRY(T.end());
     // B2f
     SYSML_TRY(T.begin(5));
@@ -917,7 +1090,7 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
     } else
       SYSML_TRY(tc_wgrad_spf(sc, h->a1s, h->dz2s, grads + OFF_F2, grads + OFF_B2, h->ws, st));
     SYSML_TRY(T.end());
-    SYSML_TRY(ar_bucket(h, grads + OFF_F2, NUM_PARAMS - OFF_F2, h->ev_b2, st));
+    SYSML_TRY(ar_bucket(h, grads + OFF_F2, h->num_params - OFF_F2, h->ev_b2, st));
     // B2d: input frame (pad 2) position = stored output-frame position + 34
     SYSML_TRY(T.begin(6));
     TcSpfIO io;
@@ -936,7 +1109,7 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
     SYSML_TRY(conv_bwd_filter_dispatch(c2, a1in, h->dz2, grads + OFF_F2, grads + OFF_B2, h->ws,
                                        h->ws_bytes, st));
     SYSML_TRY(T.end());
-    SYSML_TRY(ar_bucket(h, grads + OFF_F2, NUM_PARAMS - OFF_F2, h->ev_b2, st));
+    SYSML_TRY(ar_bucket(h, grads + OFF_F2, h->num_params - OFF_F2, h->ev_b2, st));
     // B2d
     SYSML_TRY(T.begin(6));
     SYSML_TRY(conv_bwd_data_dispatch(c2, params + OFF_F2, h->dz2, h->da1, h->ws, h->ws_bytes, st));
@@ -1034,9 +1207,16 @@ sysml_status sysml_optimizer_update(const sysml_optimizer_desc *d, float *params
   return SYSML_OK;
 }
 
+// end of a training step: the dropout mask stream advances (device counter, graph-replayable)
+static sysml_status step_done(sysml_lenet *h, sysml_stream_t stream) {
+  if (!h->hidden) return SYSML_OK;
+  return launch_counter_inc(h->drop_step, (cudaStream_t)stream);
+}
+
 sysml_status sysml_lenet_step(sysml_lenet *h, float *params, float *grads, const sysml_input *x,
                               const int32_t *labels, int32_t n_local, int64_t n_global,
                               float lr, void *nccl_comm, float *loss_sum, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(h, "NULL handle");
   // overlapped bucketed allreduce unless SYSML_AR_OVERLAP=0 (read per call)
   const char *ov = getenv("SYSML_AR_OVERLAP");
   if (nccl_comm && !(ov && ov[0] == '0')) {
@@ -1044,7 +1224,8 @@ sysml_status sysml_lenet_step(sysml_lenet *h, float *params, float *grads, const
     const sysml_status r = sysml_lenet_fwd_bwd(h, params, x, labels, n_local, n_global, grads, loss_sum, stream);
     h->ar_comm = nullptr;
     SYSML_TRY(r);
-    return sysml_sgd_update(params, grads, NUM_PARAMS, lr, stream);
+    SYSML_TRY(sysml_sgd_update(params, grads, h->num_params, lr, stream));
+    return step_done(h, stream);
   }
   SYSML_TRY(sysml_lenet_fwd_bwd(h, params, x, labels, n_local, n_global, grads, loss_sum, stream));
   if (nccl_comm) {
@@ -1053,14 +1234,15 @@ sysml_status sysml_lenet_step(sysml_lenet *h, float *params, float *grads, const
       set_error("ncclAllReduce could not be resolved (libnccl.so.2 not loaded in this process)");
       return SYSML_ERR_NCCL;
     }
-    const int r = s.allreduce(grads, grads, (size_t)NUM_PARAMS, /*ncclFloat32*/ 7, /*ncclSum*/ 0,
+    const int r = s.allreduce(grads, grads, (size_t)h->num_params, /*ncclFloat32*/ 7, /*ncclSum*/ 0,
                               nccl_comm, (cudaStream_t)stream);
     if (r != 0) {
       set_error("ncclAllReduce failed: %s", s.errstr ? s.errstr(r) : "?");
       return SYSML_ERR_NCCL;
     }
   }
-  return sysml_sgd_update(params, grads, NUM_PARAMS, lr, stream);
+  SYSML_TRY(sysml_sgd_update(params, grads, h->num_params, lr, stream));
+  return step_done(h, stream);
 }
 
 sysml_status sysml_lenet_step_opt(sysml_lenet *h, float *params, float *grads, float *state,
@@ -1073,7 +1255,8 @@ sysml_status sysml_lenet_step_opt(sysml_lenet *h, float *params, float *grads, f
   const sysml_status r = sysml_lenet_fwd_bwd(h, params, x, labels, n_local, n_global, grads, loss_sum, stream);
   h->ar_comm = nullptr;
   SYSML_TRY(r);
-  return sysml_optimizer_update(d, params, grads, state, NUM_PARAMS, t, stream);
+  SYSML_TRY(sysml_optimizer_update(d, params, grads, state, h->num_params, t, stream));
+  return step_done(h, stream);
 }
 
 sysml_status sysml_lenet_step_host(sysml_lenet *h, float *params, float *grads,
