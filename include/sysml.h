@@ -150,6 +150,16 @@ SYSML_API sysml_status sysml_conv2d_bwd_data(const sysml_conv_desc *d, const flo
                                    float *dx, void *workspace, size_t workspace_bytes,
                                    sysml_stream_t stream);
 
+/* affine layer forward (S:236-243 affine_forward; P:48-49 NN library; the hidden layer of
+ * LeNet-512, NEXT-4): out[m][j] = sum_k x[m][k] * W[j][k] + b[j] (b nullable), then relu
+ * (R7) if relu != 0.  x: M x K, W: N x K (out features x in features), out: M x N, all
+ * row-major device fp32, 16-byte aligned.  math TF32: tcgen05 GEMM (TMA-fed, fused
+ * epilogue; N >= 16, K % 4 == 0); FP32: CUDA cores (relu needs N % 4 == 0).
+ * Errors: SYSML_ERR_ARG (dims < 1, NULL), SYSML_ERR_UNSUPPORTED (alignment, shape).    */
+SYSML_API sysml_status sysml_affine(int32_t M, int32_t N, int32_t K, const float *x, const float *W,
+                                    const float *b, int32_t relu, int32_t math, float *out,
+                                    sysml_stream_t stream);
+
 /* bias_add (P:132 broadcasting; reading R10): y[n, k*PQ + j] += bias[k], in place.
  * y: N x (K*PQ).                                                                  */
 SYSML_API sysml_status sysml_bias_add(int32_t N, int32_t K, int32_t PQ, float *y, const float *bias,

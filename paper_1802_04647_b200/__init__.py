@@ -47,7 +47,7 @@ EXPORTS = (
     "sysml_optimizer_state_floats", "sysml_optimizer_update", "sysml_lenet_step_opt",
     "sysml_lenet_step_host_pipelined", "sysml_decide_format",
     "sysml_lenet512_num_params", "sysml_lenet512_create", "sysml_lenet_set_dropout",
-    "sysml_lenet_get_dropout_step", "sysml_lenet_handle_num_params",
+    "sysml_lenet_get_dropout_step", "sysml_lenet_handle_num_params", "sysml_affine",
     "sysml_conv2d_csr_filter", "sysml_count_nonzeros", "sysml_dense_to_csr", "sysml_lenet_predict",
 )
 
@@ -197,6 +197,7 @@ def lib(build_if_missing: bool = False):
         "sysml_lenet_set_dropout": (c_i32, [vp, c_i64, c_i64, vp]),
         "sysml_lenet_get_dropout_step": (c_i32, [vp, ctypes.POINTER(c_i64)]),
         "sysml_lenet_handle_num_params": (c_i64, [vp]),
+        "sysml_affine": (c_i32, [c_i32, c_i32, c_i32, vp, vp, vp, c_i32, c_i32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -315,6 +316,19 @@ def sysml_conv2d_bwd_data(f, dy, d: ConvDesc, dx=None, workspace=None, stream=No
     _check(L.sysml_conv2d_bwd_data(ctypes.byref(d), _ptr(f, torch.float32, "f"), _ptr(dy, torch.float32, "dy"),
                                    _ptr(dx, torch.float32, "dx"), ws, wsb, _stream(stream)))
     return dx
+
+
+def sysml_affine(x, W, b=None, relu=False, math="tf32", out=None, stream=None):
+    """Affine layer forward (sysml_affine): out = x W^T + b (relu optional); x M x K, W N x K."""
+    torch = _torch()
+    M, K = x.shape
+    N = W.shape[0]
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    _check(lib().sysml_affine(int(M), int(N), int(K), _ptr(x, torch.float32, "x"), _ptr(W, torch.float32, "W"),
+                              _ptr(b, torch.float32, "b"), int(bool(relu)), _MATH[math],
+                              _ptr(out, torch.float32, "out"), _stream(stream)))
+    return out
 
 
 def sysml_bias_add(y, bias, N, K, PQ, stream=None):

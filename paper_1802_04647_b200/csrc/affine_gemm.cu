@@ -13,15 +13,16 @@
 //   bias/relu/dropout elementwise (FP32 path) and the pool2 routing of a materialised da2
 //   into the dz2 SPF planes (TF32 path).
 //
-// Warp roles of tc_gemm_kernel (192 threads): warp 0 = TMA producer, warp 1 = MMA issuer
-// (TMEM owner), warps 2-5 = epilogue (TMEM lane quadrant = warp % 4).  One output tile of
-// (128 * mtiles) x NB per CTA; K streamed through a 3-4 stage ring.
+// tc_gemm_kernel is persistent with two TMEM accumulators (the epilogue of one tile overlaps
+// the MMAs of the next); warp roles at the kernel.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
 #include "tma.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace sysml {
 
@@ -53,12 +54,13 @@ __device__ __forceinline__ uint32_t dropout_keep4(uint64_t e0, uint64_t seed, ui
 
 namespace {
 
-constexpr int G_KB = 32;  // K floats per stage = one 128-byte swizzled row
-constexpr int G_THREADS = 192;
+constexpr int G_KB = 32;        // K floats per stage = one 128-byte swizzled row
+constexpr int G_EPI_WARPS = 8;  // two per TMEM lane quadrant, each owning half the tile columns
+constexpr int G_THREADS = 64 + 32 * G_EPI_WARPS;
 
 struct GParams {
   int M, N, K;
-  int mtiles, NB, nN;
+  int NB, nN, tiles;
   int64_t ldc;
   float *C;
   GemmEpi e;
@@ -68,33 +70,41 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return ptx::make_desc(saddr, 16, 1024) | ((uint64_t)2 << 61);
 }
 
+// Persistent GEMM: CTA b takes output tiles b, b + grid, ... (128 x NB each, n fastest so
+// concurrently running CTAs share A rows in L2).  Warp 0 = TMA producer over a STAGES-deep
+// ring, warp 1 = MMA issuer into one of two TMEM accumulators (NB columns each), warps 2..9 =
+// epilogue, which drains tile t from one accumulator while the MMAs of tile t+1 fill the
+// other.  With the dropout epilogue, the epilogue threads draw the Philox mask bits of their
+// next tile (row m, 128 or fewer units: <= 4 words of keep bits) while they wait for its
+// accumulator -- the generator cost is hidden under the MMAs.
 template <int STAGES>
 __global__ void __launch_bounds__(G_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  const uint32_t a_bytes = (uint32_t)p.mtiles * 128 * 128;
+  const uint32_t a_bytes = 128 * 128;
   const uint32_t b_bytes = (uint32_t)p.NB * 128;
   const uint32_t stage_bytes = a_bytes + b_bytes;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * stage_bytes);
   uint64_t *empty = full + STAGES;
-  uint64_t *accf = empty + STAGES;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(accf + 1);
+  uint64_t *tfull = empty + STAGES;  // [2] accumulator ready (MMA commit)
+  uint64_t *tempty = tfull + 2;      // [2] accumulator drained (one arrive per epilogue warp)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int nt = blockIdx.x % p.nN, mt0 = blockIdx.x / p.nN;
-  const int m0 = mt0 * 128 * p.mtiles, n0 = nt * p.NB;
   const int kiters = (p.K + G_KB - 1) / G_KB;
-  const uint32_t ncols = p.mtiles * p.NB <= 32 ? 32 : p.mtiles * p.NB <= 64 ? 64
-                        : p.mtiles * p.NB <= 128 ? 128 : p.mtiles * p.NB <= 256 ? 256 : 512;
+  const uint32_t ncols = 2 * p.NB <= 64 ? 64 : 2 * p.NB <= 128 ? 128 : 2 * p.NB <= 256 ? 256 : 512;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(full + s, 1);
       ptx::mbar_init(empty + s, 1);
     }
-    ptx::mbar_init(accf, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(tfull + b, 1);
+      ptx::mbar_init(tempty + b, G_EPI_WARPS);
+    }
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
@@ -110,52 +120,80 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t ph = 0;
-      for (int it = 0; it < kiters; ++it) {
-        ptx::mbar_wait(empty + stage, ph ^ 1);
-        ptx::mbar_arrive_expect_tx(full + stage, stage_bytes);
-        const uint32_t A = sbase + stage * stage_bytes;
-        ptx::tma_load_2d(A, &tmA, it * G_KB, m0, ptx::smem_u32(full + stage));
-        ptx::tma_load_2d(A + a_bytes, &tmB, it * G_KB, n0, ptx::smem_u32(full + stage));
-        if (++stage == STAGES) { stage = 0; ph ^= 1; }
+      for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+        const int m0 = (t / p.nN) * 128, n0 = (t % p.nN) * p.NB;
+        for (int it = 0; it < kiters; ++it) {
+          ptx::mbar_wait(empty + stage, ph ^ 1);
+          ptx::mbar_arrive_expect_tx(full + stage, stage_bytes);
+          const uint32_t A = sbase + stage * stage_bytes;
+          ptx::tma_load_2d(A, &tmA, it * G_KB, m0, ptx::smem_u32(full + stage));
+          ptx::tma_load_2d(A + a_bytes, &tmB, it * G_KB, n0, ptx::smem_u32(full + stage));
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
     const uint32_t idesc = ptx::make_idesc_tf32(128, p.NB);
+    const uint64_t d0 = sw128_desc(sbase);
+    const uint64_t stage_d = stage_bytes >> 4, b_d = a_bytes >> 4;
     int stage = 0;
-    uint32_t ph = 0, acc = 0;
-    for (int it = 0; it < kiters; ++it) {
-      ptx::mbar_wait(full + stage, ph);
+    uint32_t ph = 0;
+    int buf = 0;
+    uint32_t tph = 0;  // bit b = phase of accumulator b
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      ptx::mbar_wait(tempty + buf, ((tph >> buf) & 1u) ^ 1u);  // the epilogue drained this accumulator
+      tph ^= 1u << buf;
       ptx::tc_fence_after();
-      const uint32_t A = sbase + stage * stage_bytes, B = A + a_bytes;
+      const uint32_t tacc = tmem + (uint32_t)(buf * p.NB);
+      uint32_t acc = 0;
+      for (int it = 0; it < kiters; ++it) {
+        ptx::mbar_wait(full + stage, ph);
+        ptx::tc_fence_after();
+        const uint64_t ad = d0 + (uint64_t)stage * stage_d;
 #pragma unroll
-      for (int kk = 0; kk < G_KB / 8; ++kk) {  // 8 floats = 32 bytes per MMA
-        const uint64_t bd = sw128_desc(B + kk * 32);
-        for (int mt = 0; mt < p.mtiles; ++mt) {
-          if (ptx::elect_one())
-            ptx::mma_tf32(tmem + mt * p.NB, sw128_desc(A + mt * 16384 + kk * 32), bd, idesc, acc);
+        for (int kk = 0; kk < G_KB / 8; ++kk) {  // 8 floats = 32 bytes = 2 descriptor units
+          if (ptx::elect_one()) ptx::mma_tf32(tacc, ad + 2 * kk, ad + b_d + 2 * kk, idesc, acc);
           __syncwarp();
+          acc = 1;
         }
-        acc = 1;
+        if (ptx::elect_one()) ptx::mma_commit(empty + stage);
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; ph ^= 1; }
       }
-      if (ptx::elect_one()) ptx::mma_commit(empty + stage);
+      if (ptx::elect_one()) ptx::mma_commit(tfull + buf);
       __syncwarp();
-      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+      buf ^= 1;
     }
-    if (ptx::elect_one()) ptx::mma_commit(accf);
-    __syncwarp();
   } else {
-    const int qd = warp & 3;
-    if (kiters > 0) ptx::mbar_wait_sleep(accf, 0);
-    ptx::tc_fence_after();
+    const int ew = warp - 2, qd = warp & 3, half = ew >> 2;  // lane quadrant, column half
     const GemmEpi &e = p.e;
-    uint64_t step = 0;
-    if (e.dropout) step = *e.step;
-    for (int mt = 0; mt < p.mtiles; ++mt) {
-      const int m = m0 + mt * 128 + qd * 32 + lane;
-      for (int cb = 0; cb < p.NB; cb += 16) {
+    const uint64_t step = e.dropout ? *e.step : 0;
+    const int hc = p.NB / 2;  // columns per epilogue warp (multiple of 16 when NB % 32 == 0)
+    int buf = 0;
+    uint32_t tph = 0;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      const int m = (t / p.nN) * 128 + qd * 32 + lane;
+      const int cbase = (t % p.nN) * p.NB + half * hc;
+      // keep bits of this thread's row and column range, drawn while the MMAs run
+      // (hc <= 128 columns -> 4 words, kept in scalars so nothing goes to local memory)
+      uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0;
+      if (e.dropout && m < p.M) {
+        const uint64_t e0 = (uint64_t)(e.row0 + m) * (uint64_t)e.units;
+#pragma unroll 1
+        for (int c4 = 0; c4 < hc && cbase + c4 < p.N; c4 += 4) {
+          const uint32_t b = dropout_keep4(e0 + (uint64_t)(cbase + c4), e.seed, step, e.keep_T) << (c4 & 31);
+          const int w = c4 >> 5;
+          k0 |= w == 0 ? b : 0u; k1 |= w == 1 ? b : 0u; k2 |= w == 2 ? b : 0u; k3 |= w == 3 ? b : 0u;
+        }
+      }
+      ptx::mbar_wait_sleep(tfull + buf, (tph >> buf) & 1u);
+      tph ^= 1u << buf;
+      ptx::tc_fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(buf * p.NB + half * hc);
+      for (int cb = 0; cb < hc; cb += 16) {
         float v[16];
-        ptx::tmem_ld16(tmem + ((uint32_t)(qd * 32) << 16) + mt * p.NB + cb, v);
-        const int c = n0 + cb;
+        ptx::tmem_ld16(tbase + (uint32_t)cb, v);
+        const int c = cbase + cb;
         __syncwarp();
         if (m < p.M && c < p.N) {
           if (kiters == 0) {
@@ -170,15 +208,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = v[j] > 0.f ? v[j] : 0.f;  // R7: +0.0
           }
-          if (e.dropout) {  // inverted dropout, unit c + j of global row row0 + m (R23, R24)
-            const uint64_t e0 = (uint64_t)(e.row0 + m) * (uint64_t)e.units + (uint64_t)c;
+          if (e.dropout) {  // inverted dropout (R23, R24)
+            const int w = cb >> 5;
+            const uint32_t kb = (w == 0 ? k0 : w == 1 ? k1 : w == 2 ? k2 : k3) >> (cb & 31);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint32_t keep = dropout_keep4(e0 + 4 * q, e.seed, step, e.keep_T);
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                v[4 * q + j] = (keep >> j) & 1u ? __fdiv_rn(v[4 * q + j], e.keep_p) : 0.f;
-            }
+            for (int j = 0; j < 16; ++j) v[j] = (kb >> j) & 1u ? __fdiv_rn(v[j], e.keep_p) : 0.f;
           }
           float *dst = p.C + (int64_t)m * p.ldc + c;
           if (c + 16 <= p.N && (p.ldc & 3) == 0) {
@@ -192,6 +226,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           }
         }
       }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(tempty + buf);
+      buf ^= 1;
     }
   }
   ptx::tc_fence_before();
@@ -203,26 +241,27 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 }
 
 struct GPlan {
-  int mtiles, NB, nN, nM, stages;
+  int NB, nN, nM, stages, grid;
   size_t smem;
 };
 
 GPlan plan_gemm(int M, int N) {
-  // the largest tile that still puts a CTA on (nearly) every SM; 256 x 256 tiles halve the
-  // shared-memory operand traffic per FLOP of 128 x 128 ones
-  const int sms = sm_count();
-  const int cand[3][2] = {{2, 256}, {1, 256}, {1, 128}};
-  GPlan best{};
-  for (auto &cd : cand) {
-    const int mt = cd[0], nb = std::min(cd[1], (int)ceil_div(N, 16) * 16);
-    const int64_t tiles = ceil_div(M, 128 * mt) * ceil_div(N, nb);
-    best = GPlan{mt, nb, (int)ceil_div(N, nb), (int)ceil_div(M, 128 * mt), 0, 0};
-    if (tiles >= (int64_t)(0.85 * sms)) break;
-  }
-  const size_t stage = (size_t)best.mtiles * 128 * 128 + (size_t)best.NB * 128;
-  best.stages = stage * 4 + 2048 <= 200 * 1024 ? 4 : 3;
-  best.smem = 1024 + best.stages * stage + 8 * (2 * best.stages + 1) + 16;
-  return best;
+  // 128 x NB tiles, NB <= 256 (two NB-column accumulators fill TMEM), persistent grid
+  GPlan pl{};
+  static const char *nb_env = getenv("SYSML_GEMM_NB");  // A/B measurement
+  int nb = 256;
+  if (nb_env && atoi(nb_env) >= 32 && atoi(nb_env) <= 256) nb = atoi(nb_env) / 32 * 32;
+  nb = std::min(nb, (int)ceil_div(N, 32) * 32);
+  pl.NB = nb;
+  pl.nN = (int)ceil_div(N, nb);
+  pl.nM = (int)ceil_div(M, 128);
+  pl.grid = (int)std::min<int64_t>((int64_t)pl.nN * pl.nM, sm_count());
+  const size_t stage = (size_t)128 * 128 + (size_t)nb * 128;
+  static const int stages_env = getenv("SYSML_GEMM_STAGES") ? atoi(getenv("SYSML_GEMM_STAGES")) : 0;
+  pl.stages = stage * 4 + 2048 <= 200 * 1024 ? 4 : 3;
+  if (stages_env >= 2 && stages_env <= 4 && stage * stages_env + 2048 <= 220 * 1024) pl.stages = stages_env;
+  pl.smem = 1024 + pl.stages * stage + 8 * (2 * pl.stages + 4) + 16;
+  return pl;
 }
 
 }  // namespace
@@ -249,12 +288,12 @@ sysml_status tc_gemm(int M, int N, int K, const float *A, int64_t lda, const flo
     return SYSML_ERR_UNSUPPORTED;
   }
   const GPlan pl = plan_gemm(M, N);
-  GParams p{M, N, K, pl.mtiles, pl.NB, pl.nN, ldc, C, e};
+  GParams p{M, N, K, pl.NB, pl.nN, pl.nN * pl.nM, ldc, C, e};
   CUtensorMap tmA, tmB;
   {
     const uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
     const uint64_t strides[1] = {(uint64_t)lda * 4};
-    const uint32_t box[2] = {G_KB, (uint32_t)(128 * pl.mtiles)};
+    const uint32_t box[2] = {G_KB, 128};
     if (!tmap_encode_f32(&tmA, A, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return SYSML_ERR_CUDA;
   }
   {
@@ -263,15 +302,17 @@ sysml_status tc_gemm(int M, int N, int K, const float *A, int64_t lda, const flo
     const uint32_t box[2] = {G_KB, (uint32_t)pl.NB};
     if (!tmap_encode_f32(&tmB, B, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return SYSML_ERR_CUDA;
   }
-  const int grid = pl.nM * pl.nN;
-  route_note("tc_gemm_kernel [TMA + tcgen05 TF32, %dx%d tiles, %d CTAs%s]", 128 * pl.mtiles, pl.NB, grid,
-             e.dropout ? ", bias+relu+dropout epilogue" : "");
+  route_note("tc_gemm_kernel [TMA + tcgen05 TF32, persistent, 128x%d tiles x %d on %d CTAs%s]", pl.NB,
+             p.tiles, pl.grid, e.dropout ? ", bias+relu+dropout epilogue" : "");
   if (pl.stages == 4) {
     SYSML_TRY(smem_attr(tc_gemm_kernel<4>, pl.smem));
-    tc_gemm_kernel<4><<<grid, G_THREADS, pl.smem, st>>>(tmA, tmB, p);
+    tc_gemm_kernel<4><<<pl.grid, G_THREADS, pl.smem, st>>>(tmA, tmB, p);
+  } else if (pl.stages == 2) {
+    SYSML_TRY(smem_attr(tc_gemm_kernel<2>, pl.smem));
+    tc_gemm_kernel<2><<<pl.grid, G_THREADS, pl.smem, st>>>(tmA, tmB, p);
   } else {
     SYSML_TRY(smem_attr(tc_gemm_kernel<3>, pl.smem));
-    tc_gemm_kernel<3><<<grid, G_THREADS, pl.smem, st>>>(tmA, tmB, p);
+    tc_gemm_kernel<3><<<pl.grid, G_THREADS, pl.smem, st>>>(tmA, tmB, p);
   }
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;

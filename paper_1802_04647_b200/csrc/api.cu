@@ -331,6 +331,41 @@ sysml_status sysml_conv2d_bwd_data(const sysml_conv_desc *d, const float *f, con
   return conv_bwd_data_dispatch(*d, f, dy, dx, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
+sysml_status sysml_affine(int32_t M, int32_t N, int32_t K, const float *x, const float *W,
+                          const float *b, int32_t relu, int32_t math, float *out, sysml_stream_t stream) {
+  SYSML_CHECK_ARG(M >= 1 && N >= 1 && K >= 1, "affine dims must be >= 1 (M=%d N=%d K=%d)", M, N, K);
+  SYSML_CHECK_ARG(x && W && out, "NULL pointer");
+  SYSML_CHECK_ARG(math == SYSML_MATH_FP32 || math == SYSML_MATH_TF32, "bad math %d", math);
+  SYSML_CHECK_ALIGN16(x, "x");
+  SYSML_CHECK_ALIGN16(W, "W");
+  SYSML_CHECK_ALIGN16(b, "b");
+  SYSML_CHECK_ALIGN16(out, "out");
+  cudaStream_t st = (cudaStream_t)stream;
+  route_reset();
+  if (math == SYSML_MATH_TF32) {
+    if (!tc_gemm_supported(M, N, K, K, K)) {
+      set_error("affine TF32: unsupported shape M=%d N=%d K=%d (needs N >= 16, K %% 4 == 0)", M, N, K);
+      return SYSML_ERR_UNSUPPORTED;
+    }
+    GemmEpi e;
+    e.bias = b;
+    e.relu = relu ? 1 : 0;
+    return tc_gemm(M, N, K, x, K, W, K, out, N, e, st);
+  }
+  // FP32: the 1x1 convolution of M one-pixel images with K channels and N filters
+  const ConvArgs a{M, K, 1, 1, N, 1, 1, 1, 1, 0, 0, 1, 1};
+  route_note("igemm_kernel<FwdOp> [FP32 CUDA cores, affine as 1x1 conv]");
+  SYSML_TRY(simt_conv_fwd(a, x, W, b, out, st));
+  if (relu) {
+    if ((N & 3) != 0) {
+      set_error("affine FP32 relu epilogue needs N %% 4 == 0 (N=%d)", N);
+      return SYSML_ERR_UNSUPPORTED;
+    }
+    SYSML_TRY(launch_relu_dropout(out, M, N, 0, 0, nullptr, 0, 1.f, 0, st));
+  }
+  return SYSML_OK;
+}
+
 sysml_status sysml_bias_add(int32_t N, int32_t K, int32_t PQ, float *y, const float *bias,
                             sysml_stream_t stream) {
   SYSML_CHECK_ARG(N >= 1 && K >= 1 && PQ >= 1, "bias_add dims must be >= 1 (N=%d K=%d PQ=%d)", N,

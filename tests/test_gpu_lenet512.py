@@ -194,3 +194,18 @@ def test_lenet512_tf32_multi_tile_batch(S):
     g, loss, _ = _run_fwd_bwd(S, x, y, prm, "tf32", 512, keep, seed, step, row0=1000)
     _check_blocks(g, g_ref, TOL["tf32"], "n=300")
     assert abs(loss - loss_ref) <= TOL["tf32"] * abs(loss_ref)
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("M,N,K,relu", [(37, 512, 3136, True), (300, 40, 20, False), (5, 16, 4, True),
+                                        (129, 3136, 512, False)])
+def test_affine_vs_oracle_definition(S, math, M, N, K, relu):
+    # out = x W^T + b, relu (R7); the oracle's definition is the fp64 matmul
+    x = synth.uniform((M, K), seed=(780, M)).astype(np.float32)
+    W = synth.uniform((N, K), seed=(781, N)).astype(np.float32)
+    b = synth.uniform((N,), seed=(782, K)).astype(np.float32)
+    ref = x.astype(np.float64) @ W.astype(np.float64).T + b
+    if relu:
+        ref = np.maximum(ref, 0.0)
+    out = S.sysml_affine(dev(x), dev(W), dev(b), relu=relu, math=math)
+    assert_close(host(out), ref, TOL[math], f"affine {math} {M}x{N}x{K}")
