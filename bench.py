@@ -535,9 +535,56 @@ def layer_section(S, peaks, quick=False):
         res[op] = {"ms": round(med, 4), "gbs": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 4),
                    "route": S.sysml_last_route()}
     out[f"csr_lenet_conv1_N{N}"] = res
+    out["horizontal_fusion"] = horizontal_section(S, flush, reps)
     out["peak_note"] = ("frac_tf32_peak: of the burst TF32 denominator (measured bf16 x 0.5 = %.1f TFLOP/s); "
                         "frac_tf32_cublas: of cuBLAS TF32 measured live; frac_hbm: of measured HBM copy %.1f GB/s"
                         % (tf32_peak, peaks["hbm"]))
+    return out
+
+
+def horizontal_section(S, flush, reps):
+    """NEXT-2 horizontal fusion: the ResNet bottleneck's conv1 and projection
+    shortcut over one input, as two separate convs vs one call over the stacked bank."""
+    import torch
+    import synth
+    out = {}
+    for name, (N, C, H, W, ks, st) in {
+        "resnet50_stage1_block1_conv1_64+proj_256_56x56_N128": (128, 64, 56, 56, (64, 256), 1),
+        "resnet50v1_stage2_block1_conv1_128+proj_512_s2_56x56_N128": (128, 256, 56, 56, (128, 512), 2),
+    }.items():
+        P = (H - 1) // st + 1
+        K = sum(ks)
+        x = torch.from_numpy(synth.conv_problem_U(N, C, H, W, 1, 1, 1, P, P, seed=(1010,))[0]).cuda()
+        fs = [torch.from_numpy(synth.normal((k, C), (2.0 / C) ** 0.5, seed=(1011, k))).cuda() for k in ks]
+        dys = [torch.from_numpy(synth.normal((N, k * P * P), seed=(1012, k))).cuda() for k in ks]
+        dy_cat = torch.cat([dy.view(N, k, -1) for dy, k in zip(dys, ks)], 1).view(N, -1).contiguous()
+        ds = [S.conv_desc(N, C, H, W, k, 1, 1, st, 0, "tf32") for k in ks]
+        d = S.conv_desc(N, C, H, W, K, 1, 1, st, 0, "tf32")
+        ws = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+        ys = [torch.empty(N, k * P * P, device="cuda") for k in ks]
+        y_cat = torch.empty(N, K * P * P, device="cuda")
+        dx = torch.empty(N, C * H * W, device="cuda")
+        dfs = [torch.empty(k, C, device="cuda") for k in ks]
+        res = {"x_MB": round(4 * x.numel() / 1e6, 1)}
+        sep = {
+            "fwd": lambda: [S.sysml_conv2d(x, f, dd, out=y, workspace=ws) for f, dd, y in zip(fs, ds, ys)],
+            "bwd_data": lambda: [S.sysml_conv2d_bwd_data(f, dy, dd, dx=dx, workspace=ws) for f, dy, dd in zip(fs, dys, ds)],
+            "bwd_filter": lambda: [S.sysml_conv2d_bwd_filter(x, dy, dd, df=df, workspace=ws)
+                                   for dy, dd, df in zip(dys, ds, dfs)],
+        }
+        fus = {
+            "fwd": lambda: S.sysml_conv2d_multi(x, fs, d, out=y_cat, workspace=ws),
+            "bwd_data": lambda: S.sysml_conv2d_multi_bwd_data(fs, dy_cat, d, dx=dx, workspace=ws),
+            "bwd_filter": lambda: S.sysml_conv2d_multi_bwd_filter(x, dy_cat, d, ks, want_db=False, workspace=ws),
+        }
+        for op in ("fwd", "bwd_data", "bwd_filter"):
+            ms_sep, _ = time_op(sep[op], reps, flush)
+            ms_fus, _ = time_op(fus[op], reps, flush)
+            res[op] = {"separate_ms": round(ms_sep, 4), "fused_ms": round(ms_fus, 4),
+                       "speedup": round(ms_sep / ms_fus, 3), "route": S.sysml_last_route()}
+        res["note"] = ("separate bwd_data = the two adjoints alone (their sum, which the fused call "
+                       "returns, is not included)")
+        out[name] = res
     return out
 
 

@@ -150,6 +150,40 @@ SYSML_API sysml_status sysml_conv2d_bwd_data(const sysml_conv_desc *d, const flo
                                    float *dx, void *workspace, size_t workspace_bytes,
                                    sysml_stream_t stream);
 
+/* Horizontal fusion for shared inputs (NEXT-2; "horizontal fusion for shared
+ * inputs (e.g. reuse temporary im2col intermediates in presence of multiple convolution
+ * operators consuming the same input)").  n_ops (1..8) convolutions with ONE geometry
+ * (d's N, C, H, W, R, S, stride, pad, math) read the same input x; op i has k_counts[i]
+ * filters f[i] (k_counts[i] x C*R*S, device) and d->K must equal sum(k_counts).  They run
+ * as one convolution over the stacked bank [f[0]; f[1]; ...], so the staged input feeds
+ * every op and x is read once:
+ *   sysml_conv2d_multi           y_cat = N x (K*P*Q): op i's output channels are the slice
+ *                                [k_0 + ... + k_{i-1}, ... + k_i) of each row (channel
+ *                                concatenation); bias[i] nullable (bias itself nullable).
+ *   sysml_conv2d_multi_bwd_data  dx = sum_i conv2d_bwd_data(f[i], dy_i), dy_cat laid out as
+ *                                y_cat (the input gradient of all consumers of x, summed).
+ *   sysml_conv2d_multi_bwd_filter df[i] (k_i x CRS) and db[i] (nullable) of each op from
+ *                                x and dy_cat.
+ * Workspace: sysml_conv2d_multi_workspace_size(d, n_ops, k_counts, op = 0 fwd / 1 bwd_data /
+ * 2 bwd_filter, is_csr).  Errors: SYSML_ERR_ARG (n_ops, k_counts, NULL), SYSML_ERR_SHAPE
+ * (d->K != sum k_counts), otherwise as the single-op calls.                              */
+SYSML_API sysml_status sysml_conv2d_multi_workspace_size(const sysml_conv_desc *d, int32_t n_ops,
+                                                         const int32_t *k_counts, int32_t op,
+                                                         int32_t is_csr, size_t *bytes);
+SYSML_API sysml_status sysml_conv2d_multi(const sysml_conv_desc *d, int32_t n_ops, const int32_t *k_counts,
+                                          const sysml_input *x, const float *const *f,
+                                          const float *const *bias, float *y_cat, void *workspace,
+                                          size_t workspace_bytes, sysml_stream_t stream);
+SYSML_API sysml_status sysml_conv2d_multi_bwd_data(const sysml_conv_desc *d, int32_t n_ops,
+                                                   const int32_t *k_counts, const float *const *f,
+                                                   const float *dy_cat, float *dx, void *workspace,
+                                                   size_t workspace_bytes, sysml_stream_t stream);
+SYSML_API sysml_status sysml_conv2d_multi_bwd_filter(const sysml_conv_desc *d, int32_t n_ops,
+                                                     const int32_t *k_counts, const sysml_input *x,
+                                                     const float *dy_cat, float *const *df,
+                                                     float *const *db, void *workspace,
+                                                     size_t workspace_bytes, sysml_stream_t stream);
+
 /* affine layer forward (S:236-243 affine_forward; P:48-49 NN library; the hidden layer of
  * LeNet-512, NEXT-4): out[m][j] = sum_k x[m][k] * W[j][k] + b[j] (b nullable), then relu
  * (R7) if relu != 0.  x: M x K, W: N x K (out features x in features), out: M x N, all

@@ -48,6 +48,8 @@ EXPORTS = (
     "sysml_lenet_step_host_pipelined", "sysml_decide_format",
     "sysml_lenet512_num_params", "sysml_lenet512_create", "sysml_lenet_set_dropout",
     "sysml_lenet_get_dropout_step", "sysml_lenet_handle_num_params", "sysml_affine",
+    "sysml_conv2d_multi_workspace_size", "sysml_conv2d_multi", "sysml_conv2d_multi_bwd_data",
+    "sysml_conv2d_multi_bwd_filter",
     "sysml_conv2d_csr_filter", "sysml_count_nonzeros", "sysml_dense_to_csr", "sysml_lenet_predict",
 )
 
@@ -198,6 +200,10 @@ def lib(build_if_missing: bool = False):
         "sysml_lenet_get_dropout_step": (c_i32, [vp, ctypes.POINTER(c_i64)]),
         "sysml_lenet_handle_num_params": (c_i64, [vp]),
         "sysml_affine": (c_i32, [c_i32, c_i32, c_i32, vp, vp, vp, c_i32, c_i32, vp, vp]),
+        "sysml_conv2d_multi_workspace_size": (c_i32, [CD, c_i32, vp, c_i32, c_i32, psz]),
+        "sysml_conv2d_multi": (c_i32, [CD, c_i32, vp, IN, vp, vp, vp, vp, sz, vp]),
+        "sysml_conv2d_multi_bwd_data": (c_i32, [CD, c_i32, vp, vp, vp, vp, vp, sz, vp]),
+        "sysml_conv2d_multi_bwd_filter": (c_i32, [CD, c_i32, vp, IN, vp, vp, vp, vp, sz, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -316,6 +322,66 @@ def sysml_conv2d_bwd_data(f, dy, d: ConvDesc, dx=None, workspace=None, stream=No
     _check(L.sysml_conv2d_bwd_data(ctypes.byref(d), _ptr(f, torch.float32, "f"), _ptr(dy, torch.float32, "dy"),
                                    _ptr(dx, torch.float32, "dx"), ws, wsb, _stream(stream)))
     return dx
+
+
+def _ptr_array(ts, torch, what):
+    arr = (ctypes.c_void_p * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = _ptr(t, torch.float32, f"{what}[{i}]") if t is not None else None
+    return arr
+
+
+def _multi_setup(d: ConvDesc, ks, op, is_csr, workspace, stream):
+    L = lib()
+    kc = (ctypes.c_int32 * len(ks))(*[int(k) for k in ks])
+    nb = ctypes.c_size_t(0)
+    _check(L.sysml_conv2d_multi_workspace_size(ctypes.byref(d), len(ks), kc, op, int(is_csr), ctypes.byref(nb)))
+    ws, wsb = _workspace(nb.value, workspace, stream)
+    return L, kc, ws, wsb
+
+
+def sysml_conv2d_multi(x, fs, d: ConvDesc, biases=None, out=None, workspace=None, stream=None):
+    """Horizontal fusion: the convs with filter banks fs (k_i x CRS) over the shared
+    input x, as one conv; returns y_cat N x (sum k_i * P * Q) (channel concatenation)."""
+    torch = _torch()
+    ks = [f.shape[0] for f in fs]
+    inp = _input(x)
+    if out is None:
+        out = torch.empty((d.N, d.K * d.P * d.Q), dtype=torch.float32, device="cuda")
+    L, kc, ws, wsb = _multi_setup(d, ks, 0, isinstance(x, CSR), workspace, stream)
+    fa = _ptr_array(fs, torch, "f")
+    ba = _ptr_array(biases, torch, "bias") if biases is not None else None
+    _check(L.sysml_conv2d_multi(ctypes.byref(d), len(ks), kc, ctypes.byref(inp), fa, ba,
+                                _ptr(out, torch.float32, "y_cat"), ws, wsb, _stream(stream)))
+    return out
+
+
+def sysml_conv2d_multi_bwd_data(fs, dy_cat, d: ConvDesc, dx=None, workspace=None, stream=None):
+    """sum_i conv2d_bwd_data(fs[i], dy_i) in one kernel (dy_cat: channel concatenation)."""
+    torch = _torch()
+    ks = [f.shape[0] for f in fs]
+    if dx is None:
+        dx = torch.empty((d.N, d.C * d.H * d.W), dtype=torch.float32, device="cuda")
+    L, kc, ws, wsb = _multi_setup(d, ks, 1, False, workspace, stream)
+    _check(L.sysml_conv2d_multi_bwd_data(ctypes.byref(d), len(ks), kc, _ptr_array(fs, torch, "f"),
+                                         _ptr(dy_cat, torch.float32, "dy_cat"), _ptr(dx, torch.float32, "dx"),
+                                         ws, wsb, _stream(stream)))
+    return dx
+
+
+def sysml_conv2d_multi_bwd_filter(x, dy_cat, d: ConvDesc, ks, want_db=True, workspace=None, stream=None):
+    """Per-op (df_i, db_i) of the horizontally fused convs from x and dy_cat."""
+    torch = _torch()
+    inp = _input(x)
+    crs = d.C * d.R * d.S
+    dfs = [torch.empty((k, crs), dtype=torch.float32, device="cuda") for k in ks]
+    dbs = [torch.empty((k,), dtype=torch.float32, device="cuda") for k in ks] if want_db else None
+    L, kc, ws, wsb = _multi_setup(d, ks, 2, isinstance(x, CSR), workspace, stream)
+    _check(L.sysml_conv2d_multi_bwd_filter(ctypes.byref(d), len(ks), kc, ctypes.byref(inp),
+                                           _ptr(dy_cat, torch.float32, "dy_cat"), _ptr_array(dfs, torch, "df"),
+                                           _ptr_array(dbs, torch, "db") if want_db else None, ws, wsb,
+                                           _stream(stream)))
+    return dfs, dbs
 
 
 def sysml_affine(x, W, b=None, relu=False, math="tf32", out=None, stream=None):

@@ -1210,8 +1210,12 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
     p.NFpad = std::max(16, round_up(K, 16));
     p.nft = 1;
   } else {
-    p.NFpad = 256;
+    // K > 256: 256-wide filter tiles.  SYSML_TC_BALANCE_NF=1 balances the widths instead
+    // (K = 320 -> 2 x 160): measured on the horizontally fused bottleneck convs, 320 filters
+    // 239 -> 198 us but 640 filters 247 -> 316 us (the 224-wide tiles drop to MT = 1)
+    static const int bal_env = getenv("SYSML_TC_BALANCE_NF") ? atoi(getenv("SYSML_TC_BALANCE_NF")) : 0;
     p.nft = (K + 255) / 256;
+    p.NFpad = bal_env ? round_up((K + p.nft - 1) / p.nft, 16) : 256;
   }
   p.ks = (allow_ks && C == 1 && S <= 8) ? 1 : 0;
   // SN: narrow filter banks (N = NFpad <= 64 keeps the MMA SMEM-operand bound) fold
