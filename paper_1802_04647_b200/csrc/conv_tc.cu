@@ -121,7 +121,9 @@ struct TcFwdParams {
   int cl2;             // CTA-pair cluster: each CTA bulk-loads half of every filter chunk and
                        // multicasts it to both (halves the L2 -> SMEM filter stream)
   int64_t iters;       // tile iterations per CTA (cl2: equal in both CTAs, padded with empty tiles)
-  int abulk;          // 1x1 / pad 0 / NCHW input: each chunk's 8 channel rows are staged MN-major
+  int abulk;          // 1: 1x1 / pad 0 / NCHW input, 2: SPF input (any R, S): each chunk's 8
+                      // channel rows are staged MN-major by 16-byte copies, then transposed
+  int stg_row;        // floats per staged channel row (HALO; HALO + 4 for SPF: unaligned start)
                        //   ([8][HALO], 16-byte cp.async) behind the stage and transposed to the
                        //   K-major A operand by the producer threads
   int sk;              // stream-K: CTA b runs the global chunk iterations [b*I/G, (b+1)*I/G),
@@ -750,20 +752,32 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         // of consecutive positions, 16-byte row writes: conflict-free), fence generic ->
         // async proxy (their own stores only: a fence behind in-flight cp.async of the same
         // thread would wait for them), and arrive on the stage's full barrier.
-        const int ngrp = p.HALO / 4;
+        // SPF input (abulk 2): the halo of every channel is the contiguous run of stored
+        // positions [g0 + in_shift, + HALO) of its plane; it is staged from the 16-byte
+        // aligned position below it, and the transposers skip the first `dl` floats
+        const int64_t s0 = p.abulk == 2 ? g0 + p.in_shift : 0;
+        const int dl = p.abulk == 2 ? (int)(((s0 % 4) + 4) % 4) : 0;
+        const int ngrp = (p.HALO + dl + 3) / 4;
+        const int ROW = p.stg_row;
         if (tid < 64) {
           // per-segment group offsets n*C*HW + hw (int: N*C*H*W < 2^31, plan), -1 past G
           ptx::named_bar_sync(5, 64);  // the previous segment's copies have read the table
           for (int gq = tid; gq < ngrp; gq += 64) {
-            const int64_t g = g0 + 4 * gq;
             int off = -1;
-            if (g < p.G) {
-              const int64_t n = g / HW;
-              off = (int)(n * p.C * HW + (g - n * HW));
+            if (p.abulk == 2) {
+              const int64_t sp = s0 - dl + 4 * gq;  // planes hold whole 4-position groups
+              if (sp >= 0 && sp + 4 <= p.in_plane) off = (int)sp;
+            } else {
+              const int64_t g = g0 + 4 * gq;
+              if (g < p.G) {
+                const int64_t n = g / HW;
+                off = (int)(n * p.C * HW + (g - n * HW));
+              }
             }
             src_off[gq] = off;
           }
           ptx::named_bar_sync(5, 64);
+          const int64_t cstr = p.abulk == 2 ? p.in_plane : (int64_t)HW;
           for (int ch = c0; ch < c1; ++ch) {
             ptx::mbar_wait(empty + ist, iph ^ 1);
             uint8_t *A = stage_base + (size_t)ist * p.stage_bytes;
@@ -774,17 +788,17 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
               ptx::bulk_g2s(B, p.fp + ((size_t)ft * p.nchunk + ch) * (p.b_bytes / 4), p.b_bytes, full + ist);
             }
             const int cc0 = ch * 8, nc = min(8, p.C - cc0);
-            const float *xc = p.x + (int64_t)cc0 * HW;
+            const float *xc = p.x + (int64_t)cc0 * cstr;
             // item = (channel half jh, group gq): four channel rows share offset and address
             for (int base = tid; base < 2 * ngrp; base += 64) {
               const int jh = base >= ngrp ? 1 : 0, gq = base - jh * ngrp;
               const int off = src_off[gq];
-              const uint32_t dst = stg + (uint32_t)(4 * jh * p.HALO + 4 * gq) * 4;
-              const float *src = xc + off + (int64_t)(4 * jh) * HW;
+              const uint32_t dst = stg + (uint32_t)(4 * jh * ROW + 4 * gq) * 4;
+              const float *src = xc + off + (int64_t)(4 * jh) * cstr;
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj) {
                 const bool ok = off >= 0 && 4 * jh + jj < nc;
-                ptx::cp_async16(dst + (uint32_t)(jj * p.HALO) * 4, ok ? src + (int64_t)jj * HW : p.x, ok ? 16u : 0u);
+                ptx::cp_async16(dst + (uint32_t)(jj * ROW) * 4, ok ? src + (int64_t)jj * cstr : p.x, ok ? 16u : 0u);
               }
             }
             ptx::cp_async_mbar_arrive(staged + ist);
@@ -799,9 +813,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
             const uint32_t a0 = ptx::smem_u32(A);
             for (int it = tt; it < 2 * p.HALO; it += 64) {
               const int q = it >= p.HALO ? 1 : 0, pos = it - q * p.HALO;
-              st_shared_v4(a0 + (uint32_t)(q * p.HALO + pos) * 16, stg[(4 * q) * p.HALO + pos],
-                           stg[(4 * q + 1) * p.HALO + pos], stg[(4 * q + 2) * p.HALO + pos],
-                           stg[(4 * q + 3) * p.HALO + pos]);
+              const float *sr = stg + (4 * q) * ROW + pos + dl;
+              st_shared_v4(a0 + (uint32_t)(q * p.HALO + pos) * 16, sr[0], sr[ROW], sr[2 * ROW], sr[3 * ROW]);
             }
             ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(full + stage);
@@ -1173,7 +1186,7 @@ int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 // Plan the forward kernel for a stride-1 conv: input (N,C,H,W), K output channels.
 TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
-                const PoolArgs *pool, bool allow_ks = true, int sh = 1, int sw = 1) {
+                const PoolArgs *pool, bool allow_ks = true, int sh = 1, int sw = 1, int spf_in = 0) {
   TcPlan pl{};
   TcFwdParams &p = pl.p;
   p.N = N; p.C = C; p.H = H; p.W = W; p.K = K; p.R = R; p.S = S; p.ph = ph; p.pw = pw;
@@ -1206,6 +1219,13 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
   static const int abulk_env = getenv("SYSML_TC_ABULK") ? atoi(getenv("SYSML_TC_ABULK")) : -1;
   p.abulk = (abulk_env != 0 && !pool && R == 1 && S == 1 && ph == 0 && pw == 0 && !strided &&
              ((int64_t)H * W) % 4 == 0 && C > 1 && (int64_t)N * C * H * W < (1ll << 31)) ? 1 : 0;
+  // SPF input (LeNet-internal planes, zeros stored): every channel's halo is one contiguous
+  // run, so the staged 16-byte producer applies to any R, S.  Opt-in (SYSML_TC_SPF_STAGE=1):
+  // measured on the LeNet step (r02) B2d 1011K -> 982K and F2 808K -> 788K cycles per CTA, but
+  // the step 1879 -> 1910 us -- the producers were not the limit (the MMA loop is, mma_wait_full
+  // is 9% of B2d) and the staging buffer costs pipeline stages.
+  static const int spf_stage_env = getenv("SYSML_TC_SPF_STAGE") ? atoi(getenv("SYSML_TC_SPF_STAGE")) : 0;
+  if (spf_in && spf_stage_env != 0 && abulk_env != 0 && !strided && C > 1) p.abulk = 2;
   if (K <= 256) {
     p.NFpad = std::max(16, round_up(K, 16));
     p.nft = 1;
@@ -1284,7 +1304,8 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
       }
       if (attempt == 0 && mt > 1 && ntiles < nsm && !single) continue;  // keep the SMs busy first
       const uint32_t a_bytes = (uint32_t)(2 * halo * 16);
-      const uint32_t stage = a_bytes + p.b_bytes + (p.abulk ? (uint32_t)(8 * halo * 4) : 0u);
+      const int stg_row = halo + (p.abulk == 2 ? 4 : 0);
+      const uint32_t stage = a_bytes + p.b_bytes + (p.abulk ? (uint32_t)(8 * stg_row * 4) : 0u);
       p.bias_smem = K <= 4096 ? 1 : 0;
       const size_t fixed = (size_t)(halo + 8) * 4 + (p.bias_smem ? (size_t)K * 4 : 0) + 16 + 8 * 24 + 16 +
                            (p.sn ? (size_t)SN_XCH_FLOATS * 4 : 0);
@@ -1293,6 +1314,7 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
       p.MT = p.tile2d ? bb * p.CT : mt;
       p.BB = bb;
       p.HALO = halo;
+      p.stg_row = stg_row;
       p.cta_pos = cta_pos;
       p.ntiles = ntiles;
       p.a_bytes = a_bytes;
@@ -1374,7 +1396,10 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
       return SYSML_ERR_UNSUPPORTED;
     }
   }
-  if (p.abulk && (p.cl2 || p.in_plane > 0 || p.is_csr || ((uintptr_t)x & 15))) p.abulk = 0;  // NCHW only
+  if (p.abulk == 1 && (p.cl2 || p.in_plane > 0 || p.is_csr || ((uintptr_t)x & 15))) p.abulk = 0;  // NCHW only
+  if (p.abulk == 2 && (p.cl2 || p.in_plane <= 0 || (p.in_plane & 3) || p.in_phase || p.is_csr ||
+                       ((uintptr_t)x & 15)))
+    p.abulk = 0;  // SPF only
 
   float *fp = reinterpret_cast<float *>(ws);
   if (p.ks) {
@@ -1475,7 +1500,8 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
     cfg.attrs = at;
     cfg.numAttrs = na;
     route_note("tc_conv_fwd_kernel%s [tcgen05 TF32, %s%s, MT=%d, N=%d, %d tiles on %d CTAs%s]", ph ? "<phase>" : "",
-               p.ks ? "KS" : p.sn ? (p.snt < p.S ? "SN-T" : "SN") : "standard", p.is_csr ? " CSR" : "", p.MT, p.NN, (int)p.ntiles, grid,
+               p.ks ? "KS" : p.sn ? (p.snt < p.S ? "SN-T" : "SN") : "standard",
+               p.is_csr ? " CSR" : p.abulk == 2 ? " staged-SPF" : p.abulk ? " staged" : "", p.MT, p.NN, (int)p.ntiles, grid,
                p.pool ? ", pool epilogue" : "");
     SYSML_CUDA(cudaLaunchKernelEx(&cfg, ph ? tc_conv_fwd_kernel<true> : tc_conv_fwd_kernel<false>, p));
   }
@@ -2211,7 +2237,7 @@ static bool strided_1x1(const ConvArgs &a) {
   return (a.sh != 1 || a.sw != 1) && a.R == 1 && a.S == 1 && a.ph == 0 && a.pw == 0;
 }
 
-static TcPlan plan_bwd_data(const ConvArgs &a) {
+static TcPlan plan_bwd_data(const ConvArgs &a, int spf_in = 0) {
   if (strided_1x1(a)) {
     // strided 1x1: dX[n, c, p*sh, q*sw] = sum_k F[k, c] dY[n, k, p, q], zero elsewhere -- a
     // stride-1 1x1 "forward" on dY's grid whose rows land on every sh-th row / sw-th column
@@ -2224,7 +2250,7 @@ static TcPlan plan_bwd_data(const ConvArgs &a) {
   }
   // dX = conv(dY, rot180(F)^T), pad R-1-ph; input (N, K, P, Q) -> output (N, C, H, W)
   return plan_fwd(a.N, a.K, a.P, a.Q, a.C, a.R, a.S, a.R - 1 - a.ph, a.S - 1 - a.pw, nullptr,
-                  /*allow_ks=*/false);
+                  /*allow_ks=*/false, 1, 1, spf_in);
 }
 
 bool tc_bwd_data_supported(const ConvArgs &a) {
@@ -2304,7 +2330,8 @@ sysml_status tc_conv_bwd_data_phase(const ConvArgs &a, const ConvArgs &b, const 
 sysml_status tc_conv_fwd_spf(const ConvArgs &a, const TcSpfIO &io, const float *x, const float *f,
                              const float *bias, float *y, const PoolArgs *pool, float *pout,
                              int32_t *parg, void *ws, cudaStream_t st, const sysml_csr *csr) {
-  TcPlan pl = plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool);
+  TcPlan pl = plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool, true, 1, 1, 1);
+  if (!pl.ok) pl = plan_fwd(a.N, a.C, a.H, a.W, a.K, a.R, a.S, a.ph, a.pw, pool);
   if (!pl.ok || a.sh != 1 || a.sw != 1) {
     set_error("tcgen05 SPF forward: unsupported shape");
     return SYSML_ERR_UNSUPPORTED;
@@ -2324,7 +2351,8 @@ sysml_status tc_conv_bwd_data_spf(const ConvArgs &a, const TcSpfIO &io, const fl
     set_error("tcgen05 SPF bwd_data: unsupported shape");
     return SYSML_ERR_UNSUPPORTED;
   }
-  TcPlan pl = plan_bwd_data(a);
+  TcPlan pl = plan_bwd_data(a, 1);
+  if (!pl.ok || pl.fp_bytes > plan_bwd_data(a).fp_bytes) pl = plan_bwd_data(a);  // ws sized by the plain plan
   return run_fwd(pl, dy, f, 1, a.K, nullptr, dx, nullptr, nullptr, ws, st, &io);
 }
 

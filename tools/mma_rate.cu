@@ -6,7 +6,8 @@
 #include "../paper_1802_04647_b200/csrc/tc_ptx.cuh"
 using namespace sysml;
 
-__global__ void bench(int N, int sw, int rnd, int reps, unsigned long long *out) {
+template <int NACC>
+__global__ void bench(int N, int sw, int rnd, int reps, unsigned long long *out, int aoff, int halo, int boff) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar;
@@ -21,22 +22,28 @@ __global__ void bench(int N, int sw, int rnd, int reps, unsigned long long *out)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t A = ptx::smem_u32(smem), B = A + 64 * 1024;
+  const uint32_t A = ptx::smem_u32(smem), B = A + (boff ? boff : 64 * 1024);
   const uint32_t idesc = ptx::make_idesc_tf32(128, N);
+  uint32_t tm[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tm[k] = (uint32_t)((k % NACC) * N);
+  uint64_t adv[4], bdv[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    if (sw) {
+      adv[kk] = (ptx::make_desc(A + kk * 32, 16, 1024) | ((uint64_t)2 << 61));
+      bdv[kk] = (ptx::make_desc(B + kk * 32, 16, 1024) | ((uint64_t)2 << 61));
+    } else {
+      adv[kk] = halo ? ptx::make_desc(A + kk * 16 * 16 + aoff * 16, halo * 16, 128) : ptx::make_desc(A + kk * 128 * 32 + aoff * 16, 128 * 16, 128);
+      bdv[kk] = ptx::make_desc(B + kk * N * 32, N * 16, 128);
+    }
+  }
   if (threadIdx.x < 32) {
     unsigned long long t0 = clock64();
     for (int rep = 0; rep < reps; ++rep) {
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        uint64_t ad, bd;
-        if (sw) {
-          ad = (ptx::make_desc(A + kk * 32, 16, 1024) | ((uint64_t)2 << 61));
-          bd = (ptx::make_desc(B + kk * 32, 16, 1024) | ((uint64_t)2 << 61));
-        } else {
-          ad = ptx::make_desc(A + kk * 128 * 32, 128 * 16, 128);
-          bd = ptx::make_desc(B + kk * N * 32, N * 16, 128);
-        }
-        if (ptx::elect_one()) ptx::mma_tf32(0, ad, bd, idesc, 1u);
+        if (ptx::elect_one()) ptx::mma_tf32(tm[kk], adv[kk], bdv[kk], idesc, 1u);
         __syncwarp();
       }
     }
@@ -55,17 +62,25 @@ __global__ void bench(int N, int sw, int rnd, int reps, unsigned long long *out)
 int main() {
   unsigned long long *d, h[2];
   cudaMalloc(&d, 16);
-  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 170 * 1024);
+  cudaFuncSetAttribute(bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 170 * 1024);
+  cudaFuncSetAttribute(bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 170 * 1024);
+  cudaFuncSetAttribute(bench<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 170 * 1024);
   const int reps = 2000;
-  for (int sw = 0; sw < 2; ++sw)
-    for (int rnd = 0; rnd < 2; ++rnd)
-      for (int N : {64, 128, 256}) {
-        for (int grid : {1, 148}) {
-          bench<<<grid, 128, 170 * 1024>>>(N, sw, rnd, reps, d);
+  for (int cfg = 0; cfg < 4; ++cfg)
+  for (int sw = 0; sw < 1; ++sw)
+    for (int nacc : {1})
+      for (int N : {64, 96, 160}) {
+        const int aoff = 0, halo = (cfg & 1) ? 328 : 0, boff = (cfg & 2) ? 2 * 328 * 16 : 0;
+        if (nacc * N > 512) continue;
+        const int rnd = 1;
+        for (int grid : {148}) {
+          if (nacc == 1) bench<1><<<grid, 128, 170 * 1024>>>(N, sw, rnd, reps, d, aoff, halo, boff);
+          else if (nacc == 2) bench<2><<<grid, 128, 170 * 1024>>>(N, sw, rnd, reps, d, aoff, halo, boff);
+          else bench<4><<<grid, 128, 170 * 1024>>>(N, sw, rnd, reps, d, aoff, halo, boff);
           if (cudaDeviceSynchronize() != cudaSuccess) { printf("err\n"); return 1; }
           cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
           const double n = reps * 4.0;
-          printf("sw128=%d rnd=%d N=%3d grid=%3d: %.1f clk/mma (ideal %.1f at 2048 FMA/clk)\n", sw, rnd, N, grid,
+          printf("halo=%d boff=%d sw128=%d nacc=%d N=%3d grid=%3d: %.1f clk/mma (ideal %.1f at 2048 FMA/clk)\n", halo, boff, sw, nacc, N, grid,
                  h[1] / n, 128.0 * N * 8 / 2048);
         }
       }
