@@ -60,6 +60,11 @@ constexpr int TC_THREADS = 256;      // bwd_filter kernel: 4 producer warps + MM
 constexpr int TC_FWD_THREADS = 416;  // forward kernel: 4 producer, 1 MMA, 8 epilogue warps
 constexpr int TC_EPI_WARPS = 8;      // two per TMEM lane quadrant; they split the M-tiles
 constexpr int SMEM_BUDGET = 225 * 1024;
+// routed SPF input (NEXT-1): per-tile staging of the pooled gradient rows [<=RT_MAXW][64] and
+// the window codes [4][RT_MAXW], double-buffered across tiles
+constexpr int RT_MAXW = 96;
+constexpr int RT_SLOT = RT_MAXW * 64 * 4 + 4 * RT_MAXW * 8;  // 27,648 B
+constexpr int RT_BYTES = 2 * RT_SLOT;
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
@@ -109,6 +114,10 @@ struct TcFwdParams {
   int NN;              // accumulator width per M-tile: NFpad, or snt*NFpad in SN mode
   int is_csr;          // KS mode only: input rows are CSR (scattered straight into the operand)
   sysml_csr csr;
+  const float *route_val;       // routed SPF input (TcSpfIO::route_*): producer builds the values
+  const uint64_t *route_code;
+  int64_t route_cplane;
+  int route_C, route_Pp, route_Qp, route_Wf, route_Lf;
   int64_t in_plane;    // > 0: input is SPF [C][in_plane], stored position = frame pos + in_shift
   int in_shift;
   int64_t out_plane;   // > 0: pooled output to SPF [K][out_plane] at (pp+out_off)*out_Wf + pc+out_off
@@ -560,11 +569,51 @@ __device__ __forceinline__ void sk_fixup(const TcFwdParams &p, uint32_t tb, int 
   ptx::tmem_st_wait();
 }
 
-template <bool PH>
+// Routed SPF input (NEXT-1): the staged window range of the tile starting at frame position g0 --
+// first window (even, for 16-byte aligned code copies) and the even window count covering
+// every position of the halo.
+__device__ __forceinline__ int64_t rt_win_at(const TcFwdParams &p, int64_t si, int after) {
+  const int64_t n = si / p.route_Lf;
+  const int row = (int)((si - n * p.route_Lf) / p.route_Wf);
+  const int pp = min((row >> 1) + after, p.route_Pp);
+  return (n * p.route_Pp + pp) * p.route_Qp;
+}
+__device__ __forceinline__ int64_t rt_w0(const TcFwdParams &p, int64_t g0) {
+  const int64_t si0 = max(g0 + (int64_t)p.in_shift, (int64_t)0);
+  if (si0 >= p.in_plane) return 0;
+  return rt_win_at(p, si0, 0) & ~(int64_t)1;
+}
+__device__ __forceinline__ void rt_issue(const TcFwdParams &p, int64_t g0, uint8_t *buf, uint64_t *bar) {
+  const int64_t w0 = rt_w0(p, g0);
+  const int64_t si0 = max(g0 + (int64_t)p.in_shift, (int64_t)0);
+  const int64_t si1 = min(g0 + (int64_t)p.in_shift + p.HALO - 1, p.in_plane - 1);
+  int cnt = 0;
+  if (si0 <= si1 && si0 < p.in_plane) {
+    const int64_t total = (int64_t)p.N * p.route_Pp * p.route_Qp;
+    const int64_t w1 = min(rt_win_at(p, si1, 1), total);
+    cnt = (int)max((int64_t)0, (w1 - w0 + 1) & ~(int64_t)1);
+    cnt = min(cnt, RT_MAXW);
+  }
+  const int ng = (p.C + 15) / 16;
+  ptx::fence_proxy_async_smem();  // the previous tile's generic reads of this slot are ordered first
+  ptx::mbar_arrive_expect_tx(bar, (uint32_t)(cnt * p.route_C * 4 + ng * cnt * 8));
+  if (cnt > 0) {
+    ptx::bulk_g2s(buf, p.route_val + w0 * p.route_C, (uint32_t)(cnt * p.route_C * 4), bar);
+    for (int g = 0; g < ng; ++g)
+      ptx::bulk_g2s(buf + RT_MAXW * 64 * 4 + g * RT_MAXW * 8, p.route_code + g * p.route_cplane + w0,
+                    (uint32_t)(cnt * 8), bar);
+  }
+}
+
+// MODE 0: common instance; 1: phase-split modes compiled in; 2: routed SPF input (NEXT-1).
+// Separate instances so the common one keeps its register allocation.
+template <int MODE>
 __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const TcFwdParams p) {
+  constexpr bool PH = MODE == 1, RT = MODE == 2;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t *stage_base = smem;
-  int *src_off = reinterpret_cast<int *>(smem + (size_t)p.nstage * p.stage_bytes);
+  uint8_t *rt_buf = smem + (size_t)p.nstage * p.stage_bytes;  // RT: [2][RT_SLOT] tile staging
+  int *src_off = reinterpret_cast<int *>(rt_buf + (RT ? RT_BYTES : 0));
   float *bias_s = reinterpret_cast<float *>(src_off + p.HALO + 8);
   // SN epilogue exchange: [set 2][warp 4][s 8][row 4][16] floats (rows 0..3 of each warp)
   float *sn_xch = reinterpret_cast<float *>(
@@ -575,7 +624,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
   uint64_t *accf = bars + 2 * p.nstage;  // [2]
   uint64_t *acce = accf + 2;             // [2]
   uint64_t *staged = acce + 2;           // [nstage] abulk: staging buffer filled
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(staged + p.nstage);
+  uint64_t *rtfull = staged + p.nstage;  // [2] RT: tile staging landed
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rtfull + 2);
 
   // warp index via shuffle: provably warp-uniform, so role branches keep the uniform datapath
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -591,6 +641,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
       ptx::mbar_init(acce + b, TC_EPI_WARPS);
     }
     for (int s = 0; s < p.nstage; ++s) ptx::mbar_init(staged + s, 64);  // abulk: loader cp.async arrivals
+    ptx::mbar_init(rtfull, 1);
+    ptx::mbar_init(rtfull + 1, 1);
     ptx::fence_mbar_init();
   }
   if (p.bias_smem)
@@ -739,6 +791,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
     int64_t tile;
     int c0, c1;
     int ist = 0;  // abulk issuer (tid 0): stage cursor, runs up to L chunks ahead
+    int64_t rt_tl = 0;  // RT: CTA-local tile counter (tile staging slot = rt_tl & 1)
     uint32_t iph = 0;
     while (tc_next(p, wk, tile, c0, c1)) {
       const int ft = (int)(tile % p.nft);
@@ -833,6 +886,16 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         int off = -1;
         if (PH && p.in_phase) {
           off = phase_off(p, gi, cur_ab);
+        } else if (RT) {
+          // routed: (window index - the tile's first staged window) * 4 + position in the window
+          const int64_t si = gi + p.in_shift;
+          if (gi < p.G && si >= 0 && si < p.in_plane) {
+            const int n = (int)(si / p.route_Lf), rem = (int)(si - (int64_t)n * p.route_Lf);
+            const int row = rem / p.route_Wf, col = rem - row * p.route_Wf;
+            if (row < 2 * p.route_Pp && col < 2 * p.route_Qp)
+              off = ((int)(((int64_t)n * p.route_Pp + (row >> 1)) * p.route_Qp + (col >> 1) - rt_w0(p, g0))) * 4 +
+                    (row & 1) * 2 + (col & 1);
+          }
         } else if (p.in_plane > 0) {
           const int64_t si = gi + p.in_shift;  // SPF: zeros are stored, no decoding
           if (gi < p.G && si >= 0 && si < p.in_plane) off = (int)si;
@@ -846,6 +909,59 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1) tc_conv_fwd_kernel(const Tc
         src_off[pos] = off;
       }
       ptx::named_bar_sync(1, 128);
+      if (RT) {
+        // NEXT-1 vertical fusion: the unpooled gradient is built here from the
+        // pooled gradient (route_val, window-major, channel-minor) and the pool window codes
+        // -- dz2 never exists in HBM.  The tile's window rows and code words are staged in
+        // shared memory by bulk copies (issued one tile ahead, double-buffered); each chunk
+        // then expands them smem -> smem: two 16-byte loads + one code word per (position,
+        // 8 channels), two 16-byte row stores into the K-major [quad][pos][4] operand.
+        const int slot = (int)(rt_tl & 1);
+        if (tid == 0) {
+          if (rt_tl == 0) rt_issue(p, g0, rt_buf, rtfull);  // first tile: nobody prefetched it
+          const int64_t nxt = tile + gridDim.x;             // round-robin tiles (no stream-K)
+          if (nxt < p.ntiles) rt_issue(p, (nxt / p.nft) * p.cta_pos, rt_buf + (1 - slot) * RT_SLOT, rtfull + (1 - slot));
+        }
+        ptx::mbar_wait(rtfull + slot, (uint32_t)((rt_tl >> 1) & 1));
+        const float *rv = reinterpret_cast<const float *>(rt_buf + slot * RT_SLOT);
+        const unsigned long long *rc =
+            reinterpret_cast<const unsigned long long *>(rt_buf + slot * RT_SLOT + RT_MAXW * 64 * 4);
+        for (int ch = c0; ch < c1; ++ch) {
+          ptx::mbar_wait(empty + stage, phase ^ 1);
+          uint8_t *A = stage_base + (size_t)stage * p.stage_bytes;
+          if (tid == 0) {
+            ptx::mbar_arrive_expect_tx(full + stage, p.b_bytes);
+            ptx::bulk_g2s(A + p.a_bytes, p.fp + ((size_t)ft * p.nchunk + ch) * (p.b_bytes / 4), p.b_bytes,
+                          full + stage);
+          }
+          const uint32_t a0 = ptx::smem_u32(A), a1 = a0 + (uint32_t)p.HALO * 16;
+          const int cc = ch * 8, nc = min(8, p.C - cc), csh = (cc & 15) * 4;
+          const unsigned long long *rcg = rc + (cc >> 4) * RT_MAXW;
+          for (int pos = tid; pos < p.HALO; pos += 128) {
+            const int off = src_off[pos];
+            float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (off >= 0) {
+              const int lw = off >> 2, sub = off & 3;
+              const float4 v0 = *reinterpret_cast<const float4 *>(rv + lw * 64 + cc);
+              const float4 v1 = *reinterpret_cast<const float4 *>(rv + lw * 64 + cc + 4);
+              const uint32_t nib = (uint32_t)(rcg[lw] >> csh);
+              const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const uint32_t cd = (nib >> (4 * j)) & 15u;  // positive*4 + dr*2 + ds (R9)
+                o[j] = (j < nc && (cd & 4u) && (int)(cd & 3u) == sub) ? v[j] : 0.f;
+              }
+            }
+            st_shared_v4(a0 + pos * 16, o[0], o[1], o[2], o[3]);
+            st_shared_v4(a1 + pos * 16, o[4], o[5], o[6], o[7]);
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(full + stage);
+          if (++stage == p.nstage) { stage = 0; phase ^= 1; }
+        }
+        ++rt_tl;
+        continue;
+      }
       for (int ch = c0; ch < c1; ++ch) {
         const long long t_e0 = clock64();
         ptx::mbar_wait(empty + stage, phase ^ 1);
@@ -1186,7 +1302,8 @@ int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 // Plan the forward kernel for a stride-1 conv: input (N,C,H,W), K output channels.
 TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
-                const PoolArgs *pool, bool allow_ks = true, int sh = 1, int sw = 1, int spf_in = 0) {
+                const PoolArgs *pool, bool allow_ks = true, int sh = 1, int sw = 1, int spf_in = 0,
+                int route = 0) {
   TcPlan pl{};
   TcFwdParams &p = pl.p;
   p.N = N; p.C = C; p.H = H; p.W = W; p.K = K; p.R = R; p.S = S; p.ph = ph; p.pw = pw;
@@ -1307,7 +1424,8 @@ TcPlan plan_fwd(int N, int C, int H, int W, int K, int R, int S, int ph, int pw,
       const int stg_row = halo + (p.abulk == 2 ? 4 : 0);
       const uint32_t stage = a_bytes + p.b_bytes + (p.abulk ? (uint32_t)(8 * stg_row * 4) : 0u);
       p.bias_smem = K <= 4096 ? 1 : 0;
-      const size_t fixed = (size_t)(halo + 8) * 4 + (p.bias_smem ? (size_t)K * 4 : 0) + 16 + 8 * 24 + 16 +
+      const size_t fixed = (size_t)(halo + 8) * 4 + (p.bias_smem ? (size_t)K * 4 : 0) + 16 + 8 * 24 + 16 + 16 +
+                           (route ? (size_t)RT_BYTES : 0) +
                            (p.sn ? (size_t)SN_XCH_FLOATS * 4 : 0);
       const int nst = (int)((SMEM_BUDGET - (int64_t)fixed) / (int64_t)stage);
       if (nst < 2) continue;
@@ -1380,6 +1498,19 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
   if (io) {
     p.in_plane = io->in_plane;
     p.in_shift = io->in_shift;
+    p.route_val = io->route_val;
+    p.route_code = io->route_code;
+    p.route_cplane = io->route_cplane;
+    p.route_C = io->route_C;
+    p.route_Pp = io->route_Pp;
+    p.route_Qp = io->route_Qp;
+    p.route_Wf = io->route_Wf;
+    p.route_Lf = io->route_Lf;
+    if (p.route_val && (p.ks || p.is_csr || p.in_plane <= 0 || (p.route_C != 64) || p.C > p.route_C || p.HALO > 384 || p.sk || (p.route_cplane & 1) ||
+                        ((uintptr_t)p.route_val & 15))) {
+      set_error("tcgen05 forward: routed SPF input needs C %% 8 == 0 planes and 16-byte aligned values");
+      return SYSML_ERR_UNSUPPORTED;
+    }
     p.out_plane = io->out_plane;
     p.out_Wf = io->out_Wf;
     p.out_Lf = io->out_Lf;
@@ -1398,7 +1529,7 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
   }
   if (p.abulk == 1 && (p.cl2 || p.in_plane > 0 || p.is_csr || ((uintptr_t)x & 15))) p.abulk = 0;  // NCHW only
   if (p.abulk == 2 && (p.cl2 || p.in_plane <= 0 || (p.in_plane & 3) || p.in_phase || p.is_csr ||
-                       ((uintptr_t)x & 15)))
+                       ((uintptr_t)x & 15) || p.route_val))
     p.abulk = 0;  // SPF only
 
   float *fp = reinterpret_cast<float *>(ws);
@@ -1439,9 +1570,11 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
   if (!bias) p.bias_smem = 0;
   const bool ph = p.in_phase || p.out_phase;
   if (ph) {
-    SYSML_TRY(smem_attr(tc_conv_fwd_kernel<true>, pl.smem));
+    SYSML_TRY(smem_attr(tc_conv_fwd_kernel<1>, pl.smem));
+  } else if (p.route_val) {
+    SYSML_TRY(smem_attr(tc_conv_fwd_kernel<2>, pl.smem));
   } else {
-    SYSML_TRY(smem_attr(tc_conv_fwd_kernel<false>, pl.smem));
+    SYSML_TRY(smem_attr(tc_conv_fwd_kernel<0>, pl.smem));
   }
   int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
   // stream-K (opt-in, SYSML_TC_SK=1): even chunk-iteration ranges per CTA instead of whole
@@ -1503,7 +1636,7 @@ sysml_status run_fwd(TcPlan &pl, const float *x, const float *f, int flip, int f
                p.ks ? "KS" : p.sn ? (p.snt < p.S ? "SN-T" : "SN") : "standard",
                p.is_csr ? " CSR" : p.abulk == 2 ? " staged-SPF" : p.abulk ? " staged" : "", p.MT, p.NN, (int)p.ntiles, grid,
                p.pool ? ", pool epilogue" : "");
-    SYSML_CUDA(cudaLaunchKernelEx(&cfg, ph ? tc_conv_fwd_kernel<true> : tc_conv_fwd_kernel<false>, p));
+    SYSML_CUDA(cudaLaunchKernelEx(&cfg, ph ? tc_conv_fwd_kernel<1> : p.route_val ? tc_conv_fwd_kernel<2> : tc_conv_fwd_kernel<0>, p));
   }
   SYSML_LAUNCH_CHECK();
   if (prof) {
@@ -2237,7 +2370,7 @@ static bool strided_1x1(const ConvArgs &a) {
   return (a.sh != 1 || a.sw != 1) && a.R == 1 && a.S == 1 && a.ph == 0 && a.pw == 0;
 }
 
-static TcPlan plan_bwd_data(const ConvArgs &a, int spf_in = 0) {
+static TcPlan plan_bwd_data(const ConvArgs &a, int spf_in = 0, int route = 0) {
   if (strided_1x1(a)) {
     // strided 1x1: dX[n, c, p*sh, q*sw] = sum_k F[k, c] dY[n, k, p, q], zero elsewhere -- a
     // stride-1 1x1 "forward" on dY's grid whose rows land on every sh-th row / sw-th column
@@ -2250,7 +2383,7 @@ static TcPlan plan_bwd_data(const ConvArgs &a, int spf_in = 0) {
   }
   // dX = conv(dY, rot180(F)^T), pad R-1-ph; input (N, K, P, Q) -> output (N, C, H, W)
   return plan_fwd(a.N, a.K, a.P, a.Q, a.C, a.R, a.S, a.R - 1 - a.ph, a.S - 1 - a.pw, nullptr,
-                  /*allow_ks=*/false, 1, 1, spf_in);
+                  /*allow_ks=*/false, 1, 1, spf_in, route);
 }
 
 bool tc_bwd_data_supported(const ConvArgs &a) {
@@ -2351,8 +2484,13 @@ sysml_status tc_conv_bwd_data_spf(const ConvArgs &a, const TcSpfIO &io, const fl
     set_error("tcgen05 SPF bwd_data: unsupported shape");
     return SYSML_ERR_UNSUPPORTED;
   }
-  TcPlan pl = plan_bwd_data(a, 1);
-  if (!pl.ok || pl.fp_bytes > plan_bwd_data(a).fp_bytes) pl = plan_bwd_data(a);  // ws sized by the plain plan
+  const int route = io.route_val ? 1 : 0;
+  TcPlan pl = plan_bwd_data(a, route ? 0 : 1, route);
+  if (!route && (!pl.ok || pl.fp_bytes > plan_bwd_data(a).fp_bytes)) pl = plan_bwd_data(a);  // ws sized by the plain plan
+  if (!pl.ok || pl.fp_bytes > plan_bwd_data(a).fp_bytes) {
+    set_error("tcgen05 SPF bwd_data: no plan for this shape%s", route ? " with routed input" : "");
+    return SYSML_ERR_UNSUPPORTED;
+  }
   return run_fwd(pl, dy, f, 1, a.K, nullptr, dx, nullptr, nullptr, ws, st, &io);
 }
 

@@ -73,6 +73,16 @@ struct TcSpfIO {
   int64_t code_plane = 0;    // code[k/16][n*PpQp + pp*Qp + pc]: bits 4j..4j+3 of channel
                              // 16g + j = positive*4 + dr*2 + ds (window winner (2pp+dr, 2pc+ds))
   int out_nhwc = 0;          // SN epilogue (bwd_data): y channel-minor [n][P*Q][K], K % 4 == 0
+  // Routed SPF input (NEXT-1 vertical fusion; LeNet conv2 backward): the input is NOT read
+  // from planes -- the producer builds each unpooled gradient value from the pooled gradient
+  // route_val[(n*PpQp + window)*route_C + c] and the window code of (c, n, window) in
+  // route_code (layout of `code` above): value = positive && winner == (dr, ds) ? val : 0.
+  // Frame geometry: in_plane / in_shift as for SPF input (output-frame convention, Lf
+  // positions per image, Wf per row); windows 2x2/2 over route_Pp x route_Qp.
+  const float *route_val = nullptr;
+  const uint64_t *route_code = nullptr;
+  int64_t route_cplane = 0;
+  int route_C = 0, route_Pp = 0, route_Qp = 0, route_Wf = 0, route_Lf = 0;
 };
 
 // conv_tc.cu : tcgen05 TF32 implicit GEMM (SYSML_MATH_TF32)

@@ -407,6 +407,42 @@ __global__ void __launch_bounds__(256) affine_bwd_route_spf_kernel(
   dbpart[(int64_t)blockIdx.y * D3 + d] = gsum;
 }
 
+// B2p, vertically fused form (NEXT-1): da2 = ds W3 (P:58-84 affine backward) in the
+// window-major, channel-minor layout da2w[n][pp*7 + pc][64] that the conv2 backward producers
+// route through the window codes themselves -- the unpooled dz2 is never written.  Values are
+// masked by the relu bit of the window code (R9), so da2w holds exactly the gradient each
+// window routes to its winner.  Block = 64 channels x 4 windows x a chunk of 32 images; each
+// thread keeps its W3 column in registers.  dbpart[chunk][k*49 + window] = db2 partials.
+__global__ void __launch_bounds__(256) affine_bwd_da2w_kernel(
+    int n, const float *__restrict__ ds, const float *__restrict__ W3, const uint64_t *__restrict__ c2,
+    int64_t cplane, float *__restrict__ da2w, float *__restrict__ dbpart) {
+  __shared__ float dss[B2P_IMGS * NCLS];
+  const int k = threadIdx.x & 63, win = blockIdx.x * 4 + (threadIdx.x >> 6);
+  const int s0 = blockIdx.y * B2P_IMGS, s1 = min(n, s0 + B2P_IMGS);
+  for (int i = threadIdx.x; i < (s1 - s0) * NCLS; i += 256) dss[i] = __ldg(ds + (int64_t)s0 * NCLS + i);
+  __syncthreads();
+  if (win >= 49) return;
+  const int d = k * 49 + win;
+  float w[NCLS];
+#pragma unroll
+  for (int j = 0; j < NCLS; ++j) w[j] = __ldg(W3 + j * D3 + d);
+  const unsigned long long *cw = reinterpret_cast<const unsigned long long *>(c2) + (int64_t)(k >> 4) * cplane + win;
+  const int sh = 4 * (k & 15);
+  float gsum = 0.f;
+  for (int s = s0; s < s1; ++s) {
+    const uint32_t cd = (uint32_t)(__ldg(cw + (int64_t)s * 49) >> sh) & 15u;
+    float g = 0.f;
+    if (cd & 4u) {
+      const float *dsr = dss + (s - s0) * NCLS;
+#pragma unroll
+      for (int j = 0; j < NCLS; ++j) g = fmaf(dsr[j], w[j], g);
+    }
+    gsum += g;
+    __stcs(da2w + ((int64_t)s * 49 + win) * 64 + k, g);
+  }
+  dbpart[(int64_t)blockIdx.y * D3 + d] = gsum;
+}
+
 // db2[k] = fixed-order sum of the B2p partials: block k, thread t sums chunks t, t + 256, ...
 // (each over the 49 windows in order), then a fixed shared-memory tree
 __global__ void __launch_bounds__(256) db2_reduce_kernel(const float *__restrict__ dbpart, int chunks,
@@ -558,6 +594,10 @@ struct sysml_lenet {
   // TF32 path: pool argmax as packed 2-bit window codes, one u32 per (16 channels, window)
   uint64_t *c1 = nullptr, *c2 = nullptr;  // [2][b*196], [4][b*49] (kernels.cuh TcSpfIO::code)
   float *db2part = nullptr;                // B2p's conv2 bias-gradient partials [chunks][3136]
+  // NEXT-1 vertical fusion: the conv2 backward producers route the pooled gradient da2w
+  // ([n][49 windows][64], relu-masked) through the window codes themselves
+  int route = 0;                           // B2d routed (SYSML_ROUTE=1, opt-in)
+  float *da2w = nullptr;
   // LeNet-512 (hidden = 512; 0 = LeNet-min): affine 3136->512 + relu + inverted dropout
   int hidden = 0;
   int64_t num_params = NUM_PARAMS;
@@ -578,6 +618,10 @@ sysml_conv_desc conv2_desc(int n, int math) {
 }
 sysml_pool_desc pool1_desc(int n) { return sysml_pool_desc{n, 32, 28, 28, 2, 2, 2, 2, 0, 0, 1}; }
 sysml_pool_desc pool2_desc(int n) { return sysml_pool_desc{n, 64, 14, 14, 2, 2, 2, 2, 0, 0, 1}; }
+
+// pool2 window-code plane stride (64-bit words per 16-channel group): even, so the routed
+// producers' per-tile bulk copies of code words start 16-byte aligned
+int64_t c2_plane_of(int64_t max_b) { return (max_b * 49 + 1) / 2 * 2; }
 
 int dw3_chunks_for(int n) {
   // about 16 samples per chunk, at most one chunk per SM (x 4 column blocks)
@@ -761,11 +805,18 @@ static sysml_status lenet_create_impl(int32_t max_local_batch, int32_t math, int
       if (cudaMalloc(&h->db2part, sizeof(float) * D3 * (size_t)ceil_div(max_local_batch, B2P_IMGS)) !=
               cudaSuccess ||
           cudaMalloc(&h->c1, sizeof(uint64_t) * 2 * (size_t)max_local_batch * 196) != cudaSuccess ||
-          cudaMalloc(&h->c2, sizeof(uint64_t) * 4 * (size_t)max_local_batch * 49) != cudaSuccess) {
+          cudaMalloc(&h->c2, sizeof(uint64_t) * (4 * (size_t)c2_plane_of(max_local_batch) + 2)) != cudaSuccess) {
         set_error("cudaMalloc failed for the window-code buffers");
         return fail(SYSML_ERR_CUDA);
       }
       ALLOC(h->dz2s, 64 * h->spf_plane);
+      // opt-in (SYSML_ROUTE=1): measured slower (r02, batch 8192): B2d 1.01M -> 1.14M cycles per
+      // CTA with register-pipelined global loads, 1.36M with per-tile smem staging (2 pipeline
+      // stages left); its MMA loop is shared-memory-operand bound, so expanding the pooled
+      // gradient in the producer costs more than writing dz2 once (DESIGN.md §7 NEXT-1)
+      static const int route_env = getenv("SYSML_ROUTE") ? atoi(getenv("SYSML_ROUTE")) : 0;
+      h->route = route_env ? 1 : 0;
+      if (h->route) ALLOC(h->da2w, b * D3 + 64);  // + one window: the routed staging reads even counts
       if (cudaMemset(h->a1s, 0, sizeof(float) * 32 * h->spf_plane) != cudaSuccess ||
           cudaMemset(h->dz2s, 0, sizeof(float) * 64 * h->spf_plane) != cudaSuccess) {
         set_error("cudaMemset of the SPF activation buffers failed");
@@ -841,7 +892,7 @@ sysml_status sysml_lenet_destroy(sysml_lenet *h) {
   cudaFree(h->ws);
   cudaFree(h->a1s); cudaFree(h->dz2s);
   cudaFree(h->h3); cudaFree(h->dz3); cudaFree(h->dz3T); cudaFree(h->a2T); cudaFree(h->W3T);
-  cudaFree(h->part4); cudaFree(h->drop_step);
+  cudaFree(h->part4); cudaFree(h->drop_step); cudaFree(h->da2w);
   for (auto &e : h->pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (int i = 0; i < NSTAGES; ++i)
     for (auto &e : h->pending[i]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -947,7 +998,7 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
     io.in_plane = h->spf_plane;
     io.in_shift = 0;
     io.code = h->c2;
-    io.code_plane = (int64_t)h->max_b * 49;
+    io.code_plane = c2_plane_of(h->max_b);
     SYSML_TRY(tc_conv_fwd_spf(ca2, io, h->a1s, params + OFF_F2, params + OFF_B2, nullptr, &pa2, h->a2,
                               nullptr, h->ws, st));
   } else {
@@ -1068,12 +1119,17 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
     SYSML_TRY(T.begin(4));
     if (hid) {
       static_assert(B2P_IMGS == 32, "route_da2_spf_kernel chunks db2 partials by 32 images");
-      SYSML_TRY(launch_route_da2_spf(n, h->da2, h->c2, (int64_t)h->max_b * 49, h->dz2s, h->spf_plane,
+      SYSML_TRY(launch_route_da2_spf(n, h->da2, h->c2, c2_plane_of(h->max_b), h->dz2s, h->spf_plane,
                                      h->db2part, st));
     } else {
+      if (h->route) {
+        affine_bwd_da2w_kernel<<<dim3(13, (unsigned)ceil_div(n, B2P_IMGS)), 256, 0, st>>>(
+            n, h->ds, params + OFF_W3, h->c2, c2_plane_of(h->max_b), h->da2w, h->db2part);
+        SYSML_LAUNCH_CHECK();
+      }
       affine_bwd_route_spf_kernel<<<dim3((unsigned)ceil_div(D3, 256), (unsigned)ceil_div(n, B2P_IMGS)),
                                     256, 0, st>>>(n, h->ds, params + OFF_W3, h->c2,
-                                                  (int64_t)h->max_b * 49, h->dz2s, h->spf_plane,
+                                                  c2_plane_of(h->max_b), h->dz2s, h->spf_plane,
                                                   h->db2part);
       SYSML_LAUNCH_CHECK();
     }
@@ -1097,6 +1153,16 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
     io.in_plane = h->spf_plane;
     io.in_shift = -(2 * 16 + 2);
     io.out_nhwc = h->da1_nhwc;  // da1 channel-minor: whole-vector stores, read only by B1
+    if (h->route && !hid) {  // NEXT-1: the producer routes da2w through the pool2 codes
+      io.route_val = h->da2w;
+      io.route_code = h->c2;
+      io.route_cplane = c2_plane_of(h->max_b);
+      io.route_C = 64;
+      io.route_Pp = 7;
+      io.route_Qp = 7;
+      io.route_Wf = 16;
+      io.route_Lf = 256;
+    }
     SYSML_TRY(tc_conv_bwd_data_spf(ca2, io, params + OFF_F2, h->dz2s, h->da1, h->ws, st));
     SYSML_TRY(T.end());
   } else {

@@ -428,3 +428,19 @@ def test_lenet_csr_cfg3_n256(S, math, dyadic):
         assert_close(gh[OFFS[i]:OFFS[i + 1]], g_ref[OFFS[i]:OFFS[i + 1]], TOL[math], f"{name} cfg3")
     assert_close(host(p), oracle.sgd_update(prm, gh, 0.01), 1e-6, "sgd cfg3")
     assert abs(host(loss)[0] - loss_ref) <= 1e-5 * abs(loss_ref)
+
+
+def test_lenet_routed_b2d_opt_in_parity(S):
+    """NEXT-1 opt-in (SYSML_ROUTE=1): conv2 bwd_data builds its input from da2w and the pool2
+    window codes inside the producer; the step must equal the oracle exactly as the default."""
+    import subprocess, sys
+    code = ("import tests.test_gpu_parity as T, paper_1802_04647_b200 as S, numpy as np, torch, oracle;"
+            "x,y,prm=T._lenet_case(37, True);"
+            "g_ref,_=oracle.lenet_fwd_bwd(x,y,prm,n_global=40);"
+            "net=S.LeNet(40, math='tf32'); g=torch.empty(83466,device='cuda');"
+            "net.fwd_bwd(T.dev(prm),T.dev(x),T.dev(y,torch.int32),40,g);"
+            "T.assert_close(T.host(g),g_ref,T.TOL['tf32'],'routed');print('ok')")
+    env = dict(os.environ, SYSML_ROUTE="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
