@@ -26,8 +26,10 @@
 //   B: filters, repacked once into [filter tile][chunk][tap][quad][filter][4 ch] and
 //      streamed per chunk with one bulk async copy (cp.async.bulk, TMA 1-D).
 //   D: fp32 accumulators in TMEM; MT M-tiles share every B chunk (MT*NF <= 512 cols).
-//   Roles (256 threads, persistent, 1 CTA/SM): warps 0-3 stage A and issue the B
-//   copy; warp 4 lane 0 issues tcgen05.mma; warps 4-7 drain TMEM in the epilogue.
+//   Roles (TC_FWD_THREADS = 416 threads, persistent, 1 CTA/SM): warps 0-3 stage A and
+//   issue the B copy (the staged modes split them into 16-byte loaders and transposers);
+//   warp 4 issues tcgen05.mma (the whole warp runs the loop, one elected lane issues);
+//   warps 5-12 drain TMEM in the epilogue, two per lane quadrant.
 // bwd_data = the forward kernel on dY with the filter bank transposed and
 // rotated 180 degrees, padding R-1-ph (stride 1).
 //

@@ -32,6 +32,8 @@ constexpr int FB_THREADS = 256;
 struct FusedB1Args {
   int N, H, W, K, R, S, ph, pw, P, Q, Pp, Qp;  // conv (C = 1) + pooled extents
   int Hp, Wp;                                   // padded image in smem
+  int P4;                                       // bulk kernel, dense input: row pitch of the 4
+                                                //   shifted image copies (0 = one scalar copy)
   int tpk;                                      // threads per filter
   int n_per_cta;
   int64_t mask_plane;                           // > 0: mask is SPF [K][mask_plane]
@@ -149,7 +151,7 @@ constexpr int FBB_STAGES = 2;
 constexpr int FBB_THREADS = FB_THREADS + 32;
 
 template <int R_, int S_>
-__global__ void __launch_bounds__(FBB_THREADS)
+__global__ void __launch_bounds__(FBB_THREADS, 2)
     pool_bwd_wgrad_c1_bulk_kernel(FusedB1Args a, const float *__restrict__ x, sysml_csr xcsr,
                                   int is_csr, const float *__restrict__ dpool,
                                   float *__restrict__ part) {
@@ -161,12 +163,17 @@ __global__ void __launch_bounds__(FBB_THREADS)
                  x_bytes = is_csr ? 0u : (uint32_t)(HW * 4);
   const uint32_t stage_bytes = (g_bytes + G * c_bytes + x_bytes + 15) & ~15u;
   float *img = reinterpret_cast<float *>(fbb_smem + FBB_STAGES * stage_bytes);  // Hp x Wp
-  uint64_t *full = reinterpret_cast<uint64_t *>(img + ((a.Hp * a.Wp + 3) & ~3));
+  // dense input: four copies of the padded image, copy j shifted left by j columns, rows of
+  // a.P4 floats (16-byte aligned), so every window row is one aligned float4 (+ a scalar for
+  // S = 5) whatever its start column; copy bases staggered by 16 banks, a.P4 = 8 mod 32
+  const int copy_stride = a.Hp * a.P4 + 16;
+  const bool vec = !is_csr && a.P4 > 0;
+  uint64_t *full = reinterpret_cast<uint64_t *>(img + (vec ? ((4 * copy_stride + 3) & ~3) : ((a.Hp * a.Wp + 3) & ~3)));
   uint64_t *empty = full + FBB_STAGES;
   const int t = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, t >> 5, 0), lane = t & 31;
   const int n0 = blockIdx.x * a.n_per_cta, n1 = min(a.N, n0 + a.n_per_cta);
-  for (int i = t; i < a.Hp * a.Wp; i += blockDim.x) img[i] = 0.f;  // zero border (= padding)
+  for (int i = t; i < (vec ? 4 * copy_stride : a.Hp * a.Wp); i += blockDim.x) img[i] = 0.f;  // zero border
   if (t == 0) {
     for (int s_ = 0; s_ < FBB_STAGES; ++s_) {
       ptx::mbar_init(full + s_, 1);
@@ -212,7 +219,17 @@ __global__ void __launch_bounds__(FBB_THREADS)
     const float *gs = reinterpret_cast<const float *>(sb);
     const unsigned long long *cs = reinterpret_cast<const unsigned long long *>(sb + g_bytes);
     ptx::named_bar_sync(1, FB_THREADS);  // previous image's window reads are done
-    if (!is_csr) {
+    if (vec) {
+      const float *xs = reinterpret_cast<const float *>(sb + g_bytes + G * c_bytes);
+      for (int i = t; i < HW; i += FB_THREADS) {
+        const int h = __float2int_rz(((float)i + 0.5f) * invW), w = i - h * a.W;
+        const float v = xs[i];
+        float *row = img + (h + a.ph) * a.P4 + w + a.pw;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (w + a.pw - j >= 0) row[j * copy_stride - j] = v;
+      }
+    } else if (!is_csr) {
       const float *xs = reinterpret_cast<const float *>(sb + g_bytes + G * c_bytes);
       for (int i = t; i < HW; i += FB_THREADS) {
         const int h = __float2int_rz(((float)i + 0.5f) * invW), w = i - h * a.W;
@@ -247,12 +264,26 @@ __global__ void __launch_bounds__(FBB_THREADS)
         // masked (reading R9) lanes add g = 0: every lane stays on the same path
         const float g = (kok && (cd & 4u)) ? g0 : 0.f;
         const int pr = __float2int_rz(((float)pp + 0.5f) * invQ), pc = pp - pr * a.Qp;
-        const float *win = img + (2 * pr + (int)((cd >> 1) & 1u)) * a.Wp + 2 * pc + (int)(cd & 1u);
         dbacc += g;
+        if (vec) {
+          const int row0 = 2 * pr + (int)((cd >> 1) & 1u), col0 = 2 * pc + (int)(cd & 1u), j = col0 & 3;
+          const float *win = img + j * copy_stride + row0 * a.P4 + (col0 - j);  // 16-byte aligned
 #pragma unroll
-        for (int r = 0; r < R_; ++r)
+          for (int r = 0; r < R_; ++r) {
+            const float4 q = *reinterpret_cast<const float4 *>(win + r * a.P4);
+            acc[r * S_ + 0] = fmaf(g, q.x, acc[r * S_ + 0]);
+            if (S_ > 1) acc[r * S_ + 1] = fmaf(g, q.y, acc[r * S_ + 1]);
+            if (S_ > 2) acc[r * S_ + 2] = fmaf(g, q.z, acc[r * S_ + 2]);
+            if (S_ > 3) acc[r * S_ + 3] = fmaf(g, q.w, acc[r * S_ + 3]);
+            if (S_ == 5) acc[r * S_ + 4] = fmaf(g, win[r * a.P4 + 4], acc[r * S_ + 4]);
+          }
+        } else {
+          const float *win = img + (2 * pr + (int)((cd >> 1) & 1u)) * a.Wp + 2 * pc + (int)(cd & 1u);
 #pragma unroll
-          for (int s_ = 0; s_ < S_; ++s_) acc[r * S_ + s_] = fmaf(g, win[r * a.Wp + s_], acc[r * S_ + s_]);
+          for (int r = 0; r < R_; ++r)
+#pragma unroll
+            for (int s_ = 0; s_ < S_; ++s_) acc[r * S_ + s_] = fmaf(g, win[r * a.Wp + s_], acc[r * S_ + s_]);
+        }
       }
     }
     __syncwarp();
@@ -367,12 +398,18 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
     // padded-image row pitch = 2 mod 32: the four 2x2-window candidates of a warp's window
     // reads ((dr, ds) offsets 0, 1, pitch, pitch+1) fall in four different banks
     a.Wp = (a.Wp + 31 - 2) / 32 * 32 + 2;
+    static const int vec_env = getenv("SYSML_B1_VEC") ? atoi(getenv("SYSML_B1_VEC")) : 1;
+    // four shifted copies, pitch = 8 mod 32 floats and >= Wp + 3 (a window row may start at
+    // any column <= W + 2 pw - S and reads 8 floats from its aligned start)
+    a.P4 = (!xcsr && vec_env && c.S <= 5) ? (c.W + 2 * c.pw + 3 + 31 - 8) / 32 * 32 + 8 : 0;
+    const size_t img_bytes = a.P4 ? align_up((size_t)4 * (a.Hp * a.P4 + 16) * 4, 16)
+                                  : align_up((size_t)a.Hp * a.Wp * 4, 16);
     const int G = (c.K + 15) / 16;
     const size_t stage = align_up((size_t)c.K * pa.P * pa.Q * 4 + (size_t)G * pa.P * pa.Q * 8 +
                                       (xcsr ? 0 : (size_t)c.H * c.W * 4), 16);
-    const size_t smem_b = std::max(FBB_STAGES * stage, (size_t)FB_THREADS * (RS + 1) * 4) +
-                          align_up((size_t)a.Hp * a.Wp * 4, 16) + 8 * 2 * FBB_STAGES;
-    const size_t smem_bulk = FBB_STAGES * stage + align_up((size_t)a.Hp * a.Wp * 4, 16) + 8 * 2 * FBB_STAGES;
+    const size_t smem_b = std::max(FBB_STAGES * stage, (size_t)FB_THREADS * (RS + 1) * 4) + img_bytes +
+                          8 * 2 * FBB_STAGES;
+    const size_t smem_bulk = FBB_STAGES * stage + img_bytes + 8 * 2 * FBB_STAGES;
     const size_t sm_need = std::max(smem_b, smem_bulk);
     auto kern = RS == 25 ? pool_bwd_wgrad_c1_bulk_kernel<5, 5> : pool_bwd_wgrad_c1_bulk_kernel<3, 3>;
     SYSML_TRY(smem_attr(kern, sm_need));

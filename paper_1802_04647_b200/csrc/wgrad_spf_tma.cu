@@ -13,8 +13,10 @@
 // consecutive A atoms (no halo re-fetch).  All RG accumulators (RG * S*C columns) live
 // in TMEM; split-K over positions, partials reduced in a fixed order.
 //
-// Warp roles: warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 db (during the loop,
-// from the staged dY atoms) and epilogue (TMEM quadrant warp % 4).
+// Warp roles (W2_THREADS = 352): warp 0 = dY (A) TMA producer, warp 6 = X (B) TMA producer
+// of the s % 4 == 0 column taps, warp 1 = MMA issuer, warps 2-5 and 7-10 = helpers that build
+// the other column shifts of each X atom in shared memory; warps 2-5 also sum db from the
+// staged dY atoms during the loop and run the epilogue (TMEM quadrant warp % 4).
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
