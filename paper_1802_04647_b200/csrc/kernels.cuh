@@ -192,6 +192,13 @@ sysml_status launch_maxpool_bwd_spf(const PoolArgs &a, const int32_t *argmax, co
 sysml_status launch_nchw_to_spf(int N, int C, int H, int W, const float *x, float *spf,
                                 int64_t plane, int Wf, int Lf, int off, cudaStream_t st);
 
+// sn_tmem.cu : narrow-filter SN bwd_data with the A operand in TMEM and resident filters
+// (LeNet conv2 bwd_data on SPF planes; output frame Wf x (Lf / Wf))
+bool sn_tmem_supported(const ConvArgs &a, int Wf, int Lf);
+size_t sn_tmem_ws(const ConvArgs &a, int Wf, int Lf);
+sysml_status sn_tmem_bwd_data_spf(const ConvArgs &a, const TcSpfIO &io, int Wf, int Lf, const float *f,
+                                  const float *dy, float *dx, void *ws, cudaStream_t st);
+
 // affine_gemm.cu : the affine layers of the LeNet-512 step (NEXT-4)
 // Fused epilogue of tc_gemm: C = acc (+ bias[col]) (relu) (inverted dropout of unit col of
 // global row row0 + row: Philox4x64-10 stream (seed, *step), kept iff (raw >> 32) < keep_T)

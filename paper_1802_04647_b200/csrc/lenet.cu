@@ -799,6 +799,7 @@ static sysml_status lenet_create_impl(int32_t max_local_batch, int32_t math, int
       need = std::max(need, conv1_pool_ws(a1a, &pa1));
       need = std::max(need, tc_fwd_ws(a2a));
       need = std::max(need, tc_bwd_data_ws(a2a));
+      need = std::max(need, sn_tmem_ws(a2a, 16, 256));
       need = std::max(need, tc_wgrad_spf_ws(sc));
       if (tc_wgrad_spf_tma_supported(sc)) need = std::max(need, tc_wgrad_spf_tma_ws(sc));
       ALLOC(h->a1s, 32 * h->spf_plane);
@@ -1163,7 +1164,11 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
       io.route_Wf = 16;
       io.route_Lf = 256;
     }
-    SYSML_TRY(tc_conv_bwd_data_spf(ca2, io, params + OFF_F2, h->dz2s, h->da1, h->ws, st));
+    static const int sn_tmem_env = getenv("SYSML_SN_TMEM") ? atoi(getenv("SYSML_SN_TMEM")) : 1;
+    if (sn_tmem_env && !io.route_val && sn_tmem_supported(ca2, 16, 256))
+      SYSML_TRY(sn_tmem_bwd_data_spf(ca2, io, 16, 256, params + OFF_F2, h->dz2s, h->da1, h->ws, st));
+    else
+      SYSML_TRY(tc_conv_bwd_data_spf(ca2, io, params + OFF_F2, h->dz2s, h->da1, h->ws, st));
     SYSML_TRY(T.end());
   } else {
     // B2p
