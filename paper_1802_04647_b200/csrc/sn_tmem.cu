@@ -138,18 +138,29 @@ __global__ void __launch_bounds__(ST_THREADS, 1) sn_tmem_kernel(const StParams p
       // blocks of this warp and the next two (one coalesced load each per channel) and copies
       // 1, 3 are half-block shifts of them (one shuffle each): 3 loads per channel, not 5.  The
       // set's next chunk is loaded before the current one is stored (two register buffers).
-      auto load = [&](int64_t q, float (&v)[3][8]) {
-        const int64_t tile = blockIdx.x + (q / p.nchunk) * gridDim.x;
-        const int ch = (int)(q % p.nchunk);
-        const int64_t gm = tile * p.cta_pos + m;
-        const int nc = min(8, p.Cin - ch * 8);
+      // per-channel plane offsets (loop invariant); chunk -> (tile, channel block) is advanced
+      // incrementally (no 64-bit division per chunk): the producers are issue bound
+      int coff[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) coff[c] = c * plane;
+      auto load = [&](int64_t tile, int ch, float (&v)[3][8]) {
+        const int gp = (int)(tile * p.cta_pos) + m + p.in_shift;  // plane position of copy 0
         const float *xc = p.x + (int64_t)(ch * 8) * plane;
+        if (gp >= 0 && gp + 64 < plane && ch * 8 + 8 <= p.Cin) {
+          const float *xb = xc + gp;
 #pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const int64_t sv = gm + 32 * b + p.in_shift;
-          const int sb = (sv >= 0 && sv < p.plane) ? (int)sv : -1;
+          for (int b = 0; b < 3; ++b)
 #pragma unroll
-          for (int c = 0; c < 8; ++c) v[b][c] = (sb >= 0 && c < nc) ? __ldg(xc + (sb + c * plane)) : 0.f;
+            for (int c = 0; c < 8; ++c) v[b][c] = __ldg(xb + (32 * b + coff[c]));
+        } else {
+          const int nc = min(8, p.Cin - ch * 8);
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            const int sv = gp + 32 * b;
+            const bool ok = sv >= 0 && sv < plane;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[b][c] = (ok && c < nc) ? __ldg(xc + (sv + coff[c])) : 0.f;
+          }
         }
       };
       auto store = [&](int64_t q, const float (&v)[3][8]) {
@@ -174,10 +185,15 @@ __global__ void __launch_bounds__(ST_THREADS, 1) sn_tmem_kernel(const StParams p
         ptx::tc_fence_before();
         ptx::mbar_arrive(afull + stage);
       };
+      int64_t tile = blockIdx.x;
+      int ch = set;
+      while (ch >= p.nchunk) { ch -= p.nchunk; tile += gridDim.x; }
       for (int64_t q = set; q < qtot; q += ST_PSETS) {
         float va[3][8];
-        load(q, va);
+        load(tile, ch, va);
         store(q, va);
+        ch += ST_PSETS;
+        while (ch >= p.nchunk) { ch -= p.nchunk; tile += gridDim.x; }
       }
     } else {
       int64_t q = 0;  // CTA-local chunk counter (over all tiles)
