@@ -288,35 +288,36 @@ __global__ void __launch_bounds__(ST_THREADS, 1) sn_tmem_kernel(const StParams p
       ptx::tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + buf * (uint32_t)p.NN;
       for (int c16 = eset; c16 < nc16; c16 += 2) {
-        // 1) the first S-1 rows of this quadrant for every s >= 1 (read by the quadrant above)
-        for (int s_ = 1; s_ < p.S; ++s_) {
-          float t[16];
-          ptx::tmem_ld16(tbase + (uint32_t)(s_ * p.NFpad + c16 * 16), t);
-          if (lane < p.S - 1) {
-            float *dst = xs + xidx(qd, s_, lane);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) dst[j] = t[j];
-          }
-        }
-        ptx::named_bar_sync(2 + eset, 128);
+        // rows l + s of this quadrant by shuffles; lanes < S-1 publish their s >= 1 values for
+        // the quadrant above (every block is loaded once), whose rows l + s >= 32 come from it
         const int k0 = c16 * 16;
         float acc[16];
         ptx::tmem_ld16(tbase + (uint32_t)(c16 * 16), acc);
         for (int s_ = 1; s_ < p.S; ++s_) {
           float t[16];
           ptx::tmem_ld16(tbase + (uint32_t)(s_ * p.NFpad + c16 * 16), t);
+          if (lane < p.S - 1) {
+            float4 *dst = reinterpret_cast<float4 *>(xs + xidx(qd, s_, lane));
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) dst[j4] = make_float4(t[4 * j4], t[4 * j4 + 1], t[4 * j4 + 2], t[4 * j4 + 3]);
+          }
           const bool from_next = lane + s_ >= 32;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const float vv = __shfl_down_sync(0xffffffffu, t[j], s_);
             if (!from_next) acc[j] += vv;
           }
-          if (from_next && qd < 3) {  // rows of the next quadrant (quadrant 3: rows >= cta_pos)
-            const float4 *src = reinterpret_cast<const float4 *>(xs + xidx(qd + 1, s_, lane + s_ - 32));
+        }
+        ptx::named_bar_sync(2 + eset, 128);
+        if (qd < 3) {  // quadrant 3: rows >= cta_pos need no next-quadrant terms
+          for (int s_ = 1; s_ < p.S; ++s_) {
+            if (lane + s_ >= 32) {
+              const float4 *src = reinterpret_cast<const float4 *>(xs + xidx(qd + 1, s_, lane + s_ - 32));
 #pragma unroll
-            for (int j4 = 0; j4 < 4; ++j4) {
-              const float4 u = src[j4];
-              acc[4 * j4] += u.x; acc[4 * j4 + 1] += u.y; acc[4 * j4 + 2] += u.z; acc[4 * j4 + 3] += u.w;
+              for (int j4 = 0; j4 < 4; ++j4) {
+                const float4 u = src[j4];
+                acc[4 * j4] += u.x; acc[4 * j4 + 1] += u.y; acc[4 * j4 + 2] += u.z; acc[4 * j4 + 3] += u.w;
+              }
             }
           }
         }
