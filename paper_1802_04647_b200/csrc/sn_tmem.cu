@@ -29,6 +29,10 @@
 #include "tc_ptx.cuh"
 
 #include <algorithm>
+
+#ifndef SN_DIRECT13
+#define SN_DIRECT13 1  // copies 1, 3 loaded directly (L1 hits) instead of half-warp shuffles: fewer MIO ops
+#endif
 #include <cstdio>
 #include <cstdlib>
 
@@ -143,6 +147,9 @@ __global__ void __launch_bounds__(ST_THREADS, 1) sn_tmem_kernel(const StParams p
       int coff[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) coff[c] = c * plane;
+#if SN_DIRECT13
+      float d1[8], d3[8];
+#endif
       auto load = [&](int64_t tile, int ch, float (&v)[3][8]) {
         const int gp = (int)(tile * p.cta_pos) + m + p.in_shift;  // plane position of copy 0
         const float *xc = p.x + (int64_t)(ch * 8) * plane;
@@ -152,6 +159,13 @@ __global__ void __launch_bounds__(ST_THREADS, 1) sn_tmem_kernel(const StParams p
           for (int b = 0; b < 3; ++b)
 #pragma unroll
             for (int c = 0; c < 8; ++c) v[b][c] = __ldg(xb + (32 * b + coff[c]));
+#if SN_DIRECT13
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            d1[c] = __ldg(xb + (16 + coff[c]));
+            d3[c] = __ldg(xb + (48 + coff[c]));
+          }
+#endif
         } else {
           const int nc = min(8, p.Cin - ch * 8);
 #pragma unroll
@@ -161,11 +175,23 @@ __global__ void __launch_bounds__(ST_THREADS, 1) sn_tmem_kernel(const StParams p
 #pragma unroll
             for (int c = 0; c < 8; ++c) v[b][c] = (ok && c < nc) ? __ldg(xc + (sv + coff[c])) : 0.f;
           }
+#if SN_DIRECT13
+          const int s1 = gp + 16, s3 = gp + 48;
+          const bool ok1 = s1 >= 0 && s1 < plane, ok3 = s3 >= 0 && s3 < plane;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            d1[c] = (ok1 && c < nc) ? __ldg(xc + (s1 + coff[c])) : 0.f;
+            d3[c] = (ok3 && c < nc) ? __ldg(xc + (s3 + coff[c])) : 0.f;
+          }
+#endif
         }
       };
       auto store = [&](int64_t q, const float (&v)[3][8]) {
         const int stage = (int)(q % ST_ASTAGES);
         const uint32_t ph = (uint32_t)((q / ST_ASTAGES) & 1);
+#if SN_DIRECT13
+        float (&w1)[8] = d1, (&w3)[8] = d3;
+#else
         float w1[8], w3[8];
         const int src = (lane + 16) & 31;
 #pragma unroll
@@ -173,6 +199,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) sn_tmem_kernel(const StParams p
           w1[c] = __shfl_sync(0xffffffffu, lane >= 16 ? v[0][c] : v[1][c], src);
           w3[c] = __shfl_sync(0xffffffffu, lane >= 16 ? v[1][c] : v[2][c], src);
         }
+#endif
         ptx::mbar_wait(aempty + stage, ph ^ 1);
         ptx::tc_fence_after();
         const uint32_t ta = trow + acol + (uint32_t)stage * astride;
