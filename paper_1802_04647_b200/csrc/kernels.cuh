@@ -192,6 +192,12 @@ sysml_status launch_maxpool_bwd_spf(const PoolArgs &a, const int32_t *argmax, co
 sysml_status launch_nchw_to_spf(int N, int C, int H, int W, const float *x, float *spf,
                                 int64_t plane, int Wf, int Lf, int off, cudaStream_t st);
 
+// snt_fwd.cu : LeNet conv2 forward + bias + relu + 2x2 pool, SN-T (T = 3) with resident filters
+bool snt_fwd_pool_supported(const ConvArgs &a, const PoolArgs *pool, int Wf, int Lf);
+size_t snt_fwd_pool_ws(const ConvArgs &a);
+sysml_status snt_fwd_pool_spf(const ConvArgs &a, const TcSpfIO &io, const float *x, const float *f,
+                              const float *bias, float *pout, void *ws, cudaStream_t st);
+
 // sn_tmem.cu : narrow-filter SN bwd_data with the A operand in TMEM and resident filters
 // (LeNet conv2 bwd_data on SPF planes; output frame Wf x (Lf / Wf))
 bool sn_tmem_supported(const ConvArgs &a, int Wf, int Lf);

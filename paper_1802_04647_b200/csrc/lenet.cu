@@ -800,6 +800,7 @@ static sysml_status lenet_create_impl(int32_t max_local_batch, int32_t math, int
       need = std::max(need, tc_fwd_ws(a2a));
       need = std::max(need, tc_bwd_data_ws(a2a));
       need = std::max(need, sn_tmem_ws(a2a, 16, 256));
+      need = std::max(need, snt_fwd_pool_ws(a2a));
       need = std::max(need, tc_wgrad_spf_ws(sc));
       if (tc_wgrad_spf_tma_supported(sc)) need = std::max(need, tc_wgrad_spf_tma_ws(sc));
       ALLOC(h->a1s, 32 * h->spf_plane);
@@ -1000,8 +1001,12 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
     io.in_shift = 0;
     io.code = h->c2;
     io.code_plane = c2_plane_of(h->max_b);
-    SYSML_TRY(tc_conv_fwd_spf(ca2, io, h->a1s, params + OFF_F2, params + OFF_B2, nullptr, &pa2, h->a2,
-                              nullptr, h->ws, st));
+    static const int snt_env = getenv("SYSML_F2_SNT") ? atoi(getenv("SYSML_F2_SNT")) : 1;
+    if (snt_env && snt_fwd_pool_supported(ca2, &pa2, 16, 256))
+      SYSML_TRY(snt_fwd_pool_spf(ca2, io, h->a1s, params + OFF_F2, params + OFF_B2, h->a2, h->ws, st));
+    else
+      SYSML_TRY(tc_conv_fwd_spf(ca2, io, h->a1s, params + OFF_F2, params + OFF_B2, nullptr, &pa2, h->a2,
+                                nullptr, h->ws, st));
   } else {
     SYSML_TRY(conv_fwd_dispatch(c2, a1in, params + OFF_F2, params + OFF_B2, nullptr, &p2, h->a2,
                                 h->i2, h->ws, h->ws_bytes, st));
