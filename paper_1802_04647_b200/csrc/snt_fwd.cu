@@ -17,11 +17,11 @@
 // is lanes l, l^1, l^16, l^17 of one warp (reduce-scatter butterfly as in conv_tc.cu).
 // Operand bytes per tap row: 8 KB of A + 10 KB of B over 160 clocks of math (vs 30 KB over 160
 // for five N = 64 MMAs).  The 205 KB packed bank is loaded once per CTA (bulk copies), so the only
-// streamed operand is A: three 6.4 KB stages, K-major no-swizzle [quad][position][4 ch], gathered
-// from the SPF planes by two producer sets (global loads -> 16-byte shared stores).
+// streamed operand is A: four 6.4 KB stages, K-major no-swizzle [quad][position][4 ch], gathered
+// from the SPF planes by three producer sets (global loads -> 16-byte shared stores).
 //
-// Warps (persistent, 1 CTA/SM): 0-7 producers (set = warp / 4 takes chunks q % 2 == set), 8 MMA
-// issuer, 9-16 epilogue (quadrant = warp % 4, channel half = (warp - 9) / 4).
+// Warps (persistent, 1 CTA/SM): 0-11 producers (set = warp / 4 takes chunks q % 3 == set), 12 MMA
+// issuer, 13-20 epilogue (quadrant = warp % 4, channel half = (warp - 13) / 4).
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
@@ -34,11 +34,11 @@ namespace sysml {
 
 namespace {
 
-constexpr int SF_PSETS = 2;
+constexpr int SF_PSETS = 3;
 constexpr int SF_PWARPS = 4 * SF_PSETS;
 constexpr int SF_MMAW = SF_PWARPS;
 constexpr int SF_THREADS = 32 * (SF_PWARPS + 1 + 8);
-constexpr int SF_ASTAGES = 3;
+constexpr int SF_ASTAGES = 4;
 static_assert(SF_PSETS <= SF_ASTAGES, "producer sets would run a full ring ahead");
 constexpr int SF_T = 3;                 // taps s < T in MMA 1, s >= T in MMA 2 (A shifted by T)
 constexpr int SF_NF = 64;               // output channels
