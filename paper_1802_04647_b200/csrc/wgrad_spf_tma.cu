@@ -185,21 +185,21 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         if (sl >= p.nbr) sl -= p.nbr;
         bdesc[a] = sw128(sB + (uint32_t)sl * b_slot);
       }
+      // one elected lane issues the atom's MMAs and commits as one block (a per-MMA elect /
+      // __syncwarp round trip costs more than an N = 160 MMA: tools/mma_snstream.cu)
+      if (ptx::elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < W2_ATOM / 8; ++kk) {
-        const uint32_t acc = (ai | kk) != 0 ? 1u : 0u;
+        for (int kk = 0; kk < W2_ATOM / 8; ++kk) {
+          const uint32_t acc = (ai | kk) != 0 ? 1u : 0u;
 #pragma unroll
-        for (int rb = 0; rb < 4; ++rb) {
-          if (rb < p.RG) {
-            const int t = 8 * kk + rb * shift;  // compile-time when SHIFT != 0
-            const uint64_t bd = bdesc[(t >> 5) & 3] + (uint64_t)((t & 31) >> 2);
-            if (!p.dbg && ptx::elect_one())
-              ptx::mma_tf32(tmem + rb * p.N, adesc + (uint64_t)(kk * 2), bd, idesc, acc);
-            __syncwarp();
+          for (int rb = 0; rb < 4; ++rb) {
+            if (rb < p.RG) {
+              const int t = 8 * kk + rb * shift;  // compile-time when SHIFT != 0
+              const uint64_t bd = bdesc[(t >> 5) & 3] + (uint64_t)((t & 31) >> 2);
+              if (!p.dbg) ptx::mma_tf32(tmem + rb * p.N, adesc + (uint64_t)(kk * 2), bd, idesc, acc);
+            }
           }
         }
-      }
-      if (ptx::elect_one()) {
         ptx::mma_commit(emptyA + sa);
         ptx::mma_commit(emptyB + s_ai);  // B atom ai has no later user
       }
