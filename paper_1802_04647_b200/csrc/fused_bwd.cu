@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(FBB_THREADS, 2)
       const float *gk = gs + kk * gsk;
       const unsigned long long *ck = cs + (kk >> 4) * PpQp;
       const int sh = 4 * (kk & 15);
+#pragma unroll 2
       for (int pp = wq; pp < PpQp; pp += FB_THREADS / 32) {
         const float g0 = gk[pp * gsp];
         const uint32_t cd = (uint32_t)(ck[pp] >> sh) & 15u;
