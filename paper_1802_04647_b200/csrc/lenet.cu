@@ -928,6 +928,7 @@ static sysml_status lenet_run(sysml_lenet *h, const float *params, const sysml_i
                               float *grads, float *loss_sum, sysml_stream_t stream, int32_t *pred,
                               float *probs) {
   SYSML_CHECK_ARG(h && params && x && ((labels && grads) || pred || probs), "NULL argument to sysml_lenet_fwd_bwd / predict");
+  route_reset();  // sysml_last_route then lists this call's kernels
   SYSML_CHECK_ARG(n_local >= 1 && n_local <= h->max_b,
                   "n_local %d out of range [1, max_local_batch=%d]", n_local, h->max_b);
   SYSML_CHECK_ARG(n_global >= n_local, "n_global %lld < n_local %d", (long long)n_global, n_local);

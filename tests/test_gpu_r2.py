@@ -444,3 +444,32 @@ def test_lenet_routed_b2d_opt_in_parity(S):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("env", [{"SYSML_F2_SNT": "0"}, {"SYSML_SN_TMEM": "0"}, {"SYSML_F2_SNT": "0", "SYSML_SN_TMEM": "0"}])
+def test_lenet_kernel_fallbacks_match_oracle(S, env):
+    """The LeNet step's dedicated conv2 kernels (snt_fwd_pool_kernel for F2, sn_tmem_kernel for
+    B2d) have general-kernel fallbacks (K3 / K6 SN); with either switched off the step must still
+    equal the oracle exactly on dyadic inputs (TF32), and the route log must name the fallback."""
+    import subprocess, sys
+    code = ("import tests.test_gpu_parity as T, paper_1802_04647_b200 as S, numpy as np, torch, oracle;"
+            "x,y,prm=T._lenet_case(37, True);"
+            "g_ref,_=oracle.lenet_fwd_bwd(x,y,prm,n_global=40);"
+            "net=S.LeNet(40, math='tf32'); g=torch.empty(83466,device='cuda');"
+            "net.fwd_bwd(T.dev(prm),T.dev(x),T.dev(y,torch.int32),40,g);"
+            "T.assert_close(T.host(g),g_ref,T.TOL['tf32'],'fallback');print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_lenet_dedicated_conv2_kernels_route(S):
+    """The default LeNet step runs F2 on snt_fwd_pool_kernel and B2d on sn_tmem_kernel (route log)."""
+    import tests.test_gpu_parity as T
+    x, y, prm = T._lenet_case(40, True)
+    net = S.LeNet(40, math="tf32")
+    g = torch.empty(83466, device="cuda")
+    net.fwd_bwd(T.dev(prm), T.dev(x), T.dev(y, torch.int32), 40, g)
+    torch.cuda.synchronize()
+    routes = S.sysml_last_route()
+    assert "snt_fwd_pool_kernel" in routes and "sn_tmem_kernel" in routes, routes
