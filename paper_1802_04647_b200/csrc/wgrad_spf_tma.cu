@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       int sa = 0;
       uint32_t pa = 0;
       for (int ia = 0; ia < (int)nA; ++ia) {
-        const long long t0 = clock64();
+        const long long t0 = p.clk ? clock64() : 0;
         ptx::mbar_wait(emptyA + sa, pa ^ 1);
         if (p.clk) p.clk[blockIdx.x * 8 + 4] += clock64() - t0;
         // the bytes the copies below deliver: copies x Kc rows (< 128 rows when copies*Kc < 128;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       int sb = 0;
       uint32_t pb = 0;
       for (int ib = 0; ib < nBt; ++ib) {
-        const long long t0 = clock64();
+        const long long t0 = p.clk ? clock64() : 0;
         ptx::mbar_wait(emptyB + sb, pb ^ 1);
         if (p.clk) p.clk[blockIdx.x * 8 + 5] += clock64() - t0;
         ptx::mbar_arrive_expect_tx(fullBt + sb, (uint32_t)(p.ntma_s * p.Ct * 128));
@@ -165,9 +165,9 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
     // positions 8*kk + rb*shift (constant across atoms)
     const int shift = SHIFT ? SHIFT : p.shift;
     for (int ai = 0; ai < (int)nA; ++ai) {
-      const long long t0 = clock64();
+      const long long t0 = p.clk ? clock64() : 0;
       ptx::mbar_wait(fullA + sa, pa);
-      const long long t1 = clock64();
+      const long long t1 = p.clk ? clock64() : 0;
       ptx::mbar_wait(fullB + sbw, pbw);  // newest B atom this group needs (ai + L)
       if (++sbw == p.nbr) { sbw = 0; pbw ^= 1; }
       if (p.clk && lane == 0) {
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       if (bi < nB) {
         const int slot = sb, slot1 = sb + 1 == p.nbr ? 0 : sb + 1;
         const uint32_t ph1 = sb + 1 == p.nbr ? pb ^ 1 : pb;
-        const long long t0 = clock64();
+        const long long t0 = p.clk ? clock64() : 0;
         ptx::mbar_wait(fullBt + slot, pb);
         ptx::mbar_wait(fullBt + slot1, ph1);
         if (p.clk && et == 0) p.clk[blockIdx.x * 8 + 2] += clock64() - t0;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       }
       if (step >= 0 && do_db && main_helper) {
         const int slotA = sa;
-        const long long t0 = clock64();
+        const long long t0 = p.clk ? clock64() : 0;
         ptx::mbar_wait(fullA + slotA, pa);
         if (++sa == W2_NA) { sa = 0; pa ^= 1; }
         if (p.clk && et == 0) p.clk[blockIdx.x * 8 + 3] += clock64() - t0;
