@@ -34,14 +34,12 @@ namespace sysml {
 
 namespace {
 
-// producer sets / epilogue sets (2 / 4 in pair mode starved the MMA of A stages: 412 us)
-constexpr int sf_psets(int pair) { return pair ? 3 : 3; }
-constexpr int sf_esets(int pair) { return pair ? 2 : 2; }
-constexpr int sf_mmaw(int pair) { return 4 * sf_psets(pair); }
-constexpr int sf_threads(int pair) { return 32 * (4 * sf_psets(pair) + 1 + 4 * sf_esets(pair)); }
+constexpr int SF_PSETS = 3;
+constexpr int SF_PWARPS = 4 * SF_PSETS;
+constexpr int SF_MMAW = SF_PWARPS;
+constexpr int SF_THREADS = 32 * (SF_PWARPS + 1 + 8);
 constexpr int SF_ASTAGES = 4;
-constexpr int SF_ASTAGES_PAIR = 8;  // half banks leave room for eight A stages
-static_assert(sf_psets(0) <= SF_ASTAGES, "producer sets would run a full ring ahead");
+static_assert(SF_PSETS <= SF_ASTAGES, "producer sets would run a full ring ahead");
 constexpr int SF_T = 3;                 // taps s < T in MMA 1, s >= T in MMA 2 (A shifted by T)
 constexpr int SF_NF = 64;               // output channels
 constexpr int SF_S = 5, SF_R = 5, SF_WF = 16;
@@ -52,38 +50,6 @@ constexpr int SF_HALO = 200;            // staged positions: 128 + (R-1)*Wf + T 
 constexpr uint32_t SF_QUAD_BYTES = SF_HALO * 16;
 constexpr uint32_t SF_STAGE_BYTES = 2 * SF_QUAD_BYTES;
 constexpr uint32_t SF_ACC_STRIDE = 256;  // TMEM columns per accumulator buffer (N1 = 192 used)
-
-// CTA-pair helpers (cta_group::2; semantics validated by tools/mma_pair.cu)
-__device__ __forceinline__ void mma_tf32_pair(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                              uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void commit_pair_mc(uint64_t *bar) {  // arrives on `bar` in both CTAs
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          ptx::smem_u32(bar)),
-      "h"((uint16_t)3)
-      : "memory");
-}
-__device__ __forceinline__ void arrive_rank0(uint64_t *bar) {  // the same barrier in CTA rank 0
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(ptx::smem_u32(bar)));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
-}
-__device__ __forceinline__ void wait_acq_cluster(uint64_t *bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done)
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(ptx::smem_u32(bar)), "r"(parity)
-        : "memory");
-}
 
 struct SfParams {
   const float *x;       // SPF planes [Cin][plane], stored position = frame position + in_shift
@@ -100,92 +66,63 @@ struct SfParams {
   long long *clk;
 };
 
-// PAIR = 1: a CTA pair (cluster of 2) issues M = 256 MMAs (cta_group::2).  CTA rank h stages
-// the A rows of tile 2u + h and holds HALF of every B block (MMA 1: rows [96h, 96h + 96), MMA 2:
-// [64h, 64h + 64) of the N = 192 / 128 blocks) at the same shared-memory offset, so each CTA's
-// shared memory feeds 8 KB of A + 5 KB of B per tap row (was 18 KB).  Rank 0 issues; both CTAs'
-// producers and epilogues signal rank 0's barriers; commits multicast to both CTAs.
-template <int PAIR>
-__global__ void __launch_bounds__(sf_threads(PAIR), 1) snt_fwd_pool_kernel(const SfParams p) {
-  constexpr int NS = PAIR ? SF_ASTAGES_PAIR : SF_ASTAGES;
-  constexpr int PSETS = sf_psets(PAIR), ESETS = sf_esets(PAIR), MMAW = sf_mmaw(PAIR), PWARPS = 4 * PSETS;
-  static_assert(PSETS <= NS, "producer sets would run a full ring ahead");
+__global__ void __launch_bounds__(SF_THREADS, 1) snt_fwd_pool_kernel(const SfParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint8_t *Bs = smem;
   uint8_t *As = smem + p.b_bytes;  // b_bytes is a multiple of 1024
-  float *bias_s = reinterpret_cast<float *>(As + NS * SF_STAGE_BYTES);
+  float *bias_s = reinterpret_cast<float *>(As + SF_ASTAGES * SF_STAGE_BYTES);
   uint64_t *bars = reinterpret_cast<uint64_t *>(bias_s + SF_NF);
   uint64_t *bfull = bars;
-  uint64_t *afull = bars + 1;               // [NS]
-  uint64_t *aempty = afull + NS;            // [NS]
-  uint64_t *accf = aempty + NS;             // [2]
+  uint64_t *afull = bars + 1;               // [SF_ASTAGES]
+  uint64_t *aempty = afull + SF_ASTAGES;    // [SF_ASTAGES]
+  uint64_t *accf = aempty + SF_ASTAGES;     // [2]
   uint64_t *acce = accf + 2;                // [2]
   uint32_t *tslot = reinterpret_cast<uint32_t *>(acce + 2);
 
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     ptx::mbar_init(bfull, 1);
-    for (int s = 0; s < NS; ++s) {
-      ptx::mbar_init(afull + s, PAIR ? 8 : 128);  // PAIR: lane 0 of one set's 4 warps x 2 CTAs
-      ptx::mbar_init(aempty + s, 1);              // tcgen05.commit (multicast in PAIR mode)
+    for (int s = 0; s < SF_ASTAGES; ++s) {
+      ptx::mbar_init(afull + s, 128);  // one producer set
+      ptx::mbar_init(aempty + s, 1);   // tcgen05.commit
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(accf + b, 1);
-      ptx::mbar_init(acce + b, (PAIR ? 2 : 1) * 4 * ESETS);  // the epilogue warps (of both CTAs)
+      ptx::mbar_init(acce + b, 8);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == MMAW) {
-    if (PAIR) {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(tslot)),
-                   "r"(512)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    } else {
-      ptx::tmem_alloc(tslot, 512);
-    }
-  }
+  if (warp == SF_MMAW) ptx::tmem_alloc(tslot, 512);
   ptx::tc_fence_before();
   __syncthreads();
-  if (PAIR) ptx::cluster_sync();  // both CTAs' barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
-  // work units: tiles, or pair tiles (2 tiles; this CTA's tile = 2u + rank)
-  const int64_t cid = PAIR ? blockIdx.x / 2 : blockIdx.x, ncl = PAIR ? gridDim.x / 2 : gridDim.x;
-  const int64_t nunits = PAIR ? p.ntiles / 2 : p.ntiles;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // packed filters and a1 ready (PDL)
   for (int k = threadIdx.x; k < SF_NF; k += blockDim.x) bias_s[k] = p.bias ? p.bias[k] : 0.f;
   if (threadIdx.x == 0) {
     ptx::mbar_arrive_expect_tx(bfull, p.b_bytes);
-    const uint8_t *src = reinterpret_cast<const uint8_t *>(p.fp) + (size_t)rank * p.b_bytes;  // PAIR: this half
     for (uint32_t off = 0; off < p.b_bytes; off += 32768u) {
       const uint32_t nb = min(32768u, p.b_bytes - off);
-      ptx::bulk_g2s(const_cast<uint8_t *>(Bs) + off, src + off, nb, bfull);
+      ptx::bulk_g2s(const_cast<uint8_t *>(Bs) + off, reinterpret_cast<const uint8_t *>(p.fp) + off, nb, bfull);
     }
   }
   __syncthreads();  // bias_s visible to the epilogue
-  if (PAIR) {  // both halves of the bank resident before rank 0 issues (barrier.cluster: all threads)
-    ptx::mbar_wait(bfull, 0);
-    ptx::cluster_sync();
-  }
 
-  if (warp < PWARPS) {
+  if (warp < SF_PWARPS) {
     // ================= producers: thread t of the set stages positions t and t + 128 (< HALO)
     const int set = warp >> 2, t = (warp & 3) * 32 + lane;
     const int plane = (int)p.plane;  // Cin * plane < 2^31 (launcher)
-    const int64_t my_units = nunits > cid ? (nunits - 1 - cid) / ncl + 1 : 0;
-    const int64_t qtot = my_units * p.nchunk;
+    const int64_t my_tiles = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t qtot = my_tiles * p.nchunk;
     int coff[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) coff[c] = c * plane;
-    int64_t unit = cid;
+    int64_t tile = blockIdx.x;
     int ch = set;
-    while (ch >= p.nchunk) { ch -= p.nchunk; unit += ncl; }
-    for (int64_t q = set; q < qtot; q += PSETS) {
-      const int stage = (int)(q % NS);
-      const uint32_t ph = (uint32_t)((q / NS) & 1);
-      const int64_t tile = PAIR ? 2 * unit + rank : unit;
+    while (ch >= p.nchunk) { ch -= p.nchunk; tile += gridDim.x; }
+    for (int64_t q = set; q < qtot; q += SF_PSETS) {
+      const int stage = (int)(q % SF_ASTAGES);
+      const uint32_t ph = (uint32_t)((q / SF_ASTAGES) & 1);
       const int g0 = (int)(tile * 128) + p.in_shift;
       const float *xc = p.x + (int64_t)(ch * 8) * plane;
       float v[2][8];
@@ -209,94 +146,68 @@ __global__ void __launch_bounds__(sf_threads(PAIR), 1) snt_fwd_pool_kernel(const
         }
       }
       ptx::fence_proxy_async_smem();
-      if (PAIR) {
-        __syncwarp();
-        if (lane == 0) arrive_rank0(afull + stage);  // release.cluster: this warp's stores
-      } else {
-        ptx::mbar_arrive(afull + stage);
-      }
-      ch += PSETS;
-      while (ch >= p.nchunk) { ch -= p.nchunk; unit += ncl; }
+      ptx::mbar_arrive(afull + stage);
+      ch += SF_PSETS;
+      while (ch >= p.nchunk) { ch -= p.nchunk; tile += gridDim.x; }
     }
-  } else if (warp == MMAW) {
-    // ================= MMA issuer (rank 0 only in PAIR mode): one elected lane issues each
-    // chunk's 2*R MMAs and the commit
-    if (PAIR && rank != 0) {
-      // nothing to issue
-    } else {
-      ptx::mbar_wait(bfull, 0);
+  } else if (warp == SF_MMAW) {
+    // ================= MMA issuer: one elected lane issues each chunk's 2*R MMAs and the commit
+    ptx::mbar_wait(bfull, 0);
+    ptx::tc_fence_after();
+    const uint32_t idesc1 = ptx::make_idesc_tf32(128, SF_N1), idesc2 = ptx::make_idesc_tf32(128, SF_N2);
+    const uint32_t bbase = ptx::smem_u32(Bs), abase = ptx::smem_u32(As);
+    int64_t q = 0;
+    uint32_t tcount = 0;
+    long long t_acce = 0, t_afull = 0;
+    const long long t_start = clock64();
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++tcount) {
+      const uint32_t buf = tcount & 1u, bph = (tcount >> 1) & 1u;
+      const long long t0 = clock64();
+      ptx::mbar_wait(acce + buf, bph ^ 1);
+      t_acce += clock64() - t0;
       ptx::tc_fence_after();
-      const int MM = PAIR ? 256 : 128;
-      const uint32_t idesc1 = ptx::make_idesc_tf32(MM, SF_N1), idesc2 = ptx::make_idesc_tf32(MM, SF_N2);
-      // B rows per (chunk, r) block in this CTA's shared memory and the MMA 2 offset
-      constexpr uint32_t BROWS = PAIR ? (SF_N1 + SF_N2) / 2 : SF_NN, B2OFF = PAIR ? SF_N1 / 2 : SF_N1;
-      const uint32_t bbase = ptx::smem_u32(Bs), abase = ptx::smem_u32(As);
-      int64_t q = 0;
-      uint32_t tcount = 0;
-      long long t_acce = 0, t_afull = 0;
-      const long long t_start = clock64();
-      for (int64_t unit = cid; unit < nunits; unit += ncl, ++tcount) {
-        const uint32_t buf = tcount & 1u, bph = (tcount >> 1) & 1u;
-        const long long t0 = p.clk ? clock64() : 0;
-        if (PAIR) wait_acq_cluster(acce + buf, bph ^ 1);
-        else ptx::mbar_wait(acce + buf, bph ^ 1);
-        if (p.clk) t_acce += clock64() - t0;
+      const uint32_t d = tmem + buf * SF_ACC_STRIDE;
+      for (int ch = 0; ch < p.nchunk; ++ch, ++q) {
+        const int stage = (int)(q % SF_ASTAGES);
+        const long long t1 = clock64();
+        ptx::mbar_wait(afull + stage, (uint32_t)((q / SF_ASTAGES) & 1));
+        t_afull += clock64() - t1;
         ptx::tc_fence_after();
-        const uint32_t d = tmem + buf * SF_ACC_STRIDE;
-        for (int ch = 0; ch < p.nchunk; ++ch, ++q) {
-          const int stage = (int)(q % NS);
-          const long long t1 = p.clk ? clock64() : 0;
-          if (PAIR) wait_acq_cluster(afull + stage, (uint32_t)((q / NS) & 1));
-          else ptx::mbar_wait(afull + stage, (uint32_t)((q / NS) & 1));
-          if (p.clk) t_afull += clock64() - t1;
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-            const uint32_t a0 = abase + (uint32_t)stage * SF_STAGE_BYTES;
-            const uint32_t b0 = bbase + (uint32_t)(ch * SF_R) * (2u * BROWS * 16u);
-#pragma unroll
-            for (int r = 0; r < SF_R; ++r) {
-              const uint32_t ar = a0 + (uint32_t)(r * SF_WF) * 16u;
-              const uint32_t br = b0 + (uint32_t)r * (2u * BROWS * 16u);
-              const uint64_t ad1 = ptx::make_desc(ar, SF_QUAD_BYTES, 128);
-              const uint64_t ad2 = ptx::make_desc(ar + SF_T * 16u, SF_QUAD_BYTES, 128);
-              const uint64_t bd1 = ptx::make_desc(br, BROWS * 16u, 128);
-              const uint64_t bd2 = ptx::make_desc(br + B2OFF * 16u, BROWS * 16u, 128);
-              if (PAIR) {
-                mma_tf32_pair(d, ad1, bd1, idesc1, (ch | r) ? 1u : 0u);
-                mma_tf32_pair(d, ad2, bd2, idesc2, 1u);
-              } else {
-                ptx::mma_tf32(d, ad1, bd1, idesc1, (ch | r) ? 1u : 0u);
-                ptx::mma_tf32(d, ad2, bd2, idesc2, 1u);
-              }
-            }
-            if (PAIR) commit_pair_mc(aempty + stage);
-            else ptx::mma_commit(aempty + stage);
-          }
-          __syncwarp();
-        }
         if (ptx::elect_one()) {
-          if (PAIR) commit_pair_mc(accf + buf);
-          else ptx::mma_commit(accf + buf);
+          const uint32_t a0 = abase + (uint32_t)stage * SF_STAGE_BYTES;
+          const uint32_t b0 = bbase + (uint32_t)(ch * SF_R) * (2u * SF_NN * 16u);
+#pragma unroll
+          for (int r = 0; r < SF_R; ++r) {
+            const uint32_t ar = a0 + (uint32_t)(r * SF_WF) * 16u;
+            const uint32_t br = b0 + (uint32_t)r * (2u * SF_NN * 16u);
+            const uint64_t ad1 = ptx::make_desc(ar, SF_QUAD_BYTES, 128);
+            const uint64_t ad2 = ptx::make_desc(ar + SF_T * 16u, SF_QUAD_BYTES, 128);
+            const uint64_t bd1 = ptx::make_desc(br, SF_NN * 16u, 128);
+            const uint64_t bd2 = ptx::make_desc(br + SF_N1 * 16u, SF_NN * 16u, 128);
+            ptx::mma_tf32(d, ad1, bd1, idesc1, (ch | r) ? 1u : 0u);
+            ptx::mma_tf32(d, ad2, bd2, idesc2, 1u);
+          }
+          ptx::mma_commit(aempty + stage);
         }
         __syncwarp();
       }
-      if (p.clk && lane == 0) {
-        p.clk[blockIdx.x * 4 + 0] = t_acce;
-        p.clk[blockIdx.x * 4 + 1] = t_afull;
-        p.clk[blockIdx.x * 4 + 2] = clock64() - t_start;
-      }
+      if (ptx::elect_one()) ptx::mma_commit(accf + buf);
+      __syncwarp();
+    }
+    if (p.clk && lane == 0) {
+      p.clk[blockIdx.x * 4 + 0] = t_acce;
+      p.clk[blockIdx.x * 4 + 1] = t_afull;
+      p.clk[blockIdx.x * 4 + 2] = clock64() - t_start;
     }
   } else {
     // ================= epilogue: SN-T shift-add, bias, relu, 2x2 pool, codes
-    const int qd = warp & 3, eh = (warp - MMAW - 1) >> 2;  // channels [eh * 64 / ESETS, +64 / ESETS)
+    const int qd = warp & 3, eh = (warp - SF_MMAW - 1) >> 2;  // channel half [32*eh, +32)
     const int PpQp = p.Pp * p.Qp;
     const uint32_t odd_c = lane & 1, odd_r = (lane >> 4) & 1;
     const int cb = (int)(odd_c * 8 + odd_r * 4);  // first of the 4 channels this lane ends with
     const int col = lane & 15;
     uint32_t tcount = 0;
-    long long t_ework = 0, t_eld = 0;
-    for (int64_t unit = cid; unit < nunits; unit += ncl, ++tcount) {
-      const int64_t tile = PAIR ? 2 * unit + rank : unit;
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++tcount) {
       const uint32_t buf = tcount & 1u, bph = (tcount >> 1) & 1u;
       const int grow = (int)(tile * 8) + qd * 2 + (int)odd_r;  // global frame row
       const int n = grow / p.Hs, hh = grow - n * p.Hs;
@@ -304,20 +215,17 @@ __global__ void __launch_bounds__(sf_threads(PAIR), 1) snt_fwd_pool_kernel(const
       const bool store = n < p.N && pp < p.Pp && pc < p.Qp;
       const int64_t wi = store ? (int64_t)n * PpQp + pp * p.Qp + pc : 0;  // window index
       ptx::mbar_wait_sleep(accf + buf, bph);
-      const long long e1 = p.clk ? clock64() : 0;
       __syncwarp();
       ptx::tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + buf * SF_ACC_STRIDE;
 #pragma unroll 1
-      for (int g = eh * (SF_NF / 16 / ESETS); g < (eh + 1) * (SF_NF / 16 / ESETS); ++g) {  // contiguous groups
-        const int k0 = g * 16;
+      for (int g = 0; g < 2; ++g) {
+        const int k0 = eh * 32 + g * 16;
         uint32_t r0[16], r1[16], r2[16];
-        const long long l0 = p.clk ? clock64() : 0;
         ptx::tmem_ld16_issue(tbase + (uint32_t)k0, r0);
         ptx::tmem_ld16_issue(tbase + (uint32_t)(SF_NF + k0), r1);
         ptx::tmem_ld16_issue(tbase + (uint32_t)(2 * SF_NF + k0), r2);
         ptx::tmem_ld_wait(r0);
-        if (p.clk) t_eld += clock64() - l0;
         ptx::tmem_ld_pin(r1);
         ptx::tmem_ld_pin(r2);
         uint32_t u[16];
@@ -364,55 +272,29 @@ __global__ void __launch_bounds__(sf_threads(PAIR), 1) snt_fwd_pool_kernel(const
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        if (PAIR) arrive_rank0(acce + buf);
-        else ptx::mbar_arrive(acce + buf);
-      }
-      if (p.clk) t_ework += clock64() - e1;
-    }
-    if (p.clk && warp == MMAW + 1 && lane == 0) {
-      p.clk[blockIdx.x * 4 + 3] = t_ework;
-      p.clk[2048 + blockIdx.x] = t_eld;
+      if (lane == 0) ptx::mbar_arrive(acce + buf);
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (PAIR) ptx::cluster_sync();  // no CTA frees TMEM or exits while its peer may still signal it
-  if (warp == MMAW) {
+  if (warp == SF_MMAW) {
     ptx::tc_fence_after();
-    if (PAIR)
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
-    else
-      ptx::tmem_dealloc(tmem, 512);
+    ptx::tmem_dealloc(tmem, 512);
   }
 }
 
 // packed(chunk, r, quad, n, e) = F[k][c = chunk*8 + quad*4 + e][r][s]: n < N1 -> (s = n / 64,
-// k = n % 64); n >= N1 -> (s = T + (n - N1) / 64, k = (n - N1) % 64).  Pair layout: two halves
-// [h][chunk][r][quad][160][4], half h holding MMA 1 rows [96h, +96) then MMA 2 rows [64h, +64).
-__global__ void snt_fwd_pack_kernel(const float *__restrict__ f, float *__restrict__ fp, int Cin, int nchunk,
-                                    int pair) {
+// k = n % 64); n >= N1 -> (s = T + (n - N1) / 64, k = (n - N1) % 64)
+__global__ void snt_fwd_pack_kernel(const float *__restrict__ f, float *__restrict__ fp, int Cin, int nchunk) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t total = (int64_t)nchunk * SF_R * 2 * SF_NN * 4;
-  constexpr int HR = SF_NN / 2;  // rows per half block (160)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = i;
     const int e = (int)(t % 4); t /= 4;
-    int n;
-    int g, r, ch;
-    if (pair) {
-      const int nh = (int)(t % HR); t /= HR;
-      g = (int)(t % 2); t /= 2;
-      r = (int)(t % SF_R); t /= SF_R;
-      ch = (int)(t % nchunk); t /= nchunk;
-      const int h = (int)t;
-      n = nh < SF_N1 / 2 ? h * (SF_N1 / 2) + nh : SF_N1 + h * (SF_N2 / 2) + (nh - SF_N1 / 2);
-    } else {
-      n = (int)(t % SF_NN); t /= SF_NN;
-      g = (int)(t % 2); t /= 2;
-      r = (int)(t % SF_R); t /= SF_R;
-      ch = (int)t;
-    }
+    const int n = (int)(t % SF_NN); t /= SF_NN;
+    const int g = (int)(t % 2); t /= 2;
+    const int r = (int)(t % SF_R); t /= SF_R;
+    const int ch = (int)t;
     const int s_ = n < SF_N1 ? n / SF_NF : SF_T + (n - SF_N1) / SF_NF;
     const int k = n < SF_N1 ? n % SF_NF : (n - SF_N1) % SF_NF;
     const int c = ch * 8 + g * 4 + e;
@@ -421,9 +303,8 @@ __global__ void snt_fwd_pack_kernel(const float *__restrict__ f, float *__restri
 }
 
 size_t sf_b_bytes(int Cin) { return (size_t)((Cin + 7) / 8) * SF_R * 2 * SF_NN * 16; }
-size_t sf_smem(int Cin, int pair) {
-  const int ns = pair ? SF_ASTAGES_PAIR : SF_ASTAGES;
-  return sf_b_bytes(Cin) / (pair ? 2 : 1) + ns * SF_STAGE_BYTES + SF_NF * 4 + 8 * (1 + 2 * ns + 4) + 16;
+size_t sf_smem(int Cin) {
+  return sf_b_bytes(Cin) + SF_ASTAGES * SF_STAGE_BYTES + SF_NF * 4 + 8 * (1 + 2 * SF_ASTAGES + 4) + 16;
 }
 
 }  // namespace
@@ -435,7 +316,7 @@ bool snt_fwd_pool_supported(const ConvArgs &a, const PoolArgs *pool, int Wf, int
   if (!pool || pool->R != 2 || pool->S != 2 || pool->sh != 2 || pool->sw != 2 || pool->ph || pool->pw) return false;
   if (a.K != SF_NF || a.R != SF_R || a.S != SF_S || a.sh != 1 || a.sw != 1 || a.ph != 2 || a.pw != 2) return false;
   if (a.H != 14 || a.W != 14 || Wf != SF_WF || Lf != 256 || a.C > 64) return false;
-  return sf_smem(a.C, 0) <= 227 * 1024;
+  return sf_smem(a.C) <= 227 * 1024;
 }
 
 size_t snt_fwd_pool_ws(const ConvArgs &a) { return align_up(sf_b_bytes(a.C), 256); }
@@ -461,62 +342,44 @@ sysml_status snt_fwd_pool_spf(const ConvArgs &a, const TcSpfIO &io, const float 
   p.Pp = 7;
   p.Qp = 7;
   p.ntiles = (int64_t)a.N * 2;  // 256 frame positions per image
-  // the pair mode is exact but not faster: its MMAs retire a tile per CTA every ~3200 clocks and
-  // the epilogue (shuffle / LSU bound, ~3800 clocks per tile) becomes the limit
-  static const int pair_env = getenv("SYSML_F2_PAIR") ? atoi(getenv("SYSML_F2_PAIR")) : 0;
-  const int pair = pair_env && sm_count() >= 2 ? 1 : 0;  // pair units = images (2 tiles each)
-  p.b_bytes = (uint32_t)(sf_b_bytes(a.C) / (pair ? 2 : 1));
+  p.b_bytes = (uint32_t)sf_b_bytes(a.C);
   float *fp = reinterpret_cast<float *>(ws);
   {
     const int64_t total = (int64_t)p.nchunk * SF_R * 2 * SF_NN * 4;
     snt_fwd_pack_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4 * sm_count()), 256, 0, st>>>(
-        f, fp, a.C, p.nchunk, pair);
+        f, fp, a.C, p.nchunk);
     SYSML_LAUNCH_CHECK();
   }
   p.fp = fp;
-  const size_t smem = sf_smem(a.C, pair);
-  auto kern = pair ? snt_fwd_pool_kernel<1> : snt_fwd_pool_kernel<0>;
-  SYSML_TRY(smem_attr(kern, smem));
-  const int64_t units = pair ? a.N : p.ntiles;
-  int grid = (int)std::min<int64_t>(units, pair ? sm_count() / 2 : sm_count());
-  if (pair) grid *= 2;
+  const size_t smem = sf_smem(a.C);
+  SYSML_TRY(smem_attr(snt_fwd_pool_kernel, smem));
+  const int grid = (int)std::min<int64_t>(p.ntiles, sm_count());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(sf_threads(pair));
+  cfg.blockDim = dim3(SF_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
-  at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = pair ? 2 : 1;
-  at[1].val.clusterDim.y = 1;
-  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
-  route_note("snt_fwd_pool_kernel [tcgen05 TF32, SN-T T=3 (N = 192 + 128), resident filters, fused pool%s, %lld tiles on %d CTAs]",
-             pair ? ", cta_group::2 pairs (M = 256, half banks)" : "", (long long)p.ntiles, grid);
+  cfg.numAttrs = 1;
+  route_note("snt_fwd_pool_kernel [tcgen05 TF32, SN-T T=3 (N = 192 + 128), resident filters, fused pool, %lld tiles on %d CTAs]",
+             (long long)p.ntiles, grid);
   static long long *dclk = nullptr;
   const bool prof = getenv("SYSML_TC_PROFILE") != nullptr;
   if (prof && !dclk) cudaMalloc(&dclk, sizeof(long long) * 4 * 1024);
   p.clk = prof ? dclk : nullptr;
-  SYSML_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+  SYSML_CUDA(cudaLaunchKernelEx(&cfg, snt_fwd_pool_kernel, p));
   SYSML_LAUNCH_CHECK();
   if (prof) {
     static long long h[4 * 1024];
     cudaMemcpyAsync(h, dclk, sizeof(long long) * 4 * 1024, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    double s4[4] = {0, 0, 0, 0};
-    const int step = pair ? 2 : 1;  // issuing CTAs
-    for (int b = 0; b < grid; b += step)
-      for (int j = 0; j < 3; ++j) s4[j] += (double)h[b * 4 + j] / (grid / step);
-    double eld = 0;
-    for (int b = 0; b < grid; ++b) {
-      s4[3] += (double)h[b * 4 + 3] / grid;
-      eld += (double)h[2048 + b] / grid;
-    }
-    fprintf(stderr, "[snt_fwd] mma_wait_acce %.0f mma_wait_afull %.0f mma_total %.0f epi_work %.0f epi_tmem_ld %.0f\n",
-            s4[0], s4[1], s4[2], s4[3], eld);
+    double s3[3] = {0, 0, 0};
+    for (int b = 0; b < grid; ++b)
+      for (int j = 0; j < 3; ++j) s3[j] += (double)h[b * 4 + j] / grid;
+    fprintf(stderr, "[snt_fwd] mma_wait_acce %.0f mma_wait_afull %.0f mma_total %.0f\n", s3[0], s3[1], s3[2]);
   }
   return SYSML_OK;
 }

@@ -474,18 +474,3 @@ def test_lenet_dedicated_conv2_kernels_route(S):
     routes = S.sysml_last_route()
     assert "snt_fwd_pool_kernel" in routes and "sn_tmem_kernel" in routes, routes
 
-
-def test_lenet_f2_pair_mode_opt_in(S):
-    """SYSML_F2_PAIR=1 runs F2 as cta_group::2 pairs (M = 256, half filter banks per CTA, remote
-    mbarrier arrives, multicast commits); the step must equal the oracle exactly on dyadic inputs."""
-    import subprocess, sys
-    code = ("import tests.test_gpu_parity as T, paper_1802_04647_b200 as S, numpy as np, torch, oracle;"
-            "x,y,prm=T._lenet_case(37, True);"
-            "g_ref,_=oracle.lenet_fwd_bwd(x,y,prm,n_global=40);"
-            "net=S.LeNet(40, math='tf32'); g=torch.empty(83466,device='cuda');"
-            "net.fwd_bwd(T.dev(prm),T.dev(x),T.dev(y,torch.int32),40,g);"
-            "assert 'cta_group::2' in S.sysml_last_route(), S.sysml_last_route();"
-            "T.assert_close(T.host(g),g_ref,T.TOL['tf32'],'pair');print('ok')")
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SYSML_F2_PAIR="1"), capture_output=True,
-                       text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
