@@ -52,6 +52,8 @@ sysml_status conv_fwd_ws(const sysml_conv_desc &cd, const sysml_pool_desc *pd, i
       else if (use_tc && !pap && phase_fwd_supported(a)) b += phase_fwd_ws(a);
       else if (pd) b += align_up((size_t)g.N * g.KPQ() * sizeof(float), 256);
     }
+  } else if (use_tc && !pap && pair_conv_supported(a, 0)) {
+    b += pair_conv_ws(a, 0);  // CTA-pair (cta_group::2) kernel for 256-wide filter banks
   } else if (use_tc && tc_fwd_supported(a, pap)) {
     b += tc_fwd_ws(a);
   } else if (use_tc && !pap && phase_fwd_supported(a)) {
@@ -127,6 +129,11 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
     SYSML_WS_FITS(wc);
     SYSML_TRY(csr_densify(x.csr, dense, st));
     xd = dense;
+  }
+  if (cd.math == SYSML_MATH_TF32 && !pap && !x.is_csr && pair_conv_supported(a, 0)) {
+    void *tws = wc.take<char>(pair_conv_ws(a, 0));
+    SYSML_WS_FITS(wc);
+    return pair_conv(a, 0, xd, f, bias, y, tws, st);
   }
   if (use_tc) {
     void *tws = wc.take<char>(tc_fwd_ws(a));
@@ -244,7 +251,8 @@ sysml_status conv_bwd_data_ws(const sysml_conv_desc &cd, size_t *bytes) {
   SYSML_TRY(validate_conv(&cd, &g));
   const ConvArgs a = conv_args(g);
   *bytes = 0;
-  if (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a)) *bytes = tc_bwd_data_ws(a);
+  if (cd.math == SYSML_MATH_TF32 && pair_conv_supported(a, 1)) *bytes = pair_conv_ws(a, 1);
+  else if (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a)) *bytes = tc_bwd_data_ws(a);
   else if (cd.math == SYSML_MATH_TF32 && phase_bwd_data_supported(a)) *bytes = phase_bwd_data_ws(a);
   else if (phase_simt_bwd_data_supported(a)) *bytes = phase_simt_bwd_data_ws(a);
   return SYSML_OK;
@@ -267,6 +275,7 @@ sysml_status conv_bwd_data_dispatch(const sysml_conv_desc &cd, const float *f, c
     set_error("workspace too small: need %zu bytes, got %zu", need, ws ? ws_bytes : 0);
     return SYSML_ERR_WORKSPACE;
   }
+  if (cd.math == SYSML_MATH_TF32 && pair_conv_supported(a, 1)) return pair_conv(a, 1, dy, f, nullptr, dx, ws, st);
   if (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a))
     return tc_conv_bwd_data(a, f, dy, dx, ws, st);
   if (cd.math == SYSML_MATH_TF32 && phase_bwd_data_supported(a)) {

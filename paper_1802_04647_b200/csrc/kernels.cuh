@@ -192,6 +192,13 @@ sysml_status launch_maxpool_bwd_spf(const PoolArgs &a, const int32_t *argmax, co
 sysml_status launch_nchw_to_spf(int N, int C, int H, int W, const float *x, float *spf,
                                 int64_t plane, int Wf, int Lf, int off, cudaStream_t st);
 
+// pair_conv.cu : stride-1 conv fwd / bwd_data on CTA pairs (cta_group::2, M = 256) for 256-wide
+// filter banks; bwd_data = 1 computes dX = conv(dY, rot180(F)^T)
+bool pair_conv_supported(const ConvArgs &a, int bwd_data);
+size_t pair_conv_ws(const ConvArgs &a, int bwd_data);
+sysml_status pair_conv(const ConvArgs &a, int bwd_data, const float *x, const float *f, const float *bias,
+                       float *y, void *ws, cudaStream_t st);
+
 // snt_fwd.cu : LeNet conv2 forward + bias + relu + 2x2 pool, SN-T (T = 3) with resident filters
 bool snt_fwd_pool_supported(const ConvArgs &a, const PoolArgs *pool, int Wf, int Lf);
 size_t snt_fwd_pool_ws(const ConvArgs &a);

@@ -474,3 +474,38 @@ def test_lenet_dedicated_conv2_kernels_route(S):
     routes = S.sysml_last_route()
     assert "snt_fwd_pool_kernel" in routes and "sn_tmem_kernel" in routes, routes
 
+
+
+_PAIR_CODE = r"""
+import numpy as np, torch, synth, oracle, paper_1802_04647_b200 as S
+from tests.test_gpu_parity import TOL, assert_close, dev, host
+shapes = [(3, 64, 14, 14, 256, 3, 1), (2, 32, 9, 11, 512, 3, 1), (3, 128, 7, 7, 256, 1, 0),
+          (2, 256, 14, 14, 64, 3, 1), (2, 256, 8, 8, 128, 1, 0), (1, 16, 5, 6, 256, 3, 1)]
+for i, (N, C, H, W, K, R, pd) in enumerate(shapes):
+    P, Q = H + 2 * pd - R + 1, W + 2 * pd - R + 1
+    x, f, b, dy = synth.conv_problem_U(N, C, H, W, K, R, R, P, Q, seed=(990 + i,))
+    d = S.conv_desc(N, C, H, W, K, R, R, 1, pd, "tf32")
+    if K % 256 == 0:
+        y = host(S.sysml_conv2d(dev(x), dev(f), d, bias=dev(b)))
+        assert "pair_conv_kernel" in S.sysml_last_route(), S.sysml_last_route()
+        yr = oracle.conv2d_fwd(x, f, N, C, H, W, K, R, R, (1, 1), (pd, pd), bias=b)
+        assert_close(y.reshape(yr.shape), yr, TOL["tf32"], f"pair fwd {i}")
+    if C % 256 == 0:
+        dx = host(S.sysml_conv2d_bwd_data(dev(f), dev(dy), d))
+        assert "pair_conv_kernel" in S.sysml_last_route(), S.sysml_last_route()
+        dxr = oracle.conv2d_bwd_data(f, dy, N, C, H, W, K, R, R, (1, 1), (pd, pd))
+        assert_close(dx.reshape(dxr.shape), dxr, TOL["tf32"], f"pair bwd_data {i}")
+print("ok")
+"""
+
+
+def test_pair_conv_forced_small_shapes(S):
+    """The CTA-pair conv kernel (pair_conv.cu: cta_group::2, M = 256, half filter chunks per CTA,
+    relay of rank 1's stage events) against the oracle on small / ragged shapes, forced on with
+    SYSML_PAIR_CONV=2: 3x3 / 1x1, non-square planes, K = 256 and 512 (two filter tiles),
+    bwd_data through flipped filters (C = 256), a partial last pair tile."""
+    import subprocess, sys
+    r = subprocess.run([sys.executable, "-c", _PAIR_CODE], env=dict(os.environ, SYSML_PAIR_CONV="2"),
+                       capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
