@@ -330,7 +330,8 @@ PcPlan plan_pair(int N, int Cin, int H, int W, int Kout, int R, int S, int ph, i
     const int64_t u = p.npt * (Kout / nt);
     return (double)u / (double)(ceil_div(u, (int64_t)pairs) * pairs);
   };
-  p.NT = (Kout % 256 || eff(128) > 1.15 * eff(256)) ? 128 : 256;
+  static const int nt_env = getenv("SYSML_PAIR_NT") ? atoi(getenv("SYSML_PAIR_NT")) : 0;
+  p.NT = nt_env == 128 || (Kout % 256 || eff(128) > 1.15 * eff(256)) ? 128 : 256;
   p.nft = Kout / p.NT;
   p.nunits = p.npt * p.nft;
   if ((int64_t)N * Cin * H * W >= (1ll << 31) || (int64_t)N * Kout * p.P * p.Q >= (1ll << 40)) return pl;
