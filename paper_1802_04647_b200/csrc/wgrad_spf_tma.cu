@@ -57,6 +57,12 @@ __device__ __forceinline__ void st_shared_v4_w2(uint32_t addr, float a, float b,
                : "memory");
 }
 
+__device__ __forceinline__ float4 ld_shared_v4_w2(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
   return ptx::make_desc(saddr, 16, 1024) | ((uint64_t)2 << 61);
 }
@@ -239,18 +245,19 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         ptx::mbar_wait(fullBt + slot1, ph1);
         if (p.clk && et == 0) p.clk[blockIdx.x * 8 + 2] += clock64() - t0;
         if (++sb == p.nbr) { sb = 0; pb ^= 1; }
-        const uint8_t *B0 = Bring + slot * b_slot, *B1 = Bring + slot1 * b_slot;
-        const uint32_t Bs = sB + slot * b_slot;
-        // all six 16-byte loads of this thread's (up to) three tasks first, then the shifts
+        const uint32_t Bs = sB + slot * b_slot, B1s = sB + slot1 * b_slot;
+        // all 16-byte loads of this thread's (up to) two tasks first, then the shifts; explicit
+        // ld.shared.v4 (a generic pointer here compiled to split generic loads: 2.7x the
+        // shared-memory wavefronts)
         float4 v0[2], v1[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int t = et + u * 256;
           if (t < ntask) {
             const int c = t >> 3, q = t & 7;
-            v0[u] = *reinterpret_cast<const float4 *>(B0 + c * 128 + ((q ^ (c & 7)) << 4));
-            v1[u] = q < 7 ? *reinterpret_cast<const float4 *>(B0 + c * 128 + (((q + 1) ^ (c & 7)) << 4))
-                          : *reinterpret_cast<const float4 *>(B1 + c * 128 + ((c & 7) << 4));
+            v0[u] = ld_shared_v4_w2(Bs + (uint32_t)(c * 128 + ((q ^ (c & 7)) << 4)));
+            v1[u] = ld_shared_v4_w2(q < 7 ? Bs + (uint32_t)(c * 128 + (((q + 1) ^ (c & 7)) << 4))
+                                          : B1s + (uint32_t)(c * 128 + ((c & 7) << 4)));
           }
         }
 #pragma unroll
