@@ -49,6 +49,8 @@ struct W2Params {
   const float *x;                 // X plane base (+ x_shift) for the shifted B rows
   int64_t G, plane_x;
   int ntma_s;                     // column taps s with s % 4 == 0 (TMA-loaded)
+  int hcopy;                      // 1: A copies j >= 1 built by the helpers ((copies - 1) * Wf <= 32)
+  int hb4;                        // 1: B tap s = 4 built by the helpers (else TMA-loaded)
   long long *clk;                 // optional per-CTA cycle counters (SYSML_TC_PROFILE)
 };
 
@@ -76,9 +78,10 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
   const uint32_t a_slot = 128 * 128;                  // 16 KB
   const uint32_t b_slot = (uint32_t)p.N * 128;        // N rows x 128 B
   uint8_t *Aring = smem, *Bring = smem + W2_NA * a_slot;
-  uint64_t *fullA = reinterpret_cast<uint64_t *>(Bring + p.nbr * b_slot);
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(Bring + p.nbr * b_slot);  // A atom complete (helpers)
   uint64_t *emptyA = fullA + W2_NA;
-  uint64_t *fullB = emptyA + W2_NA;    // B atom complete (helper warps)
+  uint64_t *fullAt = emptyA + W2_NA;   // TMA part of an A atom landed
+  uint64_t *fullB = fullAt + W2_NA;    // B atom complete (helper warps)
   uint64_t *emptyB = fullB + p.nbr;
   uint64_t *fullBt = emptyB + p.nbr;   // TMA part of a B atom landed
   uint64_t *accf = fullBt + p.nbr;
@@ -93,8 +96,12 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < W2_NA; ++i) {
-      ptx::mbar_init(fullA + i, 1);
-      ptx::mbar_init(emptyA + i, do_db ? 2 : 1);
+      // A copies j >= 1 (dY shifted by j frame rows) are built by the helper warps from the
+      // TMA-loaded copy 0 of this atom and the previous one (fewer TMA row requests: the TMA
+      // engine handles ~1 128-byte row per 9-10 clocks here, which paced the whole kernel)
+      ptx::mbar_init(fullA + i, W2_HELP_WARPS);
+      ptx::mbar_init(fullAt + i, 1);
+      ptx::mbar_init(emptyA + i, 1 + (p.copies > 1 && p.hcopy ? W2_HELP_WARPS : 0) + (do_db ? 1 : 0));
     }
     for (int i = 0; i < p.nbr; ++i) {
       ptx::mbar_init(fullB + i, W2_HELP_WARPS);  // the helper warps (after they saw the TMA part)
@@ -129,11 +136,13 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         if (p.clk) p.clk[blockIdx.x * 8 + 4] += clock64() - t0;
         // the bytes the copies below deliver: copies x Kc rows (< 128 rows when copies*Kc < 128;
         // the slot's other rows only feed accumulator rows the reduce skips)
-        ptx::mbar_arrive_expect_tx(fullA + sa, (uint32_t)(p.copies * p.Kc * 128));
+        // copy 0 only, except for the CTA's first atom (no previous atom to build the rest from)
+        const int ncp = (ia == 0 || !p.hcopy) ? p.copies : 1;
+        ptx::mbar_arrive_expect_tx(fullAt + sa, (uint32_t)(ncp * p.Kc * 128));
         const int g = (int)((a0 + ia) * W2_ATOM);
-        for (int j = 0; j < p.copies; ++j)
+        for (int j = 0; j < ncp; ++j)
           ptx::tma_load_3d(sA + sa * a_slot + j * p.Kc * 128, &tmDy, g - j * p.Wf, k0, 0,
-                           ptx::smem_u32(fullA + sa));
+                           ptx::smem_u32(fullAt + sa));
         if (++sa == W2_NA) { sa = 0; pa ^= 1; }
       }
     }
@@ -149,11 +158,12 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         const long long t0 = p.clk ? clock64() : 0;
         ptx::mbar_wait(emptyB + sb, pb ^ 1);
         if (p.clk) p.clk[blockIdx.x * 8 + 5] += clock64() - t0;
-        ptx::mbar_arrive_expect_tx(fullBt + sb, (uint32_t)(p.ntma_s * p.Ct * 128));
+        // the s = 0 rows (and s = 4 unless the helpers build it): helpers build the others
+        const bool t4 = !p.hb4 && p.S > 4;
+        ptx::mbar_arrive_expect_tx(fullBt + sb, (uint32_t)((t4 ? 2 : 1) * p.Ct * 128));
         const int g = (int)((a0 + ib) * W2_ATOM);
-        for (int s = 0; s < p.S; s += 4)
-          ptx::tma_load_3d(sB + sb * b_slot + s * p.Ct * 128, &tmX, g + s, c0, 0,
-                           ptx::smem_u32(fullBt + sb));
+        ptx::tma_load_3d(sB + sb * b_slot, &tmX, g, c0, 0, ptx::smem_u32(fullBt + sb));
+        if (t4) ptx::tma_load_3d(sB + sb * b_slot + 4 * p.Ct * 128, &tmX, g + 4, c0, 0, ptx::smem_u32(fullBt + sb));
         if (++sb == p.nbr) { sb = 0; pb ^= 1; }
       }
     }
@@ -266,26 +276,50 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           if (t >= ntask) continue;
           const int c = t >> 3, q = t & 7;
           const float e[8] = {v0[u].x, v0[u].y, v0[u].z, v0[u].w, v1[u].x, v1[u].y, v1[u].z, v1[u].w};
-          // taps unrolled to W2_MAXS with predication: the 1..3-position select is static
+          // taps s = 1 .. S-1 (S <= 5): positions 4q + s .. 4q + s + 3 of the s = 0 row
 #pragma unroll
-          for (int s_ = 1; s_ < W2_MAXS; ++s_) {
-            if (s_ >= p.S || (s_ & 3) == 0) continue;
+          for (int s_ = 1; s_ < 5; ++s_) {
+            if (s_ >= p.S || (s_ == 4 && !p.hb4)) break;
             const int row = s_ * p.Ct + c;
             const uint32_t dst = Bs + row * 128 + ((q ^ (row & 7)) << 4);
-            const int o = s_ & 3;
-            st_shared_v4_w2(dst, e[o], e[o + 1], e[o + 2], e[o + 3]);
+            st_shared_v4_w2(dst, e[s_], e[s_ + 1], e[s_ + 2], e[s_ + 3]);
           }
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(fullB + slot);
       }
+      if (step >= 0) {
+        // A atom `step`: wait its TMA rows; build copies j >= 1 (rows j*Kc + k) from copy 0 of
+        // this atom and the previous one: copy j = positions g - 16j .. g - 16j + 31 = the last
+        // j * Wf / 4 16-byte chunks of the previous atom's row, then the first ones of this row
+        const int slotA = sa, slotP = sa == 0 ? W2_NA - 1 : sa - 1;
+        const long long t0 = p.clk ? clock64() : 0;
+        ptx::mbar_wait(fullAt + slotA, pa);
+        if (p.clk && et == 0) p.clk[blockIdx.x * 8 + 3] += clock64() - t0;
+        if (step > 0 && p.copies > 1 && p.hcopy) {
+          const uint32_t As = sA + slotA * a_slot, Ps = sA + slotP * a_slot;
+          const int nrow = (p.copies - 1) * p.Kc;
+          for (int t = et; t < nrow * 8; t += 256) {
+            const int rr = t >> 3, q = t & 7;
+            const int j = 1 + rr / p.Kc, k = rr - (j - 1) * p.Kc;
+            const int sh = j * p.Wf / 4;  // chunks (Wf % 4 == 0)
+            const int srow = k;           // copy 0 row of filter k ((srow & 7) == (row & 7): Kc % 8 == 0)
+            const float4 v = q < sh ? ld_shared_v4_w2(Ps + srow * 128 + (((q + 8 - sh) ^ (srow & 7)) << 4))
+                                    : ld_shared_v4_w2(As + srow * 128 + (((q - sh) ^ (srow & 7)) << 4));
+            const int row = j * p.Kc + k;
+            st_shared_v4_w2(As + row * 128 + ((q ^ (row & 7)) << 4), v.x, v.y, v.z, v.w);
+          }
+          ptx::fence_proxy_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(fullA + slotA);
+          if (step > 0 && p.copies > 1 && p.hcopy) ptx::mbar_arrive(emptyA + slotP);  // previous atom no longer read
+        }
+      }
       if (step >= 0 && do_db && main_helper) {
         const int slotA = sa;
-        const long long t0 = p.clk ? clock64() : 0;
-        ptx::mbar_wait(fullA + slotA, pa);
-        if (++sa == W2_NA) { sa = 0; pa ^= 1; }
-        if (p.clk && et == 0) p.clk[blockIdx.x * 8 + 3] += clock64() - t0;
         if (drow < p.Kc) {
           const float4 *rp = reinterpret_cast<const float4 *>(Aring + slotA * a_slot + drow * 128) + dhalf * 4;
 #pragma unroll
@@ -298,6 +332,9 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
         }
         ptx::named_bar_sync(1, 128);
         if (et == 0) ptx::mbar_arrive(emptyA + slotA);
+      }
+      if (step >= 0) {
+        if (++sa == W2_NA) { sa = 0; pa ^= 1; }
       }
     }
     if (do_db && main_helper) {
@@ -461,7 +498,7 @@ W2Plan plan_w2(const SpfConv &sc) {
   pl.ok = false;
   p.K = sc.K; p.C = sc.C; p.R = sc.R; p.S = sc.S; p.Wf = sc.Wf;
   if (sc.C % 8 || sc.x_shift % 4 || sc.dy_shift % 4 || sc.plane_x % 4 || sc.plane_dy % 4 ||
-      sc.G <= 0 || sc.Wf % 8 || sc.S > 8)
+      sc.G <= 0 || sc.Wf % 8 || sc.S > 5)  // taps s = 1 .. 4 are built from the s = 0 rows
     return pl;
   // A rows (j, k): Kc filters per copy, copies of dY shifted by j frame rows
   p.Kc = sc.K <= 16 ? 16 : sc.K <= 32 ? 32 : sc.K <= 64 ? 64 : 128;
@@ -469,6 +506,13 @@ W2Plan plan_w2(const SpfConv &sc) {
   p.nkt = (int)ceil_div(sc.K, p.Kc);
   p.RG = (sc.R + p.copies - 1) / p.copies;
   p.shift = p.copies * sc.Wf;
+  {
+    // helper-built A copies: exact but slower (457 vs 392 us on LeNet B2f), opt-in
+    static const int hc_env = getenv("SYSML_W2_HCOPY") ? atoi(getenv("SYSML_W2_HCOPY")) : 0;
+    static const int hb_env = getenv("SYSML_W2_HB4") ? atoi(getenv("SYSML_W2_HB4")) : 1;
+    p.hcopy = hc_env && (p.copies - 1) * sc.Wf <= 32 ? 1 : 0;
+    p.hb4 = hb_env;
+  }
   // channel tile: Ct <= 48 (3 helper tasks per thread), S*Ct % 16 == 0, RG*S*Ct TMEM
   // columns <= 512; the widest tile wins (the last one may be ragged: TMA zero-fills)
   p.Ct = 0;
