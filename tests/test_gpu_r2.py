@@ -509,3 +509,20 @@ def test_pair_conv_forced_small_shapes(S):
                        capture_output=True, text=True,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("env", [{"SYSML_W2_HCOPY": "1"}, {"SYSML_W2_HB4": "0"}])
+def test_lenet_b2f_staging_variants_match_oracle(S, env):
+    """conv2 bwd_filter staging variants (wgrad_spf_tma.cu): the second dY copy built by the helper
+    warps from two TMA-loaded atoms (SYSML_W2_HCOPY=1), and tap s = 4 TMA-loaded instead of built
+    (SYSML_W2_HB4=0); the step must still equal the oracle exactly on dyadic inputs."""
+    import subprocess, sys
+    code = ("import tests.test_gpu_parity as T, paper_1802_04647_b200 as S, numpy as np, torch, oracle;"
+            "x,y,prm=T._lenet_case(37, True);"
+            "g_ref,_=oracle.lenet_fwd_bwd(x,y,prm,n_global=40);"
+            "net=S.LeNet(40, math='tf32'); g=torch.empty(83466,device='cuda');"
+            "net.fwd_bwd(T.dev(prm),T.dev(x),T.dev(y,torch.int32),40,g);"
+            "T.assert_close(T.host(g),g_ref,T.TOL['tf32'],'b2f variant');print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
