@@ -412,6 +412,14 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
                           8 * 2 * FBB_STAGES;
     const size_t smem_bulk = FBB_STAGES * stage + img_bytes + 8 * 2 * FBB_STAGES;
     const size_t sm_need = std::max(smem_b, smem_bulk);
+    if (b1_tc_supported(c, pa, true, dpool_nhwc != 0, xcsr != nullptr)) {  // tensor-core form (b1_tc.cu)
+      int used_tc = 0;
+      SYSML_TRY(b1_tc(c, x, dpool, a.code, a.code_plane, part, ctas, &used_tc, st));
+      fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 32), dim3(32, 8), 0, st>>>(
+          part, used_tc, c.K, RS, df, db);
+      SYSML_LAUNCH_CHECK();
+      return SYSML_OK;
+    }
     auto kern = RS == 25 ? pool_bwd_wgrad_c1_bulk_kernel<5, 5> : pool_bwd_wgrad_c1_bulk_kernel<3, 3>;
     SYSML_TRY(smem_attr(kern, sm_need));
     kern<<<used, FBB_THREADS, sm_need, st>>>(a, x, cs, xcsr != nullptr, dpool, part);

@@ -199,6 +199,11 @@ size_t pair_conv_ws(const ConvArgs &a, int bwd_data);
 sysml_status pair_conv(const ConvArgs &a, int bwd_data, const float *x, const float *f, const float *bias,
                        float *y, void *ws, cudaStream_t st);
 
+// b1_tc.cu : LeNet conv1 wgrad + pool1 backward on the tensor cores (window candidates stacked)
+bool b1_tc_supported(const ConvArgs &c, const PoolArgs &pa, bool has_codes, bool nhwc, bool csr);
+sysml_status b1_tc(const ConvArgs &c, const float *x, const float *dpool, const uint64_t *code, int64_t code_plane,
+                   float *part, int max_ctas, int *used, cudaStream_t st);
+
 // snt_fwd.cu : LeNet conv2 forward + bias + relu + 2x2 pool, SN-T (T = 3) with resident filters
 bool snt_fwd_pool_supported(const ConvArgs &a, const PoolArgs *pool, int Wf, int Lf);
 size_t snt_fwd_pool_ws(const ConvArgs &a);
