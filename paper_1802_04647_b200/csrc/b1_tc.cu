@@ -55,6 +55,7 @@ constexpr uint32_t B1T_XG = B1T_XPRE + B1T_X_BYTES;               // g after the
 constexpr uint32_t B1T_STAGE = (B1T_XG - B1T_X_BYTES + B1T_STAGE_TX + 127) / 128 * 128;
 constexpr uint32_t B1T_ABYTES = B1T_KQ * 128 * 16, B1T_BBYTES = B1T_KQ * B1T_N * 16;
 constexpr uint32_t B1T_OPB = B1T_ABYTES + B1T_BBYTES;       // one operand buffer
+constexpr int B1T_NBUF = 3;                         // operand buffers in flight
 static_assert(B1T_AITEMS % 32 == 0 && B1T_BUILD % 32 == 0, "warp-uniform A/B split");
 
 struct B1tParams {
@@ -69,12 +70,14 @@ __global__ void __launch_bounds__(B1T_THREADS, 1)
     b1_tc_kernel(const __grid_constant__ CUtensorMap tmX, const B1tParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t *ops = smem;                                  // [2] operand buffers (A then B)
-  uint8_t *stage = ops + 2 * B1T_OPB;                   // [2] image inputs
-  float *red = reinterpret_cast<float *>(stage + 2 * B1T_STAGE);  // [4][32][48] + [16][32] (end)
-  int *ppoff = reinterpret_cast<int *>(red + 4 * 32 * B1T_N + 16 * 32);  // [216]: x(2 pr - 2, 2 pc - 2) (-1: pad)
+  uint8_t *stage = ops + B1T_NBUF * B1T_OPB;            // [2] image inputs
+  float *red = reinterpret_cast<float *>(ops);          // [4][32][48] (end; over the drained operands)
+  float *dbr = reinterpret_cast<float *>(stage + 2 * B1T_STAGE);  // [16 warps][32]
+  int *ppoff = reinterpret_cast<int *>(dbr + 16 * 32);  // [216]: x(2 pr - 2, 2 pc - 2) (-1: pad)
   uint64_t *bars = reinterpret_cast<uint64_t *>(ppoff + 216);
-  uint64_t *sfull = bars, *sempty = bars + 2, *ofull = bars + 4, *oempty = bars + 6, *accf = bars + 8;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 9);
+  uint64_t *sfull = bars, *sempty = bars + 2, *ofull = bars + 4, *oempty = bars + 4 + B1T_NBUF;
+  uint64_t *accf = bars + 4 + 2 * B1T_NBUF;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(accf + 1);
 
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * p.n_per_cta, n1 = min(p.N, n0 + p.n_per_cta);
@@ -83,14 +86,16 @@ __global__ void __launch_bounds__(B1T_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(sfull + s, 1);
       ptx::mbar_init(sempty + s, B1T_BUILD / 32);
-      ptx::mbar_init(ofull + s, B1T_BUILD / 32);
-      ptx::mbar_init(oempty + s, 1);
+    }
+    for (int b = 0; b < B1T_NBUF; ++b) {
+      ptx::mbar_init(ofull + b, B1T_BUILD / 32);
+      ptx::mbar_init(oempty + b, 1);
     }
     ptx::mbar_init(accf, 1);
     ptx::fence_mbar_init();
   }
-  // zero the B padding rows 36..47 of both buffers (never written again)
-  for (int i = threadIdx.x; i < 2 * B1T_KQ * (B1T_N - B1T_UV) * 4; i += blockDim.x) {
+  // zero the B padding rows 36..47 of every buffer (never written again)
+  for (int i = threadIdx.x; i < B1T_NBUF * B1T_KQ * (B1T_N - B1T_UV) * 4; i += blockDim.x) {
     const int b = i / (B1T_KQ * (B1T_N - B1T_UV) * 4), rem = i % (B1T_KQ * (B1T_N - B1T_UV) * 4);
     const int q = rem / ((B1T_N - B1T_UV) * 4), r2 = rem % ((B1T_N - B1T_UV) * 4);
     reinterpret_cast<float *>(ops + b * B1T_OPB + B1T_ABYTES + q * (B1T_N * 16) + B1T_UV * 16)[r2] = 0.f;
@@ -132,8 +137,8 @@ __global__ void __launch_bounds__(B1T_THREADS, 1)
     int q = 0;
     for (int i = 0; i < nimg; ++i)
       for (int ci = 0; ci < B1T_NCHUNK; ++ci, ++q) {
-        const int b = q & 1;
-        ptx::mbar_wait(ofull + b, (uint32_t)((q >> 1) & 1));
+        const int b = q % B1T_NBUF;
+        ptx::mbar_wait(ofull + b, (uint32_t)((q / B1T_NBUF) & 1));
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           const uint32_t A = obase + b * B1T_OPB, B = A + B1T_ABYTES;
@@ -155,6 +160,14 @@ __global__ void __launch_bounds__(B1T_THREADS, 1)
     const int kmine = t & 31;  // every A item of this thread has filter k = t % 32
     // the 4-bit code of (k, pp) sits in 32-bit half (k >> 3) & 1 of word k >> 4, at bit 4 (k & 7)
     const int cword = (kmine >> 4) * B1T_PP * 2 + ((kmine >> 3) & 1), cshift = 4 * (kmine & 7);
+    // B item j = uv + 36 pq; threads 64.. (one A item each) take j = t - 64 and j + 448
+    static_assert(B1T_AITEMS - B1T_BUILD == 64 && B1T_ITEMS - B1T_AITEMS <= 2 * (B1T_BUILD - 64), "B split");
+    int bpq0 = -1, buv0 = 0, broff0 = 0, bpq1 = -1, buv1 = 0, broff1 = 0;
+    if (t >= 64) {
+      const int j0 = t - 64, j1 = j0 + (B1T_BUILD - 64);
+      bpq0 = j0 / B1T_UV; buv0 = j0 - bpq0 * B1T_UV; broff0 = buv0 / 6 * B1T_XP + buv0 % 6;
+      if (j1 < B1T_ITEMS - B1T_AITEMS) { bpq1 = j1 / B1T_UV; buv1 = j1 - bpq1 * B1T_UV; broff1 = buv1 / 6 * B1T_XP + buv1 % 6; }
+    }
     float dbacc = 0.f;
     int q = 0;
     for (int i = 0; i < nimg; ++i) {
@@ -165,45 +178,55 @@ __global__ void __launch_bounds__(B1T_THREADS, 1)
       const uint32_t *cs = reinterpret_cast<const uint32_t *>(st + B1T_XG + B1T_G_BYTES) + cword;
       const float *xs = reinterpret_cast<const float *>(st);
       for (int ci = 0; ci < B1T_NCHUNK; ++ci, ++q) {
-        const int b = q & 1;
-        ptx::mbar_wait(oempty + b, (uint32_t)(((q >> 1) & 1) ^ 1));
+        const int b = q % B1T_NBUF;
+        ptx::mbar_wait(oempty + b, (uint32_t)(((q / B1T_NBUF) & 1) ^ 1));
         uint8_t *A = ops + b * B1T_OPB;
         uint8_t *Bm = A + B1T_ABYTES;
         const int pbase = ci * B1T_CHUNK;
-        for (int it = t; it < B1T_ITEMS; it += B1T_BUILD) {
-          if (it < B1T_AITEMS) {
-            // A item (pq, k): the four candidates d get the masked g of their own winners
-            const int pq = it >> 5;
-            float v[4][4];
+        // A items (pq, k): the four candidates d get the masked g of their own winners
+        for (int it = t; it < B1T_AITEMS; it += B1T_BUILD) {
+          const int pq = it >> 5;
+          float v[4][4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int pp = pbase + pq * 4 + e;
-              float gv = 0.f;
-              uint32_t cd = 0;
-              if (pp < B1T_PP) {
-                gv = gs[pp * B1T_K + kmine];
-                cd = (cs[2 * pp] >> cshift) & 15u;
-              }
-              const float gm = (cd & 4u) ? gv : 0.f;  // window max > 0 (reading R9)
-              dbacc += gm;
-#pragma unroll
-              for (int d = 0; d < 4; ++d) v[d][e] = ((cd & 3u) == (uint32_t)d) ? gm : 0.f;
+          for (int e = 0; e < 4; ++e) {
+            const int pp = pbase + pq * 4 + e;
+            float gv = 0.f;
+            uint32_t cd = 0;
+            if (pp < B1T_PP) {
+              gv = gs[pp * B1T_K + kmine];
+              cd = (cs[2 * pp] >> cshift) & 15u;
             }
+            dbacc += (cd & 4u) ? gv : 0.f;  // window max > 0 (reading R9)
 #pragma unroll
-            for (int d = 0; d < 4; ++d)
-              *reinterpret_cast<float4 *>(A + pq * (128 * 16) + (d * 32 + kmine) * 16) =
-                  make_float4(v[d][0], v[d][1], v[d][2], v[d][3]);
-          } else {
-            // B item (uv, pq): x at offset (u, v) = (dr + r, ds + s) from each window origin
-            const int j = it - B1T_AITEMS, pq = j / B1T_UV, uv = j - pq * B1T_UV;
-            const int u = uv / 6, roff = u * B1T_XP + (uv - u * 6);
-            float v[4];
+            for (int d = 0; d < 4; ++d) v[d][e] = (cd == 4u + (uint32_t)d) ? gv : 0.f;
+          }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int o = ppoff[pbase + pq * 4 + e];
-              v[e] = o >= 0 ? xs[o + roff] : 0.f;
+          for (int d = 0; d < 4; ++d)
+            *reinterpret_cast<float4 *>(A + pq * (128 * 16) + (d * 32 + kmine) * 16) =
+                make_float4(v[d][0], v[d][1], v[d][2], v[d][3]);
+        }
+        // B items (uv, pq): x at offset (u, v) = (dr + r, ds + s) from each window origin; the
+        // threads with one A item take them (nb0 / nb1 = this thread's first / second, -1: none)
+        {
+          float v[2][4];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int pq = h ? bpq1 : bpq0;
+            if (pq >= 0) {
+              const int4 o = *reinterpret_cast<const int4 *>(ppoff + pbase + pq * 4);
+              const int rf = h ? broff1 : broff0;
+              v[h][0] = o.x >= 0 ? xs[o.x + rf] : 0.f;
+              v[h][1] = o.y >= 0 ? xs[o.y + rf] : 0.f;
+              v[h][2] = o.z >= 0 ? xs[o.z + rf] : 0.f;
+              v[h][3] = o.w >= 0 ? xs[o.w + rf] : 0.f;
             }
-            *reinterpret_cast<float4 *>(Bm + pq * (B1T_N * 16) + uv * 16) = make_float4(v[0], v[1], v[2], v[3]);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int pq = h ? bpq1 : bpq0;
+            if (pq >= 0)
+              *reinterpret_cast<float4 *>(Bm + pq * (B1T_N * 16) + (h ? buv1 : buv0) * 16) =
+                  make_float4(v[h][0], v[h][1], v[h][2], v[h][3]);
           }
         }
         ptx::fence_proxy_async_smem();
@@ -215,7 +238,6 @@ __global__ void __launch_bounds__(B1T_THREADS, 1)
     }
     // ================= partials: D[(d, k)][(u, v)] (warps 0-3 = TMEM lane quadrants = d);
     // dF1[k][r][s] = sum_d D[(d, k)][(dr + r, ds + s)]
-    float *dbr = red + 4 * 32 * B1T_N;  // [16 warps][32]
     dbr[(t >> 5) * 32 + kmine] = dbacc;
     if (warp < 4) {
       if (nimg > 0) ptx::mbar_wait_sleep(accf, 0);
@@ -259,7 +281,8 @@ __global__ void __launch_bounds__(B1T_THREADS, 1)
 }
 
 size_t b1_tc_smem() {
-  return 2 * (size_t)B1T_OPB + 2 * (size_t)B1T_STAGE + (4 * 32 * B1T_N + 16 * 32) * 4 + 216 * 4 + 8 * 9 + 16;
+  static_assert(4 * 32 * B1T_N * 4 <= B1T_NBUF * B1T_OPB, "red fits over the operand buffers");
+  return B1T_NBUF * (size_t)B1T_OPB + 2 * (size_t)B1T_STAGE + 16 * 32 * 4 + 216 * 4 + 8 * (5 + 2 * B1T_NBUF) + 16;
 }
 
 }  // namespace
