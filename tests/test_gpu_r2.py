@@ -446,10 +446,12 @@ def test_lenet_routed_b2d_opt_in_parity(S):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("env", [{"SYSML_F2_SNT": "0"}, {"SYSML_SN_TMEM": "0"}, {"SYSML_F2_SNT": "0", "SYSML_SN_TMEM": "0"}])
+@pytest.mark.parametrize("env", [{"SYSML_F2_SNT": "0"}, {"SYSML_SN_TMEM": "0"}, {"SYSML_F2_SNT": "0", "SYSML_SN_TMEM": "0"},
+                                 {"SYSML_B1_TC": "0"}])
 def test_lenet_kernel_fallbacks_match_oracle(S, env):
     """The LeNet step's dedicated conv2 kernels (snt_fwd_pool_kernel for F2, sn_tmem_kernel for
-    B2d) have general-kernel fallbacks (K3 / K6 SN); with either switched off the step must still
+    B2d) have general-kernel fallbacks (K3 / K6 SN), and the tensor-core B1 (b1_tc_kernel) the
+    SIMT pool_bwd_wgrad_c1_bulk_kernel; with any switched off the step must still
     equal the oracle exactly on dyadic inputs (TF32), and the route log must name the fallback."""
     import subprocess, sys
     code = ("import tests.test_gpu_parity as T, paper_1802_04647_b200 as S, numpy as np, torch, oracle;"
@@ -464,7 +466,8 @@ def test_lenet_kernel_fallbacks_match_oracle(S, env):
 
 
 def test_lenet_dedicated_conv2_kernels_route(S):
-    """The default LeNet step runs F2 on snt_fwd_pool_kernel and B2d on sn_tmem_kernel (route log)."""
+    """The default LeNet step runs F2 on snt_fwd_pool_kernel, B2d on sn_tmem_kernel and B1 on
+    b1_tc_kernel (route log)."""
     import tests.test_gpu_parity as T
     x, y, prm = T._lenet_case(40, True)
     net = S.LeNet(40, math="tf32")
@@ -473,6 +476,7 @@ def test_lenet_dedicated_conv2_kernels_route(S):
     torch.cuda.synchronize()
     routes = S.sysml_last_route()
     assert "snt_fwd_pool_kernel" in routes and "sn_tmem_kernel" in routes, routes
+    assert "b1_tc_kernel" in routes, routes
 
 
 
