@@ -33,6 +33,7 @@ constexpr int W2_NA = 6;          // A ring (dY atoms)
 constexpr int W2_THREADS = 352;  // warps 0 A producer, 1 MMA, 2-5 + 7-10 helpers, 6 B producer
 constexpr int W2_HELP_WARPS = 8;
 constexpr int W2_ATOM = 32;       // positions per atom (128-byte swizzled row)
+constexpr int W2_MAXL = 7;        // B lookahead (atoms): descriptors of atoms ai .. ai + 7
 
 struct W2Params {
   int K, C, R, S, Wf;
@@ -194,11 +195,12 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       // descriptors built once per atom; K-steps / sub-atom shifts are start-address
       // increments (16-byte units) -- keeps the issue loop to a few uniform adds per MMA
       const uint64_t adesc = sw128(sA + sa * a_slot);
-      uint64_t bdesc[4];
+      uint64_t bdesc[W2_MAXL + 1];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
+      for (int a = 0; a <= W2_MAXL; ++a) {
         int sl = s_ai + a;
         if (sl >= p.nbr) sl -= p.nbr;
+        if (sl >= p.nbr) sl -= p.nbr;  // a > L (unused) with a small ring
         bdesc[a] = sw128(sB + (uint32_t)sl * b_slot);
       }
       // one elected lane issues the atom's MMAs and commits as one block (a per-MMA elect /
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
           for (int rb = 0; rb < 4; ++rb) {
             if (rb < p.RG) {
               const int t = 8 * kk + rb * shift;  // compile-time when SHIFT != 0
-              const uint64_t bd = bdesc[(t >> 5) & 3] + (uint64_t)((t & 31) >> 2);
+              const uint64_t bd = bdesc[(t >> 5) & W2_MAXL] + (uint64_t)((t & 31) >> 2);
               if (!p.dbg) ptx::mma_tf32(tmem + rb * p.N, adesc + (uint64_t)(kk * 2), bd, idesc, acc);
             }
           }
@@ -514,18 +516,19 @@ W2Plan plan_w2(const SpfConv &sc) {
     p.hb4 = hb_env;
   }
   // channel tile: Ct <= 48 (3 helper tasks per thread), S*Ct % 16 == 0, RG*S*Ct TMEM
-  // columns <= 512; the widest tile wins (the last one may be ragged: TMA zero-fills)
+  // columns <= 512; the fewest tiles win, then the narrowest such tile (least zero-filled
+  // padding in the ragged last one: C = 64 takes 2 x 32, not 2 x 48)
   p.Ct = 0;
   for (int ct = std::min(48, (sc.C + 7) / 8 * 8); ct >= 8; ct -= 8)
     if ((sc.S * ct) % 16 == 0 && sc.S * ct <= 256 && p.RG * sc.S * ct <= 512) {
+      if (p.Ct && ceil_div(sc.C, ct) > ceil_div(sc.C, p.Ct)) break;
       p.Ct = ct;
-      break;
     }
   if (!p.Ct || p.RG > 4) return pl;
   p.nct = (int)ceil_div(sc.C, p.Ct);
   p.N = sc.S * p.Ct;
   p.L = (24 + (p.RG - 1) * p.shift) / W2_ATOM;
-  if (p.L > 3) return pl;  // B descriptors of atoms ai .. ai + 3
+  if (p.L > W2_MAXL) return pl;  // B descriptors of atoms ai .. ai + W2_MAXL
   // B ring: >= L + 2 (atom bi + 1 resident while bi is shifted) plus run-ahead slots
   size_t smem = 0;
   for (p.nbr = p.L + 6; p.nbr >= p.L + 3; --p.nbr) {
