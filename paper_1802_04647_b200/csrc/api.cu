@@ -53,7 +53,9 @@ sysml_status conv_fwd_ws(const sysml_conv_desc &cd, const sysml_pool_desc *pd, i
       else if (pd) b += align_up((size_t)g.N * g.KPQ() * sizeof(float), 256);
     }
   } else if (use_tc && !pap && pair_conv_supported(a, 0)) {
-    b += pair_conv_ws(a, 0);  // CTA-pair (cta_group::2) kernel for 256-wide filter banks
+    b += pair_conv_ws(a, 0);  // CTA-pair (cta_group::2) kernel for 256-wide filter banks (opt-in)
+  } else if (use_tc && !pap && c1x1_supported(a, 0)) {
+    b += c1x1_ws(a, 0);  // 1x1: activation transposed through TMEM
   } else if (use_tc && tc_fwd_supported(a, pap)) {
     b += tc_fwd_ws(a);
   } else if (use_tc && !pap && phase_fwd_supported(a)) {
@@ -134,6 +136,11 @@ sysml_status conv_fwd_dispatch(const sysml_conv_desc &cd, const sysml_input &x, 
     void *tws = wc.take<char>(pair_conv_ws(a, 0));
     SYSML_WS_FITS(wc);
     return pair_conv(a, 0, xd, f, bias, y, tws, st);
+  }
+  if (cd.math == SYSML_MATH_TF32 && !pap && !x.is_csr && c1x1_supported(a, 0)) {
+    void *tws = wc.take<char>(c1x1_ws(a, 0));
+    SYSML_WS_FITS(wc);
+    return c1x1_conv(a, 0, xd, f, bias, y, tws, st);
   }
   if (use_tc) {
     void *tws = wc.take<char>(tc_fwd_ws(a));
@@ -252,6 +259,7 @@ sysml_status conv_bwd_data_ws(const sysml_conv_desc &cd, size_t *bytes) {
   const ConvArgs a = conv_args(g);
   *bytes = 0;
   if (cd.math == SYSML_MATH_TF32 && pair_conv_supported(a, 1)) *bytes = pair_conv_ws(a, 1);
+  else if (cd.math == SYSML_MATH_TF32 && c1x1_supported(a, 1)) *bytes = c1x1_ws(a, 1);
   else if (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a)) *bytes = tc_bwd_data_ws(a);
   else if (cd.math == SYSML_MATH_TF32 && phase_bwd_data_supported(a)) *bytes = phase_bwd_data_ws(a);
   else if (phase_simt_bwd_data_supported(a)) *bytes = phase_simt_bwd_data_ws(a);
@@ -276,6 +284,7 @@ sysml_status conv_bwd_data_dispatch(const sysml_conv_desc &cd, const float *f, c
     return SYSML_ERR_WORKSPACE;
   }
   if (cd.math == SYSML_MATH_TF32 && pair_conv_supported(a, 1)) return pair_conv(a, 1, dy, f, nullptr, dx, ws, st);
+  if (cd.math == SYSML_MATH_TF32 && c1x1_supported(a, 1)) return c1x1_conv(a, 1, dy, f, nullptr, dx, ws, st);
   if (cd.math == SYSML_MATH_TF32 && tc_bwd_data_supported(a))
     return tc_conv_bwd_data(a, f, dy, dx, ws, st);
   if (cd.math == SYSML_MATH_TF32 && phase_bwd_data_supported(a)) {

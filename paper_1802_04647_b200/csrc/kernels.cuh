@@ -192,6 +192,12 @@ sysml_status launch_maxpool_bwd_spf(const PoolArgs &a, const int32_t *argmax, co
 sysml_status launch_nchw_to_spf(int N, int C, int H, int W, const float *x, float *spf,
                                 int64_t plane, int Wf, int Lf, int off, cudaStream_t st);
 
+// conv1x1_tmem.cu : 1x1 stride-1 conv fwd / bwd_data, activation transposed through TMEM
+bool c1x1_supported(const ConvArgs &a, int bwd_data);
+size_t c1x1_ws(const ConvArgs &a, int bwd_data);
+sysml_status c1x1_conv(const ConvArgs &a, int bwd_data, const float *in, const float *f, const float *bias,
+                       float *out, void *ws, cudaStream_t st);
+
 // pair_conv.cu : stride-1 conv fwd / bwd_data on CTA pairs (cta_group::2, M = 256) for 256-wide
 // filter banks; bwd_data = 1 computes dX = conv(dY, rot180(F)^T)
 bool pair_conv_supported(const ConvArgs &a, int bwd_data);

@@ -530,3 +530,39 @@ def test_lenet_b2f_staging_variants_match_oracle(S, env):
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+_C1X1_CODE = r"""
+import numpy as np, torch, synth, oracle, paper_1802_04647_b200 as S
+from tests.test_gpu_parity import TOL, assert_close, dev, host
+# (N, C, H, W, K): ragged position tiles (N*H*W % 128 != 0, tiles straddling images), C not a
+# multiple of 32 (zero-padded last chunk), K not a multiple of 16 (TMA zero rows, masked stores),
+# H*W % 4 != 0 (direct epilogue), several output tiles (K > 128), tiny planes (5 images per tile)
+shapes = [(3, 36, 7, 9, 40), (2, 64, 14, 14, 200), (5, 256, 7, 7, 64), (2, 1024, 3, 5, 24),
+          (3, 48, 8, 8, 136), (40, 32, 2, 2, 16)]
+for i, (N, C, H, W, K) in enumerate(shapes):
+    x, f, b, dy = synth.conv_problem_U(N, C, H, W, K, 1, 1, H, W, seed=(700 + i,))
+    d = S.conv_desc(N, C, H, W, K, 1, 1, 1, 0, "tf32")
+    y = S.sysml_conv2d(dev(x), dev(f), d, bias=dev(b))
+    assert "c1x1_kernel" in S.sysml_last_route(), S.sysml_last_route()
+    assert_close(host(y), oracle.conv2d_fwd(x, f, N, C, H, W, K, 1, 1, (1, 1), (0, 0), bias=b), TOL["tf32"], f"fwd {i}")
+    dx = S.sysml_conv2d_bwd_data(dev(f), dev(dy), d)
+    if C >= 16:
+        assert "c1x1_kernel" in S.sysml_last_route(), S.sysml_last_route()
+    assert_close(host(dx), oracle.conv2d_bwd_data(f, dy, N, C, H, W, K, 1, 1, (1, 1), (0, 0)), TOL["tf32"], f"bwd_data {i}")
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"SYSML_C1X1_MT2": "2"}, {"SYSML_C1X1_ON": "256"}, {"SYSML_C1X1_BLOCKED": "1"},
+                                 {"SYSML_C1X1_DIRECT": "1"}])
+def test_c1x1_tmem_kernel_vs_oracle(S, env):
+    """The 1x1 fwd / bwd_data kernel that transposes the activation through TMEM (conv1x1_tmem.cu)
+    against the oracle on ragged shapes, in its default configuration and with the variants its
+    plan can take: two M tiles per unit (SYSML_C1X1_MT2=2), 256-wide output tiles with one
+    accumulator buffer (SYSML_C1X1_ON=256), contiguous unit ranges (SYSML_C1X1_BLOCKED=1), and the
+    unstaged epilogue (SYSML_C1X1_DIRECT=1)."""
+    import subprocess, sys
+    r = subprocess.run([sys.executable, "-c", _C1X1_CODE], env=dict(os.environ, **env), capture_output=True,
+                       text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
