@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
     // shift tasks (channel c, 16-byte chunk q) of this thread: t = et + 128u (Ct*8 <= 384).
     // Source: the TMA-loaded s = 0 tile of atom bi (chunk q) and, for q = 7, chunk 0 of
     // atom bi + 1 (next ring slot); both rows are 128-byte swizzled (chunk q at q ^ (c & 7)).
-    const int ntask = p.Ct * 8;
+    const int ntask = p.S > 1 ? p.Ct * 8 : 0;  // S = 1: no shifted taps to build
     int sb = 0, sa = 0;
     uint32_t pb = 0, pa = 0;
     for (int step = -npre; step < (int)nA; ++step) {
@@ -518,8 +518,10 @@ W2Plan plan_w2(const SpfConv &sc) {
   // channel tile: Ct <= 48 (3 helper tasks per thread), S*Ct % 16 == 0, RG*S*Ct TMEM
   // columns <= 512; the fewest tiles win, then the narrowest such tile (least zero-filled
   // padding in the ragged last one: C = 64 takes 2 x 32, not 2 x 48)
+  // S = 1 has no helper-built taps, so the tile may be as wide as the MMA (N <= 256): fewer TMA
+  // rows per unit of work (1x1 convs on planes whose rows are not 16-byte multiples, 7x7)
   p.Ct = 0;
-  for (int ct = std::min(48, (sc.C + 7) / 8 * 8); ct >= 8; ct -= 8)
+  for (int ct = std::min(sc.S == 1 ? 256 : 48, (sc.C + 7) / 8 * 8); ct >= 8; ct -= 8)
     if ((sc.S * ct) % 16 == 0 && sc.S * ct <= 256 && p.RG * sc.S * ct <= 512) {
       if (p.Ct && ceil_div(sc.C, ct) > ceil_div(sc.C, p.Ct)) break;
       p.Ct = ct;
