@@ -26,7 +26,8 @@ namespace sysml {
 
 namespace {
 
-constexpr int C1P_THREADS = 416;
+constexpr int C1P_THREADS = 544;  // 0-3 producers, 4 MMA, 5-12 epilogue, 13-16 extra CSR producers
+constexpr int C1P_CSR_PW = 8;     // CSR producer warps (0-3 and 13-16), each filling every 8th M-tile
 constexpr int C1P_MT = 2;  // M-tiles per CTA tile (one per epilogue warp set)
 
 struct C1pParams {
@@ -143,8 +144,8 @@ __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pPar
   const uint32_t tmem = *tslot;
   const int PpQp = p.Pp * p.Qp;
 
-  if (warp < 4 && p.is_csr) {
-    // ---------------- CSR producers: warp w fills every 4th M-tile alone -- zero the T
+  if ((warp < 4 || warp >= 13) && p.is_csr) {
+    // ---------------- CSR producers: producer pw fills every 8th M-tile alone -- zero the T
     // row blocks, then each non-zero (h, w, v) of the overlapping images adds v to the
     // (window, t, e) slots with 2pp + t = h + ph and 2pc + e = w + pw (work ~ nnz,
     // P:168-170; duplicates summed, reading R15)
@@ -155,13 +156,13 @@ __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pPar
     }
     const int HW = p.H * p.W;
     const float invW = 1.0f / (float)p.W;
-    int lm = warp;  // CTA-local M-tile counter of this warp
+    const int pw = warp < 4 ? warp : warp - 9;  // 0..7
     for (int64_t it = 0;; ++it) {
       const int64_t tile = blockIdx.x + it * gridDim.x;
       if (tile >= p.ntiles) break;
       for (int i = 0; i < C1P_MT; ++i) {
         const int mine = (int)(it * C1P_MT + i);
-        if ((mine & 3) != warp) continue;
+        if (mine % C1P_CSR_PW != pw) continue;
         const int stage = mine % p.nstage;
         const uint32_t phase = (uint32_t)((mine / p.nstage) & 1);
         ptx::mbar_wait(empty + stage, phase ^ 1);
@@ -224,7 +225,8 @@ __global__ void __launch_bounds__(C1P_THREADS, 1) conv1_pool_kernel(const C1pPar
         if (lane == 0) ptx::mbar_arrive(full + stage);
       }
     }
-    (void)lm;
+  } else if (warp >= 13) {
+    // extra CSR producers: idle on dense input
   } else if (warp < 4) {
     // ---------------- producers: thread tid owns row m = tid of every stage
     const int tid = threadIdx.x;

@@ -1,5 +1,5 @@
 """Time one conv op (CUDA events, median of reps, L2 flushed).
-usage: time_conv.py {fwd,fwdpool,bwd_data,bwd_filter} N C H W K R pad [math]"""
+usage: time_conv.py [csr]{fwd,fwdpool,bwd_data,bwd_filter} N C H W K R pad [math]"""
 import sys, os, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
@@ -10,6 +10,10 @@ math = sys.argv[9] if len(sys.argv) > 9 else "tf32"
 P = H + 2 * pd - R + 1
 x, f, b, dy = synth.conv_problem_U(N, C, H, W, K, R, R, P, P)
 x, f, b, dy = (torch.from_numpy(t).cuda() for t in (x, f, b, dy))
+if op.startswith("csr"):  # MNIST-like sparse input (C must be 1, 28x28), as in prof_conv.py
+    xs = torch.from_numpy(synth.mnist_like(N, seed=(9,))).cuda().to_sparse_csr()
+    x = S.CSR(xs.crow_indices().int(), xs.col_indices().int(), xs.values().float(), N, C * H * W)
+    op = op[3:]
 d = S.conv_desc(N, C, H, W, K, R, R, 1, pd, math)
 pdsc = S.pool_desc(N, K, P, P, 2, 2, 2, 0, True)
 ws = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
