@@ -311,10 +311,11 @@ __global__ void __launch_bounds__(FBB_THREADS, 2)
 // partials in order; the row sums are added in row order (deterministic)
 __global__ void fused_b1_reduce_kernel(const float *__restrict__ part, int parts, int K, int RS,
                                        float *__restrict__ df, float *__restrict__ db) {
-  __shared__ float red[8][33];
+  __shared__ float red[32][33];
   const int nout = K * (RS + 1);
   const int x = threadIdx.x, y = threadIdx.y;
-  const int c0 = y * parts / 8, c1 = (y + 1) * parts / 8;
+  const int ny = blockDim.y;  // <= 32 slices of the partials, summed in slice order
+  const int c0 = y * parts / ny, c1 = (y + 1) * parts / ny;
   for (int base = blockIdx.x * 32; base < nout; base += gridDim.x * 32) {
     const int o = base + x;
     float s = 0.f;
@@ -324,8 +325,7 @@ __global__ void fused_b1_reduce_kernel(const float *__restrict__ part, int parts
     __syncthreads();
     if (y == 0 && o < nout) {
       float t = 0.f;
-#pragma unroll
-      for (int g = 0; g < 8; ++g) t += red[g][x];
+      for (int g = 0; g < ny; ++g) t += red[g][x];
       const int kk = o / (RS + 1), i = o - kk * (RS + 1);
       if (i < RS) df[kk * RS + i] = t;
       else if (db) db[kk] = t;
@@ -415,7 +415,7 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
     if (b1_tc_supported(c, pa, true, dpool_nhwc != 0, xcsr != nullptr)) {  // tensor-core form (b1_tc.cu)
       int used_tc = 0;
       SYSML_TRY(b1_tc(c, x, dpool, a.code, a.code_plane, part, ctas, &used_tc, st));
-      fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 32), dim3(32, 8), 0, st>>>(
+      fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 32), dim3(32, 32), 0, st>>>(
           part, used_tc, c.K, RS, df, db);
       SYSML_LAUNCH_CHECK();
       return SYSML_OK;
@@ -424,7 +424,7 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
     SYSML_TRY(smem_attr(kern, sm_need));
     kern<<<used, FBB_THREADS, sm_need, st>>>(a, x, cs, xcsr != nullptr, dpool, part);
     SYSML_LAUNCH_CHECK();
-    fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 32), dim3(32, 8), 0, st>>>(
+    fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 32), dim3(32, 32), 0, st>>>(
         part, used, c.K, RS, df, db);
     SYSML_LAUNCH_CHECK();
     return SYSML_OK;
@@ -439,7 +439,7 @@ sysml_status fused_pool_bwd_wgrad(const ConvArgs &c, const PoolArgs &pa, const f
                                                                 argmax, mask, part);
   }
   SYSML_LAUNCH_CHECK();
-  fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 32), dim3(32, 8), 0, st>>>(
+  fused_b1_reduce_kernel<<<(unsigned)ceil_div((int64_t)c.K * (RS + 1), 32), dim3(32, 32), 0, st>>>(
       part, used, c.K, RS, df, db);
   SYSML_LAUNCH_CHECK();
   return SYSML_OK;

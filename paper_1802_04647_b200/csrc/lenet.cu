@@ -75,10 +75,12 @@ __global__ void __launch_bounds__(F3_THREADS) affine_softmax_ce_smem_kernel(
     for (int j = 0; j < NCLS; ++j) ptx::bulk_g2s(w3s + j * (D3 / 4), W3 + j * D3, D3 * 4, &w3bar);
   }
   __syncthreads();
-  ptx::mbar_wait(&w3bar, 0);
   float *mylg = lg + warp * 2 * NCLS;
   const int npair = (n + 1) >> 1;
-  for (int pr = blockIdx.x * F3_WARPS + warp; pr < npair; pr += gridDim.x * F3_WARPS) {
+  // pairs spread over the CTAs first (small batches use every SM), and the first batch of a2
+  // loads is issued before waiting for this CTA's W3 copy (the copy's latency overlaps it)
+  bool w3ready = false;
+  for (int pr = warp * gridDim.x + blockIdx.x; pr < npair; pr += gridDim.x * F3_WARPS) {
     const int i0 = 2 * pr;
     const bool two = i0 + 1 < n;
     const float4 *r0 = reinterpret_cast<const float4 *>(a2 + (int64_t)i0 * D3);
@@ -99,6 +101,10 @@ __global__ void __launch_bounds__(F3_THREADS) affine_softmax_ce_smem_kernel(
         } else {
           xa[u] = xb[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+      }
+      if (!w3ready) {
+        ptx::mbar_wait(&w3bar, 0);
+        w3ready = true;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
