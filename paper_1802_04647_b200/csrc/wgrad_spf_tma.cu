@@ -344,13 +344,19 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
       if ((!dsplit || (et & 1) == 0) && drow < p.Kc && k0 + drow < p.K)
         p.dbpart[(int64_t)z * p.K + k0 + drow] = dbv;
     }
-    if (main_helper) {
+    {
+    // accumulator dump by both helper sets (TMEM quadrant = warp % 4): set main takes the even
+    // 16-column groups, the other set the odd ones; rows whose tap r = rb*copies + j is past R
+    // (R = 5 in row groups of two) are skipped -- the reduce skips them too
     if (nA > 0) ptx::mbar_wait_sleep(accf, 0);
     ptx::tc_fence_after();
     const int row = qd * 32 + lane;
+    const int jrow = row / p.Kc;
     float *dst = p.part + (int64_t)blockIdx.x * p.RG * 128 * p.N;
-    for (int rb = 0; rb < p.RG; ++rb)
-      for (int cb = 0; cb < p.N; cb += 16) {
+    for (int rb = 0; rb < p.RG; ++rb) {
+      const bool dead = rb * p.copies + jrow >= p.R || jrow >= p.copies;
+      if (__all_sync(0xffffffffu, dead)) continue;  // tcgen05.ld is warp-collective
+      for (int cb = main_helper ? 0 : 16; cb < p.N; cb += 32) {
         float v[16];
         if (nA > 0) {
           ptx::tmem_ld16(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(rb * p.N + cb), v);
@@ -358,12 +364,14 @@ __global__ void __launch_bounds__(W2_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = 0.f;
         }
+        if (dead) continue;
         float4 *o = reinterpret_cast<float4 *>(dst + ((int64_t)rb * 128 + row) * p.N + cb);
         o[0] = make_float4(v[0], v[1], v[2], v[3]);
         o[1] = make_float4(v[4], v[5], v[6], v[7]);
         o[2] = make_float4(v[8], v[9], v[10], v[11]);
         o[3] = make_float4(v[12], v[13], v[14], v[15]);
       }
+    }
     }
   }
   if (p.clk && threadIdx.x == 32) p.clk[blockIdx.x * 8 + 6] = clock64() - tk0;
@@ -431,9 +439,15 @@ __global__ void __launch_bounds__(W2R_GROUPS * W2R_Q) w2_reduce_wide_kernel(
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   int tile = 0;
   int64_t w = 0;
+  bool live = false;
   if (g < groups) {
     tile = (int)(g * 4 / per_cta);
     w = g * 4 - (int64_t)tile * per_cta;
+    // a group of 4 lies in one accumulator row; rows of taps past R were never written
+    const int rb = (int)(w / (128 * p.N)), row = (int)(w - (int64_t)rb * 128 * p.N) / p.N;
+    live = rb * p.copies + row / p.Kc < p.R && row / p.Kc < p.copies;
+  }
+  if (live) {
     const float4 *src =
         reinterpret_cast<const float4 *>(p.part + (int64_t)tile * p.splits * per_cta + w);
     const int64_t stride4 = per_cta / 4;
@@ -453,7 +467,7 @@ __global__ void __launch_bounds__(W2R_GROUPS * W2R_Q) w2_reduce_wide_kernel(
   }
   red[q][gl] = acc;
   __syncthreads();
-  if (q == 0 && g < groups) {
+  if (q == 0 && live) {
     float4 t = red[0][gl];
 #pragma unroll
     for (int qq = 1; qq < W2R_Q; ++qq) {
