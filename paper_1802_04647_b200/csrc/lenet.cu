@@ -630,8 +630,9 @@ sysml_pool_desc pool2_desc(int n) { return sysml_pool_desc{n, 64, 14, 14, 2, 2, 
 int64_t c2_plane_of(int64_t max_b) { return (max_b * 49 + 1) / 2 * 2; }
 
 int dw3_chunks_for(int n) {
-  // about 16 samples per chunk, at most one chunk per SM (x 4 column blocks)
-  int64_t c = std::min<int64_t>(sm_count(), ceil_div(n, 16));
+  // about 32 samples per chunk (16 measured slower at batch 1024: twice the partials to
+  // reduce), at most one chunk per SM (x 4 column blocks)
+  int64_t c = std::min<int64_t>(sm_count(), ceil_div(n, 32));
   return (int)(c < 1 ? 1 : c);
 }
 
